@@ -1,0 +1,323 @@
+"""CPU oracle for the Distill grid-search hot path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product package ``paper_2110_15425_b200`` never imports it and the two share
+no code (see ``distill_oracle.h``).
+
+This module only builds ``distill_oracle.c`` with gcc and marshals numpy
+arrays through ctypes; every arithmetic step is in the C file.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "distill_oracle.c")
+_HDR = os.path.join(_HERE, "distill_oracle.h")
+LIB = os.path.join(_HERE, "liboracle.so")
+LIB_COUNT = os.path.join(_HERE, "liboracle_count.so")
+CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-mfma",
+          "-fPIC", "-shared", "-Wall"]
+
+
+def build(force: bool = False) -> None:
+    """Compile the oracle (and its flop-counting twin) with gcc."""
+    for out, extra in ((LIB, []), (LIB_COUNT, ["-DOD_COUNT_FLOPS"])):
+        if (not force and os.path.exists(out)
+                and os.path.getmtime(out) >= max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))):
+            continue
+        subprocess.check_call(["gcc", *CFLAGS, *extra, _SRC, "-o", out + ".tmp", "-lm"])
+        os.replace(out + ".tmp", out)
+
+
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C")
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C")
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C")
+
+
+class DdmParams(C.Structure):
+    _fields_ = [("drift", C.c_float), ("noise", C.c_float), ("threshold", C.c_float),
+                ("x0", C.c_float), ("dt", C.c_float), ("n_steps", C.c_uint32),
+                ("rt_bin_steps", C.c_uint32), ("n_x_bins", C.c_uint32),
+                ("x_lo", C.c_float), ("x_hi", C.c_float)]
+
+
+def _bind(path: str) -> C.CDLL:
+    lib = C.CDLL(path)
+    u64, u32, f32 = C.c_uint64, C.c_uint32, C.c_float
+    sig = {
+        "od_philox4x32_10": (None, [_u32p, _u32p, _u32p]),
+        "od_ln": (f32, [f32]),
+        "od_rsqrt": (f32, [f32]),
+        "od_sincos2pi": (None, [u32, C.POINTER(f32), C.POINTER(f32)]),
+        "od_ln_array": (None, [_f32p, _f32p, u64]),
+        "od_rsqrt_array": (None, [_f32p, _f32p, u64]),
+        "od_sincos2pi_array": (None, [_u32p, _f32p, _f32p, u64]),
+        "od_normal_quad": (None, [u64, u64, u64, u64, _f32p]),
+        "od_normal_sextet": (None, [u64, u32, u32, u32, _f32p]),
+        "od_pp_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u64, u64, u32, u64, u32, C.c_void_p]),
+        "od_pp_eval_f64": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u64, u64, u32, u64, u32, C.c_void_p]),
+        "od_key": (u64, [f32, u32]),
+        "od_argmax_net": (C.c_int, [_f32p, u64, u64, C.POINTER(u64)]),
+        "od_ddm_trial": (None, [C.POINTER(DdmParams), u64, u64, C.POINTER(C.c_int), C.POINTER(u32), C.POINTER(f32)]),
+        "od_ddm_batch": (C.c_int, [C.POINTER(DdmParams), u64, u64, u64, _u64p, _u64p, _u64p]),
+        "od_lci_trial": (None, [f32, f32, f32, f32, f32, f32, u32, u64, u64,
+                                C.POINTER(C.c_int), C.POINTER(u32), C.POINTER(f32)]),
+        "od_stroop_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u64, u32, u32, u32, u64, C.c_void_p, C.c_void_p]),
+        "od_stroop_value": (f32, [_f32p, _f32p, f32, f32, u32, u64, u64, u64]),
+        "od_stroop_trial": (None, [_f32p, f32, f32, u64, u64, u32, C.POINTER(C.c_int), C.POINTER(u32)]),
+        "od_flops_read": (C.c_ulonglong, []),
+        "od_flops_reset": (None, []),
+        "od_is_counting_build": (C.c_int, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = None
+_lib_count = None
+_lock = threading.Lock()
+
+
+def lib(counting: bool = False) -> C.CDLL:
+    global _lib, _lib_count
+    with _lock:
+        if counting:
+            if _lib_count is None:
+                build()
+                _lib_count = _bind(LIB_COUNT)
+            return _lib_count
+        if _lib is None:
+            build()
+            _lib = _bind(LIB)
+        return _lib
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+
+
+def _u32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint32))
+
+
+# ---------------------------------------------------------------- RNG
+
+def philox(ctr, key) -> np.ndarray:
+    out = np.zeros(4, np.uint32)
+    lib().od_philox4x32_10(_u32(ctr), _u32(key), out)
+    return out
+
+
+def ln(x: float) -> float:
+    return lib().od_ln(float(x))
+
+
+def rsqrt(x: float) -> float:
+    return lib().od_rsqrt(float(x))
+
+
+def sincos2pi(a: int):
+    c, s = C.c_float(), C.c_float()
+    lib().od_sincos2pi(int(a), C.byref(c), C.byref(s))
+    return c.value, s.value
+
+
+def ln_array(x) -> np.ndarray:
+    x = _f32(x)
+    y = np.empty_like(x)
+    lib().od_ln_array(x, y, x.size)
+    return y
+
+
+def rsqrt_array(x) -> np.ndarray:
+    x = _f32(x)
+    y = np.empty_like(x)
+    lib().od_rsqrt_array(x, y, x.size)
+    return y
+
+
+def sincos2pi_array(a):
+    a = _u32(a)
+    c = np.empty(a.size, np.float32)
+    s = np.empty(a.size, np.float32)
+    lib().od_sincos2pi_array(a, c, s, a.size)
+    return c, s
+
+
+def normal_quad(seed: int, unit: int, first: int, n: int) -> np.ndarray:
+    out = np.zeros(n, np.float32)
+    lib().od_normal_quad(seed, unit, first, n, out)
+    return out
+
+
+def normal_sextet(seed: int, alloc: int, sample: int, invocation: int = 0) -> np.ndarray:
+    out = np.zeros(6, np.float32)
+    lib().od_normal_sextet(seed, alloc, sample, invocation, out)
+    return out
+
+
+# ---------------------------------------------------------------- predator-prey
+
+def pp_eval(n_levels, levels, w, params, inputs, begin, end, n_samples, seed,
+            invocation=0, f64=False, counting=False) -> np.ndarray:
+    n = int(end) - int(begin)
+    out = np.zeros(max(n, 0), np.float64 if f64 else np.float32)
+    L = lib(counting)
+    fn = L.od_pp_eval_f64 if f64 else L.od_pp_eval
+    rc = fn(_u32(n_levels), _f32(levels), _f32(w), _f32(params), _f32(inputs),
+            int(begin), int(end), int(n_samples), int(seed), int(invocation),
+            out.ctypes.data_as(C.c_void_p))
+    if rc != 0:
+        raise ValueError("od_pp_eval rejected its arguments")
+    return out
+
+
+def pp_eval_threads(n_levels, levels, w, params, inputs, begin, end, n_samples, seed,
+                    invocation=0, threads=1) -> np.ndarray:
+    """Contiguous segments over Python threads (ctypes drops the GIL) — the
+    paper's multicore scheme.  Timing helper only."""
+    n = int(end) - int(begin)
+    out = np.zeros(n, np.float32)
+    threads = max(1, min(int(threads), max(n, 1)))
+    seg = (n + threads - 1) // threads
+    args = (_u32(n_levels), _f32(levels), _f32(w), _f32(params), _f32(inputs))
+    L = lib()
+
+    def work(t):
+        b = begin + t * seg
+        e = min(begin + n, b + seg)
+        if e <= b:
+            return
+        view = out[b - begin:e - begin]
+        L.od_pp_eval(*args, b, e, int(n_samples), int(seed), int(invocation),
+                     view.ctypes.data_as(C.c_void_p))
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return out
+
+
+def key(cost: float, index: int) -> int:
+    return int(lib().od_key(float(cost), int(index)))
+
+
+def argmax_net(net, base=0):
+    k = C.c_uint64()
+    arr = _f32(net)
+    rc = lib().od_argmax_net(arr, arr.size, int(base), C.byref(k))
+    return int(k.value), rc
+
+
+def key_decode(k: int):
+    hi = (k >> 32) & 0xFFFFFFFF
+    idx = k & 0xFFFFFFFF
+    if hi == 0xFFFFFFFF:
+        return float("nan"), idx
+    b = (hi & 0x7FFFFFFF) if (hi >> 31) else (~hi & 0xFFFFFFFF)
+    return float(np.array([b], np.uint32).view(np.float32)[0]), idx
+
+
+# ---------------------------------------------------------------- DDM / LCI
+
+def ddm_params(drift, noise, threshold, x0, dt, n_steps, rt_bin_steps, n_x_bins, x_lo, x_hi):
+    return DdmParams(drift, noise, threshold, x0, dt, n_steps, rt_bin_steps, n_x_bins, x_lo, x_hi)
+
+
+def ddm_trial(p: DdmParams, seed: int, trial: int):
+    ch, st, xe = C.c_int(), C.c_uint32(), C.c_float()
+    lib().od_ddm_trial(C.byref(p), seed, trial, C.byref(ch), C.byref(st), C.byref(xe))
+    return ch.value, st.value, xe.value
+
+
+def ddm_hist_sizes(p: DdmParams):
+    nb = (p.n_steps + p.rt_bin_steps - 1) // p.rt_bin_steps
+    return 2 * nb + 1, 2, p.n_x_bins + 2
+
+
+def ddm_batch(p: DdmParams, seed: int, t0: int, t1: int, threads: int = 1):
+    a, b, c = ddm_hist_sizes(p)
+    threads = max(1, min(int(threads), max(t1 - t0, 1)))
+    seg = (t1 - t0 + threads - 1) // threads
+    parts = [(np.zeros(a, np.uint64), np.zeros(b, np.uint64), np.zeros(c, np.uint64)) for _ in range(threads)]
+    L = lib()
+
+    def work(t):
+        s = t0 + t * seg
+        e = min(t1, s + seg)
+        if e > s:
+            L.od_ddm_batch(C.byref(p), seed, s, e, *parts[t])
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return tuple(sum(p_[k] for p_ in parts) for k in range(3))
+
+
+def lci_trial(inp, leak, offset, noise, dt, threshold, n_steps, seed, unit):
+    ch, st, xe = C.c_int(), C.c_uint32(), C.c_float()
+    lib().od_lci_trial(inp, leak, offset, noise, dt, threshold, n_steps, seed, unit,
+                       C.byref(ch), C.byref(st), C.byref(xe))
+    return ch.value, st.value, xe.value
+
+
+# ---------------------------------------------------------------- Stroop
+
+def stroop_eval(n_levels, levels, w, params, begin, end, n_trials, seed,
+                trial_begin=0, trial_end=None, threads=1):
+    """Returns (counts[n,3] uint64, net[n] float32 or None if a trial sub-range)."""
+    if trial_end is None:
+        trial_end = n_trials
+    n = int(end) - int(begin)
+    counts = np.zeros((n, 3), np.uint64)
+    full = (trial_begin == 0 and trial_end == n_trials)
+    net = np.zeros(n, np.float32) if full else None
+    args = (_u32(n_levels), _f32(levels), _f32(w), _f32(params))
+    L = lib()
+    threads = max(1, min(int(threads), max(n, 1)))
+    seg = (n + threads - 1) // threads
+
+    def work(t):
+        b = begin + t * seg
+        e = min(begin + n, b + seg)
+        if e <= b:
+            return
+        cv = counts[b - begin:e - begin]
+        nv = net[b - begin:e - begin].ctypes.data_as(C.c_void_p) if full else None
+        rc = L.od_stroop_eval(*args, b, e, int(n_trials), int(trial_begin), int(trial_end),
+                              int(seed), cv.ctypes.data_as(C.c_void_p), nv)
+        if rc != 0:
+            raise ValueError("od_stroop_eval rejected its arguments")
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return counts, net
+
+
+def stroop_trial(params, u_c, u_s, seed, unit, trial):
+    r, st = C.c_int(), C.c_uint32()
+    lib().od_stroop_trial(_f32(params), u_c, u_s, seed, unit, trial, C.byref(r), C.byref(st))
+    return r.value, st.value
+
+
+def stroop_value(params, w, u_c, u_s, n_trials, n_correct, n_undecided, rt_sum):
+    return lib().od_stroop_value(_f32(params), _f32(w), u_c, u_s, n_trials,
+                                 int(n_correct), int(n_undecided), int(rt_sum))

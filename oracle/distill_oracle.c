@@ -1,0 +1,487 @@
+/*
+ * distill_oracle.c — CPU oracle for the Distill grid-search hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY (see distill_oracle.h): never linked into, loaded
+ * by, or called from the product path.  Written from spec/RNG.md and
+ * spec/MODELS.md, which restate PAPER.md (arXiv 2110.15425):
+ *   - per-evaluation independent random draws            P:356-358 (§3.6)
+ *   - predator-prey Control/Obs/Action/Objective nodes    P:140-167 (§2.1, Fig. 1)
+ *   - exhaustive grid search, lowest cost wins
+ *   - ties                                                P:306 (§3.3)
+ *   - DDM / LCI accumulation, Fig. 3 clone pinning        P:466-477 (§4.4)
+ *   - Botvinick Stroop                                    P:525 (§5)
+ * Readings of everything the paper leaves open are DESIGN.md §3 (R1...).
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -shared -fPIC
+ *        (+ -DOD_COUNT_FLOPS for the flop-counting build).  No FTZ/DAZ.
+ * Every binary32 operation is written out; the FADD/FMUL/... macros only add
+ * a flop counter in the counting build (fma = 2 flops, others 1).
+ */
+#include "distill_oracle.h"
+#include <math.h>
+#include <string.h>
+
+#ifdef OD_COUNT_FLOPS
+static _Thread_local unsigned long long od_flops;
+#define CNT(n) (od_flops += (n))
+#else
+#define CNT(n) ((void)0)
+#endif
+unsigned long long od_flops_read(void) {
+#ifdef OD_COUNT_FLOPS
+    return od_flops;
+#else
+    return 0;
+#endif
+}
+void od_flops_reset(void) {
+#ifdef OD_COUNT_FLOPS
+    od_flops = 0;
+#endif
+}
+int od_is_counting_build(void) {
+#ifdef OD_COUNT_FLOPS
+    return 1;
+#else
+    return 0;
+#endif
+}
+
+/* one counted binary32 operation each */
+static inline float FADD(float a, float b) { CNT(1); return a + b; }
+static inline float FSUB(float a, float b) { CNT(1); return a - b; }
+static inline float FMUL(float a, float b) { CNT(1); return a * b; }
+static inline float FDIV(float a, float b) { CNT(1); return a / b; }
+static inline float FFMA(float a, float b, float c) { CNT(2); return fmaf(a, b, c); }
+static inline float FSQRT(float a) { CNT(1); return sqrtf(a); }
+
+static inline uint32_t f2u(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
+static inline float u2f(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+
+/* ------------------------------------------------------------------------ */
+/* spec/RNG.md §1: Philox4x32-10                                             */
+/* ------------------------------------------------------------------------ */
+void od_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* ------------------------------------------------------------------------ */
+/* spec/RNG.md §3: ln_spec                                                   */
+/* ------------------------------------------------------------------------ */
+#define LN2_HI 0x1.62e4p-1f
+#define LN2_LO 0x1.7f7d1cp-20f
+static const float OD_L[8] = {
+    -0x1.fffff4p-2f, 0x1.5556e8p-2f, -0x1.0006c4p-2f, 0x1.98da38p-3f,
+    -0x1.52fb94p-3f, 0x1.30d0aap-3f, -0x1.277224p-3f, 0x1.6fc72p-4f };
+
+float od_ln(float x) {
+    uint32_t i = f2u(x);
+    int32_t e = ((int32_t)(i - 0x3F3504F3u)) >> 23;
+    float m = u2f(i - ((uint32_t)e << 23));
+    float f = FSUB(m, 1.0f);
+    float P = OD_L[7];
+    for (int k = 6; k >= 0; --k) P = FFMA(P, f, OD_L[k]);
+    float f2 = FMUL(f, f);
+    float y = FFMA(f2, P, f);
+    float fe = (float)e;
+    y = FFMA(fe, LN2_LO, y);
+    y = FFMA(fe, LN2_HI, y);
+    return y;
+}
+
+/* ------------------------------------------------------------------------ */
+/* spec/RNG.md §4: rsqrt_spec                                                */
+/* ------------------------------------------------------------------------ */
+float od_rsqrt(float x) {
+    float y = u2f(0x5F375A86u - (f2u(x) >> 1));
+    float h = FMUL(0.5f, x);
+    for (int k = 0; k < 3; ++k) {
+        float t = FMUL(y, y);
+        t = FFMA(-h, t, 1.5f);
+        y = FMUL(y, t);
+    }
+    return y;
+}
+
+/* ------------------------------------------------------------------------ */
+/* spec/RNG.md §5: sincos2pi_spec                                            */
+/* ------------------------------------------------------------------------ */
+static const float OD_S[4] = { 0x1.921fb6p+0f, -0x1.4abbbap-1f, 0x1.465ec8p-4f, -0x1.2d9c2p-8f };
+static const float OD_C[4] = { -0x1.3bd3ccp+0f, 0x1.03c1dep-2f, -0x1.55c666p-6f, 0x1.d9f828p-11f };
+
+void od_sincos2pi(uint32_t a, float* cs, float* sn) {
+    uint32_t s = a + 0x20000000u;
+    uint32_t q = s >> 30;
+    int32_t ri = (int32_t)(s & 0x3FFFFFFFu) - 0x20000000;
+    float r = (float)ri * 0x1p-30f;           /* exact: power-of-two scaling of an exact value */
+    float t = FMUL(r, r);
+    float S = FFMA(FFMA(FFMA(OD_S[3], t, OD_S[2]), t, OD_S[1]), t, OD_S[0]);
+    float C = FFMA(FFMA(FFMA(OD_C[3], t, OD_C[2]), t, OD_C[1]), t, OD_C[0]);
+    float cq = FFMA(C, t, 1.0f);
+    float sq = FMUL(S, r);
+    switch (q) {
+    case 0:  *cs = cq;  *sn = sq;  break;
+    case 1:  *cs = -sq; *sn = cq;  break;
+    case 2:  *cs = -cq; *sn = -sq; break;
+    default: *cs = sq;  *sn = -cq; break;
+    }
+}
+
+/* array forms of the three primitives, for the exhaustive accuracy pins */
+void od_ln_array(const float* x, float* y, uint64_t n) { for (uint64_t j = 0; j < n; ++j) y[j] = od_ln(x[j]); }
+void od_rsqrt_array(const float* x, float* y, uint64_t n) { for (uint64_t j = 0; j < n; ++j) y[j] = od_rsqrt(x[j]); }
+void od_sincos2pi_array(const uint32_t* a, float* c, float* s, uint64_t n) {
+    for (uint64_t j = 0; j < n; ++j) od_sincos2pi(a[j], &c[j], &s[j]);
+}
+
+/* spec/RNG.md §2 + §6: one Box-Muller pair */
+static void od_bm_pair(uint32_t R, uint32_t A, float* z0, float* z1) {
+    float u1 = (float)((R >> 8) | 1u) * 0x1p-24f;   /* exact */
+    float s = -2.0f * od_ln(u1);                     /* exact scaling, not counted */
+    float rad = FMUL(s, od_rsqrt(s));                /* sqrt_spec */
+    float c, n;
+    od_sincos2pi(A, &c, &n);
+    *z0 = FMUL(rad, c);
+    *z1 = FMUL(rad, n);
+}
+
+static inline void od_key_of_seed(uint64_t seed, uint32_t key[2]) {
+    key[0] = (uint32_t)seed;
+    key[1] = (uint32_t)(seed >> 32);
+}
+
+void od_normal_quad(uint64_t seed, uint64_t unit, uint64_t first, uint64_t n, float* out) {
+    uint32_t key[2];
+    od_key_of_seed(seed, key);
+    for (uint64_t j = first; j < first + n; ++j) {
+        uint32_t ctr[4] = { (uint32_t)unit, (uint32_t)(j >> 2), (uint32_t)(unit >> 32), 2u };
+        uint32_t X[4];
+        od_philox4x32_10(ctr, key, X);
+        float z[4];
+        od_bm_pair(X[0], X[1] & 0xFFFFFF00u, &z[0], &z[1]);
+        od_bm_pair(X[2], X[3] & 0xFFFFFF00u, &z[2], &z[3]);
+        out[j - first] = z[j & 3];
+    }
+}
+
+void od_normal_sextet(uint64_t seed, uint32_t alloc, uint32_t sample, uint32_t invocation, float* out) {
+    uint32_t key[2];
+    od_key_of_seed(seed, key);
+    uint32_t ctr[4] = { alloc, sample, invocation, 1u };
+    uint32_t X[4];
+    od_philox4x32_10(ctr, key, X);
+    uint32_t A0 = X[3] << 16;
+    uint32_t A1 = X[3] & 0xFFFF0000u;
+    uint32_t A2 = (X[0] << 24) | ((X[1] & 0xFFu) << 16) | ((X[2] & 0xFFu) << 8);
+    od_bm_pair(X[0], A0, &out[0], &out[1]);
+    od_bm_pair(X[1], A1, &out[2], &out[3]);
+    od_bm_pair(X[2], A2, &out[4], &out[5]);
+}
+
+/* ------------------------------------------------------------------------ */
+/* spec/MODELS.md §1-2: predator-prey                                        */
+/* ------------------------------------------------------------------------ */
+typedef struct { float x, y; } v2;
+
+static v2 od_unit(v2 v) {
+    float n2 = FFMA(v.y, v.y, FMUL(v.x, v.x));
+    float y = (n2 == 0.0f) ? 0.0f : od_rsqrt(n2);
+    v2 r = { FMUL(v.x, y), FMUL(v.y, y) };
+    return r;
+}
+static v2 od_sub(v2 a, v2 b) { v2 r = { FSUB(a.x, b.x), FSUB(a.y, b.y) }; return r; }
+/* Action node: unit toward prey minus kappa * unit toward predator */
+static v2 od_action(v2 prey, v2 pred, v2 player, float kappa) {
+    v2 up = od_unit(od_sub(prey, player));
+    v2 ud = od_unit(od_sub(pred, player));
+    v2 d = { FFMA(-kappa, ud.x, up.x), FFMA(-kappa, ud.y, up.y) };
+    return d;
+}
+
+/* mixed-radix decode, dim 0 most significant */
+static void od_decode(uint64_t i, int D, const uint32_t* L, uint32_t* k) {
+    for (int d = D - 1; d >= 0; --d) { k[d] = (uint32_t)(i % L[d]); i /= L[d]; }
+}
+
+int od_pp_eval(const uint32_t n_levels[3], const float* levels, const float w[3],
+               const float params[3], const float inputs[6],
+               uint64_t begin, uint64_t end, uint32_t n_samples, uint64_t seed,
+               uint32_t invocation, float* cost) {
+    if (!n_levels || !levels || !w || !params || !inputs || n_samples == 0 || end < begin) return -1;
+    uint64_t N = (uint64_t)n_levels[0] * n_levels[1] * n_levels[2];
+    if (N == 0 || end > N || N > 0xFFFFFFFFull) return -1;
+    const float* lev[3] = { levels, levels + n_levels[0], levels + n_levels[0] + n_levels[1] };
+    float smax = params[0], smin = params[1], kappa = params[2];
+    v2 p[3] = { { inputs[0], inputs[1] }, { inputs[2], inputs[3] }, { inputs[4], inputs[5] } };
+    float dsig = FSUB(smin, smax);
+    v2 ustar = od_unit(od_action(p[0], p[1], p[2], kappa));
+
+    for (uint64_t i = begin; i < end; ++i) {
+        uint32_t k[3];
+        od_decode(i, 3, n_levels, k);
+        float a[3] = { lev[0][k[0]], lev[1][k[1]], lev[2][k[2]] };
+        float sig[3];
+        for (int e = 0; e < 3; ++e) sig[e] = FFMA(a[e], dsig, smax);
+        float K = FFMA(w[2], a[2], FFMA(w[1], a[1], FMUL(w[0], a[0])));
+        float acc = 0.0f;
+        for (uint32_t s = 0; s < n_samples; ++s) {
+            float z[6];
+            od_normal_sextet(seed, (uint32_t)i, s, invocation, z);
+            v2 o[3];
+            for (int e = 0; e < 3; ++e) {
+                o[e].x = FFMA(sig[e], z[2 * e], p[e].x);
+                o[e].y = FFMA(sig[e], z[2 * e + 1], p[e].y);
+            }
+            v2 uh = od_unit(od_action(o[0], o[1], o[2], kappa));
+            v2 dl = od_sub(uh, ustar);
+            float e2 = FFMA(dl.y, dl.y, FMUL(dl.x, dl.x));
+            acc = FADD(acc, e2);
+        }
+        cost[i - begin] = FADD(FDIV(acc, (float)n_samples), K);
+    }
+    return 0;
+}
+
+/* Same model in binary64 (the "plain definition" re-evaluation): normals from
+ * the same Philox bits with exact libm Box-Muller, body with 1/sqrt. */
+typedef struct { double x, y; } d2;
+static d2 d_unit(d2 v) {
+    double n2 = v.x * v.x + v.y * v.y;
+    double y = (n2 == 0.0) ? 0.0 : 1.0 / sqrt(n2);
+    d2 r = { v.x * y, v.y * y };
+    return r;
+}
+static d2 d_action(d2 prey, d2 pred, d2 player, double kappa) {
+    d2 a = { prey.x - player.x, prey.y - player.y }, b = { pred.x - player.x, pred.y - player.y };
+    d2 up = d_unit(a), ud = d_unit(b);
+    d2 d = { up.x - kappa * ud.x, up.y - kappa * ud.y };
+    return d;
+}
+static void d_bm(uint32_t R, uint32_t A, double* z0, double* z1) {
+    const double TWO_PI = 6.283185307179586476925286766559;
+    double u1 = (double)((R >> 8) | 1u) * 0x1p-24;
+    double t = (double)A * 0x1p-32;
+    double rad = sqrt(-2.0 * log(u1));
+    *z0 = rad * cos(TWO_PI * t);
+    *z1 = rad * sin(TWO_PI * t);
+}
+
+int od_pp_eval_f64(const uint32_t n_levels[3], const float* levels, const float w[3],
+                   const float params[3], const float inputs[6],
+                   uint64_t begin, uint64_t end, uint32_t n_samples, uint64_t seed,
+                   uint32_t invocation, double* cost) {
+    if (!n_levels || !levels || !w || !params || !inputs || n_samples == 0 || end < begin) return -1;
+    uint64_t N = (uint64_t)n_levels[0] * n_levels[1] * n_levels[2];
+    if (N == 0 || end > N || N > 0xFFFFFFFFull) return -1;
+    const float* lev[3] = { levels, levels + n_levels[0], levels + n_levels[0] + n_levels[1] };
+    double smax = params[0], smin = params[1], kappa = params[2];
+    d2 p[3] = { { inputs[0], inputs[1] }, { inputs[2], inputs[3] }, { inputs[4], inputs[5] } };
+    d2 ustar = d_unit(d_action(p[0], p[1], p[2], kappa));
+    uint32_t key[2];
+    od_key_of_seed(seed, key);
+    for (uint64_t i = begin; i < end; ++i) {
+        uint32_t k[3];
+        od_decode(i, 3, n_levels, k);
+        double a[3] = { lev[0][k[0]], lev[1][k[1]], lev[2][k[2]] };
+        double sig[3];
+        for (int e = 0; e < 3; ++e) sig[e] = smax + a[e] * (smin - smax);
+        double K = (double)w[0] * a[0] + (double)w[1] * a[1] + (double)w[2] * a[2];
+        double acc = 0.0;
+        for (uint32_t s = 0; s < n_samples; ++s) {
+            uint32_t ctr[4] = { (uint32_t)i, s, invocation, 1u }, X[4];
+            od_philox4x32_10(ctr, key, X);
+            uint32_t A[3] = { X[3] << 16, X[3] & 0xFFFF0000u,
+                              (X[0] << 24) | ((X[1] & 0xFFu) << 16) | ((X[2] & 0xFFu) << 8) };
+            d2 o[3];
+            for (int e = 0; e < 3; ++e) {
+                double zx, zy;
+                d_bm(X[e], A[e], &zx, &zy);
+                o[e].x = p[e].x + sig[e] * zx;
+                o[e].y = p[e].y + sig[e] * zy;
+            }
+            d2 uh = d_unit(d_action(o[0], o[1], o[2], kappa));
+            double dx = uh.x - ustar.x, dy = uh.y - ustar.y;
+            acc += dx * dx + dy * dy;
+        }
+        cost[i - begin] = acc / (double)n_samples + K;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* spec/MODELS.md §3: argmax keys                                            */
+/* ------------------------------------------------------------------------ */
+uint64_t od_key(float cost, uint32_t index) {
+    uint32_t hi;
+    if (isnan(cost)) {
+        hi = 0xFFFFFFFFu;
+    } else {
+        if (cost == 0.0f) cost = 0.0f;              /* -0 -> +0 */
+        uint32_t b = f2u(cost);
+        hi = (b >> 31) ? ~b : (b | 0x80000000u);
+    }
+    return ((uint64_t)hi << 32) | index;
+}
+
+int od_argmax_net(const float* net, uint64_t n, uint64_t base, uint64_t* key) {
+    uint64_t best = 0xFFFFFFFFFFFFFFFFull;
+    for (uint64_t j = 0; j < n; ++j) {
+        uint64_t k = od_key(-net[j], (uint32_t)(base + j));
+        if (k < best) best = k;
+    }
+    *key = best;
+    return (n == 0 || (best >> 32) == 0xFFFFFFFFull) ? 1 : 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* spec/MODELS.md §4: DDM                                                    */
+/* ------------------------------------------------------------------------ */
+void od_ddm_trial(const od_ddm_params* p, uint64_t seed, uint64_t trial,
+                  int* choice, uint32_t* step, float* x_end) {
+    float nsd = FMUL(p->noise, FSQRT(p->dt));
+    float x = p->x0;
+    int ch = 2;
+    uint32_t st = 0;
+    for (uint32_t n = 1; n <= p->n_steps; ++n) {
+        float g;
+        od_normal_quad(seed, trial, n - 1, 1, &g);
+        x = FFMA(nsd, g, FFMA(p->dt, p->drift, x));
+        if (ch == 2) {
+            if (x >= p->threshold) { ch = 0; st = n; }
+            else if (x <= -p->threshold) { ch = 1; st = n; }
+        }
+    }
+    *choice = ch; *step = st; *x_end = x;
+}
+
+int od_ddm_batch(const od_ddm_params* p, uint64_t seed, uint64_t t0, uint64_t t1,
+                 uint64_t* rt_hist, uint64_t* rt_sum, uint64_t* x_hist) {
+    if (!p || p->n_steps == 0 || p->rt_bin_steps == 0 || p->n_x_bins == 0 || t1 < t0) return -1;
+    uint32_t nb = (p->n_steps + p->rt_bin_steps - 1) / p->rt_bin_steps;
+    float sc = (float)p->n_x_bins / (p->x_hi - p->x_lo);
+    for (uint64_t t = t0; t < t1; ++t) {
+        int ch; uint32_t st; float xe;
+        od_ddm_trial(p, seed, t, &ch, &st, &xe);
+        if (ch == 2) rt_hist[2 * nb] += 1;
+        else { rt_hist[(uint32_t)ch * nb + (st - 1) / p->rt_bin_steps] += 1; rt_sum[ch] += st; }
+        float u = (xe - p->x_lo) * sc;
+        uint32_t bin;
+        if (u < 0.0f) bin = 0;
+        else if (!(u < (float)p->n_x_bins)) bin = p->n_x_bins + 1;
+        else bin = 1 + (uint32_t)u;
+        x_hist[bin] += 1;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* spec/MODELS.md §5: LCI (Fig. 3 clone of the DDM integrator)               */
+/* ------------------------------------------------------------------------ */
+void od_lci_trial(float input, float leak, float offset, float noise, float dt,
+                  float threshold, uint32_t n_steps, uint64_t seed, uint64_t unit,
+                  int* choice, uint32_t* step, float* x_end) {
+    float nsd = FMUL(noise, FSQRT(dt));
+    float x = 0.0f;
+    int ch = 2;
+    uint32_t st = 0;
+    for (uint32_t n = 1; n <= n_steps; ++n) {
+        float g;
+        od_normal_quad(seed, unit, n - 1, 1, &g);
+        x = FFMA(nsd, g, FADD(FFMA(dt, FFMA(-leak, x, input), x), offset));
+        if (ch == 2) {
+            if (x >= threshold) { ch = 0; st = n; }
+            else if (x <= -threshold) { ch = 1; st = n; }
+        }
+    }
+    *choice = ch; *step = st; *x_end = x;
+}
+
+/* ------------------------------------------------------------------------ */
+/* spec/MODELS.md §6: Stroop-LCA                                             */
+/* ------------------------------------------------------------------------ */
+enum { SP_GC, SP_GW, SP_TAU, SP_LEAK, SP_INH, SP_NOISE, SP_DT, SP_THR, SP_R, SP_CRT, SP_N };
+
+void od_stroop_trial(const float P[11], float u_c, float u_s, uint64_t seed,
+                     uint64_t unit, uint32_t trial, int* resp, uint32_t* step) {
+    uint32_t kind = trial % 3, color = (trial / 3) % 2;
+    int word = (kind == 0) ? (int)color : (kind == 1) ? (int)(1 - color) : -1;
+    float ic = FMUL(P[SP_GC], u_c);
+    float iw = FMUL(P[SP_GW], FSUB(1.0f, u_s));
+    float I[2];
+    for (int k = 0; k < 2; ++k) {
+        float a = ((uint32_t)k == color) ? ic : 0.0f;
+        float b = (k == word) ? iw : 0.0f;
+        I[k] = FADD(a, b);
+    }
+    uint32_t N = (uint32_t)P[SP_N];
+    float nsd = FMUL(P[SP_NOISE], FSQRT(P[SP_DT]));
+    float h[2] = { 0.0f, 0.0f }, x[2] = { 0.0f, 0.0f };
+    int r = -1;
+    uint32_t st = 0;
+    for (uint32_t n = 1; n <= N; ++n) {
+        for (int k = 0; k < 2; ++k) h[k] = FFMA(P[SP_TAU], FSUB(I[k], h[k]), h[k]);
+        float g[2];
+        od_normal_quad(seed, unit, 2ull * (n - 1), 2, g);
+        float xn[2];
+        for (int k = 0; k < 2; ++k) {
+            float q = FFMA(-P[SP_INH], x[1 - k], FFMA(-P[SP_LEAK], x[k], h[k]));
+            float y = FFMA(nsd, g[k], FFMA(P[SP_DT], q, x[k]));
+            xn[k] = fmaxf(y, 0.0f);
+        }
+        x[0] = xn[0]; x[1] = xn[1];
+        if (r < 0) {
+            if (x[0] >= P[SP_THR]) { r = 0; st = n; }
+            else if (x[1] >= P[SP_THR]) { r = 1; st = n; }
+        }
+    }
+    *resp = r; *step = st;
+}
+
+float od_stroop_value(const float P[11], const float w[2], float u_c, float u_s,
+                      uint32_t n_trials, uint64_t n_correct, uint64_t n_undecided, uint64_t rt_sum) {
+    double T = (double)n_trials;
+    double N = (double)(uint32_t)P[SP_N];
+    double v = (double)P[SP_R] * (double)n_correct / T;
+    v = v - (double)P[SP_CRT] * (double)P[SP_DT] * ((double)rt_sum + (double)n_undecided * N) / T;
+    v = v - ((double)w[0] * (double)u_c + (double)w[1] * (double)u_s);
+    return (float)v;
+}
+
+int od_stroop_eval(const uint32_t n_levels[2], const float* levels, const float w[2],
+                   const float P[11], uint64_t begin, uint64_t end, uint32_t n_trials,
+                   uint32_t trial_begin, uint32_t trial_end, uint64_t seed,
+                   uint64_t* counts, float* net) {
+    if (!n_levels || !levels || !w || !P || n_trials == 0 || end < begin ||
+        trial_end < trial_begin || trial_end > n_trials) return -1;
+    uint64_t N = (uint64_t)n_levels[0] * n_levels[1];
+    if (N == 0 || end > N || N * (uint64_t)n_trials > 0xFFFFFFFFFFFFull) return -1;
+    for (uint64_t i = begin; i < end; ++i) {
+        uint32_t k[2];
+        od_decode(i, 2, n_levels, k);
+        float uc = levels[k[0]], us = levels[n_levels[0] + k[1]];
+        uint64_t* c = counts + 3 * (i - begin);
+        for (uint32_t j = trial_begin; j < trial_end; ++j) {
+            uint32_t colour = (j / 3) % 2;
+            int resp; uint32_t st;
+            od_stroop_trial(P, uc, us, seed, i * (uint64_t)n_trials + j, j, &resp, &st);
+            if (resp < 0) c[1] += 1;
+            else { if ((uint32_t)resp == colour) c[0] += 1; c[2] += st; }
+        }
+        if (net) net[i - begin] = od_stroop_value(P, w, uc, us, n_trials, c[0], c[1], c[2]);
+    }
+    return 0;
+}

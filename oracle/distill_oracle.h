@@ -1,0 +1,106 @@
+/*
+ * distill_oracle.h — plain, slow, obviously-correct CPU oracle for the Distill
+ * grid-search hot path (arXiv 2110.15425, §2.1 and §3.6).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header or constant table with the CUDA path: both are
+ * written independently from spec/RNG.md and spec/MODELS.md.
+ *
+ * Every function is scalar, single-threaded and re-entrant; callers that want
+ * parallelism (bench timing) split the allocation range into contiguous
+ * segments exactly like the paper's multicore scheme.
+ *
+ * Parity status per function:
+ *   od_philox4x32_10     pinned: Random123 known-answer vectors
+ *   od_ln / od_rsqrt / od_sincos2pi   pinned: exhaustive / dense accuracy vs binary64 libm
+ *   od_normal_*          pinned: moments, KS vs Phi, closed-form endpoints
+ *   od_pp_eval           pinned: zero-noise closed forms, monotonicity, planted optimum,
+ *                        small-noise delta-method expectation, fp64 re-evaluation
+ *   od_argmax_keys       pinned: brute-force min over (C, i), NaN/-0 rules
+ *   od_ddm_*             pinned: zero-noise first passage, closed-form ER/DT, endpoint law
+ *   od_lci_trial         pinned: Fig. 3 clone relation to od_ddm_trial (bit-identical)
+ *   od_stroop_eval       pinned: zero-noise deterministic RT, conservation, Stroop effect;
+ *                        absolute values parity unpinned (the paper prints none)
+ */
+#ifndef DISTILL_ORACLE_H
+#define DISTILL_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- RNG (spec/RNG.md) ---- */
+void  od_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+float od_ln(float x);
+float od_rsqrt(float x);
+void  od_sincos2pi(uint32_t angle_word, float* c, float* s);
+void  od_ln_array(const float* x, float* y, uint64_t n);
+void  od_rsqrt_array(const float* x, float* y, uint64_t n);
+void  od_sincos2pi_array(const uint32_t* a, float* c, float* s, uint64_t n);
+/* normals [first, first+n) of unit U on stream 2, quad packing */
+void  od_normal_quad(uint64_t seed, uint64_t unit, uint64_t first, uint64_t n, float* out);
+/* the three 2-D noise vectors (prey, predator, player) of sample s: out[6] */
+void  od_normal_sextet(uint64_t seed, uint32_t alloc, uint32_t sample, uint32_t invocation, float* out);
+
+/* ---- predator-prey grid (spec/MODELS.md §1-3) ---- */
+/* levels: L0+L1+L2 floats, dim 0 first.  w[3].  params = {sigma_max, sigma_min, kappa}.
+ * inputs = {prey.x, prey.y, pred.x, pred.y, player.x, player.y}.
+ * Writes cost[i-begin] (C, binary32) for i in [begin, end).  Returns 0, or -1 on bad args. */
+int od_pp_eval(const uint32_t n_levels[3], const float* levels, const float w[3],
+               const float params[3], const float inputs[6],
+               uint64_t begin, uint64_t end, uint32_t n_samples, uint64_t seed,
+               uint32_t invocation, float* cost);
+/* Same evaluation in binary64 from the same Philox bits (libm log/sqrt/cos/sin). */
+int od_pp_eval_f64(const uint32_t n_levels[3], const float* levels, const float w[3],
+                   const float params[3], const float inputs[6],
+                   uint64_t begin, uint64_t end, uint32_t n_samples, uint64_t seed,
+                   uint32_t invocation, double* cost);
+
+/* ---- argmax keys (spec/MODELS.md §3) ---- */
+uint64_t od_key(float cost, uint32_t index);
+/* min over key(-net[j], base+j); returns 0 ok, 1 if no finite/inf candidate (all NaN or n == 0) */
+int od_argmax_net(const float* net, uint64_t n, uint64_t base, uint64_t* key);
+
+/* ---- DDM (spec/MODELS.md §4) ---- */
+typedef struct {
+    float drift, noise, threshold, x0, dt;
+    uint32_t n_steps, rt_bin_steps, n_x_bins;
+    float x_lo, x_hi;
+} od_ddm_params;
+/* one trial: choice 0 = upper, 1 = lower, 2 = undecided; step (1-based, 0 if undecided); x_N */
+void od_ddm_trial(const od_ddm_params* p, uint64_t seed, uint64_t trial,
+                  int* choice, uint32_t* step, float* x_end);
+/* histogram accumulate (+=) over trials [t0, t1) */
+int od_ddm_batch(const od_ddm_params* p, uint64_t seed, uint64_t t0, uint64_t t1,
+                 uint64_t* rt_hist, uint64_t* rt_sum, uint64_t* x_hist);
+
+/* ---- LCI single unit (spec/MODELS.md §5) — Fig. 3 pin ---- */
+void od_lci_trial(float input, float leak, float offset, float noise, float dt,
+                  float threshold, uint32_t n_steps, uint64_t seed, uint64_t unit,
+                  int* choice, uint32_t* step, float* x_end);
+
+/* ---- Stroop-LCA grid (spec/MODELS.md §6) ---- */
+/* params = {g_c, g_w, tau, leak, inhibition, noise, dt, threshold, reward, rt_cost, n_steps}
+ * counts[3*(i-begin) + {0,1,2}] = {n_correct, n_undecided, rt_sum}; net[i-begin] = V. */
+int od_stroop_eval(const uint32_t n_levels[2], const float* levels, const float w[2],
+                   const float params[11], uint64_t begin, uint64_t end, uint32_t n_trials,
+                   uint32_t trial_begin, uint32_t trial_end, uint64_t seed,
+                   uint64_t* counts, float* net);
+/* V from finished integer counts (binary64 then one rounding). */
+float od_stroop_value(const float params[11], const float w[2], float u_c, float u_s,
+                      uint32_t n_trials, uint64_t n_correct, uint64_t n_undecided, uint64_t rt_sum);
+/* single Stroop trial (for tests) */
+void od_stroop_trial(const float params[11], float u_c, float u_s, uint64_t seed,
+                     uint64_t unit, uint32_t trial, int* resp, uint32_t* step);
+
+/* ---- flop counting (only meaningful in the -DOD_COUNT_FLOPS build) ---- */
+unsigned long long od_flops_read(void);
+void od_flops_reset(void);
+int od_is_counting_build(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

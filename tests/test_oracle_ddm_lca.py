@@ -1,0 +1,144 @@
+"""Pins for the DDM, LCI and Stroop-LCA oracle (spec/MODELS.md §4-6).
+
+DDM: deterministic first passage in binary32, the closed-form error rate and
+decision time of the drift-diffusion model (Bogacz et al. 2006, the DDM the
+paper cites at P:466) with the discrete-monitoring (Siegmund) correction, and
+the exact Gaussian law of the Euler endpoint.  LCI: the Fig. 3 clone relation
+(P:477).  Stroop: zero-noise determinism, the Stroop effect, conservation.
+"""
+import math
+
+import numpy as np
+import pytest
+from scipy import stats
+
+import workloads as W
+
+
+def ddm(orc, **kw):
+    c = W.DDMConfig(**kw)
+    return c, orc.ddm_params(c.drift, c.noise, c.threshold, c.x0, c.dt, c.n_steps,
+                             c.rt_bin_steps, c.n_x_bins, c.x_lo, c.x_hi)
+
+
+@pytest.mark.parametrize("drift,dt,want", [(1.0, 0.01, 101), (1.0, 0.005, 201), (2.0, 0.01, 51),
+                                           (-1.0, 0.01, 101)])
+def test_ddm_zero_noise_first_passage_binary32(orc, drift, dt, want):
+    """x_n = fma(dt, A, x) accumulated in binary32 crosses z = 1 at step 101 for
+    A dt = 0.01 (100 in real arithmetic): the oracle mirrors binary32 exactly."""
+    # reference: the same recurrence evaluated by numpy binary32 (dt*A is exact here)
+    x = np.float32(0)
+    n_ref = None
+    for n in range(1, 2000):
+        x = np.float32(x + np.float32(np.float32(dt) * np.float32(drift)))
+        if abs(x) >= 1:
+            n_ref = n
+            break
+    assert n_ref == want
+    c, p = ddm(orc, drift=drift, noise=0.0, dt=dt, n_steps=1000)
+    ch, st, _ = orc.ddm_trial(p, 1, 0)
+    assert st == want and ch == (0 if drift > 0 else 1)
+
+
+def _siegmund(A, s, z, dt):
+    zp = z + 0.5826 * s * math.sqrt(dt)
+    er = 1.0 / (1.0 + math.exp(2 * A * zp / s ** 2))
+    rt = zp / A * math.tanh(A * zp / s ** 2)
+    return er, rt
+
+
+def test_ddm_closed_form_error_rate_and_decision_time(orc):
+    c, p = ddm(orc)  # cfg2 parameters: A = sigma = z = 1, dt = 0.01, N = 1000
+    n = 200_000
+    rt_hist, rt_sum, x_hist = orc.ddm_batch(p, 11, 0, n, threads=8)
+    nb = c.n_rt_bins
+    up, lo, und = int(rt_hist[:nb].sum()), int(rt_hist[nb:2 * nb].sum()), int(rt_hist[2 * nb])
+    assert up + lo + und == n and int(x_hist.sum()) == n
+    er_mc = lo / (up + lo)
+    rt_mc = (int(rt_sum[0]) + int(rt_sum[1])) / (up + lo) * c.dt
+    er_cf, rt_cf = _siegmund(1.0, 1.0, 1.0, c.dt)
+    se_er = math.sqrt(er_cf * (1 - er_cf) / n)
+    assert abs(er_mc - er_cf) <= 4 * se_er + 0.005 * er_cf
+    assert abs(rt_mc - rt_cf) <= 0.01 * rt_cf
+    # the uncorrected continuous-time law is clearly rejected (the pin has power)
+    er_raw = 1 / (1 + math.exp(2.0))
+    assert abs(er_mc - er_raw) > 8 * se_er
+
+
+def test_ddm_endpoint_is_exact_gaussian(orc):
+    """Euler with Gaussian increments: x_N ~ N(x0 + A N dt, sigma^2 N dt) exactly."""
+    c, p = ddm(orc, n_steps=200, drift=0.5, noise=1.3)
+    xs = np.array([orc.ddm_trial(p, 5, t)[2] for t in range(4000)], np.float64)
+    mu, sd = 0.5 * 200 * c.dt, 1.3 * math.sqrt(200 * c.dt)
+    assert stats.kstest((xs - mu) / sd, "norm").pvalue > 1e-3
+
+
+def test_ddm_histograms_conserve_and_add_over_shards(orc):
+    c, p = ddm(orc, n_steps=300)
+    full = orc.ddm_batch(p, 3, 0, 3000)
+    a = orc.ddm_batch(p, 3, 0, 1234)
+    b = orc.ddm_batch(p, 3, 1234, 3000)
+    for f, x, y in zip(full, a, b):
+        assert np.array_equal(f, x + y)
+    assert int(full[0].sum()) == 3000 and int(full[2].sum()) == 3000
+    # rt_sum is consistent with per-trial steps
+    s = [0, 0]
+    for t in range(3000):
+        ch, st, _ = orc.ddm_trial(p, 3, t)
+        if ch < 2:
+            s[ch] += st
+    assert [int(v) for v in full[1]] == s
+
+
+def test_lci_is_a_bit_exact_clone_of_ddm(orc):
+    """Fig. 3: rate_LCI = 0, offset = 0, noise N(0,1) vs rate_DDI = 1,
+    noise 1 perform identical computation -> identical trajectories."""
+    c, p = ddm(orc, drift=0.7, noise=1.0, threshold=1.0, n_steps=400)
+    for t in range(300):
+        d = orc.ddm_trial(p, 9, t)
+        l = orc.lci_trial(0.7, 0.0, 0.0, 1.0, c.dt, 1.0, 400, 9, t)
+        assert d[0] == l[0] and d[1] == l[1]
+        assert np.float32(d[2]).view(np.uint32) == np.float32(l[2]).view(np.uint32)
+    # and a leak breaks the equivalence
+    diff = sum(orc.ddm_trial(p, 9, t)[2] != orc.lci_trial(0.7, 0.3, 0.0, 1.0, c.dt, 1.0, 400, 9, t)[2]
+               for t in range(20))
+    assert diff == 20
+
+
+def test_stroop_zero_noise_deterministic_and_stroop_effect(orc):
+    P = W.STROOP_PARAMS.copy()
+    P[5] = 0.0  # noise off
+    rts = {}
+    for j in range(12):
+        r, st = orc.stroop_trial(P, 1.0, 0.5, 1, 1000 + j, j)
+        kind, colour = j % 3, (j // 3) % 2
+        rts.setdefault(kind, set()).add(st)
+        assert r == colour          # word at half strength (0.75 < 1.0) loses
+        # without suppression the stronger word wins the incongruent trial: an error
+        r0, _ = orc.stroop_trial(P, 1.0, 0.0, 1, 1000 + j, j)
+        assert (r0 == colour) == (kind != 1)
+    # deterministic: one RT per stimulus kind regardless of unit id / colour
+    assert all(len(v) == 1 for v in rts.values())
+    cong, incong, neut = rts[0].pop(), rts[1].pop(), rts[2].pop()
+    assert cong < neut < incong, (cong, neut, incong)  # Stroop interference
+
+
+def test_stroop_counts_conserve_and_add(orc):
+    c = W.stroop_small()
+    counts, net = orc.stroop_eval(c.n_levels, c.levels, c.w, c.params, 10, 20, c.n_trials, c.seed)
+    a, _ = orc.stroop_eval(c.n_levels, c.levels, c.w, c.params, 10, 20, c.n_trials, c.seed, 0, 100)
+    b, _ = orc.stroop_eval(c.n_levels, c.levels, c.w, c.params, 10, 20, c.n_trials, c.seed, 100, 300)
+    assert np.array_equal(counts, a + b)
+    assert (counts[:, 0] + counts[:, 1] <= c.n_trials).all()
+    # rt_sum bounded by decided trials x N
+    assert (counts[:, 2] <= (c.n_trials - counts[:, 1]) * c.n_steps).all()
+
+
+def test_stroop_value_is_correctly_rounded_binary64_formula(orc):
+    from fractions import Fraction as F
+    P, w = W.STROOP_PARAMS, W.STROOP_W
+    for nc, nu, rs in [(0, 0, 0), (150, 3, 9000), (299, 0, 12345)]:
+        v = orc.stroop_value(P, w, 0.5, 0.25, 300, nc, nu, rs)
+        exact = (F(float(P[8])) * nc / 300 - F(float(P[9])) * F(float(P[6])) * (rs + nu * 200) / 300
+                 - (F(float(w[0])) * F(1, 2) + F(float(w[1])) * F(1, 4)))
+        assert abs(F(float(v)) - exact) <= abs(exact) * F(1, 2 ** 23) + F(1, 2 ** 60)

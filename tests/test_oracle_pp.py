@@ -1,0 +1,202 @@
+"""Pins for the predator-prey oracle (spec/MODELS.md §1-3; §2.1).
+
+The paper prints no cost values, so the pins are mathematics the model must
+satisfy: zero-noise closed forms, mixed-radix decode order, a planted optimum,
+the small-noise expectation from the Jacobians of the Action node, the
+binary64 re-evaluation, and the paper's evaluation counts.
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+
+def f32_round(fr: Fraction) -> np.float32:
+    """Correct round-to-nearest-even of an exact rational to binary32."""
+    f = np.float32(float(fr))
+    best = f
+    for cand in (np.nextafter(f, np.float32(-np.inf)), np.nextafter(f, np.float32(np.inf))):
+        dc, db = abs(Fraction(float(cand)) - fr), abs(Fraction(float(best)) - fr)
+        if dc < db or (dc == db and (int(np.array([cand]).view(np.uint32)[0]) & 1) == 0):
+            best = cand
+    return best
+
+
+def fma32(a, b, c) -> np.float32:
+    return f32_round(Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c)))
+
+
+def run(orc, cfg, begin=0, end=None, **kw):
+    end = cfg.n_alloc if end is None else end
+    return orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, begin, end,
+                       cfg.n_samples, cfg.seed, **kw)
+
+
+@pytest.mark.parametrize("L,count", [(2, 8), (4, 64), (6, 216), (100, 1_000_000)])
+def test_evaluation_counts_match_paper(orc, L, count):
+    """S/M/L/XL: 2/4/6/100 levels -> 8/64/216/1,000,000 evaluations."""
+    cfg = W.PPConfig("x", (L, L, L), 1)
+    assert cfg.n_alloc == count
+    if count <= 216:
+        assert run(orc, cfg).shape == (count,)
+
+
+def test_zero_noise_cost_is_control_cost_exactly(orc):
+    """sigma = 0 -> o = p exactly -> u_hat = u_star -> e = 0 -> C = K."""
+    cfg = W.pp_cfg1()
+    cfg.params = np.array([0.0, 0.0, 0.5], np.float32)
+    C = run(orc, cfg)
+    for i in range(cfg.n_alloc):
+        k = [i // 9, (i // 3) % 3, i % 3]
+        a = [cfg.levels[3 * d + k[d]] for d in range(3)]
+        w = cfg.w
+        K = fma32(w[2], a[2], fma32(w[1], a[1], f32_round(Fraction(float(w[0])) * Fraction(float(a[0])))))
+        assert C[i] == K, (i, C[i], K)
+    # monotone non-decreasing in every level for w >= 0, argmin at index 0
+    Cg = C.reshape(3, 3, 3)
+    for ax in range(3):
+        assert (np.diff(Cg, axis=ax) >= 0).all()
+    key, rc = orc.argmax_net(-C)
+    assert rc == 0 and key & 0xFFFFFFFF == 0
+
+
+def test_mixed_radix_decode_dim0_most_significant(orc):
+    """levels a_k = k and w = (L^2, L, 1) make C = K = i exactly."""
+    L = 100
+    cfg = W.PPConfig("decode", (L, L, L), 1)
+    cfg.levels = np.concatenate([np.arange(L, dtype=np.float32)] * 3)
+    cfg.w = np.array([L * L, L, 1], np.float32)
+    cfg.params = np.array([0.0, 0.0, 0.5], np.float32)
+    idx = np.array([0, 1, 99, 100, 12345, 999999])
+    for i in idx:
+        assert run(orc, cfg, i, i + 1)[0] == float(i)
+
+
+def test_planted_optimum(orc):
+    """Zero noise, negative weight on dim 0 only: unique argmin at its top level."""
+    cfg = W.PPConfig("planted", (6, 6, 6), 3)
+    cfg.params = np.array([0.0, 0.0, 0.5], np.float32)
+    cfg.w = np.array([-0.1, 0.1, 0.1], np.float32)
+    key, rc = orc.argmax_net(-run(orc, cfg))
+    assert rc == 0 and key & 0xFFFFFFFF == 5 * 36
+
+
+def test_all_ties_lowest_index_any_split(orc):
+    cfg = W.PPConfig("ties", (4, 4, 4), 5)
+    cfg.params = np.array([0.0, 0.0, 0.5], np.float32)
+    cfg.w = np.zeros(3, np.float32)
+    C = run(orc, cfg)
+    assert (C == C[0]).all()
+    for cut in (1, 17, 40, 63):
+        k1, _ = orc.argmax_net(-C[:cut], 0)
+        k2, _ = orc.argmax_net(-C[cut:], cut)
+        assert min(k1, k2) & 0xFFFFFFFF == 0
+
+
+def _unit_jac(v):
+    n = np.linalg.norm(v)
+    u = v / n
+    return (np.eye(2) - np.outer(u, u)) / n
+
+
+def test_small_noise_expectation_matches_action_jacobians(orc):
+    """E||u_hat - u*||^2 ~= sum_e sigma_e^2 ||G_e||_F^2 for small noise, with
+    G_e = d u_hat / d p_e from the Jacobian of unit(v), (I - u u^T)/|v| —
+    an analytic derivation, independent of the oracle's code path."""
+    prey, pred, player = np.array([4.0, 1.0]), np.array([-3.0, 2.0]), np.array([0.0, 0.0])
+    kappa = 0.5
+    v1, v2 = prey - player, pred - player
+    d = v1 / np.linalg.norm(v1) - kappa * v2 / np.linalg.norm(v2)
+    Jd = _unit_jac(d)
+    G0 = Jd @ _unit_jac(v1)
+    G1 = Jd @ (-kappa * _unit_jac(v2))
+    G2 = -(G0 + G1)
+    g = np.array([np.sum(G0 ** 2), np.sum(G1 ** 2), np.sum(G2 ** 2)])
+
+    cfg = W.PPConfig("delta", (1, 1, 1), 40000)
+    cfg.levels = np.array([0.0, 0.5, 1.0], np.float32)     # a = (0, .5, 1)
+    cfg.params = np.array([0.004, 0.001, kappa], np.float32)
+    cfg.w = np.zeros(3, np.float32)
+    sig = np.array([0.004, 0.0025, 0.001])
+    pred_e = float(np.sum(sig ** 2 * g))
+    C = float(run(orc, cfg)[0])
+    assert abs(C / pred_e - 1) < 0.03, (C, pred_e)
+    # the test has power: swapping two entities' noise moves the prediction by > 10 %
+    assert abs(float(np.sum(sig[[1, 0, 2]] ** 2 * g)) / pred_e - 1) > 0.1
+
+
+def test_more_attention_less_error(orc):
+    """Objective error falls as attention to the prey rises."""
+    cfg = W.PPConfig("mono", (5, 1, 1), 4000)
+    cfg.levels = np.concatenate([W.linear_levels(5), [0.5], [0.5]]).astype(np.float32)
+    cfg.w = np.zeros(3, np.float32)
+    C = run(orc, cfg)
+    assert (np.diff(C) < 0).all(), C
+
+
+def test_binary64_reevaluation_within_north_star_tolerance(orc):
+    """binary32 oracle vs the same model in binary64 (libm Box-Muller): 1e-5 relative."""
+    for cfg, b, e in [(W.pp_cfg1(), 0, 27), (W.pp_cfg3(), 0, 300), (W.pp_cfg3(), 654321, 654521)]:
+        c32 = run(orc, cfg, b, e).astype(np.float64)
+        c64 = run(orc, cfg, b, e, f64=True)
+        rel = np.abs(c32 - c64) / np.abs(c64)
+        assert rel.max() < 1e-5, rel.max()
+
+
+def test_argmax_brute_force_cfg1(orc):
+    cfg = W.pp_cfg1()
+    C = run(orc, cfg)
+    best = min(range(cfg.n_alloc), key=lambda i: (float(C[i]), i))
+    key, rc = orc.argmax_net(-C)
+    assert rc == 0 and key & 0xFFFFFFFF == best
+    assert orc.key_decode(key) == (float(C[best]), best)
+
+
+def test_segments_equal_full_run(orc):
+    """Contiguous segments reproduce the serial run bit-exactly."""
+    cfg = W.PPConfig("L", (6, 6, 6), 20)
+    full = run(orc, cfg)
+    for threads in (1, 2, 4, 8, 12):
+        par = orc.pp_eval_threads(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs,
+                                  0, cfg.n_alloc, cfg.n_samples, cfg.seed, threads=threads)
+        assert np.array_equal(full.view(np.uint32), par.view(np.uint32))
+
+
+def test_invocation_changes_stream(orc):
+    cfg = W.pp_cfg1()
+    a = run(orc, cfg, invocation=0)
+    b = run(orc, cfg, invocation=1)
+    assert not np.array_equal(a, b)
+
+
+def test_golden_cfg1(orc):
+    """Regression fixture written by tests/golden/make_golden.py (oracle only)."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "pp_cfg1_costs.txt")
+    want = [l.split() for l in open(path) if l.strip() and not l.startswith("#")]
+    C = run(orc, W.pp_cfg1())
+    for i, h in want:
+        assert float(C[int(i)]).hex() == h
+
+
+def test_flop_count_per_sample_matches_hand_count(orc):
+    """Counting build: 242 binary32 flops per PP sample (fma = 2), the figure
+    DESIGN.md §6 derives by hand from spec/RNG.md + spec/MODELS.md:
+    3 Box-Muller pairs x 54 + obs 12 + action 44 + unit(d) 18 + objective 6."""
+    L = orc.lib(counting=True)
+    assert L.od_is_counting_build() == 1
+    cfg = W.pp_cfg3()
+
+    def flops(S):
+        L.od_flops_reset()
+        orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, 10, S, 1, counting=True)
+        return L.od_flops_read()
+
+    assert (flops(101) - flops(100)) == 10 * 242
+    per_alloc = (flops(100) - 10 * 100 * 242)
+    # per call: u_star (2 units + action) = 4 + 2*18 + 4 + 18 = 62, plus dsig 1;
+    # per allocation: 3 sigma fma (6) + K (5) + mean (2) = 13
+    assert per_alloc == 63 + 10 * 13

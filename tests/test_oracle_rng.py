@@ -1,0 +1,132 @@
+"""Pins for the oracle's counter-based normal generator (spec/RNG.md).
+
+Each pin is something other than the oracle itself: published known-answer
+vectors, binary64 libm, the normal law's moments and CDF.
+"""
+import math
+
+import numpy as np
+import pytest
+from scipy import stats
+
+
+# Random123 kat_vectors for philox4x32-10 (spec/RNG.md §1)
+KATS = [
+    ([0, 0, 0, 0], [0, 0], [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+    ([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2, [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+    ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+     [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]),
+]
+
+
+@pytest.mark.parametrize("ctr,key,want", KATS)
+def test_philox_known_answers(orc, ctr, key, want):
+    assert [int(v) for v in orc.philox(ctr, key)] == want
+
+
+def _ulp32(ref):
+    return np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+
+
+def test_ln_exhaustive_on_uniform_domain(orc):
+    """Every binary32 in [2^-24, 1): |ln_spec - log| <= 4 ulp (binary64 libm)."""
+    worst = 0.0
+    for e in range(-24, 0):
+        b0 = np.float32(2.0 ** e).view(np.uint32)
+        b1 = np.float32(2.0 ** (e + 1)).view(np.uint32)
+        x = np.arange(b0, b1, dtype=np.uint32).view(np.float32)
+        y = orc.ln_array(x).astype(np.float64)
+        ref = np.log(x.astype(np.float64))
+        worst = max(worst, float((np.abs(y - ref) / _ulp32(ref)).max()))
+    assert worst <= 4.0, worst
+    assert orc.ln(1.0) == 0.0
+
+
+def test_ln_wide_range_sampled(orc):
+    x = np.random.default_rng(1).uniform(-60, 60, 200000)
+    x = np.exp2(x).astype(np.float32)
+    y = orc.ln_array(x).astype(np.float64)
+    ref = np.log(x.astype(np.float64))
+    assert (np.abs(y - ref) / _ulp32(ref)).max() <= 4.0
+
+
+def test_rsqrt_dense(orc):
+    worst = 0.0
+    for e in range(-60, 60, 3):
+        b0 = np.float32(2.0 ** e).view(np.uint32)
+        b1 = np.float32(2.0 ** (e + 2)).view(np.uint32)
+        x = np.arange(b0, b1, 5, dtype=np.uint32).view(np.float32)
+        y = orc.rsqrt_array(x).astype(np.float64)
+        ref = 1.0 / np.sqrt(x.astype(np.float64))
+        worst = max(worst, float((np.abs(y - ref) / ref).max()))
+    assert worst <= 4 * 2.0 ** -24, worst
+
+
+def test_sincos2pi_exhaustive_24bit(orc):
+    """All 2^24 angle words with the low byte clear."""
+    a = (np.arange(2 ** 24, dtype=np.uint64) << 8).astype(np.uint32)
+    c, s = orc.sincos2pi_array(a)
+    th = a.astype(np.float64) * (2 * math.pi / 2.0 ** 32)
+    assert np.abs(c - np.cos(th)).max() <= 2 * 2.0 ** -24
+    assert np.abs(s - np.sin(th)).max() <= 2 * 2.0 ** -24
+    # quarter turns are exact
+    for k, (cc, ss) in enumerate([(1, 0), (0, 1), (-1, 0), (0, -1)]):
+        c1, s1 = orc.sincos2pi(k << 30)
+        assert (c1, s1) == (cc, ss)
+
+
+def test_box_muller_pair_matches_definition(orc):
+    """Quad normals equal sqrt(-2 ln u1)(cos, sin)(2 pi t) from the raw Philox
+    words (binary64 libm), within the primitives' error bounds."""
+    seed, unit = 12345, 77
+    for blk in range(64):
+        X = orc.philox([unit, blk, 0, 2], [seed & 0xFFFFFFFF, seed >> 32])
+        z = orc.normal_quad(seed, unit, 4 * blk, 4)
+        for p in range(2):
+            R, A = int(X[2 * p]), int(X[2 * p + 1]) & 0xFFFFFF00
+            u1 = ((R >> 8) | 1) * 2.0 ** -24
+            rad = math.sqrt(-2 * math.log(u1))
+            th = 2 * math.pi * A / 2.0 ** 32
+            assert abs(z[2 * p] - rad * math.cos(th)) <= 1e-6 * max(1, rad)
+            assert abs(z[2 * p + 1] - rad * math.sin(th)) <= 1e-6 * max(1, rad)
+
+
+def test_sextet_packing_matches_definition(orc):
+    seed = 42
+    for i, s in [(0, 0), (5, 3), (123456, 99), (999999, 0)]:
+        X = [int(v) for v in orc.philox([i, s, 0, 1], [seed, 0])]
+        A = [(X[3] << 16) & 0xFFFFFFFF, X[3] & 0xFFFF0000,
+             ((X[0] << 24) | ((X[1] & 0xFF) << 16) | ((X[2] & 0xFF) << 8)) & 0xFFFFFFFF]
+        z = orc.normal_sextet(seed, i, s, 0)
+        for e in range(3):
+            rad = math.sqrt(-2 * math.log(((X[e] >> 8) | 1) * 2.0 ** -24))
+            th = 2 * math.pi * A[e] / 2.0 ** 32
+            assert abs(z[2 * e] - rad * math.cos(th)) <= 1e-6 * max(1, rad)
+            assert abs(z[2 * e + 1] - rad * math.sin(th)) <= 1e-6 * max(1, rad)
+
+
+def test_quad_normals_moments_and_ks(orc):
+    """10^6 normals: mean within +-0.004, variance within +-0.01 (S:343 bounds),
+    kurtosis 3, KS vs Phi."""
+    z = np.concatenate([orc.normal_quad(7, u, 0, 10000) for u in range(100)]).astype(np.float64)
+    assert abs(z.mean()) < 0.004
+    assert abs(z.var() - 1) < 0.01
+    assert abs(((z - z.mean()) ** 4).mean() - 3) < 0.05
+    assert stats.kstest(z, "norm").pvalue > 1e-3
+
+
+def test_sextet_normals_moments_independence(orc):
+    z = np.array([orc.normal_sextet(3, i, s) for i in range(2000) for s in range(50)], np.float64)
+    assert np.abs(z.mean(0)).max() < 0.02
+    assert np.abs(z.var(0) - 1).max() < 0.03
+    cc = np.corrcoef(z.T)
+    assert np.abs(cc - np.eye(6)).max() < 0.02
+    assert stats.kstest(z.ravel(), "norm").pvalue > 1e-3
+
+
+def test_uniform_endpoints(orc):
+    """u1 = 2^-24 gives the largest radius sqrt(48 ln 2); u1 = 1-2^-24 the smallest."""
+    big = orc.ln(2.0 ** -24)
+    assert abs(-2 * big - 48 * math.log(2)) < 1e-5
+    small = orc.ln(1 - 2.0 ** -24)
+    assert small < 0 and abs(small + 2.0 ** -24) < 1e-12
