@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark: predator-prey grid search (BASELINE.json metric) on 1..8 B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One *step* = one controller grid search over the whole grid: key reset,
+fused pp_eval_grid kernel on this rank's contiguous shard (decode, Philox,
+Box-Muller, Obs/Action/Objective, mean + cost, net-value store, (value,
+index) argmin), and for N > 1 the single NCCL all-reduce of the packed key.
+Workload (weak scaling, ~1e6 allocations per GPU): N=1 -> cfg3 (100^3 x 100
+samples), N=8 -> cfg5 (200^3 x 100), N=2/4 -> round(100 N^(1/3))^3 x 100.
+
+Prints ONE JSON line (rank 0).  `value` = allocations x samples per second
+over all ranks (max-over-ranks device time), `e2e` = the same metric through
+the host-buffer C-ABI call (positions in, net values + best key out),
+`roofline` = the fused kernel's algorithmic FP32 rate against the FP32 ALU
+peak, `cpu_baseline` = the CPU oracle on this host's cores on a bounded slice.
+DDM (cfg2) and Stroop-LCA (cfg4) are measured once each and reported under
+`also` (they are §8 rows a5/a6/a10, not the headline).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "model evaluations/sec (allocations×samples) at 1/2/4/8 B200; % FP32 peak"
+UNIT = "evals/s"
+FLOPS_PER_SAMPLE = 242        # DESIGN.md §6, pinned by tests/test_oracle_pp.py (counting oracle)
+FLOPS_PER_ALLOC = 13
+FLOPS_PER_CALL = 63
+FP32_LANES_PER_SM = 128       # FFMA lanes per SM (4 SMSP x 32), 2 flops per FMA
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (200 ms)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows for j in range(4) if r[5 + j].lower() == "active"})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle arm
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def oracle_rate(cfg: W.PPConfig, target_cpu_s: float = 15.0):
+    """Time the CPU oracle (as it stands) over all host cores on a bounded slice
+    of the workload: contiguous allocation segments, all samples."""
+    import oracle
+    oracle.build()
+    cores = host_cores()
+    t = time.perf_counter()
+    oracle.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, 500, cfg.n_samples, cfg.seed)
+    per_alloc = (time.perf_counter() - t) / 500
+    n = int(min(cfg.n_alloc, max(cores * 64, target_cpu_s / per_alloc)))
+    t = time.perf_counter()
+    oracle.pp_eval_threads(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, n, cfg.n_samples,
+                           cfg.seed, threads=cores)
+    wall = time.perf_counter() - t
+    return {"value": n * cfg.n_samples / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{cfg.name}: allocations [0, {n}) x {cfg.n_samples} samples on {cores} threads "
+                      f"({wall:.2f} s wall)"}
+
+
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    if rank != 0:
+        return 0
+    cfg = W.pp_weak(world)
+    import oracle
+    oracle.build()
+    cores = host_cores()
+    t = time.perf_counter()
+    oracle.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, 300, cfg.n_samples, cfg.seed)
+    per_alloc = (time.perf_counter() - t) / 300
+    # each step: a bounded slice, sized so warmup + steps take about two minutes
+    n = int(min(cfg.n_alloc, max(cores * 16, 120.0 * cores / max(1, args.steps + args.warmup) / per_alloc)))
+    times = []
+    for s in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        oracle.pp_eval_threads(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, n, cfg.n_samples,
+                               cfg.seed, threads=cores)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t)
+    ms = 1e3 * sum(times) / len(times)
+    value = n * cfg.n_samples / (ms / 1e3)
+    sample = f"{cfg.name}: allocations [0, {n}) x {cfg.n_samples} samples per step on {cores} threads"
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+           "config": {"workload": cfg.name, "grid": list(cfg.n_levels), "samples": cfg.n_samples,
+                      "slice_allocations": n},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2110_15425_b200 as D
+    from paper_2110_15425_b200.api import key_from_tensor
+
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    cfg = W.pp_weak(world)
+    b, e = D.shard_range(cfg.n_alloc, rank, world)
+    count = e - b
+    model = D.load_model(W.KIND_PREDATOR_PREY, cfg.n_levels, cfg.levels, cfg.w, cfg.params, device=local)
+    net = torch.empty(max(count, 1), dtype=torch.float32, device=dev)
+    best = torch.empty(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step(ev_k0=None, ev_k1=None):
+        D.key_reset(best)
+        if ev_k0 is not None:
+            ev_k0.record(stream)
+        D.eval_grid(model, cfg.inputs, cfg.n_samples, cfg.seed, b, e, net=net, best=best)
+        if ev_k1 is not None:
+            ev_k1.record(stream)
+        if world > 1:
+            D.best_allreduce(best)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+
+    sampler = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
+    sampler.start()
+    time.sleep(0.3)
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    launches0 = D.launch_count()
+    torch.cuda.synchronize()
+    barrier()
+    for s in range(K):
+        flush.fill_(float(s))                       # L2 flush between timed steps (outside the step events)
+        evs[s][0].record(stream)
+        step(evs[s][1], evs[s][2])
+        evs[s][3].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = D.launch_count() - launches0
+    clocks = sampler.stop()
+    step_ms = [evs[s][0].elapsed_time(evs[s][3]) for s in range(K)]
+    kern_ms = [evs[s][1].elapsed_time(evs[s][2]) for s in range(K)]
+    ms_step = max_over_ranks(sum(step_ms) / K)
+    ms_kern = max_over_ranks(sum(kern_ms) / K)
+    evals = cfg.n_alloc * cfg.n_samples
+    value = evals / (ms_step / 1e3)
+    key = key_from_tensor(best)
+    best_cost, best_idx = D.key_decode(key)
+
+    # ---- e2e: host-buffer C-ABI call per rank (+ key all-reduce across ranks), every step
+    h_net = torch.empty(max(count, 1), dtype=torch.float32, pin_memory=True).numpy()
+    h_key = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    d_key = torch.empty(1, dtype=torch.int64, device=dev)
+    h2d = 6 * 4 + (8 if world > 1 else 0)
+    d2h = count * 4 + 8 + (8 if world > 1 else 0)
+
+    def e2e_step():
+        k = D.eval_grid_host(model, cfg.inputs, cfg.n_samples, cfg.seed, b, e, net_out=h_net[:count])
+        if world > 1:
+            h_key[0] = k if k < 2 ** 63 else k - 2 ** 64
+            d_key.copy_(h_key, non_blocking=True)
+            D.best_allreduce(d_key)
+            h_key.copy_(d_key)
+            torch.cuda.synchronize()
+        return k
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / K)
+    barrier()
+
+    also = {}
+    if not args.no_extras:
+        also = run_extras(D, torch, dev, rank, world, args)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    props = torch.cuda.get_device_properties(dev)
+    n_sm = props.multi_processor_count
+    sm_max = clocks.get("sm_max_mhz") or 1965.0
+    peak = n_sm * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12               # TFLOP/s at max clock
+    flops_launch = count * (cfg.n_samples * FLOPS_PER_SAMPLE + FLOPS_PER_ALLOC) + FLOPS_PER_CALL
+    achieved = flops_launch / (ms_kern / 1e3) / 1e12
+    sm_load = clocks.get("sm_mhz")
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "pp_eval_grid_kernel", "kernel_ms": ms_kern,
+            "algorithmic_flops_per_launch": flops_launch,
+            "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz (max clock)",
+            "frac_at_measured_clock": (achieved / (n_sm * FP32_LANES_PER_SM * 2 * sm_load * 1e6 / 1e12)
+                                       if sm_load else None),
+            "kernel_share_of_step": ms_kern / ms_step}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_rate(cfg)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+           "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32", "data": "synthetic",
+           "config": {"workload": cfg.name, "grid": list(cfg.n_levels), "samples": cfg.n_samples,
+                      "allocations": cfg.n_alloc, "allocations_per_gpu": count, "parallelism": f"grid-dp{world}",
+                      "l2": "flushed (512 MiB write) before every timed step, outside the step events",
+                      "best": {"index": best_idx, "cost": best_cost}},
+           "roofline": roof, "cpu_baseline": cpu,
+           "e2e": {"value": evals / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                   "api": "distill_eval_grid_host (positions in, net values + best key out, pinned host)"},
+           "clocks": clocks, "gpu_launches": launches, "gpu_launches_per_step": launches / K,
+           "also": also}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_extras(D, torch, dev, rank, world, args):
+    """DDM cfg2 and Stroop cfg4, one timed pass each (sharded over ranks)."""
+    import torch.distributed as dist
+    out = {}
+    d = W.ddm_cfg2()
+    tb, te = D.shard_range(d.n_trials, rank, world)
+    rh, rs, xh = (torch.zeros(n, dtype=torch.int64, device=dev) for n in d.hist_sizes)
+
+    def ddm_once():
+        for t in (rh, rs, xh):
+            t.zero_()
+        D.ddm_batch(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
+                    d.x_lo, d.x_hi, tb, te, d.seed, rh, rs, xh)
+        if world > 1:
+            D.hist_allreduce([rh, rs, xh])
+
+    ddm_once()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    e0.record()
+    for _ in range(reps):
+        ddm_once()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nb = d.n_rt_bins
+    up, lo = int(rh[:nb].sum()), int(rh[nb:2 * nb].sum())
+    out["ddm_cfg2"] = {"trials_per_s": d.n_trials / (ms / 1e3), "steps_per_s": d.n_trials * d.n_steps / (ms / 1e3),
+                       "ms": ms, "error_rate": lo / max(1, up + lo),
+                       "mean_rt_s": (int(rs[0]) + int(rs[1])) / max(1, up + lo) * d.dt}
+    if args.stroop:
+        c = W.stroop_cfg4()
+        m = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=dev.index)
+        sb, se = D.shard_range(c.n_alloc, rank, world)
+        net = torch.empty(max(1, se - sb), dtype=torch.float32, device=dev)
+        best = torch.empty(1, dtype=torch.int64, device=dev)
+        counts = torch.empty(3 * max(1, se - sb), dtype=torch.int64, device=dev)
+        D.key_reset(best)
+        e0.record()
+        D.eval_grid(m, None, c.n_trials, c.seed, sb, se, net=net, best=best, counts=counts)
+        if world > 1:
+            D.best_allreduce(best)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        from paper_2110_15425_b200.api import key_from_tensor
+        cost, idx = D.key_decode(key_from_tensor(best))
+        out["stroop_cfg4"] = {"evals_per_s": c.evals / (ms / 1e3),
+                              "step_updates_per_s": c.evals * c.n_steps / (ms / 1e3), "ms": ms,
+                              "best": {"index": idx, "u_c_level": idx // c.n_levels[1],
+                                       "u_s_level": idx % c.n_levels[1], "net_value": -cost}}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stroop", action="store_true", help="also time one full cfg4 Stroop grid (~seconds)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

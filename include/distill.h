@@ -1,0 +1,141 @@
+/*
+ * distill.h — C ABI of the B200 grid-search library (libdistill.so).
+ *
+ * The hot path of Distill (arXiv 2110.15425) that the paper offloads to the
+ * GPU: the Control node's exhaustive grid search, where every control
+ * allocation runs independent noisy simulations of the compiled model and the
+ * lowest-cost allocation wins (§2.1; §3.6).
+ * Exact op-by-op semantics: spec/MODELS.md and spec/RNG.md.
+ *
+ * Conventions (all entry points):
+ *   - extern "C", plain pointers and sizes; no exceptions cross the ABI and the
+ *     library never aborts.  Every call returns a distill_status; the
+ *     thread-local distill_last_error() string says why a call failed.
+ *   - "d_" pointers are DEVICE memory owned by the caller; "h_" pointers are
+ *     host memory owned by the caller.  The library owns only the model handle
+ *     and its device copy of the read-only model block.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Work is stream-ordered and asynchronous unless stated; argument errors are
+ *     detected synchronously and enqueue nothing; an asynchronous CUDA fault
+ *     surfaces as DISTILL_E_CUDA on a later call.
+ *   - A model handle is read-only during evaluation: several streams/threads may
+ *     evaluate the same handle concurrently.
+ */
+#ifndef DISTILL_H
+#define DISTILL_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DISTILL_ABI_VERSION 1
+
+typedef enum {
+    DISTILL_OK = 0,
+    DISTILL_E_INVALID_ARG = 1,  /* NULL/size/range error; nothing enqueued            */
+    DISTILL_E_OVERFLOW = 2,     /* grid > 2^32-1 allocations (key packs a 32-bit index) */
+    DISTILL_E_UNSUPPORTED = 3,  /* model kind / shape not implemented                  */
+    DISTILL_E_CUDA = 4,         /* CUDA runtime error (see distill_last_error)         */
+    DISTILL_E_NO_VALID = 5      /* key decode: no finite candidate (all NaN / empty)   */
+} distill_status;
+
+typedef enum {
+    DISTILL_MODEL_PREDATOR_PREY = 1,  /* P:140-167, Fig. 1                      */
+    DISTILL_MODEL_STROOP_LCA = 2      /* P:525 (surrogate, spec/MODELS.md §6)   */
+} distill_model_kind;
+
+/* "No candidate" value of a packed (value, index) key; initialise d_best to it. */
+#define DISTILL_KEY_INIT 0xFFFFFFFFFFFFFFFFull
+
+typedef struct distill_model distill_model;  /* opaque, library-owned */
+
+/* Model description.  Copied by distill_load_model; host arrays may be freed
+ * after it returns.  Grid = Cartesian product of the per-signal levels
+ * ("searches over all possible attention allocations"), enumerated in
+ * mixed radix with signal 0 most significant (spec/MODELS.md §1).
+ *   PREDATOR_PREY: n_signals = 3 (prey, predator, player attention);
+ *                  params = {sigma_max, sigma_min, kappa}, n_params = 3.
+ *   STROOP_LCA:    n_signals = 2 (colour attention u_c, word suppression u_s);
+ *                  params = {g_c, g_w, tau, leak, inhibition, noise, dt,
+ *                            threshold, reward, rt_cost, n_steps}, n_params = 11. */
+typedef struct {
+    uint32_t kind;               /* distill_model_kind                               */
+    uint32_t n_signals;          /* D                                                */
+    const uint32_t* n_levels;    /* host [D], each >= 1                              */
+    const float* levels;         /* host [sum n_levels], signal 0 first              */
+    const float* cost_weights;   /* host [D]: control cost K = sum_d w_d a_d */
+    const float* params;         /* host [n_params]                                  */
+    uint32_t n_params;
+} distill_model_desc;
+
+/* One grid evaluation (a shard [begin, end) of the global allocation range). */
+typedef struct {
+    const float* inputs;         /* host; PP: prey, predator, player (x, y) = 6 floats; Stroop: unused */
+    uint32_t n_inputs;
+    uint64_t begin, end;         /* global allocation indices, begin <= end <= grid size */
+    uint32_t n_samples;          /* PP: samples per allocation (>= 1); Stroop: trials T per allocation */
+    uint32_t invocation;         /* PP: controller invocation t (RNG counter word, spec/RNG.md §1); Stroop: 0 */
+    uint64_t seed;               /* Philox key */
+    float* d_net;                /* device [end-begin] or NULL: net value V = -C per allocation       */
+    unsigned long long* d_best;  /* device [1] or NULL: atomicMin of key(C_i, i) (spec/MODELS.md §3)  */
+    unsigned long long* d_counts;/* Stroop only, device [(end-begin)*3] u64 or NULL (library scratch):
+                                    {n_correct, n_undecided, rt_sum}; overwritten                     */
+    uint32_t trial_begin, trial_end; /* Stroop: simulate trials [trial_begin, trial_end) only; (0,0) = all.
+                                    d_net/d_best are produced only when the range is all T trials.    */
+} distill_eval_args;
+
+/* DDM Monte Carlo batch (Fig. 3; spec/MODELS.md §4). */
+typedef struct {
+    float drift, noise, threshold, x0, dt;  /* A, sigma, z (bounds +-z), start, step      */
+    uint32_t n_steps;                       /* fixed trip N >= 1                         */
+    uint32_t rt_bin_steps;                  /* RT bin width in steps, >= 1               */
+    uint32_t n_x_bins;                      /* endpoint bins >= 1 (+ under/overflow bins) */
+    float x_lo, x_hi;                       /* endpoint histogram range, x_lo < x_hi     */
+    uint64_t trial_begin, trial_end, seed;  /* global trial ids (RNG unit) and Philox key */
+    unsigned long long* d_rt_hist;  /* device [2*ceil(N/B)+1]: upper bins, lower bins, undecided (+=) */
+    unsigned long long* d_rt_sum;   /* device [2]: sum of first-passage steps, upper / lower      (+=) */
+    unsigned long long* d_x_hist;   /* device [n_x_bins+2]: underflow, bins, overflow              (+=) */
+} distill_ddm_args;
+
+int            distill_abi_version(void);
+const char*    distill_last_error(void);
+
+/* Validate the description and copy its read-only block to `device`. */
+distill_status distill_load_model(const distill_model_desc* desc, int device, distill_model** out);
+/* NULL-safe.  The caller synchronises streams that use the model first. */
+void           distill_free_model(distill_model* model);
+distill_status distill_grid_size(const distill_model* model, uint64_t* n_alloc);
+
+/* Evaluate allocations [begin, end): per allocation, n_samples noisy simulations
+ * averaged, plus control cost.  One fused kernel for PP;
+ * simulate + finalize kernels for Stroop.  Stream-ordered, asynchronous. */
+distill_status distill_eval_grid(const distill_model* model, const distill_eval_args* args, void* stream);
+
+/* Same evaluation from HOST buffers (the end-to-end call): copies, evaluates on
+ * `stream`, copies V (if h_net) and the best key back, synchronises the stream.
+ * Uses a library-owned device scratch area of the handle; NOT concurrent-safe per handle. */
+distill_status distill_eval_grid_host(const distill_model* model, const float* h_inputs, uint32_t n_inputs,
+                                      uint64_t begin, uint64_t end, uint32_t n_samples,
+                                      uint32_t invocation, uint64_t seed,
+                                      float* h_net, unsigned long long* h_best, void* stream);
+
+/* argmax over a device array of net values: atomicMin of key(-d_values[j], index_base + j)
+ * into *d_best (max V <=> min key, lowest index on ties). */
+distill_status distill_argmax(const float* d_values, uint64_t n, uint64_t index_base,
+                              unsigned long long* d_best, void* stream);
+/* Set *d_best = DISTILL_KEY_INIT (stream-ordered). */
+distill_status distill_key_reset(unsigned long long* d_best, void* stream);
+/* Host, pure: key -> (cost C, global index).  DISTILL_E_NO_VALID for an all-NaN/empty key. */
+distill_status distill_key_decode(unsigned long long key, float* cost, uint64_t* index);
+
+/* DDM batch over trials [trial_begin, trial_end): histograms accumulated with atomics. */
+distill_status distill_ddm_batch(const distill_ddm_args* args, void* stream);
+
+/* Kernels launched by this library since load (all threads), for launch accounting. */
+uint64_t       distill_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

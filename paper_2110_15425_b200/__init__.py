@@ -1,0 +1,22 @@
+"""B200-native grid-search hot path of Distill (arXiv 2110.15425).
+
+Public Python API (thin wrappers over the C ABI in include/distill.h):
+
+    load_model(kind, n_levels, levels, cost_weights, params, device=0) -> Model
+    eval_grid(model, inputs, n_samples, seed, begin=0, end=None, net=None, best=None, ...)
+    eval_grid_host(model, inputs, n_samples, seed, ...)   # host buffers, end to end
+    argmax(values, index_base, best)
+    key_reset(best) / key_decode(key)
+    ddm_batch(...)
+    shard_range(n, rank, world) / best_allreduce(key, group)   # multi-GPU plumbing
+
+Importing this package does not touch the GPU; the shared library is loaded
+on first use and there is no CPU fallback.
+"""
+from .api import (KEY_INIT, Model, argmax, ddm_batch, eval_grid, eval_grid_host, key_decode,
+                  key_reset, launch_count, load_model)
+from .dist import best_allreduce, hist_allreduce, key_to_i64, i64_to_key, shard_range
+
+__all__ = ["KEY_INIT", "Model", "argmax", "ddm_batch", "eval_grid", "eval_grid_host", "key_decode",
+           "key_reset", "launch_count", "load_model", "best_allreduce", "hist_allreduce", "key_to_i64",
+           "i64_to_key", "shard_range"]

@@ -1,0 +1,97 @@
+"""ctypes binding of libdistill.so (include/distill.h) — argument marshalling only.
+
+Names mirror the C ABI (``distill_load_model`` -> ``load_model`` ...).  Device
+buffers are torch CUDA tensors (PyTorch is plumbing: memory, streams, process
+groups); every step of the hot path runs in the library's kernels.  There is
+no CPU fallback: if the shared library is missing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdistill.so")
+
+OK, E_INVALID_ARG, E_OVERFLOW, E_UNSUPPORTED, E_CUDA, E_NO_VALID = range(6)
+MODEL_PREDATOR_PREY = 1
+MODEL_STROOP_LCA = 2
+KEY_INIT = 0xFFFFFFFFFFFFFFFF
+
+
+class DistillError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"distill status {status}: {msg}")
+        self.status = status
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("n_signals", C.c_uint32),
+                ("n_levels", C.POINTER(C.c_uint32)), ("levels", C.POINTER(C.c_float)),
+                ("cost_weights", C.POINTER(C.c_float)), ("params", C.POINTER(C.c_float)),
+                ("n_params", C.c_uint32)]
+
+
+class EvalArgs(C.Structure):
+    _fields_ = [("inputs", C.POINTER(C.c_float)), ("n_inputs", C.c_uint32),
+                ("begin", C.c_uint64), ("end", C.c_uint64),
+                ("n_samples", C.c_uint32), ("invocation", C.c_uint32), ("seed", C.c_uint64),
+                ("d_net", C.c_void_p), ("d_best", C.c_void_p), ("d_counts", C.c_void_p),
+                ("trial_begin", C.c_uint32), ("trial_end", C.c_uint32)]
+
+
+class DdmArgs(C.Structure):
+    _fields_ = [("drift", C.c_float), ("noise", C.c_float), ("threshold", C.c_float),
+                ("x0", C.c_float), ("dt", C.c_float), ("n_steps", C.c_uint32),
+                ("rt_bin_steps", C.c_uint32), ("n_x_bins", C.c_uint32),
+                ("x_lo", C.c_float), ("x_hi", C.c_float),
+                ("trial_begin", C.c_uint64), ("trial_end", C.c_uint64), ("seed", C.c_uint64),
+                ("d_rt_hist", C.c_void_p), ("d_rt_sum", C.c_void_p), ("d_x_hist", C.c_void_p)]
+
+
+EXPORTS = {
+    "distill_abi_version": (C.c_int, []),
+    "distill_last_error": (C.c_char_p, []),
+    "distill_load_model": (C.c_int, [C.POINTER(ModelDesc), C.c_int, C.POINTER(C.c_void_p)]),
+    "distill_free_model": (None, [C.c_void_p]),
+    "distill_grid_size": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "distill_eval_grid": (C.c_int, [C.c_void_p, C.POINTER(EvalArgs), C.c_void_p]),
+    "distill_eval_grid_host": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_uint32, C.c_uint64, C.c_uint64,
+                                         C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p,
+                                         C.POINTER(C.c_uint64), C.c_void_p]),
+    "distill_argmax": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "distill_key_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "distill_key_decode": (C.c_int, [C.c_uint64, C.POINTER(C.c_float), C.POINTER(C.c_uint64)]),
+    "distill_ddm_batch": (C.c_int, [C.POINTER(DdmArgs), C.c_void_p]),
+    "distill_launch_count": (C.c_uint64, []),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libdistill.so (raises if it has not been built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != OK:
+        raise DistillError(status, lib().distill_last_error().decode(errors="replace"))
+
+
+def _fptr(arr):
+    return arr.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _uptr(arr):
+    return arr.ctypes.data_as(C.POINTER(C.c_uint32))

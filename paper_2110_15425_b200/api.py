@@ -1,0 +1,152 @@
+"""Python face of the C ABI: the same calls, torch tensors for device memory.
+
+Each function only marshals arguments and forwards to libdistill.so
+(include/distill.h documents semantics, layouts, ownership and errors).
+Keys live in int64 tensors holding the raw unsigned 64-bit pattern.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _abi
+from ._abi import KEY_INIT, DistillError, check, lib
+
+
+def _stream_handle(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _dev_ptr(t, dtype_name: str, numel: Optional[int] = None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError(f"{dtype_name} buffer must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{dtype_name} buffer must be contiguous")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"{dtype_name} buffer too small: {t.numel()} < {numel}")
+    return t.data_ptr()
+
+
+class Model:
+    """Owns a distill_model handle (device read-only block)."""
+
+    def __init__(self, kind: int, n_levels, levels, cost_weights, params, device: int = 0):
+        self.kind = int(kind)
+        self.n_levels = np.ascontiguousarray(np.asarray(n_levels, np.uint32))
+        self.levels = np.ascontiguousarray(np.asarray(levels, np.float32))
+        self.cost_weights = np.ascontiguousarray(np.asarray(cost_weights, np.float32))
+        self.params = np.ascontiguousarray(np.asarray(params, np.float32))
+        self.device = int(device)
+        desc = _abi.ModelDesc(self.kind, self.n_levels.size, _abi._uptr(self.n_levels), _abi._fptr(self.levels),
+                              _abi._fptr(self.cost_weights), _abi._fptr(self.params), self.params.size)
+        h = C.c_void_p()
+        check(lib().distill_load_model(C.byref(desc), self.device, C.byref(h)))
+        self._h = h
+        n = C.c_uint64()
+        check(lib().distill_grid_size(self._h, C.byref(n)))
+        self.n_alloc = int(n.value)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().distill_free_model(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def load_model(kind, n_levels, levels, cost_weights, params, device: int = 0) -> Model:
+    return Model(kind, n_levels, levels, cost_weights, params, device)
+
+
+def eval_grid(model: Model, inputs, n_samples: int, seed: int, begin: int = 0, end: Optional[int] = None,
+              net=None, best=None, invocation: int = 0, counts=None, trial_range=(0, 0), stream=None) -> None:
+    """distill_eval_grid: allocations [begin, end) -> net[end-begin] (V = -C), best (atomicMin key)."""
+    end = model.n_alloc if end is None else int(end)
+    n = end - int(begin)
+    inp = np.ascontiguousarray(np.asarray(inputs if inputs is not None else np.zeros(0), np.float32))
+    a = _abi.EvalArgs()
+    a.inputs = _abi._fptr(inp) if inp.size else None
+    a.n_inputs = inp.size
+    a.begin, a.end = int(begin), end
+    a.n_samples, a.invocation, a.seed = int(n_samples), int(invocation), int(seed) & (2 ** 64 - 1)
+    a.d_net = _dev_ptr(net, "net", n)
+    a.d_best = _dev_ptr(best, "best", 1)
+    a.d_counts = _dev_ptr(counts, "counts", 3 * n)
+    a.trial_begin, a.trial_end = int(trial_range[0]), int(trial_range[1])
+    check(lib().distill_eval_grid(model.handle, C.byref(a), _stream_handle(stream)))
+
+
+def eval_grid_host(model: Model, inputs, n_samples: int, seed: int, begin: int = 0, end: Optional[int] = None,
+                   net_out: Optional[np.ndarray] = None, invocation: int = 0, stream=None) -> int:
+    """distill_eval_grid_host: host inputs in, host V (optional) and best key out; synchronous."""
+    end = model.n_alloc if end is None else int(end)
+    inp = np.ascontiguousarray(np.asarray(inputs, np.float32))
+    key = C.c_uint64()
+    net_ptr = None
+    if net_out is not None:
+        if net_out.dtype != np.float32 or not net_out.flags.c_contiguous or net_out.size < end - begin:
+            raise ValueError("net_out must be a contiguous float32 array of end-begin elements")
+        net_ptr = net_out.ctypes.data
+    check(lib().distill_eval_grid_host(model.handle, _abi._fptr(inp), inp.size, int(begin), end, int(n_samples),
+                                       int(invocation), int(seed) & (2 ** 64 - 1), net_ptr, C.byref(key),
+                                       _stream_handle(stream)))
+    return int(key.value)
+
+
+def argmax(values, index_base: int, best, stream=None) -> None:
+    """distill_argmax: atomicMin of key(-values[j], index_base + j) into best."""
+    check(lib().distill_argmax(_dev_ptr(values, "values"), values.numel(), int(index_base),
+                               _dev_ptr(best, "best", 1), _stream_handle(stream)))
+
+
+def key_reset(best, stream=None) -> None:
+    check(lib().distill_key_reset(_dev_ptr(best, "best", 1), _stream_handle(stream)))
+
+
+def key_decode(key: int):
+    """-> (cost C, global index); raises DistillError(E_NO_VALID) for an all-NaN/empty key."""
+    c = C.c_float()
+    idx = C.c_uint64()
+    st = lib().distill_key_decode(int(key) & (2 ** 64 - 1), C.byref(c), C.byref(idx))
+    check(st)
+    return c.value, int(idx.value)
+
+
+def ddm_batch(drift, noise, threshold, x0, dt, n_steps, rt_bin_steps, n_x_bins, x_lo, x_hi,
+              trial_begin, trial_end, seed, rt_hist, rt_sum, x_hist, stream=None) -> None:
+    """distill_ddm_batch: histograms (int64 tensors) accumulated on the device."""
+    a = _abi.DdmArgs(drift, noise, threshold, x0, dt, int(n_steps), int(rt_bin_steps), int(n_x_bins),
+                     x_lo, x_hi, int(trial_begin), int(trial_end), int(seed) & (2 ** 64 - 1),
+                     _dev_ptr(rt_hist, "rt_hist"), _dev_ptr(rt_sum, "rt_sum", 2), _dev_ptr(x_hist, "x_hist"))
+    nb = (int(n_steps) + int(rt_bin_steps) - 1) // int(rt_bin_steps)
+    if rt_hist.numel() < 2 * nb + 1 or x_hist.numel() < int(n_x_bins) + 2:
+        raise ValueError("histogram buffers too small")
+    check(lib().distill_ddm_batch(C.byref(a), _stream_handle(stream)))
+
+
+def launch_count() -> int:
+    return int(lib().distill_launch_count())
+
+
+def key_from_tensor(best) -> int:
+    """Raw unsigned key from an int64 tensor (one device->host read)."""
+    return int(best.reshape(-1)[0].item()) & (2 ** 64 - 1)
+
+
+__all__ = ["KEY_INIT", "DistillError", "Model", "load_model", "eval_grid", "eval_grid_host", "argmax",
+           "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor"]

@@ -1,0 +1,91 @@
+// ddm.cuh — K3 ddm_batch: fixed-trip Euler drift-diffusion Monte Carlo with
+// first-passage latching and histogram reduction (spec/MODELS.md §4;
+// PAPER.md P:466 DDM, Fig. 3; "build histograms of outcomes").
+//
+// One thread = one trial (RNG unit = global trial id); the walk runs all N
+// steps (no divergence, reading Q14).  Per block: shared-memory u32 histograms
+// -> one global u64 atomicAdd per non-empty bin at the end (grid-stride, so
+// blocks are few and the flush is amortised over many trials).
+#pragma once
+#include "rng.cuh"
+
+namespace distill {
+
+struct DDMArgs {
+    float drift, noise, threshold, x0, dt, x_lo, x_hi;
+    uint32_t n_steps, rt_bin_steps, n_rt_bins, n_x_bins;
+    uint32_t key0, key1;
+    uint64_t trial_begin, n_trials;
+    unsigned long long* __restrict__ rt_hist;  // [2*nb+1]
+    unsigned long long* __restrict__ rt_sum;   // [2]
+    unsigned long long* __restrict__ x_hist;   // [nx+2]
+};
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) ddm_batch_kernel(const DDMArgs a) {
+    extern __shared__ uint32_t s_hist[];  // [2*nb+1] rt bins then [nx+2] x bins
+    const uint32_t n_rt = 2 * a.n_rt_bins + 1, n_x = a.n_x_bins + 2, n_all = n_rt + n_x;
+    for (uint32_t b = threadIdx.x; b < n_all; b += BLOCK) s_hist[b] = 0;
+    __syncthreads();
+
+    const float nsd = __fmul_rn(a.noise, __fsqrt_rn(a.dt));
+    const float sc = __fdiv_rn(__uint2float_rn(a.n_x_bins), __fadd_rn(a.x_hi, -a.x_lo));
+    const float fnx = __uint2float_rn(a.n_x_bins);
+    const float z = a.threshold, nz = -a.threshold;
+    unsigned long long sum_up = 0, sum_lo = 0;
+
+    for (uint64_t t = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; t < a.n_trials;
+         t += (uint64_t)gridDim.x * BLOCK) {
+        const uint64_t unit = a.trial_begin + t;
+        float x = a.x0;
+        uint32_t st = 0, ch = 2;
+        const uint32_t nblk = (a.n_steps + 3) >> 2;
+        for (uint32_t kb = 0; kb < nblk; ++kb) {
+            const float4 g = normal_quad(unit, kb, a.key0, a.key1);
+            const float gg[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const uint32_t n = 4 * kb + l + 1;
+                if (n <= a.n_steps) {
+                    x = __fmaf_rn(nsd, gg[l], __fmaf_rn(a.dt, a.drift, x));
+                    if (st == 0) {
+                        if (x >= z) { st = n; ch = 0; }
+                        else if (x <= nz) { st = n; ch = 1; }
+                    }
+                }
+            }
+        }
+        uint32_t rb;
+        if (ch == 2) rb = 2 * a.n_rt_bins;
+        else rb = ch * a.n_rt_bins + (st - 1) / a.rt_bin_steps;
+        atomicAdd(&s_hist[rb], 1u);
+        if (ch == 0) sum_up += st;
+        else if (ch == 1) sum_lo += st;
+        const float u = __fmul_rn(__fadd_rn(x, -a.x_lo), sc);
+        uint32_t xb;
+        if (u < 0.0f) xb = 0;
+        else if (!(u < fnx)) xb = a.n_x_bins + 1;
+        else xb = 1 + (uint32_t)u;
+        atomicAdd(&s_hist[n_rt + xb], 1u);
+    }
+    // rt sums: warp reduce then one atomic per warp
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        sum_up += __shfl_xor_sync(0xFFFFFFFFu, sum_up, off);
+        sum_lo += __shfl_xor_sync(0xFFFFFFFFu, sum_lo, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (sum_up) atomicAdd(a.rt_sum + 0, sum_up);
+        if (sum_lo) atomicAdd(a.rt_sum + 1, sum_lo);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < n_all; b += BLOCK) {
+        const uint32_t v = s_hist[b];
+        if (v) {
+            if (b < n_rt) atomicAdd(a.rt_hist + b, (unsigned long long)v);
+            else atomicAdd(a.x_hist + (b - n_rt), (unsigned long long)v);
+        }
+    }
+}
+
+}  // namespace distill

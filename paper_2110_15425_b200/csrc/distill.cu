@@ -1,0 +1,356 @@
+// distill.cu — host side of the C ABI declared in include/distill.h:
+// validation, the model handle (device read-only block), launch
+// configuration, and the host-buffer end-to-end entry.  All arithmetic of the
+// hot path runs in the kernels of pp.cuh / keys.cuh / ddm.cuh / stroop.cuh.
+#include "../../include/distill.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "ddm.cuh"
+#include "keys.cuh"
+#include "pp.cuh"
+#include "stroop.cuh"
+
+using namespace distill;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+distill_status fail(distill_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (expr);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(DISTILL_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                              \
+    } while (0)
+
+constexpr int PP_BLOCK = 256;
+constexpr int ARGMAX_BLOCK = 256;
+constexpr int DDM_BLOCK = 256;
+constexpr int STROOP_BLOCK = 256;
+
+}  // namespace
+
+struct distill_model {
+    uint32_t kind = 0, D = 0;
+    int device = 0;
+    uint32_t L[8] = {0};
+    uint64_t n_alloc = 0;
+    float w[8] = {0};
+    std::vector<float> params;
+    float* d_levels = nullptr;      // device RO block
+    int n_sm = 148;
+    // scratch for the host-buffer entry and Stroop counts (lazily grown)
+    std::mutex scratch_mu;
+    void* d_scratch = nullptr;
+    size_t scratch_bytes = 0;
+};
+
+static distill_status ensure_scratch(distill_model* m, size_t bytes) {
+    if (m->scratch_bytes >= bytes) return DISTILL_OK;
+    if (m->d_scratch) cudaFree(m->d_scratch);
+    m->d_scratch = nullptr;
+    m->scratch_bytes = 0;
+    CUDA_TRY(cudaMalloc(&m->d_scratch, bytes));
+    m->scratch_bytes = bytes;
+    return DISTILL_OK;
+}
+
+extern "C" {
+
+int distill_abi_version(void) { return DISTILL_ABI_VERSION; }
+
+const char* distill_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t distill_launch_count(void) { return g_launches.load(); }
+
+distill_status distill_load_model(const distill_model_desc* desc, int device, distill_model** out) {
+    if (!desc || !out) return fail(DISTILL_E_INVALID_ARG, "load_model: NULL desc/out");
+    *out = nullptr;
+    if (!desc->n_levels || !desc->levels || !desc->cost_weights || (!desc->params && desc->n_params))
+        return fail(DISTILL_E_INVALID_ARG, "load_model: NULL array in desc");
+    uint32_t want_D, want_p;
+    if (desc->kind == DISTILL_MODEL_PREDATOR_PREY) { want_D = 3; want_p = 3; }
+    else if (desc->kind == DISTILL_MODEL_STROOP_LCA) { want_D = 2; want_p = 11; }
+    else return fail(DISTILL_E_UNSUPPORTED, "load_model: unknown model kind %u", desc->kind);
+    if (desc->n_signals != want_D)
+        return fail(DISTILL_E_UNSUPPORTED, "load_model: kind %u needs %u signals, got %u", desc->kind, want_D,
+                    desc->n_signals);
+    if (desc->n_params != want_p)
+        return fail(DISTILL_E_INVALID_ARG, "load_model: kind %u needs %u params, got %u", desc->kind, want_p,
+                    desc->n_params);
+    uint64_t n = 1, total = 0;
+    for (uint32_t d = 0; d < want_D; ++d) {
+        if (desc->n_levels[d] == 0) return fail(DISTILL_E_INVALID_ARG, "load_model: signal %u has 0 levels", d);
+        n *= desc->n_levels[d];
+        total += desc->n_levels[d];
+        if (n > 0xFFFFFFFFull)
+            return fail(DISTILL_E_OVERFLOW, "load_model: grid exceeds 2^32-1 allocations");
+    }
+    if (desc->kind == DISTILL_MODEL_STROOP_LCA) {
+        const float ns = desc->params[10];
+        if (!(ns >= 1.0f) || ns != std::floor(ns) || ns > 1e7f)
+            return fail(DISTILL_E_INVALID_ARG, "load_model: Stroop n_steps must be a positive integer");
+    }
+    int n_dev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&n_dev));
+    if (device < 0 || device >= n_dev) return fail(DISTILL_E_INVALID_ARG, "load_model: bad device %d", device);
+    distill_model* m = new (std::nothrow) distill_model();
+    if (!m) return fail(DISTILL_E_CUDA, "load_model: out of host memory");
+    m->kind = desc->kind;
+    m->D = want_D;
+    m->device = device;
+    m->n_alloc = n;
+    for (uint32_t d = 0; d < want_D; ++d) {
+        m->L[d] = desc->n_levels[d];
+        m->w[d] = desc->cost_weights[d];
+    }
+    m->params.assign(desc->params, desc->params + desc->n_params);
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&m->n_sm, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_levels, total * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(m->d_levels, desc->levels, total * sizeof(float), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (m->d_levels) cudaFree(m->d_levels);
+        delete m;
+        return fail(DISTILL_E_CUDA, "load_model: %s", cudaGetErrorString(e));
+    }
+    *out = m;
+    return DISTILL_OK;
+}
+
+void distill_free_model(distill_model* m) {
+    if (!m) return;
+    cudaSetDevice(m->device);
+    if (m->d_levels) cudaFree(m->d_levels);
+    if (m->d_scratch) cudaFree(m->d_scratch);
+    delete m;
+}
+
+distill_status distill_grid_size(const distill_model* m, uint64_t* n_alloc) {
+    if (!m || !n_alloc) return fail(DISTILL_E_INVALID_ARG, "grid_size: NULL argument");
+    *n_alloc = m->n_alloc;
+    return DISTILL_OK;
+}
+
+static distill_status launch_pp(const distill_model* m, const distill_eval_args* a, cudaStream_t st) {
+    if (!a->inputs || a->n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): needs 6 host inputs");
+    if (a->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): n_samples must be >= 1");
+    if ((a->trial_begin | a->trial_end) != 0)
+        return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): trial range is a Stroop-only field");
+    const uint64_t count = a->end - a->begin;
+    if (count == 0) return DISTILL_OK;
+    PPArgs p;
+    p.prey_x = a->inputs[0]; p.prey_y = a->inputs[1];
+    p.pred_x = a->inputs[2]; p.pred_y = a->inputs[3];
+    p.pl_x = a->inputs[4]; p.pl_y = a->inputs[5];
+    p.sigma_max = m->params[0]; p.sigma_min = m->params[1]; p.kappa = m->params[2];
+    p.w0 = m->w[0]; p.w1 = m->w[1]; p.w2 = m->w[2];
+    p.L0 = m->L[0]; p.L1 = m->L[1]; p.L2 = m->L[2];
+    p.n_samples = a->n_samples; p.invocation = a->invocation;
+    p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
+    p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
+    p.levels = m->d_levels; p.net = a->d_net; p.best = a->d_best;
+    const unsigned grid = (unsigned)((count + PP_BLOCK - 1) / PP_BLOCK);
+    pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+static distill_status launch_stroop(distill_model* m, const distill_eval_args* a, cudaStream_t st) {
+    if (a->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop): n_samples (trials) must be >= 1");
+    if (a->invocation != 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop): invocation must be 0");
+    uint32_t tb = a->trial_begin, te = a->trial_end;
+    if (tb == 0 && te == 0) te = a->n_samples;
+    if (tb > te || te > a->n_samples) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop): bad trial range");
+    const bool full = (tb == 0 && te == a->n_samples);
+    const uint64_t count = a->end - a->begin;
+    if (count == 0) return DISTILL_OK;
+    if (a->n_samples > 0 && (uint64_t)m->n_alloc * a->n_samples >= (1ull << 63))
+        return fail(DISTILL_E_OVERFLOW, "eval_grid(Stroop): RNG unit id overflow");
+    unsigned long long* counts = a->d_counts;
+    std::unique_lock<std::mutex> lock(m->scratch_mu, std::defer_lock);
+    if (!counts) {
+        lock.lock();
+        distill_status s = ensure_scratch(m, count * 3 * sizeof(unsigned long long));
+        if (s != DISTILL_OK) return s;
+        counts = (unsigned long long*)m->d_scratch;
+    }
+    CUDA_TRY(cudaMemsetAsync(counts, 0, count * 3 * sizeof(unsigned long long), st));
+    StroopArgs p;
+    const float* P = m->params.data();
+    p.g_c = P[0]; p.g_w = P[1]; p.tau = P[2]; p.leak = P[3]; p.inh = P[4]; p.noise = P[5];
+    p.dt = P[6]; p.thr = P[7]; p.reward = P[8]; p.rt_cost = P[9]; p.n_steps = (uint32_t)P[10];
+    p.w0 = m->w[0]; p.w1 = m->w[1];
+    p.L0 = m->L[0]; p.L1 = m->L[1];
+    p.n_trials = a->n_samples; p.trial_begin = tb; p.trial_end = te;
+    p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
+    p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
+    p.levels = m->d_levels; p.counts = counts; p.net = a->d_net; p.best = a->d_best;
+    const uint32_t tr = te - tb;
+    if (tr > 0) {
+        // enough blocks along trials to fill the machine, capped so each thread runs >= 1 trial
+        uint32_t chunks = (tr + STROOP_BLOCK - 1) / STROOP_BLOCK;
+        const uint64_t want = (uint64_t)m->n_sm * 8;
+        if ((uint64_t)chunks * count > want * 64) {
+            const uint64_t c2 = (want * 64 + count - 1) / count;
+            chunks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(chunks, c2));
+        }
+        for (uint64_t off = 0; off < count; off += 65535) {
+            const unsigned gy = (unsigned)std::min<uint64_t>(65535, count - off);
+            stroop_sim_kernel<STROOP_BLOCK><<<dim3(chunks, gy), STROOP_BLOCK, 0, st>>>(p, (uint32_t)off);
+            g_launches++;
+            CUDA_TRY(cudaGetLastError());
+        }
+    }
+    if (full && (a->d_net || a->d_best)) {
+        const unsigned grid = (unsigned)((count + STROOP_BLOCK - 1) / STROOP_BLOCK);
+        stroop_finalize_kernel<STROOP_BLOCK><<<grid, STROOP_BLOCK, 0, st>>>(p);
+        g_launches++;
+        CUDA_TRY(cudaGetLastError());
+    }
+    return DISTILL_OK;
+}
+
+distill_status distill_eval_grid(const distill_model* mc, const distill_eval_args* a, void* stream) {
+    if (!mc || !a) return fail(DISTILL_E_INVALID_ARG, "eval_grid: NULL model/args");
+    distill_model* m = const_cast<distill_model*>(mc);
+    if (a->begin > a->end || a->end > m->n_alloc)
+        return fail(DISTILL_E_INVALID_ARG, "eval_grid: range [%llu, %llu) outside grid of %llu",
+                    (unsigned long long)a->begin, (unsigned long long)a->end, (unsigned long long)m->n_alloc);
+    if (a->d_net && (reinterpret_cast<uintptr_t>(a->d_net) & 3u))
+        return fail(DISTILL_E_INVALID_ARG, "eval_grid: d_net must be 4-byte aligned");
+    if (a->d_best && (reinterpret_cast<uintptr_t>(a->d_best) & 7u))
+        return fail(DISTILL_E_INVALID_ARG, "eval_grid: d_best must be 8-byte aligned");
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (m->kind == DISTILL_MODEL_PREDATOR_PREY) return launch_pp(m, a, st);
+    return launch_stroop(m, a, st);
+}
+
+distill_status distill_eval_grid_host(const distill_model* mc, const float* h_inputs, uint32_t n_inputs,
+                                      uint64_t begin, uint64_t end, uint32_t n_samples, uint32_t invocation,
+                                      uint64_t seed, float* h_net, unsigned long long* h_best, void* stream) {
+    if (!mc || !h_best) return fail(DISTILL_E_INVALID_ARG, "eval_grid_host: NULL model/h_best");
+    distill_model* m = const_cast<distill_model*>(mc);
+    if (m->kind != DISTILL_MODEL_PREDATOR_PREY)
+        return fail(DISTILL_E_UNSUPPORTED, "eval_grid_host: predator-prey models only");
+    if (begin > end || end > m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "eval_grid_host: bad range");
+    CUDA_TRY(cudaSetDevice(m->device));
+    std::lock_guard<std::mutex> lock(m->scratch_mu);
+    const uint64_t count = end - begin;
+    const size_t net_off = 256;
+    distill_status s = ensure_scratch(m, net_off + count * sizeof(float));
+    if (s != DISTILL_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* d_best = (unsigned long long*)m->d_scratch;
+    float* d_net = h_net ? (float*)((char*)m->d_scratch + net_off) : nullptr;
+    // Host->device: this step's inputs (the 6 positions, 24 B) travel inside the
+    // kernel's launch parameters; device->host: V (if h_net) and the best key.
+    if (!h_inputs || n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "eval_grid_host: needs 6 inputs");
+    CUDA_TRY(cudaMemsetAsync(d_best, 0xFF, sizeof(unsigned long long), st));
+    distill_eval_args a;
+    memset(&a, 0, sizeof a);
+    a.inputs = h_inputs; a.n_inputs = n_inputs; a.begin = begin; a.end = end;
+    a.n_samples = n_samples; a.invocation = invocation; a.seed = seed;
+    a.d_net = d_net; a.d_best = d_best;
+    s = launch_pp(m, &a, st);
+    if (s != DISTILL_OK) return s;
+    if (h_net) CUDA_TRY(cudaMemcpyAsync(h_net, d_net, count * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(h_best, d_best, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return DISTILL_OK;
+}
+
+distill_status distill_argmax(const float* d_values, uint64_t n, uint64_t index_base,
+                              unsigned long long* d_best, void* stream) {
+    if (!d_best || (!d_values && n)) return fail(DISTILL_E_INVALID_ARG, "argmax: NULL pointer");
+    if (index_base + n > 0x100000000ull) return fail(DISTILL_E_OVERFLOW, "argmax: index exceeds 32 bits");
+    if (n == 0) return DISTILL_OK;
+    int dev = 0, n_sm = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    const uint64_t need = (n / 4 + ARGMAX_BLOCK - 1) / ARGMAX_BLOCK + 1;
+    const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)n_sm * 8);
+    argmax_net_kernel<ARGMAX_BLOCK><<<grid, ARGMAX_BLOCK, 0, (cudaStream_t)stream>>>(d_values, n, (uint32_t)index_base,
+                                                                                      d_best);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+distill_status distill_key_reset(unsigned long long* d_best, void* stream) {
+    if (!d_best) return fail(DISTILL_E_INVALID_ARG, "key_reset: NULL");
+    CUDA_TRY(cudaMemsetAsync(d_best, 0xFF, sizeof(unsigned long long), (cudaStream_t)stream));
+    return DISTILL_OK;
+}
+
+distill_status distill_key_decode(unsigned long long key, float* cost, uint64_t* index) {
+    if (!cost || !index) return fail(DISTILL_E_INVALID_ARG, "key_decode: NULL");
+    const uint32_t hi = (uint32_t)(key >> 32);
+    *index = (uint32_t)key;
+    if (hi == 0xFFFFFFFFu) {
+        *cost = NAN;
+        return fail(DISTILL_E_NO_VALID, "key_decode: no valid candidate");
+    }
+    const uint32_t b = (hi >> 31) ? (hi & 0x7FFFFFFFu) : ~hi;
+    memcpy(cost, &b, 4);
+    return DISTILL_OK;
+}
+
+distill_status distill_ddm_batch(const distill_ddm_args* a, void* stream) {
+    if (!a || !a->d_rt_hist || !a->d_rt_sum || !a->d_x_hist)
+        return fail(DISTILL_E_INVALID_ARG, "ddm_batch: NULL argument");
+    if (a->n_steps == 0 || a->rt_bin_steps == 0 || a->n_x_bins == 0)
+        return fail(DISTILL_E_INVALID_ARG, "ddm_batch: n_steps, rt_bin_steps, n_x_bins must be >= 1");
+    if (!(a->x_lo < a->x_hi) || !(a->dt >= 0.0f)) return fail(DISTILL_E_INVALID_ARG, "ddm_batch: bad x range / dt");
+    if (a->trial_begin > a->trial_end) return fail(DISTILL_E_INVALID_ARG, "ddm_batch: bad trial range");
+    const uint32_t nb = (a->n_steps + a->rt_bin_steps - 1) / a->rt_bin_steps;
+    const size_t smem = (size_t)(2 * nb + 1 + a->n_x_bins + 2) * sizeof(uint32_t);
+    if (smem > 160 * 1024) return fail(DISTILL_E_UNSUPPORTED, "ddm_batch: histograms exceed shared memory");
+    const uint64_t n = a->trial_end - a->trial_begin;
+    if (n == 0) return DISTILL_OK;
+    int dev = 0, n_sm = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    if (smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(ddm_batch_kernel<DDM_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    DDMArgs p;
+    p.drift = a->drift; p.noise = a->noise; p.threshold = a->threshold; p.x0 = a->x0; p.dt = a->dt;
+    p.x_lo = a->x_lo; p.x_hi = a->x_hi;
+    p.n_steps = a->n_steps; p.rt_bin_steps = a->rt_bin_steps; p.n_rt_bins = nb; p.n_x_bins = a->n_x_bins;
+    p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
+    p.trial_begin = a->trial_begin; p.n_trials = n;
+    p.rt_hist = a->d_rt_hist; p.rt_sum = a->d_rt_sum; p.x_hist = a->d_x_hist;
+    const uint64_t need = (n + DDM_BLOCK - 1) / DDM_BLOCK;
+    const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)n_sm * 1024);
+    ddm_batch_kernel<DDM_BLOCK><<<grid, DDM_BLOCK, smem, (cudaStream_t)stream>>>(p);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// stroop.cuh — K4 stroop_eval_grid: Stroop-LCA control grid (spec/MODELS.md §6;
+// PAPER.md P:525 Botvinick Stroop, LCA accumulation P:466).
+//
+// Simulate kernel: blockIdx.y = allocation, blocks along x stride over that
+// allocation's trials; one thread = one (allocation, trial) simulation of
+// N steps (pathway integration + 2-unit rectified LCA + first-passage latch).
+// Outcomes are exact integers, block-reduced and atomically added per
+// allocation, so the result is independent of the reduction order.
+// Finalize kernel: per allocation V in binary64 from the integers, key, argmax.
+#pragma once
+#include "keys.cuh"
+#include "rng.cuh"
+
+namespace distill {
+
+struct StroopArgs {
+    float g_c, g_w, tau, leak, inh, noise, dt, thr, reward, rt_cost;
+    uint32_t n_steps;
+    float w0, w1;
+    uint32_t L0, L1;
+    uint32_t n_trials, trial_begin, trial_end;
+    uint32_t key0, key1;
+    uint32_t begin, count;                     // allocation range of this launch
+    const float* __restrict__ levels;          // L0 + L1 floats
+    unsigned long long* __restrict__ counts;   // [count][3]
+    float* __restrict__ net;
+    key_t* __restrict__ best;
+};
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) stroop_sim_kernel(const StroopArgs a, uint32_t alloc_off) {
+    const uint32_t t_alloc = alloc_off + blockIdx.y;           // index within [0, count)
+    const uint32_t i = a.begin + t_alloc;
+    const uint32_t k1 = i % a.L1, k0 = i / a.L1;
+    const float uc = __ldg(a.levels + k0), us = __ldg(a.levels + a.L0 + k1);
+    const float ic = __fmul_rn(a.g_c, uc);
+    const float iw = __fmul_rn(a.g_w, __fadd_rn(1.0f, -us));
+    const float nsd = __fmul_rn(a.noise, __fsqrt_rn(a.dt));
+    const float nleak = -a.leak, ninh = -a.inh;
+
+    uint32_t n_corr = 0, n_und = 0;
+    unsigned long long rts = 0;
+    for (uint32_t j = a.trial_begin + blockIdx.x * BLOCK + threadIdx.x; j < a.trial_end;
+         j += gridDim.x * BLOCK) {
+        const uint32_t kind = j % 3, colour = (j / 3) & 1;
+        const int word = (kind == 0) ? (int)colour : (kind == 1) ? (int)(1 - colour) : -1;
+        const float I0 = __fadd_rn(colour == 0 ? ic : 0.0f, word == 0 ? iw : 0.0f);
+        const float I1 = __fadd_rn(colour == 1 ? ic : 0.0f, word == 1 ? iw : 0.0f);
+        const uint64_t unit = (uint64_t)i * a.n_trials + j;
+        float h0 = 0.f, h1 = 0.f, x0 = 0.f, x1 = 0.f;
+        int resp = -1;
+        uint32_t st = 0;
+        const uint32_t nblk = (a.n_steps + 1) >> 1;   // 2 steps per quad block
+        for (uint32_t kb = 0; kb < nblk; ++kb) {
+            const float4 g = normal_quad(unit, kb, a.key0, a.key1);
+#pragma unroll
+            for (int l = 0; l < 2; ++l) {
+                const uint32_t n = 2 * kb + l + 1;
+                if (n <= a.n_steps) {
+                    h0 = __fmaf_rn(a.tau, __fadd_rn(I0, -h0), h0);
+                    h1 = __fmaf_rn(a.tau, __fadd_rn(I1, -h1), h1);
+                    const float g0 = l ? g.z : g.x, g1 = l ? g.w : g.y;
+                    const float q0 = __fmaf_rn(ninh, x1, __fmaf_rn(nleak, x0, h0));
+                    const float q1 = __fmaf_rn(ninh, x0, __fmaf_rn(nleak, x1, h1));
+                    const float y0 = __fmaf_rn(nsd, g0, __fmaf_rn(a.dt, q0, x0));
+                    const float y1 = __fmaf_rn(nsd, g1, __fmaf_rn(a.dt, q1, x1));
+                    x0 = fmaxf(y0, 0.0f);
+                    x1 = fmaxf(y1, 0.0f);
+                    if (resp < 0) {
+                        if (x0 >= a.thr) { resp = 0; st = n; }
+                        else if (x1 >= a.thr) { resp = 1; st = n; }
+                    }
+                }
+            }
+        }
+        if (resp < 0) ++n_und;
+        else { n_corr += ((uint32_t)resp == colour); rts += st; }
+    }
+    // block reduction of the three integer outcomes
+    __shared__ unsigned long long s_red[3][BLOCK / 32];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        n_corr += __shfl_xor_sync(0xFFFFFFFFu, n_corr, off);
+        n_und += __shfl_xor_sync(0xFFFFFFFFu, n_und, off);
+        rts += __shfl_xor_sync(0xFFFFFFFFu, rts, off);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { s_red[0][wid] = n_corr; s_red[1][wid] = n_und; s_red[2][wid] = rts; }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        unsigned long long v = 0;
+        for (int w = 0; w < BLOCK / 32; ++w) v += s_red[threadIdx.x][w];
+        if (v) atomicAdd(a.counts + 3ull * t_alloc + threadIdx.x, v);
+    }
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) stroop_finalize_kernel(const StroopArgs a) {
+    const uint32_t t = blockIdx.x * BLOCK + threadIdx.x;
+    key_t k = KEY_INIT;
+    if (t < a.count) {
+        const uint32_t i = a.begin + t;
+        const uint32_t k1 = i % a.L1, k0 = i / a.L1;
+        const float uc = __ldg(a.levels + k0), us = __ldg(a.levels + a.L0 + k1);
+        const unsigned long long nc = a.counts[3ull * t], nu = a.counts[3ull * t + 1], rs = a.counts[3ull * t + 2];
+        const double T = (double)a.n_trials, N = (double)a.n_steps;
+        double v = __ddiv_rn(__dmul_rn((double)a.reward, (double)nc), T);
+        v = __dsub_rn(v, __ddiv_rn(__dmul_rn(__dmul_rn((double)a.rt_cost, (double)a.dt),
+                                             __dadd_rn((double)rs, __dmul_rn((double)nu, N))), T));
+        v = __dsub_rn(v, __dadd_rn(__dmul_rn((double)a.w0, (double)uc), __dmul_rn((double)a.w1, (double)us)));
+        const float V = __double2float_rn(v);
+        if (a.net) a.net[t] = V;
+        k = make_key(-V, i);
+    }
+    if (a.best) block_min_key_atomic<BLOCK>(k, a.best);
+}
+
+}  // namespace distill

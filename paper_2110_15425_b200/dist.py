@@ -1,0 +1,65 @@
+"""Multi-GPU plumbing: contiguous grid shards and the single key all-reduce.
+
+The paper gives each CPU thread "a segment of the grid search space"
+(P:349-352); here each rank (one process per GPU) owns one contiguous shard
+of the global allocation range, runs the fused kernel on it, and the shards'
+best keys are combined with ONE all-reduce of an int64 (NCCL over NVLink /
+NVSwitch; gloo in the CPU tests).  DDM trial shards combine their u64
+histograms with one SUM all-reduce.  Both reductions are associative and
+commutative over exact integers, so results are bit-identical for any world
+size (spec/MODELS.md §3).
+"""
+from __future__ import annotations
+
+from typing import Tuple
+
+SIGN = 1 << 63
+MASK = (1 << 64) - 1
+
+
+def shard_range(n: int, rank: int, world: int, align: int = 4) -> Tuple[int, int]:
+    """Contiguous shard [b, e) of [0, n) for `rank`: ceil(n/world) rounded up to
+    a multiple of `align` per rank (the last ranks may be short or empty)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    per = -(-n // world)
+    per = -(-per // align) * align
+    b = min(n, rank * per)
+    e = min(n, b + per)
+    return b, e
+
+
+def key_to_i64(key: int) -> int:
+    """Unsigned key -> signed int64 with the same order (flip bit 63)."""
+    v = (int(key) & MASK) ^ SIGN
+    return v - (1 << 64) if v >= SIGN else v
+
+
+def i64_to_key(v: int) -> int:
+    return (int(v) & MASK) ^ SIGN
+
+
+def best_allreduce(best, group=None):
+    """In-place: global min key across ranks.  `best` is an int64 tensor with the
+    raw key bits; flips bit 63 so signed MIN == unsigned min, all-reduces, flips back."""
+    import torch
+    import torch.distributed as dist
+    flip = torch.tensor(-(1 << 63), dtype=torch.int64, device=best.device)
+    best.bitwise_xor_(flip)
+    dist.all_reduce(best, op=dist.ReduceOp.MIN, group=group)
+    best.bitwise_xor_(flip)
+    return best
+
+
+def hist_allreduce(tensors, group=None):
+    """SUM all-reduce of int64 histograms (DDM trial shards), fused into one call."""
+    import torch
+    import torch.distributed as dist
+    flat = torch.cat([t.reshape(-1) for t in tensors])
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    off = 0
+    for t in tensors:
+        n = t.numel()
+        t.copy_(flat[off:off + n].view_as(t))
+        off += n
+    return tensors

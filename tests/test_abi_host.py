@@ -1,0 +1,101 @@
+"""CPU-only checks of the boundary: libdistill.so loads, exports every symbol
+include/distill.h declares, validates arguments before touching CUDA, and its
+pure host key decoder agrees with the oracle's key encoder.  No kernel runs."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def abi():
+    import __graft_entry__ as g
+    g.build_cuda()
+    from paper_2110_15425_b200 import _abi
+    return _abi
+
+
+def test_every_declared_symbol_is_exported(abi):
+    hdr = open(os.path.join(ROOT, "include", "distill.h")).read()
+    names = set(re.findall(r"\b(distill_[a-z_0-9]+)\s*\(", hdr))
+    assert len(names) >= 12
+    L = abi.lib()
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(abi.EXPORTS) == names
+
+
+def test_abi_version_matches_header(abi):
+    hdr = open(os.path.join(ROOT, "include", "distill.h")).read()
+    v = int(re.search(r"#define DISTILL_ABI_VERSION (\d+)", hdr).group(1))
+    assert abi.lib().distill_abi_version() == v
+
+
+def test_library_has_sm100a_code():
+    import subprocess
+    lib = os.path.join(ROOT, "paper_2110_15425_b200", "libdistill.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _desc(abi, kind=1, D=3, L=(2, 2, 2), n_params=3):
+    L = np.asarray(L, np.uint32)
+    lev = np.zeros(int(L.sum()), np.float32)
+    w = np.zeros(D, np.float32)
+    p = np.zeros(max(n_params, 1), np.float32)
+    keep = (L, lev, w, p)
+    d = abi.ModelDesc(kind, D, abi._uptr(L), abi._fptr(lev), abi._fptr(w), abi._fptr(p), n_params)
+    return d, keep
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(kind=99), 3),                               # unknown kind -> UNSUPPORTED
+    (dict(D=2, L=(2, 2)), 3),                         # PP needs 3 signals
+    (dict(L=(2, 0, 2)), 1),                           # zero levels -> INVALID_ARG
+    (dict(n_params=2), 1),                            # wrong param count
+    (dict(L=(65536, 65536, 2)), 2),                   # > 2^32-1 allocations -> OVERFLOW
+])
+def test_load_model_validates_before_cuda(abi, kw, status):
+    import ctypes as C
+    d, keep = _desc(abi, **kw)
+    h = C.c_void_p()
+    st = abi.lib().distill_load_model(C.byref(d), 0, C.byref(h))
+    assert st == status, abi.lib().distill_last_error()
+    assert not h.value
+    assert abi.lib().distill_last_error()
+
+
+def test_null_arguments_rejected(abi):
+    import ctypes as C
+    L = abi.lib()
+    assert L.distill_load_model(None, 0, None) == abi.E_INVALID_ARG
+    assert L.distill_eval_grid(None, None, None) == abi.E_INVALID_ARG
+    assert L.distill_ddm_batch(None, None) == abi.E_INVALID_ARG
+    assert L.distill_argmax(None, 10, 0, None, None) == abi.E_INVALID_ARG
+    L.distill_free_model(None)  # NULL-safe
+
+
+def test_key_decode_inverts_oracle_keys(abi, orc):
+    import ctypes as C
+    rng = np.random.default_rng(1)
+    vals = list(rng.normal(size=50).astype(np.float32) * 1e3) + [0.0, -0.0, np.inf, -np.inf, 1e-40]
+    for i, v in enumerate(vals):
+        k = orc.key(float(v), 1000 + i)
+        c, idx = C.c_float(), C.c_uint64()
+        assert abi.lib().distill_key_decode(k, C.byref(c), C.byref(idx)) == abi.OK
+        assert idx.value == 1000 + i
+        assert c.value == (0.0 if v == 0 else float(np.float32(v)))
+    c, idx = C.c_float(), C.c_uint64()
+    assert abi.lib().distill_key_decode(orc.key(float("nan"), 3), C.byref(c), C.byref(idx)) == abi.E_NO_VALID
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2110_15425_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"(import\s+oracle|from\s+oracle|liboracle|distill_oracle|\bod_[a-z])", src), f

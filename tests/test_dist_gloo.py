@@ -1,0 +1,101 @@
+"""Multi-rank host logic on CPU (gloo, world size 2): contiguous shards, the
+key all-reduce (int64 MIN with bit 63 flipped) and the histogram SUM give the
+single-process result bit-exactly.  Shard evaluation uses the oracle here;
+on GPUs the same code path runs the CUDA kernels with NCCL."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_shard_range_partitions():
+    from paper_2110_15425_b200.dist import shard_range
+    for n in (0, 1, 3, 27, 1000, 999_999, 8_000_000):
+        for world in range(1, 9):
+            rs = [shard_range(n, r, world) for r in range(world)]
+            covered = []
+            for b, e in rs:
+                assert 0 <= b <= e <= n
+                assert b % 4 == 0 or b == n
+                covered.extend(range(b, e)) if n < 5000 else None
+            if n < 5000:
+                assert covered == list(range(n))
+            else:
+                assert rs[0][0] == 0 and rs[-1][1] == n
+                assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1) if rs[i + 1][0] < n)
+
+
+def test_key_flip_order():
+    from paper_2110_15425_b200.dist import i64_to_key, key_to_i64
+    rng = np.random.default_rng(0)
+    keys = [int(x) for x in rng.integers(0, 2 ** 63, 200, dtype=np.uint64)] + [0, 2 ** 64 - 1, 2 ** 63, 2 ** 63 - 1]
+    keys += [k | (1 << 63) for k in keys[:50]]
+    assert sorted(keys) == sorted(keys, key=key_to_i64)
+    assert all(i64_to_key(key_to_i64(k)) == k for k in keys)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2110_15425_b200.dist import best_allreduce, hist_allreduce, shard_range
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = W.PPConfig("g", (6, 7, 5), 12)
+    b, e = shard_range(cfg.n_alloc, rank, world)
+    C = oracle.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, b, e, cfg.n_samples, cfg.seed)
+    k, _ = oracle.argmax_net(-C, b)
+    u = k if k < 2 ** 63 else k - 2 ** 64        # raw bits into int64 storage
+    best = torch.tensor([u], dtype=torch.int64)
+    best_allreduce(best)
+    key = int(best.item()) & (2 ** 64 - 1)
+    d = W.DDMConfig(n_steps=120)
+    p = oracle.ddm_params(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
+                          d.x_lo, d.x_hi)
+    tb, te = shard_range(600, rank, world)
+    h = [torch.from_numpy(x.astype(np.int64)) for x in oracle.ddm_batch(p, 5, tb, te)]
+    hist_allreduce(h)
+    q.put((rank, key, [x.numpy().copy() for x in h]))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_key_and_hist_allreduce(orc):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = W.PPConfig("g", (6, 7, 5), 12)
+    C = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc, cfg.n_samples,
+                    cfg.seed)
+    k_full, _ = orc.argmax_net(-C)
+    d = W.DDMConfig(n_steps=120)
+    p = orc.ddm_params(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
+                       d.x_lo, d.x_hi)
+    h_full = orc.ddm_batch(p, 5, 0, 600)
+    for rank, key, h in res:
+        assert key == k_full
+        for a, b in zip(h, h_full):
+            assert np.array_equal(a.astype(np.uint64), b)

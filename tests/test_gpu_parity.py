@@ -1,0 +1,284 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by element.
+
+Bar: binary32 costs/net values bit-exact (stronger than the
+north star's 1e-5 relative, which is also asserted against the binary64
+re-evaluation); keys, argmax indices, counts and histograms bit-exact.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def D():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no fallback)"
+    torch.cuda.set_device(0)
+    import paper_2110_15425_b200 as D
+    return D
+
+
+def _model(D, cfg, kind=W.KIND_PREDATOR_PREY):
+    return D.load_model(kind, cfg.n_levels, cfg.levels, cfg.w, cfg.params, device=0)
+
+
+def _gpu_pp(D, m, cfg, begin=0, end=None, invocation=0, seed=None, inputs=None):
+    import torch
+    end = cfg.n_alloc if end is None else end
+    net = torch.empty(max(end - begin, 1), dtype=torch.float32, device="cuda")
+    best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.eval_grid(m, cfg.inputs if inputs is None else inputs, cfg.n_samples, cfg.seed if seed is None else seed,
+                begin, end, net=net, best=best, invocation=invocation)
+    torch.cuda.synchronize()
+    return -net.cpu().numpy()[:end - begin], int(best.item()) & (2 ** 64 - 1)
+
+
+def _bits(a):
+    return np.asarray(a, np.float32).view(np.uint32)
+
+
+def test_pp_cfg1_bit_exact(D, orc):
+    cfg = W.pp_cfg1()
+    m = _model(D, cfg)
+    C, key = _gpu_pp(D, m, cfg)
+    want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, 27, cfg.n_samples, cfg.seed)
+    assert np.array_equal(_bits(C), _bits(want))
+    assert key == orc.argmax_net(-want)[0]
+
+
+@pytest.mark.parametrize("shape,S", [((7, 11, 13), 37), ((1, 1, 1), 1), ((2, 3, 700), 5), ((33, 1, 1), 100)])
+def test_pp_ragged_grids_bit_exact(D, orc, shape, S):
+    """Grids spanning several 256-thread tiles with a ragged tail, S = 1 and odd S."""
+    cfg = W.PPConfig("r", shape, S)
+    m = _model(D, cfg)
+    C, key = _gpu_pp(D, m, cfg)
+    want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc, S, cfg.seed)
+    assert np.array_equal(_bits(C), _bits(want))
+    assert key == orc.argmax_net(-want)[0]
+
+
+def test_pp_shards_concatenate_to_full_run(D, orc):
+    """Shard invariance: any split [b, e) reproduces the full run; min of shard keys = full key."""
+    cfg = W.PPConfig("s", (9, 10, 11), 20)
+    m = _model(D, cfg)
+    full, kfull = _gpu_pp(D, m, cfg)
+    cuts = [0, 1, 257, 500, 511, 990]
+    parts, keys = [], []
+    for b, e in zip(cuts, cuts[1:]):
+        c, k = _gpu_pp(D, m, cfg, b, e)
+        parts.append(c)
+        keys.append(k)
+    assert np.array_equal(_bits(np.concatenate(parts)), _bits(full))
+    assert min(keys) == kfull
+    for rank in range(3):
+        b, e = D.shard_range(cfg.n_alloc, rank, 3)
+        c, _ = _gpu_pp(D, m, cfg, b, e)
+        assert np.array_equal(_bits(c), _bits(full[b:e]))
+
+
+def test_pp_seed_high_bits_and_invocation(D, orc):
+    cfg = W.PPConfig("k", (5, 4, 3), 9)
+    m = _model(D, cfg)
+    seed = (0xDEADBEEF << 32) | 17
+    inp = W.random_positions(3)
+    for t in range(3):
+        C, key = _gpu_pp(D, m, cfg, invocation=t, seed=seed, inputs=inp[t])
+        want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, inp[t], 0, cfg.n_alloc, 9, seed,
+                           invocation=t)
+        assert np.array_equal(_bits(C), _bits(want))
+        assert key == orc.argmax_net(-want)[0]
+
+
+def test_pp_zero_noise_and_ties(D, orc):
+    cfg = W.PPConfig("z", (6, 6, 6), 4)
+    cfg.params = np.array([0.0, 0.0, 0.5], np.float32)
+    cfg.w = np.zeros(3, np.float32)
+    m = _model(D, cfg)
+    C, key = _gpu_pp(D, m, cfg)
+    assert (C == 0).all() and key & 0xFFFFFFFF == 0
+
+
+def test_pp_coincident_positions_and_nan(D, orc):
+    """Degenerate inputs: coincident entities (|v| = 0 branch) and NaN positions."""
+    cfg = W.PPConfig("d", (3, 3, 3), 6)
+    cfg.inputs = np.array([0.0, 0.0, 0.0, 0.0, 0.0, 0.0], np.float32)
+    cfg.params = np.array([0.0, 0.0, 0.5], np.float32)
+    m = _model(D, cfg)
+    C, key = _gpu_pp(D, m, cfg)
+    want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, 27, 6, cfg.seed)
+    assert np.array_equal(_bits(C), _bits(want))
+    cfg2 = W.PPConfig("n", (3, 3, 3), 6)
+    m2 = _model(D, cfg2)
+    C2, key2 = _gpu_pp(D, m2, cfg2, inputs=np.array([np.nan, 0, 1, 1, 0, 0], np.float32))
+    assert np.isnan(C2).all()
+    with pytest.raises(D.api.DistillError):
+        D.key_decode(key2)
+
+
+def test_pp_cfg3_full_size_argmax_and_sampled_costs(D, orc):
+    """cfg3 (1e6 allocations x 100 samples) in the bench launch configuration:
+    argmax key bit-exact against the full oracle grid search (north-star target),
+    and 4096 sampled costs bit-exact."""
+    import os
+    cfg = W.pp_cfg3()
+    m = _model(D, cfg)
+    C, key = _gpu_pp(D, m, cfg)
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([rng.integers(0, cfg.n_alloc, 4000), np.arange(64),
+                                    np.arange(cfg.n_alloc - 32, cfg.n_alloc)]))
+    for i in idx[:4096]:
+        w = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, int(i), int(i) + 1,
+                        cfg.n_samples, cfg.seed)
+        assert _bits(C[i:i + 1])[0] == _bits(w)[0], int(i)
+    full = orc.pp_eval_threads(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc,
+                               cfg.n_samples, cfg.seed, threads=os.cpu_count() or 8)
+    assert np.array_equal(_bits(C), _bits(full))
+    assert key == orc.argmax_net(-full)[0]
+
+
+def test_pp_within_north_star_tolerance_of_binary64(D, orc):
+    cfg = W.pp_cfg3()
+    m = _model(D, cfg)
+    C, _ = _gpu_pp(D, m, cfg, 400000, 400512)
+    c64 = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 400000, 400512,
+                      cfg.n_samples, cfg.seed, f64=True)
+    assert (np.abs(C - c64) / np.abs(c64)).max() < 1e-5
+
+
+@pytest.mark.parametrize("n,off", [(1, 0), (5, 1), (1000, 3), (4096, 0), (100003, 2), (8_000_000, 0)])
+def test_argmax_kernel_vs_oracle(D, orc, n, off):
+    import torch
+    rng = np.random.default_rng(n)
+    v = rng.integers(-50, 50, size=n + off).astype(np.float32)
+    v[rng.integers(0, n + off, size=max(1, n // 50))] = np.nan
+    v[rng.integers(0, n + off, size=max(1, n // 70))] = -0.0
+    t = torch.from_numpy(v).cuda()
+    best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.argmax(t[off:], 1000, best)
+    torch.cuda.synchronize()
+    k_or, rc = orc.argmax_net(v[off:], 1000)
+    assert (int(best.item()) & (2 ** 64 - 1)) == k_or
+
+
+def test_argmax_all_nan_and_empty(D, orc):
+    import torch
+    t = torch.full((10,), float("nan"), device="cuda")
+    best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.argmax(t, 0, best)
+    D.argmax(t[:0], 0, best)
+    torch.cuda.synchronize()
+    k = int(best.item()) & (2 ** 64 - 1)
+    assert k >> 32 == 0xFFFFFFFF
+    with pytest.raises(D.api.DistillError):
+        D.key_decode(k)
+
+
+def test_eval_grid_argument_errors(D):
+    import torch
+    cfg = W.pp_cfg1()
+    m = _model(D, cfg)
+    net = torch.empty(27, device="cuda")
+    with pytest.raises(D.api.DistillError):
+        D.eval_grid(m, cfg.inputs, 10, 1, 0, 28, net=net)          # past the grid
+    with pytest.raises(D.api.DistillError):
+        D.eval_grid(m, cfg.inputs, 0, 1, 0, 27, net=net)           # zero samples
+    with pytest.raises(D.api.DistillError):
+        D.eval_grid(m, cfg.inputs[:4], 10, 1, 0, 27, net=net)      # wrong input count
+    D.eval_grid(m, cfg.inputs, 10, 1, 5, 5, net=net)               # empty shard is a no-op
+
+
+def _ddm_gpu(D, d, t0, t1, seed):
+    import torch
+    rh, rs, xh = (torch.zeros(n, dtype=torch.int64, device="cuda") for n in d.hist_sizes)
+    D.ddm_batch(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
+                d.x_lo, d.x_hi, t0, t1, seed, rh, rs, xh)
+    torch.cuda.synchronize()
+    return [x.cpu().numpy().astype(np.uint64) for x in (rh, rs, xh)]
+
+
+def _ddm_p(orc, d):
+    return orc.ddm_params(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps,
+                          d.n_x_bins, d.x_lo, d.x_hi)
+
+
+@pytest.mark.parametrize("kw,t0,t1", [({}, 0, 4000), ({"n_steps": 333, "rt_bin_steps": 7}, 1000, 3001),
+                                       ({"drift": -0.3, "noise": 2.0, "threshold": 2.5}, 123456, 125000),
+                                       ({"n_steps": 1}, 0, 100)])
+def test_ddm_histograms_bit_exact(D, orc, kw, t0, t1):
+    import os
+    d = W.DDMConfig(**kw)
+    got = _ddm_gpu(D, d, t0, t1, 77)
+    want = orc.ddm_batch(_ddm_p(orc, d), 77, t0, t1, threads=os.cpu_count() or 8)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+def test_ddm_cfg2_full_size_properties(D, orc):
+    """cfg2 (1e6 x 1000) in the bench launch configuration: conservation, shard
+    additivity against a differently-launched split, a bit-exact oracle slice,
+    and the closed-form error rate / decision time."""
+    import math
+    import os
+    d = W.ddm_cfg2()
+    full = _ddm_gpu(D, d, 0, d.n_trials, d.seed)
+    a = _ddm_gpu(D, d, 0, 300001, d.seed)
+    b = _ddm_gpu(D, d, 300001, d.n_trials, d.seed)
+    for f, x, y in zip(full, a, b):
+        assert np.array_equal(f, x + y)
+    assert int(full[0].sum()) == d.n_trials and int(full[2].sum()) == d.n_trials
+    sl = _ddm_gpu(D, d, 999000, d.n_trials, d.seed)
+    want = orc.ddm_batch(_ddm_p(orc, d), d.seed, 999000, d.n_trials, threads=os.cpu_count() or 8)
+    for g, w in zip(sl, want):
+        assert np.array_equal(g, w)
+    nb = d.n_rt_bins
+    up, lo = int(full[0][:nb].sum()), int(full[0][nb:2 * nb].sum())
+    zp = 1 + 0.5826 * math.sqrt(d.dt)
+    er_cf, rt_cf = 1 / (1 + math.exp(2 * zp)), zp * math.tanh(zp)
+    er = lo / (up + lo)
+    assert abs(er - er_cf) < 4 * math.sqrt(er_cf * (1 - er_cf) / d.n_trials) + 0.005 * er_cf
+    rt = (int(full[1][0]) + int(full[1][1])) / (up + lo) * d.dt
+    assert abs(rt - rt_cf) < 0.005 * rt_cf
+
+
+def _stroop_gpu(D, m, c, begin, end, trial_range=(0, 0)):
+    import torch
+    n = end - begin
+    net = torch.empty(n, dtype=torch.float32, device="cuda")
+    best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    counts = torch.zeros(3 * n, dtype=torch.int64, device="cuda")
+    D.eval_grid(m, None, c.n_trials, c.seed, begin, end, net=net, best=best, counts=counts,
+                trial_range=trial_range)
+    torch.cuda.synchronize()
+    return (counts.cpu().numpy().astype(np.uint64).reshape(n, 3), net.cpu().numpy(),
+            int(best.item()) & (2 ** 64 - 1))
+
+
+def test_stroop_small_grid_bit_exact(D, orc):
+    c = W.stroop_small()
+    m = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=0)
+    cnt, net, key = _stroop_gpu(D, m, c, 0, c.n_alloc)
+    wc, wn = orc.stroop_eval(c.n_levels, c.levels, c.w, c.params, 0, c.n_alloc, c.n_trials, c.seed, threads=8)
+    assert np.array_equal(cnt, wc)
+    assert np.array_equal(_bits(net), _bits(wn))
+    assert key == orc.argmax_net(wn)[0]
+    # a shard and a trial sub-range
+    cnt2, _, _ = _stroop_gpu(D, m, c, 37, 61, trial_range=(5, 250))
+    wc2, _ = orc.stroop_eval(c.n_levels, c.levels, c.w, c.params, 37, 61, c.n_trials, c.seed, 5, 250)
+    assert np.array_equal(cnt2, wc2)
+
+
+def test_stroop_cfg4_sampled_allocations_full_trials(D, orc):
+    """cfg4 grid (1e4 allocations), T = 1e5 trials: sampled allocations simulated
+    over all trials, counts and V bit-exact."""
+    import os
+    c = W.stroop_cfg4()
+    m = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=0)
+    for b in (0, 4321, 9998):
+        cnt, net, _ = _stroop_gpu(D, m, c, b, b + 2)
+        wc, wn = orc.stroop_eval(c.n_levels, c.levels, c.w, c.params, b, b + 2, c.n_trials, c.seed,
+                                 threads=os.cpu_count() or 8)
+        assert np.array_equal(cnt, wc)
+        assert np.array_equal(_bits(net), _bits(wn))
