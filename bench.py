@@ -38,9 +38,9 @@ import workloads as W  # noqa: E402
 
 METRIC = "model evaluations/sec (allocations×samples) at 1/2/4/8 B200; % FP32 peak"
 UNIT = "evals/s"
-FLOPS_PER_SAMPLE = 242        # DESIGN.md §6, pinned by tests/test_oracle_pp.py (counting oracle)
+FLOPS_PER_SAMPLE = 257        # DESIGN.md §6, pinned by tests/test_oracle_pp.py (counting oracle)
 FLOPS_PER_ALLOC = 13
-FLOPS_PER_CALL = 63
+FLOPS_PER_CALL = 66
 FP32_LANES_PER_SM = 128       # FFMA lanes per SM (4 SMSP x 32), 2 flops per FMA
 
 
@@ -68,7 +68,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (OSError, FileNotFoundError):
             self.proc = None
@@ -386,7 +386,7 @@ def run_extras(D, torch, dev, rank, world, args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-extras", action="store_true")

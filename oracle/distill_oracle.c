@@ -118,27 +118,23 @@ float od_rsqrt(float x) {
 }
 
 /* ------------------------------------------------------------------------ */
-/* spec/RNG.md §5: sincos2pi_spec                                            */
+/* spec/RNG.md §5: sincos_spec — (cos, sin)(2 pi A / 2^32 - pi/2)            */
 /* ------------------------------------------------------------------------ */
-static const float OD_S[4] = { 0x1.921fb6p+0f, -0x1.4abbbap-1f, 0x1.465ec8p-4f, -0x1.2d9c2p-8f };
-static const float OD_C[4] = { -0x1.3bd3ccp+0f, 0x1.03c1dep-2f, -0x1.55c666p-6f, 0x1.d9f828p-11f };
+static const float OD_S[5] = { 0x1.921fb4p+1f, -0x1.4abbb6p+2f, 0x1.46676ep+1f, -0x1.323308p-1f, 0x1.3c4c1p-4f };
+static const float OD_C[5] = { -0x1.3bd3ccp+2f, 0x1.03c1e6p+2f, -0x1.55d0bap+0f, 0x1.e12f96p-3f, -0x1.901cb4p-6f };
 
 void od_sincos2pi(uint32_t a, float* cs, float* sn) {
-    uint32_t s = a + 0x20000000u;
-    uint32_t q = s >> 30;
-    int32_t ri = (int32_t)(s & 0x3FFFFFFFu) - 0x20000000;
-    float r = (float)ri * 0x1p-30f;           /* exact: power-of-two scaling of an exact value */
+    uint32_t h = a >> 31;
+    /* exact: (a & 0x7FFFFFFF) has at most 23 significant bits, the scaling is a power of two,
+       and g - 1/2 is representable for every such g */
+    float r = (float)(a & 0x7FFFFFFFu) * 0x1p-31f - 0.5f;
     float t = FMUL(r, r);
-    float S = FFMA(FFMA(FFMA(OD_S[3], t, OD_S[2]), t, OD_S[1]), t, OD_S[0]);
-    float C = FFMA(FFMA(FFMA(OD_C[3], t, OD_C[2]), t, OD_C[1]), t, OD_C[0]);
+    float S = FFMA(FFMA(FFMA(FFMA(OD_S[4], t, OD_S[3]), t, OD_S[2]), t, OD_S[1]), t, OD_S[0]);
+    float C = FFMA(FFMA(FFMA(FFMA(OD_C[4], t, OD_C[3]), t, OD_C[2]), t, OD_C[1]), t, OD_C[0]);
     float cq = FFMA(C, t, 1.0f);
     float sq = FMUL(S, r);
-    switch (q) {
-    case 0:  *cs = cq;  *sn = sq;  break;
-    case 1:  *cs = -sq; *sn = cq;  break;
-    case 2:  *cs = -cq; *sn = -sq; break;
-    default: *cs = sq;  *sn = -cq; break;
-    }
+    if (h) { *cs = -cq; *sn = -sq; }
+    else   { *cs = cq;  *sn = sq; }
 }
 
 /* array forms of the three primitives, for the exhaustive accuracy pins */
@@ -186,7 +182,7 @@ void od_normal_sextet(uint64_t seed, uint32_t alloc, uint32_t sample, uint32_t i
     od_philox4x32_10(ctr, key, X);
     uint32_t A0 = X[3] << 16;
     uint32_t A1 = X[3] & 0xFFFF0000u;
-    uint32_t A2 = (X[0] << 24) | ((X[1] & 0xFFu) << 16) | ((X[2] & 0xFFu) << 8);
+    uint32_t A2 = (X[0] << 24) | ((X[1] & 0xFFu) << 16);
     od_bm_pair(X[0], A0, &out[0], &out[1]);
     od_bm_pair(X[1], A1, &out[2], &out[3]);
     od_bm_pair(X[2], A2, &out[4], &out[5]);
@@ -198,8 +194,8 @@ void od_normal_sextet(uint64_t seed, uint32_t alloc, uint32_t sample, uint32_t i
 typedef struct { float x, y; } v2;
 
 static v2 od_unit(v2 v) {
-    float n2 = FFMA(v.y, v.y, FMUL(v.x, v.x));
-    float y = (n2 == 0.0f) ? 0.0f : od_rsqrt(n2);
+    float n2 = FFMA(v.y, v.y, FFMA(v.x, v.x, 0x1p-126f));   /* never 0: + smallest normal */
+    float y = od_rsqrt(n2);
     v2 r = { FMUL(v.x, y), FMUL(v.y, y) };
     return r;
 }
@@ -274,7 +270,7 @@ static d2 d_action(d2 prey, d2 pred, d2 player, double kappa) {
 static void d_bm(uint32_t R, uint32_t A, double* z0, double* z1) {
     const double TWO_PI = 6.283185307179586476925286766559;
     double u1 = (double)((R >> 8) | 1u) * 0x1p-24;
-    double t = (double)A * 0x1p-32;
+    double t = (double)A * 0x1p-32 - 0.25;    /* angle 2 pi A / 2^32 - pi/2 */
     double rad = sqrt(-2.0 * log(u1));
     *z0 = rad * cos(TWO_PI * t);
     *z1 = rad * sin(TWO_PI * t);
@@ -304,8 +300,7 @@ int od_pp_eval_f64(const uint32_t n_levels[3], const float* levels, const float 
         for (uint32_t s = 0; s < n_samples; ++s) {
             uint32_t ctr[4] = { (uint32_t)i, s, invocation, 1u }, X[4];
             od_philox4x32_10(ctr, key, X);
-            uint32_t A[3] = { X[3] << 16, X[3] & 0xFFFF0000u,
-                              (X[0] << 24) | ((X[1] & 0xFFu) << 16) | ((X[2] & 0xFFu) << 8) };
+            uint32_t A[3] = { X[3] << 16, X[3] & 0xFFFF0000u, (X[0] << 24) | ((X[1] & 0xFFu) << 16) };
             d2 o[3];
             for (int e = 0; e < 3; ++e) {
                 double zx, zy;

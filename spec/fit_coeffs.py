@@ -35,24 +35,24 @@ def fit_log():
 
 
 def fit_sin():
-    # sin(pi/2 r) = r * S(r^2), r in [-1/2, 1/2]
-    r = np.linspace(1e-6, 0.5, 100001)
+    # sin(pi r) = r * S(r^2), r in [-1/2, 1/2] (half-turn reduction, RNG.md §5)
+    r = np.linspace(1e-6, 0.5, 200001)
     t = r * r
-    target = np.sin(np.pi / 2 * r) / r
-    basis = lambda x: np.vander(x, 4, increasing=True)
-    c, e = lawson(t, target, basis, np.ones_like(t))
+    target = np.sin(np.pi * r) / r
+    basis = lambda x: np.vander(x, 5, increasing=True)
+    c, e = lawson(t, target, basis, r)          # absolute error of sin
     return c, e
 
 
 def fit_cos():
-    r = np.linspace(0, 0.5, 100001)
+    # cos(pi r) = 1 + r^2 C(r^2)
+    r = np.linspace(0, 0.5, 200001)
     t = r * r
-    target = np.cos(np.pi / 2 * r)
-    # constant term pinned to 1: fit (cos-1)/t
+    target = np.cos(np.pi * r)
     tt = t[1:]
     tg = (target[1:] - 1) / tt
-    basis = lambda x: np.vander(x, 4, increasing=True)
-    c, e = lawson(tt, tg, basis, tt)
+    basis = lambda x: np.vander(x, 5, increasing=True)
+    c, e = lawson(tt, tg, basis, tt)             # absolute error of cos
     return c, e
 
 

@@ -180,9 +180,11 @@ def test_eval_grid_argument_errors(D):
     import torch
     cfg = W.pp_cfg1()
     m = _model(D, cfg)
-    net = torch.empty(27, device="cuda")
+    net = torch.empty(28, device="cuda")
     with pytest.raises(D.api.DistillError):
         D.eval_grid(m, cfg.inputs, 10, 1, 0, 28, net=net)          # past the grid
+    with pytest.raises(ValueError):
+        D.eval_grid(m, cfg.inputs, 10, 1, 0, 27, net=net[:20])     # buffer too small (caught in Python)
     with pytest.raises(D.api.DistillError):
         D.eval_grid(m, cfg.inputs, 0, 1, 0, 27, net=net)           # zero samples
     with pytest.raises(D.api.DistillError):

@@ -66,13 +66,14 @@ def test_sincos2pi_exhaustive_24bit(orc):
     """All 2^24 angle words with the low byte clear."""
     a = (np.arange(2 ** 24, dtype=np.uint64) << 8).astype(np.uint32)
     c, s = orc.sincos2pi_array(a)
-    th = a.astype(np.float64) * (2 * math.pi / 2.0 ** 32)
-    assert np.abs(c - np.cos(th)).max() <= 2 * 2.0 ** -24
-    assert np.abs(s - np.sin(th)).max() <= 2 * 2.0 ** -24
-    # quarter turns are exact
-    for k, (cc, ss) in enumerate([(1, 0), (0, 1), (-1, 0), (0, -1)]):
-        c1, s1 = orc.sincos2pi(k << 30)
-        assert (c1, s1) == (cc, ss)
+    th = a.astype(np.float64) * (2 * math.pi / 2.0 ** 32) - math.pi / 2
+    assert np.abs(c - np.cos(th)).max() <= 4 * 2.0 ** -24
+    assert np.abs(s - np.sin(th)).max() <= 4 * 2.0 ** -24
+    # half-turn symmetry is exact: A and A + 2^31 give negated pairs
+    c2, s2 = orc.sincos2pi_array(a ^ np.uint32(0x80000000))
+    assert np.array_equal(c2, -c) and np.array_equal(s2, -s)
+    # phi = 0 at A = 2^30 (r = 0): exactly (1, 0)
+    assert orc.sincos2pi(1 << 30) == (1.0, 0.0)
 
 
 def test_box_muller_pair_matches_definition(orc):
@@ -86,7 +87,7 @@ def test_box_muller_pair_matches_definition(orc):
             R, A = int(X[2 * p]), int(X[2 * p + 1]) & 0xFFFFFF00
             u1 = ((R >> 8) | 1) * 2.0 ** -24
             rad = math.sqrt(-2 * math.log(u1))
-            th = 2 * math.pi * A / 2.0 ** 32
+            th = 2 * math.pi * A / 2.0 ** 32 - math.pi / 2
             assert abs(z[2 * p] - rad * math.cos(th)) <= 1e-6 * max(1, rad)
             assert abs(z[2 * p + 1] - rad * math.sin(th)) <= 1e-6 * max(1, rad)
 
@@ -96,11 +97,11 @@ def test_sextet_packing_matches_definition(orc):
     for i, s in [(0, 0), (5, 3), (123456, 99), (999999, 0)]:
         X = [int(v) for v in orc.philox([i, s, 0, 1], [seed, 0])]
         A = [(X[3] << 16) & 0xFFFFFFFF, X[3] & 0xFFFF0000,
-             ((X[0] << 24) | ((X[1] & 0xFF) << 16) | ((X[2] & 0xFF) << 8)) & 0xFFFFFFFF]
+             ((X[0] << 24) | ((X[1] & 0xFF) << 16)) & 0xFFFFFFFF]
         z = orc.normal_sextet(seed, i, s, 0)
         for e in range(3):
             rad = math.sqrt(-2 * math.log(((X[e] >> 8) | 1) * 2.0 ** -24))
-            th = 2 * math.pi * A[e] / 2.0 ** 32
+            th = 2 * math.pi * A[e] / 2.0 ** 32 - math.pi / 2
             assert abs(z[2 * e] - rad * math.cos(th)) <= 1e-6 * max(1, rad)
             assert abs(z[2 * e + 1] - rad * math.sin(th)) <= 1e-6 * max(1, rad)
 
