@@ -2,13 +2,22 @@
 //
 // One thread owns one allocation of the grid (the paper's "each thread
 // evaluates one point in the grid search space") and runs the whole
-// compiled model for every sample in ascending order (spec/MODELS.md §2):
-//   decode i -> levels -> sigma_e, K     (Control node)
+// compiled model for every sample (spec/MODELS.md §2):
+//   decode i -> levels -> sigma_e, K                    (Control node)
 //   per sample: Philox sextet -> 3 Box-Muller pairs -> Obs -> Action ->
-//               Objective e = ||u_hat - u*||^2, acc += e
+//               Objective e = ||u_hat - u*||^2,  acc += e (ascending s)
 //   C = acc / S + K ; store V = -C ; key(C, i) -> warp/block min -> atomicMin
-// State per thread is registers only (the paper's 7.5 kB MT19937 state per
-// thread, becomes the Philox counter).
+//
+// B200 mapping.  The kernel is bound by instruction issue and the FP32 pipe,
+// not memory (4 B written per 100 evaluations).  Samples are processed in
+// PAIRS (s, s+1) held in the two lanes of a float2, so every floating-point
+// step is one packed FFMA2 / FMUL2 / FADD2 (sm_100, crt/sm_100_rt.h:90-100;
+// each lane rounds exactly like the scalar op) — half the FP issue slots of
+// scalar code, bit-identical results.  The two lanes also give two
+// independent Philox chains (integer ILP).  Philox rounds 1-3 are partly
+// sample-invariant (counter = (i, s, t, 1)) and are hoisted per thread.
+// State is registers only (the paper's 7.5 kB MT19937 state per thread,
+// P:632, becomes 6 words of Philox counter/key).
 #pragma once
 #include "keys.cuh"
 #include "rng.cuh"
@@ -27,31 +36,119 @@ struct PPArgs {
     key_t* __restrict__ best;                          // [1] or nullptr
 };
 
-struct f2 { float x, y; };
+// ------------------------------------------------------------ packed binary32 helpers
+typedef float2 F2;
+__device__ __forceinline__ F2 bc(float a) { return make_float2(a, a); }
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ F2 add2(F2 a, F2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ F2 neg2(F2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) { return __fadd2_rn(a, neg2(b)); }  // a - b exactly
 
-__device__ __forceinline__ f2 v_sub(f2 a, f2 b) { return {__fadd_rn(a.x, -b.x), __fadd_rn(a.y, -b.y)}; }
-
-// unit(v) = v * rsqrt_spec(|v|^2), (0,0)-scaled when |v|^2 == 0 (spec/MODELS.md §2)
-__device__ __forceinline__ f2 v_unit(f2 v) {
-    const float n2 = __fmaf_rn(v.y, v.y, __fmul_rn(v.x, v.x));
-    const float r = rsqrt_spec(n2);
-    const float y = (n2 == 0.0f) ? 0.0f : r;
-    return {__fmul_rn(v.x, y), __fmul_rn(v.y, y)};
+// rsqrt_spec on both lanes given y0 bits and h = 0.5 x (spec/RNG.md §4);
+// `mh` = -h (passed so callers that already hold -h save the multiply).
+__device__ __forceinline__ F2 rsqrt2_from(F2 x, F2 mh) {
+    F2 y = make_float2(__uint_as_float(0x5F375A86u - (__float_as_uint(x.x) >> 1)),
+                       __uint_as_float(0x5F375A86u - (__float_as_uint(x.y) >> 1)));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        F2 t = mul2(y, y);
+        t = fma2(mh, t, bc(1.5f));
+        y = mul2(y, t);
+    }
+    return y;
 }
 
-// Action node: unit toward prey minus kappa * unit toward predator
-__device__ __forceinline__ f2 action(f2 prey, f2 pred, f2 pl, float kappa) {
-    const f2 up = v_unit(v_sub(prey, pl));
-    const f2 ud = v_unit(v_sub(pred, pl));
-    return {__fmaf_rn(-kappa, ud.x, up.x), __fmaf_rn(-kappa, ud.y, up.y)};
+struct V2 { F2 x, y; };   // a 2-D vector for the two samples of a pair
+
+__device__ __forceinline__ V2 vsub(V2 a, V2 b) { return {sub2(a.x, b.x), sub2(a.y, b.y)}; }
+
+// unit(v) (spec/MODELS.md §2): n2 = fma(v.y, v.y, fma(v.x, v.x, 2^-126)), v * rsqrt_spec(n2)
+__device__ __forceinline__ V2 vunit(V2 v) {
+    const F2 n2 = fma2(v.y, v.y, fma2(v.x, v.x, bc(0x1p-126f)));
+    const F2 y = rsqrt2_from(n2, mul2(n2, bc(-0.5f)));
+    return {mul2(v.x, y), mul2(v.y, y)};
 }
+
+// Box-Muller pair for both samples: radius words R, angle words A (low 16 bits clear)
+// z = (rad * cos phi, rad * sin phi), spec/RNG.md §2-§6.
+__device__ __forceinline__ void bm_pair2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay, V2& z) {
+    // u1 = ((R >> 8) | 1) * 2^-24: convert the odd integer exactly and fold the
+    // 2^-24 into the exponent constants of ln_spec (bits(u1) = bits(float(m)) - 24<<23)
+    const uint32_t ix = __float_as_uint(__uint2float_rn((Rx >> 8) | 1u));
+    const uint32_t iy = __float_as_uint(__uint2float_rn((Ry >> 8) | 1u));
+    const uint32_t tx = ix - 0x4B3504F3u, ty = iy - 0x4B3504F3u;        // = bits(u1) - 0x3F3504F3
+    const F2 m = make_float2(__uint_as_float((tx & 0x7FFFFFu) + 0x3F3504F3u),
+                             __uint_as_float((ty & 0x7FFFFFu) + 0x3F3504F3u));
+    const F2 fe = make_float2(__int2float_rn((int32_t)tx >> 23), __int2float_rn((int32_t)ty >> 23));
+    const F2 f = add2(m, bc(-1.0f));
+    F2 P = fma2(bc(D_L7), f, bc(D_L6));
+    P = fma2(P, f, bc(D_L5));
+    P = fma2(P, f, bc(D_L4));
+    P = fma2(P, f, bc(D_L3));
+    P = fma2(P, f, bc(D_L2));
+    P = fma2(P, f, bc(D_L1));
+    P = fma2(P, f, bc(D_L0));
+    F2 y = fma2(mul2(f, f), P, f);
+    y = fma2(fe, bc(D_LN2_LO), y);
+    y = fma2(fe, bc(D_LN2_HI), y);                       // y = ln_spec(u1) < 0
+    const F2 s = mul2(y, bc(-2.0f));                     // s = -2 ln u1 (exact scaling)
+    const F2 rad = mul2(s, rsqrt2_from(s, y));           // -h = -0.5 s = y exactly
+    // sincos_spec: r from the angle bits, half-turn sign applied to rad
+    const F2 r = add2(make_float2(__uint_as_float(((Ax >> 8) & 0x7FFFFFu) | 0x3F800000u),
+                                  __uint_as_float(((Ay >> 8) & 0x7FFFFFu) | 0x3F800000u)),
+                      bc(-1.5f));
+    const F2 t = mul2(r, r);
+    const F2 S = fma2(fma2(fma2(fma2(bc(D_S4), t, bc(D_S3)), t, bc(D_S2)), t, bc(D_S1)), t, bc(D_S0));
+    const F2 C = fma2(fma2(fma2(fma2(bc(D_C4), t, bc(D_C3)), t, bc(D_C2)), t, bc(D_C1)), t, bc(D_C0));
+    const F2 cq = fma2(C, t, bc(1.0f));
+    const F2 sq = mul2(S, r);
+    const F2 rs = make_float2(__uint_as_float(__float_as_uint(rad.x) ^ (Ax & 0x80000000u)),
+                              __uint_as_float(__float_as_uint(rad.y) ^ (Ay & 0x80000000u)));
+    z.x = mul2(rs, cq);   // (-rad) * c == -(rad * c) bit for bit
+    z.y = mul2(rs, sq);
+}
+
+// Philox4x32-10 on counter (i, s, t, 1): rounds 1-3 with their sample-invariant
+// parts hoisted into PhiloxPP (computed once per thread), rounds 4-10 generic.
+struct PhiloxPP {
+    uint32_t a1, y0k_unused, x3k, b_c1k, c3k, z3, k0, k1;
+    __device__ __forceinline__ void init(uint32_t i, uint32_t t, uint32_t key0, uint32_t key1) {
+        k0 = key0; k1 = key1;
+        uint32_t hi0, lo0, hi1, lo1;
+        mulhilo(PHILOX_M0, i, hi0, lo0);                 // round 1: c0 = i
+        mulhilo(PHILOX_M1, t, hi1, lo1);                 //          c2 = t
+        a1 = hi1 ^ k0;                                   // x0 = a1 ^ s
+        const uint32_t x1 = lo1, x2 = hi0 ^ 1u ^ k1, x3 = lo0;
+        uint32_t H1, L1;
+        mulhilo(PHILOX_M1, x2, H1, L1);                  // round 2: p1 = M1 * x2 (invariant)
+        const uint32_t y0 = H1 ^ x1 ^ (k0 + PHILOX_W0);
+        const uint32_t y1 = L1;
+        x3k = x3 ^ (k1 + PHILOX_W1);                     // y2 = hi(M0 * x0) ^ x3k
+        uint32_t G0h, G0l;
+        mulhilo(PHILOX_M0, y0, G0h, G0l);                // round 3: p0 = M0 * y0 (invariant)
+        b_c1k = y1 ^ (k0 + 2u * PHILOX_W0);              // z0 = hi(M1 * y2) ^ b_c1k
+        c3k = G0h ^ (k1 + 2u * PHILOX_W1);               // z2 = c3k ^ y3
+        z3 = G0l;
+        y0k_unused = 0;
+    }
+    __device__ __forceinline__ uint4 operator()(uint32_t s) const {
+        uint32_t P0h, P0l;
+        mulhilo(PHILOX_M0, a1 ^ s, P0h, P0l);            // round 2: p0 = M0 * x0
+        const uint32_t y2 = P0h ^ x3k, y3 = P0l;
+        uint32_t Qh, Ql;
+        mulhilo(PHILOX_M1, y2, Qh, Ql);                  // round 3: p1 = M1 * y2
+        const uint4 c = make_uint4(Qh ^ b_c1k, Ql, c3k ^ y3, z3);
+        return philox_from<3>(c, k0, k1);                // rounds 4..10
+    }
+};
 
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) pp_eval_grid_kernel(const PPArgs a) {
-    const uint32_t t = blockIdx.x * BLOCK + threadIdx.x;
-    key_t k = KEY_INIT;
-    if (t < a.count) {
-        const uint32_t i = a.begin + t;
+    const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
+    key_t key = KEY_INIT;
+    if (tid < a.count) {
+        const uint32_t i = a.begin + tid;
         // a1: mixed-radix decode, signal 0 most significant
         const uint32_t k2 = i % a.L2, r = i / a.L2;
         const uint32_t k1 = r % a.L1, k0 = r / a.L1;
@@ -63,37 +160,45 @@ __global__ void __launch_bounds__(BLOCK) pp_eval_grid_kernel(const PPArgs a) {
         const float s1 = __fmaf_rn(a1, dsig, a.sigma_max);
         const float s2 = __fmaf_rn(a2, dsig, a.sigma_max);
         const float K = __fmaf_rn(a.w2, a2, __fmaf_rn(a.w1, a1, __fmul_rn(a.w0, a0)));
-        const f2 py = {a.prey_x, a.prey_y}, pd = {a.pred_x, a.pred_y}, pl = {a.pl_x, a.pl_y};
-        const f2 us = v_unit(action(py, pd, pl, a.kappa));
 
+        // u* = unit(action(true positions)), computed in lane x of the packed helpers
+        const V2 P0 = {bc(a.prey_x), bc(a.prey_y)}, P1 = {bc(a.pred_x), bc(a.pred_y)};
+        const V2 P2 = {bc(a.pl_x), bc(a.pl_y)};
+        const F2 mk = bc(-a.kappa);
+        V2 up = vunit(vsub(P0, P2)), ud = vunit(vsub(P1, P2));
+        const V2 us = vunit({fma2(mk, ud.x, up.x), fma2(mk, ud.y, up.y)});
+
+        PhiloxPP rng;
+        rng.init(i, a.invocation, a.key0, a.key1);
         float acc = 0.0f;
-        for (uint32_t s = 0; s < a.n_samples; ++s) {
-            // a2: one Philox block per sample (sextet packing, spec/RNG.md §6)
-            const uint4 X = philox4x32_10(make_uint4(i, s, a.invocation, 1u), a.key0, a.key1);
-            const uint32_t A0 = X.w << 16;
-            const uint32_t A1 = X.w & 0xFFFF0000u;
-            const uint32_t A2 = (X.x << 24) | ((X.y & 0xFFu) << 16) | ((X.z & 0xFFu) << 8);
-            // a3: Box-Muller, one 2-D pair per entity
-            f2 z0, z1, z2;
-            bm_pair(X.x, A0, z0.x, z0.y);
-            bm_pair(X.y, A1, z1.x, z1.y);
-            bm_pair(X.z, A2, z2.x, z2.y);
+        for (uint32_t s = 0; s < a.n_samples; s += 2) {
+            // a2: one Philox block per sample, two samples per iteration
+            const uint4 X = rng(s);
+            const uint4 Y = rng(s + 1);
+            // a3: sextet packing -> three 2-D Box-Muller pairs (spec/RNG.md §6)
+            V2 z0, z1, z2;
+            bm_pair2(X.x, Y.x, X.w << 16, Y.w << 16, z0);
+            bm_pair2(X.y, Y.y, X.w & 0xFFFF0000u, Y.w & 0xFFFF0000u, z1);
+            bm_pair2(X.z, Y.z, (X.x << 24) | ((X.y & 0xFFu) << 16), (Y.x << 24) | ((Y.y & 0xFFu) << 16), z2);
             // a4: Obs -> Action -> Objective
-            const f2 o0 = {__fmaf_rn(s0, z0.x, py.x), __fmaf_rn(s0, z0.y, py.y)};
-            const f2 o1 = {__fmaf_rn(s1, z1.x, pd.x), __fmaf_rn(s1, z1.y, pd.y)};
-            const f2 o2 = {__fmaf_rn(s2, z2.x, pl.x), __fmaf_rn(s2, z2.y, pl.y)};
-            const f2 uh = v_unit(action(o0, o1, o2, a.kappa));
-            const f2 dl = v_sub(uh, us);
-            const float e = __fmaf_rn(dl.y, dl.y, __fmul_rn(dl.x, dl.x));
-            acc = __fadd_rn(acc, e);      // a7: sequential sum, ascending s
+            const V2 o0 = {fma2(bc(s0), z0.x, P0.x), fma2(bc(s0), z0.y, P0.y)};
+            const V2 o1 = {fma2(bc(s1), z1.x, P1.x), fma2(bc(s1), z1.y, P1.y)};
+            const V2 o2 = {fma2(bc(s2), z2.x, P2.x), fma2(bc(s2), z2.y, P2.y)};
+            const V2 vp = vunit(vsub(o0, o2)), vd = vunit(vsub(o1, o2));
+            const V2 uh = vunit({fma2(mk, vd.x, vp.x), fma2(mk, vd.y, vp.y)});
+            const F2 dx = sub2(uh.x, us.x), dy = sub2(uh.y, us.y);
+            const F2 e = fma2(dy, dy, mul2(dx, dx));
+            // a7: sequential sum in ascending sample order
+            acc = __fadd_rn(acc, e.x);
+            if (s + 1 < a.n_samples) acc = __fadd_rn(acc, e.y);
         }
         // a8: net of cost
         const float C = __fadd_rn(__fdiv_rn(acc, __uint2float_rn(a.n_samples)), K);
-        if (a.net) a.net[t] = -C;
-        k = make_key(C, i);
+        if (a.net) a.net[tid] = -C;
+        key = make_key(C, i);
     }
     // a9: (value, index) argmin -> one atomic per block
-    if (a.best) block_min_key_atomic<BLOCK>(k, a.best);
+    if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
 }
 
 }  // namespace distill

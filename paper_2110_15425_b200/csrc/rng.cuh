@@ -55,14 +55,16 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 #define D_L5 0x1.30d0aap-3f
 #define D_L6 (-0x1.277224p-3f)
 #define D_L7 0x1.6fc72p-4f
-#define D_S0 0x1.921fb6p+0f
-#define D_S1 (-0x1.4abbbap-1f)
-#define D_S2 0x1.465ec8p-4f
-#define D_S3 (-0x1.2d9c2p-8f)
-#define D_C0 (-0x1.3bd3ccp+0f)
-#define D_C1 0x1.03c1dep-2f
-#define D_C2 (-0x1.55c666p-6f)
-#define D_C3 0x1.d9f828p-11f
+#define D_S0 0x1.921fb4p+1f
+#define D_S1 (-0x1.4abbb6p+2f)
+#define D_S2 0x1.46676ep+1f
+#define D_S3 (-0x1.323308p-1f)
+#define D_S4 0x1.3c4c1p-4f
+#define D_C0 (-0x1.3bd3ccp+2f)
+#define D_C1 0x1.03c1e6p+2f
+#define D_C2 (-0x1.55d0bap+0f)
+#define D_C3 0x1.e12f96p-3f
+#define D_C4 (-0x1.901cb4p-6f)
 
 // ln_spec(x) for positive normal x (spec/RNG.md §3)
 __device__ __forceinline__ float ln_spec(float x) {
@@ -99,21 +101,22 @@ __device__ __forceinline__ float rsqrt_spec(float x) {
     return y;
 }
 
-// sincos2pi_spec(A) for an angle word with its low 8 bits clear (spec/RNG.md §5)
-__device__ __forceinline__ void sincos2pi_spec(uint32_t a, float& c, float& s) {
-    const uint32_t w = a + 0x20000000u;
-    const uint32_t q = w >> 30;
-    const int32_t ri = (int32_t)(w & 0x3FFFFFFFu) - 0x20000000;
-    const float r = __fmul_rn(__int2float_rn(ri), 0x1p-30f);  // exact
+// r of sincos_spec: (A mod 2^31)/2^31 - 1/2, built from the bits (exact, spec/RNG.md §5)
+__device__ __forceinline__ float half_turn_r(uint32_t a) {
+    return __fadd_rn(__uint_as_float(((a >> 8) & 0x7FFFFFu) | 0x3F800000u), -1.5f);
+}
+
+// sincos_spec(A) = (cos, sin)(2 pi A/2^32 - pi/2), half-turn reduction (spec/RNG.md §5)
+__device__ __forceinline__ void sincos_spec(uint32_t a, float& c, float& s) {
+    const float r = half_turn_r(a);
     const float t = __fmul_rn(r, r);
-    const float S = __fmaf_rn(__fmaf_rn(__fmaf_rn(D_S3, t, D_S2), t, D_S1), t, D_S0);
-    const float C = __fmaf_rn(__fmaf_rn(__fmaf_rn(D_C3, t, D_C2), t, D_C1), t, D_C0);
+    const float S = __fmaf_rn(__fmaf_rn(__fmaf_rn(__fmaf_rn(D_S4, t, D_S3), t, D_S2), t, D_S1), t, D_S0);
+    const float C = __fmaf_rn(__fmaf_rn(__fmaf_rn(__fmaf_rn(D_C4, t, D_C3), t, D_C2), t, D_C1), t, D_C0);
     const float cq = __fmaf_rn(C, t, 1.0f);
     const float sq = __fmul_rn(S, r);
-    const float cc = (q & 1) ? sq : cq;   // |cos| after rotation by q quarter turns
-    const float ss = (q & 1) ? cq : sq;
-    c = ((q + 1) & 2) ? -cc : cc;         // q = 1, 2 negate cos
-    s = (q & 2) ? -ss : ss;               // q = 2, 3 negate sin
+    const bool h = (a >> 31) != 0;
+    c = h ? -cq : cq;
+    s = h ? -sq : sq;
 }
 
 // One Box-Muller pair from a radius word R and an angle word A (spec/RNG.md §6)
@@ -122,7 +125,7 @@ __device__ __forceinline__ void bm_pair(uint32_t R, uint32_t A, float& z0, float
     const float s = __fmul_rn(-2.0f, ln_spec(u1));                          // exact scaling
     const float rad = __fmul_rn(s, rsqrt_spec(s));
     float c, n;
-    sincos2pi_spec(A, c, n);
+    sincos_spec(A, c, n);
     z0 = __fmul_rn(rad, c);
     z1 = __fmul_rn(rad, n);
 }
