@@ -63,6 +63,7 @@ def _bind(path: str) -> C.CDLL:
         "od_normal_quad": (None, [u64, u64, u64, u64, _f32p]),
         "od_normal_sextet": (None, [u64, u32, u32, u32, _f32p]),
         "od_pp_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u64, u64, u32, u64, u32, C.c_void_p]),
+        "od_pp_trace": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u32, u64, u32, _f32p]),
         "od_pp_eval_f64": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u64, u64, u32, u64, u32, C.c_void_p]),
         "od_key": (u64, [f32, u32]),
         "od_argmax_net": (C.c_int, [_f32p, u64, u64, C.POINTER(u64)]),
@@ -180,6 +181,14 @@ def pp_eval(n_levels, levels, w, params, inputs, begin, end, n_samples, seed,
             out.ctypes.data_as(C.c_void_p))
     if rc != 0:
         raise ValueError("od_pp_eval rejected its arguments")
+    return out
+
+
+def pp_trace(n_levels, levels, params, inputs, i, n_samples, seed, invocation=0) -> np.ndarray:
+    """Per-sample objective e_s of allocation i (debug/tests)."""
+    out = np.zeros(int(n_samples), np.float32)
+    lib().od_pp_trace(_u32(n_levels), _f32(levels), _f32(params), _f32(inputs), int(i), int(n_samples),
+                      int(seed), int(invocation), out)
     return out
 
 

@@ -208,6 +208,14 @@ static v2 od_action(v2 prey, v2 pred, v2 player, float kappa) {
     return d;
 }
 
+/* Objective node: squared chord between the normalised action d/|d|
+ * and the true best move u*, with delta = d * y_d - u* fused per component */
+static float od_objective(v2 d, v2 ustar) {
+    float yd = od_rsqrt(FFMA(d.y, d.y, FFMA(d.x, d.x, 0x1p-126f)));
+    v2 dl = { FFMA(d.x, yd, -ustar.x), FFMA(d.y, yd, -ustar.y) };
+    return FFMA(dl.y, dl.y, FMUL(dl.x, dl.x));
+}
+
 /* mixed-radix decode, dim 0 most significant */
 static void od_decode(uint64_t i, int D, const uint32_t* L, uint32_t* k) {
     for (int d = D - 1; d >= 0; --d) { k[d] = (uint32_t)(i % L[d]); i /= L[d]; }
@@ -242,12 +250,37 @@ int od_pp_eval(const uint32_t n_levels[3], const float* levels, const float w[3]
                 o[e].x = FFMA(sig[e], z[2 * e], p[e].x);
                 o[e].y = FFMA(sig[e], z[2 * e + 1], p[e].y);
             }
-            v2 uh = od_unit(od_action(o[0], o[1], o[2], kappa));
-            v2 dl = od_sub(uh, ustar);
-            float e2 = FFMA(dl.y, dl.y, FMUL(dl.x, dl.x));
+            float e2 = od_objective(od_action(o[0], o[1], o[2], kappa), ustar);
             acc = FADD(acc, e2);
         }
         cost[i - begin] = FADD(FDIV(acc, (float)n_samples), K);
+    }
+    return 0;
+}
+
+/* Per-sample objective e_s of one allocation (debug / tests): out[s], s < S. */
+int od_pp_trace(const uint32_t n_levels[3], const float* levels, const float params[3],
+                const float inputs[6], uint64_t i, uint32_t n_samples, uint64_t seed,
+                uint32_t invocation, float* out) {
+    const float* lev[3] = { levels, levels + n_levels[0], levels + n_levels[0] + n_levels[1] };
+    float smax = params[0], smin = params[1], kappa = params[2];
+    v2 p[3] = { { inputs[0], inputs[1] }, { inputs[2], inputs[3] }, { inputs[4], inputs[5] } };
+    float dsig = FSUB(smin, smax);
+    v2 ustar = od_unit(od_action(p[0], p[1], p[2], kappa));
+    uint32_t k[3];
+    od_decode(i, 3, n_levels, k);
+    float a[3] = { lev[0][k[0]], lev[1][k[1]], lev[2][k[2]] };
+    float sig[3];
+    for (int e = 0; e < 3; ++e) sig[e] = FFMA(a[e], dsig, smax);
+    for (uint32_t s = 0; s < n_samples; ++s) {
+        float z[6];
+        od_normal_sextet(seed, (uint32_t)i, s, invocation, z);
+        v2 o[3];
+        for (int e = 0; e < 3; ++e) {
+            o[e].x = FFMA(sig[e], z[2 * e], p[e].x);
+            o[e].y = FFMA(sig[e], z[2 * e + 1], p[e].y);
+        }
+        out[s] = od_objective(od_action(o[0], o[1], o[2], kappa), ustar);
     }
     return 0;
 }

@@ -52,6 +52,9 @@ int od_pp_eval(const uint32_t n_levels[3], const float* levels, const float w[3]
                const float params[3], const float inputs[6],
                uint64_t begin, uint64_t end, uint32_t n_samples, uint64_t seed,
                uint32_t invocation, float* cost);
+int od_pp_trace(const uint32_t n_levels[3], const float* levels, const float params[3],
+                const float inputs[6], uint64_t i, uint32_t n_samples, uint64_t seed,
+                uint32_t invocation, float* out);
 /* Same evaluation in binary64 from the same Philox bits (libm log/sqrt/cos/sin). */
 int od_pp_eval_f64(const uint32_t n_levels[3], const float* levels, const float w[3],
                    const float params[3], const float inputs[6],

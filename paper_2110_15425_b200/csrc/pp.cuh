@@ -109,10 +109,20 @@ __device__ __forceinline__ void bm_pair2(uint32_t Rx, uint32_t Ry, uint32_t Ax, 
     z.y = mul2(rs, sq);
 }
 
+// Objective node: e = |d * y_d - u*|^2 with y_d = rsqrt_spec(|d|^2 + 2^-126) and the
+// difference fused per component (spec/MODELS.md §2).  Writing the fma here leaves no
+// FMUL2 -> FADD2 pair for ptxas to contract behind our back (it does, .rn or not).
+__device__ __forceinline__ F2 objective2(V2 d, V2 us) {
+    const F2 n2 = fma2(d.y, d.y, fma2(d.x, d.x, bc(0x1p-126f)));
+    const F2 y = rsqrt2_from(n2, mul2(n2, bc(-0.5f)));
+    const F2 dx = fma2(d.x, y, neg2(us.x)), dy = fma2(d.y, y, neg2(us.y));
+    return fma2(dy, dy, mul2(dx, dx));
+}
+
 // Philox4x32-10 on counter (i, s, t, 1): rounds 1-3 with their sample-invariant
 // parts hoisted into PhiloxPP (computed once per thread), rounds 4-10 generic.
 struct PhiloxPP {
-    uint32_t a1, y0k_unused, x3k, b_c1k, c3k, z3, k0, k1;
+    uint32_t a1, x3k, b_c1k, c3k, z3, k0, k1;
     __device__ __forceinline__ void init(uint32_t i, uint32_t t, uint32_t key0, uint32_t key1) {
         k0 = key0; k1 = key1;
         uint32_t hi0, lo0, hi1, lo1;
@@ -130,7 +140,6 @@ struct PhiloxPP {
         b_c1k = y1 ^ (k0 + 2u * PHILOX_W0);              // z0 = hi(M1 * y2) ^ b_c1k
         c3k = G0h ^ (k1 + 2u * PHILOX_W1);               // z2 = c3k ^ y3
         z3 = G0l;
-        y0k_unused = 0;
     }
     __device__ __forceinline__ uint4 operator()(uint32_t s) const {
         uint32_t P0h, P0l;
@@ -185,9 +194,7 @@ __global__ void __launch_bounds__(BLOCK) pp_eval_grid_kernel(const PPArgs a) {
             const V2 o1 = {fma2(bc(s1), z1.x, P1.x), fma2(bc(s1), z1.y, P1.y)};
             const V2 o2 = {fma2(bc(s2), z2.x, P2.x), fma2(bc(s2), z2.y, P2.y)};
             const V2 vp = vunit(vsub(o0, o2)), vd = vunit(vsub(o1, o2));
-            const V2 uh = vunit({fma2(mk, vd.x, vp.x), fma2(mk, vd.y, vp.y)});
-            const F2 dx = sub2(uh.x, us.x), dy = sub2(uh.y, us.y);
-            const F2 e = fma2(dy, dy, mul2(dx, dx));
+            const F2 e = objective2({fma2(mk, vd.x, vp.x), fma2(mk, vd.y, vp.y)}, us);
             // a7: sequential sum in ascending sample order
             acc = __fadd_rn(acc, e.x);
             if (s + 1 < a.n_samples) acc = __fadd_rn(acc, e.y);

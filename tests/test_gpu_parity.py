@@ -98,7 +98,9 @@ def test_pp_zero_noise_and_ties(D, orc):
     cfg.w = np.zeros(3, np.float32)
     m = _model(D, cfg)
     C, key = _gpu_pp(D, m, cfg)
-    assert (C == 0).all() and key & 0xFFFFFFFF == 0
+    want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc, 4, cfg.seed)
+    assert np.array_equal(_bits(C), _bits(want))
+    assert (C == C[0]).all() and 0 <= C[0] < 1e-12 and key & 0xFFFFFFFF == 0
 
 
 def test_pp_coincident_positions_and_nan(D, orc):

@@ -44,8 +44,11 @@ def test_evaluation_counts_match_paper(orc, L, count):
         assert run(orc, cfg).shape == (count,)
 
 
-def test_zero_noise_cost_is_control_cost_exactly(orc):
-    """sigma = 0 -> o = p exactly -> u_hat = u_star -> e = 0 -> C = K."""
+def test_zero_noise_cost_is_control_cost(orc):
+    """sigma = 0 -> o = p exactly -> every sample's action equals the true best
+    move, so e is the same tiny constant e0 for every allocation (the rounding
+    residual of u*, |e0| <= (4 ulp)^2 ~ 1e-13) and C = K exactly whenever
+    K >= 1e-6 absorbs it."""
     cfg = W.pp_cfg1()
     cfg.params = np.array([0.0, 0.0, 0.5], np.float32)
     C = run(orc, cfg)
@@ -54,7 +57,10 @@ def test_zero_noise_cost_is_control_cost_exactly(orc):
         a = [cfg.levels[3 * d + k[d]] for d in range(3)]
         w = cfg.w
         K = fma32(w[2], a[2], fma32(w[1], a[1], f32_round(Fraction(float(w[0])) * Fraction(float(a[0])))))
-        assert C[i] == K, (i, C[i], K)
+        if K >= 1e-6:
+            assert C[i] == K, (i, C[i], K)
+        else:
+            assert 0 <= C[i] - K < 1e-12
     # monotone non-decreasing in every level for w >= 0, argmin at index 0
     Cg = C.reshape(3, 3, 3)
     for ax in range(3):
@@ -70,8 +76,8 @@ def test_mixed_radix_decode_dim0_most_significant(orc):
     cfg.levels = np.concatenate([np.arange(L, dtype=np.float32)] * 3)
     cfg.w = np.array([L * L, L, 1], np.float32)
     cfg.params = np.array([0.0, 0.0, 0.5], np.float32)
-    idx = np.array([0, 1, 99, 100, 12345, 999999])
-    for i in idx:
+    assert 0 <= run(orc, cfg, 0, 1)[0] < 1e-12
+    for i in (1, 99, 100, 12345, 999999):
         assert run(orc, cfg, i, i + 1)[0] == float(i)
 
 
@@ -89,7 +95,7 @@ def test_all_ties_lowest_index_any_split(orc):
     cfg.params = np.array([0.0, 0.0, 0.5], np.float32)
     cfg.w = np.zeros(3, np.float32)
     C = run(orc, cfg)
-    assert (C == C[0]).all()
+    assert (C == C[0]).all() and 0 <= C[0] < 1e-12
     for cut in (1, 17, 40, 63):
         k1, _ = orc.argmax_net(-C[:cut], 0)
         k2, _ = orc.argmax_net(-C[cut:], cut)
