@@ -7,11 +7,11 @@
 
 namespace distill {
 
-typedef unsigned long long key_t;
-constexpr key_t KEY_INIT = 0xFFFFFFFFFFFFFFFFull;
+typedef unsigned long long key64_t;
+constexpr key64_t KEY_INIT = 0xFFFFFFFFFFFFFFFFull;
 
 // key(C, i) = ord(canon(C)) << 32 | i : min key = lowest cost, then lowest index.
-__device__ __forceinline__ key_t make_key(float C, uint32_t idx) {
+__device__ __forceinline__ key64_t make_key(float C, uint32_t idx) {
     uint32_t hi;
     if (C != C) {
         hi = 0xFFFFFFFFu;                     // NaN never wins
@@ -19,13 +19,13 @@ __device__ __forceinline__ key_t make_key(float C, uint32_t idx) {
         const uint32_t b = __float_as_uint(C == 0.0f ? 0.0f : C);   // -0 -> +0
         hi = (b >> 31) ? ~b : (b | 0x80000000u);
     }
-    return ((key_t)hi << 32) | idx;
+    return ((key64_t)hi << 32) | idx;
 }
 
-__device__ __forceinline__ key_t warp_min_key(key_t k) {
+__device__ __forceinline__ key64_t warp_min_key(key64_t k) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-        const key_t o = __shfl_xor_sync(0xFFFFFFFFu, k, off);
+        const key64_t o = __shfl_xor_sync(0xFFFFFFFFu, k, off);
         k = o < k ? o : k;
     }
     return k;
@@ -34,8 +34,8 @@ __device__ __forceinline__ key_t warp_min_key(key_t k) {
 // Block-wide min of one key per thread, then ONE atomicMin per block.
 // All threads of the block must call it (uses __syncthreads).
 template <int BLOCK>
-__device__ __forceinline__ void block_min_key_atomic(key_t k, key_t* dst) {
-    __shared__ key_t s_warp[BLOCK / 32];
+__device__ __forceinline__ void block_min_key_atomic(key64_t k, key64_t* dst) {
+    __shared__ key64_t s_warp[BLOCK / 32];
     k = warp_min_key(k);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (lane == 0) s_warp[wid] = k;
@@ -51,8 +51,8 @@ __device__ __forceinline__ void block_min_key_atomic(key_t k, key_t* dst) {
 // Grid-stride, vectorised float4 loads when the pointer is 16-B aligned.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) argmax_net_kernel(const float* __restrict__ v, uint64_t n,
-                                                           uint32_t base, key_t* __restrict__ best) {
-    key_t k = KEY_INIT;
+                                                           uint32_t base, key64_t* __restrict__ best) {
+    key64_t k = KEY_INIT;
     const uint64_t tid = (uint64_t)blockIdx.x * BLOCK + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
     if ((reinterpret_cast<uintptr_t>(v) & 15u) == 0) {
@@ -61,20 +61,20 @@ __global__ void __launch_bounds__(BLOCK) argmax_net_kernel(const float* __restri
         for (uint64_t j = tid; j < n4; j += stride) {
             const float4 x = __ldg(v4 + j);
             const uint32_t i0 = base + (uint32_t)(4 * j);
-            key_t a = make_key(-x.x, i0), b = make_key(-x.y, i0 + 1);
-            key_t c = make_key(-x.z, i0 + 2), d = make_key(-x.w, i0 + 3);
+            key64_t a = make_key(-x.x, i0), b = make_key(-x.y, i0 + 1);
+            key64_t c = make_key(-x.z, i0 + 2), d = make_key(-x.w, i0 + 3);
             a = a < b ? a : b;
             c = c < d ? c : d;
             a = a < c ? a : c;
             k = a < k ? a : k;
         }
         for (uint64_t j = 4 * n4 + tid; j < n; j += stride) {
-            const key_t a = make_key(-__ldg(v + j), base + (uint32_t)j);
+            const key64_t a = make_key(-__ldg(v + j), base + (uint32_t)j);
             k = a < k ? a : k;
         }
     } else {
         for (uint64_t j = tid; j < n; j += stride) {
-            const key_t a = make_key(-__ldg(v + j), base + (uint32_t)j);
+            const key64_t a = make_key(-__ldg(v + j), base + (uint32_t)j);
             k = a < k ? a : k;
         }
     }

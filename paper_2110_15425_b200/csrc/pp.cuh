@@ -33,46 +33,71 @@ struct PPArgs {
     uint32_t begin, count;                             // global index range [begin, begin+count)
     const float* __restrict__ levels;                  // device RO block: L0+L1+L2 floats
     float* __restrict__ net;                           // [count] or nullptr
-    key_t* __restrict__ best;                          // [1] or nullptr
+    key64_t* __restrict__ best;                          // [1] or nullptr
 };
 
-// ------------------------------------------------------------ packed binary32 helpers
+// ------------------------------------------------------------ two-lane binary32 helpers
+// Ops<false>: one packed FFMA2/FMUL2/FADD2 per step (both lanes in one
+// instruction, full 32-lane FMA datapath for 2 cycles).  Ops<true>: the same
+// step as two scalar FFMA/FMUL/FADD, which the scheduler can place on the
+// fmalite sub-pipe while fmaheavy runs the Philox IMAD.WIDEs.  Both round
+// every lane exactly like the scalar op, so the choice is pure scheduling.
 typedef float2 F2;
 __device__ __forceinline__ F2 bc(float a) { return make_float2(a, a); }
-__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ F2 mul2(F2 a, F2 b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ F2 add2(F2 a, F2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ F2 neg2(F2 a) { return make_float2(-a.x, -a.y); }
-__device__ __forceinline__ F2 sub2(F2 a, F2 b) { return __fadd2_rn(a, neg2(b)); }  // a - b exactly
 
-// rsqrt_spec on both lanes given y0 bits and h = 0.5 x (spec/RNG.md §4);
-// `mh` = -h (passed so callers that already hold -h save the multiply).
+template <bool SC> struct Ops {
+    static __device__ __forceinline__ F2 fma(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
+    static __device__ __forceinline__ F2 mul(F2 a, F2 b) { return __fmul2_rn(a, b); }
+    static __device__ __forceinline__ F2 add(F2 a, F2 b) { return __fadd2_rn(a, b); }
+};
+template <> struct Ops<true> {
+    static __device__ __forceinline__ F2 fma(F2 a, F2 b, F2 c) {
+        return make_float2(__fmaf_rn(a.x, b.x, c.x), __fmaf_rn(a.y, b.y, c.y));
+    }
+    static __device__ __forceinline__ F2 mul(F2 a, F2 b) { return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)); }
+    static __device__ __forceinline__ F2 add(F2 a, F2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
+};
+
+// rsqrt_spec on both lanes (spec/RNG.md §4); `mh` = -h = -0.5 x (callers that
+// already hold -h pass it and save the multiply).
+template <bool SC>
 __device__ __forceinline__ F2 rsqrt2_from(F2 x, F2 mh) {
+    using O = Ops<SC>;
     F2 y = make_float2(__uint_as_float(0x5F375A86u - (__float_as_uint(x.x) >> 1)),
                        __uint_as_float(0x5F375A86u - (__float_as_uint(x.y) >> 1)));
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        F2 t = mul2(y, y);
-        t = fma2(mh, t, bc(1.5f));
-        y = mul2(y, t);
+        F2 t = O::mul(y, y);
+        t = O::fma(mh, t, bc(1.5f));
+        y = O::mul(y, t);
     }
     return y;
 }
 
 struct V2 { F2 x, y; };   // a 2-D vector for the two samples of a pair
 
-__device__ __forceinline__ V2 vsub(V2 a, V2 b) { return {sub2(a.x, b.x), sub2(a.y, b.y)}; }
+template <bool SC>
+__device__ __forceinline__ V2 vsub(V2 a, V2 b) {
+    return {Ops<SC>::add(a.x, neg2(b.x)), Ops<SC>::add(a.y, neg2(b.y))};   // a - b exactly
+}
 
 // unit(v) (spec/MODELS.md §2): n2 = fma(v.y, v.y, fma(v.x, v.x, 2^-126)), v * rsqrt_spec(n2)
+template <bool SC>
 __device__ __forceinline__ V2 vunit(V2 v) {
-    const F2 n2 = fma2(v.y, v.y, fma2(v.x, v.x, bc(0x1p-126f)));
-    const F2 y = rsqrt2_from(n2, mul2(n2, bc(-0.5f)));
-    return {mul2(v.x, y), mul2(v.y, y)};
+    using O = Ops<SC>;
+    const F2 n2 = O::fma(v.y, v.y, O::fma(v.x, v.x, bc(0x1p-126f)));
+    const F2 y = rsqrt2_from<SC>(n2, O::mul(n2, bc(-0.5f)));
+    return {O::mul(v.x, y), O::mul(v.y, y)};
 }
 
 // Box-Muller pair for both samples: radius words R, angle words A (low 16 bits clear)
-// z = (rad * cos phi, rad * sin phi), spec/RNG.md §2-§6.
+// z = (rad * cos phi, rad * sin phi), spec/RNG.md §2-§6.  SLN/SRS/SSC choose
+// scalar lanes for the ln, rsqrt and sincos parts.
+template <bool SLN, bool SRS, bool SSC>
 __device__ __forceinline__ void bm_pair2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay, V2& z) {
+    using L = Ops<SLN>;
+    using Q = Ops<SSC>;
     // u1 = ((R >> 8) | 1) * 2^-24: convert the odd integer exactly and fold the
     // 2^-24 into the exponent constants of ln_spec (bits(u1) = bits(float(m)) - 24<<23)
     const uint32_t ix = __float_as_uint(__uint2float_rn((Rx >> 8) | 1u));
@@ -81,42 +106,44 @@ __device__ __forceinline__ void bm_pair2(uint32_t Rx, uint32_t Ry, uint32_t Ax, 
     const F2 m = make_float2(__uint_as_float((tx & 0x7FFFFFu) + 0x3F3504F3u),
                              __uint_as_float((ty & 0x7FFFFFu) + 0x3F3504F3u));
     const F2 fe = make_float2(__int2float_rn((int32_t)tx >> 23), __int2float_rn((int32_t)ty >> 23));
-    const F2 f = add2(m, bc(-1.0f));
-    F2 P = fma2(bc(D_L7), f, bc(D_L6));
-    P = fma2(P, f, bc(D_L5));
-    P = fma2(P, f, bc(D_L4));
-    P = fma2(P, f, bc(D_L3));
-    P = fma2(P, f, bc(D_L2));
-    P = fma2(P, f, bc(D_L1));
-    P = fma2(P, f, bc(D_L0));
-    F2 y = fma2(mul2(f, f), P, f);
-    y = fma2(fe, bc(D_LN2_LO), y);
-    y = fma2(fe, bc(D_LN2_HI), y);                       // y = ln_spec(u1) < 0
-    const F2 s = mul2(y, bc(-2.0f));                     // s = -2 ln u1 (exact scaling)
-    const F2 rad = mul2(s, rsqrt2_from(s, y));           // -h = -0.5 s = y exactly
+    const F2 f = L::add(m, bc(-1.0f));
+    F2 P = L::fma(bc(D_L7), f, bc(D_L6));
+    P = L::fma(P, f, bc(D_L5));
+    P = L::fma(P, f, bc(D_L4));
+    P = L::fma(P, f, bc(D_L3));
+    P = L::fma(P, f, bc(D_L2));
+    P = L::fma(P, f, bc(D_L1));
+    P = L::fma(P, f, bc(D_L0));
+    F2 y = L::fma(L::mul(f, f), P, f);
+    y = L::fma(fe, bc(D_LN2_LO), y);
+    y = L::fma(fe, bc(D_LN2_HI), y);                          // y = ln_spec(u1) < 0
+    const F2 s = Ops<SRS>::mul(y, bc(-2.0f));                 // s = -2 ln u1 (exact scaling)
+    const F2 rad = Ops<SRS>::mul(s, rsqrt2_from<SRS>(s, y));  // -h = -0.5 s = y exactly
     // sincos_spec: r from the angle bits, half-turn sign applied to rad
-    const F2 r = add2(make_float2(__uint_as_float(((Ax >> 8) & 0x7FFFFFu) | 0x3F800000u),
-                                  __uint_as_float(((Ay >> 8) & 0x7FFFFFu) | 0x3F800000u)),
-                      bc(-1.5f));
-    const F2 t = mul2(r, r);
-    const F2 S = fma2(fma2(fma2(fma2(bc(D_S4), t, bc(D_S3)), t, bc(D_S2)), t, bc(D_S1)), t, bc(D_S0));
-    const F2 C = fma2(fma2(fma2(fma2(bc(D_C4), t, bc(D_C3)), t, bc(D_C2)), t, bc(D_C1)), t, bc(D_C0));
-    const F2 cq = fma2(C, t, bc(1.0f));
-    const F2 sq = mul2(S, r);
+    const F2 r = Q::add(make_float2(__uint_as_float(((Ax >> 8) & 0x7FFFFFu) | 0x3F800000u),
+                                    __uint_as_float(((Ay >> 8) & 0x7FFFFFu) | 0x3F800000u)),
+                        bc(-1.5f));
+    const F2 t = Q::mul(r, r);
+    const F2 S = Q::fma(Q::fma(Q::fma(Q::fma(bc(D_S4), t, bc(D_S3)), t, bc(D_S2)), t, bc(D_S1)), t, bc(D_S0));
+    const F2 C = Q::fma(Q::fma(Q::fma(Q::fma(bc(D_C4), t, bc(D_C3)), t, bc(D_C2)), t, bc(D_C1)), t, bc(D_C0));
+    const F2 cq = Q::fma(C, t, bc(1.0f));
+    const F2 sq = Q::mul(S, r);
     const F2 rs = make_float2(__uint_as_float(__float_as_uint(rad.x) ^ (Ax & 0x80000000u)),
                               __uint_as_float(__float_as_uint(rad.y) ^ (Ay & 0x80000000u)));
-    z.x = mul2(rs, cq);   // (-rad) * c == -(rad * c) bit for bit
-    z.y = mul2(rs, sq);
+    z.x = Q::mul(rs, cq);   // (-rad) * c == -(rad * c) bit for bit
+    z.y = Q::mul(rs, sq);
 }
 
 // Objective node: e = |d * y_d - u*|^2 with y_d = rsqrt_spec(|d|^2 + 2^-126) and the
 // difference fused per component (spec/MODELS.md §2).  Writing the fma here leaves no
 // FMUL2 -> FADD2 pair for ptxas to contract behind our back (it does, .rn or not).
+template <bool SC>
 __device__ __forceinline__ F2 objective2(V2 d, V2 us) {
-    const F2 n2 = fma2(d.y, d.y, fma2(d.x, d.x, bc(0x1p-126f)));
-    const F2 y = rsqrt2_from(n2, mul2(n2, bc(-0.5f)));
-    const F2 dx = fma2(d.x, y, neg2(us.x)), dy = fma2(d.y, y, neg2(us.y));
-    return fma2(dy, dy, mul2(dx, dx));
+    using O = Ops<SC>;
+    const F2 n2 = O::fma(d.y, d.y, O::fma(d.x, d.x, bc(0x1p-126f)));
+    const F2 y = rsqrt2_from<SC>(n2, O::mul(n2, bc(-0.5f)));
+    const F2 dx = O::fma(d.x, y, neg2(us.x)), dy = O::fma(d.y, y, neg2(us.y));
+    return O::fma(dy, dy, O::mul(dx, dx));
 }
 
 // Philox4x32-10 on counter (i, s, t, 1): rounds 1-3 with their sample-invariant
@@ -152,10 +179,29 @@ struct PhiloxPP {
     }
 };
 
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) pp_eval_grid_kernel(const PPArgs a) {
+// Scheduling variants (all bit-identical; tools/pp_tune.cu measures them):
+// which two-lane steps run as scalar FFMA pairs instead of packed FFMA2.
+enum : int {
+    PP_SC_OBJECTIVE = 1,    // unit(d) + objective
+    PP_SC_UNIT_PRED = 2,    // unit(o_pred - o_player)
+    PP_SC_UNIT_PREY = 4,    // unit(o_prey - o_player)
+    PP_SC_LN2 = 8,          // ln of entity 2 (player)
+    PP_SC_RSQ2 = 16,        // sqrt of entity 2
+    PP_SC_SC2 = 32,         // sincos of entity 2
+};
+#ifndef DISTILL_PP_MASK
+#define DISTILL_PP_MASK 0
+#endif
+#ifndef DISTILL_PP_MINB
+#define DISTILL_PP_MINB 0
+#endif
+
+template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs a) {
+    constexpr bool SOBJ = MASK & PP_SC_OBJECTIVE, SUPD = MASK & PP_SC_UNIT_PRED, SUPY = MASK & PP_SC_UNIT_PREY;
+    constexpr bool SLN2 = MASK & PP_SC_LN2, SRS2 = MASK & PP_SC_RSQ2, SSC2 = MASK & PP_SC_SC2;
     const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
-    key_t key = KEY_INIT;
+    key64_t key = KEY_INIT;
     if (tid < a.count) {
         const uint32_t i = a.begin + tid;
         // a1: mixed-radix decode, signal 0 most significant
@@ -174,8 +220,8 @@ __global__ void __launch_bounds__(BLOCK) pp_eval_grid_kernel(const PPArgs a) {
         const V2 P0 = {bc(a.prey_x), bc(a.prey_y)}, P1 = {bc(a.pred_x), bc(a.pred_y)};
         const V2 P2 = {bc(a.pl_x), bc(a.pl_y)};
         const F2 mk = bc(-a.kappa);
-        V2 up = vunit(vsub(P0, P2)), ud = vunit(vsub(P1, P2));
-        const V2 us = vunit({fma2(mk, ud.x, up.x), fma2(mk, ud.y, up.y)});
+        const V2 up = vunit<false>(vsub<false>(P0, P2)), ud = vunit<false>(vsub<false>(P1, P2));
+        const V2 us = vunit<false>({__ffma2_rn(mk, ud.x, up.x), __ffma2_rn(mk, ud.y, up.y)});
 
         PhiloxPP rng;
         rng.init(i, a.invocation, a.key0, a.key1);
@@ -186,15 +232,18 @@ __global__ void __launch_bounds__(BLOCK) pp_eval_grid_kernel(const PPArgs a) {
             const uint4 Y = rng(s + 1);
             // a3: sextet packing -> three 2-D Box-Muller pairs (spec/RNG.md §6)
             V2 z0, z1, z2;
-            bm_pair2(X.x, Y.x, X.w << 16, Y.w << 16, z0);
-            bm_pair2(X.y, Y.y, X.w & 0xFFFF0000u, Y.w & 0xFFFF0000u, z1);
-            bm_pair2(X.z, Y.z, (X.x << 24) | ((X.y & 0xFFu) << 16), (Y.x << 24) | ((Y.y & 0xFFu) << 16), z2);
+            bm_pair2<false, false, false>(X.x, Y.x, X.w << 16, Y.w << 16, z0);
+            bm_pair2<false, false, false>(X.y, Y.y, X.w & 0xFFFF0000u, Y.w & 0xFFFF0000u, z1);
+            bm_pair2<SLN2, SRS2, SSC2>(X.z, Y.z, (X.x << 24) | ((X.y & 0xFFu) << 16),
+                                       (Y.x << 24) | ((Y.y & 0xFFu) << 16), z2);
             // a4: Obs -> Action -> Objective
-            const V2 o0 = {fma2(bc(s0), z0.x, P0.x), fma2(bc(s0), z0.y, P0.y)};
-            const V2 o1 = {fma2(bc(s1), z1.x, P1.x), fma2(bc(s1), z1.y, P1.y)};
-            const V2 o2 = {fma2(bc(s2), z2.x, P2.x), fma2(bc(s2), z2.y, P2.y)};
-            const V2 vp = vunit(vsub(o0, o2)), vd = vunit(vsub(o1, o2));
-            const F2 e = objective2({fma2(mk, vd.x, vp.x), fma2(mk, vd.y, vp.y)}, us);
+            using O = Ops<false>;
+            const V2 o0 = {O::fma(bc(s0), z0.x, P0.x), O::fma(bc(s0), z0.y, P0.y)};
+            const V2 o1 = {O::fma(bc(s1), z1.x, P1.x), O::fma(bc(s1), z1.y, P1.y)};
+            const V2 o2 = {O::fma(bc(s2), z2.x, P2.x), O::fma(bc(s2), z2.y, P2.y)};
+            const V2 vp = vunit<SUPY>(vsub<SUPY>(o0, o2)), vd = vunit<SUPD>(vsub<SUPD>(o1, o2));
+            const V2 d = {Ops<SOBJ>::fma(mk, vd.x, vp.x), Ops<SOBJ>::fma(mk, vd.y, vp.y)};
+            const F2 e = objective2<SOBJ>(d, us);
             // a7: sequential sum in ascending sample order
             acc = __fadd_rn(acc, e.x);
             if (s + 1 < a.n_samples) acc = __fadd_rn(acc, e.y);

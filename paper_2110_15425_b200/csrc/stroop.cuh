@@ -24,7 +24,7 @@ struct StroopArgs {
     const float* __restrict__ levels;          // L0 + L1 floats
     unsigned long long* __restrict__ counts;   // [count][3]
     float* __restrict__ net;
-    key_t* __restrict__ best;
+    key64_t* __restrict__ best;
 };
 
 template <int BLOCK>
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(BLOCK) stroop_sim_kernel(const StroopArgs a, u
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) stroop_finalize_kernel(const StroopArgs a) {
     const uint32_t t = blockIdx.x * BLOCK + threadIdx.x;
-    key_t k = KEY_INIT;
+    key64_t k = KEY_INIT;
     if (t < a.count) {
         const uint32_t i = a.begin + t;
         const uint32_t k1 = i % a.L1, k0 = i / a.L1;
