@@ -110,9 +110,9 @@ float od_rsqrt(float x) {
     float y = u2f(0x5F375A86u - (f2u(x) >> 1));
     float h = FMUL(0.5f, x);
     for (int k = 0; k < 3; ++k) {
-        float t = FMUL(y, y);
-        t = FFMA(-h, t, 1.5f);
-        y = FMUL(y, t);
+        float p = FMUL(h, y);
+        float r = FFMA(-p, y, 0.5f);
+        y = FFMA(y, r, y);
     }
     return y;
 }

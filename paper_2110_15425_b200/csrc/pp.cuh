@@ -59,8 +59,10 @@ template <> struct Ops<true> {
     static __device__ __forceinline__ F2 add(F2 a, F2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
 };
 
-// rsqrt_spec on both lanes (spec/RNG.md §4); `mh` = -h = -0.5 x (callers that
-// already hold -h pass it and save the multiply).
+// rsqrt_spec on both lanes (spec/RNG.md §4), residual Newton form
+//   p = h y ; r = fma(-p, y, 0.5) ; y = fma(y, r, y)
+// `mh` = -h = -0.5 x (callers that already hold -h pass it and save the
+// multiply): -p = mh * y exactly, so r = fma(mh * y, y, 0.5).
 template <bool SC>
 __device__ __forceinline__ F2 rsqrt2_from(F2 x, F2 mh) {
     using O = Ops<SC>;
@@ -68,9 +70,9 @@ __device__ __forceinline__ F2 rsqrt2_from(F2 x, F2 mh) {
                        __uint_as_float(0x5F375A86u - (__float_as_uint(x.y) >> 1)));
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        F2 t = O::mul(y, y);
-        t = O::fma(mh, t, bc(1.5f));
-        y = O::mul(y, t);
+        const F2 q = O::mul(mh, y);              // -p
+        const F2 r = O::fma(q, y, bc(0.5f));
+        y = O::fma(y, r, y);
     }
     return y;
 }
@@ -196,64 +198,105 @@ enum : int {
 #define DISTILL_PP_MINB 0
 #endif
 
-template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB>
-__global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs a) {
+// Full evaluation of allocation i (a1-a8): returns the cost C.
+template <int MASK, bool PIPE>
+__device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i) {
     constexpr bool SOBJ = MASK & PP_SC_OBJECTIVE, SUPD = MASK & PP_SC_UNIT_PRED, SUPY = MASK & PP_SC_UNIT_PREY;
     constexpr bool SLN2 = MASK & PP_SC_LN2, SRS2 = MASK & PP_SC_RSQ2, SSC2 = MASK & PP_SC_SC2;
+    // a1: mixed-radix decode, signal 0 most significant
+    const uint32_t k2 = i % a.L2, r = i / a.L2;
+    const uint32_t k1 = r % a.L1, k0 = r / a.L1;
+    const float a0 = __ldg(a.levels + k0);
+    const float a1 = __ldg(a.levels + a.L0 + k1);
+    const float a2 = __ldg(a.levels + a.L0 + a.L1 + k2);
+    const float dsig = __fadd_rn(a.sigma_min, -a.sigma_max);
+    const float s0 = __fmaf_rn(a0, dsig, a.sigma_max);
+    const float s1 = __fmaf_rn(a1, dsig, a.sigma_max);
+    const float s2 = __fmaf_rn(a2, dsig, a.sigma_max);
+    const float K = __fmaf_rn(a.w2, a2, __fmaf_rn(a.w1, a1, __fmul_rn(a.w0, a0)));
+
+    // u* = unit(action(true positions)) on broadcast lanes
+    const V2 P0 = {bc(a.prey_x), bc(a.prey_y)}, P1 = {bc(a.pred_x), bc(a.pred_y)};
+    const V2 P2 = {bc(a.pl_x), bc(a.pl_y)};
+    const F2 mk = bc(-a.kappa);
+    const V2 up = vunit<false>(vsub<false>(P0, P2)), ud = vunit<false>(vsub<false>(P1, P2));
+    const V2 us = vunit<false>({__ffma2_rn(mk, ud.x, up.x), __ffma2_rn(mk, ud.y, up.y)});
+
+    PhiloxPP rng;
+    rng.init(i, a.invocation, a.key0, a.key1);
+    float acc = 0.0f;
+    uint4 Xn, Yn;
+    if (PIPE) { Xn = rng(0); Yn = rng(1); }
+    for (uint32_t s = 0; s < a.n_samples; s += 2) {
+        // a2: one Philox block per sample, two samples per iteration
+        uint4 X, Y;
+        if (PIPE) {            // software pipelining: next pair's Philox overlaps this pair's math
+            X = Xn; Y = Yn;
+            Xn = rng(s + 2); Yn = rng(s + 3);
+        } else {
+            X = rng(s); Y = rng(s + 1);
+        }
+        // a3: sextet packing -> three 2-D Box-Muller pairs (spec/RNG.md §6)
+        V2 z0, z1, z2;
+        bm_pair2<false, false, false>(X.x, Y.x, X.w << 16, Y.w << 16, z0);
+        bm_pair2<false, false, false>(X.y, Y.y, X.w & 0xFFFF0000u, Y.w & 0xFFFF0000u, z1);
+        bm_pair2<SLN2, SRS2, SSC2>(X.z, Y.z, (X.x << 24) | ((X.y & 0xFFu) << 16),
+                                   (Y.x << 24) | ((Y.y & 0xFFu) << 16), z2);
+        // a4: Obs -> Action -> Objective
+        using O = Ops<false>;
+        const V2 o0 = {O::fma(bc(s0), z0.x, P0.x), O::fma(bc(s0), z0.y, P0.y)};
+        const V2 o1 = {O::fma(bc(s1), z1.x, P1.x), O::fma(bc(s1), z1.y, P1.y)};
+        const V2 o2 = {O::fma(bc(s2), z2.x, P2.x), O::fma(bc(s2), z2.y, P2.y)};
+        const V2 vp = vunit<SUPY>(vsub<SUPY>(o0, o2)), vd = vunit<SUPD>(vsub<SUPD>(o1, o2));
+        const V2 d = {Ops<SOBJ>::fma(mk, vd.x, vp.x), Ops<SOBJ>::fma(mk, vd.y, vp.y)};
+        const F2 e = objective2<SOBJ>(d, us);
+        // a7: sequential sum in ascending sample order
+        acc = __fadd_rn(acc, e.x);
+        if (s + 1 < a.n_samples) acc = __fadd_rn(acc, e.y);
+    }
+    // a8: net of cost
+    return __fadd_rn(__fdiv_rn(acc, __uint2float_rn(a.n_samples)), K);
+}
+
+// One thread per allocation; one atomicMin per block.
+template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false>
+__global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs a) {
     const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
     key64_t key = KEY_INIT;
     if (tid < a.count) {
         const uint32_t i = a.begin + tid;
-        // a1: mixed-radix decode, signal 0 most significant
-        const uint32_t k2 = i % a.L2, r = i / a.L2;
-        const uint32_t k1 = r % a.L1, k0 = r / a.L1;
-        const float a0 = __ldg(a.levels + k0);
-        const float a1 = __ldg(a.levels + a.L0 + k1);
-        const float a2 = __ldg(a.levels + a.L0 + a.L1 + k2);
-        const float dsig = __fadd_rn(a.sigma_min, -a.sigma_max);
-        const float s0 = __fmaf_rn(a0, dsig, a.sigma_max);
-        const float s1 = __fmaf_rn(a1, dsig, a.sigma_max);
-        const float s2 = __fmaf_rn(a2, dsig, a.sigma_max);
-        const float K = __fmaf_rn(a.w2, a2, __fmaf_rn(a.w1, a1, __fmul_rn(a.w0, a0)));
-
-        // u* = unit(action(true positions)), computed in lane x of the packed helpers
-        const V2 P0 = {bc(a.prey_x), bc(a.prey_y)}, P1 = {bc(a.pred_x), bc(a.pred_y)};
-        const V2 P2 = {bc(a.pl_x), bc(a.pl_y)};
-        const F2 mk = bc(-a.kappa);
-        const V2 up = vunit<false>(vsub<false>(P0, P2)), ud = vunit<false>(vsub<false>(P1, P2));
-        const V2 us = vunit<false>({__ffma2_rn(mk, ud.x, up.x), __ffma2_rn(mk, ud.y, up.y)});
-
-        PhiloxPP rng;
-        rng.init(i, a.invocation, a.key0, a.key1);
-        float acc = 0.0f;
-        for (uint32_t s = 0; s < a.n_samples; s += 2) {
-            // a2: one Philox block per sample, two samples per iteration
-            const uint4 X = rng(s);
-            const uint4 Y = rng(s + 1);
-            // a3: sextet packing -> three 2-D Box-Muller pairs (spec/RNG.md §6)
-            V2 z0, z1, z2;
-            bm_pair2<false, false, false>(X.x, Y.x, X.w << 16, Y.w << 16, z0);
-            bm_pair2<false, false, false>(X.y, Y.y, X.w & 0xFFFF0000u, Y.w & 0xFFFF0000u, z1);
-            bm_pair2<SLN2, SRS2, SSC2>(X.z, Y.z, (X.x << 24) | ((X.y & 0xFFu) << 16),
-                                       (Y.x << 24) | ((Y.y & 0xFFu) << 16), z2);
-            // a4: Obs -> Action -> Objective
-            using O = Ops<false>;
-            const V2 o0 = {O::fma(bc(s0), z0.x, P0.x), O::fma(bc(s0), z0.y, P0.y)};
-            const V2 o1 = {O::fma(bc(s1), z1.x, P1.x), O::fma(bc(s1), z1.y, P1.y)};
-            const V2 o2 = {O::fma(bc(s2), z2.x, P2.x), O::fma(bc(s2), z2.y, P2.y)};
-            const V2 vp = vunit<SUPY>(vsub<SUPY>(o0, o2)), vd = vunit<SUPD>(vsub<SUPD>(o1, o2));
-            const V2 d = {Ops<SOBJ>::fma(mk, vd.x, vp.x), Ops<SOBJ>::fma(mk, vd.y, vp.y)};
-            const F2 e = objective2<SOBJ>(d, us);
-            // a7: sequential sum in ascending sample order
-            acc = __fadd_rn(acc, e.x);
-            if (s + 1 < a.n_samples) acc = __fadd_rn(acc, e.y);
-        }
-        // a8: net of cost
-        const float C = __fadd_rn(__fdiv_rn(acc, __uint2float_rn(a.n_samples)), K);
+        const float C = pp_eval_alloc<MASK, PIPE>(a, i);
         if (a.net) a.net[tid] = -C;
         key = make_key(C, i);
     }
     // a9: (value, index) argmin -> one atomic per block
+    if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
+}
+
+// Persistent variant: a fixed grid of resident blocks pulls BLOCK-allocation
+// chunks from a device counter (zeroed by the caller before the launch), so
+// the last wave has no idle SMs; keys are min-combined per block across chunks.
+template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false>
+__global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_persistent_kernel(const PPArgs a,
+                                                                               unsigned int* __restrict__ counter) {
+    __shared__ unsigned int s_chunk;
+    const uint32_t n_chunks = (a.count + BLOCK - 1) / BLOCK;
+    key64_t key = KEY_INIT;
+    for (;;) {
+        if (threadIdx.x == 0) s_chunk = atomicAdd(counter, 1u);
+        __syncthreads();
+        const uint32_t c = s_chunk;
+        __syncthreads();
+        if (c >= n_chunks) break;
+        const uint32_t tid = c * BLOCK + threadIdx.x;
+        if (tid < a.count) {
+            const uint32_t i = a.begin + tid;
+            const float C = pp_eval_alloc<MASK, PIPE>(a, i);
+            if (a.net) a.net[tid] = -C;
+            const key64_t k = make_key(C, i);
+            key = k < key ? k : key;
+        }
+    }
     if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
 }
 

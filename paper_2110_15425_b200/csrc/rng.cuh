@@ -94,9 +94,9 @@ __device__ __forceinline__ float rsqrt_spec(float x) {
     const float h = __fmul_rn(0.5f, x);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        float t = __fmul_rn(y, y);
-        t = __fmaf_rn(-h, t, 1.5f);
-        y = __fmul_rn(y, t);
+        const float p = __fmul_rn(h, y);
+        const float r = __fmaf_rn(-p, y, 0.5f);
+        y = __fmaf_rn(y, r, y);
     }
     return y;
 }

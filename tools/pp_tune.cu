@@ -7,18 +7,35 @@
 #include "../paper_2110_15425_b200/csrc/pp.cuh"
 using namespace distill;
 
-template <int BLOCK, int MASK, int MINB>
+static unsigned int* g_counter = nullptr;
+
+template <int BLOCK, int MASK, int MINB, bool PIPE = false, bool PERS = false>
 void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_ref) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, pp_eval_grid_kernel<BLOCK, MASK, MINB>);
-    const unsigned grid = (a.count + BLOCK - 1) / BLOCK;
+    unsigned grid;
+    if (PERS) {
+        cudaFuncGetAttributes(&fa, pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE>);
+        int per_sm = 0, n_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE>,
+                                                      BLOCK, 0);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+        grid = per_sm * n_sm;
+    } else {
+        cudaFuncGetAttributes(&fa, pp_eval_grid_kernel<BLOCK, MASK, MINB, PIPE>);
+        grid = (a.count + BLOCK - 1) / BLOCK;
+    }
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     float best = 1e30f;
     for (int rep = 0; rep < 6; ++rep) {
         cudaMemset(a.best, 0xFF, 8);
         cudaEventRecord(e0);
-        pp_eval_grid_kernel<BLOCK, MASK, MINB><<<grid, BLOCK>>>(a);
+        if (PERS) {
+            cudaMemsetAsync(g_counter, 0, 4);
+            pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE><<<grid, BLOCK>>>(a, g_counter);
+        } else {
+            pp_eval_grid_kernel<BLOCK, MASK, MINB, PIPE><<<grid, BLOCK>>>(a);
+        }
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -30,9 +47,10 @@ void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_re
     bool same = true;
     if (is_ref) memcpy(ref_net, h.data(), a.count * 4);
     else same = memcmp(ref_net, h.data(), a.count * 4) == 0 && k == ref_key;
-    const double flops = (double)a.count * (a.n_samples * 257.0 + 13) + 66;
-    printf("%-28s block %4d mask %2d minb %d regs %3d  %8.4f ms  %6.2f TF/s  frac %.3f  %s\n", name, BLOCK, MASK, MINB,
-           fa.numRegs, best, flops / best / 1e9, flops / best / 1e9 / 74.45, same ? "bit-identical" : "MISMATCH");
+    const double flops = (double)a.count * (a.n_samples * 275.0 + 13) + 75;
+    printf("%-26s b%4d m%2d minb%d pipe%d pers%d grid %6u regs %3d %8.4f ms %6.2f TF/s frac %.3f %s\n", name, BLOCK,
+           MASK, MINB, (int)PIPE, (int)PERS, grid, fa.numRegs, best, flops / best / 1e9, flops / best / 1e9 / 74.45,
+           same ? "bit-identical" : "MISMATCH");
 }
 
 int main() {
@@ -47,29 +65,21 @@ int main() {
     a.begin = 0; a.count = L * L * L; a.levels = dl;
     cudaMalloc((void**)&a.net, a.count * 4); cudaMalloc((void**)&a.best, 8);
     std::vector<float> ref(a.count);
+    cudaMalloc((void**)&g_counter, 4);
     run<256, 0, 0>("packed (ref)", a, ref.data(), 0, true);
     key64_t rk; cudaMemcpy(&rk, a.best, 8, cudaMemcpyDeviceToHost);
-#define V(B, M, N, name) run<B, M, N>(name, a, ref.data(), rk, false)
-    V(256, 0, 1, "packed minb1");
-    V(256, 0, 2, "packed minb2");
-    V(256, 0, 3, "packed minb3");
-    V(256, 0, 4, "packed minb4");
-    V(256, 0, 6, "packed minb6");
-    V(256, 1, 0, "obj scalar");
-    V(256, 2, 0, "unit pred scalar");
-    V(256, 3, 0, "obj+unit pred");
-    V(256, 7, 0, "obj+both units");
-    V(256, 32, 0, "sincos2 scalar");
-    V(256, 33, 0, "obj+sincos2");
-    V(256, 56, 0, "entity2 BM scalar");
-    V(256, 35, 0, "obj+pred+sincos2");
-    V(256, 1, 4, "obj scalar minb4");
-    V(256, 3, 4, "obj+pred minb4");
-    V(256, 3, 3, "obj+pred minb3");
-    V(256, 1, 2, "obj scalar minb2");
-    V(128, 0, 0, "packed b128");
-    V(128, 3, 0, "obj+pred b128");
-    V(512, 0, 0, "packed b512");
+#define V(B, M, N, P, Q, name) run<B, M, N, P, Q>(name, a, ref.data(), rk, false)
+    V(128, 0, 0, false, false, "b128");
+    V(256, 0, 0, true, false, "pipe");
+    V(128, 0, 0, true, false, "pipe b128");
+    V(256, 0, 0, false, true, "persistent");
+    V(128, 0, 0, false, true, "persistent b128");
+    V(256, 0, 0, true, true, "pipe persistent");
+    V(128, 0, 0, true, true, "pipe persistent b128");
+    V(64, 0, 0, false, true, "persistent b64");
+    V(256, 0, 4, true, true, "pipe pers minb4");
+    V(128, 0, 8, false, true, "pers b128 minb8");
+    V(128, 0, 10, false, true, "pers b128 minb10");
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
