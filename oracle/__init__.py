@@ -59,6 +59,7 @@ def _bind(path: str) -> C.CDLL:
         "od_sincos2pi": (None, [u32, C.POINTER(f32), C.POINTER(f32)]),
         "od_ln_array": (None, [_f32p, _f32p, u64]),
         "od_rsqrt_array": (None, [_f32p, _f32p, u64]),
+        "od_sqrt_array": (None, [_f32p, _f32p, u64]),
         "od_sincos2pi_array": (None, [_u32p, _f32p, _f32p, u64]),
         "od_normal_quad": (None, [u64, u64, u64, u64, _f32p]),
         "od_normal_sextet": (None, [u64, u32, u32, u32, _f32p]),
@@ -145,6 +146,13 @@ def rsqrt_array(x) -> np.ndarray:
     x = _f32(x)
     y = np.empty_like(x)
     lib().od_rsqrt_array(x, y, x.size)
+    return y
+
+
+def sqrt_array(x) -> np.ndarray:
+    x = _f32(x)
+    y = np.empty_like(x)
+    lib().od_sqrt_array(x, y, x.size)
     return y
 
 

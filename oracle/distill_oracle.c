@@ -117,6 +117,20 @@ float od_rsqrt(float x) {
     return y;
 }
 
+/* spec/RNG.md §4: sqrt_spec — Goldschmidt from the rsqrt seed (Box-Muller radius) */
+float od_sqrt(float x) {
+    float y = u2f(0x5F375A86u - (f2u(x) >> 1));
+    float g = FMUL(x, y);
+    float h = FMUL(0.5f, y);
+    for (int k = 0; k < 2; ++k) {
+        float r = FFMA(-g, h, 0.5f);
+        g = FFMA(g, r, g);
+        h = FFMA(h, r, h);
+    }
+    float r = FFMA(-g, h, 0.5f);
+    return FFMA(g, r, g);
+}
+
 /* ------------------------------------------------------------------------ */
 /* spec/RNG.md §5: sincos_spec — (cos, sin)(2 pi A / 2^32 - pi/2)            */
 /* ------------------------------------------------------------------------ */
@@ -138,6 +152,7 @@ void od_sincos2pi(uint32_t a, float* cs, float* sn) {
 }
 
 /* array forms of the three primitives, for the exhaustive accuracy pins */
+void od_sqrt_array(const float* x, float* y, uint64_t n) { for (uint64_t j = 0; j < n; ++j) y[j] = od_sqrt(x[j]); }
 void od_ln_array(const float* x, float* y, uint64_t n) { for (uint64_t j = 0; j < n; ++j) y[j] = od_ln(x[j]); }
 void od_rsqrt_array(const float* x, float* y, uint64_t n) { for (uint64_t j = 0; j < n; ++j) y[j] = od_rsqrt(x[j]); }
 void od_sincos2pi_array(const uint32_t* a, float* c, float* s, uint64_t n) {
@@ -148,7 +163,7 @@ void od_sincos2pi_array(const uint32_t* a, float* c, float* s, uint64_t n) {
 static void od_bm_pair(uint32_t R, uint32_t A, float* z0, float* z1) {
     float u1 = (float)((R >> 8) | 1u) * 0x1p-24f;   /* exact */
     float s = -2.0f * od_ln(u1);                     /* exact scaling, not counted */
-    float rad = FMUL(s, od_rsqrt(s));                /* sqrt_spec */
+    float rad = od_sqrt(s);                          /* sqrt_spec */
     float c, n;
     od_sincos2pi(A, &c, &n);
     *z0 = FMUL(rad, c);

@@ -35,6 +35,8 @@ extern "C" {
 void  od_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 float od_ln(float x);
 float od_rsqrt(float x);
+float od_sqrt(float x);
+void  od_sqrt_array(const float* x, float* y, uint64_t n);
 void  od_sincos2pi(uint32_t angle_word, float* c, float* s);
 void  od_ln_array(const float* x, float* y, uint64_t n);
 void  od_rsqrt_array(const float* x, float* y, uint64_t n);

@@ -45,7 +45,7 @@ distill_status fail(distill_status s, const char* fmt, ...) {
                         __LINE__);                                                              \
     } while (0)
 
-constexpr int PP_BLOCK = 256;
+constexpr int PP_BLOCK = 128;
 constexpr int ARGMAX_BLOCK = 256;
 constexpr int DDM_BLOCK = 256;
 constexpr int STROOP_BLOCK = 256;

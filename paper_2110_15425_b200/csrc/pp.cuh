@@ -119,8 +119,22 @@ __device__ __forceinline__ void bm_pair2(uint32_t Rx, uint32_t Ry, uint32_t Ax, 
     F2 y = L::fma(L::mul(f, f), P, f);
     y = L::fma(fe, bc(D_LN2_LO), y);
     y = L::fma(fe, bc(D_LN2_HI), y);                          // y = ln_spec(u1) < 0
-    const F2 s = Ops<SRS>::mul(y, bc(-2.0f));                 // s = -2 ln u1 (exact scaling)
-    const F2 rad = Ops<SRS>::mul(s, rsqrt2_from<SRS>(s, y));  // -h = -0.5 s = y exactly
+    // rad = sqrt_spec(s), s = -2y (spec/RNG.md §4, Goldschmidt).  s is never formed:
+    // its bits are bits(y) + 0x80800000 (sign off, exponent + 1), and the first
+    // product g = s * y0 equals y * (-2 y0) exactly, with -2 y0 and h = 0.5 y0
+    // obtained by adjusting the seed's exponent bits.
+    using G = Ops<SRS>;
+    const uint32_t shx = (__float_as_uint(y.x) + 0x80800000u) >> 1, shy = (__float_as_uint(y.y) + 0x80800000u) >> 1;
+    const F2 y0m2 = make_float2(__uint_as_float(0xDFB75A86u - shx), __uint_as_float(0xDFB75A86u - shy));  // -2 y0
+    F2 h = make_float2(__uint_as_float(0x5EB75A86u - shx), __uint_as_float(0x5EB75A86u - shy));           // y0 / 2
+    F2 g = G::mul(y, y0m2);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const F2 rr = G::fma(neg2(g), h, bc(0.5f));
+        g = G::fma(g, rr, g);
+        h = G::fma(h, rr, h);
+    }
+    const F2 rad = G::fma(g, G::fma(neg2(g), h, bc(0.5f)), g);
     // sincos_spec: r from the angle bits, half-turn sign applied to rad
     const F2 r = Q::add(make_float2(__uint_as_float(((Ax >> 8) & 0x7FFFFFu) | 0x3F800000u),
                                     __uint_as_float(((Ay >> 8) & 0x7FFFFFu) | 0x3F800000u)),

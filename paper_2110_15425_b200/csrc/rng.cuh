@@ -101,6 +101,21 @@ __device__ __forceinline__ float rsqrt_spec(float x) {
     return y;
 }
 
+// sqrt_spec(x) (spec/RNG.md §4): Goldschmidt from the rsqrt seed, 3 steps, last h skipped.
+__device__ __forceinline__ float sqrt_spec(float x) {
+    const float y = __uint_as_float(0x5F375A86u - (__float_as_uint(x) >> 1));
+    float g = __fmul_rn(x, y);
+    float h = __fmul_rn(0.5f, y);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float r = __fmaf_rn(-g, h, 0.5f);
+        g = __fmaf_rn(g, r, g);
+        h = __fmaf_rn(h, r, h);
+    }
+    const float r = __fmaf_rn(-g, h, 0.5f);
+    return __fmaf_rn(g, r, g);
+}
+
 // r of sincos_spec: (A mod 2^31)/2^31 - 1/2, built from the bits (exact, spec/RNG.md §5)
 __device__ __forceinline__ float half_turn_r(uint32_t a) {
     return __fadd_rn(__uint_as_float(((a >> 8) & 0x7FFFFFu) | 0x3F800000u), -1.5f);
@@ -123,7 +138,7 @@ __device__ __forceinline__ void sincos_spec(uint32_t a, float& c, float& s) {
 __device__ __forceinline__ void bm_pair(uint32_t R, uint32_t A, float& z0, float& z1) {
     const float u1 = __fmul_rn(__uint2float_rn((R >> 8) | 1u), 0x1p-24f);  // exact
     const float s = __fmul_rn(-2.0f, ln_spec(u1));                          // exact scaling
-    const float rad = __fmul_rn(s, rsqrt_spec(s));
+    const float rad = sqrt_spec(s);
     float c, n;
     sincos_spec(A, c, n);
     z0 = __fmul_rn(rad, c);

@@ -62,6 +62,19 @@ def test_rsqrt_dense(orc):
     assert worst <= 4 * 2.0 ** -24, worst
 
 
+def test_sqrt_goldschmidt_on_radius_domain(orc):
+    """sqrt_spec over every binary32 in [6e-8, 34] (the Box-Muller s = -2 ln u1 range)."""
+    lo = np.float32(5.9e-8).view(np.uint32)
+    hi = np.float32(34.0).view(np.uint32)
+    worst = 0.0
+    for b0 in range(int(lo), int(hi), 1 << 23):
+        x = np.arange(b0, min(int(hi), b0 + (1 << 23)), dtype=np.uint32).view(np.float32)
+        y = orc.sqrt_array(x).astype(np.float64)
+        ref = np.sqrt(x.astype(np.float64))
+        worst = max(worst, float((np.abs(y - ref) / ref).max()))
+    assert worst <= 4 * 2.0 ** -24, worst
+
+
 def test_sincos2pi_exhaustive_24bit(orc):
     """All 2^24 angle words with the low byte clear."""
     a = (np.arange(2 ** 24, dtype=np.uint64) << 8).astype(np.uint32)
