@@ -37,11 +37,13 @@ __global__ void __launch_bounds__(BLOCK) ddm_batch_kernel(const DDMArgs a) {
     for (uint64_t t = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; t < a.n_trials;
          t += (uint64_t)gridDim.x * BLOCK) {
         const uint64_t unit = a.trial_begin + t;
+        PhiloxHoisted rng;
+        rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
         float x = a.x0;
         uint32_t st = 0, ch = 2;
         const uint32_t nblk = (a.n_steps + 3) >> 2;
         for (uint32_t kb = 0; kb < nblk; ++kb) {
-            const float4 g = normal_quad(unit, kb, a.key0, a.key1);
+            const float4 g = normal_quad_h(rng, kb);
             const float gg[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
             for (int l = 0; l < 4; ++l) {

@@ -173,7 +173,10 @@ static distill_status launch_pp(const distill_model* m, const distill_eval_args*
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
     p.levels = m->d_levels; p.net = a->d_net; p.best = a->d_best;
     const unsigned grid = (unsigned)((count + PP_BLOCK - 1) / PP_BLOCK);
-    pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
+    if ((a->n_samples & 1u) == 0)
+        pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+    else
+        pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;

@@ -154,4 +154,150 @@ __device__ __forceinline__ float4 normal_quad(uint64_t unit, uint32_t k, uint32_
     return z;
 }
 
+
+// ------------------------------------------------------------ two-lane binary32 helpers
+// Ops<false>: one packed FFMA2/FMUL2/FADD2 per step (both lanes in one
+// instruction, full 32-lane FMA datapath for 2 cycles).  Ops<true>: the same
+// step as two scalar FFMA/FMUL/FADD, which the scheduler can place on the
+// fmalite sub-pipe while fmaheavy runs the Philox IMAD.WIDEs.  Both round
+// every lane exactly like the scalar op, so the choice is pure scheduling.
+typedef float2 F2;
+__device__ __forceinline__ F2 bc(float a) { return make_float2(a, a); }
+__device__ __forceinline__ F2 neg2(F2 a) { return make_float2(-a.x, -a.y); }
+
+template <bool SC> struct Ops {
+    static __device__ __forceinline__ F2 fma(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
+    static __device__ __forceinline__ F2 mul(F2 a, F2 b) { return __fmul2_rn(a, b); }
+    static __device__ __forceinline__ F2 add(F2 a, F2 b) { return __fadd2_rn(a, b); }
+};
+template <> struct Ops<true> {
+    static __device__ __forceinline__ F2 fma(F2 a, F2 b, F2 c) {
+        return make_float2(__fmaf_rn(a.x, b.x, c.x), __fmaf_rn(a.y, b.y, c.y));
+    }
+    static __device__ __forceinline__ F2 mul(F2 a, F2 b) { return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)); }
+    static __device__ __forceinline__ F2 add(F2 a, F2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
+};
+
+// rsqrt_spec on both lanes (spec/RNG.md §4), residual Newton form
+//   p = h y ; r = fma(-p, y, 0.5) ; y = fma(y, r, y)
+// `mh` = -h = -0.5 x (callers that already hold -h pass it and save the
+// multiply): -p = mh * y exactly, so r = fma(mh * y, y, 0.5).
+template <bool SC>
+__device__ __forceinline__ F2 rsqrt2_from(F2 x, F2 mh) {
+    using O = Ops<SC>;
+    F2 y = make_float2(__uint_as_float(0x5F375A86u - (__float_as_uint(x.x) >> 1)),
+                       __uint_as_float(0x5F375A86u - (__float_as_uint(x.y) >> 1)));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const F2 q = O::mul(mh, y);              // -p
+        const F2 r = O::fma(q, y, bc(0.5f));
+        y = O::fma(y, r, y);
+    }
+    return y;
+}
+
+// Two Box-Muller pairs at once (lane x: (Rx, Ax), lane y: (Ry, Ay)); angle words
+// have their low 8 bits clear.  zc = rad * cos phi, zs = rad * sin phi per lane
+// (spec/RNG.md §2-§6).  SLN/SRS/SSC choose scalar lanes for the ln, sqrt and
+// sincos parts (scheduling only; identical results).
+template <bool SLN, bool SRS, bool SSC>
+__device__ __forceinline__ void bm_pair2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay, F2& zc, F2& zs) {
+    using L = Ops<SLN>;
+    using Q = Ops<SSC>;
+    // u1 = ((R >> 8) | 1) * 2^-24: convert the odd integer exactly and fold the
+    // 2^-24 into the exponent constants of ln_spec (bits(u1) = bits(float(m)) - 24<<23)
+    const uint32_t ix = __float_as_uint(__uint2float_rn((Rx >> 8) | 1u));
+    const uint32_t iy = __float_as_uint(__uint2float_rn((Ry >> 8) | 1u));
+    const uint32_t tx = ix - 0x4B3504F3u, ty = iy - 0x4B3504F3u;        // = bits(u1) - 0x3F3504F3
+    const F2 m = make_float2(__uint_as_float((tx & 0x7FFFFFu) + 0x3F3504F3u),
+                             __uint_as_float((ty & 0x7FFFFFu) + 0x3F3504F3u));
+    const F2 fe = make_float2(__int2float_rn((int32_t)tx >> 23), __int2float_rn((int32_t)ty >> 23));
+    const F2 f = L::add(m, bc(-1.0f));
+    F2 P = L::fma(bc(D_L7), f, bc(D_L6));
+    P = L::fma(P, f, bc(D_L5));
+    P = L::fma(P, f, bc(D_L4));
+    P = L::fma(P, f, bc(D_L3));
+    P = L::fma(P, f, bc(D_L2));
+    P = L::fma(P, f, bc(D_L1));
+    P = L::fma(P, f, bc(D_L0));
+    F2 y = L::fma(L::mul(f, f), P, f);
+    y = L::fma(fe, bc(D_LN2_LO), y);
+    y = L::fma(fe, bc(D_LN2_HI), y);                          // y = ln_spec(u1) < 0
+    // rad = sqrt_spec(s), s = -2y (spec/RNG.md §4, Goldschmidt).  s is never formed:
+    // its bits are bits(y) + 0x80800000 (sign off, exponent + 1), and the first
+    // product g = s * y0 equals y * (-2 y0) exactly, with -2 y0 and h = 0.5 y0
+    // obtained by adjusting the seed's exponent bits.
+    using G = Ops<SRS>;
+    const uint32_t shx = (__float_as_uint(y.x) + 0x80800000u) >> 1, shy = (__float_as_uint(y.y) + 0x80800000u) >> 1;
+    const F2 y0m2 = make_float2(__uint_as_float(0xDFB75A86u - shx), __uint_as_float(0xDFB75A86u - shy));  // -2 y0
+    F2 h = make_float2(__uint_as_float(0x5EB75A86u - shx), __uint_as_float(0x5EB75A86u - shy));           // y0 / 2
+    F2 g = G::mul(y, y0m2);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const F2 rr = G::fma(neg2(g), h, bc(0.5f));
+        g = G::fma(g, rr, g);
+        h = G::fma(h, rr, h);
+    }
+    const F2 rad = G::fma(g, G::fma(neg2(g), h, bc(0.5f)), g);
+    // sincos_spec: r from the angle bits, half-turn sign applied to rad
+    const F2 r = Q::add(make_float2(__uint_as_float(((Ax >> 8) & 0x7FFFFFu) | 0x3F800000u),
+                                    __uint_as_float(((Ay >> 8) & 0x7FFFFFu) | 0x3F800000u)),
+                        bc(-1.5f));
+    const F2 t = Q::mul(r, r);
+    const F2 S = Q::fma(Q::fma(Q::fma(Q::fma(bc(D_S4), t, bc(D_S3)), t, bc(D_S2)), t, bc(D_S1)), t, bc(D_S0));
+    const F2 C = Q::fma(Q::fma(Q::fma(Q::fma(bc(D_C4), t, bc(D_C3)), t, bc(D_C2)), t, bc(D_C1)), t, bc(D_C0));
+    const F2 cq = Q::fma(C, t, bc(1.0f));
+    const F2 sq = Q::mul(S, r);
+    const F2 rs = make_float2(__uint_as_float(__float_as_uint(rad.x) ^ (Ax & 0x80000000u)),
+                              __uint_as_float(__float_as_uint(rad.y) ^ (Ay & 0x80000000u)));
+    zc = Q::mul(rs, cq);   // (-rad) * c == -(rad * c) bit for bit
+    zs = Q::mul(rs, sq);
+}
+
+// Philox4x32-10 on counter (c0, s, c2, c3) for a loop over the block index s
+// (c0, c2, c3 fixed per thread): rounds 1-3 with their s-invariant parts
+// hoisted into init() (once per thread), rounds 4-10 generic.  15 instead of
+// 20 IMAD.WIDE per block; the s-dependent round-2 product is warp-uniform.
+//   PP   (spec/RNG.md §1, stream 1): c0 = allocation i, s = sample, c2 = invocation, c3 = 1
+//   DDM / Stroop (stream 2):         c0 = unit lo, s = block k, c2 = unit hi, c3 = 2
+struct PhiloxHoisted {
+    uint32_t a1, x3k, b_c1k, c3k, z3, k0, k1;
+    __device__ __forceinline__ void init(uint32_t c0, uint32_t c2, uint32_t c3, uint32_t key0, uint32_t key1) {
+        k0 = key0; k1 = key1;
+        uint32_t hi0, lo0, hi1, lo1;
+        mulhilo(PHILOX_M0, c0, hi0, lo0);                // round 1: p0 = M0 * c0
+        mulhilo(PHILOX_M1, c2, hi1, lo1);                //          p1 = M1 * c2
+        a1 = hi1 ^ k0;                                   // x0 = a1 ^ s
+        const uint32_t x1 = lo1, x2 = hi0 ^ c3 ^ k1, x3 = lo0;
+        uint32_t H1, L1;
+        mulhilo(PHILOX_M1, x2, H1, L1);                  // round 2: p1 = M1 * x2 (invariant)
+        const uint32_t y0 = H1 ^ x1 ^ (k0 + PHILOX_W0);
+        const uint32_t y1 = L1;
+        x3k = x3 ^ (k1 + PHILOX_W1);                     // y2 = hi(M0 * x0) ^ x3k
+        uint32_t G0h, G0l;
+        mulhilo(PHILOX_M0, y0, G0h, G0l);                // round 3: p0 = M0 * y0 (invariant)
+        b_c1k = y1 ^ (k0 + 2u * PHILOX_W0);              // z0 = hi(M1 * y2) ^ b_c1k
+        c3k = G0h ^ (k1 + 2u * PHILOX_W1);               // z2 = c3k ^ y3
+        z3 = G0l;
+    }
+    __device__ __forceinline__ uint4 operator()(uint32_t s) const {
+        uint32_t P0h, P0l;
+        mulhilo(PHILOX_M0, a1 ^ s, P0h, P0l);            // round 2: p0 = M0 * x0
+        const uint32_t y2 = P0h ^ x3k, y3 = P0l;
+        uint32_t Qh, Ql;
+        mulhilo(PHILOX_M1, y2, Qh, Ql);                  // round 3: p1 = M1 * y2
+        const uint4 c = make_uint4(Qh ^ b_c1k, Ql, c3k ^ y3, z3);
+        return philox_from<3>(c, k0, k1);                // rounds 4..10
+    }
+};
+
+// Quad normals 4k..4k+3 of a hoisted stream-2 unit: both Box-Muller pairs of the
+// block in the two lanes of one packed evaluation (spec/RNG.md §6, quad packing).
+__device__ __forceinline__ float4 normal_quad_h(const PhiloxHoisted& rng, uint32_t k) {
+    const uint4 X = rng(k);
+    F2 zc, zs;
+    bm_pair2<false, false, false>(X.x, X.z, X.y & 0xFFFFFF00u, X.w & 0xFFFFFF00u, zc, zs);
+    return make_float4(zc.x, zs.x, zc.y, zs.y);
+}
+
 }  // namespace distill

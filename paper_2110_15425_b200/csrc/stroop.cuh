@@ -47,12 +47,14 @@ __global__ void __launch_bounds__(BLOCK) stroop_sim_kernel(const StroopArgs a, u
         const float I0 = __fadd_rn(colour == 0 ? ic : 0.0f, word == 0 ? iw : 0.0f);
         const float I1 = __fadd_rn(colour == 1 ? ic : 0.0f, word == 1 ? iw : 0.0f);
         const uint64_t unit = (uint64_t)i * a.n_trials + j;
+        PhiloxHoisted rng;
+        rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
         float h0 = 0.f, h1 = 0.f, x0 = 0.f, x1 = 0.f;
         int resp = -1;
         uint32_t st = 0;
         const uint32_t nblk = (a.n_steps + 1) >> 1;   // 2 steps per quad block
         for (uint32_t kb = 0; kb < nblk; ++kb) {
-            const float4 g = normal_quad(unit, kb, a.key0, a.key1);
+            const float4 g = normal_quad_h(rng, kb);
 #pragma unroll
             for (int l = 0; l < 2; ++l) {
                 const uint32_t n = 2 * kb + l + 1;

@@ -9,7 +9,7 @@ using namespace distill;
 
 static unsigned int* g_counter = nullptr;
 
-template <int BLOCK, int MASK, int MINB, bool PIPE = false, bool PERS = false>
+template <int BLOCK, int MASK, int MINB, bool PIPE = false, bool PERS = false, bool EVEN = false>
 void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_ref) {
     cudaFuncAttributes fa;
     unsigned grid;
@@ -21,7 +21,7 @@ void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_re
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
         grid = per_sm * n_sm;
     } else {
-        cudaFuncGetAttributes(&fa, pp_eval_grid_kernel<BLOCK, MASK, MINB, PIPE>);
+        cudaFuncGetAttributes(&fa, pp_eval_grid_kernel<BLOCK, MASK, MINB, PIPE, EVEN>);
         grid = (a.count + BLOCK - 1) / BLOCK;
     }
     cudaEvent_t e0, e1;
@@ -34,7 +34,7 @@ void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_re
             cudaMemsetAsync(g_counter, 0, 4);
             pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE><<<grid, BLOCK>>>(a, g_counter);
         } else {
-            pp_eval_grid_kernel<BLOCK, MASK, MINB, PIPE><<<grid, BLOCK>>>(a);
+            pp_eval_grid_kernel<BLOCK, MASK, MINB, PIPE, EVEN><<<grid, BLOCK>>>(a);
         }
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
@@ -48,7 +48,7 @@ void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_re
     if (is_ref) memcpy(ref_net, h.data(), a.count * 4);
     else same = memcmp(ref_net, h.data(), a.count * 4) == 0 && k == ref_key;
     const double flops = (double)a.count * (a.n_samples * 278.0 + 13) + 75;
-    printf("%-26s b%4d m%2d minb%d pipe%d pers%d grid %6u regs %3d %8.4f ms %6.2f TF/s frac %.3f %s\n", name, BLOCK,
+    printf("%-26s even%d b%4d m%2d minb%d pipe%d pers%d grid %6u regs %3d %8.4f ms %6.2f TF/s frac %.3f %s\n", name, (int)EVEN, BLOCK,
            MASK, MINB, (int)PIPE, (int)PERS, grid, fa.numRegs, best, flops / best / 1e9, flops / best / 1e9 / 74.45,
            same ? "bit-identical" : "MISMATCH");
 }
@@ -68,18 +68,13 @@ int main() {
     cudaMalloc((void**)&g_counter, 4);
     run<256, 0, 0>("packed (ref)", a, ref.data(), 0, true);
     key64_t rk; cudaMemcpy(&rk, a.best, 8, cudaMemcpyDeviceToHost);
-#define V(B, M, N, P, Q, name) run<B, M, N, P, Q>(name, a, ref.data(), rk, false)
-    V(128, 0, 0, false, false, "b128");
-    V(256, 0, 0, true, false, "pipe");
-    V(128, 0, 0, true, false, "pipe b128");
-    V(256, 0, 0, false, true, "persistent");
-    V(128, 0, 0, false, true, "persistent b128");
-    V(256, 0, 0, true, true, "pipe persistent");
-    V(128, 0, 0, true, true, "pipe persistent b128");
-    V(64, 0, 0, false, true, "persistent b64");
-    V(256, 0, 4, true, true, "pipe pers minb4");
-    V(128, 0, 8, false, true, "pers b128 minb8");
-    V(128, 0, 10, false, true, "pers b128 minb10");
+#define V(B, M, N, P, Q, E, name) run<B, M, N, P, Q, E>(name, a, ref.data(), rk, false)
+    V(128, 0, 0, false, false, false, "b128");
+    V(128, 0, 0, false, false, true, "b128 even");
+    V(256, 0, 0, false, false, true, "b256 even");
+    V(128, 0, 0, false, true, false, "persistent b128");
+    V(64, 0, 0, false, false, true, "b64 even");
+    V(128, 1, 0, false, false, true, "b128 even obj scalar");
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
