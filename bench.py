@@ -38,9 +38,9 @@ import workloads as W  # noqa: E402
 
 METRIC = "model evaluations/sec (allocations×samples) at 1/2/4/8 B200; % FP32 peak"
 UNIT = "evals/s"
-FLOPS_PER_SAMPLE = 278        # DESIGN.md §6, pinned by tests/test_oracle_pp.py (counting oracle)
+FLOPS_PER_SAMPLE = 274        # DESIGN.md §6, pinned by tests/test_oracle_pp.py (counting oracle)
 FLOPS_PER_ALLOC = 13
-FLOPS_PER_CALL = 75
+FLOPS_PER_CALL = 74
 FP32_LANES_PER_SM = 128       # FFMA lanes per SM (4 SMSP x 32), 2 flops per FMA
 
 

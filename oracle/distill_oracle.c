@@ -159,13 +159,17 @@ void od_sincos2pi_array(const uint32_t* a, float* c, float* s, uint64_t n) {
     for (uint64_t j = 0; j < n; ++j) od_sincos2pi(a[j], &c[j], &s[j]);
 }
 
-/* spec/RNG.md §2 + §6: one Box-Muller pair */
-static void od_bm_pair(uint32_t R, uint32_t A, float* z0, float* z1) {
+/* spec/RNG.md §2 + §6: one Box-Muller pair in polar form (radius, cos, sin) */
+static void od_bm_polar(uint32_t R, uint32_t A, float* rad, float* c, float* n) {
     float u1 = (float)((R >> 8) | 1u) * 0x1p-24f;   /* exact */
     float s = -2.0f * od_ln(u1);                     /* exact scaling, not counted */
-    float rad = od_sqrt(s);                          /* sqrt_spec */
-    float c, n;
-    od_sincos2pi(A, &c, &n);
+    *rad = od_sqrt(s);                               /* sqrt_spec */
+    od_sincos2pi(A, c, n);
+}
+/* ... and as the two normals z = rad * (cos, sin) */
+static void od_bm_pair(uint32_t R, uint32_t A, float* z0, float* z1) {
+    float rad, c, n;
+    od_bm_polar(R, A, &rad, &c, &n);
     *z0 = FMUL(rad, c);
     *z1 = FMUL(rad, n);
 }
@@ -215,12 +219,34 @@ static v2 od_unit(v2 v) {
     return r;
 }
 static v2 od_sub(v2 a, v2 b) { v2 r = { FSUB(a.x, b.x), FSUB(a.y, b.y) }; return r; }
-/* Action node: unit toward prey minus kappa * unit toward predator */
+/* Action node: move toward the prey and away from the predator,
+ * d = |v_p| (unit(v_p) - kappa unit(v_d)) = v_p + c v_d with c = -kappa |v_p| / |v_d|;
+ * only its direction matters (it is normalised by the Objective), spec/MODELS.md §2. */
 static v2 od_action(v2 prey, v2 pred, v2 player, float kappa) {
-    v2 up = od_unit(od_sub(prey, player));
-    v2 ud = od_unit(od_sub(pred, player));
-    v2 d = { FFMA(-kappa, ud.x, up.x), FFMA(-kappa, ud.y, up.y) };
+    v2 vp = od_sub(prey, player), vd = od_sub(pred, player);
+    float np = FFMA(vp.y, vp.y, FFMA(vp.x, vp.x, 0x1p-126f));
+    float nd = FFMA(vd.y, vd.y, FFMA(vd.x, vd.x, 0x1p-126f));
+    float yp = od_rsqrt(np), yd = od_rsqrt(nd);
+    float c = FMUL(FMUL(-kappa, yd), FMUL(np, yp));       /* -kappa |v_p| / |v_d| */
+    v2 d = { FFMA(c, vd.x, vp.x), FFMA(c, vd.y, vp.y) };
     return d;
+}
+
+/* Obs nodes: o_e = p_e + (sigma_e rad_e) (cos, sin) for the sextet pair of entity e */
+static void od_observe(uint64_t seed, uint32_t alloc, uint32_t sample, uint32_t invocation,
+                       const float sig[3], const v2 p[3], v2 o[3]) {
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    uint32_t ctr[4] = { alloc, sample, invocation, 1u };
+    uint32_t X[4];
+    od_philox4x32_10(ctr, key, X);
+    uint32_t A[3] = { X[3] << 16, X[3] & 0xFFFF0000u, (X[0] << 24) | ((X[1] & 0xFFu) << 16) };
+    for (int e = 0; e < 3; ++e) {
+        float rad, c, n;
+        od_bm_polar(X[e], A[e], &rad, &c, &n);
+        float sr = FMUL(sig[e], rad);
+        o[e].x = FFMA(sr, c, p[e].x);
+        o[e].y = FFMA(sr, n, p[e].y);
+    }
 }
 
 /* Objective node: squared chord between the normalised action d/|d|
@@ -258,13 +284,8 @@ int od_pp_eval(const uint32_t n_levels[3], const float* levels, const float w[3]
         float K = FFMA(w[2], a[2], FFMA(w[1], a[1], FMUL(w[0], a[0])));
         float acc = 0.0f;
         for (uint32_t s = 0; s < n_samples; ++s) {
-            float z[6];
-            od_normal_sextet(seed, (uint32_t)i, s, invocation, z);
             v2 o[3];
-            for (int e = 0; e < 3; ++e) {
-                o[e].x = FFMA(sig[e], z[2 * e], p[e].x);
-                o[e].y = FFMA(sig[e], z[2 * e + 1], p[e].y);
-            }
+            od_observe(seed, (uint32_t)i, s, invocation, sig, p, o);
             float e2 = od_objective(od_action(o[0], o[1], o[2], kappa), ustar);
             acc = FADD(acc, e2);
         }
@@ -288,13 +309,8 @@ int od_pp_trace(const uint32_t n_levels[3], const float* levels, const float par
     float sig[3];
     for (int e = 0; e < 3; ++e) sig[e] = FFMA(a[e], dsig, smax);
     for (uint32_t s = 0; s < n_samples; ++s) {
-        float z[6];
-        od_normal_sextet(seed, (uint32_t)i, s, invocation, z);
         v2 o[3];
-        for (int e = 0; e < 3; ++e) {
-            o[e].x = FFMA(sig[e], z[2 * e], p[e].x);
-            o[e].y = FFMA(sig[e], z[2 * e + 1], p[e].y);
-        }
+        od_observe(seed, (uint32_t)i, s, invocation, sig, p, o);
         out[s] = od_objective(od_action(o[0], o[1], o[2], kappa), ustar);
     }
     return 0;

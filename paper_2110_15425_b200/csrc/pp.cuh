@@ -52,6 +52,20 @@ __device__ __forceinline__ V2 vunit(V2 v) {
     return {O::mul(v.x, y), O::mul(v.y, y)};
 }
 
+// Action node (spec/MODELS.md §2): d = v_p + c v_d with c = -kappa |v_p| / |v_d|,
+// i.e. |v_p| (unit(v_p) - kappa unit(v_d)); only its direction is used downstream.
+template <bool SC>
+__device__ __forceinline__ V2 action2(V2 q0, V2 q1, V2 q2, F2 mk) {
+    using O = Ops<SC>;
+    const V2 vp = vsub<SC>(q0, q2), vd = vsub<SC>(q1, q2);
+    const F2 np = O::fma(vp.y, vp.y, O::fma(vp.x, vp.x, bc(0x1p-126f)));
+    const F2 nd = O::fma(vd.y, vd.y, O::fma(vd.x, vd.x, bc(0x1p-126f)));
+    const F2 yp = rsqrt2_from<SC>(np, O::mul(np, bc(-0.5f)));
+    const F2 yd = rsqrt2_from<SC>(nd, O::mul(nd, bc(-0.5f)));
+    const F2 c = O::mul(O::mul(mk, yd), O::mul(np, yp));
+    return {O::fma(c, vd.x, vp.x), O::fma(c, vd.y, vp.y)};
+}
+
 // Objective node: e = |d * y_d - u*|^2 with y_d = rsqrt_spec(|d|^2 + 2^-126) and the
 // difference fused per component (spec/MODELS.md §2).  Writing the fma here leaves no
 // FMUL2 -> FADD2 pair for ptxas to contract behind our back (it does, .rn or not).
@@ -87,8 +101,7 @@ __device__ __forceinline__ float2 pp_ustar(const PPArgs& a) {
     const V2 P0 = {bc(a.prey_x), bc(a.prey_y)}, P1 = {bc(a.pred_x), bc(a.pred_y)};
     const V2 P2 = {bc(a.pl_x), bc(a.pl_y)};
     const F2 mk = bc(-a.kappa);
-    const V2 up = vunit<false>(vsub<false>(P0, P2)), ud = vunit<false>(vsub<false>(P1, P2));
-    const V2 us = vunit<false>({__ffma2_rn(mk, ud.x, up.x), __ffma2_rn(mk, ud.y, up.y)});
+    const V2 us = vunit<false>(action2<false>(P0, P1, P2, mk));
     return make_float2(us.x.x, us.y.x);
 }
 
@@ -102,7 +115,7 @@ __device__ __forceinline__ float2 pp_ustar_block(const PPArgs& a) {
 
 template <int MASK, bool PIPE, bool EVEN = false>
 __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, float2 ustar) {
-    constexpr bool SOBJ = MASK & PP_SC_OBJECTIVE, SUPD = MASK & PP_SC_UNIT_PRED, SUPY = MASK & PP_SC_UNIT_PREY;
+    constexpr bool SOBJ = MASK & PP_SC_OBJECTIVE;
     constexpr bool SLN2 = MASK & PP_SC_LN2, SRS2 = MASK & PP_SC_RSQ2, SSC2 = MASK & PP_SC_SC2;
     // a1: mixed-radix decode, signal 0 most significant
     const uint32_t k2 = i % a.L2, r = i / a.L2;
@@ -136,18 +149,18 @@ __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, floa
             X = rng(s); Y = rng(s + 1);
         }
         // a3: sextet packing -> three 2-D Box-Muller pairs (spec/RNG.md §6)
-        V2 z0, z1, z2;
-        bm_pair2<false, false, false>(X.x, Y.x, X.w << 16, Y.w << 16, z0.x, z0.y);
-        bm_pair2<false, false, false>(X.y, Y.y, X.w & 0xFFFF0000u, Y.w & 0xFFFF0000u, z1.x, z1.y);
-        bm_pair2<SLN2, SRS2, SSC2>(X.z, Y.z, (X.x << 24) | ((X.y & 0xFFu) << 16),
-                                   (Y.x << 24) | ((Y.y & 0xFFu) << 16), z2.x, z2.y);
-        // a4: Obs -> Action -> Objective
+        F2 r0, c0, n0, r1, c1, n1, r2, c2, n2;
+        bm_polar2<false, false, false>(X.x, Y.x, X.w << 16, Y.w << 16, r0, c0, n0);
+        bm_polar2<false, false, false>(X.y, Y.y, X.w & 0xFFFF0000u, Y.w & 0xFFFF0000u, r1, c1, n1);
+        bm_polar2<SLN2, SRS2, SSC2>(X.z, Y.z, (X.x << 24) | ((X.y & 0xFFu) << 16),
+                                    (Y.x << 24) | ((Y.y & 0xFFu) << 16), r2, c2, n2);
+        // a4: Obs (p + sigma rad (cos, sin)) -> Action -> Objective
         using O = Ops<false>;
-        const V2 o0 = {O::fma(bc(s0), z0.x, P0.x), O::fma(bc(s0), z0.y, P0.y)};
-        const V2 o1 = {O::fma(bc(s1), z1.x, P1.x), O::fma(bc(s1), z1.y, P1.y)};
-        const V2 o2 = {O::fma(bc(s2), z2.x, P2.x), O::fma(bc(s2), z2.y, P2.y)};
-        const V2 vp = vunit<SUPY>(vsub<SUPY>(o0, o2)), vd = vunit<SUPD>(vsub<SUPD>(o1, o2));
-        const V2 d = {Ops<SOBJ>::fma(mk, vd.x, vp.x), Ops<SOBJ>::fma(mk, vd.y, vp.y)};
+        const F2 q0 = O::mul(bc(s0), r0), q1 = O::mul(bc(s1), r1), q2 = O::mul(bc(s2), r2);
+        const V2 o0 = {O::fma(q0, c0, P0.x), O::fma(q0, n0, P0.y)};
+        const V2 o1 = {O::fma(q1, c1, P1.x), O::fma(q1, n1, P1.y)};
+        const V2 o2 = {O::fma(q2, c2, P2.x), O::fma(q2, n2, P2.y)};
+        const V2 d = action2<SOBJ>(o0, o1, o2, mk);
         const F2 e = objective2<SOBJ>(d, us);
         // a7: sequential sum in ascending sample order
         acc = __fadd_rn(acc, e.x);

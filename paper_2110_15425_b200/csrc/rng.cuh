@@ -201,7 +201,7 @@ __device__ __forceinline__ F2 rsqrt2_from(F2 x, F2 mh) {
 // (spec/RNG.md §2-§6).  SLN/SRS/SSC choose scalar lanes for the ln, sqrt and
 // sincos parts (scheduling only; identical results).
 template <bool SLN, bool SRS, bool SSC>
-__device__ __forceinline__ void bm_pair2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay, F2& zc, F2& zs) {
+__device__ __forceinline__ void bm_polar2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay, F2& rs, F2& cq, F2& sq) {
     using L = Ops<SLN>;
     using Q = Ops<SSC>;
     // u1 = ((R >> 8) | 1) * 2^-24: convert the odd integer exactly and fold the
@@ -246,12 +246,20 @@ __device__ __forceinline__ void bm_pair2(uint32_t Rx, uint32_t Ry, uint32_t Ax, 
     const F2 t = Q::mul(r, r);
     const F2 S = Q::fma(Q::fma(Q::fma(Q::fma(bc(D_S4), t, bc(D_S3)), t, bc(D_S2)), t, bc(D_S1)), t, bc(D_S0));
     const F2 C = Q::fma(Q::fma(Q::fma(Q::fma(bc(D_C4), t, bc(D_C3)), t, bc(D_C2)), t, bc(D_C1)), t, bc(D_C0));
-    const F2 cq = Q::fma(C, t, bc(1.0f));
-    const F2 sq = Q::mul(S, r);
-    const F2 rs = make_float2(__uint_as_float(__float_as_uint(rad.x) ^ (Ax & 0x80000000u)),
-                              __uint_as_float(__float_as_uint(rad.y) ^ (Ay & 0x80000000u)));
-    zc = Q::mul(rs, cq);   // (-rad) * c == -(rad * c) bit for bit
-    zs = Q::mul(rs, sq);
+    cq = Q::fma(C, t, bc(1.0f));
+    sq = Q::mul(S, r);
+    // half-turn sign on the radius: (-rad) * c == -(rad * c) bit for bit
+    rs = make_float2(__uint_as_float(__float_as_uint(rad.x) ^ (Ax & 0x80000000u)),
+                     __uint_as_float(__float_as_uint(rad.y) ^ (Ay & 0x80000000u)));
+}
+
+// ... and as normals zc = rad cos phi, zs = rad sin phi.
+template <bool SLN, bool SRS, bool SSC>
+__device__ __forceinline__ void bm_pair2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay, F2& zc, F2& zs) {
+    F2 rs, cq, sq;
+    bm_polar2<SLN, SRS, SSC>(Rx, Ry, Ax, Ay, rs, cq, sq);
+    zc = Ops<SSC>::mul(rs, cq);
+    zs = Ops<SSC>::mul(rs, sq);
 }
 
 // Philox4x32-10 on counter (c0, s, c2, c3) for a loop over the block index s

@@ -189,10 +189,10 @@ def test_golden_cfg1(orc):
 
 
 def test_flop_count_per_sample_matches_hand_count(orc):
-    """Counting build: 278 binary32 flops per PP sample (fma = 2), the figure
+    """Counting build: 274 binary32 flops per PP sample (fma = 2), the figure
     DESIGN.md §6 derives by hand from spec/RNG.md + spec/MODELS.md:
-    3 Box-Muller pairs x 62 (ln 22, Goldschmidt sqrt 18, sincos 20, 2 products)
-    + obs 12 + action 52 + objective 28."""
+    3 x (Box-Muller polar 60 (ln 22, Goldschmidt sqrt 18, sincos 20) + obs 5)
+    + action 51 + objective 28."""
     L = orc.lib(counting=True)
     assert L.od_is_counting_build() == 1
     cfg = W.pp_cfg3()
@@ -202,8 +202,8 @@ def test_flop_count_per_sample_matches_hand_count(orc):
         orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, 10, S, 1, counting=True)
         return L.od_flops_read()
 
-    assert (flops(101) - flops(100)) == 10 * 278
-    per_alloc = (flops(100) - 10 * 100 * 278)
-    # per call: u_star (2 units + action + unit) = 4 + 2*22 + 4 + 22 = 74, plus dsig 1;
+    assert (flops(101) - flops(100)) == 10 * 274
+    per_alloc = (flops(100) - 10 * 100 * 274)
+    # per call: u_star = action 51 + unit 22 = 73, plus dsig 1;
     # per allocation: 3 sigma fma (6) + K (5) + mean (2) = 13
-    assert per_alloc == 75 + 10 * 13
+    assert per_alloc == 74 + 10 * 13

@@ -47,7 +47,7 @@ void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_re
     bool same = true;
     if (is_ref) memcpy(ref_net, h.data(), a.count * 4);
     else same = memcmp(ref_net, h.data(), a.count * 4) == 0 && k == ref_key;
-    const double flops = (double)a.count * (a.n_samples * 278.0 + 13) + 75;
+    const double flops = (double)a.count * (a.n_samples * 274.0 + 13) + 74;
     printf("%-26s even%d b%4d m%2d minb%d pipe%d pers%d grid %6u regs %3d %8.4f ms %6.2f TF/s frac %.3f %s\n", name, (int)EVEN, BLOCK,
            MASK, MINB, (int)PIPE, (int)PERS, grid, fa.numRegs, best, flops / best / 1e9, flops / best / 1e9 / 74.45,
            same ? "bit-identical" : "MISMATCH");
