@@ -291,8 +291,15 @@ def run_ours(args):
     flops_launch = count * (cfg.n_samples * FLOPS_PER_SAMPLE + FLOPS_PER_ALLOC) + FLOPS_PER_CALL
     achieved = flops_launch / (ms_kern / 1e3) / 1e12
     sm_load = clocks.get("sm_mhz")
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_pp_traffic.json")
+    if os.path.exists(tpath):   # dram read + write per launch from the committed ncu --set full capture
+        t = json.load(open(tpath))
+        traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "pp_eval_grid_kernel", "kernel_ms": ms_kern,
+            "traffic": traffic, "traffic_source": "profiles/r01_pp_traffic.json (ncu --set full, cfg3)",
+            "algorithmic_bytes_per_launch": count * 4 + 8 + sum(cfg.n_levels) * 4,
+            "kernel": "pp_eval_grid_kernel", "kernel_ms": ms_kern,
             "algorithmic_flops_per_launch": flops_launch,
             "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz (max clock)",
             "frac_at_measured_clock": (achieved / (n_sm * FP32_LANES_PER_SM * 2 * sm_load * 1e6 / 1e12)
