@@ -362,6 +362,26 @@ def run_extras(D, torch, dev, rank, world, args):
     out["ddm_cfg2"] = {"trials_per_s": d.n_trials / (ms / 1e3), "steps_per_s": d.n_trials * d.n_steps / (ms / 1e3),
                        "ms": ms, "error_rate": lo / max(1, up + lo),
                        "mean_rt_s": (int(rs[0]) + int(rs[1])) / max(1, up + lo) * d.dt}
+    # NEXT-1: closed-loop episode on the cfg3 grid (T grid searches + T step kernels, on the device)
+    if world == 1:
+        c3 = W.pp_cfg3()
+        m3 = D.load_model(W.KIND_PREDATOR_PREY, c3.n_levels, c3.levels, c3.w, c3.params, device=dev.index)
+        T = 16
+        tr = torch.empty((T + 1, 6), dtype=torch.float32, device=dev)
+        ks = torch.empty(T, dtype=torch.int64, device=dev)
+        stt = torch.empty(2, dtype=torch.int32, device=dev)
+        D.pp_episode(m3, c3.inputs, T, c3.n_samples, c3.seed, speeds=(1.0, 0.8, 0.6), traj=tr, keys=ks, status=stt)
+        torch.cuda.synchronize()
+        e0.record()
+        D.pp_episode(m3, c3.inputs, T, c3.n_samples, c3.seed, speeds=(1.0, 0.8, 0.6), traj=tr, keys=ks, status=stt)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        st_h = stt.cpu().numpy()
+        steps_run = int(st_h[1]) if int(st_h[0]) != 0 else T
+        out["pp_episode_cfg3"] = {"ms": ms, "steps": steps_run, "outcome": int(st_h[0]),
+                                  "evals_per_s": c3.evals * steps_run / (ms / 1e3),
+                                  "note": "T=16 closed-loop steps, each a full cfg3 grid search + device step kernel"}
     if args.stroop:
         c = W.stroop_cfg4()
         m = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=dev.index)

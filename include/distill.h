@@ -98,6 +98,29 @@ typedef struct {
     unsigned long long* d_x_hist;   /* device [n_x_bins+2]: underflow, bins, overflow              (+=) */
 } distill_ddm_args;
 
+/* Closed-loop predator-prey episode (NEXT-1; "the entire process
+ * ... is repeated for each time step until the prey or the player is captured";
+ * spec/MODELS.md §7).  Per step t: one full grid search on the current positions
+ * (invocation t), the chosen attention draws the executed observation (Philox
+ * stream 4), player/prey/predator move, capture is tested.  Everything stays on
+ * the device: 2 launches per step, no host round trip, capturable in a CUDA
+ * graph.  After capture later steps are no-ops (fixed trip).
+ * Predator-prey models only; d_traj[0..5] must hold the initial positions unless
+ * h_init is given (then it is copied in, stream-ordered). */
+typedef struct {
+    uint32_t n_steps;            /* T >= 1                                                  */
+    uint32_t n_samples;          /* samples per allocation in every grid search, >= 1      */
+    uint64_t seed;
+    float v_player, v_prey, v_predator;   /* step lengths per time step                   */
+    float capture_radius;        /* capture when |prey - player| or |predator - player| <= r */
+    const float* h_init;         /* host [6] (prey, predator, player x/y) or NULL           */
+    float* d_traj;               /* device [(T+1)*6] positions, caller-owned                */
+    unsigned long long* d_keys;  /* device [T] best key per step (KEY_INIT after the end)   */
+    int* d_status;               /* device [2] {outcome 0 running/1 prey caught/2 player caught/3 no valid, steps} */
+} distill_episode_args;
+
+distill_status distill_pp_episode(const distill_model* model, const distill_episode_args* args, void* stream);
+
 int            distill_abi_version(void);
 const char*    distill_last_error(void);
 

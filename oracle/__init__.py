@@ -75,6 +75,8 @@ def _bind(path: str) -> C.CDLL:
         "od_stroop_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u64, u32, u32, u32, u64, C.c_void_p, C.c_void_p]),
         "od_stroop_value": (f32, [_f32p, _f32p, f32, f32, u32, u64, u64, u64]),
         "od_stroop_trial": (None, [_f32p, f32, f32, u64, u64, u32, C.POINTER(C.c_int), C.POINTER(u32)]),
+        "od_pp_episode": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u32, u32, u64, _f32p, f32,
+                                    _f32p, _u64p, np.ctypeslib.ndpointer(np.int32, flags="C")]),
         "od_flops_read": (C.c_ulonglong, []),
         "od_flops_reset": (None, []),
         "od_is_counting_build": (C.c_int, []),
@@ -246,6 +248,19 @@ def key_decode(k: int):
         return float("nan"), idx
     b = (hi & 0x7FFFFFFF) if (hi >> 31) else (~hi & 0xFFFFFFFF)
     return float(np.array([b], np.uint32).view(np.float32)[0]), idx
+
+
+def pp_episode(n_levels, levels, w, params, init, n_steps, n_samples, seed, speeds=(1.0, 0.8, 0.6),
+               capture_radius=0.5):
+    """Closed-loop episode (spec/MODELS.md §7): (traj[T+1,6], keys[T], (outcome, steps))."""
+    traj = np.zeros((int(n_steps) + 1) * 6, np.float32)
+    keys = np.zeros(int(n_steps), np.uint64)
+    status = np.zeros(2, np.int32)
+    rc = lib().od_pp_episode(_u32(n_levels), _f32(levels), _f32(w), _f32(params), _f32(init), int(n_steps),
+                             int(n_samples), int(seed), _f32(speeds), float(capture_radius), traj, keys, status)
+    if rc != 0:
+        raise ValueError("od_pp_episode rejected its arguments")
+    return traj.reshape(-1, 6), keys, (int(status[0]), int(status[1]))
 
 
 # ---------------------------------------------------------------- DDM / LCI

@@ -19,6 +19,7 @@
  */
 #include "distill_oracle.h"
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #ifdef OD_COUNT_FLOPS
@@ -542,5 +543,68 @@ int od_stroop_eval(const uint32_t n_levels[2], const float* levels, const float 
         }
         if (net) net[i - begin] = od_stroop_value(P, w, uc, us, n_trials, c[0], c[1], c[2]);
     }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* spec/MODELS.md §7: closed-loop predator-prey episode (NEXT-1)             */
+/* ------------------------------------------------------------------------ */
+int od_pp_episode(const uint32_t n_levels[3], const float* levels, const float w[3],
+                  const float params[3], const float init[6], uint32_t n_steps, uint32_t n_samples,
+                  uint64_t seed, const float speeds[3], float capture_radius,
+                  float* traj, uint64_t* keys, int* status) {
+    uint64_t N = (uint64_t)n_levels[0] * n_levels[1] * n_levels[2];
+    if (N == 0 || N > 0xFFFFFFFFull || n_samples == 0) return -1;
+    const float* lev[3] = { levels, levels + n_levels[0], levels + n_levels[0] + n_levels[1] };
+    float smax = params[0], smin = params[1], kappa = params[2];
+    float dsig = FSUB(smin, smax);
+    float rc2 = FMUL(capture_radius, capture_radius);
+    for (int k = 0; k < 6; ++k) traj[k] = init[k];
+    status[0] = 0; status[1] = 0;
+    float* cost = (float*)malloc(N * sizeof(float));
+    if (!cost) return -1;
+    for (uint32_t t = 0; t < n_steps; ++t) {
+        float* cur = traj + 6 * (size_t)t;
+        float* nxt = traj + 6 * (size_t)(t + 1);
+        keys[t] = 0xFFFFFFFFFFFFFFFFull;
+        if (status[0] != 0) { for (int k = 0; k < 6; ++k) nxt[k] = cur[k]; continue; }
+        /* 1. grid search on the current positions */
+        od_pp_eval(n_levels, levels, w, params, cur, 0, N, n_samples, seed, t, cost);
+        uint64_t best = 0xFFFFFFFFFFFFFFFFull;
+        for (uint64_t i = 0; i < N; ++i) { uint64_t k = od_key(cost[i], (uint32_t)i); if (k < best) best = k; }
+        keys[t] = best;
+        if ((best >> 32) == 0xFFFFFFFFull) { status[0] = 3; status[1] = (int)(t + 1); for (int k = 0; k < 6; ++k) nxt[k] = cur[k]; continue; }
+        uint32_t ka[3];
+        od_decode((uint32_t)best, 3, n_levels, ka);
+        float sig[3];
+        for (int e = 0; e < 3; ++e) sig[e] = FFMA(lev[e][ka[e]], dsig, smax);
+        /* 2. execution observation on stream 4 */
+        v2 p[3] = { { cur[0], cur[1] }, { cur[2], cur[3] }, { cur[4], cur[5] } };
+        uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+        uint32_t ctr[4] = { t, 0u, 0u, 4u }, X[4];
+        od_philox4x32_10(ctr, key, X);
+        uint32_t A[3] = { X[3] << 16, X[3] & 0xFFFF0000u, (X[0] << 24) | ((X[1] & 0xFFu) << 16) };
+        v2 o[3];
+        for (int e = 0; e < 3; ++e) {
+            float rad, c, n;
+            od_bm_polar(X[e], A[e], &rad, &c, &n);
+            float sr = FMUL(sig[e], rad);
+            o[e].x = FFMA(sr, c, p[e].x);
+            o[e].y = FFMA(sr, n, p[e].y);
+        }
+        /* 3. moves (all directions from the pre-move positions) */
+        v2 up = od_unit(od_action(o[0], o[1], o[2], kappa));
+        v2 uy = od_unit(od_sub(p[0], p[2]));
+        v2 ud = od_unit(od_sub(p[2], p[1]));
+        v2 pl = { FFMA(speeds[0], up.x, p[2].x), FFMA(speeds[0], up.y, p[2].y) };
+        v2 py = { FFMA(speeds[1], uy.x, p[0].x), FFMA(speeds[1], uy.y, p[0].y) };
+        v2 pd = { FFMA(speeds[2], ud.x, p[1].x), FFMA(speeds[2], ud.y, p[1].y) };
+        nxt[0] = py.x; nxt[1] = py.y; nxt[2] = pd.x; nxt[3] = pd.y; nxt[4] = pl.x; nxt[5] = pl.y;
+        /* 4. capture */
+        v2 qy = od_sub(py, pl), qd = od_sub(pd, pl);
+        if (FFMA(qy.y, qy.y, FMUL(qy.x, qy.x)) <= rc2) { status[0] = 1; status[1] = (int)(t + 1); }
+        else if (FFMA(qd.y, qd.y, FMUL(qd.x, qd.x)) <= rc2) { status[0] = 2; status[1] = (int)(t + 1); }
+    }
+    free(cost);
     return 0;
 }

@@ -100,6 +100,13 @@ float od_stroop_value(const float params[11], const float w[2], float u_c, float
 void od_stroop_trial(const float params[11], float u_c, float u_s, uint64_t seed,
                      uint64_t unit, uint32_t trial, int* resp, uint32_t* step);
 
+/* ---- closed-loop predator-prey episode (spec/MODELS.md §7) ---- */
+/* traj[(n_steps+1)*6], keys[n_steps], status[2] = {outcome, steps}; speeds = {v_player, v_prey, v_predator} */
+int od_pp_episode(const uint32_t n_levels[3], const float* levels, const float w[3],
+                  const float params[3], const float init[6], uint32_t n_steps, uint32_t n_samples,
+                  uint64_t seed, const float speeds[3], float capture_radius,
+                  float* traj, uint64_t* keys, int* status);
+
 /* ---- flop counting (only meaningful in the -DOD_COUNT_FLOPS build) ---- */
 unsigned long long od_flops_read(void);
 void od_flops_reset(void);

@@ -8,15 +8,16 @@ Public Python API (thin wrappers over the C ABI in include/distill.h):
     argmax(values, index_base, best)
     key_reset(best) / key_decode(key)
     ddm_batch(...)
+    pp_episode(model, init, n_steps, n_samples, seed, ...)   # closed loop, on the device
     shard_range(n, rank, world) / best_allreduce(key, group)   # multi-GPU plumbing
 
 Importing this package does not touch the GPU; the shared library is loaded
 on first use and there is no CPU fallback.
 """
 from .api import (KEY_INIT, Model, argmax, ddm_batch, eval_grid, eval_grid_host, key_decode,
-                  key_reset, launch_count, load_model)
+                  key_reset, launch_count, load_model, pp_episode)
 from .dist import best_allreduce, hist_allreduce, key_to_i64, i64_to_key, shard_range
 
-__all__ = ["KEY_INIT", "Model", "argmax", "ddm_batch", "eval_grid", "eval_grid_host", "key_decode",
+__all__ = ["KEY_INIT", "Model", "argmax", "ddm_batch", "eval_grid", "eval_grid_host", "key_decode", "pp_episode",
            "key_reset", "launch_count", "load_model", "best_allreduce", "hist_allreduce", "key_to_i64",
            "i64_to_key", "shard_range"]

@@ -49,6 +49,13 @@ class DdmArgs(C.Structure):
                 ("d_rt_hist", C.c_void_p), ("d_rt_sum", C.c_void_p), ("d_x_hist", C.c_void_p)]
 
 
+class EpisodeArgs(C.Structure):
+    _fields_ = [("n_steps", C.c_uint32), ("n_samples", C.c_uint32), ("seed", C.c_uint64),
+                ("v_player", C.c_float), ("v_prey", C.c_float), ("v_predator", C.c_float),
+                ("capture_radius", C.c_float), ("h_init", C.POINTER(C.c_float)),
+                ("d_traj", C.c_void_p), ("d_keys", C.c_void_p), ("d_status", C.c_void_p)]
+
+
 EXPORTS = {
     "distill_abi_version": (C.c_int, []),
     "distill_last_error": (C.c_char_p, []),
@@ -64,6 +71,7 @@ EXPORTS = {
     "distill_key_decode": (C.c_int, [C.c_uint64, C.POINTER(C.c_float), C.POINTER(C.c_uint64)]),
     "distill_ddm_batch": (C.c_int, [C.POINTER(DdmArgs), C.c_void_p]),
     "distill_launch_count": (C.c_uint64, []),
+    "distill_pp_episode": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_void_p]),
 }
 
 _lib = None

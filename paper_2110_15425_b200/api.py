@@ -139,6 +139,28 @@ def ddm_batch(drift, noise, threshold, x0, dt, n_steps, rt_bin_steps, n_x_bins, 
     check(lib().distill_ddm_batch(C.byref(a), _stream_handle(stream)))
 
 
+def pp_episode(model: Model, init, n_steps: int, n_samples: int, seed: int, speeds=(1.0, 0.8, 0.6),
+               capture_radius: float = 0.5, traj=None, keys=None, status=None, stream=None):
+    """distill_pp_episode: closed-loop episode on the device (spec/MODELS.md §7).
+
+    Returns (traj[(T+1),6] float32, keys[T] int64 raw key bits, status[2] int32) CUDA tensors.
+    If `init` is None, traj[0] must already hold the initial positions."""
+    import torch
+    dev = torch.device("cuda", model.device)
+    T = int(n_steps)
+    traj = torch.empty((T + 1, 6), dtype=torch.float32, device=dev) if traj is None else traj
+    keys = torch.empty(T, dtype=torch.int64, device=dev) if keys is None else keys
+    status = torch.empty(2, dtype=torch.int32, device=dev) if status is None else status
+    init_arr = None if init is None else np.ascontiguousarray(np.asarray(init, np.float32))
+    a = _abi.EpisodeArgs(T, int(n_samples), int(seed) & (2 ** 64 - 1), float(speeds[0]), float(speeds[1]),
+                         float(speeds[2]), float(capture_radius),
+                         _abi._fptr(init_arr) if init_arr is not None else None,
+                         _dev_ptr(traj, "traj", 6 * (T + 1)), _dev_ptr(keys, "keys", T),
+                         _dev_ptr(status, "status", 2))
+    check(lib().distill_pp_episode(model.handle, C.byref(a), _stream_handle(stream)))
+    return traj, keys, status
+
+
 def launch_count() -> int:
     return int(lib().distill_launch_count())
 
@@ -149,4 +171,4 @@ def key_from_tensor(best) -> int:
 
 
 __all__ = ["KEY_INIT", "DistillError", "Model", "load_model", "eval_grid", "eval_grid_host", "argmax",
-           "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor"]
+           "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode"]

@@ -172,6 +172,7 @@ static distill_status launch_pp(const distill_model* m, const distill_eval_args*
     p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
     p.levels = m->d_levels; p.net = a->d_net; p.best = a->d_best;
+    p.pos_dev = nullptr; p.status_dev = nullptr;
     const unsigned grid = (unsigned)((count + PP_BLOCK - 1) / PP_BLOCK);
     if ((a->n_samples & 1u) == 0)
         pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
@@ -284,6 +285,47 @@ distill_status distill_eval_grid_host(const distill_model* mc, const float* h_in
     if (h_net) CUDA_TRY(cudaMemcpyAsync(h_net, d_net, count * sizeof(float), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(h_best, d_best, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    return DISTILL_OK;
+}
+
+distill_status distill_pp_episode(const distill_model* mc, const distill_episode_args* e, void* stream) {
+    if (!mc || !e) return fail(DISTILL_E_INVALID_ARG, "pp_episode: NULL model/args");
+    distill_model* m = const_cast<distill_model*>(mc);
+    if (m->kind != DISTILL_MODEL_PREDATOR_PREY) return fail(DISTILL_E_UNSUPPORTED, "pp_episode: predator-prey only");
+    if (e->n_steps == 0 || e->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "pp_episode: n_steps, n_samples >= 1");
+    if (!e->d_traj || !e->d_keys || !e->d_status) return fail(DISTILL_E_INVALID_ARG, "pp_episode: NULL device buffer");
+    if (!(e->capture_radius >= 0.0f)) return fail(DISTILL_E_INVALID_ARG, "pp_episode: capture_radius must be >= 0");
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (e->h_init) CUDA_TRY(cudaMemcpyAsync(e->d_traj, e->h_init, 6 * sizeof(float), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(e->d_keys, 0xFF, e->n_steps * sizeof(unsigned long long), st));
+    CUDA_TRY(cudaMemsetAsync(e->d_status, 0, 2 * sizeof(int), st));
+    PPArgs p;
+    memset(&p, 0, sizeof p);
+    p.sigma_max = m->params[0]; p.sigma_min = m->params[1]; p.kappa = m->params[2];
+    p.w0 = m->w[0]; p.w1 = m->w[1]; p.w2 = m->w[2];
+    p.L0 = m->L[0]; p.L1 = m->L[1]; p.L2 = m->L[2];
+    p.n_samples = e->n_samples;
+    p.key0 = (uint32_t)e->seed; p.key1 = (uint32_t)(e->seed >> 32);
+    p.begin = 0; p.count = (uint32_t)m->n_alloc;
+    p.levels = m->d_levels; p.net = nullptr;
+    p.status_dev = e->d_status;
+    EpisodeArgs ea;
+    ea.v_pl = e->v_player; ea.v_py = e->v_prey; ea.v_pd = e->v_predator;
+    ea.rc = e->capture_radius;
+    ea.traj = e->d_traj; ea.keys = e->d_keys; ea.status = e->d_status;
+    const unsigned grid = (unsigned)((m->n_alloc + PP_BLOCK - 1) / PP_BLOCK);
+    const bool even = (e->n_samples & 1u) == 0;
+    for (uint32_t t = 0; t < e->n_steps; ++t) {
+        p.invocation = t;
+        p.pos_dev = e->d_traj + 6ull * t;
+        p.best = e->d_keys + t;
+        if (even) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+        else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
+        pp_episode_step_kernel<<<1, 32, 0, st>>>(p, ea, t);
+        g_launches += 2;
+    }
+    CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;
 }
 

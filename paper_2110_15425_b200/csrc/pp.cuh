@@ -33,8 +33,22 @@ struct PPArgs {
     uint32_t begin, count;                             // global index range [begin, begin+count)
     const float* __restrict__ levels;                  // device RO block: L0+L1+L2 floats
     float* __restrict__ net;                           // [count] or nullptr
-    key64_t* __restrict__ best;                          // [1] or nullptr
+    key64_t* __restrict__ best;                        // [1] or nullptr
+    const float* __restrict__ pos_dev;                 // episode: positions in device memory (or nullptr)
+    const int* __restrict__ status_dev;                // episode: skip the launch when status[0] != 0
 };
+
+// Episode support: positions come from device memory (written by the previous
+// step kernel) instead of the launch parameters.
+__device__ __forceinline__ PPArgs pp_resolve_positions(const PPArgs& a) {
+    PPArgs b = a;
+    if (a.pos_dev) {
+        b.prey_x = a.pos_dev[0]; b.prey_y = a.pos_dev[1];
+        b.pred_x = a.pos_dev[2]; b.pred_y = a.pos_dev[3];
+        b.pl_x = a.pos_dev[4]; b.pl_y = a.pos_dev[5];
+    }
+    return b;
+}
 
 struct V2 { F2 x, y; };   // a 2-D vector for the two samples of a pair
 
@@ -172,7 +186,9 @@ __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, floa
 
 // One thread per allocation; one atomicMin per block.
 template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false, bool EVEN = false>
-__global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs a) {
+__global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs a0) {
+    if (a0.status_dev && *a0.status_dev != 0) return;   // episode already over (uniform branch)
+    const PPArgs a = pp_resolve_positions(a0);
     const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
     const float2 ustar = pp_ustar_block(a);
     key64_t key = KEY_INIT;
@@ -212,6 +228,71 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_persistent_kernel(co
         }
     }
     if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
+}
+
+// ---------------------------------------------------------------- NEXT-1
+// Closed-loop episode step t (spec/MODELS.md §7): read the step's best key,
+// draw the execution observation with the chosen attention (stream 4), move
+// player / prey / predator, test capture, write positions t+1.  One thread.
+struct EpisodeArgs {
+    float v_pl, v_py, v_pd, rc;                        // speeds, capture radius
+    float* __restrict__ traj;                          // [(T+1)*6]
+    const key64_t* __restrict__ keys;                  // [T]
+    int* __restrict__ status;                          // [2] {outcome, steps}
+};
+
+__device__ __forceinline__ float2 unit1(float vx, float vy) {
+    const float n2 = __fmaf_rn(vy, vy, __fmaf_rn(vx, vx, 0x1p-126f));
+    const float y = rsqrt_spec(n2);
+    return make_float2(__fmul_rn(vx, y), __fmul_rn(vy, y));
+}
+
+__global__ void pp_episode_step_kernel(const PPArgs a, const EpisodeArgs e, uint32_t t) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const float* cur = e.traj + 6ull * t;
+    float* nxt = e.traj + 6ull * (t + 1);
+    if (e.status[0] != 0) {
+        for (int k = 0; k < 6; ++k) nxt[k] = cur[k];
+        return;
+    }
+    const key64_t best = e.keys[t];
+    if ((best >> 32) == 0xFFFFFFFFull) {          // no valid allocation (all NaN)
+        for (int k = 0; k < 6; ++k) nxt[k] = cur[k];
+        e.status[0] = 3; e.status[1] = (int)(t + 1);
+        return;
+    }
+    const uint32_t i = (uint32_t)best;
+    const uint32_t k2 = i % a.L2, r = i / a.L2;
+    const uint32_t k1 = r % a.L1, k0 = r / a.L1;
+    const float dsig = __fadd_rn(a.sigma_min, -a.sigma_max);
+    const float sg[3] = {__fmaf_rn(a.levels[k0], dsig, a.sigma_max),
+                         __fmaf_rn(a.levels[a.L0 + k1], dsig, a.sigma_max),
+                         __fmaf_rn(a.levels[a.L0 + a.L1 + k2], dsig, a.sigma_max)};
+    const uint4 X = philox4x32_10(make_uint4(t, 0u, 0u, 4u), a.key0, a.key1);
+    const uint32_t R[3] = {X.x, X.y, X.z};
+    const uint32_t A[3] = {X.w << 16, X.w & 0xFFFF0000u, (X.x << 24) | ((X.y & 0xFFu) << 16)};
+    float o[6];
+    for (int q = 0; q < 3; ++q) {
+        F2 rs, cq, sq;    // lane x only is used
+        bm_polar2<true, true, true>(R[q], R[q], A[q], A[q], rs, cq, sq);
+        const float sr = __fmul_rn(sg[q], rs.x);
+        o[2 * q] = __fmaf_rn(sr, cq.x, cur[2 * q]);
+        o[2 * q + 1] = __fmaf_rn(sr, sq.x, cur[2 * q + 1]);
+    }
+    const V2 q0 = {bc(o[0]), bc(o[1])}, q1 = {bc(o[2]), bc(o[3])}, q2 = {bc(o[4]), bc(o[5])};
+    const V2 d = action2<true>(q0, q1, q2, bc(-a.kappa));
+    const float2 up = unit1(d.x.x, d.y.x);
+    const float2 uy = unit1(__fadd_rn(cur[0], -cur[4]), __fadd_rn(cur[1], -cur[5]));
+    const float2 ud = unit1(__fadd_rn(cur[4], -cur[2]), __fadd_rn(cur[5], -cur[3]));
+    const float plx = __fmaf_rn(e.v_pl, up.x, cur[4]), ply = __fmaf_rn(e.v_pl, up.y, cur[5]);
+    const float pyx = __fmaf_rn(e.v_py, uy.x, cur[0]), pyy = __fmaf_rn(e.v_py, uy.y, cur[1]);
+    const float pdx = __fmaf_rn(e.v_pd, ud.x, cur[2]), pdy = __fmaf_rn(e.v_pd, ud.y, cur[3]);
+    nxt[0] = pyx; nxt[1] = pyy; nxt[2] = pdx; nxt[3] = pdy; nxt[4] = plx; nxt[5] = ply;
+    const float rc2 = __fmul_rn(e.rc, e.rc);
+    const float qyx = __fadd_rn(pyx, -plx), qyy = __fadd_rn(pyy, -ply);
+    const float qdx = __fadd_rn(pdx, -plx), qdy = __fadd_rn(pdy, -ply);
+    if (__fmaf_rn(qyy, qyy, __fmul_rn(qyx, qyx)) <= rc2) { e.status[0] = 1; e.status[1] = (int)(t + 1); }
+    else if (__fmaf_rn(qdy, qdy, __fmul_rn(qdx, qdx)) <= rc2) { e.status[0] = 2; e.status[1] = (int)(t + 1); }
 }
 
 }  // namespace distill

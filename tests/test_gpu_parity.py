@@ -286,3 +286,52 @@ def test_stroop_cfg4_sampled_allocations_full_trials(D, orc):
                                  threads=os.cpu_count() or 8)
         assert np.array_equal(cnt, wc)
         assert np.array_equal(_bits(net), _bits(wn))
+
+
+@pytest.mark.parametrize("shape,S,T,seed", [((3, 3, 3), 10, 30, 42), ((8, 7, 6), 24, 20, 5), ((20, 20, 20), 16, 12, 9)])
+def test_pp_episode_bit_exact(D, orc, shape, S, T, seed):
+    """Closed-loop episode (spec/MODELS.md §7): every step's key, the whole trajectory
+    and the outcome bit-exact against the oracle's step-by-step loop."""
+    import torch
+    cfg = W.PPConfig("ep", shape, S)
+    m = _model(D, cfg)
+    init = np.array([4.0, 1.0, -3.0, 2.0, 0.0, 0.0], np.float32)
+    speeds = (1.0, 0.7, 0.5)
+    traj, keys, status = D.pp_episode(m, init, T, S, seed, speeds=speeds, capture_radius=0.6)
+    torch.cuda.synchronize()
+    w_traj, w_keys, w_status = orc.pp_episode(cfg.n_levels, cfg.levels, cfg.w, cfg.params, init, T, S, seed,
+                                              speeds=speeds, capture_radius=0.6)
+    assert np.array_equal(_bits(traj.cpu().numpy()), _bits(w_traj))
+    assert [int(k) & (2 ** 64 - 1) for k in keys.cpu().numpy()] == [int(k) for k in w_keys]
+    assert tuple(int(v) for v in status.cpu().numpy()) == w_status
+
+
+def test_pp_episode_capture_and_graph_replay(D, orc):
+    """Straight-chase capture (outcome 1 at the closed-form step) and a CUDA-graph
+    capture of the whole episode replays to the same result."""
+    import torch
+    cfg = W.PPConfig("ep", (3, 3, 3), 4)
+    cfg.params = np.array([0.0, 0.0, 0.0], np.float32)
+    m = _model(D, cfg)
+    init = np.array([5.0, 0.0, -1000.0, 0.0, 0.0, 0.0], np.float32)
+    traj, keys, status = D.pp_episode(m, init, 40, 4, 7, speeds=(1.0, 0.75, 0.0), capture_radius=0.5)
+    torch.cuda.synchronize()
+    assert tuple(int(v) for v in status.cpu().numpy()) == (1, 18)
+    cfg2 = W.PPConfig("ep", (6, 6, 6), 8)
+    m2 = _model(D, cfg2)
+    init2 = np.array([4.0, 1.0, -3.0, 2.0, 0.0, 0.0], np.float32)
+    t2 = torch.empty((17, 6), dtype=torch.float32, device="cuda")
+    t2[0] = torch.from_numpy(init2).cuda()
+    k2 = torch.empty(16, dtype=torch.int64, device="cuda")
+    s2 = torch.empty(2, dtype=torch.int32, device="cuda")
+    D.pp_episode(m2, None, 16, 8, 3, traj=t2, keys=k2, status=s2)     # warm-up outside capture
+    torch.cuda.synchronize()
+    ref = (t2.clone(), k2.clone(), s2.clone())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        D.pp_episode(m2, None, 16, 8, 3, traj=t2, keys=k2, status=s2)
+    t2.zero_()
+    t2[0] = torch.from_numpy(init2).cuda()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(t2, ref[0]) and torch.equal(k2, ref[1]) and torch.equal(s2, ref[2])
