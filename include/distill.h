@@ -121,6 +121,24 @@ typedef struct {
 
 distill_status distill_pp_episode(const distill_model* model, const distill_episode_args* args, void* stream);
 
+/* Coarse-to-fine (AMR-style) refinement of the predator-prey grid search
+ * (NEXT-4; §4.3, Fig. 4; spec/MODELS.md §9).  The model's
+ * n_levels give L_d per signal (its level table is not used); each round r runs
+ * a full grid search (invocation invocation0 + r) over the box r, then the box
+ * shrinks to one level spacing around the round's best allocation, clamped to
+ * the initial box.  All rounds stay on the device (3 launches per round). */
+typedef struct {
+    const float* inputs; uint32_t n_inputs;   /* host [6] positions                          */
+    float lo[3], hi[3];                       /* initial box per signal (= clamp limits)      */
+    uint32_t rounds, n_samples, invocation0;
+    uint64_t seed;
+    unsigned long long* d_keys;   /* device [rounds] best key per round                       */
+    float* d_boxes;               /* device [(rounds+1)*6]: (lo, hi) per signal per round      */
+    float* d_levels;              /* device scratch [L0+L1+L2]                                 */
+} distill_amr_args;
+
+distill_status distill_pp_amr(const distill_model* model, const distill_amr_args* args, void* stream);
+
 int            distill_abi_version(void);
 const char*    distill_last_error(void);
 
@@ -147,6 +165,15 @@ distill_status distill_eval_grid_host(const distill_model* model, const float* h
  * into *d_best (max V <=> min key, lowest index on ties). */
 distill_status distill_argmax(const float* d_values, uint64_t n, uint64_t index_base,
                               unsigned long long* d_best, void* stream);
+/* Random tie-break among the minimal costs (NEXT-2; "randomly pick one";
+ * spec/MODELS.md §8).  Given *d_best from distill_argmax / distill_eval_grid
+ * (after any cross-shard all-reduce), atomicMin of (pi_i << 32 | index) over the
+ * entries whose canonical cost equals *d_best's into *d_tie (caller initialises it
+ * to DISTILL_KEY_INIT); pi_i = Philox stream 3.  The winner is the low 32 bits of
+ * the final *d_tie, uniform among the tied minima; shards combine with a second min. */
+distill_status distill_argmax_ties(const float* d_values, uint64_t n, uint64_t index_base, uint64_t seed,
+                                   uint32_t invocation, const unsigned long long* d_best,
+                                   unsigned long long* d_tie, void* stream);
 /* Set *d_best = DISTILL_KEY_INIT (stream-ordered). */
 distill_status distill_key_reset(unsigned long long* d_best, void* stream);
 /* Host, pure: key -> (cost C, global index).  DISTILL_E_NO_VALID for an all-NaN/empty key. */

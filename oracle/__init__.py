@@ -67,6 +67,7 @@ def _bind(path: str) -> C.CDLL:
         "od_pp_trace": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u32, u64, u32, _f32p]),
         "od_pp_eval_f64": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u64, u64, u32, u64, u32, C.c_void_p]),
         "od_key": (u64, [f32, u32]),
+        "od_argmax_random_ties": (C.c_int, [_f32p, u64, u64, u64, u32, C.POINTER(u64), C.POINTER(u64)]),
         "od_argmax_net": (C.c_int, [_f32p, u64, u64, C.POINTER(u64)]),
         "od_ddm_trial": (None, [C.POINTER(DdmParams), u64, u64, C.POINTER(C.c_int), C.POINTER(u32), C.POINTER(f32)]),
         "od_ddm_batch": (C.c_int, [C.POINTER(DdmParams), u64, u64, u64, _u64p, _u64p, _u64p]),
@@ -77,6 +78,7 @@ def _bind(path: str) -> C.CDLL:
         "od_stroop_trial": (None, [_f32p, f32, f32, u64, u64, u32, C.POINTER(C.c_int), C.POINTER(u32)]),
         "od_pp_episode": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u32, u32, u64, _f32p, f32,
                                     _f32p, _u64p, np.ctypeslib.ndpointer(np.int32, flags="C")]),
+        "od_pp_amr": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, _f32p, u32, u32, u64, u32, _u64p, _f32p]),
         "od_flops_read": (C.c_ulonglong, []),
         "od_flops_reset": (None, []),
         "od_is_counting_build": (C.c_int, []),
@@ -241,6 +243,14 @@ def argmax_net(net, base=0):
     return int(k.value), rc
 
 
+def argmax_random_ties(net, base=0, seed=0, invocation=0):
+    """(best key, tie key, rc); winner index = tie & 0xffffffff (spec/MODELS.md §8)."""
+    k, t = C.c_uint64(), C.c_uint64()
+    arr = _f32(net)
+    rc = lib().od_argmax_random_ties(arr, arr.size, int(base), int(seed), int(invocation), C.byref(k), C.byref(t))
+    return int(k.value), int(t.value), rc
+
+
 def key_decode(k: int):
     hi = (k >> 32) & 0xFFFFFFFF
     idx = k & 0xFFFFFFFF
@@ -261,6 +271,17 @@ def pp_episode(n_levels, levels, w, params, init, n_steps, n_samples, seed, spee
     if rc != 0:
         raise ValueError("od_pp_episode rejected its arguments")
     return traj.reshape(-1, 6), keys, (int(status[0]), int(status[1]))
+
+
+def pp_amr(n_levels, w, params, inputs, lo, hi, rounds, n_samples, seed, invocation0=0):
+    """Coarse-to-fine refinement (spec/MODELS.md §9): (keys[R], boxes[R+1, 3, 2])."""
+    keys = np.zeros(int(rounds), np.uint64)
+    boxes = np.zeros((int(rounds) + 1) * 6, np.float32)
+    rc = lib().od_pp_amr(_u32(n_levels), _f32(w), _f32(params), _f32(inputs), _f32(lo), _f32(hi), int(rounds),
+                         int(n_samples), int(seed), int(invocation0), keys, boxes)
+    if rc != 0:
+        raise ValueError("od_pp_amr rejected its arguments")
+    return keys, boxes.reshape(-1, 3, 2)
 
 
 # ---------------------------------------------------------------- DDM / LCI

@@ -608,3 +608,67 @@ int od_pp_episode(const uint32_t n_levels[3], const float* levels, const float w
     free(cost);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* spec/MODELS.md §8: random tie-breaking among the minimal costs (NEXT-2)   */
+/* ------------------------------------------------------------------------ */
+int od_argmax_random_ties(const float* net, uint64_t n, uint64_t base, uint64_t seed,
+                          uint32_t invocation, uint64_t* key_out, uint64_t* tie_out) {
+    uint64_t best;
+    int rc = od_argmax_net(net, n, base, &best);
+    *key_out = best;
+    *tie_out = 0xFFFFFFFFFFFFFFFFull;
+    if (rc != 0) return rc;
+    uint32_t hi = (uint32_t)(best >> 32);
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    for (uint64_t j = 0; j < n; ++j) {
+        uint64_t k = od_key(-net[j], (uint32_t)(base + j));
+        if ((uint32_t)(k >> 32) != hi) continue;              /* not among the tied minima */
+        uint32_t ctr[4] = { (uint32_t)(base + j), 0u, invocation, 3u }, X[4];
+        od_philox4x32_10(ctr, key, X);
+        uint64_t t = ((uint64_t)X[0] << 32) | (uint32_t)(base + j);
+        if (t < *tie_out) *tie_out = t;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* spec/MODELS.md §9: coarse-to-fine grid refinement (NEXT-4)                */
+/* ------------------------------------------------------------------------ */
+int od_pp_amr(const uint32_t n_levels[3], const float w[3], const float params[3], const float inputs[6],
+              const float lo0[3], const float hi0[3], uint32_t rounds, uint32_t n_samples, uint64_t seed,
+              uint32_t invocation0, uint64_t* keys, float* boxes) {
+    uint64_t N = (uint64_t)n_levels[0] * n_levels[1] * n_levels[2];
+    if (N == 0 || N > 0xFFFFFFFFull || n_samples == 0) return -1;
+    float lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) { lo[d] = lo0[d]; hi[d] = hi0[d]; boxes[2 * d] = lo[d]; boxes[2 * d + 1] = hi[d]; }
+    float* levels = (float*)malloc((n_levels[0] + n_levels[1] + n_levels[2]) * sizeof(float));
+    float* cost = (float*)malloc(N * sizeof(float));
+    if (!levels || !cost) { free(levels); free(cost); return -1; }
+    for (uint32_t r = 0; r < rounds; ++r) {
+        float step[3];
+        uint32_t off = 0;
+        for (int d = 0; d < 3; ++d) {
+            step[d] = (n_levels[d] > 1) ? FDIV(FSUB(hi[d], lo[d]), (float)(n_levels[d] - 1)) : 0.0f;
+            for (uint32_t k = 0; k < n_levels[d]; ++k) levels[off + k] = FFMA((float)k, step[d], lo[d]);
+            off += n_levels[d];
+        }
+        od_pp_eval(n_levels, levels, w, params, inputs, 0, N, n_samples, seed, invocation0 + r, cost);
+        uint64_t best = 0xFFFFFFFFFFFFFFFFull;
+        for (uint64_t i = 0; i < N; ++i) { uint64_t k = od_key(cost[i], (uint32_t)i); if (k < best) best = k; }
+        keys[r] = best;
+        uint32_t ka[3];
+        od_decode((uint32_t)best, 3, n_levels, ka);
+        off = 0;
+        for (int d = 0; d < 3; ++d) {
+            float a = levels[off + ka[d]];
+            off += n_levels[d];
+            lo[d] = fmaxf(lo0[d], FSUB(a, step[d]));
+            hi[d] = fminf(hi0[d], FADD(a, step[d]));
+            boxes[6 * (r + 1) + 2 * d] = lo[d];
+            boxes[6 * (r + 1) + 2 * d + 1] = hi[d];
+        }
+    }
+    free(levels); free(cost);
+    return 0;
+}

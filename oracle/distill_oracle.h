@@ -68,6 +68,11 @@ uint64_t od_key(float cost, uint32_t index);
 /* min over key(-net[j], base+j); returns 0 ok, 1 if no finite/inf candidate (all NaN or n == 0) */
 int od_argmax_net(const float* net, uint64_t n, uint64_t base, uint64_t* key);
 
+/* random tie-break (spec/MODELS.md §8): key_out = plain best key, tie_out = min (pi_i << 32 | i)
+ * over the tied minima; the winner is (uint32)tie_out.  Returns od_argmax_net's code. */
+int od_argmax_random_ties(const float* net, uint64_t n, uint64_t base, uint64_t seed,
+                          uint32_t invocation, uint64_t* key_out, uint64_t* tie_out);
+
 /* ---- DDM (spec/MODELS.md §4) ---- */
 typedef struct {
     float drift, noise, threshold, x0, dt;
@@ -106,6 +111,11 @@ int od_pp_episode(const uint32_t n_levels[3], const float* levels, const float w
                   const float params[3], const float init[6], uint32_t n_steps, uint32_t n_samples,
                   uint64_t seed, const float speeds[3], float capture_radius,
                   float* traj, uint64_t* keys, int* status);
+
+/* ---- coarse-to-fine refinement (spec/MODELS.md §9): keys[rounds], boxes[(rounds+1)*6] = (lo, hi) x 3 ---- */
+int od_pp_amr(const uint32_t n_levels[3], const float w[3], const float params[3], const float inputs[6],
+              const float lo0[3], const float hi0[3], uint32_t rounds, uint32_t n_samples, uint64_t seed,
+              uint32_t invocation0, uint64_t* keys, float* boxes);
 
 /* ---- flop counting (only meaningful in the -DOD_COUNT_FLOPS build) ---- */
 unsigned long long od_flops_read(void);

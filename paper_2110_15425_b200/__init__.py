@@ -5,19 +5,20 @@ Public Python API (thin wrappers over the C ABI in include/distill.h):
     load_model(kind, n_levels, levels, cost_weights, params, device=0) -> Model
     eval_grid(model, inputs, n_samples, seed, begin=0, end=None, net=None, best=None, ...)
     eval_grid_host(model, inputs, n_samples, seed, ...)   # host buffers, end to end
-    argmax(values, index_base, best)
+    argmax(values, index_base, best) / argmax_ties(values, base, seed, t, best, tie)
     key_reset(best) / key_decode(key)
     ddm_batch(...)
     pp_episode(model, init, n_steps, n_samples, seed, ...)   # closed loop, on the device
+    pp_amr(model, inputs, lo, hi, rounds, n_samples, seed)   # coarse-to-fine refinement
     shard_range(n, rank, world) / best_allreduce(key, group)   # multi-GPU plumbing
 
 Importing this package does not touch the GPU; the shared library is loaded
 on first use and there is no CPU fallback.
 """
-from .api import (KEY_INIT, Model, argmax, ddm_batch, eval_grid, eval_grid_host, key_decode,
-                  key_reset, launch_count, load_model, pp_episode)
+from .api import (KEY_INIT, Model, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, key_decode,
+                  key_reset, launch_count, load_model, pp_amr, pp_episode)
 from .dist import best_allreduce, hist_allreduce, key_to_i64, i64_to_key, shard_range
 
-__all__ = ["KEY_INIT", "Model", "argmax", "ddm_batch", "eval_grid", "eval_grid_host", "key_decode", "pp_episode",
+__all__ = ["KEY_INIT", "Model", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "key_decode", "pp_episode", "pp_amr",
            "key_reset", "launch_count", "load_model", "best_allreduce", "hist_allreduce", "key_to_i64",
            "i64_to_key", "shard_range"]

@@ -56,6 +56,13 @@ class EpisodeArgs(C.Structure):
                 ("d_traj", C.c_void_p), ("d_keys", C.c_void_p), ("d_status", C.c_void_p)]
 
 
+class AmrArgs(C.Structure):
+    _fields_ = [("inputs", C.POINTER(C.c_float)), ("n_inputs", C.c_uint32),
+                ("lo", C.c_float * 3), ("hi", C.c_float * 3),
+                ("rounds", C.c_uint32), ("n_samples", C.c_uint32), ("invocation0", C.c_uint32),
+                ("seed", C.c_uint64), ("d_keys", C.c_void_p), ("d_boxes", C.c_void_p), ("d_levels", C.c_void_p)]
+
+
 EXPORTS = {
     "distill_abi_version": (C.c_int, []),
     "distill_last_error": (C.c_char_p, []),
@@ -67,10 +74,13 @@ EXPORTS = {
                                          C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p,
                                          C.POINTER(C.c_uint64), C.c_void_p]),
     "distill_argmax": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "distill_argmax_ties": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p,
+                                      C.c_void_p, C.c_void_p]),
     "distill_key_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
     "distill_key_decode": (C.c_int, [C.c_uint64, C.POINTER(C.c_float), C.POINTER(C.c_uint64)]),
     "distill_ddm_batch": (C.c_int, [C.POINTER(DdmArgs), C.c_void_p]),
     "distill_launch_count": (C.c_uint64, []),
+    "distill_pp_amr": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_void_p]),
     "distill_pp_episode": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_void_p]),
 }
 

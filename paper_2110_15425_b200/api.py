@@ -114,6 +114,13 @@ def argmax(values, index_base: int, best, stream=None) -> None:
                                _dev_ptr(best, "best", 1), _stream_handle(stream)))
 
 
+def argmax_ties(values, index_base: int, seed: int, invocation: int, best, tie, stream=None) -> None:
+    """distill_argmax_ties: random tie-break among the minimal costs (spec/MODELS.md §8)."""
+    check(lib().distill_argmax_ties(_dev_ptr(values, "values"), values.numel(), int(index_base),
+                                    int(seed) & (2 ** 64 - 1), int(invocation), _dev_ptr(best, "best", 1),
+                                    _dev_ptr(tie, "tie", 1), _stream_handle(stream)))
+
+
 def key_reset(best, stream=None) -> None:
     check(lib().distill_key_reset(_dev_ptr(best, "best", 1), _stream_handle(stream)))
 
@@ -161,6 +168,26 @@ def pp_episode(model: Model, init, n_steps: int, n_samples: int, seed: int, spee
     return traj, keys, status
 
 
+def pp_amr(model: Model, inputs, lo, hi, rounds: int, n_samples: int, seed: int, invocation0: int = 0,
+           keys=None, boxes=None, levels=None, stream=None):
+    """distill_pp_amr: coarse-to-fine refinement on the device (spec/MODELS.md §9).
+
+    Returns (keys[R] int64 raw key bits, boxes[R+1, 3, 2] float32) CUDA tensors."""
+    import torch
+    dev = torch.device("cuda", model.device)
+    R = int(rounds)
+    keys = torch.empty(R, dtype=torch.int64, device=dev) if keys is None else keys
+    boxes = torch.empty((R + 1, 3, 2), dtype=torch.float32, device=dev) if boxes is None else boxes
+    levels = torch.empty(int(model.n_levels.sum()), dtype=torch.float32, device=dev) if levels is None else levels
+    inp = np.ascontiguousarray(np.asarray(inputs, np.float32))
+    a = _abi.AmrArgs(_abi._fptr(inp), inp.size, (C.c_float * 3)(*[float(x) for x in lo]),
+                     (C.c_float * 3)(*[float(x) for x in hi]), R, int(n_samples), int(invocation0),
+                     int(seed) & (2 ** 64 - 1), _dev_ptr(keys, "keys", R), _dev_ptr(boxes, "boxes", 6 * (R + 1)),
+                     _dev_ptr(levels, "levels", int(model.n_levels.sum())))
+    check(lib().distill_pp_amr(model.handle, C.byref(a), _stream_handle(stream)))
+    return keys, boxes
+
+
 def launch_count() -> int:
     return int(lib().distill_launch_count())
 
@@ -171,4 +198,4 @@ def key_from_tensor(best) -> int:
 
 
 __all__ = ["KEY_INIT", "DistillError", "Model", "load_model", "eval_grid", "eval_grid_host", "argmax",
-           "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode"]
+           "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode", "argmax_ties", "pp_amr"]

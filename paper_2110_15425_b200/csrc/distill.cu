@@ -329,6 +329,47 @@ distill_status distill_pp_episode(const distill_model* mc, const distill_episode
     return DISTILL_OK;
 }
 
+distill_status distill_pp_amr(const distill_model* mc, const distill_amr_args* g, void* stream) {
+    if (!mc || !g) return fail(DISTILL_E_INVALID_ARG, "pp_amr: NULL model/args");
+    distill_model* m = const_cast<distill_model*>(mc);
+    if (m->kind != DISTILL_MODEL_PREDATOR_PREY) return fail(DISTILL_E_UNSUPPORTED, "pp_amr: predator-prey only");
+    if (!g->inputs || g->n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "pp_amr: needs 6 host inputs");
+    if (g->rounds == 0 || g->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "pp_amr: rounds, n_samples >= 1");
+    if (!g->d_keys || !g->d_boxes || !g->d_levels) return fail(DISTILL_E_INVALID_ARG, "pp_amr: NULL device buffer");
+    for (int d = 0; d < 3; ++d)
+        if (!(g->lo[d] <= g->hi[d])) return fail(DISTILL_E_INVALID_ARG, "pp_amr: lo > hi for signal %d", d);
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemsetAsync(g->d_keys, 0xFF, g->rounds * sizeof(unsigned long long), st));
+    AmrArgs a;
+    for (int d = 0; d < 3; ++d) { a.lo0[d] = g->lo[d]; a.hi0[d] = g->hi[d]; a.L[d] = m->L[d]; }
+    a.levels = g->d_levels; a.boxes = g->d_boxes; a.keys = g->d_keys;
+    PPArgs p;
+    memset(&p, 0, sizeof p);
+    p.prey_x = g->inputs[0]; p.prey_y = g->inputs[1]; p.pred_x = g->inputs[2]; p.pred_y = g->inputs[3];
+    p.pl_x = g->inputs[4]; p.pl_y = g->inputs[5];
+    p.sigma_max = m->params[0]; p.sigma_min = m->params[1]; p.kappa = m->params[2];
+    p.w0 = m->w[0]; p.w1 = m->w[1]; p.w2 = m->w[2];
+    p.L0 = m->L[0]; p.L1 = m->L[1]; p.L2 = m->L[2];
+    p.n_samples = g->n_samples;
+    p.key0 = (uint32_t)g->seed; p.key1 = (uint32_t)(g->seed >> 32);
+    p.begin = 0; p.count = (uint32_t)m->n_alloc;
+    p.levels = g->d_levels;
+    const unsigned grid = (unsigned)((m->n_alloc + PP_BLOCK - 1) / PP_BLOCK);
+    const bool even = (g->n_samples & 1u) == 0;
+    for (uint32_t r = 0; r < g->rounds; ++r) {
+        amr_levels_kernel<<<1, 256, 0, st>>>(a, r);
+        p.invocation = g->invocation0 + r;
+        p.best = g->d_keys + r;
+        if (even) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+        else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
+        amr_refine_kernel<<<1, 32, 0, st>>>(a, r);
+        g_launches += 3;
+    }
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
 distill_status distill_argmax(const float* d_values, uint64_t n, uint64_t index_base,
                               unsigned long long* d_best, void* stream) {
     if (!d_best || (!d_values && n)) return fail(DISTILL_E_INVALID_ARG, "argmax: NULL pointer");
@@ -341,6 +382,24 @@ distill_status distill_argmax(const float* d_values, uint64_t n, uint64_t index_
     const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)n_sm * 8);
     argmax_net_kernel<ARGMAX_BLOCK><<<grid, ARGMAX_BLOCK, 0, (cudaStream_t)stream>>>(d_values, n, (uint32_t)index_base,
                                                                                       d_best);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+distill_status distill_argmax_ties(const float* d_values, uint64_t n, uint64_t index_base, uint64_t seed,
+                                   uint32_t invocation, const unsigned long long* d_best,
+                                   unsigned long long* d_tie, void* stream) {
+    if (!d_best || !d_tie || (!d_values && n)) return fail(DISTILL_E_INVALID_ARG, "argmax_ties: NULL pointer");
+    if (index_base + n > 0x100000000ull) return fail(DISTILL_E_OVERFLOW, "argmax_ties: index exceeds 32 bits");
+    if (n == 0) return DISTILL_OK;
+    int dev = 0, n_sm = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    const uint64_t need = (n + ARGMAX_BLOCK - 1) / ARGMAX_BLOCK;
+    const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)n_sm * 8);
+    argmax_ties_kernel<ARGMAX_BLOCK><<<grid, ARGMAX_BLOCK, 0, (cudaStream_t)stream>>>(
+        d_values, n, (uint32_t)index_base, d_best, (uint32_t)seed, (uint32_t)(seed >> 32), invocation, d_tie);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;

@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "rng.cuh"
+
 namespace distill {
 
 typedef unsigned long long key64_t;
@@ -79,6 +81,28 @@ __global__ void __launch_bounds__(BLOCK) argmax_net_kernel(const float* __restri
         }
     }
     block_min_key_atomic<BLOCK>(k, best);
+}
+
+// NEXT-2 random tie-break (spec/MODELS.md §8): among the entries whose
+// canonical cost equals the best key's (pass A result in *best), min over
+// (pi_i << 32 | i) with pi_i = Philox(key, (i, 0, t, 3)).x -> atomicMin(*tie).
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) argmax_ties_kernel(const float* __restrict__ v, uint64_t n, uint32_t base,
+                                                            const key64_t* __restrict__ best, uint32_t key0,
+                                                            uint32_t key1, uint32_t invocation,
+                                                            key64_t* __restrict__ tie) {
+    const uint32_t hi = (uint32_t)(*best >> 32);
+    key64_t k = KEY_INIT;
+    if (hi != 0xFFFFFFFFu) {
+        for (uint64_t j = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; j < n; j += (uint64_t)gridDim.x * BLOCK) {
+            const uint32_t idx = base + (uint32_t)j;
+            if ((uint32_t)(make_key(-__ldg(v + j), idx) >> 32) != hi) continue;
+            const uint4 X = philox4x32_10(make_uint4(idx, 0u, invocation, 3u), key0, key1);
+            const key64_t t = ((key64_t)X.x << 32) | idx;
+            k = t < k ? t : k;
+        }
+    }
+    block_min_key_atomic<BLOCK>(k, tie);
 }
 
 }  // namespace distill

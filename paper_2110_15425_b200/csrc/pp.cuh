@@ -295,4 +295,55 @@ __global__ void pp_episode_step_kernel(const PPArgs a, const EpisodeArgs e, uint
     else if (__fmaf_rn(qdy, qdy, __fmul_rn(qdx, qdx)) <= rc2) { e.status[0] = 2; e.status[1] = (int)(t + 1); }
 }
 
+// ---------------------------------------------------------------- NEXT-4
+// Coarse-to-fine refinement (spec/MODELS.md §9).  Round r: amr_levels_kernel
+// writes the level table of box r, the grid search runs on it, and
+// amr_refine_kernel shrinks the box to one level spacing around the best
+// allocation.  Boxes live in device memory: boxes[r][d] = (lo, hi).
+struct AmrArgs {
+    float lo0[3], hi0[3];                      // initial box = clamp limits
+    uint32_t L[3];
+    float* __restrict__ levels;                // [L0+L1+L2] scratch
+    float* __restrict__ boxes;                 // [(R+1)*6]
+    const key64_t* __restrict__ keys;          // [R]
+};
+
+__device__ __forceinline__ float amr_step(float lo, float hi, uint32_t L) {
+    return L > 1 ? __fdiv_rn(__fadd_rn(hi, -lo), __uint2float_rn(L - 1)) : 0.0f;
+}
+
+__global__ void amr_levels_kernel(const AmrArgs g, uint32_t r) {
+    float* box = g.boxes + 6ull * r;
+    if (r == 0 && threadIdx.x < 3) {          // round 0: the initial box from the launch parameters
+        box[2 * threadIdx.x] = g.lo0[threadIdx.x];
+        box[2 * threadIdx.x + 1] = g.hi0[threadIdx.x];
+    }
+    __syncthreads();
+    const uint32_t total = g.L[0] + g.L[1] + g.L[2];
+    for (uint32_t j = threadIdx.x; j < total; j += blockDim.x) {
+        const uint32_t d = j < g.L[0] ? 0 : (j < g.L[0] + g.L[1] ? 1 : 2);
+        const uint32_t k = j - (d == 0 ? 0 : (d == 1 ? g.L[0] : g.L[0] + g.L[1]));
+        const float lo = box[2 * d], hi = box[2 * d + 1];
+        g.levels[j] = __fmaf_rn(__uint2float_rn(k), amr_step(lo, hi, g.L[d]), lo);
+    }
+}
+
+__global__ void amr_refine_kernel(const AmrArgs g, uint32_t r) {
+    if (threadIdx.x != 0) return;
+    const float* box = g.boxes + 6ull * r;
+    float* nxt = g.boxes + 6ull * (r + 1);
+    const uint32_t i = (uint32_t)g.keys[r];
+    const uint32_t k2 = i % g.L[2], q = i / g.L[2];
+    const uint32_t k[3] = {q / g.L[1], q % g.L[1], k2};
+    uint32_t off = 0;
+    for (int d = 0; d < 3; ++d) {
+        const float lo = box[2 * d], hi = box[2 * d + 1];
+        const float st = amr_step(lo, hi, g.L[d]);
+        const float a = g.levels[off + k[d]];
+        off += g.L[d];
+        nxt[2 * d] = fmaxf(g.lo0[d], __fadd_rn(a, -st));
+        nxt[2 * d + 1] = fminf(g.hi0[d], __fadd_rn(a, st));
+    }
+}
+
 }  // namespace distill

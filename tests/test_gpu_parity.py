@@ -335,3 +335,55 @@ def test_pp_episode_capture_and_graph_replay(D, orc):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(t2, ref[0]) and torch.equal(k2, ref[1]) and torch.equal(s2, ref[2])
+
+
+def test_argmax_random_ties_bit_exact_and_uniform(D, orc):
+    """NEXT-2: GPU tie keys equal the oracle's for every seed; 8 tied minima each
+    win 1/8 +- 0.02 of 4000 reseeded runs; a PP grid with all-equal costs picks
+    a uniformly random allocation instead of index 0."""
+    import torch
+    net = np.full(64, -5.0, np.float32)
+    tied = [3, 7, 11, 20, 33, 40, 51, 63]
+    net[tied] = -1.0
+    t_net = torch.from_numpy(net).cuda()
+    best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.argmax(t_net, 0, best)
+    ties = torch.full((4000,), -1, dtype=torch.int64, device="cuda")
+    for seed in range(4000):
+        D.argmax_ties(t_net, 0, seed, 0, best, ties[seed:seed + 1])
+    torch.cuda.synchronize()
+    got = [int(x) & (2 ** 64 - 1) for x in ties.cpu().numpy()]
+    counts = dict.fromkeys(tied, 0)
+    for seed, t in enumerate(got):
+        k, t_or, rc = orc.argmax_random_ties(net, 0, seed)
+        assert t == t_or
+        counts[t & 0xFFFFFFFF] += 1
+    for v in counts.values():
+        assert abs(v / 4000 - 1 / 8) < 0.02
+    cfg = W.PPConfig("ties", (4, 4, 4), 4)
+    cfg.params = np.array([0.0, 0.0, 0.5], np.float32)
+    cfg.w = np.zeros(3, np.float32)
+    m = _model(D, cfg)
+    netp = torch.empty(64, device="cuda")
+    bestp = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.eval_grid(m, cfg.inputs, 4, 1, net=netp, best=bestp)
+    tie = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.argmax_ties(netp, 0, 1, 0, bestp, tie)
+    torch.cuda.synchronize()
+    _, t_or, _ = orc.argmax_random_ties(netp.cpu().numpy(), 0, 1)
+    assert int(tie.item()) & (2 ** 64 - 1) == t_or
+
+
+@pytest.mark.parametrize("shape,S,R,lo,hi", [((5, 5, 5), 16, 7, (0, 0, 0), (1, 1, 1)),
+                                             ((9, 1, 1), 100, 6, (0, .5, .5), (1, .5, .5)),
+                                             ((12, 10, 8), 12, 4, (0, 0.2, 0), (1, 0.8, 0.5))])
+def test_pp_amr_bit_exact(D, orc, shape, S, R, lo, hi):
+    """NEXT-4: every round's key and box bit-exact against the oracle's refinement loop."""
+    import torch
+    cfg = W.PPConfig("amr", shape, S)
+    m = _model(D, cfg)
+    keys, boxes = D.pp_amr(m, cfg.inputs, lo, hi, R, S, 21, invocation0=3)
+    torch.cuda.synchronize()
+    w_keys, w_boxes = orc.pp_amr(cfg.n_levels, cfg.w, cfg.params, cfg.inputs, lo, hi, R, S, 21, invocation0=3)
+    assert [int(k) & (2 ** 64 - 1) for k in keys.cpu().numpy()] == [int(k) for k in w_keys]
+    assert np.array_equal(_bits(boxes.cpu().numpy()), _bits(w_boxes))

@@ -50,3 +50,50 @@ def test_signed_int64_flip_preserves_order(orc):
     j = int(np.argmin(flipped))
     assert keys[j] == min(keys)
     assert math.isnan(orc.key_decode(orc.key(float("nan"), 3))[0])
+
+
+def test_random_ties_uniform_frequency(orc):
+    """8 tied minima among 64: over 10,000 reseeded runs each wins with
+    frequency 1/8 +- 0.02 (P:306 'randomly pick one')."""
+    net = np.full(64, -5.0, np.float32)
+    tied = [3, 7, 11, 20, 33, 40, 51, 63]
+    net[tied] = -1.0
+    counts = dict.fromkeys(tied, 0)
+    for seed in range(10000):
+        k, t, rc = orc.argmax_random_ties(net, 0, seed)
+        assert rc == 0 and k & 0xFFFFFFFF == 3       # plain rule: lowest index
+        counts[t & 0xFFFFFFFF] += 1
+    assert set(counts) == set(tied)
+    for v in counts.values():
+        assert abs(v / 10000 - 1 / 8) < 0.02
+
+
+def test_random_ties_unique_minimum_wins_regardless_of_seed(orc):
+    """One strictly minimal cost at index 5 -> it wins for every seed."""
+    net = np.linspace(-3, -1, 40).astype(np.float32)
+    net[5] = 1.0
+    for seed in range(200):
+        _, t, _ = orc.argmax_random_ties(net, 100, seed)
+        assert t & 0xFFFFFFFF == 105
+
+
+def test_random_ties_shard_combine(orc):
+    """min over shards of the tie keys == tie key of the whole array (second all-reduce)."""
+    rng = np.random.default_rng(2)
+    net = rng.integers(-3, 1, 500).astype(np.float32)
+    k_full, t_full, _ = orc.argmax_random_ties(net, 0, 77)
+    parts = []
+    for b, e in [(0, 123), (123, 300), (300, 500)]:
+        kb, _, _ = orc.argmax_random_ties(net[b:e], b, 77)
+        parts.append(kb)
+    kmin = min(parts)
+    assert kmin == k_full
+    # pass B on each shard restricted to the global minimum value
+    ties = []
+    for b, e in [(0, 123), (123, 300), (300, 500)]:
+        sub = net[b:e].copy()
+        sub[-sub > orc.key_decode(kmin)[0]] = -np.inf       # only global minima can win
+        _, tb, rc = orc.argmax_random_ties(sub, b, 77)
+        if rc == 0 and orc.argmax_net(sub, b)[0] >> 32 == kmin >> 32:
+            ties.append(tb)
+    assert min(ties) == t_full
