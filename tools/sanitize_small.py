@@ -1,0 +1,42 @@
+"""Exercise every kernel of libdistill.so on small inputs (for compute-sanitizer runs; tools only)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2110_15425_b200 as D  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+def main():
+    torch.cuda.set_device(0)
+    cfg = W.PPConfig("s", (7, 5, 3), 6)
+    m = D.load_model(W.KIND_PREDATOR_PREY, cfg.n_levels, cfg.levels, cfg.w, cfg.params, device=0)
+    net = torch.empty(cfg.n_alloc, device="cuda")
+    best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.eval_grid(m, cfg.inputs, 6, 1, net=net, best=best)
+    D.eval_grid(m, cfg.inputs, 5, 1, 3, 77, net=net, best=best)
+    D.argmax(net, 0, best)
+    tie = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.argmax_ties(net, 0, 3, 0, best, tie)
+    D.eval_grid_host(m, cfg.inputs, 6, 1, net_out=np.empty(cfg.n_alloc, np.float32))
+    D.pp_episode(m, cfg.inputs, 5, 4, 2)
+    D.pp_amr(m, cfg.inputs, (0, 0, 0), (1, 1, 1), 3, 4, 2)
+    d = W.DDMConfig(n_steps=50)
+    rh, rs, xh = (torch.zeros(n, dtype=torch.int64, device="cuda") for n in d.hist_sizes)
+    D.ddm_batch(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins, d.x_lo,
+                d.x_hi, 0, 700, 1, rh, rs, xh)
+    c = W.StroopConfig("s", (3, 4), 50)
+    ms = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=0)
+    sn = torch.empty(c.n_alloc, device="cuda")
+    D.eval_grid(ms, None, c.n_trials, 1, net=sn, best=best)
+    torch.cuda.synchronize()
+    print("sanitize-small ok", int(best.item()), int(rh.sum()))
+
+
+if __name__ == "__main__":
+    main()
