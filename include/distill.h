@@ -41,8 +41,10 @@ typedef enum {
 } distill_status;
 
 typedef enum {
-    DISTILL_MODEL_PREDATOR_PREY = 1,  /* P:140-167, Fig. 1                      */
-    DISTILL_MODEL_STROOP_LCA = 2      /* P:525 (surrogate, spec/MODELS.md §6)   */
+    DISTILL_MODEL_PREDATOR_PREY = 1,  /* P:140-167, Fig. 1                                */
+    DISTILL_MODEL_STROOP_LCA = 2,     /* P:525 (surrogate, spec/MODELS.md §6)             */
+    DISTILL_MODEL_EXT_STROOP_A = 3,   /* P:527 Extended Stroop, version A (§10, NEXT-3)   */
+    DISTILL_MODEL_EXT_STROOP_B = 4    /* P:527 version B: computationally identical to A  */
 } distill_model_kind;
 
 /* "No candidate" value of a packed (value, index) key; initialise d_best to it. */
@@ -58,7 +60,10 @@ typedef struct distill_model distill_model;  /* opaque, library-owned */
  *                  params = {sigma_max, sigma_min, kappa}, n_params = 3.
  *   STROOP_LCA:    n_signals = 2 (colour attention u_c, word suppression u_s);
  *                  params = {g_c, g_w, tau, leak, inhibition, noise, dt,
- *                            threshold, reward, rt_cost, n_steps}, n_params = 11. */
+ *                            threshold, reward, rt_cost, n_steps}, n_params = 11.
+ *   EXT_STROOP_A/B: n_signals = 2 (as Stroop); params = {g_c, g_w, tau, N_h, lambda,
+ *                  a_p, gamma, sigma_d, dt_d, z_d, N_d, reward, rt_cost}, n_params = 13;
+ *                  d_counts = {n_both_correct, n_undecided, rt_sum}. */
 typedef struct {
     uint32_t kind;               /* distill_model_kind                               */
     uint32_t n_signals;          /* D                                                */

@@ -79,6 +79,12 @@ def _bind(path: str) -> C.CDLL:
         "od_pp_episode": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u32, u32, u64, _f32p, f32,
                                     _f32p, _u64p, np.ctypeslib.ndpointer(np.int32, flags="C")]),
         "od_pp_amr": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, _f32p, u32, u32, u64, u32, _u64p, _f32p]),
+        "od_ext_stroop_eval": (C.c_int, [C.c_int, _u32p, _f32p, _f32p, _f32p, u64, u64, u32, u64,
+                                         C.c_void_p, C.c_void_p]),
+        "od_ext_stroop_trial_a": (None, [_f32p, f32, f32, u64, u64, u32, np.ctypeslib.ndpointer(np.int32, flags="C"),
+                                         _u32p]),
+        "od_ext_stroop_trial_b": (None, [_f32p, f32, f32, u64, u64, u32, np.ctypeslib.ndpointer(np.int32, flags="C"),
+                                         _u32p]),
         "od_flops_read": (C.c_ulonglong, []),
         "od_flops_reset": (None, []),
         "od_is_counting_build": (C.c_int, []),
@@ -374,3 +380,42 @@ def stroop_trial(params, u_c, u_s, seed, unit, trial):
 def stroop_value(params, w, u_c, u_s, n_trials, n_correct, n_undecided, rt_sum):
     return lib().od_stroop_value(_f32(params), _f32(w), u_c, u_s, n_trials,
                                  int(n_correct), int(n_undecided), int(rt_sum))
+
+
+# ---------------------------------------------------------------- Extended Stroop A/B
+
+def ext_stroop_eval(variant, n_levels, levels, w, params, begin, end, n_trials, seed, threads=1):
+    """variant 0 = A, 1 = B (spec/MODELS.md §10): (counts[n,3] uint64, net[n] float32)."""
+    n = int(end) - int(begin)
+    counts = np.zeros((n, 3), np.uint64)
+    net = np.zeros(n, np.float32)
+    args = (_u32(n_levels), _f32(levels), _f32(w), _f32(params))
+    L = lib()
+    threads = max(1, min(int(threads), max(n, 1)))
+    seg = (n + threads - 1) // threads
+
+    def work(t):
+        b = begin + t * seg
+        e = min(begin + n, b + seg)
+        if e <= b:
+            return
+        rc = L.od_ext_stroop_eval(int(variant), *args, b, e, int(n_trials), int(seed),
+                                  counts[b - begin:e - begin].ctypes.data_as(C.c_void_p),
+                                  net[b - begin:e - begin].ctypes.data_as(C.c_void_p))
+        if rc != 0:
+            raise ValueError("od_ext_stroop_eval rejected its arguments")
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return counts, net
+
+
+def ext_stroop_trial(variant, params, u_c, u_s, seed, unit, trial):
+    hit = np.zeros(2, np.int32)
+    st = np.zeros(2, np.uint32)
+    fn = lib().od_ext_stroop_trial_a if variant == 0 else lib().od_ext_stroop_trial_b
+    fn(_f32(params), float(u_c), float(u_s), int(seed), int(unit), int(trial), hit, st)
+    return (int(hit[0]), int(hit[1])), (int(st[0]), int(st[1]))

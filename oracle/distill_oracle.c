@@ -672,3 +672,107 @@ int od_pp_amr(const uint32_t n_levels[3], const float w[3], const float params[3
     free(levels); free(cost);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* spec/MODELS.md §10: Extended Stroop A / B (NEXT-3)                        */
+/* ------------------------------------------------------------------------ */
+enum { XS_GC, XS_GW, XS_TAU, XS_NH, XS_LAM, XS_AP, XS_GAM, XS_SIG, XS_DT, XS_Z, XS_ND, XS_R, XS_CRT };
+
+static void xs_inputs(const float P[13], float u_c, float u_s, uint32_t trial, float I[2], uint32_t* colour) {
+    uint32_t kind = trial % 3, c = (trial / 3) % 2;
+    int word = (kind == 0) ? (int)c : (kind == 1) ? (int)(1 - c) : -1;
+    float ic = FMUL(P[XS_GC], u_c);
+    float iw = FMUL(P[XS_GW], FSUB(1.0f, u_s));
+    for (int k = 0; k < 2; ++k) I[k] = FADD(((uint32_t)k == c) ? ic : 0.0f, (k == word) ? iw : 0.0f);
+    *colour = c;
+}
+
+/* version A: colour DDM first, single linear node, reward from successes */
+void od_ext_stroop_trial_a(const float P[13], float u_c, float u_s, uint64_t seed, uint64_t unit,
+                           uint32_t trial, int hit[2], uint32_t step[2]) {
+    float I[2]; uint32_t c;
+    xs_inputs(P, u_c, u_s, trial, I, &c);
+    float h[2] = { 0.0f, 0.0f };
+    for (uint32_t n = 0; n < (uint32_t)P[XS_NH]; ++n)
+        for (int k = 0; k < 2; ++k) h[k] = FFMA(P[XS_TAU], FSUB(I[k], h[k]), h[k]);
+    float E = FMUL(h[0], h[1]);
+    float A1 = FMUL(FSUB(h[c], h[1 - c]), P[XS_LAM]);
+    float A2 = FFMA(-P[XS_GAM], E, P[XS_AP]);
+    float nsd = FMUL(P[XS_SIG], FSQRT(P[XS_DT]));
+    float x1 = 0.0f, x2 = 0.0f;
+    hit[0] = hit[1] = 0; step[0] = step[1] = 0;
+    for (uint32_t n = 1; n <= (uint32_t)P[XS_ND]; ++n) {
+        float g[2];
+        od_normal_quad(seed, unit, 2ull * (n - 1), 2, g);
+        x1 = FFMA(nsd, g[0], FFMA(P[XS_DT], A1, x1));
+        x2 = FFMA(nsd, g[1], FFMA(P[XS_DT], A2, x2));
+        if (!hit[0]) { if (x1 >= P[XS_Z]) { hit[0] = 1; step[0] = n; } else if (x1 <= -P[XS_Z]) { hit[0] = 2; step[0] = n; } }
+        if (!hit[1]) { if (x2 >= P[XS_Z]) { hit[1] = 1; step[1] = n; } else if (x2 <= -P[XS_Z]) { hit[1] = 2; step[1] = n; } }
+    }
+}
+
+/* version B: pointing DDM declared first, two chained linear nodes, fma operands swapped */
+void od_ext_stroop_trial_b(const float P[13], float u_c, float u_s, uint64_t seed, uint64_t unit,
+                           uint32_t trial, int hit[2], uint32_t step[2]) {
+    float I[2]; uint32_t c;
+    xs_inputs(P, u_c, u_s, trial, I, &c);
+    float h[2] = { 0.0f, 0.0f };
+    for (uint32_t n = 0; n < (uint32_t)P[XS_NH]; ++n)
+        for (int k = 0; k < 2; ++k) h[k] = FFMA(P[XS_TAU], FSUB(I[k], h[k]), h[k]);
+    float E = FMUL(h[0], h[1]);
+    float A2p = FFMA(E, -P[XS_GAM], P[XS_AP]);                        /* pointing node */
+    float lin1 = FMUL(FSUB(h[c], h[1 - c]), FMUL(2.0f, P[XS_LAM]));  /* linear node 1: slope 2 lambda */
+    float A1p = FMUL(lin1, 0.5f);                                   /* linear node 2: slope 1/2 */
+    float nsd = FMUL(P[XS_SIG], FSQRT(P[XS_DT]));
+    float xp = 0.0f, xc = 0.0f;
+    int hp = 0, hc = 0; uint32_t sp = 0, sc = 0;
+    for (uint32_t n = 1; n <= (uint32_t)P[XS_ND]; ++n) {
+        float g[2];
+        od_normal_quad(seed, unit, 2ull * (n - 1), 2, g);
+        xp = FFMA(nsd, g[1], FFMA(P[XS_DT], A2p, xp));
+        xc = FFMA(nsd, g[0], FFMA(P[XS_DT], A1p, xc));
+        if (!hp) { if (xp >= P[XS_Z]) { hp = 1; sp = n; } else if (xp <= -P[XS_Z]) { hp = 2; sp = n; } }
+        if (!hc) { if (xc >= P[XS_Z]) { hc = 1; sc = n; } else if (xc <= -P[XS_Z]) { hc = 2; sc = n; } }
+    }
+    hit[0] = hc; hit[1] = hp; step[0] = sc; step[1] = sp;
+}
+
+float od_ext_stroop_value(int variant, const float P[13], const float w[2], float u_c, float u_s,
+                          uint32_t n_trials, uint64_t n_both, uint64_t n_undecided, uint64_t rt_sum) {
+    double T = (double)n_trials, N = (double)(uint32_t)P[XS_ND];
+    double v;
+    if (variant == 0) {
+        v = (double)P[XS_R] * (double)n_both / T;
+    } else {
+        uint64_t n_fail = (uint64_t)n_trials - n_both;
+        v = (double)P[XS_R] * (double)((uint64_t)n_trials - n_fail) / T;
+    }
+    v = v - (double)P[XS_CRT] * (double)P[XS_DT] * ((double)rt_sum + (double)n_undecided * N) / T;
+    v = v - ((double)w[0] * (double)u_c + (double)w[1] * (double)u_s);
+    return (float)v;
+}
+
+int od_ext_stroop_eval(int variant, const uint32_t n_levels[2], const float* levels, const float w[2],
+                       const float P[13], uint64_t begin, uint64_t end, uint32_t n_trials, uint64_t seed,
+                       uint64_t* counts, float* net) {
+    if (!n_levels || !levels || !w || !P || n_trials == 0 || end < begin) return -1;
+    uint64_t N = (uint64_t)n_levels[0] * n_levels[1];
+    if (N == 0 || end > N) return -1;
+    for (uint64_t i = begin; i < end; ++i) {
+        uint32_t k[2];
+        od_decode(i, 2, n_levels, k);
+        float uc = levels[k[0]], us = levels[n_levels[0] + k[1]];
+        uint64_t* c = counts + 3 * (i - begin);
+        c[0] = c[1] = c[2] = 0;
+        for (uint32_t j = 0; j < n_trials; ++j) {
+            int hit[2]; uint32_t st[2];
+            if (variant == 0) od_ext_stroop_trial_a(P, uc, us, seed, i * (uint64_t)n_trials + j, j, hit, st);
+            else od_ext_stroop_trial_b(P, uc, us, seed, i * (uint64_t)n_trials + j, j, hit, st);
+            if (hit[0] == 0 || hit[1] == 0) { c[1] += 1; continue; }
+            if (hit[0] == 1 && hit[1] == 1) c[0] += 1;
+            c[2] += st[0] > st[1] ? st[0] : st[1];
+        }
+        if (net) net[i - begin] = od_ext_stroop_value(variant, P, w, uc, us, n_trials, c[0], c[1], c[2]);
+    }
+    return 0;
+}

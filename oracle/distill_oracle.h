@@ -117,6 +117,19 @@ int od_pp_amr(const uint32_t n_levels[3], const float w[3], const float params[3
               const float lo0[3], const float hi0[3], uint32_t rounds, uint32_t n_samples, uint64_t seed,
               uint32_t invocation0, uint64_t* keys, float* boxes);
 
+/* ---- Extended Stroop A/B (spec/MODELS.md §10); variant 0 = A, 1 = B ----
+ * params = {g_c, g_w, tau, N_h, lambda, a_p, gamma, sigma_d, dt_d, z_d, N_d, reward, rt_cost}
+ * counts[3*(i-begin) + {0,1,2}] = {n_both, n_undecided, rt_sum} (overwritten); net = V */
+void od_ext_stroop_trial_a(const float P[13], float u_c, float u_s, uint64_t seed, uint64_t unit,
+                           uint32_t trial, int hit[2], uint32_t step[2]);
+void od_ext_stroop_trial_b(const float P[13], float u_c, float u_s, uint64_t seed, uint64_t unit,
+                           uint32_t trial, int hit[2], uint32_t step[2]);
+float od_ext_stroop_value(int variant, const float P[13], const float w[2], float u_c, float u_s,
+                          uint32_t n_trials, uint64_t n_both, uint64_t n_undecided, uint64_t rt_sum);
+int od_ext_stroop_eval(int variant, const uint32_t n_levels[2], const float* levels, const float w[2],
+                       const float P[13], uint64_t begin, uint64_t end, uint32_t n_trials, uint64_t seed,
+                       uint64_t* counts, float* net);
+
 /* ---- flop counting (only meaningful in the -DOD_COUNT_FLOPS build) ---- */
 unsigned long long od_flops_read(void);
 void od_flops_reset(void);

@@ -93,6 +93,7 @@ distill_status distill_load_model(const distill_model_desc* desc, int device, di
     uint32_t want_D, want_p;
     if (desc->kind == DISTILL_MODEL_PREDATOR_PREY) { want_D = 3; want_p = 3; }
     else if (desc->kind == DISTILL_MODEL_STROOP_LCA) { want_D = 2; want_p = 11; }
+    else if (desc->kind == DISTILL_MODEL_EXT_STROOP_A || desc->kind == DISTILL_MODEL_EXT_STROOP_B) { want_D = 2; want_p = 13; }
     else return fail(DISTILL_E_UNSUPPORTED, "load_model: unknown model kind %u", desc->kind);
     if (desc->n_signals != want_D)
         return fail(DISTILL_E_UNSUPPORTED, "load_model: kind %u needs %u signals, got %u", desc->kind, want_D,
@@ -112,6 +113,13 @@ distill_status distill_load_model(const distill_model_desc* desc, int device, di
         const float ns = desc->params[10];
         if (!(ns >= 1.0f) || ns != std::floor(ns) || ns > 1e7f)
             return fail(DISTILL_E_INVALID_ARG, "load_model: Stroop n_steps must be a positive integer");
+    }
+    if (desc->kind == DISTILL_MODEL_EXT_STROOP_A || desc->kind == DISTILL_MODEL_EXT_STROOP_B) {
+        for (int q : {3, 10}) {
+            const float ns = desc->params[q];
+            if (!(ns >= 0.0f) || ns != std::floor(ns) || ns > 1e7f || (q == 10 && ns < 1.0f))
+                return fail(DISTILL_E_INVALID_ARG, "load_model: Ext-Stroop N_h / N_d must be integers (N_d >= 1)");
+        }
     }
     int n_dev = 0;
     CUDA_TRY(cudaGetDeviceCount(&n_dev));
@@ -238,6 +246,62 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
     return DISTILL_OK;
 }
 
+extern "C++" {
+template <int VARIANT>
+void launch_ext_stroop_kernels(const ExtStroopArgs& p, uint32_t chunks, uint64_t count, bool sim, bool fin,
+                                      cudaStream_t st) {
+    if (sim)
+        for (uint64_t off = 0; off < count; off += 65535) {
+            const unsigned gy = (unsigned)std::min<uint64_t>(65535, count - off);
+            ext_stroop_sim_kernel<STROOP_BLOCK, VARIANT><<<dim3(chunks, gy), STROOP_BLOCK, 0, st>>>(p, (uint32_t)off);
+            g_launches++;
+        }
+    if (fin) {
+        ext_stroop_finalize_kernel<STROOP_BLOCK, VARIANT>
+            <<<(unsigned)((count + STROOP_BLOCK - 1) / STROOP_BLOCK), STROOP_BLOCK, 0, st>>>(p);
+        g_launches++;
+    }
+}
+}  // extern "C++"
+
+static distill_status launch_ext_stroop(distill_model* m, const distill_eval_args* a, cudaStream_t st) {
+    if (a->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Ext-Stroop): n_samples (trials) must be >= 1");
+    if (a->invocation != 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Ext-Stroop): invocation must be 0");
+    uint32_t tb = a->trial_begin, te = a->trial_end;
+    if (tb == 0 && te == 0) te = a->n_samples;
+    if (tb > te || te > a->n_samples) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Ext-Stroop): bad trial range");
+    const bool full = (tb == 0 && te == a->n_samples);
+    const uint64_t count = a->end - a->begin;
+    if (count == 0) return DISTILL_OK;
+    unsigned long long* counts = a->d_counts;
+    std::unique_lock<std::mutex> lock(m->scratch_mu, std::defer_lock);
+    if (!counts) {
+        lock.lock();
+        distill_status s = ensure_scratch(m, count * 3 * sizeof(unsigned long long));
+        if (s != DISTILL_OK) return s;
+        counts = (unsigned long long*)m->d_scratch;
+    }
+    CUDA_TRY(cudaMemsetAsync(counts, 0, count * 3 * sizeof(unsigned long long), st));
+    const float* P = m->params.data();
+    ExtStroopArgs p;
+    p.g_c = P[0]; p.g_w = P[1]; p.tau = P[2]; p.n_h = (uint32_t)P[3]; p.lam = P[4]; p.a_p = P[5]; p.gam = P[6];
+    p.sig = P[7]; p.dt = P[8]; p.z = P[9]; p.n_d = (uint32_t)P[10]; p.reward = P[11]; p.rt_cost = P[12];
+    p.w0 = m->w[0]; p.w1 = m->w[1]; p.L0 = m->L[0]; p.L1 = m->L[1];
+    p.n_trials = a->n_samples; p.trial_begin = tb; p.trial_end = te;
+    p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
+    p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
+    p.levels = m->d_levels; p.counts = counts; p.net = a->d_net; p.best = a->d_best;
+    const uint32_t tr = te - tb;
+    uint32_t chunks = std::max<uint32_t>(1, (tr + STROOP_BLOCK - 1) / STROOP_BLOCK);
+    const uint64_t want = (uint64_t)m->n_sm * 8 * 64;
+    if ((uint64_t)chunks * count > want) chunks = (uint32_t)std::max<uint64_t>(1, (want + count - 1) / count);
+    const bool fin = full && (a->d_net || a->d_best);
+    if (m->kind == DISTILL_MODEL_EXT_STROOP_A) launch_ext_stroop_kernels<0>(p, chunks, count, tr > 0, fin, st);
+    else launch_ext_stroop_kernels<1>(p, chunks, count, tr > 0, fin, st);
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
 distill_status distill_eval_grid(const distill_model* mc, const distill_eval_args* a, void* stream) {
     if (!mc || !a) return fail(DISTILL_E_INVALID_ARG, "eval_grid: NULL model/args");
     distill_model* m = const_cast<distill_model*>(mc);
@@ -251,7 +315,8 @@ distill_status distill_eval_grid(const distill_model* mc, const distill_eval_arg
     CUDA_TRY(cudaSetDevice(m->device));
     cudaStream_t st = (cudaStream_t)stream;
     if (m->kind == DISTILL_MODEL_PREDATOR_PREY) return launch_pp(m, a, st);
-    return launch_stroop(m, a, st);
+    if (m->kind == DISTILL_MODEL_STROOP_LCA) return launch_stroop(m, a, st);
+    return launch_ext_stroop(m, a, st);
 }
 
 distill_status distill_eval_grid_host(const distill_model* mc, const float* h_inputs, uint32_t n_inputs,

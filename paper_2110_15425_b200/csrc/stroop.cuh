@@ -117,4 +117,135 @@ __global__ void __launch_bounds__(BLOCK) stroop_finalize_kernel(const StroopArgs
     if (a.best) block_min_key_atomic<BLOCK>(k, a.best);
 }
 
+// ---------------------------------------------------------------- NEXT-3
+// Extended Stroop A/B (spec/MODELS.md §10): the Stroop pathway
+// front-end feeds two DDMs (colour naming, finger pointing) in one fused
+// per-trial simulation.  VARIANT 0 = version A, 1 = version B: B computes the
+// colour drift through two chained linear nodes, commutes the pointing fma and
+// steps the pointing DDM first — exact rewrites, so the outputs are identical.
+struct ExtStroopArgs {
+    float g_c, g_w, tau, lam, a_p, gam, sig, dt, z, reward, rt_cost;
+    uint32_t n_h, n_d;
+    float w0, w1;
+    uint32_t L0, L1, n_trials, trial_begin, trial_end, key0, key1, begin, count;
+    const float* __restrict__ levels;
+    unsigned long long* __restrict__ counts;   // [count][3] {n_both, n_undecided, rt_sum}
+    float* __restrict__ net;
+    key64_t* __restrict__ best;
+};
+
+__device__ __forceinline__ void ddm_latch(float x, float z, uint32_t n, int& hit, uint32_t& st) {
+    if (!hit) {
+        if (x >= z) { hit = 1; st = n; }
+        else if (x <= -z) { hit = 2; st = n; }
+    }
+}
+
+template <int BLOCK, int VARIANT>
+__global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopArgs a, uint32_t alloc_off) {
+    const uint32_t t_alloc = alloc_off + blockIdx.y;
+    const uint32_t i = a.begin + t_alloc;
+    const uint32_t k1 = i % a.L1, k0 = i / a.L1;
+    const float uc = __ldg(a.levels + k0), us = __ldg(a.levels + a.L0 + k1);
+    const float ic = __fmul_rn(a.g_c, uc);
+    const float iw = __fmul_rn(a.g_w, __fadd_rn(1.0f, -us));
+    const float nsd = __fmul_rn(a.sig, __fsqrt_rn(a.dt));
+    uint32_t n_both = 0, n_und = 0;
+    unsigned long long rts = 0;
+    for (uint32_t j = a.trial_begin + blockIdx.x * BLOCK + threadIdx.x; j < a.trial_end; j += gridDim.x * BLOCK) {
+        const uint32_t kind = j % 3, colour = (j / 3) & 1;
+        const int word = (kind == 0) ? (int)colour : (kind == 1) ? (int)(1 - colour) : -1;
+        const float I0 = __fadd_rn(colour == 0 ? ic : 0.0f, word == 0 ? iw : 0.0f);
+        const float I1 = __fadd_rn(colour == 1 ? ic : 0.0f, word == 1 ? iw : 0.0f);
+        float h0 = 0.0f, h1 = 0.0f;
+        for (uint32_t n = 0; n < a.n_h; ++n) {                 // pathway front-end
+            h0 = __fmaf_rn(a.tau, __fadd_rn(I0, -h0), h0);
+            h1 = __fmaf_rn(a.tau, __fadd_rn(I1, -h1), h1);
+        }
+        const float E = __fmul_rn(h0, h1);                     // decision (conflict) energy
+        const float hc = colour ? h1 : h0, hw = colour ? h0 : h1;
+        float A1, A2;
+        if (VARIANT == 0) {
+            A1 = __fmul_rn(__fadd_rn(hc, -hw), a.lam);
+            A2 = __fmaf_rn(-a.gam, E, a.a_p);
+        } else {
+            A2 = __fmaf_rn(E, -a.gam, a.a_p);
+            A1 = __fmul_rn(__fmul_rn(__fadd_rn(hc, -hw), __fmul_rn(2.0f, a.lam)), 0.5f);
+        }
+        const uint64_t unit = (uint64_t)i * a.n_trials + j;
+        PhiloxHoisted rng;
+        rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
+        float x1 = 0.0f, x2 = 0.0f;
+        int h1t = 0, h2t = 0;
+        uint32_t s1 = 0, s2 = 0;
+        const uint32_t nblk = (a.n_d + 1) >> 1;                // 2 steps (4 normals) per quad block
+        for (uint32_t kb = 0; kb < nblk; ++kb) {
+            const float4 g = normal_quad_h(rng, kb);
+#pragma unroll
+            for (int l = 0; l < 2; ++l) {
+                const uint32_t n = 2 * kb + l + 1;
+                if (n <= a.n_d) {
+                    const float g1 = l ? g.z : g.x, g2 = l ? g.w : g.y;
+                    if (VARIANT == 0) {
+                        x1 = __fmaf_rn(nsd, g1, __fmaf_rn(a.dt, A1, x1));
+                        x2 = __fmaf_rn(nsd, g2, __fmaf_rn(a.dt, A2, x2));
+                        ddm_latch(x1, a.z, n, h1t, s1);
+                        ddm_latch(x2, a.z, n, h2t, s2);
+                    } else {
+                        x2 = __fmaf_rn(nsd, g2, __fmaf_rn(a.dt, A2, x2));
+                        x1 = __fmaf_rn(nsd, g1, __fmaf_rn(a.dt, A1, x1));
+                        ddm_latch(x2, a.z, n, h2t, s2);
+                        ddm_latch(x1, a.z, n, h1t, s1);
+                    }
+                }
+            }
+        }
+        if (h1t == 0 || h2t == 0) { ++n_und; continue; }
+        n_both += (h1t == 1 && h2t == 1);
+        rts += s1 > s2 ? s1 : s2;
+    }
+    __shared__ unsigned long long s_red[3][BLOCK / 32];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        n_both += __shfl_xor_sync(0xFFFFFFFFu, n_both, off);
+        n_und += __shfl_xor_sync(0xFFFFFFFFu, n_und, off);
+        rts += __shfl_xor_sync(0xFFFFFFFFu, rts, off);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { s_red[0][wid] = n_both; s_red[1][wid] = n_und; s_red[2][wid] = rts; }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        unsigned long long v = 0;
+        for (int w = 0; w < BLOCK / 32; ++w) v += s_red[threadIdx.x][w];
+        if (v) atomicAdd(a.counts + 3ull * t_alloc + threadIdx.x, v);
+    }
+}
+
+template <int BLOCK, int VARIANT>
+__global__ void __launch_bounds__(BLOCK) ext_stroop_finalize_kernel(const ExtStroopArgs a) {
+    const uint32_t t = blockIdx.x * BLOCK + threadIdx.x;
+    key64_t k = KEY_INIT;
+    if (t < a.count) {
+        const uint32_t i = a.begin + t;
+        const uint32_t k1 = i % a.L1, k0 = i / a.L1;
+        const float uc = __ldg(a.levels + k0), us = __ldg(a.levels + a.L0 + k1);
+        const unsigned long long nb = a.counts[3ull * t], nu = a.counts[3ull * t + 1], rs = a.counts[3ull * t + 2];
+        const double T = (double)a.n_trials, N = (double)a.n_d;
+        double v;
+        if (VARIANT == 0) {
+            v = __ddiv_rn(__dmul_rn((double)a.reward, (double)nb), T);
+        } else {
+            const unsigned long long n_fail = (unsigned long long)a.n_trials - nb;
+            v = __ddiv_rn(__dmul_rn((double)a.reward, (double)((unsigned long long)a.n_trials - n_fail)), T);
+        }
+        v = __dsub_rn(v, __ddiv_rn(__dmul_rn(__dmul_rn((double)a.rt_cost, (double)a.dt),
+                                             __dadd_rn((double)rs, __dmul_rn((double)nu, N))), T));
+        v = __dsub_rn(v, __dadd_rn(__dmul_rn((double)a.w0, (double)uc), __dmul_rn((double)a.w1, (double)us)));
+        const float V = __double2float_rn(v);
+        if (a.net) a.net[t] = V;
+        k = make_key(-V, i);
+    }
+    if (a.best) block_min_key_atomic<BLOCK>(k, a.best);
+}
+
 }  // namespace distill

@@ -387,3 +387,28 @@ def test_pp_amr_bit_exact(D, orc, shape, S, R, lo, hi):
     w_keys, w_boxes = orc.pp_amr(cfg.n_levels, cfg.w, cfg.params, cfg.inputs, lo, hi, R, S, 21, invocation0=3)
     assert [int(k) & (2 ** 64 - 1) for k in keys.cpu().numpy()] == [int(k) for k in w_keys]
     assert np.array_equal(_bits(boxes.cpu().numpy()), _bits(w_boxes))
+
+
+def test_ext_stroop_a_b_bit_exact_and_identical(D, orc):
+    """NEXT-3: Extended Stroop versions A and B on the GPU — counts, V and key bit-exact
+    against the oracle, and A == B (the clone relation)."""
+    import torch
+    c = W.ext_stroop_small()
+    res = {}
+    for kind, variant in ((W.KIND_EXT_STROOP_A, 0), (W.KIND_EXT_STROOP_B, 1)):
+        m = D.load_model(kind, c.n_levels, c.levels, c.w, c.params, device=0)
+        cnt, net, key = _stroop_gpu(D, m, c, 0, c.n_alloc)
+        wc, wn = orc.ext_stroop_eval(variant, c.n_levels, c.levels, c.w, c.params, 0, c.n_alloc, c.n_trials,
+                                     c.seed, threads=8)
+        assert np.array_equal(cnt, wc)
+        assert np.array_equal(_bits(net), _bits(wn))
+        assert key == orc.argmax_net(wn)[0]
+        res[variant] = (cnt, net, key)
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(_bits(res[0][1]), _bits(res[1][1]))
+    # full-size control grid (1e4 allocations), sampled allocations, 1e4 trials
+    g = W.ext_stroop_grid()
+    m = D.load_model(W.KIND_EXT_STROOP_A, g.n_levels, g.levels, g.w, g.params, device=0)
+    for b in (0, 5050, 9998):
+        cnt, net, _ = _stroop_gpu(D, m, g, b, b + 2)
+        wc, wn = orc.ext_stroop_eval(0, g.n_levels, g.levels, g.w, g.params, b, b + 2, g.n_trials, g.seed)
+        assert np.array_equal(cnt, wc) and np.array_equal(_bits(net), _bits(wn))

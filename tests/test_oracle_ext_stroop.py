@@ -1,0 +1,61 @@
+"""Pins for the Extended Stroop A/B oracle (spec/MODELS.md §10)."""
+import numpy as np
+
+import workloads as W
+
+
+def test_versions_a_and_b_are_bit_identical(orc):
+    """'conceptually different but computationally equivalent'."""
+    c = W.ext_stroop_small()
+    ca, na = orc.ext_stroop_eval(0, c.n_levels, c.levels, c.w, c.params, 0, c.n_alloc, c.n_trials, c.seed, threads=8)
+    cb, nb = orc.ext_stroop_eval(1, c.n_levels, c.levels, c.w, c.params, 0, c.n_alloc, c.n_trials, c.seed, threads=8)
+    assert np.array_equal(ca, cb)
+    assert np.array_equal(na.view(np.uint32), nb.view(np.uint32))
+    # and each trial individually
+    for j in range(60):
+        assert orc.ext_stroop_trial(0, c.params, 0.7, 0.3, 5, 1000 + j, j) == \
+            orc.ext_stroop_trial(1, c.params, 0.7, 0.3, 5, 1000 + j, j)
+
+
+def _zero_noise():
+    P = W.EXT_STROOP_PARAMS.copy()
+    P[7] = 0.0
+    return P
+
+
+def test_zero_noise_decisions_follow_drift_signs_and_conflict_slows_pointing(orc):
+    P = _zero_noise()
+    # no word suppression: the stronger word wins the incongruent colour decision
+    (h_cong, st_cong) = orc.ext_stroop_trial(0, P, 1.0, 0.0, 1, 7, 0)      # congruent
+    (h_inc, st_inc) = orc.ext_stroop_trial(0, P, 1.0, 0.0, 1, 7, 1)        # incongruent
+    (h_neu, st_neu) = orc.ext_stroop_trial(0, P, 1.0, 0.0, 1, 7, 2)        # neutral
+    assert h_cong == (1, 1) and h_neu == (1, 1)
+    assert h_inc[0] == 2                      # colour DDM hits the lower (wrong) bound
+    # conflict energy E = h0 h1 > 0 only with both pathways active -> pointing is slower
+    (_, s_c) = orc.ext_stroop_trial(0, P, 1.0, 0.5, 1, 7, 0)
+    (h_i, s_i) = orc.ext_stroop_trial(0, P, 1.0, 0.5, 1, 7, 1)
+    (_, s_n) = orc.ext_stroop_trial(0, P, 1.0, 0.5, 1, 7, 2)
+    assert h_i[1] == 1 and s_i[1] > s_c[1]
+    assert s_c[1] == s_n[1]                   # E = 0 in both: same pointing drift
+
+
+def test_zero_noise_first_passage_is_binary32_accumulation(orc):
+    """Pointing DDM with zero noise: x_n = fma(dt, A2, x_{n-1}); first n with x >= z."""
+    P = _zero_noise()
+    (_, (_, n2)) = orc.ext_stroop_trial(0, P, 1.0, 0.0, 1, 3, 0)   # congruent: E = 0, A2 = a_p
+    a2, dt, z = np.float32(P[5]), np.float32(P[8]), np.float32(P[9])
+    x = np.float32(0)
+    want = None
+    for n in range(1, 1000):
+        x = np.float32(np.float64(dt) * np.float64(a2) + np.float64(x))   # exact product, one rounding
+        if x >= z:
+            want = n
+            break
+    assert n2 == want
+
+
+def test_counts_conserve(orc):
+    c = W.ext_stroop_small()
+    counts, _ = orc.ext_stroop_eval(0, c.n_levels, c.levels, c.w, c.params, 5, 17, c.n_trials, c.seed)
+    assert (counts[:, 0] + counts[:, 1] <= c.n_trials).all()
+    assert (counts[:, 2] <= (c.n_trials - counts[:, 1]) * int(c.params[10])).all()

@@ -165,3 +165,19 @@ def stroop_cfg4() -> StroopConfig:
 
 def stroop_small() -> StroopConfig:
     return StroopConfig("stroop_small_10x10x300", (10, 10), 300)
+
+
+# Extended Stroop A/B constants (reading R26; spec/MODELS.md §10):
+# g_c, g_w, tau, N_h, lambda, a_p, gamma, sigma_d, dt_d, z_d, N_d, reward, rt_cost
+EXT_STROOP_PARAMS = np.array([1.0, 1.5, 0.1, 30.0, 2.0, 1.2, 0.8, 1.0, 0.01, 0.5, 100.0, 1.0, 0.2], np.float32)
+KIND_EXT_STROOP_A = 3
+KIND_EXT_STROOP_B = 4
+
+
+def ext_stroop_small() -> StroopConfig:
+    return StroopConfig("ext_stroop_small_8x8x240", (8, 8), 240, params=EXT_STROOP_PARAMS.copy())
+
+
+def ext_stroop_grid() -> StroopConfig:
+    """Bench/next-row configuration: the cfg4 control grid (1e4 allocations) x 1e4 trials."""
+    return StroopConfig("ext_stroop_1e4x1e4", (100, 100), 10_000, params=EXT_STROOP_PARAMS.copy())
