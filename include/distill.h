@@ -158,9 +158,12 @@ distill_status distill_grid_size(const distill_model* model, uint64_t* n_alloc);
  * simulate + finalize kernels for Stroop.  Stream-ordered, asynchronous. */
 distill_status distill_eval_grid(const distill_model* model, const distill_eval_args* args, void* stream);
 
-/* Same evaluation from HOST buffers (the end-to-end call): copies, evaluates on
- * `stream`, copies V (if h_net) and the best key back, synchronises the stream.
- * Uses a library-owned device scratch area of the handle; NOT concurrent-safe per handle. */
+/* Same evaluation from HOST buffers (the end-to-end call): evaluates on `stream`,
+ * returns V in h_net (if non-NULL) and the best key in *h_best, synchronises the
+ * stream.  Pinned (cudaHostAlloc / page-locked, device-mapped) h_net is written by
+ * the kernel directly (zero-copy, overlapped with the computation); pageable h_net
+ * goes through a library-owned device scratch area and one copy.  Serialised per
+ * handle (the scratch area is shared). */
 distill_status distill_eval_grid_host(const distill_model* model, const float* h_inputs, uint32_t n_inputs,
                                       uint64_t begin, uint64_t end, uint32_t n_samples,
                                       uint32_t invocation, uint64_t seed,

@@ -412,3 +412,20 @@ def test_ext_stroop_a_b_bit_exact_and_identical(D, orc):
         cnt, net, _ = _stroop_gpu(D, m, g, b, b + 2)
         wc, wn = orc.ext_stroop_eval(0, g.n_levels, g.levels, g.w, g.params, b, b + 2, g.n_trials, g.seed)
         assert np.array_equal(cnt, wc) and np.array_equal(_bits(net), _bits(wn))
+
+
+def test_eval_grid_host_pinned_and_pageable(D, orc):
+    """The end-to-end host-buffer call: pinned output (zero-copy, written by the
+    kernel) and pageable output (device scratch + copy) both bit-exact."""
+    import torch
+    cfg = W.PPConfig("h", (17, 13, 11), 12)
+    m = _model(D, cfg)
+    want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 5, cfg.n_alloc, 12, cfg.seed)
+    k_or, _ = orc.argmax_net(-want, 5)
+    pinned = torch.empty(cfg.n_alloc, dtype=torch.float32, pin_memory=True).numpy()
+    pageable = np.empty(cfg.n_alloc, np.float32)
+    for out in (pinned, pageable):
+        key = D.eval_grid_host(m, cfg.inputs, 12, cfg.seed, 5, cfg.n_alloc, net_out=out[:cfg.n_alloc - 5])
+        assert key == k_or
+        assert np.array_equal(_bits(-out[:cfg.n_alloc - 5]), _bits(want))
+    assert D.eval_grid_host(m, cfg.inputs, 12, cfg.seed, 5, cfg.n_alloc) == k_or   # key only
