@@ -42,6 +42,11 @@ FLOPS_PER_SAMPLE = 274        # DESIGN.md §6, pinned by tests/test_oracle_pp.py
 FLOPS_PER_ALLOC = 13
 FLOPS_PER_CALL = 74
 FP32_LANES_PER_SM = 128       # FFMA lanes per SM (4 SMSP x 32), 2 flops per FMA
+FP32_PEAK_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12   # TFLOP/s (the extras' denominator)
+# DDM step = 1/4 quad block (2 Box-Muller pairs: 2 x 60 + 4 products = 124) + 2 fma = 35;
+# Stroop step = 1/2 quad block (62) + pathways 2 x 3 + rectified LCA 2 x 8 = 84.
+DDM_FLOPS_PER_STEP = 35
+STROOP_FLOPS_PER_STEP = 84
 
 
 def env_int(name, default):
@@ -360,9 +365,12 @@ def run_extras(D, torch, dev, rank, world, args):
         ms = float(t.item())
     nb = d.n_rt_bins
     up, lo = int(rh[:nb].sum()), int(rh[nb:2 * nb].sum())
+    tf = DDM_FLOPS_PER_STEP * d.n_trials * d.n_steps / (ms / 1e3) / 1e12
     out["ddm_cfg2"] = {"trials_per_s": d.n_trials / (ms / 1e3), "steps_per_s": d.n_trials * d.n_steps / (ms / 1e3),
                        "ms": ms, "error_rate": lo / max(1, up + lo),
-                       "mean_rt_s": (int(rs[0]) + int(rs[1])) / max(1, up + lo) * d.dt}
+                       "mean_rt_s": (int(rs[0]) + int(rs[1])) / max(1, up + lo) * d.dt,
+                       "algorithmic_tflops": tf, "frac_fp32_peak": tf / FP32_PEAK_NOMINAL,
+                       "flops_per_step": DDM_FLOPS_PER_STEP}
     # NEXT-1: closed-loop episode on the cfg3 grid (T grid searches + T step kernels, on the device)
     if world == 1:
         c3 = W.pp_cfg3()
@@ -404,8 +412,11 @@ def run_extras(D, torch, dev, rank, world, args):
             ms = float(t.item())
         from paper_2110_15425_b200.api import key_from_tensor
         cost, idx = D.key_decode(key_from_tensor(best))
+        tf = STROOP_FLOPS_PER_STEP * c.evals * c.n_steps / (ms / 1e3) / 1e12
         out["stroop_cfg4"] = {"evals_per_s": c.evals / (ms / 1e3),
                               "step_updates_per_s": c.evals * c.n_steps / (ms / 1e3), "ms": ms,
+                              "algorithmic_tflops": tf, "frac_fp32_peak": tf / FP32_PEAK_NOMINAL,
+                              "flops_per_step": STROOP_FLOPS_PER_STEP,
                               "best": {"index": idx, "u_c_level": idx // c.n_levels[1],
                                        "u_s_level": idx % c.n_levels[1], "net_value": -cost}}
     return out
