@@ -184,10 +184,15 @@ def run_ours(args):
     local = env_int("LOCAL_RANK", 0)
     if world != args.gpus:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    if args.device is not None:       # test mode: several ranks on one GPU (gloo only; timings meaningless)
+        local = args.device
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     def barrier():
         if world > 1:
@@ -431,6 +436,10 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stroop", action="store_true", help="also time one full cfg4 Stroop grid (~seconds)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collective backend for N > 1 (gloo only to exercise the multi-rank path on one GPU)")
+    ap.add_argument("--device", type=int, default=None,
+                    help="force every rank onto this CUDA device (multi-rank path test on one GPU, with gloo)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
