@@ -429,3 +429,28 @@ def test_eval_grid_host_pinned_and_pageable(D, orc):
         assert key == k_or
         assert np.array_equal(_bits(-out[:cfg.n_alloc - 5]), _bits(want))
     assert D.eval_grid_host(m, cfg.inputs, 12, cfg.seed, 5, cfg.n_alloc) == k_or   # key only
+
+
+def test_pp_cfg5_last_shard_of_eight(D, orc):
+    """cfg5 (200^3 = 8e6 allocations): the shard rank 7 of 8 owns in the N=8 run,
+    evaluated in the bench launch configuration — all 1e6 costs and the shard key
+    bit-exact against the oracle (threads over host cores)."""
+    import os
+    cfg = W.pp_cfg5()
+    m = _model(D, cfg)
+    b, e = D.shard_range(cfg.n_alloc, 7, 8)
+    C, key = _gpu_pp(D, m, cfg, b, e)
+    want = orc.pp_eval_threads(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, b, e, cfg.n_samples,
+                               cfg.seed, threads=os.cpu_count() or 8)
+    assert np.array_equal(_bits(C), _bits(want))
+    assert key == orc.argmax_net(-want, b)[0]
+
+
+def test_pp_large_odd_sample_count(D, orc):
+    """S = 1001 (odd, > 1000) on a ragged grid: the packed pair loop's odd tail."""
+    cfg = W.PPConfig("S", (3, 5, 7), 1001)
+    m = _model(D, cfg)
+    C, key = _gpu_pp(D, m, cfg)
+    want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc, 1001, cfg.seed)
+    assert np.array_equal(_bits(C), _bits(want))
+    assert key == orc.argmax_net(-want)[0]
