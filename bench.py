@@ -247,6 +247,12 @@ def run_ours(args):
     barrier()
     launches = D.launch_count() - launches0
     clocks = sampler.stop()
+    # effective SM clock right after the timed region (clock64 / globaltimer, one block per SM),
+    # run after a few more steps so the clock state is the loaded one
+    for _ in range(3):
+        step()
+    from paper_2110_15425_b200.api import sm_clock_mhz
+    clocks["sm_mhz_effective_probe"] = sm_clock_mhz(300)
     step_ms = [evs[s][0].elapsed_time(evs[s][3]) for s in range(K)]
     kern_ms = [evs[s][1].elapsed_time(evs[s][2]) for s in range(K)]
     ms_step = max_over_ranks(sum(step_ms) / K)
@@ -314,6 +320,8 @@ def run_ours(args):
             "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz (max clock)",
             "frac_at_measured_clock": (achieved / (n_sm * FP32_LANES_PER_SM * 2 * sm_load * 1e6 / 1e12)
                                        if sm_load else None),
+            "frac_at_probe_clock": achieved / (n_sm * FP32_LANES_PER_SM * 2 * clocks["sm_mhz_effective_probe"]
+                                               * 1e6 / 1e12),
             "kernel_share_of_step": ms_kern / ms_step}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

@@ -190,6 +190,12 @@ distill_status distill_key_decode(unsigned long long key, float* cost, uint64_t*
 /* DDM batch over trials [trial_begin, trial_end): histograms accumulated with atomics. */
 distill_status distill_ddm_batch(const distill_ddm_args* args, void* stream);
 
+/* Measurement utility: median effective SM clock (MHz) over one spinning block per
+ * SM for `micros` microseconds (clock64 ticks / globaltimer ns).  Synchronous.
+ * bench.py runs it right after the timed region to report the fraction of the
+ * FP32 peak at the clock the kernel actually ran at. */
+distill_status distill_sm_clock_probe(uint32_t micros, double* h_mhz, void* stream);
+
 /* Kernels launched by this library since load (all threads), for launch accounting. */
 uint64_t       distill_launch_count(void);
 

@@ -80,6 +80,7 @@ EXPORTS = {
     "distill_key_decode": (C.c_int, [C.c_uint64, C.POINTER(C.c_float), C.POINTER(C.c_uint64)]),
     "distill_ddm_batch": (C.c_int, [C.POINTER(DdmArgs), C.c_void_p]),
     "distill_launch_count": (C.c_uint64, []),
+    "distill_sm_clock_probe": (C.c_int, [C.c_uint32, C.POINTER(C.c_double), C.c_void_p]),
     "distill_pp_amr": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_void_p]),
     "distill_pp_episode": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_void_p]),
 }

@@ -188,6 +188,13 @@ def pp_amr(model: Model, inputs, lo, hi, rounds: int, n_samples: int, seed: int,
     return keys, boxes
 
 
+def sm_clock_mhz(micros: int = 200, stream=None) -> float:
+    """distill_sm_clock_probe: median effective SM clock in MHz (measurement utility)."""
+    v = C.c_double()
+    check(lib().distill_sm_clock_probe(int(micros), C.byref(v), _stream_handle(stream)))
+    return float(v.value)
+
+
 def launch_count() -> int:
     return int(lib().distill_launch_count())
 
@@ -198,4 +205,4 @@ def key_from_tensor(best) -> int:
 
 
 __all__ = ["KEY_INIT", "DistillError", "Model", "load_model", "eval_grid", "eval_grid_host", "argmax",
-           "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode", "argmax_ties", "pp_amr"]
+           "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode", "argmax_ties", "pp_amr", "sm_clock_mhz"]

@@ -485,6 +485,23 @@ distill_status distill_argmax_ties(const float* d_values, uint64_t n, uint64_t i
     return DISTILL_OK;
 }
 
+distill_status distill_sm_clock_probe(uint32_t micros, double* h_mhz, void* stream) {
+    if (!h_mhz || micros == 0) return fail(DISTILL_E_INVALID_ARG, "sm_clock_probe: NULL output / zero duration");
+    int dev = 0, n_sm = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    double* d = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&d, n_sm * sizeof(double), (cudaStream_t)stream));
+    sm_clock_probe_kernel<<<n_sm, 32, 0, (cudaStream_t)stream>>>(1000ull * micros, d);
+    std::vector<double> h(n_sm);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), d, n_sm * sizeof(double), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CUDA_TRY(cudaFreeAsync(d, (cudaStream_t)stream));
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    std::sort(h.begin(), h.end());
+    *h_mhz = h[n_sm / 2];
+    return DISTILL_OK;
+}
+
 distill_status distill_key_reset(unsigned long long* d_best, void* stream) {
     if (!d_best) return fail(DISTILL_E_INVALID_ARG, "key_reset: NULL");
     CUDA_TRY(cudaMemsetAsync(d_best, 0xFF, sizeof(unsigned long long), (cudaStream_t)stream));

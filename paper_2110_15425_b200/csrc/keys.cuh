@@ -105,4 +105,16 @@ __global__ void __launch_bounds__(BLOCK) argmax_ties_kernel(const float* __restr
     block_min_key_atomic<BLOCK>(k, tie);
 }
 
+// Measurement utility (not the hot path): effective SM clock.  One block per SM
+// spins for `ns` nanoseconds of globaltimer and reports clock64 ticks per ns.
+__global__ void sm_clock_probe_kernel(unsigned long long ns, double* __restrict__ mhz) {
+    if (threadIdx.x != 0) return;
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    const long long c0 = clock64();
+    do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1)); } while (t1 - t0 < ns);
+    const long long c1 = clock64();
+    mhz[blockIdx.x] = (double)(c1 - c0) / (double)(t1 - t0) * 1e3;
+}
+
 }  // namespace distill
