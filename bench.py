@@ -147,8 +147,9 @@ def run_reference(args):
     t = time.perf_counter()
     oracle.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, 300, cfg.n_samples, cfg.seed)
     per_alloc = (time.perf_counter() - t) / 300
-    # each step: a bounded slice, sized so warmup + steps take about two minutes
-    n = int(min(cfg.n_alloc, max(cores * 16, 120.0 * cores / max(1, args.steps + args.warmup) / per_alloc)))
+    # each step: a bounded slice, sized so warmup + steps take about `ref_budget_s` (default 2 min)
+    n = int(min(cfg.n_alloc, max(cores * 16, args.ref_budget_s * cores / max(1, args.steps + args.warmup)
+                                 / per_alloc)))
     times = []
     for s in range(args.warmup + args.steps):
         t = time.perf_counter()
@@ -426,6 +427,30 @@ def run_extras(D, torch, dev, rank, world, args):
         from paper_2110_15425_b200.api import key_from_tensor
         cost, idx = D.key_decode(key_from_tensor(best))
         tf = STROOP_FLOPS_PER_STEP * c.evals * c.n_steps / (ms / 1e3) / 1e12
+        # NEXT-3: Extended Stroop A on the cfg4 control grid, 1e4 trials per allocation
+        g = W.ext_stroop_grid()
+        mx = D.load_model(W.KIND_EXT_STROOP_A, g.n_levels, g.levels, g.w, g.params, device=dev.index)
+        xb, xe = D.shard_range(g.n_alloc, rank, world)
+        xnet = torch.empty(max(1, xe - xb), dtype=torch.float32, device=dev)
+        xbest = torch.empty(1, dtype=torch.int64, device=dev)
+        xcounts = torch.empty(3 * max(1, xe - xb), dtype=torch.int64, device=dev)
+        D.key_reset(xbest)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e2.record()
+        D.eval_grid(mx, None, g.n_trials, g.seed, xb, xe, net=xnet, best=xbest, counts=xcounts)
+        if world > 1:
+            D.best_allreduce(xbest)
+        e3.record()
+        torch.cuda.synchronize()
+        xms = e2.elapsed_time(e3)
+        if world > 1:
+            t = torch.tensor([xms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            xms = float(t.item())
+        xsteps = int(g.params[3]) + int(g.params[10])
+        out["ext_stroop_a"] = {"workload": g.name, "evals_per_s": g.evals / (xms / 1e3), "ms": xms,
+                               "trial_steps": xsteps, "best_index": key_from_tensor(xbest) & 0xFFFFFFFF}
         out["stroop_cfg4"] = {"evals_per_s": c.evals / (ms / 1e3),
                               "step_updates_per_s": c.evals * c.n_steps / (ms / 1e3), "ms": ms,
                               "algorithmic_tflops": tf, "frac_fp32_peak": tf / FP32_PEAK_NOMINAL,
@@ -443,7 +468,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--stroop", action="store_true", help="also time one full cfg4 Stroop grid (~seconds)")
+    ap.add_argument("--no-stroop", dest="stroop", action="store_false",
+                    help="skip the full cfg4 Stroop grid and the Extended Stroop grid in the extras (~1 s)")
+    ap.add_argument("--ref-budget-s", type=float, default=120.0,
+                    help="--impl reference: approximate wall seconds for warmup + steps")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="collective backend for N > 1 (gloo only to exercise the multi-rank path on one GPU)")
     ap.add_argument("--device", type=int, default=None,
