@@ -164,10 +164,14 @@ __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, floa
         }
         // a3: sextet packing -> three 2-D Box-Muller pairs (spec/RNG.md §6)
         F2 r0, c0, n0, r1, c1, n1, r2, c2, n2;
-        bm_polar2<false, false, false>(X.x, Y.x, X.w << 16, Y.w << 16, r0, c0, n0);
-        bm_polar2<false, false, false>(X.y, Y.y, X.w & 0xFFFF0000u, Y.w & 0xFFFF0000u, r1, c1, n1);
-        bm_polar2<SLN2, SRS2, SSC2>(X.z, Y.z, (X.x << 24) | ((X.y & 0xFFu) << 16),
-                                    (Y.x << 24) | ((Y.y & 0xFFu) << 16), r2, c2, n2);
+        {
+            const uint32_t wx0 = sextet_angle_word(X, 0), wy0 = sextet_angle_word(Y, 0);
+            const uint32_t wx1 = sextet_angle_word(X, 1), wy1 = sextet_angle_word(Y, 1);
+            const uint32_t wx2 = sextet_angle_word(X, 2), wy2 = sextet_angle_word(Y, 2);
+            bm_polar2_fs<false, false, false, 0x7FFF00u>(X.x, Y.x, wx0, wy0, wx0, wy0, r0, c0, n0);
+            bm_polar2_fs<false, false, false, 0x7FFF00u>(X.y, Y.y, wx1, wy1, wx1, wy1, r1, c1, n1);
+            bm_polar2_fs<SLN2, SRS2, SSC2, 0x7FFF00u>(X.z, Y.z, wx2, wy2, wx2, wy2, r2, c2, n2);
+        }
         // a4: Obs (p + sigma rad (cos, sin)) -> Action -> Objective
         using O = Ops<false>;
         const F2 q0 = O::mul(bc(s0), r0), q1 = O::mul(bc(s1), r1), q2 = O::mul(bc(s2), r2);

@@ -200,8 +200,12 @@ __device__ __forceinline__ F2 rsqrt2_from(F2 x, F2 mh) {
 // have their low 8 bits clear.  zc = rad * cos phi, zs = rad * sin phi per lane
 // (spec/RNG.md §2-§6).  SLN/SRS/SSC choose scalar lanes for the ln, sqrt and
 // sincos parts (scheduling only; identical results).
-template <bool SLN, bool SRS, bool SSC>
-__device__ __forceinline__ void bm_polar2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay, F2& rs, F2& cq, F2& sq) {
+// Angle given as (F, S): F holds the turn fraction bits of A >> 8 in MASK (bits 8..22
+// of A's bits 16..30 for 16-bit angles, 0..22 for 24-bit ones), S holds the half-turn
+// bit in bit 31.  The generic entry below derives them from an angle word A.
+template <bool SLN, bool SRS, bool SSC, uint32_t MASK>
+__device__ __forceinline__ void bm_polar2_fs(uint32_t Rx, uint32_t Ry, uint32_t Fx, uint32_t Fy, uint32_t Sx,
+                                             uint32_t Sy, F2& rs, F2& cq, F2& sq) {
     using L = Ops<SLN>;
     using Q = Ops<SSC>;
     // u1 = ((R >> 8) | 1) * 2^-24: convert the odd integer exactly and fold the
@@ -228,9 +232,12 @@ __device__ __forceinline__ void bm_polar2(uint32_t Rx, uint32_t Ry, uint32_t Ax,
     // product g = s * y0 equals y * (-2 y0) exactly, with -2 y0 and h = 0.5 y0
     // obtained by adjusting the seed's exponent bits.
     using G = Ops<SRS>;
-    const uint32_t shx = (__float_as_uint(y.x) + 0x80800000u) >> 1, shy = (__float_as_uint(y.y) + 0x80800000u) >> 1;
-    const F2 y0m2 = make_float2(__uint_as_float(0xDFB75A86u - shx), __uint_as_float(0xDFB75A86u - shy));  // -2 y0
-    F2 h = make_float2(__uint_as_float(0x5EB75A86u - shx), __uint_as_float(0x5EB75A86u - shy));           // y0 / 2
+    // y < 0, so bits(s) = bits(y) - 0x7F800000 and bits(s) >> 1 = (bits(y) >> 1) - 0x3FC00000
+    // exactly (even subtrahend, no wrap): the seed 0x5F375A86 - (bits(s) >> 1) and its
+    // exponent-adjusted forms fold the constant, leaving one shift and one subtract each.
+    const uint32_t shx = __float_as_uint(y.x) >> 1, shy = __float_as_uint(y.y) >> 1;
+    const F2 y0m2 = make_float2(__uint_as_float(0x1F775A86u - shx), __uint_as_float(0x1F775A86u - shy));  // -2 y0
+    F2 h = make_float2(__uint_as_float(0x9E775A86u - shx), __uint_as_float(0x9E775A86u - shy));           // y0 / 2
     F2 g = G::mul(y, y0m2);
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
@@ -240,8 +247,8 @@ __device__ __forceinline__ void bm_polar2(uint32_t Rx, uint32_t Ry, uint32_t Ax,
     }
     const F2 rad = G::fma(g, G::fma(neg2(g), h, bc(0.5f)), g);
     // sincos_spec: r from the angle bits, half-turn sign applied to rad
-    const F2 r = Q::add(make_float2(__uint_as_float(((Ax >> 8) & 0x7FFFFFu) | 0x3F800000u),
-                                    __uint_as_float(((Ay >> 8) & 0x7FFFFFu) | 0x3F800000u)),
+    const F2 r = Q::add(make_float2(__uint_as_float((Fx & MASK) | 0x3F800000u),
+                                    __uint_as_float((Fy & MASK) | 0x3F800000u)),
                         bc(-1.5f));
     const F2 t = Q::mul(r, r);
     const F2 S = Q::fma(Q::fma(Q::fma(Q::fma(bc(D_S4), t, bc(D_S3)), t, bc(D_S2)), t, bc(D_S1)), t, bc(D_S0));
@@ -249,8 +256,24 @@ __device__ __forceinline__ void bm_polar2(uint32_t Rx, uint32_t Ry, uint32_t Ax,
     cq = Q::fma(C, t, bc(1.0f));
     sq = Q::mul(S, r);
     // half-turn sign on the radius: (-rad) * c == -(rad * c) bit for bit
-    rs = make_float2(__uint_as_float(__float_as_uint(rad.x) ^ (Ax & 0x80000000u)),
-                     __uint_as_float(__float_as_uint(rad.y) ^ (Ay & 0x80000000u)));
+    rs = make_float2(__uint_as_float(__float_as_uint(rad.x) ^ (Sx & 0x80000000u)),
+                     __uint_as_float(__float_as_uint(rad.y) ^ (Sy & 0x80000000u)));
+}
+
+// Generic: angle words A with their low 8 bits clear.
+template <bool SLN, bool SRS, bool SSC>
+__device__ __forceinline__ void bm_polar2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay, F2& rs, F2& cq, F2& sq) {
+    bm_polar2_fs<SLN, SRS, SSC, 0x7FFFFFu>(Rx, Ry, Ax >> 8, Ay >> 8, Ax, Ay, rs, cq, sq);
+}
+
+// Sextet packing (spec/RNG.md §6) for entity e of a Philox block X: one byte permute
+// yields a word whose bits 8..22 are the spec angle word's bits 16..30 and whose
+// bit 31 is its half-turn bit (A0 = X3 << 16, A1 = X3 & 0xFFFF0000,
+// A2 = (X0 << 24) | ((X1 & 0xFF) << 16)).
+__device__ __forceinline__ uint32_t sextet_angle_word(const uint4& X, int e) {
+    return e == 0 ? __byte_perm(X.w, 0u, 0x1100u)        // bytes: -, X3.b0, X3.b1, X3.b1
+         : e == 1 ? __byte_perm(X.w, 0u, 0x3320u)        // bytes: -, X3.b2, X3.b3, X3.b3
+                  : __byte_perm(X.y, X.x, 0x4400u);      // bytes: X1.b0, X1.b0, X0.b0, X0.b0
 }
 
 // ... and as normals zc = rad cos phi, zs = rad sin phi.
