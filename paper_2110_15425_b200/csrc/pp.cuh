@@ -106,7 +106,7 @@ enum : int {
 #define DISTILL_PP_MASK 0
 #endif
 #ifndef DISTILL_PP_MINB
-#define DISTILL_PP_MINB 0
+#define DISTILL_PP_MINB 7
 #endif
 
 // Full evaluation of allocation i (a1-a8): returns the cost C.
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs 
 // Persistent variant: a fixed grid of resident blocks pulls BLOCK-allocation
 // chunks from a device counter (zeroed by the caller before the launch), so
 // the last wave has no idle SMs; keys are min-combined per block across chunks.
-template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false>
+template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false, bool EVEN = false>
 __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_persistent_kernel(const PPArgs a,
                                                                                unsigned int* __restrict__ counter) {
     __shared__ unsigned int s_chunk;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_persistent_kernel(co
         const uint32_t tid = c * BLOCK + threadIdx.x;
         if (tid < a.count) {
             const uint32_t i = a.begin + tid;
-            const float C = pp_eval_alloc<MASK, PIPE>(a, i, ustar);
+            const float C = pp_eval_alloc<MASK, PIPE, EVEN>(a, i, ustar);
             if (a.net) a.net[tid] = -C;
             const key64_t k = make_key(C, i);
             key = k < key ? k : key;

@@ -14,9 +14,9 @@ void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_re
     cudaFuncAttributes fa;
     unsigned grid;
     if (PERS) {
-        cudaFuncGetAttributes(&fa, pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE>);
+        cudaFuncGetAttributes(&fa, pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE, EVEN>);
         int per_sm = 0, n_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE, EVEN>,
                                                       BLOCK, 0);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
         grid = per_sm * n_sm;
@@ -32,7 +32,7 @@ void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_re
         cudaEventRecord(e0);
         if (PERS) {
             cudaMemsetAsync(g_counter, 0, 4);
-            pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE><<<grid, BLOCK>>>(a, g_counter);
+            pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE, EVEN><<<grid, BLOCK>>>(a, g_counter);
         } else {
             pp_eval_grid_kernel<BLOCK, MASK, MINB, PIPE, EVEN><<<grid, BLOCK>>>(a);
         }
@@ -69,12 +69,20 @@ int main() {
     run<256, 0, 0>("packed (ref)", a, ref.data(), 0, true);
     key64_t rk; cudaMemcpy(&rk, a.best, 8, cudaMemcpyDeviceToHost);
 #define V(B, M, N, P, Q, E, name) run<B, M, N, P, Q, E>(name, a, ref.data(), rk, false)
-    V(128, 0, 0, false, false, false, "b128");
     V(128, 0, 0, false, false, true, "b128 even");
-    V(256, 0, 0, false, false, true, "b256 even");
-    V(128, 0, 0, false, true, false, "persistent b128");
-    V(64, 0, 0, false, false, true, "b64 even");
-    V(128, 1, 0, false, false, true, "b128 even obj scalar");
+    V(128, 0, 6, false, false, true, "b128 even minb6");
+    V(128, 0, 7, false, false, true, "b128 even minb7");
+    V(128, 0, 8, false, false, true, "b128 even minb8");
+    V(128, 0, 9, false, false, true, "b128 even minb9");
+    V(128, 0, 10, false, false, true, "b128 even minb10");
+    V(128, 0, 12, false, false, true, "b128 even minb12");
+    V(128, 0, 8, false, true, true, "b128 even minb8 pers");
+    V(128, 0, 7, false, true, true, "b128 even minb7 pers");
+    V(64, 0, 16, false, false, true, "b64 even minb16");
+    V(64, 0, 16, false, true, true, "b64 even minb16 pers");
+    V(256, 0, 4, false, false, true, "b256 even minb4");
+    V(256, 0, 4, false, true, true, "b256 even minb4 pers");
+    V(128, 0, 8, true, false, true, "b128 even minb8 pipe");
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
