@@ -21,8 +21,8 @@ struct DDMArgs {
     unsigned long long* __restrict__ x_hist;   // [nx+2]
 };
 
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) ddm_batch_kernel(const DDMArgs a) {
+template <int BLOCK, int MINB = 0>
+__global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a) {
     extern __shared__ uint32_t s_hist[];  // [2*nb+1] rt bins then [nx+2] x bins
     const uint32_t n_rt = 2 * a.n_rt_bins + 1, n_x = a.n_x_bins + 2, n_all = n_rt + n_x;
     for (uint32_t b = threadIdx.x; b < n_all; b += BLOCK) s_hist[b] = 0;

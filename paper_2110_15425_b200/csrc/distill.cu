@@ -47,7 +47,8 @@ distill_status fail(distill_status s, const char* fmt, ...) {
 
 constexpr int PP_BLOCK = 128;
 constexpr int ARGMAX_BLOCK = 256;
-constexpr int DDM_BLOCK = 256;
+constexpr int DDM_BLOCK = 128;
+constexpr int DDM_MINB = 8;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt)
 constexpr int STROOP_BLOCK = 256;
 
 }  // namespace
@@ -537,7 +538,7 @@ distill_status distill_ddm_batch(const distill_ddm_args* a, void* stream) {
     CUDA_TRY(cudaGetDevice(&dev));
     CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     if (smem > 48 * 1024)
-        CUDA_TRY(cudaFuncSetAttribute(ddm_batch_kernel<DDM_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_TRY(cudaFuncSetAttribute(ddm_batch_kernel<DDM_BLOCK, DDM_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     DDMArgs p;
     p.drift = a->drift; p.noise = a->noise; p.threshold = a->threshold; p.x0 = a->x0; p.dt = a->dt;
@@ -548,7 +549,7 @@ distill_status distill_ddm_batch(const distill_ddm_args* a, void* stream) {
     p.rt_hist = a->d_rt_hist; p.rt_sum = a->d_rt_sum; p.x_hist = a->d_x_hist;
     const uint64_t need = (n + DDM_BLOCK - 1) / DDM_BLOCK;
     const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)n_sm * 1024);
-    ddm_batch_kernel<DDM_BLOCK><<<grid, DDM_BLOCK, smem, (cudaStream_t)stream>>>(p);
+    ddm_batch_kernel<DDM_BLOCK, DDM_MINB><<<grid, DDM_BLOCK, smem, (cudaStream_t)stream>>>(p);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;

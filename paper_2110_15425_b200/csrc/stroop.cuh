@@ -27,8 +27,8 @@ struct StroopArgs {
     key64_t* __restrict__ best;
 };
 
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) stroop_sim_kernel(const StroopArgs a, uint32_t alloc_off) {
+template <int BLOCK, int MINB = 0>
+__global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArgs a, uint32_t alloc_off) {
     const uint32_t t_alloc = alloc_off + blockIdx.y;           // index within [0, count)
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
