@@ -84,8 +84,9 @@ typedef struct {
     uint64_t seed;               /* Philox key */
     float* d_net;                /* device [end-begin] or NULL: net value V = -C per allocation       */
     unsigned long long* d_best;  /* device [1] or NULL: atomicMin of key(C_i, i) (spec/MODELS.md §3)  */
-    unsigned long long* d_counts;/* Stroop only, device [(end-begin)*3] u64 or NULL (library scratch):
-                                    {n_correct, n_undecided, rt_sum}; overwritten                     */
+    unsigned long long* d_counts;/* Stroop kinds: REQUIRED device [(end-begin)*3] u64, 8-B aligned:
+                                    {n_correct (n_both for Ext-Stroop), n_undecided, rt_sum}; overwritten.
+                                    PP: unused (NULL)                                                  */
     uint32_t trial_begin, trial_end; /* Stroop: simulate trials [trial_begin, trial_end) only; (0,0) = all.
                                     d_net/d_best are produced only when the range is all T trials.    */
 } distill_eval_args;

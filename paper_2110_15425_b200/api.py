@@ -86,6 +86,9 @@ def eval_grid(model: Model, inputs, n_samples: int, seed: int, begin: int = 0, e
     a.n_samples, a.invocation, a.seed = int(n_samples), int(invocation), int(seed) & (2 ** 64 - 1)
     a.d_net = _dev_ptr(net, "net", n)
     a.d_best = _dev_ptr(best, "best", 1)
+    if counts is None and model.kind != _abi.MODEL_PREDATOR_PREY:
+        import torch
+        counts = torch.empty(3 * max(n, 1), dtype=torch.int64, device=torch.device("cuda", model.device))
     a.d_counts = _dev_ptr(counts, "counts", 3 * n)
     a.trial_begin, a.trial_end = int(trial_range[0]), int(trial_range[1])
     check(lib().distill_eval_grid(model.handle, C.byref(a), _stream_handle(stream)))

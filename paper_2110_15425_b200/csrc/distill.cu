@@ -62,7 +62,7 @@ struct distill_model {
     std::vector<float> params;
     float* d_levels = nullptr;      // device RO block
     int n_sm = 148;
-    // scratch for the host-buffer entry and Stroop counts (lazily grown)
+    // device scratch of the synchronous host-buffer entry (lazily grown, guarded by the mutex)
     std::mutex scratch_mu;
     void* d_scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -203,14 +203,12 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
     if (count == 0) return DISTILL_OK;
     if (a->n_samples > 0 && (uint64_t)m->n_alloc * a->n_samples >= (1ull << 63))
         return fail(DISTILL_E_OVERFLOW, "eval_grid(Stroop): RNG unit id overflow");
+    // Caller-owned counts: the integer outcomes live between the simulate and
+    // finalize kernels, and a shared library scratch area would race between
+    // streams evaluating the same handle concurrently.
     unsigned long long* counts = a->d_counts;
-    std::unique_lock<std::mutex> lock(m->scratch_mu, std::defer_lock);
-    if (!counts) {
-        lock.lock();
-        distill_status s = ensure_scratch(m, count * 3 * sizeof(unsigned long long));
-        if (s != DISTILL_OK) return s;
-        counts = (unsigned long long*)m->d_scratch;
-    }
+    if (!counts) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop kinds): d_counts is required");
+    if (reinterpret_cast<uintptr_t>(counts) & 7u) return fail(DISTILL_E_INVALID_ARG, "eval_grid: d_counts must be 8-byte aligned");
     CUDA_TRY(cudaMemsetAsync(counts, 0, count * 3 * sizeof(unsigned long long), st));
     StroopArgs p;
     const float* P = m->params.data();
@@ -274,14 +272,12 @@ static distill_status launch_ext_stroop(distill_model* m, const distill_eval_arg
     const bool full = (tb == 0 && te == a->n_samples);
     const uint64_t count = a->end - a->begin;
     if (count == 0) return DISTILL_OK;
+    // Caller-owned counts: the integer outcomes live between the simulate and
+    // finalize kernels, and a shared library scratch area would race between
+    // streams evaluating the same handle concurrently.
     unsigned long long* counts = a->d_counts;
-    std::unique_lock<std::mutex> lock(m->scratch_mu, std::defer_lock);
-    if (!counts) {
-        lock.lock();
-        distill_status s = ensure_scratch(m, count * 3 * sizeof(unsigned long long));
-        if (s != DISTILL_OK) return s;
-        counts = (unsigned long long*)m->d_scratch;
-    }
+    if (!counts) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop kinds): d_counts is required");
+    if (reinterpret_cast<uintptr_t>(counts) & 7u) return fail(DISTILL_E_INVALID_ARG, "eval_grid: d_counts must be 8-byte aligned");
     CUDA_TRY(cudaMemsetAsync(counts, 0, count * 3 * sizeof(unsigned long long), st));
     const float* P = m->params.data();
     ExtStroopArgs p;
