@@ -99,3 +99,20 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(import\s+oracle|from\s+oracle|liboracle|distill_oracle|\bod_[a-z])", src), f
+
+
+def test_next_row_entry_points_validate_before_cuda(abi):
+    """NEXT-1/2/4 entry points reject bad arguments with E_INVALID_ARG and never abort."""
+    import ctypes as C
+    L = abi.lib()
+    e = abi.EpisodeArgs()
+    assert L.distill_pp_episode(None, C.byref(e), None) == abi.E_INVALID_ARG
+    g = abi.AmrArgs()
+    assert L.distill_pp_amr(None, C.byref(g), None) == abi.E_INVALID_ARG
+    assert L.distill_argmax_ties(None, 5, 0, 0, 0, None, None, None) == abi.E_INVALID_ARG
+    # empty input is a no-op (no CUDA call needed)
+    dummy = C.c_uint64(0)
+    assert L.distill_argmax_ties(None, 0, 0, 0, 0, C.addressof(dummy), C.addressof(dummy), None) == abi.OK
+    assert L.distill_argmax(None, 0, 0, C.addressof(dummy), None) == abi.OK
+    assert L.distill_argmax(None, 1, 0xFFFFFFFF, C.addressof(dummy), None) == abi.E_INVALID_ARG
+    assert L.distill_sm_clock_probe(0, None, None) == abi.E_INVALID_ARG

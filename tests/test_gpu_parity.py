@@ -454,3 +454,46 @@ def test_pp_large_odd_sample_count(D, orc):
     want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc, 1001, cfg.seed)
     assert np.array_equal(_bits(C), _bits(want))
     assert key == orc.argmax_net(-want)[0]
+
+
+def test_ddm_cfg2_endpoint_chi_square(D, orc):
+    """cfg2 at full size: the Euler endpoint x_N is exactly N(x0 + A N dt, sigma^2 N dt)
+    (Gaussian increments); chi-square of the 128-bin histogram (+ tails) against it."""
+    import math
+    from scipy import stats
+    d = W.ddm_cfg2()
+    _, _, xh = _ddm_gpu(D, d, 0, d.n_trials, d.seed)
+    mu, sd = d.x0 + d.drift * d.n_steps * d.dt, d.noise * math.sqrt(d.n_steps * d.dt)
+    edges = np.linspace(np.float32(d.x_lo), np.float32(d.x_hi), d.n_x_bins + 1)
+    cdf = stats.norm.cdf((edges - mu) / sd)
+    p = np.concatenate([[cdf[0]], np.diff(cdf), [1 - cdf[-1]]])
+    obs = xh.astype(np.float64)
+    expct = p * d.n_trials
+    keep = expct > 20
+    chi2 = float(((obs[keep] - expct[keep]) ** 2 / expct[keep]).sum())
+    dof = int(keep.sum()) - 1
+    assert stats.chi2.sf(chi2, dof) > 1e-4, (chi2, dof)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 200), (1, 50, 1), (200, 1, 1)])
+def test_pp_degenerate_single_level_signals(D, orc, shape):
+    cfg = W.PPConfig("deg", shape, 6)
+    m = _model(D, cfg)
+    C, key = _gpu_pp(D, m, cfg)
+    want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc, 6, cfg.seed)
+    assert np.array_equal(_bits(C), _bits(want))
+    for i in (0, cfg.n_alloc - 1):      # one-allocation shards at both ends
+        c1, k1 = _gpu_pp(D, m, cfg, i, i + 1)
+        assert _bits(c1)[0] == _bits(want[i:i + 1])[0] and k1 == orc.key(float(want[i]), i)
+
+
+def test_argmax_ties_all_nan_and_empty(D, orc):
+    import torch
+    t = torch.full((16,), float("nan"), device="cuda")
+    best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.argmax(t, 0, best)
+    tie = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.argmax_ties(t, 0, 1, 0, best, tie)
+    D.argmax_ties(t[:0], 0, 1, 0, best, tie)
+    torch.cuda.synchronize()
+    assert int(tie.item()) == -1          # KEY_INIT: nothing can win
