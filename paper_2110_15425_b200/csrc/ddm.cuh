@@ -41,15 +41,40 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
         rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
         float x = a.x0;
         uint32_t st = 0, ch = 2;
-        const uint32_t nblk = (a.n_steps + 3) >> 2;
-        for (uint32_t kb = 0; kb < nblk; ++kb) {
+        // Latch test: (x >= z) || (x <= -z)  <=>  |x| >= z for every z and
+        // non-NaN x (NaN fails both), so one max-|x| test per quad of steps
+        // (ALU pipe) finds the quads that hold a first passage; the rare quad
+        // that does is resolved step by step with the spec's compares.
+        const uint32_t nfull = a.n_steps >> 2;
+        const float dtA = a.dt, drift = a.drift;
+        for (uint32_t kb = 0; kb < nfull; ++kb) {
             const float4 g = normal_quad_h(rng, kb);
+            float xs[4];
+            x = __fmaf_rn(nsd, g.x, __fmaf_rn(dtA, drift, x)); xs[0] = x;
+            x = __fmaf_rn(nsd, g.y, __fmaf_rn(dtA, drift, x)); xs[1] = x;
+            x = __fmaf_rn(nsd, g.z, __fmaf_rn(dtA, drift, x)); xs[2] = x;
+            x = __fmaf_rn(nsd, g.w, __fmaf_rn(dtA, drift, x)); xs[3] = x;
+            if (st == 0) {
+                const float m = fmaxf(fmaxf(fabsf(xs[0]), fabsf(xs[1])), fmaxf(fabsf(xs[2]), fabsf(xs[3])));
+                if (m >= z) {
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) {
+                        if (st == 0) {
+                            if (xs[l] >= z) { st = 4 * kb + l + 1; ch = 0; }
+                            else if (xs[l] <= nz) { st = 4 * kb + l + 1; ch = 1; }
+                        }
+                    }
+                }
+            }
+        }
+        if (a.n_steps & 3u) {  // ragged last quad
+            const float4 g = normal_quad_h(rng, nfull);
             const float gg[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const uint32_t n = 4 * kb + l + 1;
+            for (int l = 0; l < 3; ++l) {
+                const uint32_t n = 4 * nfull + l + 1;
                 if (n <= a.n_steps) {
-                    x = __fmaf_rn(nsd, gg[l], __fmaf_rn(a.dt, a.drift, x));
+                    x = __fmaf_rn(nsd, gg[l], __fmaf_rn(dtA, drift, x));
                     if (st == 0) {
                         if (x >= z) { st = n; ch = 0; }
                         else if (x <= nz) { st = n; ch = 1; }
