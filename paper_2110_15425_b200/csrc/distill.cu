@@ -48,7 +48,7 @@ distill_status fail(distill_status s, const char* fmt, ...) {
 constexpr int PP_BLOCK = 128;
 constexpr int ARGMAX_BLOCK = 256;
 constexpr int DDM_BLOCK = 128;
-constexpr int DDM_MINB = 8;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt)
+constexpr int DDM_MINB = 0;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt)
 constexpr int STROOP_BLOCK = 256;
 
 }  // namespace

@@ -27,6 +27,18 @@ struct StroopArgs {
     key64_t* __restrict__ best;
 };
 
+// One LCA step of both response units (spec/MODELS.md §6 loop body; the old
+// x of both units feeds both q's).
+__device__ __forceinline__ void lca_step(const StroopArgs& a, float I0, float I1, float nleak, float ninh, float nsd,
+                                         float g0, float g1, float& h0, float& h1, float& x0, float& x1) {
+    h0 = __fmaf_rn(a.tau, __fadd_rn(I0, -h0), h0);
+    h1 = __fmaf_rn(a.tau, __fadd_rn(I1, -h1), h1);
+    const float q0 = __fmaf_rn(ninh, x1, __fmaf_rn(nleak, x0, h0));
+    const float q1 = __fmaf_rn(ninh, x0, __fmaf_rn(nleak, x1, h1));
+    x0 = fmaxf(__fmaf_rn(nsd, g0, __fmaf_rn(a.dt, q0, x0)), 0.0f);
+    x1 = fmaxf(__fmaf_rn(nsd, g1, __fmaf_rn(a.dt, q1, x1)), 0.0f);
+}
+
 template <int BLOCK, int MINB = 0>
 __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArgs a, uint32_t alloc_off) {
     const uint32_t t_alloc = alloc_off + blockIdx.y;           // index within [0, count)
@@ -52,27 +64,31 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
         float h0 = 0.f, h1 = 0.f, x0 = 0.f, x1 = 0.f;
         int resp = -1;
         uint32_t st = 0;
-        const uint32_t nblk = (a.n_steps + 1) >> 1;   // 2 steps per quad block
-        for (uint32_t kb = 0; kb < nblk; ++kb) {
+        // x_k >= 0 after the rectification (fmaxf(NaN, 0) = 0 as well), so
+        // "x0 >= θ or x1 >= θ" at either step of a quad block <=> the max of
+        // the four states >= θ: one test per two steps; the rare block that
+        // passes is resolved in the spec's order.
+        const uint32_t nfull = a.n_steps >> 1;    // 2 steps per quad block
+        for (uint32_t kb = 0; kb < nfull; ++kb) {
             const float4 g = normal_quad_h(rng, kb);
-#pragma unroll
-            for (int l = 0; l < 2; ++l) {
-                const uint32_t n = 2 * kb + l + 1;
-                if (n <= a.n_steps) {
-                    h0 = __fmaf_rn(a.tau, __fadd_rn(I0, -h0), h0);
-                    h1 = __fmaf_rn(a.tau, __fadd_rn(I1, -h1), h1);
-                    const float g0 = l ? g.z : g.x, g1 = l ? g.w : g.y;
-                    const float q0 = __fmaf_rn(ninh, x1, __fmaf_rn(nleak, x0, h0));
-                    const float q1 = __fmaf_rn(ninh, x0, __fmaf_rn(nleak, x1, h1));
-                    const float y0 = __fmaf_rn(nsd, g0, __fmaf_rn(a.dt, q0, x0));
-                    const float y1 = __fmaf_rn(nsd, g1, __fmaf_rn(a.dt, q1, x1));
-                    x0 = fmaxf(y0, 0.0f);
-                    x1 = fmaxf(y1, 0.0f);
-                    if (resp < 0) {
-                        if (x0 >= a.thr) { resp = 0; st = n; }
-                        else if (x1 >= a.thr) { resp = 1; st = n; }
-                    }
-                }
+            float xa0, xa1;
+            lca_step(a, I0, I1, nleak, ninh, nsd, g.x, g.y, h0, h1, x0, x1);
+            xa0 = x0; xa1 = x1;
+            lca_step(a, I0, I1, nleak, ninh, nsd, g.z, g.w, h0, h1, x0, x1);
+            if (resp < 0 && fmaxf(fmaxf(xa0, xa1), fmaxf(x0, x1)) >= a.thr) {
+                const uint32_t n = 2 * kb + 1;
+                if (xa0 >= a.thr) { resp = 0; st = n; }
+                else if (xa1 >= a.thr) { resp = 1; st = n; }
+                else if (x0 >= a.thr) { resp = 0; st = n + 1; }
+                else { resp = 1; st = n + 1; }
+            }
+        }
+        if (a.n_steps & 1u) {  // ragged last step
+            const float4 g = normal_quad_h(rng, nfull);
+            lca_step(a, I0, I1, nleak, ninh, nsd, g.x, g.y, h0, h1, x0, x1);
+            if (resp < 0) {
+                if (x0 >= a.thr) { resp = 0; st = a.n_steps; }
+                else if (x1 >= a.thr) { resp = 1; st = a.n_steps; }
             }
         }
         if (resp < 0) ++n_und;
