@@ -21,7 +21,7 @@ struct DDMArgs {
     unsigned long long* __restrict__ x_hist;   // [nx+2]
 };
 
-template <int BLOCK, int MINB = 0>
+template <int BLOCK, int MINB = 0, int BMV = 0>
 __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a) {
     extern __shared__ uint32_t s_hist[];  // [2*nb+1] rt bins then [nx+2] x bins
     const uint32_t n_rt = 2 * a.n_rt_bins + 1, n_x = a.n_x_bins + 2, n_all = n_rt + n_x;
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
         const uint32_t nfull = a.n_steps >> 2;
         const float dtA = a.dt, drift = a.drift;
         for (uint32_t kb = 0; kb < nfull; ++kb) {
-            const float4 g = normal_quad_h(rng, kb);
+            const float4 g = normal_quad_h<BMV>(rng, kb);
             float xs[4];
             x = __fmaf_rn(nsd, g.x, __fmaf_rn(dtA, drift, x)); xs[0] = x;
             x = __fmaf_rn(nsd, g.y, __fmaf_rn(dtA, drift, x)); xs[1] = x;
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
             }
         }
         if (a.n_steps & 3u) {  // ragged last quad
-            const float4 g = normal_quad_h(rng, nfull);
+            const float4 g = normal_quad_h<BMV>(rng, nfull);
             const float gg[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
             for (int l = 0; l < 3; ++l) {

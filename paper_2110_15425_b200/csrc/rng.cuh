@@ -324,10 +324,13 @@ struct PhiloxHoisted {
 
 // Quad normals 4k..4k+3 of a hoisted stream-2 unit: both Box-Muller pairs of the
 // block in the two lanes of one packed evaluation (spec/RNG.md §6, quad packing).
+// BMV selects the scalar (bit set) or packed-pair form of ln / rsqrt / sincos
+// (bits 1 / 2 / 4); all variants are the same binary32 operations.
+template <int BMV = 0>
 __device__ __forceinline__ float4 normal_quad_h(const PhiloxHoisted& rng, uint32_t k) {
     const uint4 X = rng(k);
     F2 zc, zs;
-    bm_pair2<false, false, false>(X.x, X.z, X.y & 0xFFFFFF00u, X.w & 0xFFFFFF00u, zc, zs);
+    bm_pair2<(BMV & 1) != 0, (BMV & 2) != 0, (BMV & 4) != 0>(X.x, X.z, X.y & 0xFFFFFF00u, X.w & 0xFFFFFF00u, zc, zs);
     return make_float4(zc.x, zs.x, zc.y, zs.y);
 }
 

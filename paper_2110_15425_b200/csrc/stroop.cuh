@@ -39,7 +39,7 @@ __device__ __forceinline__ void lca_step(const StroopArgs& a, float I0, float I1
     x1 = fmaxf(__fmaf_rn(nsd, g1, __fmaf_rn(a.dt, q1, x1)), 0.0f);
 }
 
-template <int BLOCK, int MINB = 0>
+template <int BLOCK, int MINB = 0, int BMV = 0>
 __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArgs a, uint32_t alloc_off) {
     const uint32_t t_alloc = alloc_off + blockIdx.y;           // index within [0, count)
     const uint32_t i = a.begin + t_alloc;
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
         // passes is resolved in the spec's order.
         const uint32_t nfull = a.n_steps >> 1;    // 2 steps per quad block
         for (uint32_t kb = 0; kb < nfull; ++kb) {
-            const float4 g = normal_quad_h(rng, kb);
+            const float4 g = normal_quad_h<BMV>(rng, kb);
             float xa0, xa1;
             lca_step(a, I0, I1, nleak, ninh, nsd, g.x, g.y, h0, h1, x0, x1);
             xa0 = x0; xa1 = x1;
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
             }
         }
         if (a.n_steps & 1u) {  // ragged last step
-            const float4 g = normal_quad_h(rng, nfull);
+            const float4 g = normal_quad_h<BMV>(rng, nfull);
             lca_step(a, I0, I1, nleak, ninh, nsd, g.x, g.y, h0, h1, x0, x1);
             if (resp < 0) {
                 if (x0 >= a.thr) { resp = 0; st = a.n_steps; }
