@@ -68,6 +68,12 @@ int main() {
     cudaMalloc((void**)&g_counter, 4);
     run<256, 0, 0>("packed (ref)", a, ref.data(), 0, true);
     key64_t rk; cudaMemcpy(&rk, a.best, 8, cudaMemcpyDeviceToHost);
+    {
+        unsigned long long hsh = 1469598103934665603ull;
+        const unsigned char* b = (const unsigned char*)ref.data();
+        for (size_t q = 0; q < ref.size() * 4; ++q) hsh = (hsh ^ b[q]) * 1099511628211ull;
+        printf("ref key %016llx net fnv1a %016llx\n", (unsigned long long)rk, hsh);
+    }
 #define V(B, M, N, P, Q, E, name) run<B, M, N, P, Q, E>(name, a, ref.data(), rk, false)
     V(128, 0, 0, false, false, true, "b128 even");
     V(128, 0, 6, false, false, true, "b128 even minb6");
