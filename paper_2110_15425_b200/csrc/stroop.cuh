@@ -194,27 +194,33 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
         float x1 = 0.0f, x2 = 0.0f;
         int h1t = 0, h2t = 0;
         uint32_t s1 = 0, s2 = 0;
-        const uint32_t nblk = (a.n_d + 1) >> 1;                // 2 steps (4 normals) per quad block
-        for (uint32_t kb = 0; kb < nblk; ++kb) {
+        // 2 steps (4 normals) per quad block; each DDM's latch is tested once
+        // per block on max(|x|) (|x| >= z <=> x >= z or x <= -z, DDM kernel).
+        const uint32_t nfull = a.n_d >> 1;
+        for (uint32_t kb = 0; kb < nfull; ++kb) {
             const float4 g = normal_quad_h(rng, kb);
-#pragma unroll
-            for (int l = 0; l < 2; ++l) {
-                const uint32_t n = 2 * kb + l + 1;
-                if (n <= a.n_d) {
-                    const float g1 = l ? g.z : g.x, g2 = l ? g.w : g.y;
-                    if (VARIANT == 0) {
-                        x1 = __fmaf_rn(nsd, g1, __fmaf_rn(a.dt, A1, x1));
-                        x2 = __fmaf_rn(nsd, g2, __fmaf_rn(a.dt, A2, x2));
-                        ddm_latch(x1, a.z, n, h1t, s1);
-                        ddm_latch(x2, a.z, n, h2t, s2);
-                    } else {
-                        x2 = __fmaf_rn(nsd, g2, __fmaf_rn(a.dt, A2, x2));
-                        x1 = __fmaf_rn(nsd, g1, __fmaf_rn(a.dt, A1, x1));
-                        ddm_latch(x2, a.z, n, h2t, s2);
-                        ddm_latch(x1, a.z, n, h1t, s1);
-                    }
-                }
+            float x1a, x2a;
+            if (VARIANT == 0) {
+                x1a = x1 = __fmaf_rn(nsd, g.x, __fmaf_rn(a.dt, A1, x1));
+                x2a = x2 = __fmaf_rn(nsd, g.y, __fmaf_rn(a.dt, A2, x2));
+                x1 = __fmaf_rn(nsd, g.z, __fmaf_rn(a.dt, A1, x1));
+                x2 = __fmaf_rn(nsd, g.w, __fmaf_rn(a.dt, A2, x2));
+            } else {
+                x2a = x2 = __fmaf_rn(nsd, g.y, __fmaf_rn(a.dt, A2, x2));
+                x1a = x1 = __fmaf_rn(nsd, g.x, __fmaf_rn(a.dt, A1, x1));
+                x2 = __fmaf_rn(nsd, g.w, __fmaf_rn(a.dt, A2, x2));
+                x1 = __fmaf_rn(nsd, g.z, __fmaf_rn(a.dt, A1, x1));
             }
+            const uint32_t n = 2 * kb + 1;
+            if (!h1t && fmaxf(fabsf(x1a), fabsf(x1)) >= a.z) { ddm_latch(x1a, a.z, n, h1t, s1); ddm_latch(x1, a.z, n + 1, h1t, s1); }
+            if (!h2t && fmaxf(fabsf(x2a), fabsf(x2)) >= a.z) { ddm_latch(x2a, a.z, n, h2t, s2); ddm_latch(x2, a.z, n + 1, h2t, s2); }
+        }
+        if (a.n_d & 1u) {  // ragged last step
+            const float4 g = normal_quad_h(rng, nfull);
+            x1 = __fmaf_rn(nsd, g.x, __fmaf_rn(a.dt, A1, x1));
+            x2 = __fmaf_rn(nsd, g.y, __fmaf_rn(a.dt, A2, x2));
+            ddm_latch(x1, a.z, a.n_d, h1t, s1);
+            ddm_latch(x2, a.z, a.n_d, h2t, s2);
         }
         if (h1t == 0 || h2t == 0) { ++n_und; continue; }
         n_both += (h1t == 1 && h2t == 1);

@@ -497,3 +497,29 @@ def test_argmax_ties_all_nan_and_empty(D, orc):
     D.argmax_ties(t[:0], 0, 1, 0, best, tie)
     torch.cuda.synchronize()
     assert int(tie.item()) == -1          # KEY_INIT: nothing can win
+
+
+@pytest.mark.parametrize("kind,variant,n_idx,n_val,thr_idx,thr", [
+    (W.KIND_STROOP_LCA, None, 10, 37, 7, 0.4),        # odd trip count, low threshold: many early passages
+    (W.KIND_STROOP_LCA, None, 10, 1, 7, 1.0),         # single step (only the ragged path runs)
+    (W.KIND_EXT_STROOP_A, 0, 10, 37, 9, 0.3),
+    (W.KIND_EXT_STROOP_B, 1, 10, 37, 9, 0.3),
+    (W.KIND_EXT_STROOP_A, 0, 10, 1, 9, 0.05)])
+def test_stroop_kinds_odd_trip_counts_bit_exact(D, orc, kind, variant, n_idx, n_val, thr_idx, thr):
+    """Ragged last quad block and the two-step latch test on both Stroop kernels."""
+    ext = variant is not None
+    c = W.ext_stroop_small() if ext else W.stroop_small()
+    c.params = c.params.copy()
+    c.params[n_idx] = n_val
+    c.params[thr_idx] = thr
+    m = D.load_model(kind, c.n_levels, c.levels, c.w, c.params, device=0)
+    cnt, net, key = _stroop_gpu(D, m, c, 0, c.n_alloc)
+    if ext:
+        wc, wn = orc.ext_stroop_eval(variant, c.n_levels, c.levels, c.w, c.params, 0, c.n_alloc, c.n_trials,
+                                     c.seed, threads=8)
+    else:
+        wc, wn = orc.stroop_eval(c.n_levels, c.levels, c.w, c.params, 0, c.n_alloc, c.n_trials, c.seed, threads=8)
+    assert np.array_equal(cnt, wc)
+    assert np.array_equal(_bits(net), _bits(wn))
+    assert key == orc.argmax_net(wn)[0]
+    assert cnt[:, 1].sum() < cnt.shape[0] * c.n_trials or n_val == 1   # some trials decide
