@@ -28,6 +28,32 @@ def _ulp32(ref):
     return np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
 
 
+def test_philox_matches_curand_host_generator(orc):
+    """Library pin: cuRAND's host-side PHILOX4_32_10 generator (default ordering)
+    emits block t = Philox4x32-10(ctr = (t >> 16, 0, t & 0xFFFF, 0), key = seed)
+    — 70,000 blocks (both sides of the 2^16 subsequence wrap) must equal the oracle."""
+    import ctypes
+    import os
+    path = "/usr/local/cuda/lib64/libcurand.so"
+    if not os.path.exists(path):
+        pytest.skip("libcurand not present")
+    cr = ctypes.CDLL(path)
+    for seed in (0, 0xDEADBEEF12345678):
+        gen = ctypes.c_void_p()          # a fresh generator per seed (offset 0)
+        assert cr.curandCreateGeneratorHost(ctypes.byref(gen), 161) == 0     # CURAND_RNG_PSEUDO_PHILOX4_32_10
+        try:
+            assert cr.curandSetPseudoRandomGeneratorSeed(gen, ctypes.c_ulonglong(seed)) == 0
+            n = 70_000
+            out = np.zeros(4 * n, np.uint32)
+            assert cr.curandGenerate(gen, out.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(4 * n)) == 0
+        finally:
+            cr.curandDestroyGenerator(gen)
+        blk = out.reshape(-1, 4)
+        key = (seed & 0xFFFFFFFF, seed >> 32)
+        for t in list(range(0, n, 37)) + [65535, 65536, n - 1]:
+            assert np.array_equal(blk[t], orc.philox((t >> 16, 0, t & 0xFFFF, 0), key)), (seed, t)
+
+
 def test_ln_exhaustive_on_uniform_domain(orc):
     """Every binary32 in [2^-24, 1): |ln_spec - log| <= 4 ulp (binary64 libm)."""
     worst = 0.0
