@@ -1,6 +1,6 @@
 """Small driver for ncu captures of the DDM and Stroop kernels (tools only).
 
-    python tools/profile_extras.py       # cfg2 DDM batch + a 100-allocation slice of cfg4
+    python tools/profile_extras.py [--pp]      # cfg2 DDM batch + 100-allocation slices of cfg4 and the Ext Stroop grid
 """
 import os
 import sys
@@ -16,6 +16,13 @@ import workloads as W  # noqa: E402
 
 def main():
     torch.cuda.set_device(0)
+    if "--pp" in sys.argv:      # one cfg3 grid search first (for metric-only captures)
+        c3 = W.pp_cfg3()
+        mp = D.load_model(W.KIND_PREDATOR_PREY, c3.n_levels, c3.levels, c3.w, c3.params, device=0)
+        pnet = torch.empty(c3.n_alloc, device="cuda")
+        pbest = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        for _ in range(2):
+            D.eval_grid(mp, c3.inputs, c3.n_samples, c3.seed, net=pnet, best=pbest)
     d = W.ddm_cfg2()
     rh, rs, xh = (torch.zeros(n, dtype=torch.int64, device="cuda") for n in d.hist_sizes)
     for _ in range(2):
@@ -29,6 +36,10 @@ def main():
     counts = torch.empty(3 * n, dtype=torch.int64, device="cuda")
     for _ in range(2):
         D.eval_grid(m, None, c.n_trials, c.seed, 0, n, net=net, best=best, counts=counts)
+    g = W.ext_stroop_grid()
+    mx = D.load_model(W.KIND_EXT_STROOP_A, g.n_levels, g.levels, g.w, g.params, device=0)
+    for _ in range(2):
+        D.eval_grid(mx, None, g.n_trials, g.seed, 0, n, net=net, best=best, counts=counts)
     torch.cuda.synchronize()
     print("ok", int(rh.sum()), float(net[0]))
 
