@@ -405,6 +405,24 @@ def run_extras(D, torch, dev, rank, world, args):
         out["pp_episode_cfg3"] = {"ms": ms, "steps": steps_run, "outcome": int(st_h[0]),
                                   "evals_per_s": c3.evals * steps_run / (ms / 1e3),
                                   "note": "T=16 closed-loop steps, each a full cfg3 grid search + device step kernel"}
+        # Listing-1 multi-invocation run: 16 invocations of the cfg3 grid search on
+        # 16 synthetic position sets in ONE launch (SURVEY §8(d) cfg3 variant)
+        sets = torch.from_numpy(W.pp_positions(T)).to(dev)
+        mnet = torch.empty((T, c3.n_alloc), dtype=torch.float32, device=dev)
+        mbest = torch.empty(T, dtype=torch.int64, device=dev)
+        mbest.fill_(-1)
+        D.eval_grid_multi(m3, sets, T, c3.n_samples, c3.seed, net=mnet, best=mbest)
+        torch.cuda.synchronize()
+        mbest.fill_(-1)
+        e0.record()
+        D.eval_grid_multi(m3, sets, T, c3.n_samples, c3.seed, net=mnet, best=mbest)
+        e1.record()
+        torch.cuda.synchronize()
+        mms = e0.elapsed_time(e1)
+        out["pp_cfg3_x16_multi"] = {"ms": mms, "invocations": T, "evals_per_s": c3.evals * T / (mms / 1e3),
+                                    "frac_fp32_peak": (FLOPS_PER_SAMPLE * c3.evals + FLOPS_PER_ALLOC * c3.n_alloc) * T / (mms / 1e3) / 1e12
+                                    / FP32_PEAK_NOMINAL,
+                                    "note": "16 invocations x cfg3 (positions uniform in [-10,10]^2) in one launch"}
     if args.stroop:
         c = W.stroop_cfg4()
         m = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=dev.index)

@@ -159,6 +159,30 @@ distill_status distill_grid_size(const distill_model* model, uint64_t* n_alloc);
  * simulate + finalize kernels for Stroop.  Stream-ordered, asynchronous. */
 distill_status distill_eval_grid(const distill_model* model, const distill_eval_args* args, void* stream);
 
+/* Many controller invocations in one launch (Listing 1, P:190-199:
+ * `composition.run(inputs, num_trials)` invokes the controller once per trial
+ * with `inputs[num_trial % len]` — reading Q17 of the garbled `%`).  Invocation
+ * t (0 <= t < n_invocations) evaluates allocations [begin, end) on position set
+ * t mod n_sets with RNG invocation word invocation0 + t, writes its V row
+ * d_net[t*(end-begin) ...] and atomicMin's its key into d_best[t].  Identical,
+ * bit for bit, to n_invocations separate distill_eval_grid calls.
+ * Predator-prey only (E_UNSUPPORTED otherwise); n_invocations <= 65535 per call
+ * (E_INVALID_ARG beyond); invocation0 + n_invocations must fit in 32 bits
+ * (E_OVERFLOW).  Stream-ordered, one kernel launch. */
+typedef struct {
+    const float* d_inputs;       /* device, caller-owned [n_sets][6]: prey, predator, player (x, y) */
+    uint32_t n_sets;             /* >= 1                                                           */
+    uint32_t n_invocations;      /* T, 0 = no-op                                                   */
+    uint32_t invocation0;        /* RNG invocation word of t = 0                                   */
+    uint32_t n_samples;          /* samples per allocation, >= 1                                   */
+    uint64_t begin, end;         /* global allocation range (a shard)                              */
+    uint64_t seed;               /* Philox key                                                     */
+    float* d_net;                /* device [T][end-begin] or NULL                                  */
+    unsigned long long* d_best;  /* device [T] keys or NULL; caller initialises to DISTILL_KEY_INIT */
+} distill_multi_args;
+
+distill_status distill_eval_grid_multi(const distill_model* model, const distill_multi_args* args, void* stream);
+
 /* Same evaluation from HOST buffers (the end-to-end call): evaluates on `stream`,
  * returns V in h_net (if non-NULL) and the best key in *h_best, synchronises the
  * stream.  Pinned (cudaHostAlloc / page-locked, device-mapped) h_net is written by

@@ -188,6 +188,17 @@ def normal_sextet(seed: int, alloc: int, sample: int, invocation: int = 0) -> np
 
 # ---------------------------------------------------------------- predator-prey
 
+def pp_eval_multi(n_levels, levels, w, params, input_sets, n_invocations, begin, end, n_samples, seed,
+                  invocation0=0):
+    """PAPER.md Listing 1: one controller invocation per trial t with
+    inputs[t % len] (reading Q17); here invocation t uses set t mod n_sets and RNG
+    invocation word invocation0 + t.  Returns float32 costs C [T, end-begin]."""
+    sets = np.asarray(input_sets, np.float32).reshape(-1, 6)
+    return np.stack([pp_eval(n_levels, levels, w, params, sets[t % len(sets)], begin, end, n_samples, seed,
+                             invocation=invocation0 + t) for t in range(int(n_invocations))]) \
+        if n_invocations else np.zeros((0, int(end) - int(begin)), np.float32)
+
+
 def pp_eval(n_levels, levels, w, params, inputs, begin, end, n_samples, seed,
             invocation=0, f64=False, counting=False) -> np.ndarray:
     n = int(end) - int(begin)

@@ -5,6 +5,7 @@ Public Python API (thin wrappers over the C ABI in include/distill.h):
     load_model(kind, n_levels, levels, cost_weights, params, device=0) -> Model
     eval_grid(model, inputs, n_samples, seed, begin=0, end=None, net=None, best=None, ...)
     eval_grid_host(model, inputs, n_samples, seed, ...)   # host buffers, end to end
+    eval_grid_multi(model, d_inputs, n_invocations, n_samples, seed, ...)   # many invocations, one launch
     argmax(values, index_base, best) / argmax_ties(values, base, seed, t, best, tie)
     key_reset(best) / key_decode(key)
     ddm_batch(...)
@@ -15,10 +16,10 @@ Public Python API (thin wrappers over the C ABI in include/distill.h):
 Importing this package does not touch the GPU; the shared library is loaded
 on first use and there is no CPU fallback.
 """
-from .api import (KEY_INIT, Model, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, key_decode,
+from .api import (KEY_INIT, Model, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_multi, key_decode,
                   key_reset, launch_count, load_model, pp_amr, pp_episode)
 from .dist import best_allreduce, hist_allreduce, key_to_i64, i64_to_key, shard_range
 
-__all__ = ["KEY_INIT", "Model", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "key_decode", "pp_episode", "pp_amr",
+__all__ = ["KEY_INIT", "Model", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "eval_grid_multi", "key_decode", "pp_episode", "pp_amr",
            "key_reset", "launch_count", "load_model", "best_allreduce", "hist_allreduce", "key_to_i64",
            "i64_to_key", "shard_range"]

@@ -63,6 +63,13 @@ class AmrArgs(C.Structure):
                 ("seed", C.c_uint64), ("d_keys", C.c_void_p), ("d_boxes", C.c_void_p), ("d_levels", C.c_void_p)]
 
 
+class MultiArgs(C.Structure):
+    _fields_ = [("d_inputs", C.c_void_p), ("n_sets", C.c_uint32), ("n_invocations", C.c_uint32),
+                ("invocation0", C.c_uint32), ("n_samples", C.c_uint32),
+                ("begin", C.c_uint64), ("end", C.c_uint64), ("seed", C.c_uint64),
+                ("d_net", C.c_void_p), ("d_best", C.c_void_p)]
+
+
 EXPORTS = {
     "distill_abi_version": (C.c_int, []),
     "distill_last_error": (C.c_char_p, []),
@@ -82,6 +89,7 @@ EXPORTS = {
     "distill_launch_count": (C.c_uint64, []),
     "distill_sm_clock_probe": (C.c_int, [C.c_uint32, C.POINTER(C.c_double), C.c_void_p]),
     "distill_pp_amr": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_void_p]),
+    "distill_eval_grid_multi": (C.c_int, [C.c_void_p, C.POINTER(MultiArgs), C.c_void_p]),
     "distill_pp_episode": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_void_p]),
 }
 

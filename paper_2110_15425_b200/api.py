@@ -94,6 +94,21 @@ def eval_grid(model: Model, inputs, n_samples: int, seed: int, begin: int = 0, e
     check(lib().distill_eval_grid(model.handle, C.byref(a), _stream_handle(stream)))
 
 
+def eval_grid_multi(model: Model, inputs, n_invocations: int, n_samples: int, seed: int, begin: int = 0,
+                    end: Optional[int] = None, invocation0: int = 0, net=None, best=None, stream=None) -> None:
+    """distill_eval_grid_multi: invocation t on position set t mod n_sets, RNG invocation invocation0 + t.
+
+    `inputs` is a CUDA float32 tensor [n_sets, 6]; net [T, end-begin] and best [T] as in eval_grid."""
+    end = model.n_alloc if end is None else int(end)
+    n, T = end - int(begin), int(n_invocations)
+    if inputs.dtype.itemsize != 4 or inputs.dim() != 2 or inputs.shape[1] != 6:
+        raise ValueError("inputs must be a float32 CUDA tensor of shape [n_sets, 6]")
+    a = _abi.MultiArgs(_dev_ptr(inputs, "inputs"), int(inputs.shape[0]), T, int(invocation0), int(n_samples),
+                       int(begin), end, int(seed) & (2 ** 64 - 1), _dev_ptr(net, "net", T * n),
+                       _dev_ptr(best, "best", T))
+    check(lib().distill_eval_grid_multi(model.handle, C.byref(a), _stream_handle(stream)))
+
+
 def eval_grid_host(model: Model, inputs, n_samples: int, seed: int, begin: int = 0, end: Optional[int] = None,
                    net_out: Optional[np.ndarray] = None, invocation: int = 0, stream=None) -> int:
     """distill_eval_grid_host: host inputs in, host V (optional) and best key out; synchronous."""
@@ -207,5 +222,5 @@ def key_from_tensor(best) -> int:
     return int(best.reshape(-1)[0].item()) & (2 ** 64 - 1)
 
 
-__all__ = ["KEY_INIT", "DistillError", "Model", "load_model", "eval_grid", "eval_grid_host", "argmax",
+__all__ = ["KEY_INIT", "DistillError", "Model", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",
            "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode", "argmax_ties", "pp_amr", "sm_clock_mhz"]

@@ -192,6 +192,40 @@ static distill_status launch_pp(const distill_model* m, const distill_eval_args*
     return DISTILL_OK;
 }
 
+distill_status distill_eval_grid_multi(const distill_model* m, const distill_multi_args* a, void* stream) {
+    if (!m || !a) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: NULL model/args");
+    if (m->kind != DISTILL_MODEL_PREDATOR_PREY) return fail(DISTILL_E_UNSUPPORTED, "eval_grid_multi: predator-prey only");
+    if (!a->d_inputs || a->n_sets == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: needs n_sets >= 1 device position sets");
+    if (reinterpret_cast<uintptr_t>(a->d_inputs) & 3u) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: d_inputs misaligned");
+    if (a->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: n_samples must be >= 1");
+    if (a->n_invocations > 65535u) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: at most 65535 invocations per call");
+    if (a->begin > a->end || a->end > m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: bad allocation range");
+    if ((uint64_t)a->invocation0 + a->n_invocations > 0xFFFFFFFFull)
+        return fail(DISTILL_E_OVERFLOW, "eval_grid_multi: invocation counter overflow");
+    const uint64_t count = a->end - a->begin;
+    if (count == 0 || a->n_invocations == 0) return DISTILL_OK;
+    CUDA_TRY(cudaSetDevice(m->device));
+    PPArgs p;
+    p.prey_x = p.prey_y = p.pred_x = p.pred_y = p.pl_x = p.pl_y = 0.0f;   // read from d_inputs
+    p.sigma_max = m->params[0]; p.sigma_min = m->params[1]; p.kappa = m->params[2];
+    p.w0 = m->w[0]; p.w1 = m->w[1]; p.w2 = m->w[2];
+    p.L0 = m->L[0]; p.L1 = m->L[1]; p.L2 = m->L[2];
+    p.n_samples = a->n_samples; p.invocation = a->invocation0;
+    p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
+    p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
+    p.levels = m->d_levels; p.net = a->d_net; p.best = a->d_best;
+    p.pos_dev = a->d_inputs; p.status_dev = nullptr; p.n_sets = a->n_sets;
+    const dim3 grid((unsigned)((count + PP_BLOCK - 1) / PP_BLOCK), a->n_invocations);
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((a->n_samples & 1u) == 0)
+        pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+    else
+        pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
 static distill_status launch_stroop(distill_model* m, const distill_eval_args* a, cudaStream_t st) {
     if (a->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop): n_samples (trials) must be >= 1");
     if (a->invocation != 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop): invocation must be 0");

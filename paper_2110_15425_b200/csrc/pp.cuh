@@ -34,9 +34,24 @@ struct PPArgs {
     const float* __restrict__ levels;                  // device RO block: L0+L1+L2 floats
     float* __restrict__ net;                           // [count] or nullptr
     key64_t* __restrict__ best;                        // [1] or nullptr
-    const float* __restrict__ pos_dev;                 // episode: positions in device memory (or nullptr)
+    const float* __restrict__ pos_dev;                 // episode / multi: positions in device memory (or nullptr)
     const int* __restrict__ status_dev;                // episode: skip the launch when status[0] != 0
+    uint32_t n_sets = 1;                               // multi: position sets; invocation t uses set t mod n_sets
 };
+
+// Multi-invocation launches (distill_eval_grid_multi) put invocation t on
+// blockIdx.y: RNG invocation + t, position set t mod n_sets, its own net row
+// and key.  t = 0 is the plain single-invocation launch.
+__device__ __forceinline__ PPArgs pp_select_invocation(const PPArgs& a, uint32_t t) {
+    PPArgs b = a;
+    if (t) {
+        b.invocation = a.invocation + t;
+        if (a.pos_dev) b.pos_dev = a.pos_dev + 6u * (t % a.n_sets);
+        if (a.net) b.net = a.net + (size_t)t * a.count;
+        if (a.best) b.best = a.best + t;
+    }
+    return b;
+}
 
 // Episode support: positions come from device memory (written by the previous
 // step kernel) instead of the launch parameters.
@@ -192,7 +207,7 @@ __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, floa
 template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false, bool EVEN = false>
 __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs a0) {
     if (a0.status_dev && *a0.status_dev != 0) return;   // episode already over (uniform branch)
-    const PPArgs a = pp_resolve_positions(a0);
+    const PPArgs a = pp_resolve_positions(pp_select_invocation(a0, blockIdx.y));
     const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
     const float2 ustar = pp_ustar_block(a);
     key64_t key = KEY_INIT;

@@ -116,3 +116,11 @@ def test_next_row_entry_points_validate_before_cuda(abi):
     assert L.distill_argmax(None, 0, 0, C.addressof(dummy), None) == abi.OK
     assert L.distill_argmax(None, 1, 0xFFFFFFFF, C.addressof(dummy), None) == abi.E_INVALID_ARG
     assert L.distill_sm_clock_probe(0, None, None) == abi.E_INVALID_ARG
+
+
+def test_eval_grid_multi_validates_before_cuda(abi):
+    import ctypes as C
+    L = abi.lib()
+    a = abi.MultiArgs()
+    assert L.distill_eval_grid_multi(None, C.byref(a), None) == abi.E_INVALID_ARG
+    assert L.distill_eval_grid_multi(None, None, None) == abi.E_INVALID_ARG

@@ -523,3 +523,54 @@ def test_stroop_kinds_odd_trip_counts_bit_exact(D, orc, kind, variant, n_idx, n_
     assert np.array_equal(_bits(net), _bits(wn))
     assert key == orc.argmax_net(wn)[0]
     assert cnt[:, 1].sum() < cnt.shape[0] * c.n_trials or n_val == 1   # some trials decide
+
+
+@pytest.mark.parametrize("shape,S,T,n_sets,inv0,rng_", [((8, 7, 6), 24, 7, 3, 5, (0, None)),
+                                                        ((5, 5, 5), 9, 4, 1, 0, (17, 101)),
+                                                        ((33, 1, 3), 2, 16, 16, 1000, (0, None))])
+def test_eval_grid_multi_bit_exact(D, orc, shape, S, T, n_sets, inv0, rng_):
+    """Listing-1 multi-invocation launch: every invocation's costs and key bit-exact
+    against the oracle's per-trial loop."""
+    import torch
+    cfg = W.PPConfig("multi", shape, S)
+    m = _model(D, cfg)
+    b, e = rng_[0], (cfg.n_alloc if rng_[1] is None else rng_[1])
+    sets = W.pp_positions(n_sets, seed=3)
+    d_sets = torch.from_numpy(sets).cuda()
+    net = torch.empty((T, e - b), dtype=torch.float32, device="cuda")
+    best = torch.full((T,), -1, dtype=torch.int64, device="cuda")
+    D.eval_grid_multi(m, d_sets, T, S, cfg.seed, b, e, invocation0=inv0, net=net, best=best)
+    torch.cuda.synchronize()
+    want = orc.pp_eval_multi(cfg.n_levels, cfg.levels, cfg.w, cfg.params, sets, T, b, e, S, cfg.seed, invocation0=inv0)
+    assert np.array_equal(_bits(-net.cpu().numpy()), _bits(want))
+    keys = [int(k) & (2 ** 64 - 1) for k in best.cpu().numpy()]
+    assert keys == [orc.argmax_net(-want[t], b)[0] for t in range(T)]
+
+
+def test_eval_grid_multi_cfg3_x16_matches_single_calls(D, orc):
+    """Full-size cfg3 with 16 invocations (SURVEY §8(d) cfg3 variant) in one launch ==
+    16 single-invocation calls (bit-exact net rows and keys); two rows and keys also
+    against the oracle."""
+    import torch
+    cfg = W.pp_cfg3()
+    m = _model(D, cfg)
+    T = 16
+    sets = W.pp_positions(T)
+    d_sets = torch.from_numpy(sets).cuda()
+    net = torch.empty((T, cfg.n_alloc), dtype=torch.float32, device="cuda")
+    best = torch.full((T,), -1, dtype=torch.int64, device="cuda")
+    D.eval_grid_multi(m, d_sets, T, cfg.n_samples, cfg.seed, net=net, best=best)
+    net1 = torch.empty(cfg.n_alloc, dtype=torch.float32, device="cuda")
+    best1 = torch.empty(1, dtype=torch.int64, device="cuda")
+    for t in range(T):
+        best1.fill_(-1)
+        D.eval_grid(m, sets[t], cfg.n_samples, cfg.seed, invocation=t, net=net1, best=best1)
+        torch.cuda.synchronize()
+        assert torch.equal(net1.view(torch.int32), net[t].view(torch.int32))
+        assert int(best1.item()) == int(best[t].item())
+    for t in (0, T - 1):
+        row = -net[t].cpu().numpy()
+        for i in np.random.default_rng(t).integers(0, cfg.n_alloc, 64):
+            w = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, sets[t], int(i), int(i) + 1,
+                            cfg.n_samples, cfg.seed, invocation=t)
+            assert _bits(row[int(i)]) == _bits(w)[0]

@@ -207,3 +207,21 @@ def test_flop_count_per_sample_matches_hand_count(orc):
     # per call: u_star = action 51 + unit 22 = 73, plus dsig 1;
     # per allocation: 3 sigma fma (6) + K (5) + mean (2) = 13
     assert per_alloc == 74 + 10 * 13
+
+
+def test_multi_invocation_is_the_listing1_loop(orc):
+    """pp_eval_multi = one pp_eval per trial t on inputs[t % len] with invocation0 + t
+    (reading Q17); distinct invocations draw distinct noise."""
+    import workloads as W
+    cfg = W.PPConfig("m", (3, 4, 2), 6)
+    sets = W.pp_positions(3, seed=11)
+    C = orc.pp_eval_multi(cfg.n_levels, cfg.levels, cfg.w, cfg.params, sets, 5, 0, cfg.n_alloc, 6, 9, invocation0=2)
+    assert C.shape == (5, cfg.n_alloc)
+    for t in range(5):
+        want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, sets[t % 3], 0, cfg.n_alloc, 6, 9,
+                           invocation=2 + t)
+        assert np.array_equal(C[t].view(np.uint32), want.view(np.uint32))
+    # same positions, different invocation -> different samples
+    assert not np.array_equal(C[0], orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, sets[0], 0,
+                                                 cfg.n_alloc, 6, 9, invocation=5))
+    assert np.all(np.abs(sets) <= 10) and sets.dtype == np.float32

@@ -65,6 +65,12 @@ def pp_cfg1() -> PPConfig:
     return PPConfig("pp_cfg1_3x3x3_s10", (3, 3, 3), 10)
 
 
+def pp_positions(n_sets: int, seed: int = SEED) -> np.ndarray:
+    """Synthetic multi-invocation inputs (SURVEY §8(d) cfg3 16-invocation variant):
+    prey, predator, player positions uniform in [-10, 10]^2, float32 [n_sets, 6]."""
+    return np.random.default_rng(seed).uniform(-10.0, 10.0, size=(int(n_sets), 6)).astype(np.float32)
+
+
 def pp_cfg3() -> PPConfig:
     return PPConfig("pp_cfg3_100^3_s100", (100, 100, 100), 100)
 
