@@ -218,9 +218,9 @@ distill_status distill_eval_grid_multi(const distill_model* m, const distill_mul
     const dim3 grid((unsigned)((count + PP_BLOCK - 1) / PP_BLOCK), a->n_invocations);
     cudaStream_t st = (cudaStream_t)stream;
     if ((a->n_samples & 1u) == 0)
-        pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+        pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true, true><<<grid, PP_BLOCK, 0, st>>>(p);
     else
-        pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
+        pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;

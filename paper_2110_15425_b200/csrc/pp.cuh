@@ -41,20 +41,8 @@ struct PPArgs {
 
 // Multi-invocation launches (distill_eval_grid_multi) put invocation t on
 // blockIdx.y: RNG invocation + t, position set t mod n_sets, its own net row
-// and key.  t = 0 is the plain single-invocation launch.
-__device__ __forceinline__ PPArgs pp_select_invocation(const PPArgs& a, uint32_t t) {
-    PPArgs b = a;
-    if (t) {
-        b.invocation = a.invocation + t;
-        if (a.pos_dev) b.pos_dev = a.pos_dev + 6u * (t % a.n_sets);
-        if (a.net) b.net = a.net + (size_t)t * a.count;
-        if (a.best) b.best = a.best + t;
-    }
-    return b;
-}
+// and key (pp_eval_grid_kernel<..., MULTI = true>).
 
-// Episode support: positions come from device memory (written by the previous
-// step kernel) instead of the launch parameters.
 __device__ __forceinline__ PPArgs pp_resolve_positions(const PPArgs& a) {
     PPArgs b = a;
     if (a.pos_dev) {
@@ -204,21 +192,32 @@ __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, floa
 }
 
 // One thread per allocation; one atomicMin per block.
-template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false, bool EVEN = false>
+template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false, bool EVEN = false,
+          bool MULTI = false>
 __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs a0) {
     if (a0.status_dev && *a0.status_dev != 0) return;   // episode already over (uniform branch)
-    const PPArgs a = pp_resolve_positions(pp_select_invocation(a0, blockIdx.y));
+    // Multi-invocation: only the invocation word and the position set feed the
+    // sample loop; the output row/key pointers are formed after it (keeping them
+    // live across the loop costs registers and ~4 % time).
+    PPArgs a = a0;
+    if (MULTI) {
+        a.invocation = a0.invocation + blockIdx.y;
+        a.pos_dev = a0.pos_dev + 6u * (blockIdx.y % a0.n_sets);
+    }
+    a = pp_resolve_positions(a);
     const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
     const float2 ustar = pp_ustar_block(a);
     key64_t key = KEY_INIT;
+    float C = 0.0f;
     if (tid < a.count) {
         const uint32_t i = a.begin + tid;
-        const float C = pp_eval_alloc<MASK, PIPE, EVEN>(a, i, ustar);
-        if (a.net) a.net[tid] = -C;
+        C = pp_eval_alloc<MASK, PIPE, EVEN>(a, i, ustar);
         key = make_key(C, i);
     }
+    const size_t row = MULTI ? (size_t)blockIdx.y : 0;
+    if (a0.net && tid < a0.count) a0.net[row * a0.count + tid] = -C;
     // a9: (value, index) argmin -> one atomic per block
-    if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
+    if (a0.best) block_min_key_atomic<BLOCK>(key, a0.best + row);
 }
 
 // Persistent variant: a fixed grid of resident blocks pulls BLOCK-allocation
