@@ -116,6 +116,18 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+def hbm_peak_gbps():
+    """Measured HBM copy bandwidth from the driver-written MEASURED_PEAKS.json, else the guide's fallback."""
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        for k in ("hbm_gbs", "hbm_GBps"):
+            if k in mp:
+                return float(mp[k])
+    except Exception:
+        pass
+    return None
+
+
 def oracle_rate(cfg: W.PPConfig, target_cpu_s: float = 15.0):
     """Time the CPU oracle (as it stands) over all host cores on a bounded slice
     of the workload: contiguous allocation segments, all samples."""
@@ -323,7 +335,13 @@ def run_ours(args):
                                        if sm_load else None),
             "frac_at_probe_clock": achieved / (n_sm * FP32_LANES_PER_SM * 2 * clocks["sm_mhz_effective_probe"]
                                                * 1e6 / 1e12),
-            "kernel_share_of_step": ms_kern / ms_step}
+            "kernel_share_of_step": ms_kern / ms_step,
+            # north star: "achieved HBM GB/s for the cost-array write" (4 B per allocation per launch;
+            # the kernel is ALU-bound, the write is a rounding error next to the HBM peak)
+            "cost_array_write": {"bytes_per_launch": count * 4, "GBps": count * 4 / (ms_kern / 1e3) / 1e9,
+                                 "hbm_peak_GBps": hbm_peak_gbps(),
+                                 "dram_write_bytes_per_launch": (json.load(open(tpath))["dram_bytes_write"]
+                                                                 if os.path.exists(tpath) else None)}}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = oracle_rate(cfg)
