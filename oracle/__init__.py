@@ -61,7 +61,7 @@ def _bind(path: str) -> C.CDLL:
         "od_rsqrt_array": (None, [_f32p, _f32p, u64]),
         "od_sqrt_array": (None, [_f32p, _f32p, u64]),
         "od_sincos2pi_array": (None, [_u32p, _f32p, _f32p, u64]),
-        "od_normal_quad": (None, [u64, u64, u64, u64, _f32p]),
+        "od_normal_acc": (None, [u64, u64, u64, u64, _f32p]),
         "od_normal_sextet": (None, [u64, u32, u32, u32, _f32p]),
         "od_pp_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u64, u64, u32, u64, u32, C.c_void_p]),
         "od_pp_trace": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u32, u64, u32, _f32p]),
@@ -174,9 +174,9 @@ def sincos2pi_array(a):
     return c, s
 
 
-def normal_quad(seed: int, unit: int, first: int, n: int) -> np.ndarray:
+def normal_acc(seed: int, unit: int, first: int, n: int) -> np.ndarray:
     out = np.zeros(n, np.float32)
-    lib().od_normal_quad(seed, unit, first, n, out)
+    lib().od_normal_acc(seed, unit, first, n, out)
     return out
 
 

@@ -180,17 +180,28 @@ static inline void od_key_of_seed(uint64_t seed, uint32_t key[2]) {
     key[1] = (uint32_t)(seed >> 32);
 }
 
-void od_normal_quad(uint64_t seed, uint64_t unit, uint64_t first, uint64_t n, float* out) {
+/* spec/RNG.md §6: the sextet packing of one Philox block X (three pairs) */
+static void od_sextet_of_block(const uint32_t X[4], float out[6]) {
+    uint32_t A0 = X[3] << 16;
+    uint32_t A1 = X[3] & 0xFFFF0000u;
+    uint32_t A2 = (X[0] << 24) | ((X[1] & 0xFFu) << 16);
+    od_bm_pair(X[0], A0, &out[0], &out[1]);
+    od_bm_pair(X[1], A1, &out[2], &out[3]);
+    od_bm_pair(X[2], A2, &out[4], &out[5]);
+}
+
+/* Accumulator-model normals [first, first+n) of unit U (stream 2): normal j is
+ * lane j mod 6 of the sextet of block X = Philox(key, (U_lo, j div 6, U_hi, 2)). */
+void od_normal_acc(uint64_t seed, uint64_t unit, uint64_t first, uint64_t n, float* out) {
     uint32_t key[2];
     od_key_of_seed(seed, key);
     for (uint64_t j = first; j < first + n; ++j) {
-        uint32_t ctr[4] = { (uint32_t)unit, (uint32_t)(j >> 2), (uint32_t)(unit >> 32), 2u };
+        uint32_t ctr[4] = { (uint32_t)unit, (uint32_t)(j / 6), (uint32_t)(unit >> 32), 2u };
         uint32_t X[4];
         od_philox4x32_10(ctr, key, X);
-        float z[4];
-        od_bm_pair(X[0], X[1] & 0xFFFFFF00u, &z[0], &z[1]);
-        od_bm_pair(X[2], X[3] & 0xFFFFFF00u, &z[2], &z[3]);
-        out[j - first] = z[j & 3];
+        float z[6];
+        od_sextet_of_block(X, z);
+        out[j - first] = z[j % 6];
     }
 }
 
@@ -200,12 +211,7 @@ void od_normal_sextet(uint64_t seed, uint32_t alloc, uint32_t sample, uint32_t i
     uint32_t ctr[4] = { alloc, sample, invocation, 1u };
     uint32_t X[4];
     od_philox4x32_10(ctr, key, X);
-    uint32_t A0 = X[3] << 16;
-    uint32_t A1 = X[3] & 0xFFFF0000u;
-    uint32_t A2 = (X[0] << 24) | ((X[1] & 0xFFu) << 16);
-    od_bm_pair(X[0], A0, &out[0], &out[1]);
-    od_bm_pair(X[1], A1, &out[2], &out[3]);
-    od_bm_pair(X[2], A2, &out[4], &out[5]);
+    od_sextet_of_block(X, out);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -418,7 +424,7 @@ void od_ddm_trial(const od_ddm_params* p, uint64_t seed, uint64_t trial,
     uint32_t st = 0;
     for (uint32_t n = 1; n <= p->n_steps; ++n) {
         float g;
-        od_normal_quad(seed, trial, n - 1, 1, &g);
+        od_normal_acc(seed, trial, n - 1, 1, &g);
         x = FFMA(nsd, g, FFMA(p->dt, p->drift, x));
         if (ch == 2) {
             if (x >= p->threshold) { ch = 0; st = n; }
@@ -460,7 +466,7 @@ void od_lci_trial(float input, float leak, float offset, float noise, float dt,
     uint32_t st = 0;
     for (uint32_t n = 1; n <= n_steps; ++n) {
         float g;
-        od_normal_quad(seed, unit, n - 1, 1, &g);
+        od_normal_acc(seed, unit, n - 1, 1, &g);
         x = FFMA(nsd, g, FADD(FFMA(dt, FFMA(-leak, x, input), x), offset));
         if (ch == 2) {
             if (x >= threshold) { ch = 0; st = n; }
@@ -495,7 +501,7 @@ void od_stroop_trial(const float P[11], float u_c, float u_s, uint64_t seed,
     for (uint32_t n = 1; n <= N; ++n) {
         for (int k = 0; k < 2; ++k) h[k] = FFMA(P[SP_TAU], FSUB(I[k], h[k]), h[k]);
         float g[2];
-        od_normal_quad(seed, unit, 2ull * (n - 1), 2, g);
+        od_normal_acc(seed, unit, 2ull * (n - 1), 2, g);
         float xn[2];
         for (int k = 0; k < 2; ++k) {
             float q = FFMA(-P[SP_INH], x[1 - k], FFMA(-P[SP_LEAK], x[k], h[k]));
@@ -703,7 +709,7 @@ void od_ext_stroop_trial_a(const float P[13], float u_c, float u_s, uint64_t see
     hit[0] = hit[1] = 0; step[0] = step[1] = 0;
     for (uint32_t n = 1; n <= (uint32_t)P[XS_ND]; ++n) {
         float g[2];
-        od_normal_quad(seed, unit, 2ull * (n - 1), 2, g);
+        od_normal_acc(seed, unit, 2ull * (n - 1), 2, g);
         x1 = FFMA(nsd, g[0], FFMA(P[XS_DT], A1, x1));
         x2 = FFMA(nsd, g[1], FFMA(P[XS_DT], A2, x2));
         if (!hit[0]) { if (x1 >= P[XS_Z]) { hit[0] = 1; step[0] = n; } else if (x1 <= -P[XS_Z]) { hit[0] = 2; step[0] = n; } }
@@ -728,7 +734,7 @@ void od_ext_stroop_trial_b(const float P[13], float u_c, float u_s, uint64_t see
     int hp = 0, hc = 0; uint32_t sp = 0, sc = 0;
     for (uint32_t n = 1; n <= (uint32_t)P[XS_ND]; ++n) {
         float g[2];
-        od_normal_quad(seed, unit, 2ull * (n - 1), 2, g);
+        od_normal_acc(seed, unit, 2ull * (n - 1), 2, g);
         xp = FFMA(nsd, g[1], FFMA(P[XS_DT], A2p, xp));
         xc = FFMA(nsd, g[0], FFMA(P[XS_DT], A1p, xc));
         if (!hp) { if (xp >= P[XS_Z]) { hp = 1; sp = n; } else if (xp <= -P[XS_Z]) { hp = 2; sp = n; } }

@@ -47,8 +47,8 @@ void  od_sincos2pi(uint32_t angle_word, float* c, float* s);
 void  od_ln_array(const float* x, float* y, uint64_t n);
 void  od_rsqrt_array(const float* x, float* y, uint64_t n);
 void  od_sincos2pi_array(const uint32_t* a, float* c, float* s, uint64_t n);
-/* normals [first, first+n) of unit U on stream 2, quad packing */
-void  od_normal_quad(uint64_t seed, uint64_t unit, uint64_t first, uint64_t n, float* out);
+/* normals [first, first+n) of unit U on stream 2 (accumulator models), sextet packing */
+void  od_normal_acc(uint64_t seed, uint64_t unit, uint64_t first, uint64_t n, float* out);
 /* the three 2-D noise vectors (prey, predator, player) of sample s: out[6] */
 void  od_normal_sextet(uint64_t seed, uint32_t alloc, uint32_t sample, uint32_t invocation, float* out);
 

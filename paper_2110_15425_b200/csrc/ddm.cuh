@@ -3,7 +3,8 @@
 // PAPER.md P:466 DDM, Fig. 3; "build histograms of outcomes").
 //
 // One thread = one trial (RNG unit = global trial id); the walk runs all N
-// steps (no divergence, reading Q14).  Per block: shared-memory u32 histograms
+// steps (no divergence, reading Q14); stream-2 normals come in sextets, two
+// Philox blocks (12 steps) at a time.  Per block: shared-memory u32 histograms
 // -> one global u64 atomicAdd per non-empty bin at the end (grid-stride, so
 // blocks are few and the flush is amortised over many trials).
 #pragma once
@@ -21,7 +22,7 @@ struct DDMArgs {
     unsigned long long* __restrict__ x_hist;   // [nx+2]
 };
 
-template <int BLOCK, int MINB = 0, int BMV = 0>
+template <int BLOCK, int MINB = 0>
 __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a) {
     extern __shared__ uint32_t s_hist[];  // [2*nb+1] rt bins then [nx+2] x bins
     const uint32_t n_rt = 2 * a.n_rt_bins + 1, n_x = a.n_x_bins + 2, n_all = n_rt + n_x;
@@ -41,43 +42,43 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
         rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
         float x = a.x0;
         uint32_t st = 0, ch = 2;
-        // Latch test: (x >= z) || (x <= -z)  <=>  |x| >= z for every z and
-        // non-NaN x (NaN fails both), so one max-|x| test per quad of steps
-        // (ALU pipe) finds the quads that hold a first passage; the rare quad
-        // that does is resolved step by step with the spec's compares.
-        const uint32_t nfull = a.n_steps >> 2;
-        const float dtA = a.dt, drift = a.drift;
-        for (uint32_t kb = 0; kb < nfull; ++kb) {
-            const float4 g = normal_quad_h<BMV>(rng, kb);
-            float xs[4];
-            x = __fmaf_rn(nsd, g.x, __fmaf_rn(dtA, drift, x)); xs[0] = x;
-            x = __fmaf_rn(nsd, g.y, __fmaf_rn(dtA, drift, x)); xs[1] = x;
-            x = __fmaf_rn(nsd, g.z, __fmaf_rn(dtA, drift, x)); xs[2] = x;
-            x = __fmaf_rn(nsd, g.w, __fmaf_rn(dtA, drift, x)); xs[3] = x;
+        // 12 steps per pair of sextet blocks.  Latch test: (x >= z) || (x <= -z)
+        // <=> |x| >= z for every z and non-NaN x (NaN fails both), so one
+        // max-|x| over the 12 states (ALU pipe) finds the group that holds the
+        // first passage; that rare group is resolved step by step in the spec's
+        // order.  The ragged last group is peeled.
+        const uint32_t n12 = a.n_steps / 12;
+        for (uint32_t j = 0; j < n12; ++j) {
+            float g[12], xs[12];
+            acc_normals12(rng, j, g);
+#pragma unroll
+            for (int l = 0; l < 12; ++l) { x = __fmaf_rn(nsd, g[l], __fmaf_rn(a.dt, a.drift, x)); xs[l] = x; }
             if (st == 0) {
-                const float m = fmaxf(fmaxf(fabsf(xs[0]), fabsf(xs[1])), fmaxf(fabsf(xs[2]), fabsf(xs[3])));
+                float m = fabsf(xs[0]);
+#pragma unroll
+                for (int l = 1; l < 12; ++l) m = fmaxf(m, fabsf(xs[l]));
                 if (m >= z) {
 #pragma unroll
-                    for (int l = 0; l < 4; ++l) {
+                    for (int l = 0; l < 12; ++l) {
                         if (st == 0) {
-                            if (xs[l] >= z) { st = 4 * kb + l + 1; ch = 0; }
-                            else if (xs[l] <= nz) { st = 4 * kb + l + 1; ch = 1; }
+                            if (xs[l] >= z) { st = 12 * j + l + 1; ch = 0; }
+                            else if (xs[l] <= nz) { st = 12 * j + l + 1; ch = 1; }
                         }
                     }
                 }
             }
         }
-        if (a.n_steps & 3u) {  // ragged last quad
-            const float4 g = normal_quad_h<BMV>(rng, nfull);
-            const float gg[4] = {g.x, g.y, g.z, g.w};
+        const uint32_t rem = a.n_steps - 12 * n12;
+        if (rem) {
+            float g[12];
+            acc_normals12(rng, n12, g);
 #pragma unroll
-            for (int l = 0; l < 3; ++l) {
-                const uint32_t n = 4 * nfull + l + 1;
-                if (n <= a.n_steps) {
-                    x = __fmaf_rn(nsd, gg[l], __fmaf_rn(dtA, drift, x));
+            for (int l = 0; l < 11; ++l) {
+                if ((uint32_t)l < rem) {
+                    x = __fmaf_rn(nsd, g[l], __fmaf_rn(a.dt, a.drift, x));
                     if (st == 0) {
-                        if (x >= z) { st = n; ch = 0; }
-                        else if (x <= nz) { st = n; ch = 1; }
+                        if (x >= z) { st = 12 * n12 + l + 1; ch = 0; }
+                        else if (x <= nz) { st = 12 * n12 + l + 1; ch = 1; }
                     }
                 }
             }

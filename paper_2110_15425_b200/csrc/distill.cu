@@ -48,8 +48,9 @@ distill_status fail(distill_status s, const char* fmt, ...) {
 constexpr int PP_BLOCK = 128;
 constexpr int ARGMAX_BLOCK = 256;
 constexpr int DDM_BLOCK = 128;
-constexpr int DDM_MINB = 0;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt)
-constexpr int STROOP_BLOCK = 256;
+constexpr int DDM_MINB = 6;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt, v5)
+constexpr int STROOP_BLOCK = 128;
+constexpr int STROOP_MINB = 6;   // same sweep
 
 }  // namespace
 
@@ -265,7 +266,7 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
         }
         for (uint64_t off = 0; off < count; off += 65535) {
             const unsigned gy = (unsigned)std::min<uint64_t>(65535, count - off);
-            stroop_sim_kernel<STROOP_BLOCK><<<dim3(chunks, gy), STROOP_BLOCK, 0, st>>>(p, (uint32_t)off);
+            stroop_sim_kernel<STROOP_BLOCK, STROOP_MINB><<<dim3(chunks, gy), STROOP_BLOCK, 0, st>>>(p, (uint32_t)off);
             g_launches++;
             CUDA_TRY(cudaGetLastError());
         }

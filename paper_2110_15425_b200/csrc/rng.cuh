@@ -322,16 +322,31 @@ struct PhiloxHoisted {
     }
 };
 
-// Quad normals 4k..4k+3 of a hoisted stream-2 unit: both Box-Muller pairs of the
-// block in the two lanes of one packed evaluation (spec/RNG.md §6, quad packing).
-// BMV selects the scalar (bit set) or packed-pair form of ln / rsqrt / sincos
-// (bits 1 / 2 / 4); all variants are the same binary32 operations.
-template <int BMV = 0>
-__device__ __forceinline__ float4 normal_quad_h(const PhiloxHoisted& rng, uint32_t k) {
-    const uint4 X = rng(k);
-    F2 zc, zs;
-    bm_pair2<(BMV & 1) != 0, (BMV & 2) != 0, (BMV & 4) != 0>(X.x, X.z, X.y & 0xFFFFFF00u, X.w & 0xFFFFFF00u, zc, zs);
-    return make_float4(zc.x, zs.x, zc.y, zs.y);
+// Sextet normals 12j..12j+11 of a hoisted stream unit: blocks 2j (lane x) and
+// 2j+1 (lane y), entity pairs e = 0, 1, 2 of each (spec/RNG.md §6 sextet
+// packing): normal 6b + 2e is zc[e], 6b + 2e + 1 is zs[e] of block b's lane.
+__device__ __forceinline__ void normal_sextet2_h(const PhiloxHoisted& rng, uint32_t j, F2 zc[3], F2 zs[3]) {
+    const uint4 X = rng(2 * j), Y = rng(2 * j + 1);
+    const uint32_t RX[3] = {X.x, X.y, X.z}, RY[3] = {Y.x, Y.y, Y.z};
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        const uint32_t wx = sextet_angle_word(X, e), wy = sextet_angle_word(Y, e);
+        F2 rs, cq, sq;
+        bm_polar2_fs<false, false, false, 0x7FFF00u>(RX[e], RY[e], wx, wy, wx, wy, rs, cq, sq);
+        zc[e] = Ops<false>::mul(rs, cq);
+        zs[e] = Ops<false>::mul(rs, sq);
+    }
+}
+
+// Twelve stream-2 normals 12j..12j+11 as an array in stream order (blocks 2j, 2j+1).
+__device__ __forceinline__ void acc_normals12(const PhiloxHoisted& rng, uint32_t j, float g[12]) {
+    F2 zc[3], zs[3];
+    normal_sextet2_h(rng, j, zc, zs);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        g[2 * e] = zc[e].x; g[2 * e + 1] = zs[e].x;
+        g[6 + 2 * e] = zc[e].y; g[6 + 2 * e + 1] = zs[e].y;
+    }
 }
 
 }  // namespace distill

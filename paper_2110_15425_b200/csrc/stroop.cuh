@@ -39,7 +39,7 @@ __device__ __forceinline__ void lca_step(const StroopArgs& a, float I0, float I1
     x1 = fmaxf(__fmaf_rn(nsd, g1, __fmaf_rn(a.dt, q1, x1)), 0.0f);
 }
 
-template <int BLOCK, int MINB = 0, int BMV = 0>
+template <int BLOCK, int MINB = 0>
 __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArgs a, uint32_t alloc_off) {
     const uint32_t t_alloc = alloc_off + blockIdx.y;           // index within [0, count)
     const uint32_t i = a.begin + t_alloc;
@@ -64,31 +64,47 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
         float h0 = 0.f, h1 = 0.f, x0 = 0.f, x1 = 0.f;
         int resp = -1;
         uint32_t st = 0;
-        // x_k >= 0 after the rectification (fmaxf(NaN, 0) = 0 as well), so
-        // "x0 >= θ or x1 >= θ" at either step of a quad block <=> the max of
-        // the four states >= θ: one test per two steps; the rare block that
-        // passes is resolved in the spec's order.
-        const uint32_t nfull = a.n_steps >> 1;    // 2 steps per quad block
-        for (uint32_t kb = 0; kb < nfull; ++kb) {
-            const float4 g = normal_quad_h<BMV>(rng, kb);
-            float xa0, xa1;
-            lca_step(a, I0, I1, nleak, ninh, nsd, g.x, g.y, h0, h1, x0, x1);
-            xa0 = x0; xa1 = x1;
-            lca_step(a, I0, I1, nleak, ninh, nsd, g.z, g.w, h0, h1, x0, x1);
-            if (resp < 0 && fmaxf(fmaxf(xa0, xa1), fmaxf(x0, x1)) >= a.thr) {
-                const uint32_t n = 2 * kb + 1;
-                if (xa0 >= a.thr) { resp = 0; st = n; }
-                else if (xa1 >= a.thr) { resp = 1; st = n; }
-                else if (x0 >= a.thr) { resp = 0; st = n + 1; }
-                else { resp = 1; st = n + 1; }
+        // Six steps (12 normals, two sextet blocks) per group.  x_k >= 0 after
+        // the rectification (fmaxf(NaN, 0) = 0 as well), so "x0 >= θ or x1 >= θ"
+        // at any step of the group <=> the max of its 12 states >= θ: one test
+        // per group; the rare group that passes is resolved in the spec's order.
+        const uint32_t n6 = a.n_steps / 6;
+        for (uint32_t j = 0; j < n6; ++j) {
+            float g[12], s0[6], s1[6];
+            acc_normals12(rng, j, g);
+#pragma unroll
+            for (int l = 0; l < 6; ++l) {
+                lca_step(a, I0, I1, nleak, ninh, nsd, g[2 * l], g[2 * l + 1], h0, h1, x0, x1);
+                s0[l] = x0; s1[l] = x1;
+            }
+            if (resp < 0) {
+                float m = fmaxf(s0[0], s1[0]);
+#pragma unroll
+                for (int l = 1; l < 6; ++l) m = fmaxf(m, fmaxf(s0[l], s1[l]));
+                if (m >= a.thr) {
+#pragma unroll
+                    for (int l = 0; l < 6; ++l) {
+                        if (resp < 0) {
+                            if (s0[l] >= a.thr) { resp = 0; st = 6 * j + l + 1; }
+                            else if (s1[l] >= a.thr) { resp = 1; st = 6 * j + l + 1; }
+                        }
+                    }
+                }
             }
         }
-        if (a.n_steps & 1u) {  // ragged last step
-            const float4 g = normal_quad_h<BMV>(rng, nfull);
-            lca_step(a, I0, I1, nleak, ninh, nsd, g.x, g.y, h0, h1, x0, x1);
-            if (resp < 0) {
-                if (x0 >= a.thr) { resp = 0; st = a.n_steps; }
-                else if (x1 >= a.thr) { resp = 1; st = a.n_steps; }
+        const uint32_t rem = a.n_steps - 6 * n6;
+        if (rem) {  // ragged last group
+            float g[12];
+            acc_normals12(rng, n6, g);
+#pragma unroll
+            for (int l = 0; l < 5; ++l) {
+                if ((uint32_t)l < rem) {
+                    lca_step(a, I0, I1, nleak, ninh, nsd, g[2 * l], g[2 * l + 1], h0, h1, x0, x1);
+                    if (resp < 0) {
+                        if (x0 >= a.thr) { resp = 0; st = 6 * n6 + l + 1; }
+                        else if (x1 >= a.thr) { resp = 1; st = 6 * n6 + l + 1; }
+                    }
+                }
             }
         }
         if (resp < 0) ++n_und;
@@ -194,33 +210,48 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
         float x1 = 0.0f, x2 = 0.0f;
         int h1t = 0, h2t = 0;
         uint32_t s1 = 0, s2 = 0;
-        // 2 steps (4 normals) per quad block; each DDM's latch is tested once
-        // per block on max(|x|) (|x| >= z <=> x >= z or x <= -z, DDM kernel).
-        const uint32_t nfull = a.n_d >> 1;
-        for (uint32_t kb = 0; kb < nfull; ++kb) {
-            const float4 g = normal_quad_h(rng, kb);
-            float x1a, x2a;
-            if (VARIANT == 0) {
-                x1a = x1 = __fmaf_rn(nsd, g.x, __fmaf_rn(a.dt, A1, x1));
-                x2a = x2 = __fmaf_rn(nsd, g.y, __fmaf_rn(a.dt, A2, x2));
-                x1 = __fmaf_rn(nsd, g.z, __fmaf_rn(a.dt, A1, x1));
-                x2 = __fmaf_rn(nsd, g.w, __fmaf_rn(a.dt, A2, x2));
-            } else {
-                x2a = x2 = __fmaf_rn(nsd, g.y, __fmaf_rn(a.dt, A2, x2));
-                x1a = x1 = __fmaf_rn(nsd, g.x, __fmaf_rn(a.dt, A1, x1));
-                x2 = __fmaf_rn(nsd, g.w, __fmaf_rn(a.dt, A2, x2));
-                x1 = __fmaf_rn(nsd, g.z, __fmaf_rn(a.dt, A1, x1));
+        // Six steps (12 normals) per group; each DDM's latch is tested once per
+        // group on max |x| (|x| >= z <=> x >= z or x <= -z, DDM kernel).
+        const uint32_t n6 = a.n_d / 6;
+        for (uint32_t j = 0; j < n6; ++j) {
+            float g[12], y1[6], y2[6];
+            acc_normals12(rng, j, g);
+#pragma unroll
+            for (int l = 0; l < 6; ++l) {
+                if (VARIANT == 0) {
+                    x1 = __fmaf_rn(nsd, g[2 * l], __fmaf_rn(a.dt, A1, x1));
+                    x2 = __fmaf_rn(nsd, g[2 * l + 1], __fmaf_rn(a.dt, A2, x2));
+                } else {
+                    x2 = __fmaf_rn(nsd, g[2 * l + 1], __fmaf_rn(a.dt, A2, x2));
+                    x1 = __fmaf_rn(nsd, g[2 * l], __fmaf_rn(a.dt, A1, x1));
+                }
+                y1[l] = x1; y2[l] = x2;
             }
-            const uint32_t n = 2 * kb + 1;
-            if (!h1t && fmaxf(fabsf(x1a), fabsf(x1)) >= a.z) { ddm_latch(x1a, a.z, n, h1t, s1); ddm_latch(x1, a.z, n + 1, h1t, s1); }
-            if (!h2t && fmaxf(fabsf(x2a), fabsf(x2)) >= a.z) { ddm_latch(x2a, a.z, n, h2t, s2); ddm_latch(x2, a.z, n + 1, h2t, s2); }
+            float m1 = fabsf(y1[0]), m2 = fabsf(y2[0]);
+#pragma unroll
+            for (int l = 1; l < 6; ++l) { m1 = fmaxf(m1, fabsf(y1[l])); m2 = fmaxf(m2, fabsf(y2[l])); }
+            if (!h1t && m1 >= a.z) {
+#pragma unroll
+                for (int l = 0; l < 6; ++l) ddm_latch(y1[l], a.z, 6 * j + l + 1, h1t, s1);
+            }
+            if (!h2t && m2 >= a.z) {
+#pragma unroll
+                for (int l = 0; l < 6; ++l) ddm_latch(y2[l], a.z, 6 * j + l + 1, h2t, s2);
+            }
         }
-        if (a.n_d & 1u) {  // ragged last step
-            const float4 g = normal_quad_h(rng, nfull);
-            x1 = __fmaf_rn(nsd, g.x, __fmaf_rn(a.dt, A1, x1));
-            x2 = __fmaf_rn(nsd, g.y, __fmaf_rn(a.dt, A2, x2));
-            ddm_latch(x1, a.z, a.n_d, h1t, s1);
-            ddm_latch(x2, a.z, a.n_d, h2t, s2);
+        const uint32_t rem = a.n_d - 6 * n6;
+        if (rem) {  // ragged last group
+            float g[12];
+            acc_normals12(rng, n6, g);
+#pragma unroll
+            for (int l = 0; l < 5; ++l) {
+                if ((uint32_t)l < rem) {
+                    x1 = __fmaf_rn(nsd, g[2 * l], __fmaf_rn(a.dt, A1, x1));
+                    x2 = __fmaf_rn(nsd, g[2 * l + 1], __fmaf_rn(a.dt, A2, x2));
+                    ddm_latch(x1, a.z, 6 * n6 + l + 1, h1t, s1);
+                    ddm_latch(x2, a.z, 6 * n6 + l + 1, h2t, s2);
+                }
+            }
         }
         if (h1t == 0 || h2t == 0) { ++n_und; continue; }
         n_both += (h1t == 1 && h2t == 1);

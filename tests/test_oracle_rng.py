@@ -115,20 +115,25 @@ def test_sincos2pi_exhaustive_24bit(orc):
     assert orc.sincos2pi(1 << 30) == (1.0, 0.0)
 
 
-def test_box_muller_pair_matches_definition(orc):
-    """Quad normals equal sqrt(-2 ln u1)(cos, sin)(2 pi t) from the raw Philox
-    words (binary64 libm), within the primitives' error bounds."""
-    seed, unit = 12345, 77
-    for blk in range(64):
-        X = orc.philox([unit, blk, 0, 2], [seed & 0xFFFFFFFF, seed >> 32])
-        z = orc.normal_quad(seed, unit, 4 * blk, 4)
-        for p in range(2):
-            R, A = int(X[2 * p]), int(X[2 * p + 1]) & 0xFFFFFF00
-            u1 = ((R >> 8) | 1) * 2.0 ** -24
-            rad = math.sqrt(-2 * math.log(u1))
-            th = 2 * math.pi * A / 2.0 ** 32 - math.pi / 2
-            assert abs(z[2 * p] - rad * math.cos(th)) <= 1e-6 * max(1, rad)
-            assert abs(z[2 * p + 1] - rad * math.sin(th)) <= 1e-6 * max(1, rad)
+def test_accumulator_normals_match_definition(orc):
+    """Stream-2 (accumulator) normals 6k..6k+5 of a unit are the sextet of block
+    Philox(key, (U_lo, k, U_hi, 2)): sqrt(-2 ln u1)(cos, sin)(2 pi A / 2^32 - pi/2)
+    from the raw words (binary64 libm), within the primitives' error bounds, and
+    a 64-bit unit id splits into (lo, hi) counter words."""
+    seed = 12345
+    for unit in (77, (5 << 32) | 9):
+        z = orc.normal_acc(seed, unit, 0, 6 * 64)
+        for blk in range(64):
+            X = [int(v) for v in orc.philox([unit & 0xFFFFFFFF, blk, unit >> 32, 2], [seed & 0xFFFFFFFF, seed >> 32])]
+            A = [(X[3] << 16) & 0xFFFFFFFF, X[3] & 0xFFFF0000, ((X[0] << 24) | ((X[1] & 0xFF) << 16)) & 0xFFFFFFFF]
+            for e in range(3):
+                u1 = ((X[e] >> 8) | 1) * 2.0 ** -24
+                rad = math.sqrt(-2 * math.log(u1))
+                th = 2 * math.pi * A[e] / 2.0 ** 32 - math.pi / 2
+                assert abs(z[6 * blk + 2 * e] - rad * math.cos(th)) <= 1e-6 * max(1, rad)
+                assert abs(z[6 * blk + 2 * e + 1] - rad * math.sin(th)) <= 1e-6 * max(1, rad)
+        # any window [first, first+n) is the same stream
+        assert np.array_equal(orc.normal_acc(seed, unit, 17, 50), z[17:67])
 
 
 def test_sextet_packing_matches_definition(orc):
@@ -145,10 +150,10 @@ def test_sextet_packing_matches_definition(orc):
             assert abs(z[2 * e + 1] - rad * math.sin(th)) <= 1e-6 * max(1, rad)
 
 
-def test_quad_normals_moments_and_ks(orc):
+def test_accumulator_normals_moments_and_ks(orc):
     """10^6 normals: mean within +-0.004, variance within +-0.01 (S:343 bounds),
     kurtosis 3, KS vs Phi."""
-    z = np.concatenate([orc.normal_quad(7, u, 0, 10000) for u in range(100)]).astype(np.float64)
+    z = np.concatenate([orc.normal_acc(7, u, 0, 10000) for u in range(100)]).astype(np.float64)
     assert abs(z.mean()) < 0.004
     assert abs(z.var() - 1) < 0.01
     assert abs(((z - z.mean()) ** 4).mean() - 3) < 0.05
