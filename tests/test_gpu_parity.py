@@ -210,7 +210,10 @@ def _ddm_p(orc, d):
 
 @pytest.mark.parametrize("kw,t0,t1", [({}, 0, 4000), ({"n_steps": 333, "rt_bin_steps": 7}, 1000, 3001),
                                        ({"drift": -0.3, "noise": 2.0, "threshold": 2.5}, 123456, 125000),
-                                       ({"n_steps": 1}, 0, 100)])
+                                       ({"n_steps": 1}, 0, 100), ({"n_steps": 12, "threshold": 0.3}, 0, 3000),
+                                       ({"n_steps": 23, "threshold": 0.4, "rt_bin_steps": 1}, 7, 2500),
+                                       ({"n_steps": 24, "threshold": -0.5}, 0, 100),
+                                       ({"n_steps": 36, "threshold": 0.0, "noise": 0.01}, 0, 50)])
 def test_ddm_histograms_bit_exact(D, orc, kw, t0, t1):
     import os
     d = W.DDMConfig(**kw)
