@@ -113,6 +113,51 @@ __global__ void k_i2f(float* out, uint32_t m) {
     if (f == 1234.5f) out[threadIdx.x] = 1;
 }
 
+// I2FP.F32.U32 throughput (8 independent chains; the float result feeds back as bits)
+__global__ void k_i2fp(float* out, uint32_t m) {
+    uint32_t a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+    for (int it = 0; it < N_ITER; ++it) {
+        a0 = __float_as_uint(__uint2float_rn(a0 ^ m)); a1 = __float_as_uint(__uint2float_rn(a1 ^ m));
+        a2 = __float_as_uint(__uint2float_rn(a2 ^ m)); a3 = __float_as_uint(__uint2float_rn(a3 ^ m));
+        a4 = __float_as_uint(__uint2float_rn(a4 ^ m)); a5 = __float_as_uint(__uint2float_rn(a5 ^ m));
+        a6 = __float_as_uint(__uint2float_rn(a6 ^ m)); a7 = __float_as_uint(__uint2float_rn(a7 ^ m));
+    }
+    if ((a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7) == 12345) out[threadIdx.x] = 1;
+}
+// 8 FFMA2 + 2 I2FP per iteration (does the conversion overlap the FMA datapath?)
+__global__ void k_mix_ffma2_i2fp(float* out, float s, uint32_t m) {
+    float2 f[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = make_float2(threadIdx.x + j, j);
+    const float2 S = make_float2(s, s), H = make_float2(0.5f, 0.5f);
+    uint32_t u0 = threadIdx.x, u1 = u0 + 5;
+    for (int it = 0; it < N_ITER; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = __ffma2_rn(f[j], S, H);
+        u0 = __float_as_uint(__uint2float_rn(u0 ^ m)); u1 = __float_as_uint(__uint2float_rn(u1 ^ m));
+    }
+    float t = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += f[j].x + f[j].y;
+    if (t + (float)(u0 ^ u1) == 1234.5f) out[threadIdx.x] = 1;
+}
+__global__ void k_ffma2_8(float* out, float s, uint32_t m) {
+    float2 f[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = make_float2(threadIdx.x + j, j);
+    const float2 S = make_float2(s, s), H = make_float2(0.5f, 0.5f);
+    uint32_t u0 = threadIdx.x, u1 = u0 + 5;
+    for (int it = 0; it < N_ITER; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = __ffma2_rn(f[j], S, H);
+        u0 = (u0 ^ m) + 3; u1 = (u1 ^ m) + 5;
+    }
+    float t = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += f[j].x + f[j].y;
+    if (t + (float)(u0 ^ u1) == 1234.5f) out[threadIdx.x] = 1;
+}
+
 template <typename K, typename... Args>
 void bench(const char* name, int insts_per_iter, K kern, Args... args) {
     float* out; cudaMalloc(&out, 1 << 20);
@@ -143,6 +188,9 @@ int main() {
     bench("4 FFMA2 + 1 IMAD.WIDE", 5, k_mix_ffma2_imadwide, 1.0001f, 0xD2511F53u);
     bench("8 FFMA + 1 IMAD.WIDE", 9, k_mix_ffma_imadwide, 1.0001f, 0xD2511F53u);
     bench("4 FFMA2 + 4 LOP3", 8, k_mix_ffma2_lop3, 1.0001f, 0xD2511F53u);
+    bench("I2FP.F32.U32 (+LOP3)", 8, k_i2fp, 0xD2511F53u);
+    bench("8 FFMA2 + 2 int ops (iter)", 1, k_ffma2_8, 1.0001f, 0xD2511F53u);
+    bench("8 FFMA2 + 2 I2FP (iter)", 1, k_mix_ffma2_i2fp, 1.0001f, 0xD2511F53u);
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
