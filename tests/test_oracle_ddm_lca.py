@@ -142,3 +142,36 @@ def test_stroop_value_is_correctly_rounded_binary64_formula(orc):
         exact = (F(float(P[8])) * nc / 300 - F(float(P[9])) * F(float(P[6])) * (rs + nu * 200) / 300
                  - (F(float(w[0])) * F(1, 2) + F(float(w[1])) * F(1, 4)))
         assert abs(F(float(v)) - exact) <= abs(exact) * F(1, 2 ** 23) + F(1, 2 ** 60)
+
+
+def test_stroop_lca_unit_is_reflected_brownian_motion(orc):
+    """Closed-form pin for the noisy, rectified LCA unit (spec/MODELS.md §6).
+
+    With tau = 1 (pathway input reaches h in one step), no leak, no inhibition,
+    and the competing unit held at 0 by a strongly negative word input
+    (incongruent trial, g_w = -50), the colour unit is an Euler walk with drift
+    mu = g_c u_c and noise sigma, projected onto x >= 0 and absorbed at theta:
+    reflected Brownian motion with drift, whose mean first-passage time from 0 is
+        E[T] = theta/mu - sigma^2/(2 mu^2) (1 - exp(-2 mu theta / sigma^2)).
+    Discrete monitoring moves both barriers out by beta sigma sqrt(dt),
+    beta = 0.5826 (Siegmund's correction at the absorbing barrier, as in the
+    DDM pin; the same constant at the projected reflecting barrier), i.e.
+    theta_eff = theta + 2 beta sigma sqrt(dt).  Without the rectification the
+    mean would be theta_eff/mu (~0.26 s here) and without the discretisation
+    shift 0.142 s: both are rejected by > 8 SE."""
+    P = W.STROOP_PARAMS.copy()
+    mu, sig, th, dt, N = 2.0, 1.0, 0.5, 5e-4, 3000
+    P[0], P[1], P[2], P[3], P[4], P[5], P[6], P[7], P[10] = mu, -50.0, 1.0, 0.0, 0.0, sig, dt, th, N
+    n = 8000
+    resp, st = np.array([orc.stroop_trial(P, 1.0, 0.0, 5, u, 1) for u in range(n)]).T
+    assert np.all(resp == 0)                     # the colour unit always answers
+    T = st.astype(np.float64) * dt
+    se = T.std() / math.sqrt(n)
+
+    def ET(theta):
+        return theta / mu - sig ** 2 / (2 * mu ** 2) * (1 - math.exp(-2 * mu * theta / sig ** 2))
+
+    th_eff = th + 2 * 0.5826 * sig * math.sqrt(dt)
+    assert abs(T.mean() - ET(th_eff)) <= 4 * se + 0.01 * ET(th_eff), (T.mean(), ET(th_eff), se)
+    assert abs(T.mean() - th_eff / mu) > 50 * se          # power: rectification matters
+    assert abs(T.mean() - ET(th)) > 8 * se                # power: the discretisation shift matters
