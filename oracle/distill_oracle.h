@@ -18,16 +18,19 @@
  *   od_pp_eval           pinned: zero-noise closed forms, monotonicity, planted optimum,
  *                        small-noise delta-method expectation, fp64 re-evaluation
  *   od_argmax_keys       pinned: brute-force min over (C, i), NaN/-0 rules
+ *   od_normal_acc        pinned: raw-word Box-Muller definition, moments/kurtosis/KS; cuRAND Philox
  *   od_ddm_*             pinned: zero-noise first passage, closed-form ER/DT, endpoint law
  *   od_lci_trial         pinned: Fig. 3 clone relation to od_ddm_trial (bit-identical)
- *   od_stroop_eval       pinned: zero-noise deterministic RT, conservation, Stroop effect;
- *                        absolute values parity unpinned (the paper prints none)
+ *   od_stroop_eval       pinned: zero-noise deterministic RT, conservation, Stroop effect,
+ *                        reflected-BM closed-form mean first passage of the noisy unit;
+ *                        absolute values at the cfg4 constants parity unpinned (the paper prints none)
  *   od_pp_episode        pinned: closed-form straight-chase capture step, one-step predator capture,
  *                        per-step keys = ordinary grid searches
  *   od_argmax_random_ties pinned: uniform 1/8 frequency over 10^4 seeds, unique minimum wins
  *   od_pp_amr            pinned: zero-noise planted corner every round, Fig. 4 analogue vs a fine scan
  *   od_ext_stroop_*      pinned: A == B bit-identical, zero-noise drift signs / conflict
- *                        slowing / binary32 first passage; absolute values parity unpinned
+ *                        slowing / binary32 first passage, closed-form P(both correct) from the
+ *                        two DDM error rates; absolute values at the bench constants parity unpinned
  */
 #ifndef DISTILL_ORACLE_H
 #define DISTILL_ORACLE_H

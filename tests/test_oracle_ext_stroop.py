@@ -1,4 +1,6 @@
 """Pins for the Extended Stroop A/B oracle (spec/MODELS.md §10)."""
+import math
+
 import numpy as np
 
 import workloads as W
@@ -59,3 +61,45 @@ def test_counts_conserve(orc):
     counts, _ = orc.ext_stroop_eval(0, c.n_levels, c.levels, c.w, c.params, 5, 17, c.n_trials, c.seed)
     assert (counts[:, 0] + counts[:, 1] <= c.n_trials).all()
     assert (counts[:, 2] <= (c.n_trials - counts[:, 1]) * int(c.params[10])).all()
+
+
+def test_both_ddms_follow_the_closed_form_error_rates(orc):
+    """Closed-form pin for Extended Stroop (spec/MODELS.md §10): the
+    front-end is a geometric series, h_k = I_k (1 - (1 - tau)^N_h) in real
+    arithmetic, so the two DDM drifts are A1 = (h_c - h_w) lambda and
+    A2 = a_p - gamma h_c h_w; the DDMs draw disjoint normals, so
+    P(both hit the upper bound) = (1 - ER(A1)) (1 - ER(A2)) with the DDM error
+    rate ER(A) = 1 / (1 + exp(2 A z' / sigma^2)), z' = z + 0.5826 sigma sqrt(dt)
+    (Siegmund, as in the DDM pin), over a horizon long enough that no trial is
+    undecided.  Congruent and incongruent stimuli; a flipped conflict sign or
+    swapped colour/word pathways is rejected."""
+    P = W.EXT_STROOP_PARAMS.copy()
+    dt = 0.002
+    P[8], P[10] = dt, 2500
+    g_c, g_w, tau, Nh, lam, a_p, gam, sig, _, z = (float(v) for v in P[:10])
+    u_c, u_s = 1.0, 0.5
+    ic, iw = g_c * u_c, g_w * (1 - u_s)
+    f = 1 - (1 - tau) ** Nh
+    zp = z + 0.5826 * sig * math.sqrt(dt)
+
+    def er(A):
+        return 1 / (1 + math.exp(2 * A * zp / sig ** 2))
+
+    n = 4000
+    for trial, (Ic, Iw) in ((0, (ic + iw, 0.0)), (1, (ic, iw))):     # congruent, incongruent (colour 0)
+        hc, hw = Ic * f, Iw * f
+        A1, A2 = (hc - hw) * lam, a_p - gam * hc * hw
+        both = und = 0
+        for u in range(n):
+            (h1, h2), _ = orc.ext_stroop_trial(0, P, u_c, u_s, 9, u, trial)
+            both += (h1 == 1 and h2 == 1)
+            und += (h1 == 0 or h2 == 0)
+        assert und == 0
+        p = both / n
+        pred = (1 - er(A1)) * (1 - er(A2))
+        se = math.sqrt(pred * (1 - pred) / n)
+        assert abs(p - pred) <= 4 * se + 0.005, (trial, p, pred, se)
+        if trial == 1:
+            wrong_sign = (1 - er(A1)) * (1 - er(a_p + gam * hc * hw))
+            swapped = (1 - er(-A1)) * (1 - er(A2))
+            assert abs(p - wrong_sign) > 4 * se and abs(p - swapped) > 4 * se
