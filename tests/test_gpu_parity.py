@@ -577,3 +577,9 @@ def test_eval_grid_multi_cfg3_x16_matches_single_calls(D, orc):
             w = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, sets[t], int(i), int(i) + 1,
                             cfg.n_samples, cfg.seed, invocation=t)
             assert _bits(row[int(i)]) == _bits(w)[0]
+
+
+def test_graft_entry_smoke():
+    """The driver's smoke(): cfg1 costs + key and a DDM batch bit-exact on cuda:0."""
+    import __graft_entry__
+    __graft_entry__.smoke()
