@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
         const uint32_t rem = a.n_steps - 12 * n12;
         if (rem) {
             float g[12];
-            acc_normals12(rng, n12, g);
+            acc_normals_tail(rng, n12, rem, g);
 #pragma unroll
             for (int l = 0; l < 11; ++l) {
                 if ((uint32_t)l < rem) {

@@ -349,4 +349,21 @@ __device__ __forceinline__ void acc_normals12(const PhiloxHoisted& rng, uint32_t
     }
 }
 
+// Ragged tail: normals 12j..12j+n-1 (n <= 11).  When n <= 6 only block 2j is
+// drawn (pairs 0/1 in the two lanes, pair 2 in a second evaluation), saving a
+// Philox block and a third of the Box-Muller work; same values as acc_normals12.
+__device__ __forceinline__ void acc_normals_tail(const PhiloxHoisted& rng, uint32_t j, uint32_t n, float g[12]) {
+    if (n > 6) { acc_normals12(rng, j, g); return; }
+    const uint4 X = rng(2 * j);
+    const uint32_t w0 = sextet_angle_word(X, 0), w1 = sextet_angle_word(X, 1), w2 = sextet_angle_word(X, 2);
+    F2 rs, cq, sq;
+    bm_polar2_fs<false, false, false, 0x7FFF00u>(X.x, X.y, w0, w1, w0, w1, rs, cq, sq);
+    const F2 zc01 = Ops<false>::mul(rs, cq), zs01 = Ops<false>::mul(rs, sq);
+    bm_polar2_fs<false, false, false, 0x7FFF00u>(X.z, X.z, w2, w2, w2, w2, rs, cq, sq);
+    const F2 zc2 = Ops<false>::mul(rs, cq), zs2 = Ops<false>::mul(rs, sq);
+    g[0] = zc01.x; g[1] = zs01.x; g[2] = zc01.y; g[3] = zs01.y; g[4] = zc2.x; g[5] = zs2.x;
+#pragma unroll
+    for (int l = 6; l < 12; ++l) g[l] = 0.0f;   // never read (n <= 6)
+}
+
 }  // namespace distill

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
         const uint32_t rem = a.n_steps - 6 * n6;
         if (rem) {  // ragged last group
             float g[12];
-            acc_normals12(rng, n6, g);
+            acc_normals_tail(rng, n6, 2 * rem, g);
 #pragma unroll
             for (int l = 0; l < 5; ++l) {
                 if ((uint32_t)l < rem) {
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
         const uint32_t rem = a.n_d - 6 * n6;
         if (rem) {  // ragged last group
             float g[12];
-            acc_normals12(rng, n6, g);
+            acc_normals_tail(rng, n6, 2 * rem, g);
 #pragma unroll
             for (int l = 0; l < 5; ++l) {
                 if ((uint32_t)l < rem) {
