@@ -22,15 +22,26 @@ def _stream_handle(stream) -> Optional[int]:
     return stream.cuda_stream
 
 
-def _dev_ptr(t, dtype_name: str, numel: Optional[int] = None):
+# element type each named buffer must have (the C ABI's float* / u64* / int*);
+# u64 buffers are int64 tensors holding the raw bit pattern
+_BUF_DTYPE = {"net": "float32", "values": "float32", "inputs": "float32", "traj": "float32",
+              "boxes": "float32", "levels": "float32",
+              "best": "int64", "tie": "int64", "keys": "int64", "counts": "int64",
+              "rt_hist": "int64", "rt_sum": "int64", "x_hist": "int64", "status": "int32"}
+
+
+def _dev_ptr(t, name: str, numel: Optional[int] = None):
     if t is None:
         return None
     if not t.is_cuda:
-        raise ValueError(f"{dtype_name} buffer must be a CUDA tensor")
+        raise ValueError(f"{name} buffer must be a CUDA tensor")
     if not t.is_contiguous():
-        raise ValueError(f"{dtype_name} buffer must be contiguous")
+        raise ValueError(f"{name} buffer must be contiguous")
+    want = _BUF_DTYPE.get(name)
+    if want is not None and str(t.dtype) != f"torch.{want}":
+        raise ValueError(f"{name} buffer must be {want}, got {t.dtype}")
     if numel is not None and t.numel() < numel:
-        raise ValueError(f"{dtype_name} buffer too small: {t.numel()} < {numel}")
+        raise ValueError(f"{name} buffer too small: {t.numel()} < {numel}")
     return t.data_ptr()
 
 
@@ -101,7 +112,7 @@ def eval_grid_multi(model: Model, inputs, n_invocations: int, n_samples: int, se
     `inputs` is a CUDA float32 tensor [n_sets, 6]; net [T, end-begin] and best [T] as in eval_grid."""
     end = model.n_alloc if end is None else int(end)
     n, T = end - int(begin), int(n_invocations)
-    if inputs.dtype.itemsize != 4 or inputs.dim() != 2 or inputs.shape[1] != 6:
+    if inputs.dim() != 2 or inputs.shape[1] != 6:
         raise ValueError("inputs must be a float32 CUDA tensor of shape [n_sets, 6]")
     a = _abi.MultiArgs(_dev_ptr(inputs, "inputs"), int(inputs.shape[0]), T, int(invocation0), int(n_samples),
                        int(begin), end, int(seed) & (2 ** 64 - 1), _dev_ptr(net, "net", T * n),

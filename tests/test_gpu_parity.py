@@ -583,3 +583,20 @@ def test_graft_entry_smoke():
     """The driver's smoke(): cfg1 costs + key and a DDM batch bit-exact on cuda:0."""
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+def test_binding_rejects_wrong_buffer_dtypes(D):
+    """The thin binding checks element types before calling the ABI (a float64
+    net or an int32 key buffer would otherwise be silently misread)."""
+    import torch
+    cfg = W.pp_cfg1()
+    m = _model(D, cfg)
+    good_net = torch.empty(cfg.n_alloc, dtype=torch.float32, device="cuda")
+    good_best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError, match="float32"):
+        D.eval_grid(m, cfg.inputs, cfg.n_samples, cfg.seed, net=good_net.double(), best=good_best)
+    with pytest.raises(ValueError, match="int64"):
+        D.eval_grid(m, cfg.inputs, cfg.n_samples, cfg.seed, net=good_net, best=good_best.int())
+    with pytest.raises(ValueError, match="int64"):
+        D.argmax(good_net, 0, good_best.float())
+    D.eval_grid(m, cfg.inputs, cfg.n_samples, cfg.seed, net=good_net, best=good_best)   # still fine
