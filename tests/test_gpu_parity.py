@@ -600,3 +600,33 @@ def test_binding_rejects_wrong_buffer_dtypes(D):
     with pytest.raises(ValueError, match="int64"):
         D.argmax(good_net, 0, good_best.float())
     D.eval_grid(m, cfg.inputs, cfg.n_samples, cfg.seed, net=good_net, best=good_best)   # still fine
+
+
+def test_seed_sweep_1_to_100(D, orc):
+    """SURVEY §8(d) / S:569: parity over seeds 1..100 — cfg1 costs and keys for
+    every seed, a small DDM batch and a small Stroop grid for every tenth."""
+    import torch
+    cfg = W.pp_cfg1()
+    m = _model(D, cfg)
+    ms = D.load_model(W.KIND_STROOP_LCA, (3, 4), np.linspace(0, 1, 7).astype(np.float32), W.STROOP_W,
+                      W.STROOP_PARAMS, device=0)
+    for seed in range(1, 101):
+        C, key = _gpu_pp(D, m, cfg, seed=seed)
+        want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc,
+                           cfg.n_samples, seed)
+        assert np.array_equal(_bits(C), _bits(want)), seed
+        assert key == orc.argmax_net(-want)[0], seed
+        if seed % 10 == 0:
+            d = W.DDMConfig(n_steps=150, n_trials=700)
+            got = _ddm_gpu(D, d, 0, d.n_trials, seed)
+            for g, w in zip(got, orc.ddm_batch(_ddm_p(orc, d), seed, 0, d.n_trials)):
+                assert np.array_equal(g, w), seed
+            n = 12
+            counts = torch.zeros(3 * n, dtype=torch.int64, device="cuda")
+            net = torch.empty(n, dtype=torch.float32, device="cuda")
+            D.eval_grid(ms, None, 90, seed, 0, n, net=net, counts=counts)
+            torch.cuda.synchronize()
+            wc, wn = orc.stroop_eval((3, 4), np.linspace(0, 1, 7).astype(np.float32), W.STROOP_W, W.STROOP_PARAMS,
+                                     0, n, 90, seed)
+            assert np.array_equal(counts.cpu().numpy().astype(np.uint64).reshape(n, 3), wc), seed
+            assert np.array_equal(_bits(net.cpu().numpy()), _bits(wn)), seed
