@@ -356,7 +356,8 @@ def run_ours(args):
            "e2e": {"value": evals / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                    "api": "distill_eval_grid_host (positions in via launch params; net values stored by the "
-                          "kernel straight into pinned host memory, zero-copy; best key copied back)"},
+                          "kernel straight into pinned host memory, zero-copy; the best key published by the "
+                          "kernel's last block into pinned memory: one launch per call)"},
            "clocks": clocks, "gpu_launches": launches, "gpu_launches_per_step": launches / K,
            "also": also}
     print(json.dumps(out), flush=True)

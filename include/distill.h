@@ -187,8 +187,10 @@ distill_status distill_eval_grid_multi(const distill_model* model, const distill
  * returns V in h_net (if non-NULL) and the best key in *h_best, synchronises the
  * stream.  Pinned (cudaHostAlloc / page-locked, device-mapped) h_net is written by
  * the kernel directly (zero-copy, overlapped with the computation); pageable h_net
- * goes through a library-owned device scratch area and one copy.  Serialised per
- * handle (the scratch area is shared). */
+ * goes through a library-owned device scratch area and one copy.  A pinned h_best
+ * receives the key from the kernel's last block, which also re-arms the library's
+ * device key, so the whole call is one kernel launch; a pageable h_best costs a
+ * memset and a copy.  Serialised per handle (the scratch area is shared). */
 distill_status distill_eval_grid_host(const distill_model* model, const float* h_inputs, uint32_t n_inputs,
                                       uint64_t begin, uint64_t end, uint32_t n_samples,
                                       uint32_t invocation, uint64_t seed,

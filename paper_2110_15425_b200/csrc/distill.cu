@@ -69,12 +69,18 @@ struct distill_model {
     size_t scratch_bytes = 0;
 };
 
+// Scratch layout (eval_grid_host): [0, 8) published-path key (kept at KEY_INIT
+// between calls), [8, 12) its block counter (kept at 0), [16, 24) copy-path
+// key, [256, ...) copy-path net values.
 static distill_status ensure_scratch(distill_model* m, size_t bytes) {
     if (m->scratch_bytes >= bytes) return DISTILL_OK;
     if (m->d_scratch) cudaFree(m->d_scratch);
     m->d_scratch = nullptr;
     m->scratch_bytes = 0;
     CUDA_TRY(cudaMalloc(&m->d_scratch, bytes));
+    CUDA_TRY(cudaMemset(m->d_scratch, 0xFF, 8));
+    CUDA_TRY(cudaMemset((char*)m->d_scratch + 8, 0, 8));
+    CUDA_TRY(cudaDeviceSynchronize());
     m->scratch_bytes = bytes;
     return DISTILL_OK;
 }
@@ -164,7 +170,8 @@ distill_status distill_grid_size(const distill_model* m, uint64_t* n_alloc) {
     return DISTILL_OK;
 }
 
-static distill_status launch_pp(const distill_model* m, const distill_eval_args* a, cudaStream_t st) {
+static distill_status launch_pp(const distill_model* m, const distill_eval_args* a, cudaStream_t st,
+                                key64_t* publish = nullptr, unsigned int* done = nullptr) {
     if (!a->inputs || a->n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): needs 6 host inputs");
     if (a->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): n_samples must be >= 1");
     if ((a->trial_begin | a->trial_end) != 0)
@@ -183,11 +190,19 @@ static distill_status launch_pp(const distill_model* m, const distill_eval_args*
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
     p.levels = m->d_levels; p.net = a->d_net; p.best = a->d_best;
     p.pos_dev = nullptr; p.status_dev = nullptr;
+    p.publish = publish; p.done = done;
     const unsigned grid = (unsigned)((count + PP_BLOCK - 1) / PP_BLOCK);
-    if ((a->n_samples & 1u) == 0)
+    const bool even = (a->n_samples & 1u) == 0;
+    if (publish) {
+        if (even)
+            pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+        else
+            pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, false, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+    } else if (even) {
         pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
-    else
+    } else {
         pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
+    }
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;
@@ -366,7 +381,6 @@ distill_status distill_eval_grid_host(const distill_model* mc, const float* h_in
     distill_status s = ensure_scratch(m, net_off + count * sizeof(float));
     if (s != DISTILL_OK) return s;
     cudaStream_t st = (cudaStream_t)stream;
-    unsigned long long* d_best = (unsigned long long*)m->d_scratch;
     float* d_net = nullptr;
     bool direct = false;
     if (h_net) {
@@ -383,19 +397,39 @@ distill_status distill_eval_grid_host(const distill_model* mc, const float* h_in
             d_net = (float*)((char*)m->d_scratch + net_off);
         }
     }
+    // Pinned h_best: the kernel's last block publishes the key into it and re-arms
+    // the device key (one launch, no memset, no copy).  Pageable: memset + copy.
+    key64_t* publish = nullptr;
+    {
+        cudaPointerAttributes pb;
+        if (cudaPointerGetAttributes(&pb, h_best) == cudaSuccess && pb.type == cudaMemoryTypeHost &&
+            pb.devicePointer != nullptr && (reinterpret_cast<uintptr_t>(pb.devicePointer) & 7u) == 0)
+            publish = (key64_t*)pb.devicePointer;
+        else
+            (void)cudaGetLastError();
+    }
     // Host->device: this step's inputs (the 6 positions, 24 B) travel inside the
     // kernel's launch parameters; device->host: V (if h_net) and the best key.
     if (!h_inputs || n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "eval_grid_host: needs 6 inputs");
-    CUDA_TRY(cudaMemsetAsync(d_best, 0xFF, sizeof(unsigned long long), st));
     distill_eval_args a;
     memset(&a, 0, sizeof a);
     a.inputs = h_inputs; a.n_inputs = n_inputs; a.begin = begin; a.end = end;
     a.n_samples = n_samples; a.invocation = invocation; a.seed = seed;
-    a.d_net = d_net; a.d_best = d_best;
-    s = launch_pp(m, &a, st);
-    if (s != DISTILL_OK) return s;
-    if (h_net && !direct) CUDA_TRY(cudaMemcpyAsync(h_net, d_net, count * sizeof(float), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(h_best, d_best, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    a.d_net = d_net;
+    if (publish && count > 0) {
+        a.d_best = (unsigned long long*)m->d_scratch;
+        s = launch_pp(m, &a, st, publish, (unsigned int*)((char*)m->d_scratch + 8));
+        if (s != DISTILL_OK) return s;
+        if (h_net && !direct) CUDA_TRY(cudaMemcpyAsync(h_net, d_net, count * sizeof(float), cudaMemcpyDeviceToHost, st));
+    } else {
+        unsigned long long* d_best = (unsigned long long*)((char*)m->d_scratch + 16);
+        a.d_best = d_best;
+        CUDA_TRY(cudaMemsetAsync(d_best, 0xFF, sizeof(unsigned long long), st));
+        s = launch_pp(m, &a, st);
+        if (s != DISTILL_OK) return s;
+        if (h_net && !direct) CUDA_TRY(cudaMemcpyAsync(h_net, d_net, count * sizeof(float), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(h_best, d_best, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    }
     CUDA_TRY(cudaStreamSynchronize(st));
     return DISTILL_OK;
 }

@@ -37,6 +37,8 @@ struct PPArgs {
     const float* __restrict__ pos_dev;                 // episode / multi: positions in device memory (or nullptr)
     const int* __restrict__ status_dev;                // episode: skip the launch when status[0] != 0
     uint32_t n_sets = 1;                               // multi: position sets; invocation t uses set t mod n_sets
+    key64_t* publish = nullptr;                        // PUB: device alias of a mapped pinned host key
+    unsigned int* done = nullptr;                      // PUB: block-completion counter (0 between launches)
 };
 
 // Multi-invocation launches (distill_eval_grid_multi) put invocation t on
@@ -193,7 +195,7 @@ __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, floa
 
 // One thread per allocation; one atomicMin per block.
 template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false, bool EVEN = false,
-          bool MULTI = false>
+          bool MULTI = false, bool PUB = false>
 __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs a0) {
     if (a0.status_dev && *a0.status_dev != 0) return;   // episode already over (uniform branch)
     // Multi-invocation: only the invocation word and the position set feed the
@@ -218,6 +220,23 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs 
     if (a0.net && tid < a0.count) a0.net[row * a0.count + tid] = -C;
     // a9: (value, index) argmin -> one atomic per block
     if (a0.best) block_min_key_atomic<BLOCK>(key, a0.best + row);
+    if (PUB && threadIdx.x == 0) {
+        // End-to-end call (distill_eval_grid_host): the last block to finish
+        // publishes the combined key straight into pinned host memory and
+        // re-arms the device key and counter for the next call, so the call is
+        // one launch with no memset and no copy.  Thread 0 issued this block's
+        // atomicMin; the fence orders it before the counter increment
+        // (threadFenceReduction pattern).
+        __threadfence();
+        if (atomicAdd(a0.done, 1u) == gridDim.x * gridDim.y - 1) {
+            __threadfence();
+            const key64_t k = atomicOr(a0.best, 0ull);      // coherent read of the final key
+            *reinterpret_cast<volatile key64_t*>(a0.publish) = k;
+            __threadfence_system();
+            *a0.best = KEY_INIT;
+            *a0.done = 0u;
+        }
+    }
 }
 
 // Persistent variant: a fixed grid of resident blocks pulls BLOCK-allocation

@@ -630,3 +630,31 @@ def test_seed_sweep_1_to_100(D, orc):
                                      0, n, 90, seed)
             assert np.array_equal(counts.cpu().numpy().astype(np.uint64).reshape(n, 3), wc), seed
             assert np.array_equal(_bits(net.cpu().numpy()), _bits(wn)), seed
+
+
+def test_eval_grid_host_published_key_rearms_between_calls(D, orc):
+    """Pinned h_best: the last block publishes the key and re-arms the device key
+    and counter, so consecutive calls (other seeds, ranges, sample parities,
+    interleaved with the pageable-key copy path and an empty range) each return
+    their own key, never a min with a previous call's."""
+    import ctypes as C
+    from paper_2110_15425_b200 import _abi
+    cfg = W.PPConfig("h2", (9, 8, 7), 6)
+    m = _model(D, cfg)
+    calls = [(11, 0, cfg.n_alloc, 6), (3, 100, 300, 7), (11, 0, cfg.n_alloc, 6), (99, 7, 8, 2), (5, 0, 0, 6),
+             (42, 200, cfg.n_alloc, 5)]
+    for rep in range(2):
+        for seed, b, e, S in calls:
+            want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, b, e, S, seed)
+            k_or = orc.argmax_net(-want, b)[0] if e > b else D.KEY_INIT
+            if rep == 0:
+                got = D.eval_grid_host(m, cfg.inputs, S, seed, b, e)              # pinned key (binding)
+            else:
+                k = C.c_uint64()                                                   # pageable key: copy path
+                inp = np.ascontiguousarray(cfg.inputs, np.float32)
+                _abi.check(_abi.lib().distill_eval_grid_host(m.handle, _abi._fptr(inp), 6, b, e, S, 0, seed,
+                                                             None, C.byref(k), None))
+                got = int(k.value)
+                got2 = D.eval_grid_host(m, cfg.inputs, S, seed, b, e)             # and pinned right after
+                assert got2 == got
+            assert got == k_or, (rep, seed, b, e, S)
