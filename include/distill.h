@@ -79,7 +79,7 @@ typedef struct {
     const float* inputs;         /* host; PP: prey, predator, player (x, y) = 6 floats; Stroop: unused */
     uint32_t n_inputs;
     uint64_t begin, end;         /* global allocation indices, begin <= end <= grid size */
-    uint32_t n_samples;          /* PP: samples per allocation (>= 1); Stroop: trials T per allocation */
+    uint32_t n_samples;          /* PP: samples per allocation; Stroop: trials T per allocation; 1..2^31 */
     uint32_t invocation;         /* PP: controller invocation t (RNG counter word, spec/RNG.md §1); Stroop: 0 */
     uint64_t seed;               /* Philox key */
     float* d_net;                /* device [end-begin] or NULL: net value V = -C per allocation       */
@@ -115,7 +115,7 @@ typedef struct {
  * h_init is given (then it is copied in, stream-ordered). */
 typedef struct {
     uint32_t n_steps;            /* T >= 1                                                  */
-    uint32_t n_samples;          /* samples per allocation in every grid search, >= 1      */
+    uint32_t n_samples;          /* samples per allocation in every grid search, 1..2^31   */
     uint64_t seed;
     float v_player, v_prey, v_predator;   /* step lengths per time step                   */
     float capture_radius;        /* capture when |prey - player| or |predator - player| <= r */
@@ -174,7 +174,7 @@ typedef struct {
     uint32_t n_sets;             /* >= 1                                                           */
     uint32_t n_invocations;      /* T, 0 = no-op                                                   */
     uint32_t invocation0;        /* RNG invocation word of t = 0                                   */
-    uint32_t n_samples;          /* samples per allocation, >= 1                                   */
+    uint32_t n_samples;          /* samples per allocation, 1..2^31                                */
     uint64_t begin, end;         /* global allocation range (a shard)                              */
     uint64_t seed;               /* Philox key                                                     */
     float* d_net;                /* device [T][end-begin] or NULL                                  */

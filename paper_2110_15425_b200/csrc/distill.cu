@@ -47,6 +47,9 @@ distill_status fail(distill_status s, const char* fmt, ...) {
 
 constexpr int PP_BLOCK = 128;
 constexpr int ARGMAX_BLOCK = 256;
+// sample / trial loops step a 32-bit counter by up to 2 (PP pairs) or a grid
+// stride (Stroop): bounding the count at 2^31 keeps them from wrapping
+constexpr uint32_t MAX_SAMPLES = 1u << 31;
 constexpr int DDM_BLOCK = 128;
 constexpr int DDM_MINB = 6;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt, v5)
 constexpr int STROOP_BLOCK = 128;
@@ -173,7 +176,8 @@ distill_status distill_grid_size(const distill_model* m, uint64_t* n_alloc) {
 static distill_status launch_pp(const distill_model* m, const distill_eval_args* a, cudaStream_t st,
                                 key64_t* publish = nullptr, unsigned int* done = nullptr) {
     if (!a->inputs || a->n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): needs 6 host inputs");
-    if (a->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): n_samples must be >= 1");
+    if (a->n_samples == 0 || a->n_samples > MAX_SAMPLES)
+        return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): n_samples must be in [1, 2^31]");
     if ((a->trial_begin | a->trial_end) != 0)
         return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): trial range is a Stroop-only field");
     const uint64_t count = a->end - a->begin;
@@ -213,7 +217,8 @@ distill_status distill_eval_grid_multi(const distill_model* m, const distill_mul
     if (m->kind != DISTILL_MODEL_PREDATOR_PREY) return fail(DISTILL_E_UNSUPPORTED, "eval_grid_multi: predator-prey only");
     if (!a->d_inputs || a->n_sets == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: needs n_sets >= 1 device position sets");
     if (reinterpret_cast<uintptr_t>(a->d_inputs) & 3u) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: d_inputs misaligned");
-    if (a->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: n_samples must be >= 1");
+    if (a->n_samples == 0 || a->n_samples > MAX_SAMPLES)
+        return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: n_samples must be in [1, 2^31]");
     if (a->n_invocations > 65535u) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: at most 65535 invocations per call");
     if (a->begin > a->end || a->end > m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "eval_grid_multi: bad allocation range");
     if ((uint64_t)a->invocation0 + a->n_invocations > 0xFFFFFFFFull)
@@ -243,7 +248,8 @@ distill_status distill_eval_grid_multi(const distill_model* m, const distill_mul
 }
 
 static distill_status launch_stroop(distill_model* m, const distill_eval_args* a, cudaStream_t st) {
-    if (a->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop): n_samples (trials) must be >= 1");
+    if (a->n_samples == 0 || a->n_samples > MAX_SAMPLES)
+        return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop): n_samples (trials) must be in [1, 2^31]");
     if (a->invocation != 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop): invocation must be 0");
     uint32_t tb = a->trial_begin, te = a->trial_end;
     if (tb == 0 && te == 0) te = a->n_samples;
@@ -314,7 +320,8 @@ void launch_ext_stroop_kernels(const ExtStroopArgs& p, uint32_t chunks, uint64_t
 }  // extern "C++"
 
 static distill_status launch_ext_stroop(distill_model* m, const distill_eval_args* a, cudaStream_t st) {
-    if (a->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Ext-Stroop): n_samples (trials) must be >= 1");
+    if (a->n_samples == 0 || a->n_samples > MAX_SAMPLES)
+        return fail(DISTILL_E_INVALID_ARG, "eval_grid(Ext-Stroop): n_samples (trials) must be in [1, 2^31]");
     if (a->invocation != 0) return fail(DISTILL_E_INVALID_ARG, "eval_grid(Ext-Stroop): invocation must be 0");
     uint32_t tb = a->trial_begin, te = a->trial_end;
     if (tb == 0 && te == 0) te = a->n_samples;
@@ -438,7 +445,8 @@ distill_status distill_pp_episode(const distill_model* mc, const distill_episode
     if (!mc || !e) return fail(DISTILL_E_INVALID_ARG, "pp_episode: NULL model/args");
     distill_model* m = const_cast<distill_model*>(mc);
     if (m->kind != DISTILL_MODEL_PREDATOR_PREY) return fail(DISTILL_E_UNSUPPORTED, "pp_episode: predator-prey only");
-    if (e->n_steps == 0 || e->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "pp_episode: n_steps, n_samples >= 1");
+    if (e->n_steps == 0 || e->n_samples == 0 || e->n_samples > MAX_SAMPLES)
+        return fail(DISTILL_E_INVALID_ARG, "pp_episode: n_steps >= 1, n_samples in [1, 2^31]");
     if (!e->d_traj || !e->d_keys || !e->d_status) return fail(DISTILL_E_INVALID_ARG, "pp_episode: NULL device buffer");
     if (!(e->capture_radius >= 0.0f)) return fail(DISTILL_E_INVALID_ARG, "pp_episode: capture_radius must be >= 0");
     CUDA_TRY(cudaSetDevice(m->device));
@@ -480,7 +488,8 @@ distill_status distill_pp_amr(const distill_model* mc, const distill_amr_args* g
     distill_model* m = const_cast<distill_model*>(mc);
     if (m->kind != DISTILL_MODEL_PREDATOR_PREY) return fail(DISTILL_E_UNSUPPORTED, "pp_amr: predator-prey only");
     if (!g->inputs || g->n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "pp_amr: needs 6 host inputs");
-    if (g->rounds == 0 || g->n_samples == 0) return fail(DISTILL_E_INVALID_ARG, "pp_amr: rounds, n_samples >= 1");
+    if (g->rounds == 0 || g->n_samples == 0 || g->n_samples > MAX_SAMPLES)
+        return fail(DISTILL_E_INVALID_ARG, "pp_amr: rounds >= 1, n_samples in [1, 2^31]");
     if (!g->d_keys || !g->d_boxes || !g->d_levels) return fail(DISTILL_E_INVALID_ARG, "pp_amr: NULL device buffer");
     for (int d = 0; d < 3; ++d)
         if (!(g->lo[d] <= g->hi[d])) return fail(DISTILL_E_INVALID_ARG, "pp_amr: lo > hi for signal %d", d);

@@ -191,6 +191,12 @@ def test_eval_grid_argument_errors(D):
         D.eval_grid(m, cfg.inputs, 0, 1, 0, 27, net=net)           # zero samples
     with pytest.raises(D.api.DistillError):
         D.eval_grid(m, cfg.inputs[:4], 10, 1, 0, 27, net=net)      # wrong input count
+    with pytest.raises(D.api.DistillError):
+        D.eval_grid(m, cfg.inputs, 2 ** 31 + 1, 1, 0, 27, net=net)  # sample counter could wrap
+    ms = D.load_model(W.KIND_STROOP_LCA, (2, 2), np.array([0, 1, 0, 1], np.float32), W.STROOP_W,
+                      W.STROOP_PARAMS, device=0)
+    with pytest.raises(D.api.DistillError):
+        D.eval_grid(ms, None, 2 ** 31 + 1, 1, 0, 4)                 # trial counter could wrap
     D.eval_grid(m, cfg.inputs, 10, 1, 5, 5, net=net)               # empty shard is a no-op
 
 
