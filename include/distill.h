@@ -34,7 +34,7 @@ extern "C" {
 typedef enum {
     DISTILL_OK = 0,
     DISTILL_E_INVALID_ARG = 1,  /* NULL/size/range error; nothing enqueued            */
-    DISTILL_E_OVERFLOW = 2,     /* grid > 2^32-1 allocations (key packs a 32-bit index) */
+    DISTILL_E_OVERFLOW = 2,     /* grid > 2^32-1 allocations (32-bit key index), or an RNG unit / invocation counter past its width */
     DISTILL_E_UNSUPPORTED = 3,  /* model kind / shape not implemented                  */
     DISTILL_E_CUDA = 4,         /* CUDA runtime error (see distill_last_error)         */
     DISTILL_E_NO_VALID = 5      /* key decode: no finite candidate (all NaN / empty)   */
