@@ -15,7 +15,8 @@
  *   od_philox4x32_10     pinned: Random123 known-answer vectors
  *   od_ln / od_rsqrt / od_sincos2pi   pinned: exhaustive / dense accuracy vs binary64 libm
  *   od_normal_*          pinned: moments, KS vs Phi, closed-form endpoints
- *   od_pp_eval           pinned: zero-noise closed forms, monotonicity, planted optimum,
+ *   od_pp_eval           pinned: zero-noise closed forms, monotonicity, planted optimum, offset-Gaussian
+ *                        angle law (noisy objective in closed form),
  *                        small-noise delta-method expectation, fp64 re-evaluation
  *   od_argmax_keys       pinned: brute-force min over (C, i), NaN/-0 rules
  *   od_normal_acc        pinned: raw-word Box-Muller definition, moments/kurtosis/KS; cuRAND Philox

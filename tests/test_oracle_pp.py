@@ -225,3 +225,36 @@ def test_multi_invocation_is_the_listing1_loop(orc):
     assert not np.array_equal(C[0], orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, sets[0], 0,
                                                  cfg.n_alloc, 6, 9, invocation=5))
     assert np.all(np.abs(sets) <= 10) and sets.dtype == np.float32
+
+
+def test_noisy_prey_objective_matches_offset_gaussian_angle_law(orc):
+    """Closed-form pin of the noisy PP path (Obs -> Action -> Objective):
+    with kappa = 0 the action is the direction to the observed prey; with the
+    player and predator noise-free (level 1, sigma_min = 0) and the prey at
+    (r, 0) observed with std sigma (level 0), u* = (1, 0) and the objective
+    |u - u*|^2 = 2 - 2 cos(Theta), Theta the angle of an offset 2-D Gaussian.
+    E[cos Theta] = sqrt(pi/8) nu e^{-nu^2/4} [I0(nu^2/4) + I1(nu^2/4)], nu = r/sigma
+    (cross-checked here by quadrature of the exact angle density).  64 allocations
+    x 5000 samples; a variance-for-std mistake (nu halved) is rejected."""
+    from scipy import integrate, special
+    r, sig = 4.0, 2.0
+
+    def ecos(nu):
+        return math.sqrt(math.pi / 8) * nu * math.exp(-nu * nu / 4) * (special.i0(nu * nu / 4) + special.i1(nu * nu / 4))
+
+    nu = r / sig
+
+    def dens(t):
+        c = math.cos(t)
+        return (math.exp(-nu * nu / 2) / (2 * math.pi)
+                * (1 + math.sqrt(2 * math.pi) * nu * c * math.exp(nu * nu * c * c / 2) * special.ndtr(nu * c)))
+
+    assert abs(integrate.quad(lambda t: math.cos(t) * dens(t), -math.pi, math.pi, epsabs=1e-13)[0] - ecos(nu)) < 1e-10
+    L = 64
+    levels = np.array([0.0] * L + [1.0, 1.0], np.float32)
+    C = orc.pp_eval((L, 1, 1), levels, np.zeros(3, np.float32), np.array([sig, 0.0, 0.0], np.float32),
+                    np.array([r, 0, -3, 2, 0, 0], np.float32), 0, L, 5000, 7).astype(np.float64)
+    se = C.std() / math.sqrt(L)
+    want = 2 - 2 * ecos(nu)
+    assert abs(C.mean() - want) <= 4 * se, (C.mean(), want, se)
+    assert abs(C.mean() - (2 - 2 * ecos(r / sig ** 2))) > 20 * se
