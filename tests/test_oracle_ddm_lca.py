@@ -175,3 +175,29 @@ def test_stroop_lca_unit_is_reflected_brownian_motion(orc):
     assert abs(T.mean() - ET(th_eff)) <= 4 * se + 0.01 * ET(th_eff), (T.mean(), ET(th_eff), se)
     assert abs(T.mean() - th_eff / mu) > 50 * se          # power: rectification matters
     assert abs(T.mean() - ET(th)) > 8 * se                # power: the discretisation shift matters
+
+
+def _golden(name):
+    import os
+    return open(os.path.join(os.path.dirname(__file__), "golden", name)).read().splitlines()
+
+
+def test_golden_ddm_and_stroop(orc):
+    """Regression fixtures written by tests/golden/make_golden.py (oracle only)."""
+    d = W.DDMConfig(n_steps=250, n_trials=2000)
+    p = orc.ddm_params(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
+                       d.x_lo, d.x_hi)
+    got = orc.ddm_batch(p, d.seed, 0, d.n_trials)
+    rows = {ln.split()[0]: [int(v) for v in ln.split()[1:]] for ln in _golden("ddm_small_hist.txt")
+            if not ln.startswith("#")}
+    for name, arr in zip(("rt_hist", "rt_sum", "x_hist"), got):
+        assert [int(v) for v in arr] == rows[name], name
+    lev = np.linspace(0, 1, 4).astype(np.float32)
+    counts, net = orc.stroop_eval((4, 4), np.concatenate([lev, lev]), W.STROOP_W, W.STROOP_PARAMS, 0, 16, 60, W.SEED)
+    for ln in _golden("stroop_small_counts.txt"):
+        if ln.startswith("#"):
+            continue
+        i, nc, nu, rs, v = ln.split()
+        i = int(i)
+        assert [int(counts[i, 0]), int(counts[i, 1]), int(counts[i, 2])] == [int(nc), int(nu), int(rs)]
+        assert float(net[i]) == float.fromhex(v)
