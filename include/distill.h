@@ -127,6 +127,22 @@ typedef struct {
 
 distill_status distill_pp_episode(const distill_model* model, const distill_episode_args* args, void* stream);
 
+/* The same episode in pieces, for a grid sharded across GPUs ("one grid search +
+ * all-reduce per time step"): begin() copies h_init (if
+ * given) and resets d_keys / d_status; for each step t every rank runs
+ * search(t, [begin, end)) on its shard — atomicMin into d_keys[t] — the caller
+ * MIN-all-reduces d_keys[t] across ranks (key order = unsigned order; flip bit
+ * 63 for a signed int64 MIN), then every rank runs advance(t), which moves all
+ * entities from the global key exactly as distill_pp_episode does, so every
+ * rank holds the identical trajectory.  distill_pp_episode = begin + T x
+ * (search over the whole grid + advance).  All calls are stream-ordered;
+ * t < n_steps; begin <= end <= grid size (E_INVALID_ARG otherwise). */
+distill_status distill_pp_episode_begin(const distill_model* model, const distill_episode_args* args, void* stream);
+distill_status distill_pp_episode_search(const distill_model* model, const distill_episode_args* args, uint32_t t,
+                                         uint64_t begin, uint64_t end, void* stream);
+distill_status distill_pp_episode_advance(const distill_model* model, const distill_episode_args* args, uint32_t t,
+                                          void* stream);
+
 /* Coarse-to-fine (AMR-style) refinement of the predator-prey grid search
  * (NEXT-4; §4.3, Fig. 4; spec/MODELS.md §9).  The model's
  * n_levels give L_d per signal (its level table is not used); each round r runs

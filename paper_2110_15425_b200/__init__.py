@@ -12,14 +12,15 @@ Public Python API (thin wrappers over the C ABI in include/distill.h):
     pp_episode(model, init, n_steps, n_samples, seed, ...)   # closed loop, on the device
     pp_amr(model, inputs, lo, hi, rounds, n_samples, seed)   # coarse-to-fine refinement
     shard_range(n, rank, world) / best_allreduce(key, group)   # multi-GPU plumbing
+    pp_episode_sharded(model, init, T, S, seed, rank, world)  # closed loop over a sharded grid
 
 Importing this package does not touch the GPU; the shared library is loaded
 on first use and there is no CPU fallback.
 """
-from .api import (KEY_INIT, Model, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_multi, key_decode,
+from .api import (KEY_INIT, EpisodeRun, Model, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_multi, key_decode,
                   key_reset, launch_count, load_model, pp_amr, pp_episode)
-from .dist import best_allreduce, hist_allreduce, key_to_i64, i64_to_key, shard_range
+from .dist import best_allreduce, hist_allreduce, key_to_i64, i64_to_key, pp_episode_sharded, shard_range
 
 __all__ = ["KEY_INIT", "Model", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "eval_grid_multi", "key_decode", "pp_episode", "pp_amr",
            "key_reset", "launch_count", "load_model", "best_allreduce", "hist_allreduce", "key_to_i64",
-           "i64_to_key", "shard_range"]
+           "i64_to_key", "shard_range", "pp_episode_sharded", "EpisodeRun"]

@@ -91,6 +91,10 @@ EXPORTS = {
     "distill_pp_amr": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_void_p]),
     "distill_eval_grid_multi": (C.c_int, [C.c_void_p, C.POINTER(MultiArgs), C.c_void_p]),
     "distill_pp_episode": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_void_p]),
+    "distill_pp_episode_begin": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_void_p]),
+    "distill_pp_episode_search": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_uint32, C.c_uint64, C.c_uint64,
+                                            C.c_void_p]),
+    "distill_pp_episode_advance": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_uint32, C.c_void_p]),
 }
 
 _lib = None

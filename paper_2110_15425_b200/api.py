@@ -178,12 +178,8 @@ def ddm_batch(drift, noise, threshold, x0, dt, n_steps, rt_bin_steps, n_x_bins, 
     check(lib().distill_ddm_batch(C.byref(a), _stream_handle(stream)))
 
 
-def pp_episode(model: Model, init, n_steps: int, n_samples: int, seed: int, speeds=(1.0, 0.8, 0.6),
-               capture_radius: float = 0.5, traj=None, keys=None, status=None, stream=None):
-    """distill_pp_episode: closed-loop episode on the device (spec/MODELS.md §7).
-
-    Returns (traj[(T+1),6] float32, keys[T] int64 raw key bits, status[2] int32) CUDA tensors.
-    If `init` is None, traj[0] must already hold the initial positions."""
+def _episode_args(model: Model, init, n_steps: int, n_samples: int, seed: int, speeds, capture_radius,
+                  traj, keys, status):
     import torch
     dev = torch.device("cuda", model.device)
     T = int(n_steps)
@@ -196,6 +192,39 @@ def pp_episode(model: Model, init, n_steps: int, n_samples: int, seed: int, spee
                          _abi._fptr(init_arr) if init_arr is not None else None,
                          _dev_ptr(traj, "traj", 6 * (T + 1)), _dev_ptr(keys, "keys", T),
                          _dev_ptr(status, "status", 2))
+    return a, init_arr, traj, keys, status
+
+
+class EpisodeRun:
+    """A closed-loop episode driven step by step (distill_pp_episode_begin /
+    _search / _advance), for grids sharded across ranks: between search(t) and
+    advance(t) the caller all-reduces keys[t:t+1] (dist.best_allreduce)."""
+
+    def __init__(self, model: Model, init, n_steps: int, n_samples: int, seed: int, speeds=(1.0, 0.8, 0.6),
+                 capture_radius: float = 0.5, traj=None, keys=None, status=None, stream=None):
+        self.model, self.stream = model, stream
+        self._a, self._init, self.traj, self.keys, self.status = _episode_args(
+            model, init, n_steps, n_samples, seed, speeds, capture_radius, traj, keys, status)
+        check(lib().distill_pp_episode_begin(model.handle, C.byref(self._a), _stream_handle(stream)))
+
+    def search(self, t: int, begin: int = 0, end: Optional[int] = None) -> None:
+        end = self.model.n_alloc if end is None else int(end)
+        check(lib().distill_pp_episode_search(self.model.handle, C.byref(self._a), int(t), int(begin), end,
+                                              _stream_handle(self.stream)))
+
+    def advance(self, t: int) -> None:
+        check(lib().distill_pp_episode_advance(self.model.handle, C.byref(self._a), int(t),
+                                               _stream_handle(self.stream)))
+
+
+def pp_episode(model: Model, init, n_steps: int, n_samples: int, seed: int, speeds=(1.0, 0.8, 0.6),
+               capture_radius: float = 0.5, traj=None, keys=None, status=None, stream=None):
+    """distill_pp_episode: closed-loop episode on the device (spec/MODELS.md §7).
+
+    Returns (traj[(T+1),6] float32, keys[T] int64 raw key bits, status[2] int32) CUDA tensors.
+    If `init` is None, traj[0] must already hold the initial positions."""
+    a, _keep, traj, keys, status = _episode_args(model, init, n_steps, n_samples, seed, speeds, capture_radius,
+                                                 traj, keys, status)
     check(lib().distill_pp_episode(model.handle, C.byref(a), _stream_handle(stream)))
     return traj, keys, status
 
@@ -236,5 +265,5 @@ def key_from_tensor(best) -> int:
     return int(best.reshape(-1)[0].item()) & (2 ** 64 - 1)
 
 
-__all__ = ["KEY_INIT", "DistillError", "Model", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",
+__all__ = ["KEY_INIT", "DistillError", "EpisodeRun", "Model", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",
            "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode", "argmax_ties", "pp_amr", "sm_clock_mhz"]

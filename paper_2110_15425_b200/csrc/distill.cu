@@ -441,19 +441,18 @@ distill_status distill_eval_grid_host(const distill_model* mc, const float* h_in
     return DISTILL_OK;
 }
 
-distill_status distill_pp_episode(const distill_model* mc, const distill_episode_args* e, void* stream) {
-    if (!mc || !e) return fail(DISTILL_E_INVALID_ARG, "pp_episode: NULL model/args");
-    distill_model* m = const_cast<distill_model*>(mc);
-    if (m->kind != DISTILL_MODEL_PREDATOR_PREY) return fail(DISTILL_E_UNSUPPORTED, "pp_episode: predator-prey only");
+static distill_status episode_check(const distill_model* m, const distill_episode_args* e, const char* who) {
+    if (!m || !e) return fail(DISTILL_E_INVALID_ARG, "%s: NULL model/args", who);
+    if (m->kind != DISTILL_MODEL_PREDATOR_PREY) return fail(DISTILL_E_UNSUPPORTED, "%s: predator-prey only", who);
     if (e->n_steps == 0 || e->n_samples == 0 || e->n_samples > MAX_SAMPLES)
-        return fail(DISTILL_E_INVALID_ARG, "pp_episode: n_steps >= 1, n_samples in [1, 2^31]");
-    if (!e->d_traj || !e->d_keys || !e->d_status) return fail(DISTILL_E_INVALID_ARG, "pp_episode: NULL device buffer");
-    if (!(e->capture_radius >= 0.0f)) return fail(DISTILL_E_INVALID_ARG, "pp_episode: capture_radius must be >= 0");
-    CUDA_TRY(cudaSetDevice(m->device));
-    cudaStream_t st = (cudaStream_t)stream;
-    if (e->h_init) CUDA_TRY(cudaMemcpyAsync(e->d_traj, e->h_init, 6 * sizeof(float), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemsetAsync(e->d_keys, 0xFF, e->n_steps * sizeof(unsigned long long), st));
-    CUDA_TRY(cudaMemsetAsync(e->d_status, 0, 2 * sizeof(int), st));
+        return fail(DISTILL_E_INVALID_ARG, "%s: n_steps >= 1, n_samples in [1, 2^31]", who);
+    if (!e->d_traj || !e->d_keys || !e->d_status)
+        return fail(DISTILL_E_INVALID_ARG, "%s: NULL device buffer", who);
+    if (!(e->capture_radius >= 0.0f)) return fail(DISTILL_E_INVALID_ARG, "%s: capture_radius must be >= 0", who);
+    return DISTILL_OK;
+}
+
+static PPArgs episode_pp_args(const distill_model* m, const distill_episode_args* e) {
     PPArgs p;
     memset(&p, 0, sizeof p);
     p.sigma_max = m->params[0]; p.sigma_min = m->params[1]; p.kappa = m->params[2];
@@ -464,20 +463,75 @@ distill_status distill_pp_episode(const distill_model* mc, const distill_episode
     p.begin = 0; p.count = (uint32_t)m->n_alloc;
     p.levels = m->d_levels; p.net = nullptr;
     p.status_dev = e->d_status;
+    p.n_sets = 1;
+    return p;
+}
+
+static void episode_search(const distill_model* m, const distill_episode_args* e, PPArgs p, uint32_t t,
+                           uint64_t begin, uint64_t end, cudaStream_t st) {
+    p.invocation = t;
+    p.pos_dev = e->d_traj + 6ull * t;
+    p.best = e->d_keys + t;
+    p.begin = (uint32_t)begin; p.count = (uint32_t)(end - begin);
+    const unsigned grid = (unsigned)((end - begin + PP_BLOCK - 1) / PP_BLOCK);
+    if ((e->n_samples & 1u) == 0) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+    else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
+    g_launches++;
+}
+
+static void episode_advance(const distill_model* m, const distill_episode_args* e, const PPArgs& p, uint32_t t,
+                            cudaStream_t st) {
     EpisodeArgs ea;
     ea.v_pl = e->v_player; ea.v_py = e->v_prey; ea.v_pd = e->v_predator;
     ea.rc = e->capture_radius;
     ea.traj = e->d_traj; ea.keys = e->d_keys; ea.status = e->d_status;
-    const unsigned grid = (unsigned)((m->n_alloc + PP_BLOCK - 1) / PP_BLOCK);
-    const bool even = (e->n_samples & 1u) == 0;
+    pp_episode_step_kernel<<<1, 32, 0, st>>>(p, ea, t);
+    g_launches++;
+}
+
+distill_status distill_pp_episode_begin(const distill_model* m, const distill_episode_args* e, void* stream) {
+    distill_status s = episode_check(m, e, "pp_episode_begin");
+    if (s != DISTILL_OK) return s;
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (e->h_init) CUDA_TRY(cudaMemcpyAsync(e->d_traj, e->h_init, 6 * sizeof(float), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(e->d_keys, 0xFF, e->n_steps * sizeof(unsigned long long), st));
+    CUDA_TRY(cudaMemsetAsync(e->d_status, 0, 2 * sizeof(int), st));
+    return DISTILL_OK;
+}
+
+distill_status distill_pp_episode_search(const distill_model* m, const distill_episode_args* e, uint32_t t,
+                                         uint64_t begin, uint64_t end, void* stream) {
+    distill_status s = episode_check(m, e, "pp_episode_search");
+    if (s != DISTILL_OK) return s;
+    if (t >= e->n_steps) return fail(DISTILL_E_INVALID_ARG, "pp_episode_search: step t >= n_steps");
+    if (begin > end || end > m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "pp_episode_search: bad shard");
+    if (begin == end) return DISTILL_OK;
+    CUDA_TRY(cudaSetDevice(m->device));
+    episode_search(m, e, episode_pp_args(m, e), t, begin, end, (cudaStream_t)stream);
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+distill_status distill_pp_episode_advance(const distill_model* m, const distill_episode_args* e, uint32_t t,
+                                          void* stream) {
+    distill_status s = episode_check(m, e, "pp_episode_advance");
+    if (s != DISTILL_OK) return s;
+    if (t >= e->n_steps) return fail(DISTILL_E_INVALID_ARG, "pp_episode_advance: step t >= n_steps");
+    CUDA_TRY(cudaSetDevice(m->device));
+    episode_advance(m, e, episode_pp_args(m, e), t, (cudaStream_t)stream);
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+distill_status distill_pp_episode(const distill_model* m, const distill_episode_args* e, void* stream) {
+    distill_status s = distill_pp_episode_begin(m, e, stream);
+    if (s != DISTILL_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const PPArgs p = episode_pp_args(m, e);
     for (uint32_t t = 0; t < e->n_steps; ++t) {
-        p.invocation = t;
-        p.pos_dev = e->d_traj + 6ull * t;
-        p.best = e->d_keys + t;
-        if (even) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
-        else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
-        pp_episode_step_kernel<<<1, 32, 0, st>>>(p, ea, t);
-        g_launches += 2;
+        episode_search(m, e, p, t, 0, m->n_alloc, st);
+        episode_advance(m, e, p, t, st);
     }
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;

@@ -63,3 +63,20 @@ def hist_allreduce(tensors, group=None):
         t.copy_(flat[off:off + n].view_as(t))
         off += n
     return tensors
+
+
+def pp_episode_sharded(model, init, n_steps: int, n_samples: int, seed: int, rank: int, world: int, group=None,
+                       speeds=(1.0, 0.8, 0.6), capture_radius: float = 0.5, stream=None):
+    """Closed-loop episode over a grid sharded across ranks (SURVEY §8(f) NEXT-1:
+    one grid search + all-reduce per time step).  Each rank searches its
+    contiguous shard for step t, the keys are MIN-all-reduced, and every rank
+    advances the identical trajectory.  Returns (traj, keys, status) tensors."""
+    from .api import EpisodeRun
+    b, e = shard_range(model.n_alloc, rank, world)
+    run = EpisodeRun(model, init, n_steps, n_samples, seed, speeds, capture_radius, stream=stream)
+    for t in range(int(n_steps)):
+        run.search(t, b, e)
+        if world > 1:
+            best_allreduce(run.keys[t:t + 1], group)
+        run.advance(t)
+    return run.traj, run.keys, run.status

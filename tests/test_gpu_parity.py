@@ -664,3 +664,70 @@ def test_eval_grid_host_published_key_rearms_between_calls(D, orc):
                 got2 = D.eval_grid_host(m, cfg.inputs, S, seed, b, e)             # and pinned right after
                 assert got2 == got
             assert got == k_or, (rep, seed, b, e, S)
+
+
+def test_pp_episode_in_pieces_over_shards(D, orc):
+    """NEXT-1 over a sharded grid, emulated in one process: per step, three shard
+    searches atomicMin into keys[t] (the MIN all-reduce), then advance — every
+    key, the trajectory and the outcome bit-exact against the oracle episode."""
+    import torch
+    cfg = W.PPConfig("eps", (9, 8, 7), 10)
+    m = _model(D, cfg)
+    init = np.array([4.0, 1.0, -3.0, 2.0, 0.0, 0.0], np.float32)
+    T, seed = 15, 8
+    run = D.EpisodeRun(m, init, T, cfg.n_samples, seed, speeds=(1.0, 0.7, 0.5), capture_radius=0.6)
+    shards = [D.shard_range(cfg.n_alloc, r, 3) for r in range(3)]
+    for t in range(T):
+        for b, e in reversed(shards):
+            run.search(t, b, e)
+        run.advance(t)
+    torch.cuda.synchronize()
+    w_traj, w_keys, w_status = orc.pp_episode(cfg.n_levels, cfg.levels, cfg.w, cfg.params, init, T,
+                                              cfg.n_samples, seed, speeds=(1.0, 0.7, 0.5), capture_radius=0.6)
+    assert np.array_equal(_bits(run.traj.cpu().numpy()), _bits(w_traj))
+    assert [int(k) & (2 ** 64 - 1) for k in run.keys.cpu().numpy()] == [int(k) for k in w_keys]
+    assert tuple(int(v) for v in run.status.cpu().numpy()) == w_status
+    with pytest.raises(D.api.DistillError):
+        run.search(T, 0, 1)                      # t past the episode
+    with pytest.raises(D.api.DistillError):
+        run.search(0, 5, cfg.n_alloc + 1)        # shard past the grid
+
+
+def _episode_rank(rank, world, port, out_path):
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_2110_15425_b200 as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)                     # both ranks share the one GPU; gloo reduces on the host
+    cfg = W.PPConfig("epd", (9, 8, 7), 10)
+    m = D.load_model(W.KIND_PREDATOR_PREY, cfg.n_levels, cfg.levels, cfg.w, cfg.params, device=0)
+    traj, keys, status = D.pp_episode_sharded(m, np.array([4.0, 1.0, -3.0, 2.0, 0.0, 0.0], np.float32), 12,
+                                              cfg.n_samples, 8, rank, world, speeds=(1.0, 0.7, 0.5),
+                                              capture_radius=0.6)
+    torch.cuda.synchronize()
+    np.savez(f"{out_path}.{rank}.npz", traj=traj.cpu().numpy(), keys=keys.cpu().numpy(), status=status.cpu().numpy())
+    dist.destroy_process_group()
+
+
+def test_pp_episode_sharded_two_ranks_gloo(D, orc, tmp_path):
+    """pp_episode_sharded with two processes (gloo all-reduce on the host, both
+    ranks on the single GPU — their kernels never wait on each other): both
+    ranks hold the oracle's trajectory, keys and outcome bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    out = str(tmp_path / "ep")
+    mp.start_processes(_episode_rank, args=(2, port, out), nprocs=2, join=True, start_method="spawn")
+    cfg = W.PPConfig("epd", (9, 8, 7), 10)
+    w_traj, w_keys, w_status = orc.pp_episode(cfg.n_levels, cfg.levels, cfg.w, cfg.params,
+                                              np.array([4.0, 1.0, -3.0, 2.0, 0.0, 0.0], np.float32), 12,
+                                              cfg.n_samples, 8, speeds=(1.0, 0.7, 0.5), capture_radius=0.6)
+    for r in range(2):
+        z = np.load(f"{out}.{r}.npz")
+        assert np.array_equal(_bits(z["traj"]), _bits(w_traj))
+        assert [int(k) & (2 ** 64 - 1) for k in z["keys"]] == [int(k) for k in w_keys]
+        assert tuple(int(v) for v in z["status"]) == w_status
