@@ -404,6 +404,32 @@ def run_extras(D, torch, dev, rank, world, args):
                        "mean_rt_s": (int(rs[0]) + int(rs[1])) / max(1, up + lo) * d.dt,
                        "algorithmic_tflops": tf, "frac_fp32_peak": tf / FP32_PEAK_NOMINAL,
                        "flops_per_step": DDM_FLOPS_PER_STEP}
+    # NEXT-1 over the sharded weak-scaling grid: per step a shard search, one key
+    # all-reduce and the (replicated) step kernel on every rank
+    if world > 1:
+        try:
+            cw = W.pp_weak(world)
+            mw = D.load_model(W.KIND_PREDATOR_PREY, cw.n_levels, cw.levels, cw.w, cw.params, device=dev.index)
+            T = 16
+            D.pp_episode_sharded(mw, cw.inputs, 2, cw.n_samples, cw.seed, rank, world)     # warm-up
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0.record()
+            _, _, stt = D.pp_episode_sharded(mw, cw.inputs, T, cw.n_samples, cw.seed, rank, world)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            st_h = stt.cpu().numpy()
+            steps_run = int(st_h[1]) if int(st_h[0]) != 0 else T
+            out["pp_episode_sharded"] = {"ms": ms, "steps": steps_run, "outcome": int(st_h[0]),
+                                         "evals_per_s": cw.evals * steps_run / (ms / 1e3),
+                                         "note": f"T={T} closed-loop steps over {cw.name} sharded on {world} "
+                                                 "ranks: shard search + key all-reduce + step kernel per step"}
+        except Exception as exc:   # an extra must never sink the headline line
+            out["pp_episode_sharded"] = {"error": repr(exc)[:200]}
     # NEXT-1: closed-loop episode on the cfg3 grid (T grid searches + T step kernels, on the device)
     if world == 1:
         c3 = W.pp_cfg3()
