@@ -663,6 +663,10 @@ int od_pp_amr(const uint32_t n_levels[3], const float w[3], const float params[3
         uint64_t best = 0xFFFFFFFFFFFFFFFFull;
         for (uint64_t i = 0; i < N; ++i) { uint64_t k = od_key(cost[i], (uint32_t)i); if (k < best) best = k; }
         keys[r] = best;
+        if ((best >> 32) == 0xFFFFFFFFull) {        /* no valid allocation (all NaN): box unchanged (MODELS.md §9) */
+            for (int d = 0; d < 3; ++d) { boxes[6 * (r + 1) + 2 * d] = lo[d]; boxes[6 * (r + 1) + 2 * d + 1] = hi[d]; }
+            continue;
+        }
         uint32_t ka[3];
         od_decode((uint32_t)best, 3, n_levels, ka);
         off = 0;

@@ -369,6 +369,10 @@ __global__ void amr_refine_kernel(const AmrArgs g, uint32_t r) {
     if (threadIdx.x != 0) return;
     const float* box = g.boxes + 6ull * r;
     float* nxt = g.boxes + 6ull * (r + 1);
+    if ((g.keys[r] >> 32) == 0xFFFFFFFFull) {     // no valid allocation (all NaN): box unchanged (MODELS.md §9)
+        for (int q = 0; q < 6; ++q) nxt[q] = box[q];
+        return;
+    }
     const uint32_t i = (uint32_t)g.keys[r];
     const uint32_t k2 = i % g.L[2], q = i / g.L[2];
     const uint32_t k[3] = {q / g.L[1], q % g.L[1], k2};

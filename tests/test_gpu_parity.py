@@ -731,3 +731,16 @@ def test_pp_episode_sharded_two_ranks_gloo(D, orc, tmp_path):
         assert np.array_equal(_bits(z["traj"]), _bits(w_traj))
         assert [int(k) & (2 ** 64 - 1) for k in z["keys"]] == [int(k) for k in w_keys]
         assert tuple(int(v) for v in z["status"]) == w_status
+
+
+def test_pp_amr_no_valid_allocation(D, orc):
+    import torch
+    cfg = W.PPConfig("amr_nan", (4, 3, 2), 4)
+    m = _model(D, cfg)
+    inputs = np.array([np.nan, 1.0, -3.0, 2.0, 0.0, 0.0], np.float32)
+    lo, hi = (0.0, 0.1, 0.2), (1.0, 0.9, 0.8)
+    keys, boxes = D.pp_amr(m, inputs, lo, hi, 3, 4, 5)
+    torch.cuda.synchronize()
+    w_keys, w_boxes = orc.pp_amr(cfg.n_levels, cfg.w, cfg.params, inputs, lo, hi, 3, 4, 5)
+    assert [int(k) & (2 ** 64 - 1) for k in keys.cpu().numpy()] == [int(k) for k in w_keys]
+    assert np.array_equal(_bits(boxes.cpu().numpy()), _bits(w_boxes))

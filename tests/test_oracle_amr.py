@@ -35,3 +35,15 @@ def test_amr_matches_fine_scan_of_prey_attention(orc):
     a_scan = fine.levels[int(np.argmin(C))]
     assert 0.3 < a_scan < 0.95            # interior optimum (reading R4)
     assert abs(a_amr - a_scan) < 0.1, (a_amr, a_scan)
+
+
+def test_amr_no_valid_allocation_keeps_the_box(orc):
+    """All costs NaN (NaN prey position): every round's key has the NaN high word
+    and the box is carried over unchanged (spec/MODELS.md §9)."""
+    cfg = W.PPConfig("amr_nan", (4, 3, 2), 4)
+    inputs = np.array([np.nan, 1.0, -3.0, 2.0, 0.0, 0.0], np.float32)
+    lo, hi = (0.0, 0.1, 0.2), (1.0, 0.9, 0.8)
+    keys, boxes = orc.pp_amr(cfg.n_levels, cfg.w, cfg.params, inputs, lo, hi, 3, 4, 5)
+    assert all(int(k) >> 32 == 0xFFFFFFFF for k in keys)
+    for r in range(4):
+        assert np.array_equal(boxes[r], np.array([lo, hi], np.float32).T)
