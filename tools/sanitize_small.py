@@ -34,6 +34,19 @@ def main():
     ms = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=0)
     sn = torch.empty(c.n_alloc, device="cuda")
     D.eval_grid(ms, None, c.n_trials, 1, net=sn, best=best)
+    for kind in (W.KIND_EXT_STROOP_A, W.KIND_EXT_STROOP_B):
+        mx = D.load_model(kind, c.n_levels, c.levels, c.w, W.EXT_STROOP_PARAMS, device=0)
+        D.eval_grid(mx, None, 30, 1, net=sn, best=best)
+    sets = torch.from_numpy(W.pp_positions(3)).cuda()
+    mnet = torch.empty((4, cfg.n_alloc), device="cuda")
+    mbest = torch.full((4,), -1, dtype=torch.int64, device="cuda")
+    D.eval_grid_multi(m, sets, 4, 5, 1, net=mnet, best=mbest)
+    run = D.EpisodeRun(m, cfg.inputs, 3, 4, 2)
+    for t in range(3):
+        run.search(t, 0, 50)
+        run.search(t, 50, cfg.n_alloc)
+        run.advance(t)
+    D.eval_grid_host(m, cfg.inputs, 6, 1, net_out=torch.empty(cfg.n_alloc, pin_memory=True).numpy())
     torch.cuda.synchronize()
     print("sanitize-small ok", int(best.item()), int(rh.sum()))
 
