@@ -161,6 +161,21 @@ typedef struct {
 
 distill_status distill_pp_amr(const distill_model* model, const distill_amr_args* args, void* stream);
 
+/* The same refinement in pieces, for a grid sharded across GPUs: begin() resets
+ * d_keys; per round r every rank runs levels(r) (the level table of box r into
+ * d_levels), search(r, [begin, end)) on its shard (atomicMin into d_keys[r]);
+ * the caller MIN-all-reduces d_keys[r] across ranks; every rank runs refine(r),
+ * which writes box r+1 from the global key — identical on every rank.
+ * distill_pp_amr = begin + R x (levels + search over the whole grid + refine).
+ * r < rounds; begin <= end <= grid size (E_INVALID_ARG otherwise). */
+distill_status distill_pp_amr_begin(const distill_model* model, const distill_amr_args* args, void* stream);
+distill_status distill_pp_amr_levels(const distill_model* model, const distill_amr_args* args, uint32_t r,
+                                     void* stream);
+distill_status distill_pp_amr_search(const distill_model* model, const distill_amr_args* args, uint32_t r,
+                                     uint64_t begin, uint64_t end, void* stream);
+distill_status distill_pp_amr_refine(const distill_model* model, const distill_amr_args* args, uint32_t r,
+                                     void* stream);
+
 int            distill_abi_version(void);
 const char*    distill_last_error(void);
 

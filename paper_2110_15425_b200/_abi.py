@@ -89,6 +89,11 @@ EXPORTS = {
     "distill_launch_count": (C.c_uint64, []),
     "distill_sm_clock_probe": (C.c_int, [C.c_uint32, C.POINTER(C.c_double), C.c_void_p]),
     "distill_pp_amr": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_void_p]),
+    "distill_pp_amr_begin": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_void_p]),
+    "distill_pp_amr_levels": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_uint32, C.c_void_p]),
+    "distill_pp_amr_search": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_uint32, C.c_uint64, C.c_uint64,
+                                        C.c_void_p]),
+    "distill_pp_amr_refine": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_uint32, C.c_void_p]),
     "distill_eval_grid_multi": (C.c_int, [C.c_void_p, C.POINTER(MultiArgs), C.c_void_p]),
     "distill_pp_episode": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_void_p]),
     "distill_pp_episode_begin": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_void_p]),

@@ -229,11 +229,8 @@ def pp_episode(model: Model, init, n_steps: int, n_samples: int, seed: int, spee
     return traj, keys, status
 
 
-def pp_amr(model: Model, inputs, lo, hi, rounds: int, n_samples: int, seed: int, invocation0: int = 0,
-           keys=None, boxes=None, levels=None, stream=None):
-    """distill_pp_amr: coarse-to-fine refinement on the device (spec/MODELS.md §9).
-
-    Returns (keys[R] int64 raw key bits, boxes[R+1, 3, 2] float32) CUDA tensors."""
+def _amr_args(model: Model, inputs, lo, hi, rounds: int, n_samples: int, seed: int, invocation0: int,
+              keys, boxes, levels):
     import torch
     dev = torch.device("cuda", model.device)
     R = int(rounds)
@@ -245,8 +242,42 @@ def pp_amr(model: Model, inputs, lo, hi, rounds: int, n_samples: int, seed: int,
                      (C.c_float * 3)(*[float(x) for x in hi]), R, int(n_samples), int(invocation0),
                      int(seed) & (2 ** 64 - 1), _dev_ptr(keys, "keys", R), _dev_ptr(boxes, "boxes", 6 * (R + 1)),
                      _dev_ptr(levels, "levels", int(model.n_levels.sum())))
+    return a, inp, keys, boxes, levels
+
+
+def pp_amr(model: Model, inputs, lo, hi, rounds: int, n_samples: int, seed: int, invocation0: int = 0,
+           keys=None, boxes=None, levels=None, stream=None):
+    """distill_pp_amr: coarse-to-fine refinement on the device (spec/MODELS.md §9).
+
+    Returns (keys[R] int64 raw key bits, boxes[R+1, 3, 2] float32) CUDA tensors."""
+    a, _keep, keys, boxes, levels = _amr_args(model, inputs, lo, hi, rounds, n_samples, seed, invocation0,
+                                              keys, boxes, levels)
     check(lib().distill_pp_amr(model.handle, C.byref(a), _stream_handle(stream)))
     return keys, boxes
+
+
+class AmrRun:
+    """Coarse-to-fine refinement driven round by round (distill_pp_amr_begin /
+    _levels / _search / _refine), for grids sharded across ranks: between
+    search(r) and refine(r) the caller all-reduces keys[r:r+1]."""
+
+    def __init__(self, model: Model, inputs, lo, hi, rounds: int, n_samples: int, seed: int,
+                 invocation0: int = 0, stream=None):
+        self.model, self.stream = model, stream
+        self._a, self._inp, self.keys, self.boxes, self.levels = _amr_args(
+            model, inputs, lo, hi, rounds, n_samples, seed, invocation0, None, None, None)
+        check(lib().distill_pp_amr_begin(model.handle, C.byref(self._a), _stream_handle(stream)))
+
+    def levels_for(self, r: int) -> None:
+        check(lib().distill_pp_amr_levels(self.model.handle, C.byref(self._a), int(r), _stream_handle(self.stream)))
+
+    def search(self, r: int, begin: int = 0, end: Optional[int] = None) -> None:
+        end = self.model.n_alloc if end is None else int(end)
+        check(lib().distill_pp_amr_search(self.model.handle, C.byref(self._a), int(r), int(begin), end,
+                                          _stream_handle(self.stream)))
+
+    def refine(self, r: int) -> None:
+        check(lib().distill_pp_amr_refine(self.model.handle, C.byref(self._a), int(r), _stream_handle(self.stream)))
 
 
 def sm_clock_mhz(micros: int = 200, stream=None) -> float:
@@ -265,5 +296,5 @@ def key_from_tensor(best) -> int:
     return int(best.reshape(-1)[0].item()) & (2 ** 64 - 1)
 
 
-__all__ = ["KEY_INIT", "DistillError", "EpisodeRun", "Model", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",
+__all__ = ["KEY_INIT", "AmrRun", "DistillError", "EpisodeRun", "Model", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",
            "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode", "argmax_ties", "pp_amr", "sm_clock_mhz"]

@@ -537,22 +537,28 @@ distill_status distill_pp_episode(const distill_model* m, const distill_episode_
     return DISTILL_OK;
 }
 
-distill_status distill_pp_amr(const distill_model* mc, const distill_amr_args* g, void* stream) {
-    if (!mc || !g) return fail(DISTILL_E_INVALID_ARG, "pp_amr: NULL model/args");
-    distill_model* m = const_cast<distill_model*>(mc);
-    if (m->kind != DISTILL_MODEL_PREDATOR_PREY) return fail(DISTILL_E_UNSUPPORTED, "pp_amr: predator-prey only");
-    if (!g->inputs || g->n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "pp_amr: needs 6 host inputs");
+static distill_status amr_check(const distill_model* m, const distill_amr_args* g, const char* who) {
+    if (!m || !g) return fail(DISTILL_E_INVALID_ARG, "%s: NULL model/args", who);
+    if (m->kind != DISTILL_MODEL_PREDATOR_PREY) return fail(DISTILL_E_UNSUPPORTED, "%s: predator-prey only", who);
+    if (!g->inputs || g->n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "%s: needs 6 host inputs", who);
     if (g->rounds == 0 || g->n_samples == 0 || g->n_samples > MAX_SAMPLES)
-        return fail(DISTILL_E_INVALID_ARG, "pp_amr: rounds >= 1, n_samples in [1, 2^31]");
-    if (!g->d_keys || !g->d_boxes || !g->d_levels) return fail(DISTILL_E_INVALID_ARG, "pp_amr: NULL device buffer");
+        return fail(DISTILL_E_INVALID_ARG, "%s: rounds >= 1, n_samples in [1, 2^31]", who);
+    if (!g->d_keys || !g->d_boxes || !g->d_levels) return fail(DISTILL_E_INVALID_ARG, "%s: NULL device buffer", who);
     for (int d = 0; d < 3; ++d)
-        if (!(g->lo[d] <= g->hi[d])) return fail(DISTILL_E_INVALID_ARG, "pp_amr: lo > hi for signal %d", d);
-    CUDA_TRY(cudaSetDevice(m->device));
-    cudaStream_t st = (cudaStream_t)stream;
-    CUDA_TRY(cudaMemsetAsync(g->d_keys, 0xFF, g->rounds * sizeof(unsigned long long), st));
+        if (!(g->lo[d] <= g->hi[d])) return fail(DISTILL_E_INVALID_ARG, "%s: lo > hi for signal %d", who, d);
+    if ((uint64_t)g->invocation0 + g->rounds > 0xFFFFFFFFull)
+        return fail(DISTILL_E_OVERFLOW, "%s: invocation counter overflow", who);
+    return DISTILL_OK;
+}
+
+static AmrArgs amr_args(const distill_model* m, const distill_amr_args* g) {
     AmrArgs a;
     for (int d = 0; d < 3; ++d) { a.lo0[d] = g->lo[d]; a.hi0[d] = g->hi[d]; a.L[d] = m->L[d]; }
     a.levels = g->d_levels; a.boxes = g->d_boxes; a.keys = g->d_keys;
+    return a;
+}
+
+static PPArgs amr_pp_args(const distill_model* m, const distill_amr_args* g) {
     PPArgs p;
     memset(&p, 0, sizeof p);
     p.prey_x = g->inputs[0]; p.prey_y = g->inputs[1]; p.pred_x = g->inputs[2]; p.pred_y = g->inputs[3];
@@ -564,16 +570,75 @@ distill_status distill_pp_amr(const distill_model* mc, const distill_amr_args* g
     p.key0 = (uint32_t)g->seed; p.key1 = (uint32_t)(g->seed >> 32);
     p.begin = 0; p.count = (uint32_t)m->n_alloc;
     p.levels = g->d_levels;
-    const unsigned grid = (unsigned)((m->n_alloc + PP_BLOCK - 1) / PP_BLOCK);
-    const bool even = (g->n_samples & 1u) == 0;
+    p.n_sets = 1;
+    return p;
+}
+
+static void amr_search(const distill_amr_args* g, PPArgs p, uint32_t r, uint64_t begin, uint64_t end,
+                       cudaStream_t st) {
+    p.invocation = g->invocation0 + r;
+    p.best = g->d_keys + r;
+    p.begin = (uint32_t)begin; p.count = (uint32_t)(end - begin);
+    const unsigned grid = (unsigned)((end - begin + PP_BLOCK - 1) / PP_BLOCK);
+    if ((g->n_samples & 1u) == 0) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+    else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
+    g_launches++;
+}
+
+distill_status distill_pp_amr_begin(const distill_model* m, const distill_amr_args* g, void* stream) {
+    distill_status s = amr_check(m, g, "pp_amr_begin");
+    if (s != DISTILL_OK) return s;
+    CUDA_TRY(cudaSetDevice(m->device));
+    CUDA_TRY(cudaMemsetAsync(g->d_keys, 0xFF, g->rounds * sizeof(unsigned long long), (cudaStream_t)stream));
+    return DISTILL_OK;
+}
+
+distill_status distill_pp_amr_levels(const distill_model* m, const distill_amr_args* g, uint32_t r, void* stream) {
+    distill_status s = amr_check(m, g, "pp_amr_levels");
+    if (s != DISTILL_OK) return s;
+    if (r >= g->rounds) return fail(DISTILL_E_INVALID_ARG, "pp_amr_levels: round r >= rounds");
+    CUDA_TRY(cudaSetDevice(m->device));
+    amr_levels_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(amr_args(m, g), r);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+distill_status distill_pp_amr_search(const distill_model* m, const distill_amr_args* g, uint32_t r,
+                                     uint64_t begin, uint64_t end, void* stream) {
+    distill_status s = amr_check(m, g, "pp_amr_search");
+    if (s != DISTILL_OK) return s;
+    if (r >= g->rounds) return fail(DISTILL_E_INVALID_ARG, "pp_amr_search: round r >= rounds");
+    if (begin > end || end > m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "pp_amr_search: bad shard");
+    if (begin == end) return DISTILL_OK;
+    CUDA_TRY(cudaSetDevice(m->device));
+    amr_search(g, amr_pp_args(m, g), r, begin, end, (cudaStream_t)stream);
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+distill_status distill_pp_amr_refine(const distill_model* m, const distill_amr_args* g, uint32_t r, void* stream) {
+    distill_status s = amr_check(m, g, "pp_amr_refine");
+    if (s != DISTILL_OK) return s;
+    if (r >= g->rounds) return fail(DISTILL_E_INVALID_ARG, "pp_amr_refine: round r >= rounds");
+    CUDA_TRY(cudaSetDevice(m->device));
+    amr_refine_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(amr_args(m, g), r);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+distill_status distill_pp_amr(const distill_model* m, const distill_amr_args* g, void* stream) {
+    distill_status s = distill_pp_amr_begin(m, g, stream);
+    if (s != DISTILL_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const AmrArgs a = amr_args(m, g);
+    const PPArgs p = amr_pp_args(m, g);
     for (uint32_t r = 0; r < g->rounds; ++r) {
         amr_levels_kernel<<<1, 256, 0, st>>>(a, r);
-        p.invocation = g->invocation0 + r;
-        p.best = g->d_keys + r;
-        if (even) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
-        else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
+        amr_search(g, p, r, 0, m->n_alloc, st);
         amr_refine_kernel<<<1, 32, 0, st>>>(a, r);
-        g_launches += 3;
+        g_launches += 2;
     }
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;

@@ -80,3 +80,21 @@ def pp_episode_sharded(model, init, n_steps: int, n_samples: int, seed: int, ran
             best_allreduce(run.keys[t:t + 1], group)
         run.advance(t)
     return run.traj, run.keys, run.status
+
+
+def pp_amr_sharded(model, inputs, lo, hi, rounds: int, n_samples: int, seed: int, rank: int, world: int,
+                   group=None, invocation0: int = 0, stream=None):
+    """Coarse-to-fine refinement over a grid sharded across ranks: per round the
+    level table (replicated), a shard search, one key all-reduce and the
+    (replicated) box refinement.  Returns (keys, boxes) tensors, identical on
+    every rank."""
+    from .api import AmrRun
+    b, e = shard_range(model.n_alloc, rank, world)
+    run = AmrRun(model, inputs, lo, hi, rounds, n_samples, seed, invocation0, stream=stream)
+    for r in range(int(rounds)):
+        run.levels_for(r)
+        run.search(r, b, e)
+        if world > 1:
+            best_allreduce(run.keys[r:r + 1], group)
+        run.refine(r)
+    return run.keys, run.boxes

@@ -744,3 +744,57 @@ def test_pp_amr_no_valid_allocation(D, orc):
     w_keys, w_boxes = orc.pp_amr(cfg.n_levels, cfg.w, cfg.params, inputs, lo, hi, 3, 4, 5)
     assert [int(k) & (2 ** 64 - 1) for k in keys.cpu().numpy()] == [int(k) for k in w_keys]
     assert np.array_equal(_bits(boxes.cpu().numpy()), _bits(w_boxes))
+
+
+def test_pp_amr_in_pieces_over_shards(D, orc):
+    """NEXT-4 over a sharded grid, emulated in one process: per round the level
+    table, three shard searches (atomicMin = the MIN all-reduce), the refine —
+    keys and boxes bit-exact against the oracle."""
+    import torch
+    cfg = W.PPConfig("amrs", (6, 5, 4), 8)
+    m = _model(D, cfg)
+    lo, hi, R = (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), 5
+    run = D.AmrRun(m, cfg.inputs, lo, hi, R, 8, 13, invocation0=2)
+    shards = [D.shard_range(cfg.n_alloc, r, 3) for r in range(3)]
+    for r in range(R):
+        run.levels_for(r)
+        for b, e in shards:
+            run.search(r, b, e)
+        run.refine(r)
+    torch.cuda.synchronize()
+    w_keys, w_boxes = orc.pp_amr(cfg.n_levels, cfg.w, cfg.params, cfg.inputs, lo, hi, R, 8, 13, invocation0=2)
+    assert [int(k) & (2 ** 64 - 1) for k in run.keys.cpu().numpy()] == [int(k) for k in w_keys]
+    assert np.array_equal(_bits(run.boxes.cpu().numpy()), _bits(w_boxes))
+
+
+def _amr_rank(rank, world, port, out_path):
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_2110_15425_b200 as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    cfg = W.PPConfig("amrd", (6, 5, 4), 8)
+    m = D.load_model(W.KIND_PREDATOR_PREY, cfg.n_levels, cfg.levels, cfg.w, cfg.params, device=0)
+    keys, boxes = D.pp_amr_sharded(m, cfg.inputs, (0, 0, 0), (1, 1, 1), 5, 8, 13, rank, world, invocation0=2)
+    torch.cuda.synchronize()
+    np.savez(f"{out_path}.{rank}.npz", keys=keys.cpu().numpy(), boxes=boxes.cpu().numpy())
+    dist.destroy_process_group()
+
+
+def test_pp_amr_sharded_two_ranks_gloo(D, orc, tmp_path):
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    out = str(tmp_path / "amr")
+    mp.start_processes(_amr_rank, args=(2, port, out), nprocs=2, join=True, start_method="spawn")
+    cfg = W.PPConfig("amrd", (6, 5, 4), 8)
+    w_keys, w_boxes = orc.pp_amr(cfg.n_levels, cfg.w, cfg.params, cfg.inputs, (0, 0, 0), (1, 1, 1), 5, 8, 13,
+                                 invocation0=2)
+    for r in range(2):
+        z = np.load(f"{out}.{r}.npz")
+        assert [int(k) & (2 ** 64 - 1) for k in z["keys"]] == [int(k) for k in w_keys]
+        assert np.array_equal(_bits(z["boxes"]), _bits(w_boxes))
