@@ -3,6 +3,8 @@
 Public Python API (thin wrappers over the C ABI in include/distill.h):
 
     load_model(kind, n_levels, levels, cost_weights, params, device=0) -> Model
+    grid_search(model, inputs, n_samples, seed, shard=(rank, world)) -> (net, key)
+    best(key, group=None) -> (cost, index)        # all-reduce across ranks + decode
     eval_grid(model, inputs, n_samples, seed, begin=0, end=None, net=None, best=None, ...)
     eval_grid_host(model, inputs, n_samples, seed, ...)   # host buffers, end to end
     eval_grid_multi(model, d_inputs, n_invocations, n_samples, seed, ...)   # many invocations, one launch
@@ -17,11 +19,11 @@ Public Python API (thin wrappers over the C ABI in include/distill.h):
 Importing this package does not touch the GPU; the shared library is loaded
 on first use and there is no CPU fallback.
 """
-from .api import (KEY_INIT, AmrRun, EpisodeRun, Model, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_multi, key_decode,
+from .api import (KEY_INIT, AmrRun, EpisodeRun, Model, best, grid_search, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_multi, key_decode,
                   key_reset, launch_count, load_model, pp_amr, pp_episode)
 from .dist import (best_allreduce, hist_allreduce, key_to_i64, i64_to_key, pp_amr_sharded, pp_episode_sharded,
                    shard_range)
 
-__all__ = ["KEY_INIT", "Model", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "eval_grid_multi", "key_decode", "pp_episode", "pp_amr",
+__all__ = ["KEY_INIT", "Model", "best", "grid_search", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "eval_grid_multi", "key_decode", "pp_episode", "pp_amr",
            "key_reset", "launch_count", "load_model", "best_allreduce", "hist_allreduce", "key_to_i64",
            "i64_to_key", "shard_range", "pp_episode_sharded", "EpisodeRun", "pp_amr_sharded", "AmrRun"]

@@ -105,6 +105,33 @@ def eval_grid(model: Model, inputs, n_samples: int, seed: int, begin: int = 0, e
     check(lib().distill_eval_grid(model.handle, C.byref(a), _stream_handle(stream)))
 
 
+def grid_search(model: Model, inputs, n_samples: int, seed: int, shard=None, invocation: int = 0, stream=None):
+    """One grid search with library-allocated outputs (SURVEY §8(b) L4 shape):
+    evaluates this rank's shard (shard = (rank, world), contiguous 4-aligned
+    ranges; None = the whole grid) and returns (net, key): net = V for the
+    shard's allocations (float32 CUDA tensor), key = the shard's best key
+    (int64 CUDA tensor, raw bits; combine across ranks with best())."""
+    import torch
+    from .dist import shard_range
+    b, e = (0, model.n_alloc) if shard is None else shard_range(model.n_alloc, int(shard[0]), int(shard[1]))
+    dev = torch.device("cuda", model.device)
+    net = torch.empty(max(e - b, 1), dtype=torch.float32, device=dev)
+    key = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    eval_grid(model, inputs, n_samples, seed, b, e, net=net, best=key, invocation=invocation, stream=stream)
+    return net[:e - b], key
+
+
+def best(key, group=None):
+    """Global best allocation from a shard key tensor: MIN all-reduce across the
+    process group when torch.distributed is initialised with world size > 1
+    (in place), then decode -> (cost C, global index); V = -C."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        from .dist import best_allreduce
+        best_allreduce(key, group)
+    return key_decode(key_from_tensor(key))
+
+
 def eval_grid_multi(model: Model, inputs, n_invocations: int, n_samples: int, seed: int, begin: int = 0,
                     end: Optional[int] = None, invocation0: int = 0, net=None, best=None, stream=None) -> None:
     """distill_eval_grid_multi: invocation t on position set t mod n_sets, RNG invocation invocation0 + t.
@@ -296,5 +323,5 @@ def key_from_tensor(best) -> int:
     return int(best.reshape(-1)[0].item()) & (2 ** 64 - 1)
 
 
-__all__ = ["KEY_INIT", "AmrRun", "DistillError", "EpisodeRun", "Model", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",
+__all__ = ["KEY_INIT", "AmrRun", "DistillError", "EpisodeRun", "Model", "grid_search", "best", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",
            "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode", "argmax_ties", "pp_amr", "sm_clock_mhz"]

@@ -798,3 +798,23 @@ def test_pp_amr_sharded_two_ranks_gloo(D, orc, tmp_path):
         z = np.load(f"{out}.{r}.npz")
         assert [int(k) & (2 ** 64 - 1) for k in z["keys"]] == [int(k) for k in w_keys]
         assert np.array_equal(_bits(z["boxes"]), _bits(w_boxes))
+
+
+def test_grid_search_and_best_convenience(D, orc):
+    """L4 convenience: grid_search over shard=(rank, world) returns
+    (net, key); the min of the shard keys decodes through best() to the oracle's
+    argmax, and the shard nets concatenate to the oracle's V."""
+    cfg = W.PPConfig("gs", (11, 9, 7), 12)
+    m = _model(D, cfg)
+    want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc, 12, cfg.seed)
+    k_or = orc.argmax_net(-want)[0]
+    nets, keys = [], []
+    for r in range(3):
+        net, key = D.grid_search(m, cfg.inputs, 12, cfg.seed, shard=(r, 3))
+        nets.append(net.cpu().numpy())
+        keys.append(int(key.item()) & (2 ** 64 - 1))
+    assert np.array_equal(_bits(-np.concatenate(nets)), _bits(want))
+    assert min(keys) == k_or
+    net, key = D.grid_search(m, cfg.inputs, 12, cfg.seed)
+    cost, idx = D.best(key)
+    assert idx == k_or & 0xFFFFFFFF and np.float32(cost) == want[idx]
