@@ -63,15 +63,18 @@ def _worker(rank, world, port, q):
     k, _ = oracle.argmax_net(-C, b)
     u = k if k < 2 ** 63 else k - 2 ** 64        # raw bits into int64 storage
     best = torch.tensor([u], dtype=torch.int64)
+    best2 = best.clone()
     best_allreduce(best)
     key = int(best.item()) & (2 ** 64 - 1)
+    from paper_2110_15425_b200.api import best as best_of       # all-reduce + decode (L4 convenience)
+    decoded = best_of(best2)
     d = W.DDMConfig(n_steps=120)
     p = oracle.ddm_params(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
                           d.x_lo, d.x_hi)
     tb, te = shard_range(600, rank, world)
     h = [torch.from_numpy(x.astype(np.int64)) for x in oracle.ddm_batch(p, 5, tb, te)]
     hist_allreduce(h)
-    q.put((rank, key, [x.numpy().copy() for x in h]))
+    q.put((rank, key, decoded, [x.numpy().copy() for x in h]))
     dist.destroy_process_group()
 
 
@@ -95,7 +98,8 @@ def test_gloo_world2_key_and_hist_allreduce(orc):
     p = orc.ddm_params(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
                        d.x_lo, d.x_hi)
     h_full = orc.ddm_batch(p, 5, 0, 600)
-    for rank, key, h in res:
+    for rank, key, decoded, h in res:
         assert key == k_full
+        assert decoded[1] == k_full & 0xFFFFFFFF and np.float32(decoded[0]) == C[decoded[1]]
         for a, b in zip(h, h_full):
             assert np.array_equal(a.astype(np.uint64), b)
