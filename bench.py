@@ -46,7 +46,7 @@ FP32_PEAK_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12   # TFLOP/s (the extras' deno
 # DDM step = 1/4 quad block (2 Box-Muller pairs: 2 x 60 + 4 products = 124) + 2 fma = 35;
 # Stroop step = 1/2 quad block (62) + pathways 2 x 3 + rectified LCA 2 x 8 = 84.
 DDM_FLOPS_PER_STEP = 35
-STROOP_FLOPS_PER_STEP = 84
+STROOP_FLOPS_PER_STEP = 78   # per trial-step: 2 normals (2 x 31) + rectified LCA 16; the pathway h_k(n) is trial-invariant (per-block table)
 
 
 def env_int(name, default):

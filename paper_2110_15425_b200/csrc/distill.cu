@@ -53,7 +53,7 @@ constexpr uint32_t MAX_SAMPLES = 1u << 31;
 constexpr int DDM_BLOCK = 128;
 constexpr int DDM_MINB = 6;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt, v5)
 constexpr int STROOP_BLOCK = 128;
-constexpr int STROOP_MINB = 6;   // same sweep
+constexpr int STROOP_MINB = 0;   // same sweep
 
 }  // namespace
 
@@ -285,9 +285,15 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
             const uint64_t c2 = (want * 64 + count - 1) / count;
             chunks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(chunks, c2));
         }
+        const size_t table_bytes = 4ull * p.n_steps * sizeof(float);
         for (uint64_t off = 0; off < count; off += 65535) {
             const unsigned gy = (unsigned)std::min<uint64_t>(65535, count - off);
-            stroop_sim_kernel<STROOP_BLOCK, STROOP_MINB><<<dim3(chunks, gy), STROOP_BLOCK, 0, st>>>(p, (uint32_t)off);
+            if (table_bytes <= 48 * 1024)      // pathway table in shared memory (trial-invariant h_k(n))
+                stroop_sim_kernel<STROOP_BLOCK, STROOP_MINB, true><<<dim3(chunks, gy), STROOP_BLOCK, table_bytes, st>>>(
+                    p, (uint32_t)off);
+            else
+                stroop_sim_kernel<STROOP_BLOCK, STROOP_MINB, false><<<dim3(chunks, gy), STROOP_BLOCK, 0, st>>>(
+                    p, (uint32_t)off);
             g_launches++;
             CUDA_TRY(cudaGetLastError());
         }

@@ -28,19 +28,36 @@ struct StroopArgs {
 };
 
 // One LCA step of both response units (spec/MODELS.md §6 loop body; the old
-// x of both units feeds both q's).
-__device__ __forceinline__ void lca_step(const StroopArgs& a, float I0, float I1, float nleak, float ninh, float nsd,
-                                         float g0, float g1, float& h0, float& h1, float& x0, float& x1) {
-    h0 = __fmaf_rn(a.tau, __fadd_rn(I0, -h0), h0);
-    h1 = __fmaf_rn(a.tau, __fadd_rn(I1, -h1), h1);
+// x of both units feeds both q's), given the pathway outputs h0, h1 of this step.
+__device__ __forceinline__ void lca_update(const StroopArgs& a, float nleak, float ninh, float nsd, float g0, float g1,
+                                           float h0, float h1, float& x0, float& x1) {
     const float q0 = __fmaf_rn(ninh, x1, __fmaf_rn(nleak, x0, h0));
     const float q1 = __fmaf_rn(ninh, x0, __fmaf_rn(nleak, x1, h1));
     x0 = fmaxf(__fmaf_rn(nsd, g0, __fmaf_rn(a.dt, q0, x0)), 0.0f);
     x1 = fmaxf(__fmaf_rn(nsd, g1, __fmaf_rn(a.dt, q1, x1)), 0.0f);
 }
 
-template <int BLOCK, int MINB = 0>
+// Pathway output of step n (1-based) for the trial's input row: the recurrence
+// h = fma(τ, I - h, h) from h = 0 does not depend on the trial's noise, so
+// TABLE kernels read it from a per-block table built once (rows: I = 0, ic,
+// iw, ic + iw); otherwise it is advanced in registers.  Same values either way.
+template <bool TABLE>
+struct Pathway {
+    const float* row0; const float* row1;   // TABLE
+    float I0, I1, tau, h0, h1;              // !TABLE
+    __device__ __forceinline__ void at(uint32_t n, float& o0, float& o1) {
+        if (TABLE) { o0 = row0[n - 1]; o1 = row1[n - 1]; }
+        else {
+            h0 = __fmaf_rn(tau, __fadd_rn(I0, -h0), h0);
+            h1 = __fmaf_rn(tau, __fadd_rn(I1, -h1), h1);
+            o0 = h0; o1 = h1;
+        }
+    }
+};
+
+template <int BLOCK, int MINB = 0, bool TABLE = true>
 __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArgs a, uint32_t alloc_off) {
+    extern __shared__ float s_htab[];                         // TABLE: [4][n_steps]
     const uint32_t t_alloc = alloc_off + blockIdx.y;           // index within [0, count)
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
@@ -49,6 +66,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
     const float iw = __fmul_rn(a.g_w, __fadd_rn(1.0f, -us));
     const float nsd = __fmul_rn(a.noise, __fsqrt_rn(a.dt));
     const float nleak = -a.leak, ninh = -a.inh;
+    const uint32_t N = a.n_steps;
+    if (TABLE) {
+        for (uint32_t n = threadIdx.x; n < N; n += BLOCK) s_htab[n] = 0.0f;   // row 0: I = 0 stays +0
+        if (threadIdx.x >= 1 && threadIdx.x <= 3) {
+            const float I = threadIdx.x == 1 ? __fadd_rn(ic, 0.0f) : threadIdx.x == 2 ? __fadd_rn(0.0f, iw)
+                                                                   : __fadd_rn(ic, iw);
+            float* row = s_htab + threadIdx.x * N;
+            float h = 0.0f;
+            for (uint32_t n = 0; n < N; ++n) { h = __fmaf_rn(a.tau, __fadd_rn(I, -h), h); row[n] = h; }
+        }
+        __syncthreads();
+    }
 
     uint32_t n_corr = 0, n_und = 0;
     unsigned long long rts = 0;
@@ -56,25 +85,34 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
          j += gridDim.x * BLOCK) {
         const uint32_t kind = j % 3, colour = (j / 3) & 1;
         const int word = (kind == 0) ? (int)colour : (kind == 1) ? (int)(1 - colour) : -1;
-        const float I0 = __fadd_rn(colour == 0 ? ic : 0.0f, word == 0 ? iw : 0.0f);
-        const float I1 = __fadd_rn(colour == 1 ? ic : 0.0f, word == 1 ? iw : 0.0f);
+        Pathway<TABLE> pw;
+        if (TABLE) {
+            pw.row0 = s_htab + N * ((colour == 0 ? 1u : 0u) + (word == 0 ? 2u : 0u));
+            pw.row1 = s_htab + N * ((colour == 1 ? 1u : 0u) + (word == 1 ? 2u : 0u));
+        } else {
+            pw.I0 = __fadd_rn(colour == 0 ? ic : 0.0f, word == 0 ? iw : 0.0f);
+            pw.I1 = __fadd_rn(colour == 1 ? ic : 0.0f, word == 1 ? iw : 0.0f);
+            pw.tau = a.tau; pw.h0 = 0.0f; pw.h1 = 0.0f;
+        }
         const uint64_t unit = (uint64_t)i * a.n_trials + j;
         PhiloxHoisted rng;
         rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
-        float h0 = 0.f, h1 = 0.f, x0 = 0.f, x1 = 0.f;
+        float x0 = 0.f, x1 = 0.f;
         int resp = -1;
         uint32_t st = 0;
         // Six steps (12 normals, two sextet blocks) per group.  x_k >= 0 after
         // the rectification (fmaxf(NaN, 0) = 0 as well), so "x0 >= θ or x1 >= θ"
         // at any step of the group <=> the max of its 12 states >= θ: one test
         // per group; the rare group that passes is resolved in the spec's order.
-        const uint32_t n6 = a.n_steps / 6;
-        for (uint32_t j = 0; j < n6; ++j) {
+        const uint32_t n6 = N / 6;
+        for (uint32_t grp = 0; grp < n6; ++grp) {
             float g[12], s0[6], s1[6];
-            acc_normals12(rng, j, g);
+            acc_normals12(rng, grp, g);
 #pragma unroll
             for (int l = 0; l < 6; ++l) {
-                lca_step(a, I0, I1, nleak, ninh, nsd, g[2 * l], g[2 * l + 1], h0, h1, x0, x1);
+                float h0, h1;
+                pw.at(6 * grp + l + 1, h0, h1);
+                lca_update(a, nleak, ninh, nsd, g[2 * l], g[2 * l + 1], h0, h1, x0, x1);
                 s0[l] = x0; s1[l] = x1;
             }
             if (resp < 0) {
@@ -85,21 +123,23 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
 #pragma unroll
                     for (int l = 0; l < 6; ++l) {
                         if (resp < 0) {
-                            if (s0[l] >= a.thr) { resp = 0; st = 6 * j + l + 1; }
-                            else if (s1[l] >= a.thr) { resp = 1; st = 6 * j + l + 1; }
+                            if (s0[l] >= a.thr) { resp = 0; st = 6 * grp + l + 1; }
+                            else if (s1[l] >= a.thr) { resp = 1; st = 6 * grp + l + 1; }
                         }
                     }
                 }
             }
         }
-        const uint32_t rem = a.n_steps - 6 * n6;
+        const uint32_t rem = N - 6 * n6;
         if (rem) {  // ragged last group
             float g[12];
             acc_normals_tail(rng, n6, 2 * rem, g);
 #pragma unroll
             for (int l = 0; l < 5; ++l) {
                 if ((uint32_t)l < rem) {
-                    lca_step(a, I0, I1, nleak, ninh, nsd, g[2 * l], g[2 * l + 1], h0, h1, x0, x1);
+                    float h0, h1;
+                    pw.at(6 * n6 + l + 1, h0, h1);
+                    lca_update(a, nleak, ninh, nsd, g[2 * l], g[2 * l + 1], h0, h1, x0, x1);
                     if (resp < 0) {
                         if (x0 >= a.thr) { resp = 0; st = 6 * n6 + l + 1; }
                         else if (x1 >= a.thr) { resp = 1; st = 6 * n6 + l + 1; }
@@ -182,10 +222,12 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
     const float ic = __fmul_rn(a.g_c, uc);
     const float iw = __fmul_rn(a.g_w, __fadd_rn(1.0f, -us));
     const float nsd = __fmul_rn(a.sig, __fsqrt_rn(a.dt));
-    uint32_t n_both = 0, n_und = 0;
-    unsigned long long rts = 0;
-    for (uint32_t j = a.trial_begin + blockIdx.x * BLOCK + threadIdx.x; j < a.trial_end; j += gridDim.x * BLOCK) {
-        const uint32_t kind = j % 3, colour = (j / 3) & 1;
+    // The pathway front-end, the conflict energy and both drifts depend only on
+    // the stimulus (kind, colour) and the allocation, not on the trial's noise:
+    // six (kind, colour) combinations, computed once per block by six threads.
+    __shared__ float s_drift[6][2];
+    if (threadIdx.x < 6) {
+        const uint32_t kind = threadIdx.x >> 1, colour = threadIdx.x & 1;
         const int word = (kind == 0) ? (int)colour : (kind == 1) ? (int)(1 - colour) : -1;
         const float I0 = __fadd_rn(colour == 0 ? ic : 0.0f, word == 0 ? iw : 0.0f);
         const float I1 = __fadd_rn(colour == 1 ? ic : 0.0f, word == 1 ? iw : 0.0f);
@@ -204,6 +246,15 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
             A2 = __fmaf_rn(E, -a.gam, a.a_p);
             A1 = __fmul_rn(__fmul_rn(__fadd_rn(hc, -hw), __fmul_rn(2.0f, a.lam)), 0.5f);
         }
+        s_drift[threadIdx.x][0] = A1;
+        s_drift[threadIdx.x][1] = A2;
+    }
+    __syncthreads();
+    uint32_t n_both = 0, n_und = 0;
+    unsigned long long rts = 0;
+    for (uint32_t j = a.trial_begin + blockIdx.x * BLOCK + threadIdx.x; j < a.trial_end; j += gridDim.x * BLOCK) {
+        const uint32_t kind = j % 3, colour = (j / 3) & 1;
+        const float A1 = s_drift[2 * kind + colour][0], A2 = s_drift[2 * kind + colour][1];
         const uint64_t unit = (uint64_t)i * a.n_trials + j;
         PhiloxHoisted rng;
         rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);

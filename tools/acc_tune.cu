@@ -1,5 +1,6 @@
 // Block/occupancy sweep for the accumulator kernels (DDM cfg2, Stroop cfg4 slice); tools only.
 // Results must be identical to the reference variant (integer histograms / counts).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -36,16 +37,20 @@ void ddm(const char* name, DDMArgs a, size_t n_all, bool ref) {
            h == g_ref_ddm ? "identical" : "MISMATCH");
 }
 
-template <int BLOCK, int MINB>
+template <int BLOCK, int MINB, bool TABLE = true>
 void stroop(const char* name, StroopArgs a, bool ref) {
-    cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, stroop_sim_kernel<BLOCK, MINB>);
-    const uint32_t chunks = (a.trial_end + BLOCK - 1) / BLOCK;
+    cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, stroop_sim_kernel<BLOCK, MINB, TABLE>);
+    // the library's launch shape (distill.cu launch_stroop): chunks capped so the
+    // grid holds ~64 blocks per resident slot
+    uint32_t chunks = (a.trial_end + BLOCK - 1) / BLOCK;
+    const uint64_t want = 148ull * 8 * 64;
+    if ((uint64_t)chunks * a.count > want) chunks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(chunks, (want + a.count - 1) / a.count));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     float best = 1e30f;
     for (int r = 0; r < 3; ++r) {
         cudaMemset(a.counts, 0, a.count * 24);
         cudaEventRecord(e0);
-        stroop_sim_kernel<BLOCK, MINB><<<dim3(chunks, a.count), BLOCK>>>(a, 0);
+        stroop_sim_kernel<BLOCK, MINB, TABLE><<<dim3(chunks, a.count), BLOCK, TABLE ? 16 * a.n_steps : 0>>>(a, 0);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         if (r && ms < best) best = ms;
@@ -86,7 +91,9 @@ int main() {
     s.n_trials = 100000; s.trial_begin = 0; s.trial_end = 100000; s.key0 = 42; s.key1 = 0;
     s.begin = 5000; s.count = 200; s.levels = dl;
     cudaMalloc((void**)&s.counts, 200 * 24);
-    stroop<256, 0>("ref", s, true);
+    stroop<128, 6, false>("ref (no table)", s, true);
+    stroop<128, 6, true>("table", s, false);
+    stroop<256, 0>("", s, false);
     stroop<256, 3>("", s, false); stroop<256, 4>("", s, false); stroop<128, 0>("", s, false);
     stroop<128, 6>("", s, false); stroop<128, 8>("", s, false); stroop<64, 0>("", s, false);
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
