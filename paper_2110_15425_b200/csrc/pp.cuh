@@ -239,33 +239,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs 
     }
 }
 
-// Persistent variant: a fixed grid of resident blocks pulls BLOCK-allocation
-// chunks from a device counter (zeroed by the caller before the launch), so
-// the last wave has no idle SMs; keys are min-combined per block across chunks.
-template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false, bool EVEN = false>
-__global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_persistent_kernel(const PPArgs a,
-                                                                               unsigned int* __restrict__ counter) {
-    __shared__ unsigned int s_chunk;
-    const uint32_t n_chunks = (a.count + BLOCK - 1) / BLOCK;
-    const float2 ustar = pp_ustar_block(a);
-    key64_t key = KEY_INIT;
-    for (;;) {
-        if (threadIdx.x == 0) s_chunk = atomicAdd(counter, 1u);
-        __syncthreads();
-        const uint32_t c = s_chunk;
-        __syncthreads();
-        if (c >= n_chunks) break;
-        const uint32_t tid = c * BLOCK + threadIdx.x;
-        if (tid < a.count) {
-            const uint32_t i = a.begin + tid;
-            const float C = pp_eval_alloc<MASK, PIPE, EVEN>(a, i, ustar);
-            if (a.net) a.net[tid] = -C;
-            const key64_t k = make_key(C, i);
-            key = k < key ? k : key;
-        }
-    }
-    if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
-}
 
 // ---------------------------------------------------------------- NEXT-1
 // Closed-loop episode step t (spec/MODELS.md §7): read the step's best key,
