@@ -16,7 +16,7 @@
  *   od_ln / od_rsqrt / od_sincos2pi   pinned: exhaustive / dense accuracy vs binary64 libm
  *   od_normal_*          pinned: moments, KS vs Phi, closed-form endpoints
  *   od_pp_eval           pinned: zero-noise closed forms, monotonicity, planted optimum, offset-Gaussian
- *                        angle law (noisy objective in closed form),
+ *                        angle law (noisy objective in closed form), noisy-predator quadrature,
  *                        small-noise delta-method expectation, fp64 re-evaluation
  *   od_argmax_keys       pinned: brute-force min over (C, i), NaN/-0 rules
  *   od_normal_acc        pinned: raw-word Box-Muller definition, moments/kurtosis/KS; cuRAND Philox

@@ -258,3 +258,44 @@ def test_noisy_prey_objective_matches_offset_gaussian_angle_law(orc):
     want = 2 - 2 * ecos(nu)
     assert abs(C.mean() - want) <= 4 * se, (C.mean(), want, se)
     assert abs(C.mean() - (2 - 2 * ecos(r / sig ** 2))) > 20 * se
+
+
+def test_noisy_predator_action_matches_angle_law_quadrature(orc):
+    """Pin of the Action node's predator term under real noise (toward the
+    prey, away from the predator): prey and player noise-free, the predator
+    observed with std sigma.  Only the direction of the observed predator enters
+    (unit(v_d)), and its angle around the true direction follows the exact
+    offset-Gaussian angle density, so E[|u - u*|^2] is a 1-D integral over that
+    density of |unit(u_p - kappa u(phi0 + psi)) - u*|^2 (scipy quadrature).
+    The oracle's mean over 64 x 10^4 samples must match within 4 SE + 1 %;
+    a flipped kappa sign (0.096 vs 0.036) is rejected."""
+    from scipy import integrate, special
+    sig, kap = 2.0, 0.5
+    pp, pd = np.array([4.0, 0.0]), np.array([-3.0, 2.0])
+    nu, phi0 = math.hypot(*pd) / sig, math.atan2(pd[1], pd[0])
+
+    def dens(t):
+        c = math.cos(t)
+        return (math.exp(-nu * nu / 2) / (2 * math.pi)
+                * (1 + math.sqrt(2 * math.pi) * nu * c * math.exp(nu * nu * c * c / 2) * special.ndtr(nu * c)))
+
+    def unit(v):
+        return v / math.hypot(*v)
+
+    def expect(k):
+        up = unit(pp)
+        us = unit(up - k * np.array([math.cos(phi0), math.sin(phi0)]))
+
+        def obj(psi):
+            u = unit(up - k * np.array([math.cos(phi0 + psi), math.sin(phi0 + psi)]))
+            return float(((u - us) ** 2).sum())
+        return integrate.quad(lambda t: obj(t) * dens(t), -math.pi, math.pi, epsabs=1e-12, limit=200)[0]
+
+    L = 64
+    levels = np.array([1.0] + [0.0] * L + [1.0], np.float32)     # prey level 1, predator level 0, player level 1
+    C = orc.pp_eval((1, L, 1), levels, np.zeros(3, np.float32), np.array([sig, 0.0, kap], np.float32),
+                    np.array([4, 0, -3, 2, 0, 0], np.float32), 0, L, 10000, 11).astype(np.float64)
+    se = C.std() / math.sqrt(L)
+    want = expect(kap)
+    assert abs(C.mean() - want) <= 4 * se + 0.01 * want, (C.mean(), want, se)
+    assert abs(C.mean() - expect(-kap)) > 100 * se
