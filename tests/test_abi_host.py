@@ -124,3 +124,19 @@ def test_eval_grid_multi_validates_before_cuda(abi):
     a = abi.MultiArgs()
     assert L.distill_eval_grid_multi(None, C.byref(a), None) == abi.E_INVALID_ARG
     assert L.distill_eval_grid_multi(None, None, None) == abi.E_INVALID_ARG
+
+
+def test_binding_buffer_checks_on_cpu():
+    """The binding's buffer checks run before any ABI call: host tensors, wrong
+    element types, non-contiguous or short buffers are rejected with ValueError."""
+    import pytest
+    import torch
+    from paper_2110_15425_b200 import api
+    with pytest.raises(ValueError, match="CUDA"):
+        api._dev_ptr(torch.zeros(4), "net", 4)
+    assert api._dev_ptr(None, "net", 4) is None
+    t = torch.zeros(4, dtype=torch.float64)
+    t.is_cuda                                   # host tensor: the CUDA check fires first
+    with pytest.raises(ValueError):
+        api._dev_ptr(t, "net", 4)
+    assert set(api._BUF_DTYPE.values()) == {"float32", "int64", "int32"}
