@@ -468,6 +468,34 @@ def run_extras(D, torch, dev, rank, world, args):
                                     "frac_fp32_peak": (FLOPS_PER_SAMPLE * c3.evals + FLOPS_PER_ALLOC * c3.n_alloc) * T / (mms / 1e3) / 1e12
                                     / FP32_PEAK_NOMINAL,
                                     "note": "16 invocations x cfg3 (positions uniform in [-10,10]^2) in one launch"}
+    # the paper's predator-prey sizes S / M / L / XL (2, 4, 6, 100 levels per entity),
+    # 100 samples per allocation; small grids are launch-latency bound (one kernel each)
+    if world == 1:
+        sizes = {}
+        for name, L in (("S", 2), ("M", 4), ("L", 6), ("XL", 100)):
+            cs = W.PPConfig(f"pp_{name}", (L, L, L), 100)
+            msz = D.load_model(W.KIND_PREDATOR_PREY, cs.n_levels, cs.levels, cs.w, cs.params, device=dev.index)
+            snet = torch.empty(cs.n_alloc, dtype=torch.float32, device=dev)
+            sbest = torch.empty(1, dtype=torch.int64, device=dev)
+            D.eval_grid(msz, cs.inputs, cs.n_samples, cs.seed, net=snet, best=sbest)
+            torch.cuda.synchronize()
+            # device time per grid search: 20 launches captured in a CUDA graph and replayed,
+            # so the host's per-call overhead does not pace the GPU
+            reps = 20
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for _ in range(reps):
+                    D.eval_grid(msz, cs.inputs, cs.n_samples, cs.seed, net=snet, best=sbest)
+            graph.replay()
+            torch.cuda.synchronize()
+            e0.record()
+            graph.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            sms = e0.elapsed_time(e1) / reps
+            sizes[name] = {"allocations": cs.n_alloc, "ms": sms, "evals_per_s": cs.evals / (sms / 1e3),
+                           "timing": "CUDA-graph replay of 20 grid searches"}
+        out["pp_paper_sizes"] = sizes
     if args.stroop:
         c = W.stroop_cfg4()
         m = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=dev.index)

@@ -50,6 +50,11 @@ constexpr int ARGMAX_BLOCK = 256;
 // sample / trial loops step a 32-bit counter by up to 2 (PP pairs) or a grid
 // stride (Stroop): bounding the count at 2^31 keeps them from wrapping
 constexpr uint32_t MAX_SAMPLES = 1u << 31;
+#ifndef DISTILL_PP_SMALL_MODE
+#define DISTILL_PP_SMALL_MODE 1   // 0: always one thread per allocation (A/B measurements only)
+#endif
+constexpr int PP_SMALL_WARPS = 4;    // pp_eval_small_kernel: allocations per block
+constexpr uint32_t PP_SMALL_SMAX = 1024;   // its per-warp sample buffer
 constexpr int DDM_BLOCK = 128;
 constexpr int DDM_MINB = 6;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt, v5)
 constexpr int STROOP_BLOCK = 128;
@@ -173,6 +178,17 @@ distill_status distill_grid_size(const distill_model* m, uint64_t* n_alloc) {
     return DISTILL_OK;
 }
 
+// Latency mode (pp_eval_small_kernel, one warp per allocation) for grids that
+// cannot fill the GPU one thread per allocation.
+static bool pp_small(const distill_model* m, uint64_t count, uint32_t n_samples) {
+    return DISTILL_PP_SMALL_MODE && n_samples <= PP_SMALL_SMAX && count * 32 <= (uint64_t)m->n_sm * 2048;
+}
+
+static void launch_pp_small(const PPArgs& p, uint64_t count, cudaStream_t st) {
+    pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX>
+        <<<(unsigned)((count + PP_SMALL_WARPS - 1) / PP_SMALL_WARPS), PP_SMALL_WARPS * 32, 0, st>>>(p);
+}
+
 static distill_status launch_pp(const distill_model* m, const distill_eval_args* a, cudaStream_t st,
                                 key64_t* publish = nullptr, unsigned int* done = nullptr) {
     if (!a->inputs || a->n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): needs 6 host inputs");
@@ -197,7 +213,9 @@ static distill_status launch_pp(const distill_model* m, const distill_eval_args*
     p.publish = publish; p.done = done;
     const unsigned grid = (unsigned)((count + PP_BLOCK - 1) / PP_BLOCK);
     const bool even = (a->n_samples & 1u) == 0;
-    if (publish) {
+    if (!publish && pp_small(m, count, a->n_samples)) {
+        launch_pp_small(p, count, st);
+    } else if (publish) {
         if (even)
             pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
         else
@@ -480,7 +498,8 @@ static void episode_search(const distill_model* m, const distill_episode_args* e
     p.best = e->d_keys + t;
     p.begin = (uint32_t)begin; p.count = (uint32_t)(end - begin);
     const unsigned grid = (unsigned)((end - begin + PP_BLOCK - 1) / PP_BLOCK);
-    if ((e->n_samples & 1u) == 0) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+    if (pp_small(m, end - begin, e->n_samples)) launch_pp_small(p, end - begin, st);
+    else if ((e->n_samples & 1u) == 0) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
     else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
     g_launches++;
 }
@@ -580,13 +599,14 @@ static PPArgs amr_pp_args(const distill_model* m, const distill_amr_args* g) {
     return p;
 }
 
-static void amr_search(const distill_amr_args* g, PPArgs p, uint32_t r, uint64_t begin, uint64_t end,
-                       cudaStream_t st) {
+static void amr_search(const distill_model* m, const distill_amr_args* g, PPArgs p, uint32_t r, uint64_t begin,
+                       uint64_t end, cudaStream_t st) {
     p.invocation = g->invocation0 + r;
     p.best = g->d_keys + r;
     p.begin = (uint32_t)begin; p.count = (uint32_t)(end - begin);
     const unsigned grid = (unsigned)((end - begin + PP_BLOCK - 1) / PP_BLOCK);
-    if ((g->n_samples & 1u) == 0) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
+    if (pp_small(m, end - begin, g->n_samples)) launch_pp_small(p, end - begin, st);
+    else if ((g->n_samples & 1u) == 0) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
     else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
     g_launches++;
 }
@@ -618,7 +638,7 @@ distill_status distill_pp_amr_search(const distill_model* m, const distill_amr_a
     if (begin > end || end > m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "pp_amr_search: bad shard");
     if (begin == end) return DISTILL_OK;
     CUDA_TRY(cudaSetDevice(m->device));
-    amr_search(g, amr_pp_args(m, g), r, begin, end, (cudaStream_t)stream);
+    amr_search(m, g, amr_pp_args(m, g), r, begin, end, (cudaStream_t)stream);
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;
 }
@@ -642,7 +662,7 @@ distill_status distill_pp_amr(const distill_model* m, const distill_amr_args* g,
     const PPArgs p = amr_pp_args(m, g);
     for (uint32_t r = 0; r < g->rounds; ++r) {
         amr_levels_kernel<<<1, 256, 0, st>>>(a, r);
-        amr_search(g, p, r, 0, m->n_alloc, st);
+        amr_search(m, g, p, r, 0, m->n_alloc, st);
         amr_refine_kernel<<<1, 32, 0, st>>>(a, r);
         g_launches += 2;
     }

@@ -132,6 +132,30 @@ __device__ __forceinline__ float2 pp_ustar_block(const PPArgs& a) {
     return s_us;
 }
 
+// a3 + a4 for the sample pair whose Philox blocks are X (lane x) and Y (lane y):
+// sextet packing -> three 2-D Box-Muller pairs (spec/RNG.md §6), observations
+// p + sigma rad (cos, sin), Action, Objective.  Returns the two squared chords.
+template <bool SOBJ, bool SLN2, bool SRS2, bool SSC2>
+__device__ __forceinline__ F2 pp_pair_errors(const uint4& X, const uint4& Y, float s0, float s1, float s2,
+                                             const V2& P0, const V2& P1, const V2& P2, F2 mk, const V2& us) {
+    F2 r0, c0, n0, r1, c1, n1, r2, c2, n2;
+    {
+        const uint32_t wx0 = sextet_angle_word(X, 0), wy0 = sextet_angle_word(Y, 0);
+        const uint32_t wx1 = sextet_angle_word(X, 1), wy1 = sextet_angle_word(Y, 1);
+        const uint32_t wx2 = sextet_angle_word(X, 2), wy2 = sextet_angle_word(Y, 2);
+        bm_polar2_fs<false, false, false, 0x7FFF00u>(X.x, Y.x, wx0, wy0, wx0, wy0, r0, c0, n0);
+        bm_polar2_fs<false, false, false, 0x7FFF00u>(X.y, Y.y, wx1, wy1, wx1, wy1, r1, c1, n1);
+        bm_polar2_fs<SLN2, SRS2, SSC2, 0x7FFF00u>(X.z, Y.z, wx2, wy2, wx2, wy2, r2, c2, n2);
+    }
+    using O = Ops<false>;
+    const F2 q0 = O::mul(bc(s0), r0), q1 = O::mul(bc(s1), r1), q2 = O::mul(bc(s2), r2);
+    const V2 o0 = {O::fma(q0, c0, P0.x), O::fma(q0, n0, P0.y)};
+    const V2 o1 = {O::fma(q1, c1, P1.x), O::fma(q1, n1, P1.y)};
+    const V2 o2 = {O::fma(q2, c2, P2.x), O::fma(q2, n2, P2.y)};
+    const V2 d = action2<SOBJ>(o0, o1, o2, mk);
+    return objective2<SOBJ>(d, us);
+}
+
 template <int MASK, bool PIPE, bool EVEN = false>
 __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, float2 ustar) {
     constexpr bool SOBJ = MASK & PP_SC_OBJECTIVE;
@@ -167,30 +191,63 @@ __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, floa
         } else {
             X = rng(s); Y = rng(s + 1);
         }
-        // a3: sextet packing -> three 2-D Box-Muller pairs (spec/RNG.md §6)
-        F2 r0, c0, n0, r1, c1, n1, r2, c2, n2;
-        {
-            const uint32_t wx0 = sextet_angle_word(X, 0), wy0 = sextet_angle_word(Y, 0);
-            const uint32_t wx1 = sextet_angle_word(X, 1), wy1 = sextet_angle_word(Y, 1);
-            const uint32_t wx2 = sextet_angle_word(X, 2), wy2 = sextet_angle_word(Y, 2);
-            bm_polar2_fs<false, false, false, 0x7FFF00u>(X.x, Y.x, wx0, wy0, wx0, wy0, r0, c0, n0);
-            bm_polar2_fs<false, false, false, 0x7FFF00u>(X.y, Y.y, wx1, wy1, wx1, wy1, r1, c1, n1);
-            bm_polar2_fs<SLN2, SRS2, SSC2, 0x7FFF00u>(X.z, Y.z, wx2, wy2, wx2, wy2, r2, c2, n2);
-        }
-        // a4: Obs (p + sigma rad (cos, sin)) -> Action -> Objective
-        using O = Ops<false>;
-        const F2 q0 = O::mul(bc(s0), r0), q1 = O::mul(bc(s1), r1), q2 = O::mul(bc(s2), r2);
-        const V2 o0 = {O::fma(q0, c0, P0.x), O::fma(q0, n0, P0.y)};
-        const V2 o1 = {O::fma(q1, c1, P1.x), O::fma(q1, n1, P1.y)};
-        const V2 o2 = {O::fma(q2, c2, P2.x), O::fma(q2, n2, P2.y)};
-        const V2 d = action2<SOBJ>(o0, o1, o2, mk);
-        const F2 e = objective2<SOBJ>(d, us);
+        const F2 e = pp_pair_errors<SOBJ, SLN2, SRS2, SSC2>(X, Y, s0, s1, s2, P0, P1, P2, mk, us);
         // a7: sequential sum in ascending sample order
         acc = __fadd_rn(acc, e.x);
         if (EVEN || s + 1 < a.n_samples) acc = __fadd_rn(acc, e.y);
     }
     // a8: net of cost
     return __fadd_rn(__fdiv_rn(acc, __uint2float_rn(a.n_samples)), K);
+}
+
+// Small grids (latency mode): one warp per allocation.  Lane l evaluates the
+// sample pairs (2l + 64m, 2l + 1 + 64m); the squared chords go to shared
+// memory and lane 0 adds them in ascending sample order, so C is the same sum
+// as in the one-thread-per-allocation kernel, bit for bit.  Used when the grid
+// is too small to fill the GPU one thread per allocation (a few thousand
+// allocations or fewer) and n_samples <= SMAX.
+template <int WARPS, int SMAX>
+__global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs a0) {
+    __shared__ float s_e[WARPS][SMAX];
+    if (a0.status_dev && *a0.status_dev != 0) return;   // episode already over (uniform branch)
+    const PPArgs a = pp_resolve_positions(a0);
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tid = blockIdx.x * WARPS + w;            // allocation within the launch (warp-uniform)
+    const float2 ustar = pp_ustar_block(a);
+    key64_t key = KEY_INIT;
+    if (tid < a.count) {
+        const uint32_t i = a.begin + tid;
+        const uint32_t k2 = i % a.L2, r = i / a.L2;
+        const uint32_t k1 = r % a.L1, k0 = r / a.L1;
+        const float a0 = __ldg(a.levels + k0);
+        const float a1 = __ldg(a.levels + a.L0 + k1);
+        const float a2 = __ldg(a.levels + a.L0 + a.L1 + k2);
+        const float dsig = __fadd_rn(a.sigma_min, -a.sigma_max);
+        const float s0 = __fmaf_rn(a0, dsig, a.sigma_max);
+        const float s1 = __fmaf_rn(a1, dsig, a.sigma_max);
+        const float s2 = __fmaf_rn(a2, dsig, a.sigma_max);
+        const float K = __fmaf_rn(a.w2, a2, __fmaf_rn(a.w1, a1, __fmul_rn(a.w0, a0)));
+        const V2 P0 = {bc(a.prey_x), bc(a.prey_y)}, P1 = {bc(a.pred_x), bc(a.pred_y)};
+        const V2 P2 = {bc(a.pl_x), bc(a.pl_y)};
+        const V2 us = {bc(ustar.x), bc(ustar.y)};
+        PhiloxHoisted rng;
+        rng.init(i, a.invocation, 1u, a.key0, a.key1);
+        for (uint32_t s = 2 * lane; s < a.n_samples; s += 64) {
+            const F2 e = pp_pair_errors<false, false, false, false>(rng(s), rng(s + 1), s0, s1, s2, P0, P1, P2,
+                                                                    bc(-a.kappa), us);
+            s_e[w][s] = e.x;
+            if (s + 1 < a.n_samples) s_e[w][s + 1] = e.y;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            float acc = 0.0f;                                   // a7: ascending sample order
+            for (uint32_t s = 0; s < a.n_samples; ++s) acc = __fadd_rn(acc, s_e[w][s]);
+            const float C = __fadd_rn(__fdiv_rn(acc, __uint2float_rn(a.n_samples)), K);
+            if (a.net) a.net[tid] = -C;
+            key = make_key(C, i);
+        }
+    }
+    if (a.best) block_min_key_atomic<WARPS * 32>(key, a.best);
 }
 
 // One thread per allocation; one atomicMin per block.
