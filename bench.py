@@ -306,7 +306,11 @@ def run_ours(args):
 
     also = {}
     if not args.no_extras:
-        also = run_extras(D, torch, dev, rank, world, args)
+        try:
+            also = run_extras(D, torch, dev, rank, world, args)
+        except Exception as exc:    # the secondary measurements must never sink the headline line
+            also = {"error": repr(exc)[:300]}
+            torch.cuda.synchronize()
 
     if rank != 0:
         if world > 1:
