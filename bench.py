@@ -310,7 +310,10 @@ def run_ours(args):
             also = run_extras(D, torch, dev, rank, world, args)
         except Exception as exc:    # the secondary measurements must never sink the headline line
             also = {"error": repr(exc)[:300]}
-            torch.cuda.synchronize()
+            try:
+                torch.cuda.synchronize()
+            except Exception:
+                pass
 
     if rank != 0:
         if world > 1:
