@@ -1,0 +1,83 @@
+// Speed-of-light for pp_eval_grid's instruction mix (tools only).
+//
+// The shipped kernel's inner loop (two samples per iteration) issues, per warp
+// (cuobjdump of pp_eval_grid_kernel<128,0,7,false,true>, loop body):
+//   116 FFMA2, 31 FMUL2, 10 FADD2, 2 FADD, 30 IMAD.WIDE.U32, 1 IMAD,
+//   64 LOP3, 24 SHF, 24 IADD3, 12 I2FP, 6 VIADD, 6 PRMT   (~336 instructions)
+// This probe issues the same mix from 8 independent dependency chains per
+// thread (no data-dependence stalls), at the kernel's occupancy (128-thread
+// blocks, 7 per SM), and reports SMSP cycles per iteration: the best any
+// schedule of this instruction mix can do on the B200's pipes.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define N_ITER 256
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+__global__ void __launch_bounds__(128, 7) k_mix(float* out, float s, uint32_t m) {
+    float2 f[8], fm[4], fa[4];
+    uint32_t u[8];
+    float g[4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { f[j] = make_float2(threadIdx.x + j, j); u[j] = threadIdx.x * 7u + j; }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { fm[j] = make_float2(threadIdx.x + 3 * j, j); fa[j] = make_float2(j, threadIdx.x); }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g[j] = threadIdx.x + j;
+    const float2 S = make_float2(s, s), H = make_float2(0.5f, 0.5f);
+    for (int it = 0; it < N_ITER; ++it) {
+#pragma unroll
+        for (int k = 0; k < 116; ++k) f[k & 7] = ffma2(f[k & 7], S, H);
+#pragma unroll
+        for (int k = 0; k < 31; ++k) fm[k & 3] = __fmul2_rn(fm[k & 3], S);      // separate chains: a multiply
+#pragma unroll
+        for (int k = 0; k < 10; ++k) fa[k & 3] = __fadd2_rn(fa[k & 3], H);      // feeding an add would be fused
+        g[0] = __fadd_rn(g[0], s); g[1] = __fadd_rn(g[1], s);
+#pragma unroll
+        for (int k = 0; k < 30; ++k) {                         // IMAD.WIDE.U32 (Philox products)
+            const uint64_t p = (uint64_t)u[k & 7] * m;
+            u[k & 7] = (uint32_t)(p >> 32) ^ (uint32_t)p;      // + one LOP3 each (counted below)
+        }
+#pragma unroll
+        for (int k = 0; k < 34; ++k) u[k & 7] = (u[k & 7] ^ m) ^ u[(k + 3) & 7];   // LOP3 (64 total with the above)
+#pragma unroll
+        for (int k = 0; k < 24; ++k) u[k & 7] = __funnelshift_r(u[k & 7], u[(k + 1) & 7], 8);   // SHF
+#pragma unroll
+        for (int k = 0; k < 24; ++k) u[k & 7] = u[k & 7] + u[(k + 5) & 7] + 0x1234u;            // IADD3
+#pragma unroll
+        for (int k = 0; k < 6; ++k) u[k & 7] = __byte_perm(u[k & 7], u[(k + 2) & 7], 0x3320u);   // PRMT
+#pragma unroll
+        for (int k = 0; k < 12; ++k) g[2 + (k & 1)] = __fadd_rn(g[2 + (k & 1)], __uint2float_rn(u[k & 7]));  // I2FP (+FADD)
+    }
+    float t = g[0] + g[1] + g[2] + g[3];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += f[j].x + f[j].y + (float)u[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t += fm[j].x + fm[j].y + fa[j].x + fa[j].y;
+    if (t == 1234.5f) out[threadIdx.x] = t;
+}
+
+int main() {
+    float* out; cudaMalloc(&out, 1 << 20);
+    int n_sm, clk; cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    const int blocks = n_sm * 7, threads = 128;
+    k_mix<<<blocks, threads>>>(out, 1.0001f, 0xD2511F53u);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        k_mix<<<blocks, threads>>>(out, 1.0001f, 0xD2511F53u);
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    const double warp_iters_per_smsp = (double)blocks * threads / 32 * N_ITER / (n_sm * 4);
+    const double cycles = best * 1e-3 * clk * 1e3;
+    printf("mix probe: %.4f ms, %.1f SMSP-cycles per iteration (kernel: ~537 per pair-iteration at 1965 MHz)\n",
+           best, cycles / warp_iters_per_smsp);
+    printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
