@@ -201,3 +201,20 @@ def test_golden_ddm_and_stroop(orc):
         i = int(i)
         assert [int(counts[i, 0]), int(counts[i, 1]), int(counts[i, 2])] == [int(nc), int(nu), int(rs)]
         assert float(net[i]) == float.fromhex(v)
+
+
+def test_lci_with_leak_endpoint_is_the_ar1_law(orc):
+    """LCI with a leak is Euler-discretised Ornstein-Uhlenbeck:
+    x_{n+1} = (1 - lam dt) x_n + I dt + sigma sqrt(dt) g — an AR(1) whose
+    endpoint from x_0 = 0 is exactly Gaussian with
+        mean = I dt (1 - r^N) / (1 - r),  var = sigma^2 dt (1 - r^{2N}) / (1 - r^2),  r = 1 - lam dt.
+    KS test of 4000 endpoints; a leak applied with the wrong sign is rejected."""
+    I, lam, sig, dt, N = 0.8, 2.0, 0.7, 0.01, 300
+    xs = np.array([orc.lci_trial(I, lam, 0.0, sig, dt, 1e9, N, 17, u)[2] for u in range(4000)], np.float64)
+    r = 1 - lam * dt
+    mean = I * dt * (1 - r ** N) / (1 - r)
+    sd = math.sqrt(sig ** 2 * dt * (1 - r ** (2 * N)) / (1 - r ** 2))
+    assert stats.kstest((xs - mean) / sd, "norm").pvalue > 1e-3
+    r_bad = 1 + lam * dt
+    mean_bad = I * dt * (1 - r_bad ** N) / (1 - r_bad)
+    assert abs(xs.mean() - mean_bad) > 50 * xs.std() / math.sqrt(len(xs))
