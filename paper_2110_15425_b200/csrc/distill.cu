@@ -185,8 +185,9 @@ static bool pp_small(const distill_model* m, uint64_t count, uint32_t n_samples)
 }
 
 static void launch_pp_small(const PPArgs& p, uint64_t count, cudaStream_t st) {
-    pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX>
-        <<<(unsigned)((count + PP_SMALL_WARPS - 1) / PP_SMALL_WARPS), PP_SMALL_WARPS * 32, 0, st>>>(p);
+    const unsigned grid = (unsigned)((count + PP_SMALL_WARPS - 1) / PP_SMALL_WARPS);
+    if (p.publish) pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX, true><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
+    else pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
 }
 
 static distill_status launch_pp(const distill_model* m, const distill_eval_args* a, cudaStream_t st,
@@ -213,7 +214,7 @@ static distill_status launch_pp(const distill_model* m, const distill_eval_args*
     p.publish = publish; p.done = done;
     const unsigned grid = (unsigned)((count + PP_BLOCK - 1) / PP_BLOCK);
     const bool even = (a->n_samples & 1u) == 0;
-    if (!publish && pp_small(m, count, a->n_samples)) {
+    if (pp_small(m, count, a->n_samples)) {
         launch_pp_small(p, count, st);
     } else if (publish) {
         if (even)

@@ -200,13 +200,31 @@ __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, floa
     return __fadd_rn(__fdiv_rn(acc, __uint2float_rn(a.n_samples)), K);
 }
 
+// End-to-end call (distill_eval_grid_host), called by thread 0 of every block
+// after its atomicMin: the last block to finish publishes the combined key
+// straight into pinned host memory and re-arms the device key and counter for
+// the next call, so the call is one launch with no memset and no copy.  The
+// fence orders this block's atomicMin before its counter increment
+// (threadFenceReduction pattern).
+__device__ __forceinline__ void pp_publish_key(const PPArgs& a) {
+    __threadfence();
+    if (atomicAdd(a.done, 1u) == gridDim.x * gridDim.y - 1) {
+        __threadfence();
+        const key64_t k = atomicOr(a.best, 0ull);           // coherent read of the final key
+        *reinterpret_cast<volatile key64_t*>(a.publish) = k;
+        __threadfence_system();
+        *a.best = KEY_INIT;
+        *a.done = 0u;
+    }
+}
+
 // Small grids (latency mode): one warp per allocation.  Lane l evaluates the
 // sample pairs (2l + 64m, 2l + 1 + 64m); the squared chords go to shared
 // memory and lane 0 adds them in ascending sample order, so C is the same sum
 // as in the one-thread-per-allocation kernel, bit for bit.  Used when the grid
 // is too small to fill the GPU one thread per allocation (a few thousand
 // allocations or fewer) and n_samples <= SMAX.
-template <int WARPS, int SMAX>
+template <int WARPS, int SMAX, bool PUB = false>
 __global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs a0) {
     __shared__ float s_e[WARPS][SMAX];
     if (a0.status_dev && *a0.status_dev != 0) return;   // episode already over (uniform branch)
@@ -248,6 +266,7 @@ __global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs 
         }
     }
     if (a.best) block_min_key_atomic<WARPS * 32>(key, a.best);
+    if (PUB && threadIdx.x == 0) pp_publish_key(a0);
 }
 
 // One thread per allocation; one atomicMin per block.
@@ -277,23 +296,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs 
     if (a0.net && tid < a0.count) a0.net[row * a0.count + tid] = -C;
     // a9: (value, index) argmin -> one atomic per block
     if (a0.best) block_min_key_atomic<BLOCK>(key, a0.best + row);
-    if (PUB && threadIdx.x == 0) {
-        // End-to-end call (distill_eval_grid_host): the last block to finish
-        // publishes the combined key straight into pinned host memory and
-        // re-arms the device key and counter for the next call, so the call is
-        // one launch with no memset and no copy.  Thread 0 issued this block's
-        // atomicMin; the fence orders it before the counter increment
-        // (threadFenceReduction pattern).
-        __threadfence();
-        if (atomicAdd(a0.done, 1u) == gridDim.x * gridDim.y - 1) {
-            __threadfence();
-            const key64_t k = atomicOr(a0.best, 0ull);      // coherent read of the final key
-            *reinterpret_cast<volatile key64_t*>(a0.publish) = k;
-            __threadfence_system();
-            *a0.best = KEY_INIT;
-            *a0.done = 0u;
-        }
-    }
+    if (PUB && threadIdx.x == 0) pp_publish_key(a0);
 }
 
 
