@@ -153,18 +153,24 @@ def eval_grid_host(model: Model, inputs, n_samples: int, seed: int, begin: int =
     end = model.n_alloc if end is None else int(end)
     inp = np.ascontiguousarray(np.asarray(inputs, np.float32))
     if getattr(model, "_h_key", None) is None:      # pinned: the kernel publishes the key into it
+        import threading
         import torch
         model._h_key = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        model._h_key_lock = threading.Lock()
     key_ptr = model._h_key.data_ptr()
     net_ptr = None
     if net_out is not None:
         if net_out.dtype != np.float32 or not net_out.flags.c_contiguous or net_out.size < end - begin:
             raise ValueError("net_out must be a contiguous float32 array of end-begin elements")
         net_ptr = net_out.ctypes.data
-    check(lib().distill_eval_grid_host(model.handle, _abi._fptr(inp), inp.size, int(begin), end, int(n_samples),
-                                       int(invocation), int(seed) & (2 ** 64 - 1), net_ptr,
-                                       C.cast(key_ptr, C.POINTER(C.c_uint64)), _stream_handle(stream)))
-    return int(model._h_key[0]) & (2 ** 64 - 1)
+    # The pinned key slot is per model: hold it from the call until the key is read,
+    # so a concurrent call on another thread cannot publish over it in between
+    # (the library itself serialises host-buffer calls per handle).
+    with model._h_key_lock:
+        check(lib().distill_eval_grid_host(model.handle, _abi._fptr(inp), inp.size, int(begin), end,
+                                           int(n_samples), int(invocation), int(seed) & (2 ** 64 - 1), net_ptr,
+                                           C.cast(key_ptr, C.POINTER(C.c_uint64)), _stream_handle(stream)))
+        return int(model._h_key[0]) & (2 ** 64 - 1)
 
 
 def argmax(values, index_base: int, best, stream=None) -> None:

@@ -818,3 +818,45 @@ def test_grid_search_and_best_convenience(D, orc):
     net, key = D.grid_search(m, cfg.inputs, 12, cfg.seed)
     cost, idx = D.best(key)
     assert idx == k_or & 0xFFFFFFFF and np.float32(cost) == want[idx]
+
+
+def test_concurrent_streams_and_threads_on_one_model(D, orc):
+    """One read-only model handle evaluated from two streams at once (device
+    buffers) and from two host threads through the serialised host-buffer call:
+    every result equals its sequential counterpart."""
+    import threading
+    import torch
+    cfg = W.PPConfig("conc", (40, 30, 20), 12)
+    m = _model(D, cfg)
+    seeds = (5, 6)
+    ref = {}
+    for sd in seeds:
+        ref[sd] = _gpu_pp(D, m, cfg, seed=sd)
+    streams = [torch.cuda.Stream() for _ in seeds]
+    nets = [torch.empty(cfg.n_alloc, dtype=torch.float32, device="cuda") for _ in seeds]
+    bests = [torch.full((1,), -1, dtype=torch.int64, device="cuda") for _ in seeds]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for st, sd, net, best in zip(streams, seeds, nets, bests):
+            with torch.cuda.stream(st):
+                D.key_reset(best, stream=st)
+                D.eval_grid(m, cfg.inputs, cfg.n_samples, sd, net=net, best=best, stream=st)
+        torch.cuda.synchronize()
+        for sd, net, best in zip(seeds, nets, bests):
+            assert np.array_equal(_bits(-net.cpu().numpy()), _bits(ref[sd][0]))
+            assert int(best.item()) & (2 ** 64 - 1) == ref[sd][1]
+    out = {}
+
+    def worker(sd):
+        k = None
+        for _ in range(5):
+            k = D.eval_grid_host(m, cfg.inputs, cfg.n_samples, sd)
+        out[sd] = k
+
+    th = [threading.Thread(target=worker, args=(sd,)) for sd in seeds]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for sd in seeds:
+        assert out[sd] == ref[sd][1]
