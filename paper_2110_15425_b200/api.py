@@ -14,6 +14,10 @@ import numpy as np
 from . import _abi
 from ._abi import KEY_INIT, DistillError, check, lib
 
+import threading as _threading
+
+_INIT_LOCK = _threading.Lock()
+
 
 def _stream_handle(stream) -> Optional[int]:
     import torch
@@ -153,10 +157,12 @@ def eval_grid_host(model: Model, inputs, n_samples: int, seed: int, begin: int =
     end = model.n_alloc if end is None else int(end)
     inp = np.ascontiguousarray(np.asarray(inputs, np.float32))
     if getattr(model, "_h_key", None) is None:      # pinned: the kernel publishes the key into it
-        import threading
-        import torch
-        model._h_key = torch.empty(1, dtype=torch.int64, pin_memory=True)
-        model._h_key_lock = threading.Lock()
+        with _INIT_LOCK:
+            if getattr(model, "_h_key", None) is None:
+                import threading
+                import torch
+                model._h_key_lock = threading.Lock()
+                model._h_key = torch.empty(1, dtype=torch.int64, pin_memory=True)
     key_ptr = model._h_key.data_ptr()
     net_ptr = None
     if net_out is not None:
