@@ -53,6 +53,10 @@ constexpr uint32_t MAX_SAMPLES = 1u << 31;
 #ifndef DISTILL_PP_SMALL_MODE
 #define DISTILL_PP_SMALL_MODE 1   // 0: always one thread per allocation (A/B measurements only)
 #endif
+#ifndef DISTILL_PP_SMALL_THREADS_PER_SM
+#define DISTILL_PP_SMALL_THREADS_PER_SM 2048
+#endif
+constexpr uint64_t PP_SMALL_THREADS_PER_SM = DISTILL_PP_SMALL_THREADS_PER_SM;   // latency-mode threshold
 constexpr int PP_SMALL_WARPS = 4;    // pp_eval_small_kernel: allocations per block
 constexpr uint32_t PP_SMALL_SMAX = 1024;   // its per-warp sample buffer
 constexpr int DDM_BLOCK = 128;
@@ -181,7 +185,7 @@ distill_status distill_grid_size(const distill_model* m, uint64_t* n_alloc) {
 // Latency mode (pp_eval_small_kernel, one warp per allocation) for grids that
 // cannot fill the GPU one thread per allocation.
 static bool pp_small(const distill_model* m, uint64_t count, uint32_t n_samples) {
-    return DISTILL_PP_SMALL_MODE && n_samples <= PP_SMALL_SMAX && count * 32 <= (uint64_t)m->n_sm * 2048;
+    return DISTILL_PP_SMALL_MODE && n_samples <= PP_SMALL_SMAX && count * 32 <= (uint64_t)m->n_sm * PP_SMALL_THREADS_PER_SM;
 }
 
 static void launch_pp_small(const PPArgs& p, uint64_t count, cudaStream_t st) {
