@@ -17,7 +17,10 @@
 // independent Philox chains (integer ILP).  Philox rounds 1-3 are partly
 // sample-invariant (counter = (i, s, t, 1)) and are hoisted per thread.
 // State is registers only (the paper's 7.5 kB MT19937 state per thread,
-// P:632, becomes 6 words of Philox counter/key).
+// P:632, becomes 6 words of Philox counter/key).  Grids too small to fill the
+// GPU one thread per allocation use pp_eval_small_kernel (one warp per
+// allocation, same per-pair code, same ordered sum).  Also here: the
+// closed-loop episode step (NEXT-1) and the AMR level/refine kernels (NEXT-4).
 #pragma once
 #include "keys.cuh"
 #include "rng.cuh"
