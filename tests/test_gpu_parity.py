@@ -860,3 +860,61 @@ def test_concurrent_streams_and_threads_on_one_model(D, orc):
         t.join()
     for sd in seeds:
         assert out[sd] == ref[sd][1]
+
+
+def test_randomised_parity_fuzz(D, orc):
+    """Deterministic fuzz: 60 random PP configurations (shapes, sample counts
+    odd/even, params, positions, seeds, shards, both the warp-per-allocation and
+    the thread-per-allocation kernels) and 12 random DDM / Stroop configurations,
+    each bit-exact against the oracle."""
+    import os
+    import torch
+    rng = np.random.default_rng(int(os.environ.get("DISTILL_FUZZ_SEED", "2024")))
+    for case in range(int(os.environ.get("DISTILL_FUZZ_CASES", "60"))):
+        shape = tuple(int(x) for x in rng.integers(1, 9, 3))
+        if case % 6 == 0:
+            shape = (int(rng.integers(20, 40)),) * 3         # > 9472 allocations: thread-per-allocation kernel
+        S = int(rng.integers(1, 40))
+        cfg = W.PPConfig("fz", shape, S)
+        cfg.params = np.array([rng.uniform(0, 3), rng.uniform(0, 0.5), rng.uniform(0, 2)], np.float32)
+        cfg.w = rng.uniform(-0.2, 0.3, 3).astype(np.float32)
+        cfg.levels = rng.uniform(0, 1, sum(shape)).astype(np.float32)
+        cfg.inputs = rng.uniform(-8, 8, 6).astype(np.float32)
+        seed = int(rng.integers(0, 2 ** 63))
+        inv = int(rng.integers(0, 1000))
+        m = _model(D, cfg)
+        b = int(rng.integers(0, cfg.n_alloc))
+        e = int(rng.integers(b + 1, cfg.n_alloc + 1))
+        C, key = _gpu_pp(D, m, cfg, b, e, invocation=inv, seed=seed)
+        want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, b, e, S, seed, invocation=inv)
+        assert np.array_equal(_bits(C), _bits(want)), (case, shape, S, b, e)
+        assert key == orc.argmax_net(-want, b)[0], case
+        m.close()
+    for case in range(6):
+        d = W.DDMConfig(drift=float(rng.uniform(-2, 2)), noise=float(rng.uniform(0.2, 2)),
+                        threshold=float(rng.uniform(0.2, 2)), x0=float(rng.uniform(-0.1, 0.1)),
+                        dt=float(rng.choice([0.001, 0.005, 0.01])), n_steps=int(rng.integers(1, 400)),
+                        rt_bin_steps=int(rng.integers(1, 30)), n_x_bins=int(rng.integers(1, 60)))
+        t0 = int(rng.integers(0, 10 ** 6))
+        t1 = t0 + int(rng.integers(1, 900))
+        sd = int(rng.integers(0, 2 ** 63))
+        for g, w in zip(_ddm_gpu(D, d, t0, t1, sd), orc.ddm_batch(_ddm_p(orc, d), sd, t0, t1)):
+            assert np.array_equal(g, w), case
+    for case in range(6):
+        P = W.STROOP_PARAMS.copy()
+        P[:8] = [rng.uniform(0.5, 2), rng.uniform(0.5, 2), rng.uniform(0.02, 1), rng.uniform(0, 0.5),
+                 rng.uniform(0, 0.5), rng.uniform(0.05, 1), rng.choice([0.01, 0.05]), rng.uniform(0.3, 1.5)]
+        P[10] = int(rng.integers(1, 120))
+        Ls = (int(rng.integers(1, 6)), int(rng.integers(1, 6)))
+        lev = rng.uniform(0, 1, sum(Ls)).astype(np.float32)
+        ms = D.load_model(W.KIND_STROOP_LCA, Ls, lev, W.STROOP_W, P, device=0)
+        n = Ls[0] * Ls[1]
+        T = int(rng.integers(1, 200))
+        sd = int(rng.integers(0, 2 ** 63))
+        counts = torch.zeros(3 * n, dtype=torch.int64, device="cuda")
+        net = torch.empty(n, dtype=torch.float32, device="cuda")
+        D.eval_grid(ms, None, T, sd, 0, n, net=net, counts=counts)
+        torch.cuda.synchronize()
+        wc, wn = orc.stroop_eval(Ls, lev, W.STROOP_W, P, 0, n, T, sd)
+        assert np.array_equal(counts.cpu().numpy().astype(np.uint64).reshape(n, 3), wc), case
+        assert np.array_equal(_bits(net.cpu().numpy()), _bits(wn)), case
