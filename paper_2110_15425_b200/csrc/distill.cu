@@ -54,11 +54,16 @@ constexpr uint32_t MAX_SAMPLES = 1u << 31;
 #define DISTILL_PP_SMALL_MODE 1   // 0: always one thread per allocation (A/B measurements only)
 #endif
 #ifndef DISTILL_PP_SMALL_THREADS_PER_SM
-#define DISTILL_PP_SMALL_THREADS_PER_SM 2048
+#define DISTILL_PP_SMALL_THREADS_PER_SM 512    // 32 lanes per allocation up to 16 allocations per SM
 #endif
 constexpr uint64_t PP_SMALL_THREADS_PER_SM = DISTILL_PP_SMALL_THREADS_PER_SM;   // latency-mode threshold
 constexpr int PP_SMALL_WARPS = 4;    // pp_eval_small_kernel: allocations per block
-constexpr uint32_t PP_SMALL_SMAX = 1024;   // its per-warp sample buffer
+constexpr uint32_t PP_SMALL_SMAX = 1024;   // its per-warp sample buffer (32 lanes per allocation)
+constexpr uint32_t PP_SMALL_SMAX8 = 256;   // per-allocation buffer with 8 lanes per allocation
+#ifndef DISTILL_PP_SMALL8_THREADS_PER_SM
+#define DISTILL_PP_SMALL8_THREADS_PER_SM 768   // 8 lanes per allocation up to 96 allocations per SM
+#endif
+constexpr uint64_t PP_SMALL8_THREADS_PER_SM = DISTILL_PP_SMALL8_THREADS_PER_SM;
 constexpr int DDM_BLOCK = 128;
 constexpr int DDM_MINB = 6;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt, v5)
 constexpr int STROOP_BLOCK = 128;
@@ -184,14 +189,31 @@ distill_status distill_grid_size(const distill_model* m, uint64_t* n_alloc) {
 
 // Latency mode (pp_eval_small_kernel, one warp per allocation) for grids that
 // cannot fill the GPU one thread per allocation.
+// 0: one thread per allocation; otherwise the lanes per allocation of the
+// latency-mode kernel (32 for the smallest grids, 8 for mid-size ones).
+static int pp_small_lanes(const distill_model* m, uint64_t count, uint32_t n_samples) {
+    // measured switch points (tools/small_threshold.py, profiles/r01_small_threshold.txt)
+    if (!DISTILL_PP_SMALL_MODE) return 0;
+    const uint64_t sms = (uint64_t)m->n_sm;
+    if (n_samples <= PP_SMALL_SMAX8 && count * 8 <= sms * PP_SMALL8_THREADS_PER_SM)
+        return count * 32 <= sms * PP_SMALL_THREADS_PER_SM ? 32 : 8;
+    if (n_samples <= PP_SMALL_SMAX && count <= sms * 64) return 32;   // long sample loops: the warp kernel wins longer
+    return 0;
+}
 static bool pp_small(const distill_model* m, uint64_t count, uint32_t n_samples) {
-    return DISTILL_PP_SMALL_MODE && n_samples <= PP_SMALL_SMAX && count * 32 <= (uint64_t)m->n_sm * PP_SMALL_THREADS_PER_SM;
+    return pp_small_lanes(m, count, n_samples) != 0;
 }
 
-static void launch_pp_small(const PPArgs& p, uint64_t count, cudaStream_t st) {
-    const unsigned grid = (unsigned)((count + PP_SMALL_WARPS - 1) / PP_SMALL_WARPS);
-    if (p.publish) pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX, true><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
-    else pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
+static void launch_pp_small(const distill_model* m, const PPArgs& p, uint64_t count, cudaStream_t st) {
+    if (pp_small_lanes(m, count, p.n_samples) == 32) {
+        const unsigned grid = (unsigned)((count + PP_SMALL_WARPS - 1) / PP_SMALL_WARPS);
+        if (p.publish) pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX, 32, true><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
+        else pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX, 32><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
+    } else {
+        const unsigned grid = (unsigned)((count + PP_SMALL_WARPS * 4 - 1) / (PP_SMALL_WARPS * 4));
+        if (p.publish) pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX8, 8, true><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
+        else pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX8, 8><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
+    }
 }
 
 static distill_status launch_pp(const distill_model* m, const distill_eval_args* a, cudaStream_t st,
@@ -219,7 +241,7 @@ static distill_status launch_pp(const distill_model* m, const distill_eval_args*
     const unsigned grid = (unsigned)((count + PP_BLOCK - 1) / PP_BLOCK);
     const bool even = (a->n_samples & 1u) == 0;
     if (pp_small(m, count, a->n_samples)) {
-        launch_pp_small(p, count, st);
+        launch_pp_small(m, p, count, st);
     } else if (publish) {
         if (even)
             pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
@@ -503,7 +525,7 @@ static void episode_search(const distill_model* m, const distill_episode_args* e
     p.best = e->d_keys + t;
     p.begin = (uint32_t)begin; p.count = (uint32_t)(end - begin);
     const unsigned grid = (unsigned)((end - begin + PP_BLOCK - 1) / PP_BLOCK);
-    if (pp_small(m, end - begin, e->n_samples)) launch_pp_small(p, end - begin, st);
+    if (pp_small(m, end - begin, e->n_samples)) launch_pp_small(m, p, end - begin, st);
     else if ((e->n_samples & 1u) == 0) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
     else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
     g_launches++;
@@ -610,7 +632,7 @@ static void amr_search(const distill_model* m, const distill_amr_args* g, PPArgs
     p.best = g->d_keys + r;
     p.begin = (uint32_t)begin; p.count = (uint32_t)(end - begin);
     const unsigned grid = (unsigned)((end - begin + PP_BLOCK - 1) / PP_BLOCK);
-    if (pp_small(m, end - begin, g->n_samples)) launch_pp_small(p, end - begin, st);
+    if (pp_small(m, end - begin, g->n_samples)) launch_pp_small(m, p, end - begin, st);
     else if ((g->n_samples & 1u) == 0) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
     else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
     g_launches++;

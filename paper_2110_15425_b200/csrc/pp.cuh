@@ -221,52 +221,55 @@ __device__ __forceinline__ void pp_publish_key(const PPArgs& a) {
     }
 }
 
-// Small grids (latency mode): one warp per allocation.  Lane l evaluates the
-// sample pairs (2l + 64m, 2l + 1 + 64m); the squared chords go to shared
-// memory and lane 0 adds them in ascending sample order, so C is the same sum
-// as in the one-thread-per-allocation kernel, bit for bit.  Used when the grid
-// is too small to fill the GPU one thread per allocation (a few thousand
-// allocations or fewer) and n_samples <= SMAX.
-template <int WARPS, int SMAX, bool PUB = false>
+// Small grids (latency mode): LANES lanes per allocation (32: one warp; 8:
+// four allocations per warp).  Sub-lane l evaluates the sample pairs
+// (2l + 2·LANES·m, 2l + 1 + 2·LANES·m); the squared chords go to shared memory
+// and sub-lane 0 adds them in ascending sample order, so C is the same sum as
+// in the one-thread-per-allocation kernel, bit for bit.  Used when the grid is
+// too small to fill the GPU one thread per allocation and n_samples <= SMAX.
+template <int WARPS, int SMAX, int LANES = 32, bool PUB = false>
 __global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs a0) {
-    __shared__ float s_e[WARPS][SMAX];
+    constexpr int GPW = 32 / LANES;                          // allocations per warp
+    __shared__ float s_e[WARPS][GPW][SMAX];
     if (a0.status_dev && *a0.status_dev != 0) return;   // episode already over (uniform branch)
     const PPArgs a = pp_resolve_positions(a0);
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tid = blockIdx.x * WARPS + w;            // allocation within the launch (warp-uniform)
+    const uint32_t grp = lane / LANES, sl = lane % LANES;
+    const uint32_t tid = (blockIdx.x * WARPS + w) * GPW + grp;   // allocation within the launch
     const float2 ustar = pp_ustar_block(a);
-    key64_t key = KEY_INIT;
-    if (tid < a.count) {
-        const uint32_t i = a.begin + tid;
-        const uint32_t k2 = i % a.L2, r = i / a.L2;
-        const uint32_t k1 = r % a.L1, k0 = r / a.L1;
-        const float a0 = __ldg(a.levels + k0);
-        const float a1 = __ldg(a.levels + a.L0 + k1);
-        const float a2 = __ldg(a.levels + a.L0 + a.L1 + k2);
-        const float dsig = __fadd_rn(a.sigma_min, -a.sigma_max);
-        const float s0 = __fmaf_rn(a0, dsig, a.sigma_max);
-        const float s1 = __fmaf_rn(a1, dsig, a.sigma_max);
-        const float s2 = __fmaf_rn(a2, dsig, a.sigma_max);
-        const float K = __fmaf_rn(a.w2, a2, __fmaf_rn(a.w1, a1, __fmul_rn(a.w0, a0)));
+    const bool valid = tid < a.count;
+    const uint32_t i = a.begin + (valid ? tid : 0u);
+    const uint32_t k2 = i % a.L2, r = i / a.L2;
+    const uint32_t k1 = r % a.L1, k0 = r / a.L1;
+    const float lv0 = __ldg(a.levels + k0);
+    const float lv1 = __ldg(a.levels + a.L0 + k1);
+    const float lv2 = __ldg(a.levels + a.L0 + a.L1 + k2);
+    const float dsig = __fadd_rn(a.sigma_min, -a.sigma_max);
+    const float s0 = __fmaf_rn(lv0, dsig, a.sigma_max);
+    const float s1 = __fmaf_rn(lv1, dsig, a.sigma_max);
+    const float s2 = __fmaf_rn(lv2, dsig, a.sigma_max);
+    const float K = __fmaf_rn(a.w2, lv2, __fmaf_rn(a.w1, lv1, __fmul_rn(a.w0, lv0)));
+    if (valid) {
         const V2 P0 = {bc(a.prey_x), bc(a.prey_y)}, P1 = {bc(a.pred_x), bc(a.pred_y)};
         const V2 P2 = {bc(a.pl_x), bc(a.pl_y)};
         const V2 us = {bc(ustar.x), bc(ustar.y)};
         PhiloxHoisted rng;
         rng.init(i, a.invocation, 1u, a.key0, a.key1);
-        for (uint32_t s = 2 * lane; s < a.n_samples; s += 64) {
+        for (uint32_t s = 2 * sl; s < a.n_samples; s += 2 * LANES) {
             const F2 e = pp_pair_errors<false, false, false, false>(rng(s), rng(s + 1), s0, s1, s2, P0, P1, P2,
                                                                     bc(-a.kappa), us);
-            s_e[w][s] = e.x;
-            if (s + 1 < a.n_samples) s_e[w][s + 1] = e.y;
+            s_e[w][grp][s] = e.x;
+            if (s + 1 < a.n_samples) s_e[w][grp][s + 1] = e.y;
         }
-        __syncwarp();
-        if (lane == 0) {
-            float acc = 0.0f;                                   // a7: ascending sample order
-            for (uint32_t s = 0; s < a.n_samples; ++s) acc = __fadd_rn(acc, s_e[w][s]);
-            const float C = __fadd_rn(__fdiv_rn(acc, __uint2float_rn(a.n_samples)), K);
-            if (a.net) a.net[tid] = -C;
-            key = make_key(C, i);
-        }
+    }
+    __syncwarp();
+    key64_t key = KEY_INIT;
+    if (valid && sl == 0) {
+        float acc = 0.0f;                                        // a7: ascending sample order
+        for (uint32_t s = 0; s < a.n_samples; ++s) acc = __fadd_rn(acc, s_e[w][grp][s]);
+        const float C = __fadd_rn(__fdiv_rn(acc, __uint2float_rn(a.n_samples)), K);
+        if (a.net) a.net[tid] = -C;
+        key = make_key(C, i);
     }
     if (a.best) block_min_key_atomic<WARPS * 32>(key, a.best);
     if (PUB && threadIdx.x == 0) pp_publish_key(a0);

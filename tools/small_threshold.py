@@ -14,7 +14,7 @@ import workloads as W  # noqa: E402
 
 def main():
     torch.cuda.set_device(0)
-    for L in (6, 16, 22, 26, 32, 40, 50, 64, 80, 100):
+    for L in (4, 6, 10, 13, 16, 18, 20, 22, 24, 26, 28, 32, 40, 50, 64, 100):
         c = W.PPConfig(f"L{L}", (L, L, L), 100)
         m = D.load_model(W.KIND_PREDATOR_PREY, c.n_levels, c.levels, c.w, c.params, device=0)
         net = torch.empty(c.n_alloc, device="cuda")
