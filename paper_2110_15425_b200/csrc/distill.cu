@@ -64,6 +64,11 @@ constexpr uint32_t PP_SMALL_SMAX8 = 256;   // per-allocation buffer with 8 lanes
 #define DISTILL_PP_SMALL8_THREADS_PER_SM 768   // 8 lanes per allocation up to 96 allocations per SM
 #endif
 constexpr uint64_t PP_SMALL8_THREADS_PER_SM = DISTILL_PP_SMALL8_THREADS_PER_SM;
+constexpr uint32_t PP_SMALL_SMAX4 = 128;   // per-allocation buffer with 4 lanes per allocation
+#ifndef DISTILL_PP_SMALL4_THREADS_PER_SM
+#define DISTILL_PP_SMALL4_THREADS_PER_SM 1024   // 4 lanes per allocation up to 256 allocations per SM
+#endif
+constexpr uint64_t PP_SMALL4_THREADS_PER_SM = DISTILL_PP_SMALL4_THREADS_PER_SM;
 constexpr int DDM_BLOCK = 128;
 constexpr int DDM_MINB = 6;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt, v5)
 constexpr int STROOP_BLOCK = 128;
@@ -197,6 +202,7 @@ static int pp_small_lanes(const distill_model* m, uint64_t count, uint32_t n_sam
     const uint64_t sms = (uint64_t)m->n_sm;
     if (n_samples <= PP_SMALL_SMAX8 && count * 8 <= sms * PP_SMALL8_THREADS_PER_SM)
         return count * 32 <= sms * PP_SMALL_THREADS_PER_SM ? 32 : 8;
+    if (n_samples <= PP_SMALL_SMAX4 && count * 4 <= sms * PP_SMALL4_THREADS_PER_SM) return 4;
     if (n_samples <= PP_SMALL_SMAX && count <= sms * 64) return 32;   // long sample loops: the warp kernel wins longer
     return 0;
 }
@@ -209,10 +215,14 @@ static void launch_pp_small(const distill_model* m, const PPArgs& p, uint64_t co
         const unsigned grid = (unsigned)((count + PP_SMALL_WARPS - 1) / PP_SMALL_WARPS);
         if (p.publish) pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX, 32, true><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
         else pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX, 32><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
-    } else {
+    } else if (pp_small_lanes(m, count, p.n_samples) == 8) {
         const unsigned grid = (unsigned)((count + PP_SMALL_WARPS * 4 - 1) / (PP_SMALL_WARPS * 4));
         if (p.publish) pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX8, 8, true><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
         else pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX8, 8><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
+    } else {
+        const unsigned grid = (unsigned)((count + PP_SMALL_WARPS * 8 - 1) / (PP_SMALL_WARPS * 8));
+        if (p.publish) pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX4, 4, true><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
+        else pp_eval_small_kernel<PP_SMALL_WARPS, PP_SMALL_SMAX4, 4><<<grid, PP_SMALL_WARPS * 32, 0, st>>>(p);
     }
 }
 
