@@ -16,6 +16,7 @@
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 
+template <int ALU_PCT>   // percentage of the loop's integer/logic instructions kept (100 = the kernel's mix)
 __global__ void __launch_bounds__(128, 7) k_mix(float* out, float s, uint32_t m) {
     float2 f[8], fm[4], fa[4];
     uint32_t u[8];
@@ -41,13 +42,13 @@ __global__ void __launch_bounds__(128, 7) k_mix(float* out, float s, uint32_t m)
             u[k & 7] = (uint32_t)(p >> 32) ^ (uint32_t)p;      // + one LOP3 each (counted below)
         }
 #pragma unroll
-        for (int k = 0; k < 34; ++k) u[k & 7] = (u[k & 7] ^ m) ^ u[(k + 3) & 7];   // LOP3 (64 total with the above)
+        for (int k = 0; k < 34 * ALU_PCT / 100; ++k) u[k & 7] = (u[k & 7] ^ m) ^ u[(k + 3) & 7];   // LOP3 (64 total with the above)
 #pragma unroll
-        for (int k = 0; k < 24; ++k) u[k & 7] = __funnelshift_r(u[k & 7], u[(k + 1) & 7], 8);   // SHF
+        for (int k = 0; k < 24 * ALU_PCT / 100; ++k) u[k & 7] = __funnelshift_r(u[k & 7], u[(k + 1) & 7], 8);   // SHF
 #pragma unroll
-        for (int k = 0; k < 24; ++k) u[k & 7] = u[k & 7] + u[(k + 5) & 7] + 0x1234u;            // IADD3
+        for (int k = 0; k < 24 * ALU_PCT / 100; ++k) u[k & 7] = u[k & 7] + u[(k + 5) & 7] + 0x1234u;            // IADD3
 #pragma unroll
-        for (int k = 0; k < 6; ++k) u[k & 7] = __byte_perm(u[k & 7], u[(k + 2) & 7], 0x3320u);   // PRMT
+        for (int k = 0; k < 6 * ALU_PCT / 100; ++k) u[k & 7] = __byte_perm(u[k & 7], u[(k + 2) & 7], 0x3320u);   // PRMT
 #pragma unroll
         for (int k = 0; k < 12; ++k) g[2 + (k & 1)] = __fadd_rn(g[2 + (k & 1)], __uint2float_rn(u[k & 7]));  // I2FP (+FADD)
     }
@@ -171,20 +172,24 @@ int main() {
     int n_sm, clk; cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     const int blocks = n_sm * 7, threads = 128;
-    k_mix<<<blocks, threads>>>(out, 1.0001f, 0xD2511F53u);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    float best = 1e30f;
-    for (int r = 0; r < 5; ++r) {
-        cudaEventRecord(e0);
-        k_mix<<<blocks, threads>>>(out, 1.0001f, 0xD2511F53u);
-        cudaEventRecord(e1); cudaEventSynchronize(e1);
-        float ms; cudaEventElapsedTime(&ms, e0, e1);
-        if (ms < best) best = ms;
-    }
-    const double warp_iters_per_smsp = (double)blocks * threads / 32 * N_ITER / (n_sm * 4);
-    const double cycles = best * 1e-3 * clk * 1e3;
-    printf("mix probe: %.4f ms, %.1f SMSP-cycles per iteration (kernel: ~537 per pair-iteration at 1965 MHz)\n",
-           best, cycles / warp_iters_per_smsp);
+    auto run_pp = [&](auto kern, const char* name) {
+        kern<<<blocks, threads>>>(out, 1.0001f, 0xD2511F53u);
+        float best = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+            cudaEventRecord(e0);
+            kern<<<blocks, threads>>>(out, 1.0001f, 0xD2511F53u);
+            cudaEventRecord(e1); cudaEventSynchronize(e1);
+            float ms; cudaEventElapsedTime(&ms, e0, e1);
+            if (ms < best) best = ms;
+        }
+        const double warp_iters_per_smsp = (double)blocks * threads / 32 * N_ITER / (n_sm * 4);
+        printf("%s: %.4f ms, %.1f SMSP-cycles per iteration (kernel: ~537 per pair-iteration at 1965 MHz)\n",
+               name, best, best * 1e-3 * clk * 1e3 / warp_iters_per_smsp);
+    };
+    run_pp(k_mix<100>, "mix probe (the kernel's mix)");
+    run_pp(k_mix<50>, "mix probe, half the extra integer ops");
+    run_pp(k_mix<0>, "mix probe, no extra integer ops");
     {
         const int b2 = n_sm * 6;
         k_mix_ddm<<<b2, threads>>>(out, 1.0001f, 0xD2511F53u);
