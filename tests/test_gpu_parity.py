@@ -918,3 +918,42 @@ def test_randomised_parity_fuzz(D, orc):
         wc, wn = orc.stroop_eval(Ls, lev, W.STROOP_W, P, 0, n, T, sd)
         assert np.array_equal(counts.cpu().numpy().astype(np.uint64).reshape(n, 3), wc), case
         assert np.array_equal(_bits(net.cpu().numpy()), _bits(wn)), case
+
+
+@pytest.mark.slow
+def test_ddm_cfg2_full_size_bit_exact(D, orc):
+    """cfg2 in full (1e6 trials x 1000 steps, the bench launch configuration):
+    every histogram bin and both RT sums equal the oracle's (threads over the
+    host cores; ~30 s on the GPU box's CPU)."""
+    import os
+    d = W.ddm_cfg2()
+    got = _ddm_gpu(D, d, 0, d.n_trials, d.seed)
+    want = orc.ddm_batch(_ddm_p(orc, d), d.seed, 0, d.n_trials, threads=os.cpu_count() or 8)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+@pytest.mark.slow
+def test_ext_stroop_and_stroop_cfg4_shards_bit_exact(D, orc):
+    """Contiguous shards at the bench sizes with ALL trials: 2000 of the Extended
+    Stroop grid's 1e4 allocations x 1e4 trials, and 200 of Stroop cfg4's 1e4
+    allocations x 1e5 trials x 200 steps — every count, V and the shard key
+    bit-exact (oracle threads over the host cores; ~40 s on the GPU box)."""
+    import os
+    th = os.cpu_count() or 8
+    g = W.ext_stroop_grid()
+    m = D.load_model(W.KIND_EXT_STROOP_A, g.n_levels, g.levels, g.w, g.params, device=0)
+    b, e = 3000, 5000
+    cnt, net, key = _stroop_gpu(D, m, g, b, e)
+    wc, wn = orc.ext_stroop_eval(0, g.n_levels, g.levels, g.w, g.params, b, e, g.n_trials, g.seed, threads=th)
+    assert np.array_equal(cnt, wc)
+    assert np.array_equal(_bits(net), _bits(wn))
+    assert key == orc.argmax_net(wn, b)[0]
+    c = W.stroop_cfg4()
+    ms = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=0)
+    b, e = 4000, 4200
+    cnt, net, key = _stroop_gpu(D, ms, c, b, e)
+    wc, wn = orc.stroop_eval(c.n_levels, c.levels, c.w, c.params, b, e, c.n_trials, c.seed, threads=th)
+    assert np.array_equal(cnt, wc)
+    assert np.array_equal(_bits(net), _bits(wn))
+    assert key == orc.argmax_net(wn, b)[0]
