@@ -194,6 +194,22 @@ distill_status distill_grid_size(const distill_model* m, uint64_t* n_alloc) {
 
 // Latency mode (pp_eval_small_kernel, one warp per allocation) for grids that
 // cannot fill the GPU one thread per allocation.
+// The model-derived part of a predator-prey launch (params, weights, levels,
+// key); callers fill positions, the range and the outputs.
+static PPArgs pp_base_args(const distill_model* m, uint32_t n_samples, uint64_t seed) {
+    PPArgs p;
+    memset(&p, 0, sizeof p);
+    p.sigma_max = m->params[0]; p.sigma_min = m->params[1]; p.kappa = m->params[2];
+    p.w0 = m->w[0]; p.w1 = m->w[1]; p.w2 = m->w[2];
+    p.L0 = m->L[0]; p.L1 = m->L[1]; p.L2 = m->L[2];
+    p.n_samples = n_samples;
+    p.key0 = (uint32_t)seed; p.key1 = (uint32_t)(seed >> 32);
+    p.begin = 0; p.count = (uint32_t)m->n_alloc;
+    p.levels = m->d_levels;
+    p.n_sets = 1;
+    return p;
+}
+
 // 0: one thread per allocation; otherwise the lanes per allocation of the
 // latency-mode kernel (32 for the smallest grids, 8 for mid-size ones).
 static int pp_small_lanes(const distill_model* m, uint64_t count, uint32_t n_samples) {
@@ -235,18 +251,13 @@ static distill_status launch_pp(const distill_model* m, const distill_eval_args*
         return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): trial range is a Stroop-only field");
     const uint64_t count = a->end - a->begin;
     if (count == 0) return DISTILL_OK;
-    PPArgs p;
+    PPArgs p = pp_base_args(m, a->n_samples, a->seed);
     p.prey_x = a->inputs[0]; p.prey_y = a->inputs[1];
     p.pred_x = a->inputs[2]; p.pred_y = a->inputs[3];
     p.pl_x = a->inputs[4]; p.pl_y = a->inputs[5];
-    p.sigma_max = m->params[0]; p.sigma_min = m->params[1]; p.kappa = m->params[2];
-    p.w0 = m->w[0]; p.w1 = m->w[1]; p.w2 = m->w[2];
-    p.L0 = m->L[0]; p.L1 = m->L[1]; p.L2 = m->L[2];
-    p.n_samples = a->n_samples; p.invocation = a->invocation;
-    p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
+    p.invocation = a->invocation;
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
-    p.levels = m->d_levels; p.net = a->d_net; p.best = a->d_best;
-    p.pos_dev = nullptr; p.status_dev = nullptr;
+    p.net = a->d_net; p.best = a->d_best;
     p.publish = publish; p.done = done;
     const unsigned grid = (unsigned)((count + PP_BLOCK - 1) / PP_BLOCK);
     const bool even = (a->n_samples & 1u) == 0;
@@ -281,16 +292,11 @@ distill_status distill_eval_grid_multi(const distill_model* m, const distill_mul
     const uint64_t count = a->end - a->begin;
     if (count == 0 || a->n_invocations == 0) return DISTILL_OK;
     CUDA_TRY(cudaSetDevice(m->device));
-    PPArgs p;
-    p.prey_x = p.prey_y = p.pred_x = p.pred_y = p.pl_x = p.pl_y = 0.0f;   // read from d_inputs
-    p.sigma_max = m->params[0]; p.sigma_min = m->params[1]; p.kappa = m->params[2];
-    p.w0 = m->w[0]; p.w1 = m->w[1]; p.w2 = m->w[2];
-    p.L0 = m->L[0]; p.L1 = m->L[1]; p.L2 = m->L[2];
-    p.n_samples = a->n_samples; p.invocation = a->invocation0;
-    p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
+    PPArgs p = pp_base_args(m, a->n_samples, a->seed);   // positions come from d_inputs
+    p.invocation = a->invocation0;
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
-    p.levels = m->d_levels; p.net = a->d_net; p.best = a->d_best;
-    p.pos_dev = a->d_inputs; p.status_dev = nullptr; p.n_sets = a->n_sets;
+    p.net = a->d_net; p.best = a->d_best;
+    p.pos_dev = a->d_inputs; p.n_sets = a->n_sets;
     const dim3 grid((unsigned)((count + PP_BLOCK - 1) / PP_BLOCK), a->n_invocations);
     cudaStream_t st = (cudaStream_t)stream;
     if ((a->n_samples & 1u) == 0)
@@ -514,17 +520,8 @@ static distill_status episode_check(const distill_model* m, const distill_episod
 }
 
 static PPArgs episode_pp_args(const distill_model* m, const distill_episode_args* e) {
-    PPArgs p;
-    memset(&p, 0, sizeof p);
-    p.sigma_max = m->params[0]; p.sigma_min = m->params[1]; p.kappa = m->params[2];
-    p.w0 = m->w[0]; p.w1 = m->w[1]; p.w2 = m->w[2];
-    p.L0 = m->L[0]; p.L1 = m->L[1]; p.L2 = m->L[2];
-    p.n_samples = e->n_samples;
-    p.key0 = (uint32_t)e->seed; p.key1 = (uint32_t)(e->seed >> 32);
-    p.begin = 0; p.count = (uint32_t)m->n_alloc;
-    p.levels = m->d_levels; p.net = nullptr;
+    PPArgs p = pp_base_args(m, e->n_samples, e->seed);
     p.status_dev = e->d_status;
-    p.n_sets = 1;
     return p;
 }
 
@@ -621,18 +618,10 @@ static AmrArgs amr_args(const distill_model* m, const distill_amr_args* g) {
 }
 
 static PPArgs amr_pp_args(const distill_model* m, const distill_amr_args* g) {
-    PPArgs p;
-    memset(&p, 0, sizeof p);
+    PPArgs p = pp_base_args(m, g->n_samples, g->seed);
     p.prey_x = g->inputs[0]; p.prey_y = g->inputs[1]; p.pred_x = g->inputs[2]; p.pred_y = g->inputs[3];
     p.pl_x = g->inputs[4]; p.pl_y = g->inputs[5];
-    p.sigma_max = m->params[0]; p.sigma_min = m->params[1]; p.kappa = m->params[2];
-    p.w0 = m->w[0]; p.w1 = m->w[1]; p.w2 = m->w[2];
-    p.L0 = m->L[0]; p.L1 = m->L[1]; p.L2 = m->L[2];
-    p.n_samples = g->n_samples;
-    p.key0 = (uint32_t)g->seed; p.key1 = (uint32_t)(g->seed >> 32);
-    p.begin = 0; p.count = (uint32_t)m->n_alloc;
-    p.levels = g->d_levels;
-    p.n_sets = 1;
+    p.levels = g->d_levels;                      // the round's level table, not the model's
     return p;
 }
 
