@@ -242,6 +242,33 @@ static void launch_pp_small(const distill_model* m, const PPArgs& p, uint64_t co
     }
 }
 
+// The grid-search launch every predator-prey path uses: the latency-mode
+// kernel for grids too small to fill the GPU, otherwise one thread per
+// allocation (sample pairs in float2 lanes when S is even); several
+// invocations go on gridDim.y (MULTI); PUB publishes the key to pinned host
+// memory from the last block.
+static void launch_pp_search(const distill_model* m, const PPArgs& p, uint32_t n_invocations, cudaStream_t st) {
+    const uint64_t count = p.count;
+    if (n_invocations == 1 && pp_small(m, count, p.n_samples)) {
+        launch_pp_small(m, p, count, st);
+    } else {
+        const dim3 grid((unsigned)((count + PP_BLOCK - 1) / PP_BLOCK), n_invocations);
+        const bool even = (p.n_samples & 1u) == 0;
+        constexpr int B = PP_BLOCK, MK = DISTILL_PP_MASK, MB = DISTILL_PP_MINB;
+        if (n_invocations > 1) {
+            if (even) pp_eval_grid_kernel<B, MK, MB, false, true, true><<<grid, B, 0, st>>>(p);
+            else pp_eval_grid_kernel<B, MK, MB, false, false, true><<<grid, B, 0, st>>>(p);
+        } else if (p.publish) {
+            if (even) pp_eval_grid_kernel<B, MK, MB, false, true, false, true><<<grid, B, 0, st>>>(p);
+            else pp_eval_grid_kernel<B, MK, MB, false, false, false, true><<<grid, B, 0, st>>>(p);
+        } else {
+            if (even) pp_eval_grid_kernel<B, MK, MB, false, true><<<grid, B, 0, st>>>(p);
+            else pp_eval_grid_kernel<B, MK, MB><<<grid, B, 0, st>>>(p);
+        }
+    }
+    g_launches++;
+}
+
 static distill_status launch_pp(const distill_model* m, const distill_eval_args* a, cudaStream_t st,
                                 key64_t* publish = nullptr, unsigned int* done = nullptr) {
     if (!a->inputs || a->n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "eval_grid(PP): needs 6 host inputs");
@@ -259,21 +286,7 @@ static distill_status launch_pp(const distill_model* m, const distill_eval_args*
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
     p.net = a->d_net; p.best = a->d_best;
     p.publish = publish; p.done = done;
-    const unsigned grid = (unsigned)((count + PP_BLOCK - 1) / PP_BLOCK);
-    const bool even = (a->n_samples & 1u) == 0;
-    if (pp_small(m, count, a->n_samples)) {
-        launch_pp_small(m, p, count, st);
-    } else if (publish) {
-        if (even)
-            pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
-        else
-            pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, false, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
-    } else if (even) {
-        pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
-    } else {
-        pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
-    }
-    g_launches++;
+    launch_pp_search(m, p, 1, st);
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;
 }
@@ -297,13 +310,7 @@ distill_status distill_eval_grid_multi(const distill_model* m, const distill_mul
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
     p.net = a->d_net; p.best = a->d_best;
     p.pos_dev = a->d_inputs; p.n_sets = a->n_sets;
-    const dim3 grid((unsigned)((count + PP_BLOCK - 1) / PP_BLOCK), a->n_invocations);
-    cudaStream_t st = (cudaStream_t)stream;
-    if ((a->n_samples & 1u) == 0)
-        pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true, true><<<grid, PP_BLOCK, 0, st>>>(p);
-    else
-        pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
-    g_launches++;
+    launch_pp_search(m, p, a->n_invocations, (cudaStream_t)stream);
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;
 }
@@ -531,11 +538,7 @@ static void episode_search(const distill_model* m, const distill_episode_args* e
     p.pos_dev = e->d_traj + 6ull * t;
     p.best = e->d_keys + t;
     p.begin = (uint32_t)begin; p.count = (uint32_t)(end - begin);
-    const unsigned grid = (unsigned)((end - begin + PP_BLOCK - 1) / PP_BLOCK);
-    if (pp_small(m, end - begin, e->n_samples)) launch_pp_small(m, p, end - begin, st);
-    else if ((e->n_samples & 1u) == 0) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
-    else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
-    g_launches++;
+    launch_pp_search(m, p, 1, st);
 }
 
 static void episode_advance(const distill_model* m, const distill_episode_args* e, const PPArgs& p, uint32_t t,
@@ -630,11 +633,7 @@ static void amr_search(const distill_model* m, const distill_amr_args* g, PPArgs
     p.invocation = g->invocation0 + r;
     p.best = g->d_keys + r;
     p.begin = (uint32_t)begin; p.count = (uint32_t)(end - begin);
-    const unsigned grid = (unsigned)((end - begin + PP_BLOCK - 1) / PP_BLOCK);
-    if (pp_small(m, end - begin, g->n_samples)) launch_pp_small(m, p, end - begin, st);
-    else if ((g->n_samples & 1u) == 0) pp_eval_grid_kernel<PP_BLOCK, DISTILL_PP_MASK, DISTILL_PP_MINB, false, true><<<grid, PP_BLOCK, 0, st>>>(p);
-    else pp_eval_grid_kernel<PP_BLOCK><<<grid, PP_BLOCK, 0, st>>>(p);
-    g_launches++;
+    launch_pp_search(m, p, 1, st);
 }
 
 distill_status distill_pp_amr_begin(const distill_model* m, const distill_amr_args* g, void* stream) {
