@@ -103,3 +103,45 @@ def test_gloo_world2_key_and_hist_allreduce(orc):
         assert decoded[1] == k_full & 0xFFFFFFFF and np.float32(decoded[0]) == C[decoded[1]]
         for a, b in zip(h, h_full):
             assert np.array_equal(a.astype(np.uint64), b)
+
+
+def _worker4(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2110_15425_b200.dist import best_allreduce, shard_range
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = W.pp_weak(world)                       # the bench's weak-scaling grid for this world size
+    cfg = W.PPConfig(cfg.name, (9, 8, 7), 6)     # same code path on a grid the oracle finishes quickly
+    b, e = shard_range(cfg.n_alloc, rank, world)
+    C = oracle.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, b, e, cfg.n_samples, cfg.seed)
+    k = oracle.argmax_net(-C, b)[0] if e > b else 0xFFFFFFFFFFFFFFFF
+    best = torch.tensor([k if k < 2 ** 63 else k - 2 ** 64], dtype=torch.int64)
+    best_allreduce(best)
+    q.put((rank, int(best.item()) & (2 ** 64 - 1)))
+    dist.destroy_process_group()
+
+
+def test_gloo_world4_key_allreduce(orc):
+    """Four ranks (the N = 4 shape of the scaling run): contiguous shards and the
+    signed-flip MIN all-reduce give the single-process argmax key on every rank."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker4, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = W.PPConfig("g4", (9, 8, 7), 6)
+    C = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc, cfg.n_samples, cfg.seed)
+    k_full = orc.argmax_net(-C)[0]
+    assert sorted(r for r, _ in res) == [0, 1, 2, 3]
+    assert all(k == k_full for _, k in res)
