@@ -245,6 +245,18 @@ distill_status distill_key_reset(unsigned long long* d_best, void* stream);
 /* Host, pure: key -> (cost C, global index).  DISTILL_E_NO_VALID for an all-NaN/empty key. */
 distill_status distill_key_decode(unsigned long long key, float* cost, uint64_t* index);
 
+/* Decision energy over time of one Stroop-LCA allocation (spec/MODELS.md §6b;
+ * PAPER.md P:525 "the model is used to predict decision energy over time"):
+ * for trials [trial_begin, trial_end) of T = n_trials (the same RNG units as
+ * distill_eval_grid with n_samples = T), d_esum[n-1] += Σ_j llrint(x0_j(n)·x1_j(n)·2^24)
+ * for n = 1..N (exact integer sums, order-free).  The mean conflict energy of
+ * the response layer with lateral inhibition β is E(n) = 2β·d_esum[n-1] /
+ * ((trial_end − trial_begin)·2^24).  d_esum: device, caller-owned [N] u64,
+ * accumulated.  STROOP_LCA models only (E_UNSUPPORTED otherwise); N <= 4096. */
+distill_status distill_stroop_energy(const distill_model* model, uint64_t alloc, uint32_t n_trials,
+                                     uint32_t trial_begin, uint32_t trial_end, uint64_t seed,
+                                     unsigned long long* d_esum, void* stream);
+
 /* DDM batch over trials [trial_begin, trial_end): histograms accumulated with atomics. */
 distill_status distill_ddm_batch(const distill_ddm_args* args, void* stream);
 

@@ -76,6 +76,8 @@ def _bind(path: str) -> C.CDLL:
         "od_stroop_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u64, u32, u32, u32, u64, C.c_void_p, C.c_void_p]),
         "od_stroop_value": (f32, [_f32p, _f32p, f32, f32, u32, u64, u64, u64]),
         "od_stroop_trial": (None, [_f32p, f32, f32, u64, u64, u32, C.POINTER(C.c_int), C.POINTER(u32)]),
+        "od_stroop_energy": (None, [_f32p, f32, f32, u64, u64, u32, u32, u32,
+                                    np.ctypeslib.ndpointer(np.int64, flags="C")]),
         "od_pp_episode": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u32, u32, u64, _f32p, f32,
                                     _f32p, _u64p, np.ctypeslib.ndpointer(np.int32, flags="C")]),
         "od_pp_amr": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, _f32p, u32, u32, u64, u32, _u64p, _f32p]),
@@ -380,6 +382,30 @@ def stroop_eval(n_levels, levels, w, params, begin, end, n_trials, seed,
     for t in ts:
         t.join()
     return counts, net
+
+
+def stroop_energy(params, u_c, u_s, seed, i, n_trials, t0, t1, threads=1):
+    """Decision-energy trace (spec/MODELS.md §6b; "predict decision energy
+    over time"): int64 sums over trials [t0, t1) of llrint(x0(n) x1(n) 2^24)."""
+    N = int(np.float32(params[10]))
+    P = np.ascontiguousarray(np.asarray(params, np.float32))
+    threads = max(1, min(int(threads), max(int(t1) - int(t0), 1)))
+    seg = (int(t1) - int(t0) + threads - 1) // threads
+    parts = [np.zeros(N, np.int64) for _ in range(threads)]
+
+    def work(k):
+        s0 = int(t0) + k * seg
+        s1 = min(int(t1), s0 + seg)
+        if s1 > s0:
+            lib().od_stroop_energy(P, float(u_c), float(u_s), int(seed), int(i), int(n_trials), s0, s1, parts[k])
+
+    import threading
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return np.sum(parts, axis=0)
 
 
 def stroop_trial(params, u_c, u_s, seed, unit, trial):

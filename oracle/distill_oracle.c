@@ -481,8 +481,10 @@ void od_lci_trial(float input, float leak, float offset, float noise, float dt,
 /* ------------------------------------------------------------------------ */
 enum { SP_GC, SP_GW, SP_TAU, SP_LEAK, SP_INH, SP_NOISE, SP_DT, SP_THR, SP_R, SP_CRT, SP_N };
 
-void od_stroop_trial(const float P[11], float u_c, float u_s, uint64_t seed,
-                     uint64_t unit, uint32_t trial, int* resp, uint32_t* step) {
+/* One Stroop-LCA trial (spec/MODELS.md §6); if esum is non-NULL, also the
+ * decision-energy trace of §6b: esum[n-1] += llrint(x0(n) * x1(n) * 2^24). */
+static void stroop_trial_core(const float P[11], float u_c, float u_s, uint64_t seed,
+                              uint64_t unit, uint32_t trial, int* resp, uint32_t* step, int64_t* esum) {
     uint32_t kind = trial % 3, color = (trial / 3) % 2;
     int word = (kind == 0) ? (int)color : (kind == 1) ? (int)(1 - color) : -1;
     float ic = FMUL(P[SP_GC], u_c);
@@ -509,12 +511,29 @@ void od_stroop_trial(const float P[11], float u_c, float u_s, uint64_t seed,
             xn[k] = fmaxf(y, 0.0f);
         }
         x[0] = xn[0]; x[1] = xn[1];
+        if (esum) esum[n - 1] += llrintf(FMUL(FMUL(x[0], x[1]), 0x1p24f));   /* exact scaling; round to nearest even */
         if (r < 0) {
             if (x[0] >= P[SP_THR]) { r = 0; st = n; }
             else if (x[1] >= P[SP_THR]) { r = 1; st = n; }
         }
     }
     *resp = r; *step = st;
+}
+
+void od_stroop_trial(const float P[11], float u_c, float u_s, uint64_t seed,
+                     uint64_t unit, uint32_t trial, int* resp, uint32_t* step) {
+    stroop_trial_core(P, u_c, u_s, seed, unit, trial, resp, step, NULL);
+}
+
+/* spec/MODELS.md §6b: decision-energy trace of allocation i (u_c, u_s) over
+ * trials [t0, t1) of T: esum[n-1] += llrint(x0(n) x1(n) 2^24), n = 1..N. */
+void od_stroop_energy(const float P[11], float u_c, float u_s, uint64_t seed, uint64_t i, uint32_t n_trials,
+                      uint32_t t0, uint32_t t1, int64_t* esum) {
+    for (uint32_t j = t0; j < t1; ++j) {
+        int resp;
+        uint32_t st;
+        stroop_trial_core(P, u_c, u_s, seed, i * (uint64_t)n_trials + j, j, &resp, &st, esum);
+    }
 }
 
 float od_stroop_value(const float P[11], const float w[2], float u_c, float u_s,

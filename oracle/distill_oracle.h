@@ -24,6 +24,7 @@
  *   od_lci_trial         pinned: Fig. 3 clone relation to od_ddm_trial (bit-identical)
  *   od_stroop_eval       pinned: zero-noise deterministic RT, conservation, Stroop effect,
  *                        reflected-BM closed-form mean first passage of the noisy unit;
+ *   od_stroop_energy     pinned: zero-noise closed form n^2 dt^2 I0 I1, congruent = 0, range additivity;
  *                        absolute values at the cfg4 constants parity unpinned (the paper prints none)
  *   od_pp_episode        pinned: closed-form straight-chase capture step, one-step predator capture,
  *                        per-step keys = ordinary grid searches
@@ -112,6 +113,9 @@ int od_stroop_eval(const uint32_t n_levels[2], const float* levels, const float 
 float od_stroop_value(const float params[11], const float w[2], float u_c, float u_s,
                       uint32_t n_trials, uint64_t n_correct, uint64_t n_undecided, uint64_t rt_sum);
 /* single Stroop trial (for tests) */
+/* decision-energy trace (spec/MODELS.md §6b) of allocation i over trials [t0, t1): esum[N] += */
+void od_stroop_energy(const float params[11], float u_c, float u_s, uint64_t seed, uint64_t i, uint32_t n_trials,
+                      uint32_t t0, uint32_t t1, int64_t* esum);
 void od_stroop_trial(const float params[11], float u_c, float u_s, uint64_t seed,
                      uint64_t unit, uint32_t trial, int* resp, uint32_t* step);
 

@@ -11,6 +11,7 @@ Public Python API (thin wrappers over the C ABI in include/distill.h):
     argmax(values, index_base, best) / argmax_ties(values, base, seed, t, best, tie)
     key_reset(best) / key_decode(key)
     ddm_batch(...)
+    stroop_energy(model, alloc, n_trials, seed)   # decision energy over time
     pp_episode(model, init, n_steps, n_samples, seed, ...)   # closed loop, on the device
     pp_amr(model, inputs, lo, hi, rounds, n_samples, seed)   # coarse-to-fine refinement
     shard_range(n, rank, world) / best_allreduce(key, group)   # multi-GPU plumbing
@@ -19,11 +20,11 @@ Public Python API (thin wrappers over the C ABI in include/distill.h):
 Importing this package does not touch the GPU; the shared library is loaded
 on first use and there is no CPU fallback.
 """
-from .api import (KEY_INIT, AmrRun, EpisodeRun, Model, best, grid_search, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_multi, key_decode,
+from .api import (KEY_INIT, AmrRun, EpisodeRun, Model, best, grid_search, stroop_energy, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_multi, key_decode,
                   key_reset, launch_count, load_model, pp_amr, pp_episode)
 from .dist import (best_allreduce, hist_allreduce, key_to_i64, i64_to_key, pp_amr_sharded, pp_episode_sharded,
                    shard_range)
 
-__all__ = ["KEY_INIT", "Model", "best", "grid_search", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "eval_grid_multi", "key_decode", "pp_episode", "pp_amr",
+__all__ = ["KEY_INIT", "Model", "best", "grid_search", "stroop_energy", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "eval_grid_multi", "key_decode", "pp_episode", "pp_amr",
            "key_reset", "launch_count", "load_model", "best_allreduce", "hist_allreduce", "key_to_i64",
            "i64_to_key", "shard_range", "pp_episode_sharded", "EpisodeRun", "pp_amr_sharded", "AmrRun"]

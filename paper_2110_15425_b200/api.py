@@ -28,7 +28,7 @@ def _stream_handle(stream) -> Optional[int]:
 
 # element type each named buffer must have (the C ABI's float* / u64* / int*);
 # u64 buffers are int64 tensors holding the raw bit pattern
-_BUF_DTYPE = {"net": "float32", "values": "float32", "inputs": "float32", "traj": "float32",
+_BUF_DTYPE = {"esum": "int64", "net": "float32", "values": "float32", "inputs": "float32", "traj": "float32",
               "boxes": "float32", "levels": "float32",
               "best": "int64", "tie": "int64", "keys": "int64", "counts": "int64",
               "rt_hist": "int64", "rt_sum": "int64", "x_hist": "int64", "status": "int32"}
@@ -177,6 +177,19 @@ def eval_grid_host(model: Model, inputs, n_samples: int, seed: int, begin: int =
                                            int(n_samples), int(invocation), int(seed) & (2 ** 64 - 1), net_ptr,
                                            C.cast(key_ptr, C.POINTER(C.c_uint64)), _stream_handle(stream)))
         return int(model._h_key[0]) & (2 ** 64 - 1)
+
+
+def stroop_energy(model: Model, alloc: int, n_trials: int, seed: int, trial_range=None, esum=None, stream=None):
+    """distill_stroop_energy: per-step sums of llrint(x0·x1·2^24) over the trials of
+    one Stroop-LCA allocation (int64 CUDA tensor [N], accumulated; zeroed if allocated here)."""
+    import torch
+    N = int(model.params[10])
+    if esum is None:
+        esum = torch.zeros(N, dtype=torch.int64, device=torch.device("cuda", model.device))
+    t0, t1 = (0, int(n_trials)) if trial_range is None else (int(trial_range[0]), int(trial_range[1]))
+    check(lib().distill_stroop_energy(model.handle, int(alloc), int(n_trials), t0, t1, int(seed) & (2 ** 64 - 1),
+                                      _dev_ptr(esum, "esum", N), _stream_handle(stream)))
+    return esum
 
 
 def argmax(values, index_base: int, best, stream=None) -> None:
@@ -335,5 +348,5 @@ def key_from_tensor(best) -> int:
     return int(best.reshape(-1)[0].item()) & (2 ** 64 - 1)
 
 
-__all__ = ["KEY_INIT", "AmrRun", "DistillError", "EpisodeRun", "Model", "grid_search", "best", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",
+__all__ = ["KEY_INIT", "stroop_energy", "AmrRun", "DistillError", "EpisodeRun", "Model", "grid_search", "best", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",
            "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode", "argmax_ties", "pp_amr", "sm_clock_mhz"]

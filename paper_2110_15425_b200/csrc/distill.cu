@@ -393,6 +393,37 @@ void launch_ext_stroop_kernels(const ExtStroopArgs& p, uint32_t chunks, uint64_t
 }
 }  // extern "C++"
 
+distill_status distill_stroop_energy(const distill_model* m, uint64_t alloc, uint32_t n_trials,
+                                     uint32_t trial_begin, uint32_t trial_end, uint64_t seed,
+                                     unsigned long long* d_esum, void* stream) {
+    if (!m || !d_esum) return fail(DISTILL_E_INVALID_ARG, "stroop_energy: NULL model/d_esum");
+    if (m->kind != DISTILL_MODEL_STROOP_LCA) return fail(DISTILL_E_UNSUPPORTED, "stroop_energy: Stroop-LCA models only");
+    if (alloc >= m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "stroop_energy: allocation index past the grid");
+    if (n_trials == 0 || n_trials > MAX_SAMPLES || trial_begin > trial_end || trial_end > n_trials)
+        return fail(DISTILL_E_INVALID_ARG, "stroop_energy: bad trial range");
+    if ((uint64_t)m->n_alloc * n_trials >= (1ull << 63)) return fail(DISTILL_E_OVERFLOW, "stroop_energy: RNG unit overflow");
+    const uint32_t N = (uint32_t)m->params[10];
+    if (N > 4096) return fail(DISTILL_E_UNSUPPORTED, "stroop_energy: at most 4096 steps");
+    if (trial_begin == trial_end) return DISTILL_OK;
+    CUDA_TRY(cudaSetDevice(m->device));
+    StroopArgs p;
+    memset(&p, 0, sizeof p);
+    const float* P = m->params.data();
+    p.g_c = P[0]; p.g_w = P[1]; p.tau = P[2]; p.leak = P[3]; p.inh = P[4]; p.noise = P[5];
+    p.dt = P[6]; p.thr = P[7]; p.reward = P[8]; p.rt_cost = P[9]; p.n_steps = N;
+    p.L0 = m->L[0]; p.L1 = m->L[1];
+    p.n_trials = n_trials; p.trial_begin = trial_begin; p.trial_end = trial_end;
+    p.key0 = (uint32_t)seed; p.key1 = (uint32_t)(seed >> 32);
+    p.levels = m->d_levels;
+    const uint32_t tr = trial_end - trial_begin;
+    const unsigned grid = (unsigned)std::min<uint64_t>((tr + STROOP_BLOCK - 1) / STROOP_BLOCK, (uint64_t)m->n_sm * 8);
+    stroop_energy_kernel<STROOP_BLOCK><<<grid, STROOP_BLOCK, N * sizeof(unsigned long long), (cudaStream_t)stream>>>(
+        p, (uint32_t)alloc, d_esum);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
 static distill_status launch_ext_stroop(distill_model* m, const distill_eval_args* a, cudaStream_t st) {
     if (a->n_samples == 0 || a->n_samples > MAX_SAMPLES)
         return fail(DISTILL_E_INVALID_ARG, "eval_grid(Ext-Stroop): n_samples (trials) must be in [1, 2^31]");

@@ -168,6 +168,65 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
     }
 }
 
+// Decision-energy trace of one allocation (spec/MODELS.md §6b; "the
+// model is used to predict decision energy over time"): per step n, the
+// product x0(n)·x1(n) of every trial, scaled by 2^24 (exact) and rounded to an
+// integer, summed exactly over trials: a warp reduction per step, then one
+// shared-memory atomic per warp and one global atomic per block and step.
+// Trials run in uniform rounds so every lane of a warp reaches the shuffles.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) stroop_energy_kernel(const StroopArgs a, uint32_t alloc,
+                                                              unsigned long long* __restrict__ esum) {
+    extern __shared__ unsigned long long s_esum[];          // [n_steps]
+    const uint32_t N = a.n_steps;
+    for (uint32_t n = threadIdx.x; n < N; n += BLOCK) s_esum[n] = 0ull;
+    __syncthreads();
+    const uint32_t i = alloc;
+    const uint32_t k1 = i % a.L1, k0 = i / a.L1;
+    const float uc = __ldg(a.levels + k0), us = __ldg(a.levels + a.L0 + k1);
+    const float ic = __fmul_rn(a.g_c, uc);
+    const float iw = __fmul_rn(a.g_w, __fadd_rn(1.0f, -us));
+    const float nsd = __fmul_rn(a.noise, __fsqrt_rn(a.dt));
+    const float nleak = -a.leak, ninh = -a.inh;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t stride = gridDim.x * BLOCK;
+    const uint32_t n_tr = a.trial_end - a.trial_begin;
+    const uint32_t rounds = (n_tr + stride - 1) / stride;
+    for (uint32_t rd = 0; rd < rounds; ++rd) {
+        const uint32_t off = rd * stride + blockIdx.x * BLOCK + threadIdx.x;
+        const bool valid = off < n_tr;
+        const uint32_t j = a.trial_begin + (valid ? off : 0u);
+        const uint32_t kind = j % 3, colour = (j / 3) & 1;
+        const int word = (kind == 0) ? (int)colour : (kind == 1) ? (int)(1 - colour) : -1;
+        Pathway<false> pw;
+        pw.I0 = __fadd_rn(colour == 0 ? ic : 0.0f, word == 0 ? iw : 0.0f);
+        pw.I1 = __fadd_rn(colour == 1 ? ic : 0.0f, word == 1 ? iw : 0.0f);
+        pw.tau = a.tau; pw.h0 = 0.0f; pw.h1 = 0.0f;
+        const uint64_t unit = (uint64_t)i * a.n_trials + j;
+        PhiloxHoisted rng;
+        rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
+        float x0 = 0.f, x1 = 0.f;
+        float g[12];
+        for (uint32_t n = 1; n <= N; ++n) {
+            const uint32_t grp = (n - 1) / 6, l = (n - 1) % 6;
+            if (l == 0) {                                    // normals of steps 6grp+1 .. 6grp+6
+                if (N - 6 * grp >= 6) acc_normals12(rng, grp, g);
+                else acc_normals_tail(rng, grp, 2 * (N - 6 * grp), g);
+            }
+            float h0, h1;
+            pw.at(n, h0, h1);
+            lca_update(a, nleak, ninh, nsd, g[2 * l], g[2 * l + 1], h0, h1, x0, x1);
+            long long q = valid ? __float2ll_rn(__fmul_rn(__fmul_rn(x0, x1), 0x1p24f)) : 0ll;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xFFFFFFFFu, q, o);
+            if (lane == 0 && q) atomicAdd(&s_esum[n - 1], (unsigned long long)q);
+        }
+    }
+    __syncthreads();
+    for (uint32_t n = threadIdx.x; n < N; n += BLOCK)
+        if (s_esum[n]) atomicAdd(esum + n, s_esum[n]);
+}
+
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) stroop_finalize_kernel(const StroopArgs a) {
     const uint32_t t = blockIdx.x * BLOCK + threadIdx.x;

@@ -957,3 +957,35 @@ def test_ext_stroop_and_stroop_cfg4_shards_bit_exact(D, orc):
     assert np.array_equal(cnt, wc)
     assert np.array_equal(_bits(net), _bits(wn))
     assert key == orc.argmax_net(wn, b)[0]
+
+
+def test_stroop_energy_trace_bit_exact(D, orc):
+    """Decision energy over time (§6b): per-step integer sums bit-exact
+    against the oracle for several allocations, trial sub-ranges (accumulating
+    into one buffer), an odd step count, and the cfg4 constants with 1e5 trials."""
+    import os
+    import torch
+    c = W.stroop_small()
+    P = c.params.copy()
+    P[10] = 37
+    m = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, P, device=0)
+    for alloc in (0, 17, c.n_alloc - 1):
+        got = D.stroop_energy(m, alloc, c.n_trials, 9)
+        torch.cuda.synchronize()
+        k0, k1 = alloc // c.n_levels[1], alloc % c.n_levels[1]
+        uc, us = float(c.levels[k0]), float(c.levels[c.n_levels[0] + k1])
+        want = orc.stroop_energy(P, uc, us, 9, alloc, c.n_trials, 0, c.n_trials)
+        assert np.array_equal(got.cpu().numpy(), want), alloc
+    esum = torch.zeros(37, dtype=torch.int64, device="cuda")
+    D.stroop_energy(m, 5, c.n_trials, 4, trial_range=(0, 111), esum=esum)
+    D.stroop_energy(m, 5, c.n_trials, 4, trial_range=(111, c.n_trials), esum=esum)
+    torch.cuda.synchronize()
+    uc, us = float(c.levels[0]), float(c.levels[c.n_levels[0] + 5])
+    assert np.array_equal(esum.cpu().numpy(), orc.stroop_energy(P, uc, us, 4, 5, c.n_trials, 0, c.n_trials))
+    g = W.stroop_cfg4()
+    mg = D.load_model(W.KIND_STROOP_LCA, g.n_levels, g.levels, g.w, g.params, device=0)
+    got = D.stroop_energy(mg, 8083, g.n_trials, g.seed)
+    torch.cuda.synchronize()
+    uc, us = float(g.levels[80]), float(g.levels[100 + 83])
+    want = orc.stroop_energy(g.params, uc, us, g.seed, 8083, g.n_trials, 0, g.n_trials, threads=os.cpu_count() or 8)
+    assert np.array_equal(got.cpu().numpy(), want)

@@ -218,3 +218,25 @@ def test_lci_with_leak_endpoint_is_the_ar1_law(orc):
     r_bad = 1 + lam * dt
     mean_bad = I * dt * (1 - r_bad ** N) / (1 - r_bad)
     assert abs(xs.mean() - mean_bad) > 50 * xs.std() / math.sqrt(len(xs))
+
+
+def test_stroop_energy_trace_closed_forms(orc):
+    """Decision energy over time (spec/MODELS.md §6b): with zero noise, no
+    leak, no inhibition and tau = 1, unit k integrates x_k(n) = n dt I_k, so an
+    incongruent trial (both units driven, colour 0: I_0 = g_c u_c, I_1 = g_w (1 - u_s))
+    has energy x0 x1 = n^2 dt^2 I_0 I_1 (binary32 accumulation within 1e-5), a
+    congruent trial (only the colour unit driven) has energy 0 at every step, and
+    sums over trial ranges add."""
+    P = W.STROOP_PARAMS.copy()
+    P[2], P[3], P[4], P[5], P[6], P[7], P[10] = 1.0, 0.0, 0.0, 0.0, 0.01, 1e9, 150
+    u_c, u_s = 0.8, 0.25
+    I0, I1 = P[0] * u_c, P[1] * (1 - u_s)
+    e = orc.stroop_energy(P, u_c, u_s, 3, 7, 30, 1, 2)          # trial 1: incongruent, colour 0
+    n = np.arange(1, 151, dtype=np.float64)
+    want = n ** 2 * 0.01 ** 2 * I0 * I1 * 2 ** 24
+    assert np.all(np.abs(e - want) <= 1e-5 * want + 1)
+    assert not np.any(orc.stroop_energy(P, u_c, u_s, 3, 7, 30, 0, 1))   # trial 0: congruent -> 0
+    Q = W.STROOP_PARAMS.copy()
+    whole = orc.stroop_energy(Q, 0.6, 0.4, 11, 2, 90, 0, 90)
+    parts = orc.stroop_energy(Q, 0.6, 0.4, 11, 2, 90, 0, 37) + orc.stroop_energy(Q, 0.6, 0.4, 11, 2, 90, 37, 90)
+    assert np.array_equal(whole, parts) and whole[-1] > 0
