@@ -549,6 +549,17 @@ def run_extras(D, torch, dev, rank, world, args):
         xsteps = int(g.params[3]) + int(g.params[10])
         out["ext_stroop_a"] = {"workload": g.name, "evals_per_s": g.evals / (xms / 1e3), "ms": xms,
                                "trial_steps": xsteps, "best_index": key_from_tensor(xbest) & 0xFFFFFFFF}
+        # decision energy over time of the chosen allocation, all 1e5 trials
+        en = torch.zeros(c.n_steps, dtype=torch.int64, device=dev)
+        e2.record()
+        D.stroop_energy(m, idx, c.n_trials, c.seed, esum=en)
+        e3.record()
+        torch.cuda.synchronize()
+        beta = float(c.params[4])
+        trace = (2 * beta * en.double() / (c.n_trials * 2.0 ** 24)).cpu().numpy()
+        out["stroop_energy_best"] = {"ms": e2.elapsed_time(e3), "allocation": idx, "trials": c.n_trials,
+                                     "mean_energy_at_steps": {str(n): float(trace[n - 1])
+                                                              for n in (1, 10, 50, 100, c.n_steps)}}
         out["stroop_cfg4"] = {"evals_per_s": c.evals / (ms / 1e3),
                               "step_updates_per_s": c.evals * c.n_steps / (ms / 1e3), "ms": ms,
                               "algorithmic_tflops": tf, "frac_fp32_peak": tf / FP32_PEAK_NOMINAL,
