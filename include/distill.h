@@ -259,6 +259,12 @@ distill_status distill_stroop_energy(const distill_model* model, uint64_t alloc,
 
 /* DDM batch over trials [trial_begin, trial_end): histograms accumulated with atomics. */
 distill_status distill_ddm_batch(const distill_ddm_args* args, void* stream);
+/* Leaky competing integrator batch (spec/MODELS.md §5): the same
+ * arguments, outputs and RNG units as distill_ddm_batch with `drift` read as
+ * the input I and the step x = fma(σ√dt, g, fma(dt, fma(-leak, x, I), x) + offset).
+ * With leak = offset = 0 it is bit-identical to distill_ddm_batch (Fig. 3's
+ * "computationally equivalent" pair). */
+distill_status distill_lci_batch(const distill_ddm_args* args, float leak, float offset, void* stream);
 
 /* Measurement utility: median effective SM clock (MHz) over one spinning block per
  * SM for `micros` microseconds (clock64 ticks / globaltimer ns).  Synchronous.

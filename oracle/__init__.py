@@ -71,6 +71,7 @@ def _bind(path: str) -> C.CDLL:
         "od_argmax_net": (C.c_int, [_f32p, u64, u64, C.POINTER(u64)]),
         "od_ddm_trial": (None, [C.POINTER(DdmParams), u64, u64, C.POINTER(C.c_int), C.POINTER(u32), C.POINTER(f32)]),
         "od_ddm_batch": (C.c_int, [C.POINTER(DdmParams), u64, u64, u64, _u64p, _u64p, _u64p]),
+        "od_lci_batch": (C.c_int, [C.POINTER(DdmParams), f32, f32, u64, u64, u64, _u64p, _u64p, _u64p]),
         "od_lci_trial": (None, [f32, f32, f32, f32, f32, f32, u32, u64, u64,
                                 C.POINTER(C.c_int), C.POINTER(u32), C.POINTER(f32)]),
         "od_stroop_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u64, u32, u32, u32, u64, C.c_void_p, C.c_void_p]),
@@ -320,7 +321,9 @@ def ddm_hist_sizes(p: DdmParams):
     return 2 * nb + 1, 2, p.n_x_bins + 2
 
 
-def ddm_batch(p: DdmParams, seed: int, t0: int, t1: int, threads: int = 1):
+def ddm_batch(p: DdmParams, seed: int, t0: int, t1: int, threads: int = 1, lci=None):
+    """DDM batch histograms (spec/MODELS.md §4); with lci = (leak, offset) the
+    LCI update of §5 instead (drift = input I), binned identically."""
     a, b, c = ddm_hist_sizes(p)
     threads = max(1, min(int(threads), max(t1 - t0, 1)))
     seg = (t1 - t0 + threads - 1) // threads
@@ -331,7 +334,10 @@ def ddm_batch(p: DdmParams, seed: int, t0: int, t1: int, threads: int = 1):
         s = t0 + t * seg
         e = min(t1, s + seg)
         if e > s:
-            L.od_ddm_batch(C.byref(p), seed, s, e, *parts[t])
+            if lci is None:
+                L.od_ddm_batch(C.byref(p), seed, s, e, *parts[t])
+            else:
+                L.od_lci_batch(C.byref(p), float(lci[0]), float(lci[1]), seed, s, e, *parts[t])
 
     ts = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
     for t in ts:

@@ -457,11 +457,11 @@ int od_ddm_batch(const od_ddm_params* p, uint64_t seed, uint64_t t0, uint64_t t1
 /* ------------------------------------------------------------------------ */
 /* spec/MODELS.md §5: LCI (Fig. 3 clone of the DDM integrator)               */
 /* ------------------------------------------------------------------------ */
-void od_lci_trial(float input, float leak, float offset, float noise, float dt,
-                  float threshold, uint32_t n_steps, uint64_t seed, uint64_t unit,
-                  int* choice, uint32_t* step, float* x_end) {
+static void lci_trial_core(float input, float leak, float offset, float noise, float dt, float threshold,
+                           float x0, uint32_t n_steps, uint64_t seed, uint64_t unit,
+                           int* choice, uint32_t* step, float* x_end) {
     float nsd = FMUL(noise, FSQRT(dt));
-    float x = 0.0f;
+    float x = x0;
     int ch = 2;
     uint32_t st = 0;
     for (uint32_t n = 1; n <= n_steps; ++n) {
@@ -474,6 +474,35 @@ void od_lci_trial(float input, float leak, float offset, float noise, float dt,
         }
     }
     *choice = ch; *step = st; *x_end = x;
+}
+
+void od_lci_trial(float input, float leak, float offset, float noise, float dt,
+                  float threshold, uint32_t n_steps, uint64_t seed, uint64_t unit,
+                  int* choice, uint32_t* step, float* x_end) {
+    lci_trial_core(input, leak, offset, noise, dt, threshold, 0.0f, n_steps, seed, unit, choice, step, x_end);
+}
+
+/* LCI batch with the DDM batch's outputs (spec/MODELS.md §5): p->drift is the
+ * input I, p->x0 the start; histograms binned exactly as od_ddm_batch. */
+int od_lci_batch(const od_ddm_params* p, float leak, float offset, uint64_t seed, uint64_t t0, uint64_t t1,
+                 uint64_t* rt_hist, uint64_t* rt_sum, uint64_t* x_hist) {
+    if (!p || p->n_steps == 0 || p->rt_bin_steps == 0 || p->n_x_bins == 0 || t1 < t0) return -1;
+    uint32_t nb = (p->n_steps + p->rt_bin_steps - 1) / p->rt_bin_steps;
+    float sc = (float)p->n_x_bins / (p->x_hi - p->x_lo);
+    for (uint64_t t = t0; t < t1; ++t) {
+        int ch; uint32_t st; float xe;
+        lci_trial_core(p->drift, leak, offset, p->noise, p->dt, p->threshold, p->x0, p->n_steps, seed, t,
+                       &ch, &st, &xe);
+        if (ch == 2) rt_hist[2 * nb] += 1;
+        else { rt_hist[(uint32_t)ch * nb + (st - 1) / p->rt_bin_steps] += 1; rt_sum[ch] += st; }
+        float u = (xe - p->x_lo) * sc;
+        uint32_t bin;
+        if (u < 0.0f) bin = 0;
+        else if (!(u < (float)p->n_x_bins)) bin = p->n_x_bins + 1;
+        else bin = 1 + (uint32_t)u;
+        x_hist[bin] += 1;
+    }
+    return 0;
 }
 
 /* ------------------------------------------------------------------------ */

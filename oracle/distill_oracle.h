@@ -21,7 +21,7 @@
  *   od_argmax_keys       pinned: brute-force min over (C, i), NaN/-0 rules
  *   od_normal_acc        pinned: raw-word Box-Muller definition, moments/kurtosis/KS; cuRAND Philox
  *   od_ddm_*             pinned: zero-noise first passage, closed-form ER/DT, endpoint law
- *   od_lci_trial         pinned: Fig. 3 clone relation to od_ddm_trial (bit-identical)
+ *   od_lci_trial/_batch  pinned: Fig. 3 clone relation to od_ddm_* (bit-identical), AR(1) endpoint law
  *   od_stroop_eval       pinned: zero-noise deterministic RT, conservation, Stroop effect,
  *                        reflected-BM closed-form mean first passage of the noisy unit;
  *   od_stroop_energy     pinned: zero-noise closed form n^2 dt^2 I0 I1, congruent = 0, range additivity;
@@ -98,6 +98,8 @@ int od_ddm_batch(const od_ddm_params* p, uint64_t seed, uint64_t t0, uint64_t t1
                  uint64_t* rt_hist, uint64_t* rt_sum, uint64_t* x_hist);
 
 /* ---- LCI single unit (spec/MODELS.md §5) — Fig. 3 pin ---- */
+int od_lci_batch(const od_ddm_params* p, float leak, float offset, uint64_t seed, uint64_t t0, uint64_t t1,
+                 uint64_t* rt_hist, uint64_t* rt_sum, uint64_t* x_hist);
 void od_lci_trial(float input, float leak, float offset, float noise, float dt,
                   float threshold, uint32_t n_steps, uint64_t seed, uint64_t unit,
                   int* choice, uint32_t* step, float* x_end);

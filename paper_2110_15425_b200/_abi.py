@@ -95,6 +95,7 @@ EXPORTS = {
                                         C.c_void_p]),
     "distill_pp_amr_refine": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_uint32, C.c_void_p]),
     "distill_eval_grid_multi": (C.c_int, [C.c_void_p, C.POINTER(MultiArgs), C.c_void_p]),
+    "distill_lci_batch": (C.c_int, [C.POINTER(DdmArgs), C.c_float, C.c_float, C.c_void_p]),
     "distill_stroop_energy": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                         C.c_void_p, C.c_void_p]),
     "distill_pp_episode": (C.c_int, [C.c_void_p, C.POINTER(EpisodeArgs), C.c_void_p]),

@@ -219,7 +219,7 @@ def key_decode(key: int):
 
 
 def ddm_batch(drift, noise, threshold, x0, dt, n_steps, rt_bin_steps, n_x_bins, x_lo, x_hi,
-              trial_begin, trial_end, seed, rt_hist, rt_sum, x_hist, stream=None) -> None:
+              trial_begin, trial_end, seed, rt_hist, rt_sum, x_hist, stream=None, lci=None) -> None:
     """distill_ddm_batch: histograms (int64 tensors) accumulated on the device."""
     a = _abi.DdmArgs(drift, noise, threshold, x0, dt, int(n_steps), int(rt_bin_steps), int(n_x_bins),
                      x_lo, x_hi, int(trial_begin), int(trial_end), int(seed) & (2 ** 64 - 1),
@@ -227,7 +227,10 @@ def ddm_batch(drift, noise, threshold, x0, dt, n_steps, rt_bin_steps, n_x_bins, 
     nb = (int(n_steps) + int(rt_bin_steps) - 1) // int(rt_bin_steps)
     if rt_hist.numel() < 2 * nb + 1 or x_hist.numel() < int(n_x_bins) + 2:
         raise ValueError("histogram buffers too small")
-    check(lib().distill_ddm_batch(C.byref(a), _stream_handle(stream)))
+    if lci is None:
+        check(lib().distill_ddm_batch(C.byref(a), _stream_handle(stream)))
+    else:                                   # distill_lci_batch: drift is the input I, lci = (leak, offset)
+        check(lib().distill_lci_batch(C.byref(a), float(lci[0]), float(lci[1]), _stream_handle(stream)))
 
 
 def _episode_args(model: Model, init, n_steps: int, n_samples: int, seed: int, speeds, capture_radius,

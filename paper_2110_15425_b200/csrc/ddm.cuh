@@ -14,6 +14,7 @@ namespace distill {
 
 struct DDMArgs {
     float drift, noise, threshold, x0, dt, x_lo, x_hi;
+    float leak, offset;                        // LCI mode only (spec/MODELS.md §5; drift = input I)
     uint32_t n_steps, rt_bin_steps, n_rt_bins, n_x_bins;
     uint32_t key0, key1;
     uint64_t trial_begin, n_trials;
@@ -22,7 +23,16 @@ struct DDMArgs {
     unsigned long long* __restrict__ x_hist;   // [nx+2]
 };
 
-template <int BLOCK, int MINB = 0>
+// One integrator step: DDM x = fma(nsd, g, fma(dt, A, x)) (§4) or, in LCI
+// mode, x = fma(nsd, g, fma(dt, fma(-leak, x, I), x) + offset) (§5), which is
+// the DDM step bit for bit when leak = offset = 0 (Fig. 3).
+template <bool LCI>
+__device__ __forceinline__ float integ_step(const DDMArgs& a, float nsd, float g, float x) {
+    if (LCI) return __fmaf_rn(nsd, g, __fadd_rn(__fmaf_rn(a.dt, __fmaf_rn(-a.leak, x, a.drift), x), a.offset));
+    return __fmaf_rn(nsd, g, __fmaf_rn(a.dt, a.drift, x));
+}
+
+template <int BLOCK, int MINB = 0, bool LCI = false>
 __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a) {
     extern __shared__ uint32_t s_hist[];  // [2*nb+1] rt bins then [nx+2] x bins
     const uint32_t n_rt = 2 * a.n_rt_bins + 1, n_x = a.n_x_bins + 2, n_all = n_rt + n_x;
@@ -52,7 +62,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
             float g[12], xs[12];
             acc_normals12(rng, j, g);
 #pragma unroll
-            for (int l = 0; l < 12; ++l) { x = __fmaf_rn(nsd, g[l], __fmaf_rn(a.dt, a.drift, x)); xs[l] = x; }
+            for (int l = 0; l < 12; ++l) { x = integ_step<LCI>(a, nsd, g[l], x); xs[l] = x; }
             if (st == 0) {
                 float m = fabsf(xs[0]);
 #pragma unroll
@@ -75,7 +85,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
 #pragma unroll
             for (int l = 0; l < 11; ++l) {
                 if ((uint32_t)l < rem) {
-                    x = __fmaf_rn(nsd, g[l], __fmaf_rn(a.dt, a.drift, x));
+                    x = integ_step<LCI>(a, nsd, g[l], x);
                     if (st == 0) {
                         if (x >= z) { st = 12 * n12 + l + 1; ch = 0; }
                         else if (x <= nz) { st = 12 * n12 + l + 1; ch = 1; }

@@ -797,37 +797,51 @@ distill_status distill_key_decode(unsigned long long key, float* cost, uint64_t*
     return DISTILL_OK;
 }
 
-distill_status distill_ddm_batch(const distill_ddm_args* a, void* stream) {
+extern "C++" {
+template <bool LCI>
+static distill_status launch_integrator(const distill_ddm_args* a, float leak, float offset, void* stream,
+                                        const char* who) {
     if (!a || !a->d_rt_hist || !a->d_rt_sum || !a->d_x_hist)
-        return fail(DISTILL_E_INVALID_ARG, "ddm_batch: NULL argument");
+        return fail(DISTILL_E_INVALID_ARG, "%s: NULL argument", who);
     if (a->n_steps == 0 || a->rt_bin_steps == 0 || a->n_x_bins == 0)
-        return fail(DISTILL_E_INVALID_ARG, "ddm_batch: n_steps, rt_bin_steps, n_x_bins must be >= 1");
-    if (!(a->x_lo < a->x_hi) || !(a->dt >= 0.0f)) return fail(DISTILL_E_INVALID_ARG, "ddm_batch: bad x range / dt");
-    if (a->trial_begin > a->trial_end) return fail(DISTILL_E_INVALID_ARG, "ddm_batch: bad trial range");
+        return fail(DISTILL_E_INVALID_ARG, "%s: n_steps, rt_bin_steps, n_x_bins must be >= 1", who);
+    if (!(a->x_lo < a->x_hi) || !(a->dt >= 0.0f)) return fail(DISTILL_E_INVALID_ARG, "%s: bad x range / dt", who);
+    if (a->trial_begin > a->trial_end) return fail(DISTILL_E_INVALID_ARG, "%s: bad trial range", who);
     const uint32_t nb = (a->n_steps + a->rt_bin_steps - 1) / a->rt_bin_steps;
     const size_t smem = (size_t)(2 * nb + 1 + a->n_x_bins + 2) * sizeof(uint32_t);
-    if (smem > 160 * 1024) return fail(DISTILL_E_UNSUPPORTED, "ddm_batch: histograms exceed shared memory");
+    if (smem > 160 * 1024) return fail(DISTILL_E_UNSUPPORTED, "%s: histograms exceed shared memory", who);
     const uint64_t n = a->trial_end - a->trial_begin;
     if (n == 0) return DISTILL_OK;
     int dev = 0, n_sm = 148;
     CUDA_TRY(cudaGetDevice(&dev));
     CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     if (smem > 48 * 1024)
-        CUDA_TRY(cudaFuncSetAttribute(ddm_batch_kernel<DDM_BLOCK, DDM_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+        CUDA_TRY(cudaFuncSetAttribute(ddm_batch_kernel<DDM_BLOCK, DDM_MINB, LCI>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DDMArgs p;
     p.drift = a->drift; p.noise = a->noise; p.threshold = a->threshold; p.x0 = a->x0; p.dt = a->dt;
     p.x_lo = a->x_lo; p.x_hi = a->x_hi;
+    p.leak = leak; p.offset = offset;
     p.n_steps = a->n_steps; p.rt_bin_steps = a->rt_bin_steps; p.n_rt_bins = nb; p.n_x_bins = a->n_x_bins;
     p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
     p.trial_begin = a->trial_begin; p.n_trials = n;
     p.rt_hist = a->d_rt_hist; p.rt_sum = a->d_rt_sum; p.x_hist = a->d_x_hist;
     const uint64_t need = (n + DDM_BLOCK - 1) / DDM_BLOCK;
     const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)n_sm * 1024);
-    ddm_batch_kernel<DDM_BLOCK, DDM_MINB><<<grid, DDM_BLOCK, smem, (cudaStream_t)stream>>>(p);
+    ddm_batch_kernel<DDM_BLOCK, DDM_MINB, LCI><<<grid, DDM_BLOCK, smem, (cudaStream_t)stream>>>(p);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;
+}
+
+}  // extern "C++"
+
+distill_status distill_ddm_batch(const distill_ddm_args* a, void* stream) {
+    return launch_integrator<false>(a, 0.0f, 0.0f, stream, "ddm_batch");
+}
+
+distill_status distill_lci_batch(const distill_ddm_args* a, float leak, float offset, void* stream) {
+    return launch_integrator<true>(a, leak, offset, stream, "lci_batch");
 }
 
 }  // extern "C"

@@ -989,3 +989,29 @@ def test_stroop_energy_trace_bit_exact(D, orc):
     uc, us = float(g.levels[80]), float(g.levels[100 + 83])
     want = orc.stroop_energy(g.params, uc, us, g.seed, 8083, g.n_trials, 0, g.n_trials, threads=os.cpu_count() or 8)
     assert np.array_equal(got.cpu().numpy(), want)
+
+
+def test_lci_batch_bit_exact_and_fig3_clone(D, orc):
+    """distill_lci_batch (spec §5): histograms bit-exact against the
+    oracle with a leak and an offset, and with leak = offset = 0 bit-identical to
+    distill_ddm_batch on the same trials (the Fig. 3 'computationally
+    equivalent' pair, here exact)."""
+    import torch
+
+    def run(d, t0, t1, seed, lci):
+        rh, rs, xh = (torch.zeros(n, dtype=torch.int64, device="cuda") for n in d.hist_sizes)
+        D.ddm_batch(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
+                    d.x_lo, d.x_hi, t0, t1, seed, rh, rs, xh, lci=lci)
+        torch.cuda.synchronize()
+        return [x.cpu().numpy().astype(np.uint64) for x in (rh, rs, xh)]
+
+    for kw, lci in (({"n_steps": 300, "drift": 0.7}, (1.2, 0.0)), ({"n_steps": 77, "drift": -0.4}, (0.5, 0.003)),
+                    ({"n_steps": 1000}, (0.0, 0.0))):
+        d = W.DDMConfig(**kw)
+        got = run(d, 1000, 6000, 21, lci)
+        want = orc.ddm_batch(_ddm_p(orc, d), 21, 1000, 6000, lci=lci)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w), (kw, lci)
+    d = W.DDMConfig(n_steps=500)
+    for g, w in zip(run(d, 0, 20000, 5, (0.0, 0.0)), run(d, 0, 20000, 5, None)):
+        assert np.array_equal(g, w)

@@ -240,3 +240,16 @@ def test_stroop_energy_trace_closed_forms(orc):
     whole = orc.stroop_energy(Q, 0.6, 0.4, 11, 2, 90, 0, 90)
     parts = orc.stroop_energy(Q, 0.6, 0.4, 11, 2, 90, 0, 37) + orc.stroop_energy(Q, 0.6, 0.4, 11, 2, 90, 37, 90)
     assert np.array_equal(whole, parts) and whole[-1] > 0
+
+
+def test_lci_batch_is_the_ddm_batch_at_zero_leak(orc):
+    """Fig. 3 clone relation at batch level: LCI histograms with leak = 0,
+    offset = 0 equal the DDM's bit for bit (same stream-2 normals); a leak changes them."""
+    d = W.DDMConfig(n_steps=240, n_trials=600, x0=0.05)
+    p = orc.ddm_params(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
+                       d.x_lo, d.x_hi)
+    ddm = orc.ddm_batch(p, 13, 0, 600)
+    lci = orc.ddm_batch(p, 13, 0, 600, lci=(0.0, 0.0))
+    assert all(np.array_equal(a, b) for a, b in zip(ddm, lci))
+    leaky = orc.ddm_batch(p, 13, 0, 600, lci=(1.5, 0.0))
+    assert not np.array_equal(ddm[2], leaky[2])
