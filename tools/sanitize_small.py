@@ -47,6 +47,9 @@ def main():
         run.search(t, 50, cfg.n_alloc)
         run.advance(t)
     D.eval_grid_host(m, cfg.inputs, 6, 1, net_out=torch.empty(cfg.n_alloc, pin_memory=True).numpy())
+    D.ddm_batch(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins, d.x_lo,
+                d.x_hi, 0, 700, 1, rh, rs, xh, lci=(0.5, 0.01))
+    D.stroop_energy(ms, 3, c.n_trials, 1)
     torch.cuda.synchronize()
     print("sanitize-small ok", int(best.item()), int(rh.sum()))
 
