@@ -503,6 +503,38 @@ def run_extras(D, torch, dev, rank, world, args):
             sizes[name] = {"allocations": cs.n_alloc, "ms": sms, "evals_per_s": cs.evals / (sms / 1e3),
                            "timing": "CUDA-graph replay of 20 grid searches"}
         out["pp_paper_sizes"] = sizes
+    # DDM control grid (spec §6c): 100 x 100 allocations (attention x threshold) x 1e4 trials x 400 steps
+    try:
+        gd = W.ddmg_grid()
+        mdg = D.load_model(W.KIND_DDM_GRID, gd.n_levels, gd.levels, gd.w, gd.params, device=dev.index)
+        db, de = D.shard_range(gd.n_alloc, rank, world)
+        dnet = torch.empty(max(1, de - db), dtype=torch.float32, device=dev)
+        dbest = torch.empty(1, dtype=torch.int64, device=dev)
+        dcounts = torch.empty(3 * max(1, de - db), dtype=torch.int64, device=dev)
+        D.key_reset(dbest)
+        e0.record()
+        D.eval_grid(mdg, None, gd.n_trials, gd.seed, db, de, net=dnet, best=dbest, counts=dcounts)
+        if world > 1:
+            D.best_allreduce(dbest)
+        e1.record()
+        torch.cuda.synchronize()
+        dms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([dms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dms = float(t.item())
+        from paper_2110_15425_b200.api import key_from_tensor
+        dcost, didx = D.key_decode(key_from_tensor(dbest))
+        steps = int(gd.params[6])
+        out["ddm_grid"] = {"workload": gd.name, "ms": dms, "evals_per_s": gd.evals / (dms / 1e3),
+                           "steps_per_s": gd.evals * steps / (dms / 1e3),
+                           "frac_fp32_peak": DDM_FLOPS_PER_STEP * gd.evals * steps / (dms / 1e3) / 1e12
+                           / FP32_PEAK_NOMINAL,
+                           "best": {"index": didx, "attention": float(gd.levels[didx // gd.n_levels[1]]),
+                                    "threshold": float(gd.levels[gd.n_levels[0] + didx % gd.n_levels[1]]),
+                                    "net_value": -dcost}}
+    except Exception as exc:
+        out["ddm_grid"] = {"error": repr(exc)[:200]}
     if args.stroop:
         c = W.stroop_cfg4()
         m = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=dev.index)

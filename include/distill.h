@@ -44,7 +44,8 @@ typedef enum {
     DISTILL_MODEL_PREDATOR_PREY = 1,  /* P:140-167, Fig. 1                                */
     DISTILL_MODEL_STROOP_LCA = 2,     /* P:525 (surrogate, spec/MODELS.md §6)             */
     DISTILL_MODEL_EXT_STROOP_A = 3,   /* P:527 Extended Stroop, version A (§10, NEXT-3)   */
-    DISTILL_MODEL_EXT_STROOP_B = 4    /* P:527 version B: computationally identical to A  */
+    DISTILL_MODEL_EXT_STROOP_B = 4,   /* P:527 version B: computationally identical to A  */
+    DISTILL_MODEL_DDM_GRID = 5        /* DDM control grid (spec/MODELS.md §6c)            */
 } distill_model_kind;
 
 /* "No candidate" value of a packed (value, index) key; initialise d_best to it. */
@@ -63,7 +64,10 @@ typedef struct distill_model distill_model;  /* opaque, library-owned */
  *                            threshold, reward, rt_cost, n_steps}, n_params = 11.
  *   EXT_STROOP_A/B: n_signals = 2 (as Stroop); params = {g_c, g_w, tau, N_h, lambda,
  *                  a_p, gamma, sigma_d, dt_d, z_d, N_d, reward, rt_cost}, n_params = 13;
- *                  d_counts = {n_both_correct, n_undecided, rt_sum}. */
+ *                  d_counts = {n_both_correct, n_undecided, rt_sum}.
+ *   DDM_GRID:      n_signals = 2 (attention u0 scales the drift, threshold u1);
+ *                  params = {A0, g_a, sigma, dt, reward, rt_cost, n_steps}, n_params = 7;
+ *                  d_counts = {n_correct (upper bound), n_undecided, rt_sum}; V as Stroop. */
 typedef struct {
     uint32_t kind;               /* distill_model_kind                               */
     uint32_t n_signals;          /* D                                                */

@@ -77,6 +77,10 @@ def _bind(path: str) -> C.CDLL:
         "od_stroop_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u64, u32, u32, u32, u64, C.c_void_p, C.c_void_p]),
         "od_stroop_value": (f32, [_f32p, _f32p, f32, f32, u32, u64, u64, u64]),
         "od_stroop_trial": (None, [_f32p, f32, f32, u64, u64, u32, C.POINTER(C.c_int), C.POINTER(u32)]),
+        "od_ddmg_trial": (None, [_f32p, f32, f32, u64, u64, C.POINTER(C.c_int), C.POINTER(u32)]),
+        "od_ddmg_value": (f32, [_f32p, _f32p, f32, f32, u32, u64, u64, u64]),
+        "od_ddmg_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u64, u32, u32, u32, u64, C.c_void_p,
+                                   C.c_void_p]),
         "od_stroop_energy": (None, [_f32p, f32, f32, u64, u64, u32, u32, u32,
                                     np.ctypeslib.ndpointer(np.int64, flags="C")]),
         "od_pp_episode": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u32, u32, u64, _f32p, f32,
@@ -381,6 +385,49 @@ def stroop_eval(n_levels, levels, w, params, begin, end, n_trials, seed,
                               int(seed), cv.ctypes.data_as(C.c_void_p), nv)
         if rc != 0:
             raise ValueError("od_stroop_eval rejected its arguments")
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return counts, net
+
+
+def ddmg_trial(params, u0, u1, seed, unit):
+    """DDM control grid trial (spec/MODELS.md §6c): (resp 1 correct / 0 error / -1 undecided, step)."""
+    r, st = C.c_int(), C.c_uint32()
+    lib().od_ddmg_trial(_f32(params), float(u0), float(u1), int(seed), int(unit), C.byref(r), C.byref(st))
+    return r.value, st.value
+
+
+def ddmg_value(params, w, u0, u1, n_trials, n_correct, n_undecided, rt_sum):
+    return lib().od_ddmg_value(_f32(params), _f32(w), float(u0), float(u1), int(n_trials), int(n_correct),
+                               int(n_undecided), int(rt_sum))
+
+
+def ddmg_eval(n_levels, levels, w, params, begin, end, n_trials, seed, trial_begin=0, trial_end=None, threads=1):
+    """Returns (counts[n,3] uint64 {n_correct, n_undecided, rt_sum}, net[n] float32 or None)."""
+    if trial_end is None:
+        trial_end = n_trials
+    n = int(end) - int(begin)
+    counts = np.zeros((n, 3), np.uint64)
+    full = (trial_begin == 0 and trial_end == n_trials)
+    net = np.zeros(n, np.float32) if full else None
+    args = (_u32(n_levels), _f32(levels), _f32(w), _f32(params))
+    threads = max(1, min(int(threads), max(n, 1)))
+    seg = (n + threads - 1) // threads
+
+    def work(t):
+        b = begin + t * seg
+        e = min(begin + n, b + seg)
+        if e <= b:
+            return
+        cv = counts[b - begin:e - begin]
+        nv = net[b - begin:e - begin].ctypes.data_as(C.c_void_p) if full else None
+        if lib().od_ddmg_eval(*args, b, e, int(n_trials), int(trial_begin), int(trial_end), int(seed),
+                              cv.ctypes.data_as(C.c_void_p), nv) != 0:
+            raise ValueError("od_ddmg_eval rejected its arguments")
 
     ts = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
     for t in ts:

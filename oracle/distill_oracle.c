@@ -601,6 +601,63 @@ int od_stroop_eval(const uint32_t n_levels[2], const float* levels, const float 
 }
 
 /* ------------------------------------------------------------------------ */
+/* spec/MODELS.md §6c: DDM control grid                                      */
+/* ------------------------------------------------------------------------ */
+enum { DG_A0, DG_GA, DG_NOISE, DG_DT, DG_R, DG_CRT, DG_N };
+
+void od_ddmg_trial(const float P[7], float u0, float u1, uint64_t seed, uint64_t unit, int* resp, uint32_t* step) {
+    float A = FFMA(P[DG_GA], u0, P[DG_A0]);
+    float z = u1;
+    float nsd = FMUL(P[DG_NOISE], FSQRT(P[DG_DT]));
+    float x = 0.0f;
+    int r = -1;
+    uint32_t st = 0;
+    uint32_t N = (uint32_t)P[DG_N];
+    for (uint32_t n = 1; n <= N; ++n) {
+        float g;
+        od_normal_acc(seed, unit, n - 1, 1, &g);
+        x = FFMA(nsd, g, FFMA(P[DG_DT], A, x));
+        if (r < 0) {
+            if (x >= z) { r = 1; st = n; }
+            else if (x <= -z) { r = 0; st = n; }
+        }
+    }
+    *resp = r; *step = st;
+}
+
+float od_ddmg_value(const float P[7], const float w[2], float u0, float u1, uint32_t n_trials,
+                    uint64_t n_correct, uint64_t n_undecided, uint64_t rt_sum) {
+    double T = (double)n_trials, N = (double)(uint32_t)P[DG_N];
+    double v = (double)P[DG_R] * (double)n_correct / T;
+    v = v - (double)P[DG_CRT] * (double)P[DG_DT] * ((double)rt_sum + (double)n_undecided * N) / T;
+    v = v - ((double)w[0] * (double)u0 + (double)w[1] * (double)u1);
+    return (float)v;
+}
+
+int od_ddmg_eval(const uint32_t n_levels[2], const float* levels, const float w[2], const float P[7],
+                 uint64_t begin, uint64_t end, uint32_t n_trials, uint32_t trial_begin, uint32_t trial_end,
+                 uint64_t seed, uint64_t* counts, float* net) {
+    if (!n_levels || !levels || !w || !P || n_trials == 0 || end < begin ||
+        trial_end < trial_begin || trial_end > n_trials) return -1;
+    uint64_t NA = (uint64_t)n_levels[0] * n_levels[1];
+    if (NA == 0 || end > NA) return -1;
+    for (uint64_t i = begin; i < end; ++i) {
+        uint32_t k[2];
+        od_decode(i, 2, n_levels, k);
+        float u0 = levels[k[0]], u1 = levels[n_levels[0] + k[1]];
+        uint64_t* c = counts + 3 * (i - begin);
+        for (uint32_t j = trial_begin; j < trial_end; ++j) {
+            int resp; uint32_t st;
+            od_ddmg_trial(P, u0, u1, seed, i * (uint64_t)n_trials + j, &resp, &st);
+            if (resp < 0) c[1] += 1;
+            else { if (resp == 1) c[0] += 1; c[2] += st; }
+        }
+        if (net) net[i - begin] = od_ddmg_value(P, w, u0, u1, n_trials, c[0], c[1], c[2]);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* spec/MODELS.md §7: closed-loop predator-prey episode (NEXT-1)             */
 /* ------------------------------------------------------------------------ */
 int od_pp_episode(const uint32_t n_levels[3], const float* levels, const float w[3],

@@ -26,6 +26,8 @@
  *                        reflected-BM closed-form mean first passage of the noisy unit;
  *   od_stroop_energy     pinned: zero-noise closed form n^2 dt^2 I0 I1, congruent = 0, range additivity;
  *                        absolute values at the cfg4 constants parity unpinned (the paper prints none)
+ *   od_ddmg_*            pinned: zero-noise binary32 passage step, Siegmund-corrected closed-form accuracy and
+ *                        decision time per allocation, exact-rational value formula
  *   od_pp_episode        pinned: closed-form straight-chase capture step, one-step predator capture,
  *                        per-step keys = ordinary grid searches
  *   od_argmax_random_ties pinned: uniform 1/8 frequency over 10^4 seeds, unique minimum wins
@@ -115,6 +117,14 @@ int od_stroop_eval(const uint32_t n_levels[2], const float* levels, const float 
 float od_stroop_value(const float params[11], const float w[2], float u_c, float u_s,
                       uint32_t n_trials, uint64_t n_correct, uint64_t n_undecided, uint64_t rt_sum);
 /* single Stroop trial (for tests) */
+/* DDM control grid (spec/MODELS.md §6c): resp 1 = correct (upper), 0 = error, -1 = undecided */
+void  od_ddmg_trial(const float params[7], float u0, float u1, uint64_t seed, uint64_t unit, int* resp,
+                    uint32_t* step);
+float od_ddmg_value(const float params[7], const float w[2], float u0, float u1, uint32_t n_trials,
+                    uint64_t n_correct, uint64_t n_undecided, uint64_t rt_sum);
+int   od_ddmg_eval(const uint32_t n_levels[2], const float* levels, const float w[2], const float params[7],
+                   uint64_t begin, uint64_t end, uint32_t n_trials, uint32_t trial_begin, uint32_t trial_end,
+                   uint64_t seed, uint64_t* counts, float* net);
 /* decision-energy trace (spec/MODELS.md §6b) of allocation i over trials [t0, t1): esum[N] += */
 void od_stroop_energy(const float params[11], float u_c, float u_s, uint64_t seed, uint64_t i, uint32_t n_trials,
                       uint32_t t0, uint32_t t1, int64_t* esum);

@@ -126,4 +126,92 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
     }
 }
 
+// ---------------------------------------------------------------- DDM control grid
+// spec/MODELS.md §6c (north star: every control allocation runs a DDM): grid
+// (trial chunks, allocations) like the Stroop kernel; per allocation the
+// drift A = fma(g_a, u0, A0) and threshold z = u1; one thread = one trial of
+// N fixed-trip steps, 12 steps per pair of sextet blocks with the max-|x|
+// latch test of the batch kernel; integer outcomes {n_correct (upper),
+// n_undecided, rt_sum} block-reduced and added per allocation.  The value is
+// stroop_finalize_kernel's binary64 formula (same counts, same cost form).
+struct DdmgArgs {
+    float A0, g_a, noise, dt;
+    uint32_t n_steps, L0, L1, n_trials, trial_begin, trial_end, key0, key1, begin, count;
+    const float* __restrict__ levels;
+    unsigned long long* __restrict__ counts;   // [count][3]
+};
+
+template <int BLOCK, int MINB = 0>
+__global__ void __launch_bounds__(BLOCK, MINB) ddmg_sim_kernel(const DdmgArgs a, uint32_t alloc_off) {
+    const uint32_t t_alloc = alloc_off + blockIdx.y;
+    const uint32_t i = a.begin + t_alloc;
+    const uint32_t k1 = i % a.L1, k0 = i / a.L1;
+    const float u0 = __ldg(a.levels + k0), u1 = __ldg(a.levels + a.L0 + k1);
+    const float A = __fmaf_rn(a.g_a, u0, a.A0);
+    const float z = u1, nz = -u1;
+    const float nsd = __fmul_rn(a.noise, __fsqrt_rn(a.dt));
+    uint32_t n_corr = 0, n_und = 0;
+    unsigned long long rts = 0;
+    for (uint32_t j = a.trial_begin + blockIdx.x * BLOCK + threadIdx.x; j < a.trial_end; j += gridDim.x * BLOCK) {
+        const uint64_t unit = (uint64_t)i * a.n_trials + j;
+        PhiloxHoisted rng;
+        rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
+        float x = 0.0f;
+        uint32_t st = 0, ch = 2;                                  // ch: 0 correct (upper), 1 error, 2 none
+        const uint32_t n12 = a.n_steps / 12;
+        for (uint32_t grp = 0; grp < n12; ++grp) {
+            float g[12], xs[12];
+            acc_normals12(rng, grp, g);
+#pragma unroll
+            for (int l = 0; l < 12; ++l) { x = __fmaf_rn(nsd, g[l], __fmaf_rn(a.dt, A, x)); xs[l] = x; }
+            if (st == 0) {
+                float mx = fabsf(xs[0]);
+#pragma unroll
+                for (int l = 1; l < 12; ++l) mx = fmaxf(mx, fabsf(xs[l]));
+                if (mx >= z) {
+#pragma unroll
+                    for (int l = 0; l < 12; ++l) {
+                        if (st == 0) {
+                            if (xs[l] >= z) { st = 12 * grp + l + 1; ch = 0; }
+                            else if (xs[l] <= nz) { st = 12 * grp + l + 1; ch = 1; }
+                        }
+                    }
+                }
+            }
+        }
+        const uint32_t rem = a.n_steps - 12 * n12;
+        if (rem) {
+            float g[12];
+            acc_normals_tail(rng, n12, rem, g);
+#pragma unroll
+            for (int l = 0; l < 11; ++l) {
+                if ((uint32_t)l < rem) {
+                    x = __fmaf_rn(nsd, g[l], __fmaf_rn(a.dt, A, x));
+                    if (st == 0) {
+                        if (x >= z) { st = 12 * n12 + l + 1; ch = 0; }
+                        else if (x <= nz) { st = 12 * n12 + l + 1; ch = 1; }
+                    }
+                }
+            }
+        }
+        if (ch == 2) ++n_und;
+        else { n_corr += (ch == 0); rts += st; }
+    }
+    __shared__ unsigned long long s_red[3][BLOCK / 32];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        n_corr += __shfl_xor_sync(0xFFFFFFFFu, n_corr, off);
+        n_und += __shfl_xor_sync(0xFFFFFFFFu, n_und, off);
+        rts += __shfl_xor_sync(0xFFFFFFFFu, rts, off);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { s_red[0][wid] = n_corr; s_red[1][wid] = n_und; s_red[2][wid] = rts; }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        unsigned long long v = 0;
+        for (int w = 0; w < BLOCK / 32; ++w) v += s_red[threadIdx.x][w];
+        if (v) atomicAdd(a.counts + 3ull * t_alloc + threadIdx.x, v);
+    }
+}
+
 }  // namespace distill

@@ -124,6 +124,7 @@ distill_status distill_load_model(const distill_model_desc* desc, int device, di
     if (desc->kind == DISTILL_MODEL_PREDATOR_PREY) { want_D = 3; want_p = 3; }
     else if (desc->kind == DISTILL_MODEL_STROOP_LCA) { want_D = 2; want_p = 11; }
     else if (desc->kind == DISTILL_MODEL_EXT_STROOP_A || desc->kind == DISTILL_MODEL_EXT_STROOP_B) { want_D = 2; want_p = 13; }
+    else if (desc->kind == DISTILL_MODEL_DDM_GRID) { want_D = 2; want_p = 7; }
     else return fail(DISTILL_E_UNSUPPORTED, "load_model: unknown model kind %u", desc->kind);
     if (desc->n_signals != want_D)
         return fail(DISTILL_E_UNSUPPORTED, "load_model: kind %u needs %u signals, got %u", desc->kind, want_D,
@@ -143,6 +144,11 @@ distill_status distill_load_model(const distill_model_desc* desc, int device, di
         const float ns = desc->params[10];
         if (!(ns >= 1.0f) || ns != std::floor(ns) || ns > 1e7f)
             return fail(DISTILL_E_INVALID_ARG, "load_model: Stroop n_steps must be a positive integer");
+    }
+    if (desc->kind == DISTILL_MODEL_DDM_GRID) {
+        const float ns = desc->params[6];
+        if (!(ns >= 1.0f) || ns != std::floor(ns) || ns > 1e7f)
+            return fail(DISTILL_E_INVALID_ARG, "load_model: DDM-grid n_steps must be a positive integer");
     }
     if (desc->kind == DISTILL_MODEL_EXT_STROOP_A || desc->kind == DISTILL_MODEL_EXT_STROOP_B) {
         for (int q : {3, 10}) {
@@ -335,9 +341,15 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
     if (reinterpret_cast<uintptr_t>(counts) & 7u) return fail(DISTILL_E_INVALID_ARG, "eval_grid: d_counts must be 8-byte aligned");
     CUDA_TRY(cudaMemsetAsync(counts, 0, count * 3 * sizeof(unsigned long long), st));
     StroopArgs p;
+    memset(&p, 0, sizeof p);
     const float* P = m->params.data();
-    p.g_c = P[0]; p.g_w = P[1]; p.tau = P[2]; p.leak = P[3]; p.inh = P[4]; p.noise = P[5];
-    p.dt = P[6]; p.thr = P[7]; p.reward = P[8]; p.rt_cost = P[9]; p.n_steps = (uint32_t)P[10];
+    const bool ddmg = m->kind == DISTILL_MODEL_DDM_GRID;
+    if (ddmg) {   // spec/MODELS.md §6c: A0, g_a, sigma, dt, R, c_rt, N — the finalize needs dt, R, c_rt, N
+        p.dt = P[3]; p.reward = P[4]; p.rt_cost = P[5]; p.n_steps = (uint32_t)P[6];
+    } else {
+        p.g_c = P[0]; p.g_w = P[1]; p.tau = P[2]; p.leak = P[3]; p.inh = P[4]; p.noise = P[5];
+        p.dt = P[6]; p.thr = P[7]; p.reward = P[8]; p.rt_cost = P[9]; p.n_steps = (uint32_t)P[10];
+    }
     p.w0 = m->w[0]; p.w1 = m->w[1];
     p.L0 = m->L[0]; p.L1 = m->L[1];
     p.n_trials = a->n_samples; p.trial_begin = tb; p.trial_end = te;
@@ -354,9 +366,18 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
             chunks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(chunks, c2));
         }
         const size_t table_bytes = 4ull * p.n_steps * sizeof(float);
+        DdmgArgs q;
+        if (ddmg) {
+            q.A0 = P[0]; q.g_a = P[1]; q.noise = P[2]; q.dt = P[3]; q.n_steps = (uint32_t)P[6];
+            q.L0 = m->L[0]; q.L1 = m->L[1]; q.n_trials = a->n_samples; q.trial_begin = tb; q.trial_end = te;
+            q.key0 = p.key0; q.key1 = p.key1; q.begin = p.begin; q.count = p.count;
+            q.levels = m->d_levels; q.counts = counts;
+        }
         for (uint64_t off = 0; off < count; off += 65535) {
             const unsigned gy = (unsigned)std::min<uint64_t>(65535, count - off);
-            if (table_bytes <= 48 * 1024)      // pathway table in shared memory (trial-invariant h_k(n))
+            if (ddmg)
+                ddmg_sim_kernel<DDM_BLOCK, DDM_MINB><<<dim3(chunks, gy), DDM_BLOCK, 0, st>>>(q, (uint32_t)off);
+            else if (table_bytes <= 48 * 1024)      // pathway table in shared memory (trial-invariant h_k(n))
                 stroop_sim_kernel<STROOP_BLOCK, STROOP_MINB, true><<<dim3(chunks, gy), STROOP_BLOCK, table_bytes, st>>>(
                     p, (uint32_t)off);
             else
@@ -474,7 +495,7 @@ distill_status distill_eval_grid(const distill_model* mc, const distill_eval_arg
     CUDA_TRY(cudaSetDevice(m->device));
     cudaStream_t st = (cudaStream_t)stream;
     if (m->kind == DISTILL_MODEL_PREDATOR_PREY) return launch_pp(m, a, st);
-    if (m->kind == DISTILL_MODEL_STROOP_LCA) return launch_stroop(m, a, st);
+    if (m->kind == DISTILL_MODEL_STROOP_LCA || m->kind == DISTILL_MODEL_DDM_GRID) return launch_stroop(m, a, st);
     return launch_ext_stroop(m, a, st);
 }
 

@@ -140,3 +140,18 @@ def test_binding_buffer_checks_on_cpu():
     with pytest.raises(ValueError):
         api._dev_ptr(t, "net", 4)
     assert set(api._BUF_DTYPE.values()) == {"float32", "int64", "int32"}
+
+
+def test_ddm_grid_model_validation_without_gpu(abi):
+    """Kind 5 (DDM control grid) needs 2 signals and 7 params with an integer step count."""
+    import ctypes as C
+    import numpy as np
+    L = abi.lib()
+    nl = np.array([3, 4], np.uint32)
+    lev = np.zeros(7, np.float32)
+    w = np.zeros(2, np.float32)
+    for params, want in ((np.zeros(6, np.float32), abi.E_INVALID_ARG),
+                         (np.array([0.2, 1.5, 1.0, 0.01, 1.0, 0.5, 0.5], np.float32), abi.E_INVALID_ARG)):
+        d = abi.ModelDesc(5, 2, abi._uptr(nl), abi._fptr(lev), abi._fptr(w), abi._fptr(params), params.size)
+        h = C.c_void_p()
+        assert L.distill_load_model(C.byref(d), 0, C.byref(h)) == want

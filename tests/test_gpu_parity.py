@@ -1015,3 +1015,29 @@ def test_lci_batch_bit_exact_and_fig3_clone(D, orc):
     d = W.DDMConfig(n_steps=500)
     for g, w in zip(run(d, 0, 20000, 5, (0.0, 0.0)), run(d, 0, 20000, 5, None)):
         assert np.array_equal(g, w)
+
+
+def test_ddm_grid_bit_exact(D, orc):
+    """DDM control grid (spec/MODELS.md §6c): counts, V and key bit-exact against
+    the oracle on a small grid (odd step count, trial sub-range), and sampled
+    allocations of the 100 x 100 bench grid with all 1e4 trials."""
+    import os
+    c = W.ddmg_grid(7, 300)
+    c.params = c.params.copy()
+    c.params[6] = 257
+    m = D.load_model(W.KIND_DDM_GRID, c.n_levels, c.levels, c.w, c.params, device=0)
+    cnt, net, key = _stroop_gpu(D, m, c, 0, c.n_alloc)
+    wc, wn = orc.ddmg_eval(c.n_levels, c.levels, c.w, c.params, 0, c.n_alloc, c.n_trials, c.seed, threads=8)
+    assert np.array_equal(cnt, wc)
+    assert np.array_equal(_bits(net), _bits(wn))
+    assert key == orc.argmax_net(wn)[0]
+    cnt2, _, _ = _stroop_gpu(D, m, c, 11, 40, trial_range=(13, 222))
+    wc2, _ = orc.ddmg_eval(c.n_levels, c.levels, c.w, c.params, 11, 40, c.n_trials, c.seed, 13, 222)
+    assert np.array_equal(cnt2, wc2)
+    g = W.ddmg_grid()
+    mg = D.load_model(W.KIND_DDM_GRID, g.n_levels, g.levels, g.w, g.params, device=0)
+    for b in (0, 5050, 9998):
+        cnt, net, _ = _stroop_gpu(D, mg, g, b, b + 2)
+        wc, wn = orc.ddmg_eval(g.n_levels, g.levels, g.w, g.params, b, b + 2, g.n_trials, g.seed,
+                               threads=os.cpu_count() or 8)
+        assert np.array_equal(cnt, wc) and np.array_equal(_bits(net), _bits(wn))

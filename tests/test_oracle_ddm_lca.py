@@ -253,3 +253,46 @@ def test_lci_batch_is_the_ddm_batch_at_zero_leak(orc):
     assert all(np.array_equal(a, b) for a, b in zip(ddm, lci))
     leaky = orc.ddm_batch(p, 13, 0, 600, lci=(1.5, 0.0))
     assert not np.array_equal(ddm[2], leaky[2])
+
+
+def test_ddm_grid_zero_noise_passage_and_value(orc):
+    """DDM control grid (spec/MODELS.md §6c): with zero noise, A = 1, dt = 0.01,
+    z = 1 every trial crosses at step 101 in binary32 (not 100; the DDM pin's
+    value); a negative drift gives errors at the same step; the value is the
+    correctly rounded binary64 formula of the integer counts."""
+    from fractions import Fraction as F
+    P = W.DDMG_PARAMS.copy()
+    P[0], P[1], P[2], P[3], P[6] = 0.0, 1.0, 0.0, 0.01, 300
+    for u in range(5):
+        assert orc.ddmg_trial(P, 1.0, 1.0, 3, u) == (1, 101)
+    P[0] = -2.0                                   # A = -2 + 1 = -1
+    assert orc.ddmg_trial(P, 1.0, 1.0, 3, 0) == (0, 101)
+    w = W.DDMG_W
+    for nc, nu, rs in [(0, 0, 0), (70, 3, 9000), (99, 0, 12345)]:
+        v = orc.ddmg_value(W.DDMG_PARAMS, w, 0.5, 0.75, 100, nc, nu, rs)
+        Q = W.DDMG_PARAMS
+        exact = (F(float(Q[4])) * nc / 100 - F(float(Q[5])) * F(float(Q[3])) * (rs + nu * 400) / 100
+                 - (F(float(w[0])) * F(1, 2) + F(float(w[1])) * F(3, 4)))
+        assert abs(F(float(v)) - exact) <= abs(exact) * F(1, 2 ** 23) + F(1, 2 ** 60)
+
+
+def test_ddm_grid_accuracy_and_decision_time_closed_forms(orc):
+    """Per allocation the grid's DDM has drift A = A0 + g_a u0 and threshold z = u1:
+    accuracy 1/(1 + exp(-2 A z'/sigma^2)) and decision time z' tanh(A z'/sigma^2)/A
+    with z' = z + 0.5826 sigma sqrt(dt) (Siegmund, as the DDM pin), for three
+    allocations; 2000 trials each, a horizon with no undecided trial."""
+    P = W.DDMG_PARAMS.copy()
+    P[6] = 3000
+    sig, dt = float(P[2]), float(P[3])
+    lev = np.array([0.0, 0.4, 1.0, 0.5, 1.0, 0.8], np.float32)      # u0 levels | u1 levels
+    counts, _ = orc.ddmg_eval((3, 3), lev, W.DDMG_W, P, 0, 9, 2000, 17, threads=8)
+    for i in (1, 5, 6):
+        u0, u1 = float(lev[i // 3]), float(lev[3 + i % 3])
+        A = float(np.float32(np.float32(P[1]) * np.float32(u0) + np.float32(P[0])))
+        zp = u1 + 0.5826 * sig * math.sqrt(dt)
+        nc, nu, rs = (int(v) for v in counts[i])
+        assert nu == 0
+        acc, acc_cf = nc / 2000, 1 / (1 + math.exp(-2 * A * zp / sig ** 2))
+        assert abs(acc - acc_cf) <= 4 * math.sqrt(acc_cf * (1 - acc_cf) / 2000) + 0.01, (i, acc, acc_cf)
+        dt_mc, dt_cf = rs / 2000 * dt, zp * math.tanh(A * zp / sig ** 2) / A
+        assert abs(dt_mc - dt_cf) <= 0.05 * dt_cf, (i, dt_mc, dt_cf)

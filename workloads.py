@@ -173,6 +173,20 @@ def stroop_small() -> StroopConfig:
     return StroopConfig("stroop_small_10x10x300", (10, 10), 300)
 
 
+# DDM control grid constants (spec/MODELS.md §6c): A0, g_a, sigma, dt, R, c_rt, N;
+# signals: attention u0 in [0, 1] (drift A = A0 + g_a u0), threshold u1 in [0.3, 1.5]
+DDMG_PARAMS = np.array([0.2, 1.5, 1.0, 0.01, 1.0, 0.5, 400.0], np.float32)
+DDMG_W = np.array([0.05, 0.05], np.float32)
+KIND_DDM_GRID = 5
+
+
+def ddmg_grid(L: int = 100, n_trials: int = 10_000) -> "StroopConfig":
+    """DDM control grid: L attention levels k/(L-1) x L thresholds 0.3 + 1.2 k/(L-1)."""
+    lev = np.concatenate([linear_levels(L), (0.3 + 1.2 * linear_levels(L)).astype(np.float32)]).astype(np.float32)
+    return StroopConfig(f"ddm_grid_{L}x{L}x{n_trials}", (L, L), n_trials, params=DDMG_PARAMS.copy(),
+                        w=DDMG_W.copy(), levels=lev)
+
+
 # Extended Stroop A/B constants (reading R26; spec/MODELS.md §10):
 # g_c, g_w, tau, N_h, lambda, a_p, gamma, sigma_d, dt_d, z_d, N_d, reward, rt_cost
 EXT_STROOP_PARAMS = np.array([1.0, 1.5, 0.1, 30.0, 2.0, 1.2, 0.8, 1.0, 0.01, 0.5, 100.0, 1.0, 0.2], np.float32)
