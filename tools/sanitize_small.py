@@ -50,6 +50,9 @@ def main():
     D.ddm_batch(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins, d.x_lo,
                 d.x_hi, 0, 700, 1, rh, rs, xh, lci=(0.5, 0.01))
     D.stroop_energy(ms, 3, c.n_trials, 1)
+    gd = W.ddmg_grid(4, 60)
+    mdg = D.load_model(W.KIND_DDM_GRID, gd.n_levels, gd.levels, gd.w, gd.params, device=0)
+    D.eval_grid(mdg, None, gd.n_trials, 1, net=sn[:gd.n_alloc], best=best)
     torch.cuda.synchronize()
     print("sanitize-small ok", int(best.item()), int(rh.sum()))
 
