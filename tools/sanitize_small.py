@@ -52,7 +52,7 @@ def main():
     D.stroop_energy(ms, 3, c.n_trials, 1)
     gd = W.ddmg_grid(4, 60)
     mdg = D.load_model(W.KIND_DDM_GRID, gd.n_levels, gd.levels, gd.w, gd.params, device=0)
-    D.eval_grid(mdg, None, gd.n_trials, 1, net=sn[:gd.n_alloc], best=best)
+    D.eval_grid(mdg, None, gd.n_trials, 1, net=torch.empty(gd.n_alloc, device="cuda"), best=best)
     torch.cuda.synchronize()
     print("sanitize-small ok", int(best.item()), int(rh.sum()))
 
