@@ -10,8 +10,11 @@ Public Python API (thin wrappers over the C ABI in include/distill.h):
     eval_grid_multi(model, d_inputs, n_invocations, n_samples, seed, ...)   # many invocations, one launch
     argmax(values, index_base, best) / argmax_ties(values, base, seed, t, best, tie)
     key_reset(best) / key_decode(key)
-    ddm_batch(...)
+    ddm_batch(..., lci=None | (leak, offset))      # DDM / leaky competing integrator batches
     stroop_energy(model, alloc, n_trials, seed)   # decision energy over time
+
+Model kinds: 1 predator-prey, 2 Stroop-LCA, 3/4 Extended Stroop A/B, 5 DDM
+control grid (workloads.KIND_*); eval_grid evaluates any of them.
     pp_episode(model, init, n_steps, n_samples, seed, ...)   # closed loop, on the device
     pp_amr(model, inputs, lo, hi, rounds, n_samples, seed)   # coarse-to-fine refinement
     shard_range(n, rank, world) / best_allreduce(key, group)   # multi-GPU plumbing
