@@ -40,6 +40,16 @@ def main():
     mx = D.load_model(W.KIND_EXT_STROOP_A, g.n_levels, g.levels, g.w, g.params, device=0)
     for _ in range(2):
         D.eval_grid(mx, None, g.n_trials, g.seed, 0, n, net=net, best=best, counts=counts)
+    if "--more" in sys.argv:   # the round's additions: DDM grid slice, LCI batch, energy trace
+        gd = W.ddmg_grid()
+        mg = D.load_model(W.KIND_DDM_GRID, gd.n_levels, gd.levels, gd.w, gd.params, device=0)
+        for _ in range(2):
+            D.eval_grid(mg, None, gd.n_trials, gd.seed, 0, n, net=net, best=best, counts=counts)
+        for _ in range(2):
+            D.ddm_batch(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
+                        d.x_lo, d.x_hi, 0, d.n_trials, d.seed, rh, rs, xh, lci=(0.5, 0.0))
+        for _ in range(2):
+            D.stroop_energy(m, 8083, c.n_trials, c.seed)
     torch.cuda.synchronize()
     print("ok", int(rh.sum()), float(net[0]))
 
