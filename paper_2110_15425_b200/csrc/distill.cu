@@ -375,6 +375,7 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
         }
         for (uint64_t off = 0; off < count; off += 65535) {
             const unsigned gy = (unsigned)std::min<uint64_t>(65535, count - off);
+            static_assert(DDM_BLOCK == STROOP_BLOCK, "the trial chunks above are sized for STROOP_BLOCK");
             if (ddmg)
                 ddmg_sim_kernel<DDM_BLOCK, DDM_MINB><<<dim3(chunks, gy), DDM_BLOCK, 0, st>>>(q, (uint32_t)off);
             else if (table_bytes <= 48 * 1024)      // pathway table in shared memory (trial-invariant h_k(n))
