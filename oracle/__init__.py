@@ -77,6 +77,7 @@ def _bind(path: str) -> C.CDLL:
         "od_stroop_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u64, u32, u32, u32, u64, C.c_void_p, C.c_void_p]),
         "od_stroop_value": (f32, [_f32p, _f32p, f32, f32, u32, u64, u64, u64]),
         "od_stroop_trial": (None, [_f32p, f32, f32, u64, u64, u32, C.POINTER(C.c_int), C.POINTER(u32)]),
+        "od_stroop_trace": (None, [_f32p, f32, f32, u64, u64, u32, C.POINTER(C.c_int), C.POINTER(u32), _f32p]),
         "od_ddmg_trial": (None, [_f32p, f32, f32, u64, u64, C.POINTER(C.c_int), C.POINTER(u32)]),
         "od_ddmg_value": (f32, [_f32p, _f32p, f32, f32, u32, u64, u64, u64]),
         "od_ddmg_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u64, u32, u32, u32, u64, C.c_void_p,
@@ -465,6 +466,15 @@ def stroop_trial(params, u_c, u_s, seed, unit, trial):
     r, st = C.c_int(), C.c_uint32()
     lib().od_stroop_trial(_f32(params), u_c, u_s, seed, unit, trial, C.byref(r), C.byref(st))
     return r.value, st.value
+
+
+def stroop_trace(params, u_c, u_s, seed, unit, trial):
+    """od_stroop_trace: (resp, step, states[N, 4] = (h0, h1, x0, x1) after each step)."""
+    P = _f32(params)
+    tr = np.zeros(4 * int(P[10]), np.float32)
+    r, st = C.c_int(), C.c_uint32()
+    lib().od_stroop_trace(P, u_c, u_s, seed, unit, trial, C.byref(r), C.byref(st), tr)
+    return r.value, st.value, tr.reshape(-1, 4)
 
 
 def stroop_value(params, w, u_c, u_s, n_trials, n_correct, n_undecided, rt_sum):

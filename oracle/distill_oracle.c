@@ -511,9 +511,13 @@ int od_lci_batch(const od_ddm_params* p, float leak, float offset, uint64_t seed
 enum { SP_GC, SP_GW, SP_TAU, SP_LEAK, SP_INH, SP_NOISE, SP_DT, SP_THR, SP_R, SP_CRT, SP_N };
 
 /* One Stroop-LCA trial (spec/MODELS.md §6); if esum is non-NULL, also the
- * decision-energy trace of §6b: esum[n-1] += llrint(x0(n) * x1(n) * 2^24). */
+ * decision-energy trace of §6b: esum[n-1] += llrint(x0(n) * x1(n) * 2^24);
+ * if trace is non-NULL, the states after each step n: trace[4(n-1) ..] =
+ * (h0, h1, x0, x1) (test infrastructure: the closed-form pins of the
+ * pathway and response layers read it). */
 static void stroop_trial_core(const float P[11], float u_c, float u_s, uint64_t seed,
-                              uint64_t unit, uint32_t trial, int* resp, uint32_t* step, int64_t* esum) {
+                              uint64_t unit, uint32_t trial, int* resp, uint32_t* step, int64_t* esum,
+                              float* trace) {
     uint32_t kind = trial % 3, color = (trial / 3) % 2;
     int word = (kind == 0) ? (int)color : (kind == 1) ? (int)(1 - color) : -1;
     float ic = FMUL(P[SP_GC], u_c);
@@ -540,6 +544,10 @@ static void stroop_trial_core(const float P[11], float u_c, float u_s, uint64_t 
             xn[k] = fmaxf(y, 0.0f);
         }
         x[0] = xn[0]; x[1] = xn[1];
+        if (trace) {
+            trace[4 * (n - 1)] = h[0]; trace[4 * (n - 1) + 1] = h[1];
+            trace[4 * (n - 1) + 2] = x[0]; trace[4 * (n - 1) + 3] = x[1];
+        }
         if (esum) esum[n - 1] += llrintf(FMUL(FMUL(x[0], x[1]), 0x1p24f));   /* exact scaling; round to nearest even */
         if (r < 0) {
             if (x[0] >= P[SP_THR]) { r = 0; st = n; }
@@ -551,7 +559,13 @@ static void stroop_trial_core(const float P[11], float u_c, float u_s, uint64_t 
 
 void od_stroop_trial(const float P[11], float u_c, float u_s, uint64_t seed,
                      uint64_t unit, uint32_t trial, int* resp, uint32_t* step) {
-    stroop_trial_core(P, u_c, u_s, seed, unit, trial, resp, step, NULL);
+    stroop_trial_core(P, u_c, u_s, seed, unit, trial, resp, step, NULL, NULL);
+}
+
+/* The same trial with its per-step states (h0, h1, x0, x1) written to trace[4N]. */
+void od_stroop_trace(const float P[11], float u_c, float u_s, uint64_t seed,
+                     uint64_t unit, uint32_t trial, int* resp, uint32_t* step, float* trace) {
+    stroop_trial_core(P, u_c, u_s, seed, unit, trial, resp, step, NULL, trace);
 }
 
 /* spec/MODELS.md §6b: decision-energy trace of allocation i (u_c, u_s) over
@@ -561,7 +575,7 @@ void od_stroop_energy(const float P[11], float u_c, float u_s, uint64_t seed, ui
     for (uint32_t j = t0; j < t1; ++j) {
         int resp;
         uint32_t st;
-        stroop_trial_core(P, u_c, u_s, seed, i * (uint64_t)n_trials + j, j, &resp, &st, esum);
+        stroop_trial_core(P, u_c, u_s, seed, i * (uint64_t)n_trials + j, j, &resp, &st, esum, NULL);
     }
 }
 

@@ -130,6 +130,9 @@ void od_stroop_energy(const float params[11], float u_c, float u_s, uint64_t see
                       uint32_t t0, uint32_t t1, int64_t* esum);
 void od_stroop_trial(const float params[11], float u_c, float u_s, uint64_t seed,
                      uint64_t unit, uint32_t trial, int* resp, uint32_t* step);
+/* od_stroop_trial with the states after each step: trace[4(n-1) + (0..3)] = (h0, h1, x0, x1). */
+void od_stroop_trace(const float P[11], float u_c, float u_s, uint64_t seed,
+                     uint64_t unit, uint32_t trial, int* resp, uint32_t* step, float* trace);
 
 /* ---- closed-loop predator-prey episode (spec/MODELS.md §7) ---- */
 /* traj[(n_steps+1)*6], keys[n_steps], status[2] = {outcome, steps}; speeds = {v_player, v_prey, v_predator} */

@@ -19,11 +19,27 @@ import threading as _threading
 _INIT_LOCK = _threading.Lock()
 
 
-def _stream_handle(stream) -> Optional[int]:
+def _stream_handle(stream, device: Optional[int] = None) -> Optional[int]:
     import torch
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
     return stream.cuda_stream
+
+
+def _on_device(t):
+    """The library's model-less entries launch on the current device: make it the tensor's."""
+    import contextlib
+    import torch
+    return torch.cuda.device(t.device) if getattr(t, "is_cuda", False) else contextlib.nullcontext()
+
+
+def _on_stream(stream):
+    """Context for library-side temporaries: allocate (and zero) them on the
+    stream the kernels run on, so the caching allocator cannot hand their memory
+    to another stream while those kernels still use it."""
+    import contextlib
+    import torch
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
 
 
 # element type each named buffer must have (the C ABI's float* / u64* / int*);
@@ -101,12 +117,16 @@ def eval_grid(model: Model, inputs, n_samples: int, seed: int, begin: int = 0, e
     a.n_samples, a.invocation, a.seed = int(n_samples), int(invocation), int(seed) & (2 ** 64 - 1)
     a.d_net = _dev_ptr(net, "net", n)
     a.d_best = _dev_ptr(best, "best", 1)
+    a.trial_begin, a.trial_end = int(trial_range[0]), int(trial_range[1])
     if counts is None and model.kind != _abi.MODEL_PREDATOR_PREY:
         import torch
-        counts = torch.empty(3 * max(n, 1), dtype=torch.int64, device=torch.device("cuda", model.device))
+        with _on_stream(stream):      # freed on return: stream-ordered reuse only
+            counts = torch.empty(3 * max(n, 1), dtype=torch.int64, device=torch.device("cuda", model.device))
+            a.d_counts = _dev_ptr(counts, "counts", 3 * n)
+            check(lib().distill_eval_grid(model.handle, C.byref(a), _stream_handle(stream, model.device)))
+        return
     a.d_counts = _dev_ptr(counts, "counts", 3 * n)
-    a.trial_begin, a.trial_end = int(trial_range[0]), int(trial_range[1])
-    check(lib().distill_eval_grid(model.handle, C.byref(a), _stream_handle(stream)))
+    check(lib().distill_eval_grid(model.handle, C.byref(a), _stream_handle(stream, model.device)))
 
 
 def grid_search(model: Model, inputs, n_samples: int, seed: int, shard=None, invocation: int = 0, stream=None):
@@ -119,8 +139,9 @@ def grid_search(model: Model, inputs, n_samples: int, seed: int, shard=None, inv
     from .dist import shard_range
     b, e = (0, model.n_alloc) if shard is None else shard_range(model.n_alloc, int(shard[0]), int(shard[1]))
     dev = torch.device("cuda", model.device)
-    net = torch.empty(max(e - b, 1), dtype=torch.float32, device=dev)
-    key = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    with _on_stream(stream):
+        net = torch.empty(max(e - b, 1), dtype=torch.float32, device=dev)
+        key = torch.full((1,), -1, dtype=torch.int64, device=dev)
     eval_grid(model, inputs, n_samples, seed, b, e, net=net, best=key, invocation=invocation, stream=stream)
     return net[:e - b], key
 
@@ -148,7 +169,7 @@ def eval_grid_multi(model: Model, inputs, n_invocations: int, n_samples: int, se
     a = _abi.MultiArgs(_dev_ptr(inputs, "inputs"), int(inputs.shape[0]), T, int(invocation0), int(n_samples),
                        int(begin), end, int(seed) & (2 ** 64 - 1), _dev_ptr(net, "net", T * n),
                        _dev_ptr(best, "best", T))
-    check(lib().distill_eval_grid_multi(model.handle, C.byref(a), _stream_handle(stream)))
+    check(lib().distill_eval_grid_multi(model.handle, C.byref(a), _stream_handle(stream, model.device)))
 
 
 def eval_grid_host(model: Model, inputs, n_samples: int, seed: int, begin: int = 0, end: Optional[int] = None,
@@ -175,7 +196,7 @@ def eval_grid_host(model: Model, inputs, n_samples: int, seed: int, begin: int =
     with model._h_key_lock:
         check(lib().distill_eval_grid_host(model.handle, _abi._fptr(inp), inp.size, int(begin), end,
                                            int(n_samples), int(invocation), int(seed) & (2 ** 64 - 1), net_ptr,
-                                           C.cast(key_ptr, C.POINTER(C.c_uint64)), _stream_handle(stream)))
+                                           C.cast(key_ptr, C.POINTER(C.c_uint64)), _stream_handle(stream, model.device)))
         return int(model._h_key[0]) & (2 ** 64 - 1)
 
 
@@ -184,29 +205,33 @@ def stroop_energy(model: Model, alloc: int, n_trials: int, seed: int, trial_rang
     one Stroop-LCA allocation (int64 CUDA tensor [N], accumulated; zeroed if allocated here)."""
     import torch
     N = int(model.params[10])
-    if esum is None:
-        esum = torch.zeros(N, dtype=torch.int64, device=torch.device("cuda", model.device))
+    if esum is None:                  # zeroed on the kernel's stream (ordered before it)
+        with _on_stream(stream):
+            esum = torch.zeros(N, dtype=torch.int64, device=torch.device("cuda", model.device))
     t0, t1 = (0, int(n_trials)) if trial_range is None else (int(trial_range[0]), int(trial_range[1]))
     check(lib().distill_stroop_energy(model.handle, int(alloc), int(n_trials), t0, t1, int(seed) & (2 ** 64 - 1),
-                                      _dev_ptr(esum, "esum", N), _stream_handle(stream)))
+                                      _dev_ptr(esum, "esum", N), _stream_handle(stream, model.device)))
     return esum
 
 
 def argmax(values, index_base: int, best, stream=None) -> None:
     """distill_argmax: atomicMin of key(-values[j], index_base + j) into best."""
-    check(lib().distill_argmax(_dev_ptr(values, "values"), values.numel(), int(index_base),
-                               _dev_ptr(best, "best", 1), _stream_handle(stream)))
+    with _on_device(values):
+        check(lib().distill_argmax(_dev_ptr(values, "values"), values.numel(), int(index_base),
+                                   _dev_ptr(best, "best", 1), _stream_handle(stream, values.device.index)))
 
 
 def argmax_ties(values, index_base: int, seed: int, invocation: int, best, tie, stream=None) -> None:
     """distill_argmax_ties: random tie-break among the minimal costs (spec/MODELS.md §8)."""
-    check(lib().distill_argmax_ties(_dev_ptr(values, "values"), values.numel(), int(index_base),
-                                    int(seed) & (2 ** 64 - 1), int(invocation), _dev_ptr(best, "best", 1),
-                                    _dev_ptr(tie, "tie", 1), _stream_handle(stream)))
+    with _on_device(values):
+        check(lib().distill_argmax_ties(_dev_ptr(values, "values"), values.numel(), int(index_base),
+                                        int(seed) & (2 ** 64 - 1), int(invocation), _dev_ptr(best, "best", 1),
+                                        _dev_ptr(tie, "tie", 1), _stream_handle(stream, values.device.index)))
 
 
 def key_reset(best, stream=None) -> None:
-    check(lib().distill_key_reset(_dev_ptr(best, "best", 1), _stream_handle(stream)))
+    with _on_device(best):
+        check(lib().distill_key_reset(_dev_ptr(best, "best", 1), _stream_handle(stream, best.device.index)))
 
 
 def key_decode(key: int):
@@ -227,20 +252,23 @@ def ddm_batch(drift, noise, threshold, x0, dt, n_steps, rt_bin_steps, n_x_bins, 
     nb = (int(n_steps) + int(rt_bin_steps) - 1) // int(rt_bin_steps)
     if rt_hist.numel() < 2 * nb + 1 or x_hist.numel() < int(n_x_bins) + 2:
         raise ValueError("histogram buffers too small")
-    if lci is None:
-        check(lib().distill_ddm_batch(C.byref(a), _stream_handle(stream)))
-    else:                                   # distill_lci_batch: drift is the input I, lci = (leak, offset)
-        check(lib().distill_lci_batch(C.byref(a), float(lci[0]), float(lci[1]), _stream_handle(stream)))
+    with _on_device(rt_hist):
+        if lci is None:
+            check(lib().distill_ddm_batch(C.byref(a), _stream_handle(stream, rt_hist.device.index)))
+        else:                               # distill_lci_batch: drift is the input I, lci = (leak, offset)
+            check(lib().distill_lci_batch(C.byref(a), float(lci[0]), float(lci[1]),
+                                          _stream_handle(stream, rt_hist.device.index)))
 
 
 def _episode_args(model: Model, init, n_steps: int, n_samples: int, seed: int, speeds, capture_radius,
-                  traj, keys, status):
+                  traj, keys, status, stream=None):
     import torch
     dev = torch.device("cuda", model.device)
     T = int(n_steps)
-    traj = torch.empty((T + 1, 6), dtype=torch.float32, device=dev) if traj is None else traj
-    keys = torch.empty(T, dtype=torch.int64, device=dev) if keys is None else keys
-    status = torch.empty(2, dtype=torch.int32, device=dev) if status is None else status
+    with _on_stream(stream):
+        traj = torch.empty((T + 1, 6), dtype=torch.float32, device=dev) if traj is None else traj
+        keys = torch.empty(T, dtype=torch.int64, device=dev) if keys is None else keys
+        status = torch.empty(2, dtype=torch.int32, device=dev) if status is None else status
     init_arr = None if init is None else np.ascontiguousarray(np.asarray(init, np.float32))
     a = _abi.EpisodeArgs(T, int(n_samples), int(seed) & (2 ** 64 - 1), float(speeds[0]), float(speeds[1]),
                          float(speeds[2]), float(capture_radius),
@@ -259,17 +287,17 @@ class EpisodeRun:
                  capture_radius: float = 0.5, traj=None, keys=None, status=None, stream=None):
         self.model, self.stream = model, stream
         self._a, self._init, self.traj, self.keys, self.status = _episode_args(
-            model, init, n_steps, n_samples, seed, speeds, capture_radius, traj, keys, status)
-        check(lib().distill_pp_episode_begin(model.handle, C.byref(self._a), _stream_handle(stream)))
+            model, init, n_steps, n_samples, seed, speeds, capture_radius, traj, keys, status, stream)
+        check(lib().distill_pp_episode_begin(model.handle, C.byref(self._a), _stream_handle(stream, model.device)))
 
     def search(self, t: int, begin: int = 0, end: Optional[int] = None) -> None:
         end = self.model.n_alloc if end is None else int(end)
         check(lib().distill_pp_episode_search(self.model.handle, C.byref(self._a), int(t), int(begin), end,
-                                              _stream_handle(self.stream)))
+                                              _stream_handle(self.stream, self.model.device)))
 
     def advance(self, t: int) -> None:
         check(lib().distill_pp_episode_advance(self.model.handle, C.byref(self._a), int(t),
-                                               _stream_handle(self.stream)))
+                                               _stream_handle(self.stream, self.model.device)))
 
 
 def pp_episode(model: Model, init, n_steps: int, n_samples: int, seed: int, speeds=(1.0, 0.8, 0.6),
@@ -279,19 +307,20 @@ def pp_episode(model: Model, init, n_steps: int, n_samples: int, seed: int, spee
     Returns (traj[(T+1),6] float32, keys[T] int64 raw key bits, status[2] int32) CUDA tensors.
     If `init` is None, traj[0] must already hold the initial positions."""
     a, _keep, traj, keys, status = _episode_args(model, init, n_steps, n_samples, seed, speeds, capture_radius,
-                                                 traj, keys, status)
-    check(lib().distill_pp_episode(model.handle, C.byref(a), _stream_handle(stream)))
+                                                 traj, keys, status, stream)
+    check(lib().distill_pp_episode(model.handle, C.byref(a), _stream_handle(stream, model.device)))
     return traj, keys, status
 
 
 def _amr_args(model: Model, inputs, lo, hi, rounds: int, n_samples: int, seed: int, invocation0: int,
-              keys, boxes, levels):
+              keys, boxes, levels, stream=None):
     import torch
     dev = torch.device("cuda", model.device)
     R = int(rounds)
-    keys = torch.empty(R, dtype=torch.int64, device=dev) if keys is None else keys
-    boxes = torch.empty((R + 1, 3, 2), dtype=torch.float32, device=dev) if boxes is None else boxes
-    levels = torch.empty(int(model.n_levels.sum()), dtype=torch.float32, device=dev) if levels is None else levels
+    with _on_stream(stream):
+        keys = torch.empty(R, dtype=torch.int64, device=dev) if keys is None else keys
+        boxes = torch.empty((R + 1, 3, 2), dtype=torch.float32, device=dev) if boxes is None else boxes
+        levels = torch.empty(int(model.n_levels.sum()), dtype=torch.float32, device=dev) if levels is None else levels
     inp = np.ascontiguousarray(np.asarray(inputs, np.float32))
     a = _abi.AmrArgs(_abi._fptr(inp), inp.size, (C.c_float * 3)(*[float(x) for x in lo]),
                      (C.c_float * 3)(*[float(x) for x in hi]), R, int(n_samples), int(invocation0),
@@ -306,8 +335,8 @@ def pp_amr(model: Model, inputs, lo, hi, rounds: int, n_samples: int, seed: int,
 
     Returns (keys[R] int64 raw key bits, boxes[R+1, 3, 2] float32) CUDA tensors."""
     a, _keep, keys, boxes, levels = _amr_args(model, inputs, lo, hi, rounds, n_samples, seed, invocation0,
-                                              keys, boxes, levels)
-    check(lib().distill_pp_amr(model.handle, C.byref(a), _stream_handle(stream)))
+                                              keys, boxes, levels, stream)
+    check(lib().distill_pp_amr(model.handle, C.byref(a), _stream_handle(stream, model.device)))
     return keys, boxes
 
 
@@ -320,19 +349,19 @@ class AmrRun:
                  invocation0: int = 0, stream=None):
         self.model, self.stream = model, stream
         self._a, self._inp, self.keys, self.boxes, self.levels = _amr_args(
-            model, inputs, lo, hi, rounds, n_samples, seed, invocation0, None, None, None)
-        check(lib().distill_pp_amr_begin(model.handle, C.byref(self._a), _stream_handle(stream)))
+            model, inputs, lo, hi, rounds, n_samples, seed, invocation0, None, None, None, stream)
+        check(lib().distill_pp_amr_begin(model.handle, C.byref(self._a), _stream_handle(stream, model.device)))
 
     def levels_for(self, r: int) -> None:
-        check(lib().distill_pp_amr_levels(self.model.handle, C.byref(self._a), int(r), _stream_handle(self.stream)))
+        check(lib().distill_pp_amr_levels(self.model.handle, C.byref(self._a), int(r), _stream_handle(self.stream, self.model.device)))
 
     def search(self, r: int, begin: int = 0, end: Optional[int] = None) -> None:
         end = self.model.n_alloc if end is None else int(end)
         check(lib().distill_pp_amr_search(self.model.handle, C.byref(self._a), int(r), int(begin), end,
-                                          _stream_handle(self.stream)))
+                                          _stream_handle(self.stream, self.model.device)))
 
     def refine(self, r: int) -> None:
-        check(lib().distill_pp_amr_refine(self.model.handle, C.byref(self._a), int(r), _stream_handle(self.stream)))
+        check(lib().distill_pp_amr_refine(self.model.handle, C.byref(self._a), int(r), _stream_handle(self.stream, self.model.device)))
 
 
 def sm_clock_mhz(micros: int = 200, stream=None) -> float:

@@ -45,6 +45,30 @@ distill_status fail(distill_status s, const char* fmt, ...) {
                         __LINE__);                                                              \
     } while (0)
 
+// Scoped device selection: every entry that works on a model's device
+// restores the caller's current device on return (the library never leaves
+// the calling thread on another device).
+struct DeviceScope {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceScope(int dev) {
+        int cur = -1;
+        err = cudaGetDevice(&cur);
+        if (err == cudaSuccess && cur != dev) {
+            err = cudaSetDevice(dev);
+            if (err == cudaSuccess) prev = cur;
+        }
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceScope(const DeviceScope&) = delete;
+    DeviceScope& operator=(const DeviceScope&) = delete;
+};
+#define DEVICE_SCOPE(dev)         \
+    DeviceScope device_scope_(dev); \
+    CUDA_TRY(device_scope_.err)
+
 constexpr int PP_BLOCK = 128;
 constexpr int ARGMAX_BLOCK = 256;
 // sample / trial loops step a 32-bit counter by up to 2 (PP pairs) or a grid
@@ -171,7 +195,8 @@ distill_status distill_load_model(const distill_model_desc* desc, int device, di
         m->w[d] = desc->cost_weights[d];
     }
     m->params.assign(desc->params, desc->params + desc->n_params);
-    cudaError_t e = cudaSetDevice(device);
+    DeviceScope scope(device);
+    cudaError_t e = scope.err;
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&m->n_sm, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaMalloc(&m->d_levels, total * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(m->d_levels, desc->levels, total * sizeof(float), cudaMemcpyHostToDevice);
@@ -186,7 +211,7 @@ distill_status distill_load_model(const distill_model_desc* desc, int device, di
 
 void distill_free_model(distill_model* m) {
     if (!m) return;
-    cudaSetDevice(m->device);
+    DeviceScope scope(m->device);
     if (m->d_levels) cudaFree(m->d_levels);
     if (m->d_scratch) cudaFree(m->d_scratch);
     delete m;
@@ -310,7 +335,7 @@ distill_status distill_eval_grid_multi(const distill_model* m, const distill_mul
         return fail(DISTILL_E_OVERFLOW, "eval_grid_multi: invocation counter overflow");
     const uint64_t count = a->end - a->begin;
     if (count == 0 || a->n_invocations == 0) return DISTILL_OK;
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     PPArgs p = pp_base_args(m, a->n_samples, a->seed);   // positions come from d_inputs
     p.invocation = a->invocation0;
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
@@ -419,6 +444,7 @@ distill_status distill_stroop_energy(const distill_model* m, uint64_t alloc, uin
                                      uint32_t trial_begin, uint32_t trial_end, uint64_t seed,
                                      unsigned long long* d_esum, void* stream) {
     if (!m || !d_esum) return fail(DISTILL_E_INVALID_ARG, "stroop_energy: NULL model/d_esum");
+    if (reinterpret_cast<uintptr_t>(d_esum) & 7u) return fail(DISTILL_E_INVALID_ARG, "stroop_energy: d_esum must be 8-byte aligned");
     if (m->kind != DISTILL_MODEL_STROOP_LCA) return fail(DISTILL_E_UNSUPPORTED, "stroop_energy: Stroop-LCA models only");
     if (alloc >= m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "stroop_energy: allocation index past the grid");
     if (n_trials == 0 || n_trials > MAX_SAMPLES || trial_begin > trial_end || trial_end > n_trials)
@@ -427,7 +453,7 @@ distill_status distill_stroop_energy(const distill_model* m, uint64_t alloc, uin
     const uint32_t N = (uint32_t)m->params[10];
     if (N > 4096) return fail(DISTILL_E_UNSUPPORTED, "stroop_energy: at most 4096 steps");
     if (trial_begin == trial_end) return DISTILL_OK;
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     StroopArgs p;
     memset(&p, 0, sizeof p);
     const float* P = m->params.data();
@@ -493,7 +519,7 @@ distill_status distill_eval_grid(const distill_model* mc, const distill_eval_arg
         return fail(DISTILL_E_INVALID_ARG, "eval_grid: d_net must be 4-byte aligned");
     if (a->d_best && (reinterpret_cast<uintptr_t>(a->d_best) & 7u))
         return fail(DISTILL_E_INVALID_ARG, "eval_grid: d_best must be 8-byte aligned");
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     cudaStream_t st = (cudaStream_t)stream;
     if (m->kind == DISTILL_MODEL_PREDATOR_PREY) return launch_pp(m, a, st);
     if (m->kind == DISTILL_MODEL_STROOP_LCA || m->kind == DISTILL_MODEL_DDM_GRID) return launch_stroop(m, a, st);
@@ -508,7 +534,7 @@ distill_status distill_eval_grid_host(const distill_model* mc, const float* h_in
     if (m->kind != DISTILL_MODEL_PREDATOR_PREY)
         return fail(DISTILL_E_UNSUPPORTED, "eval_grid_host: predator-prey models only");
     if (begin > end || end > m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "eval_grid_host: bad range");
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     std::lock_guard<std::mutex> lock(m->scratch_mu);
     const uint64_t count = end - begin;
     const size_t net_off = 256;
@@ -607,7 +633,7 @@ static void episode_advance(const distill_model* m, const distill_episode_args* 
 distill_status distill_pp_episode_begin(const distill_model* m, const distill_episode_args* e, void* stream) {
     distill_status s = episode_check(m, e, "pp_episode_begin");
     if (s != DISTILL_OK) return s;
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     cudaStream_t st = (cudaStream_t)stream;
     if (e->h_init) CUDA_TRY(cudaMemcpyAsync(e->d_traj, e->h_init, 6 * sizeof(float), cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemsetAsync(e->d_keys, 0xFF, e->n_steps * sizeof(unsigned long long), st));
@@ -622,7 +648,7 @@ distill_status distill_pp_episode_search(const distill_model* m, const distill_e
     if (t >= e->n_steps) return fail(DISTILL_E_INVALID_ARG, "pp_episode_search: step t >= n_steps");
     if (begin > end || end > m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "pp_episode_search: bad shard");
     if (begin == end) return DISTILL_OK;
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     episode_search(m, e, episode_pp_args(m, e), t, begin, end, (cudaStream_t)stream);
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;
@@ -633,7 +659,7 @@ distill_status distill_pp_episode_advance(const distill_model* m, const distill_
     distill_status s = episode_check(m, e, "pp_episode_advance");
     if (s != DISTILL_OK) return s;
     if (t >= e->n_steps) return fail(DISTILL_E_INVALID_ARG, "pp_episode_advance: step t >= n_steps");
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     episode_advance(m, e, episode_pp_args(m, e), t, (cudaStream_t)stream);
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;
@@ -692,7 +718,7 @@ static void amr_search(const distill_model* m, const distill_amr_args* g, PPArgs
 distill_status distill_pp_amr_begin(const distill_model* m, const distill_amr_args* g, void* stream) {
     distill_status s = amr_check(m, g, "pp_amr_begin");
     if (s != DISTILL_OK) return s;
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     CUDA_TRY(cudaMemsetAsync(g->d_keys, 0xFF, g->rounds * sizeof(unsigned long long), (cudaStream_t)stream));
     return DISTILL_OK;
 }
@@ -701,7 +727,7 @@ distill_status distill_pp_amr_levels(const distill_model* m, const distill_amr_a
     distill_status s = amr_check(m, g, "pp_amr_levels");
     if (s != DISTILL_OK) return s;
     if (r >= g->rounds) return fail(DISTILL_E_INVALID_ARG, "pp_amr_levels: round r >= rounds");
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     amr_levels_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(amr_args(m, g), r);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
@@ -715,7 +741,7 @@ distill_status distill_pp_amr_search(const distill_model* m, const distill_amr_a
     if (r >= g->rounds) return fail(DISTILL_E_INVALID_ARG, "pp_amr_search: round r >= rounds");
     if (begin > end || end > m->n_alloc) return fail(DISTILL_E_INVALID_ARG, "pp_amr_search: bad shard");
     if (begin == end) return DISTILL_OK;
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     amr_search(m, g, amr_pp_args(m, g), r, begin, end, (cudaStream_t)stream);
     CUDA_TRY(cudaGetLastError());
     return DISTILL_OK;
@@ -725,7 +751,7 @@ distill_status distill_pp_amr_refine(const distill_model* m, const distill_amr_a
     distill_status s = amr_check(m, g, "pp_amr_refine");
     if (s != DISTILL_OK) return s;
     if (r >= g->rounds) return fail(DISTILL_E_INVALID_ARG, "pp_amr_refine: round r >= rounds");
-    CUDA_TRY(cudaSetDevice(m->device));
+    DEVICE_SCOPE(m->device);
     amr_refine_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(amr_args(m, g), r);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
@@ -825,6 +851,9 @@ static distill_status launch_integrator(const distill_ddm_args* a, float leak, f
                                         const char* who) {
     if (!a || !a->d_rt_hist || !a->d_rt_sum || !a->d_x_hist)
         return fail(DISTILL_E_INVALID_ARG, "%s: NULL argument", who);
+    if ((reinterpret_cast<uintptr_t>(a->d_rt_hist) | reinterpret_cast<uintptr_t>(a->d_rt_sum) |
+         reinterpret_cast<uintptr_t>(a->d_x_hist)) & 7u)
+        return fail(DISTILL_E_INVALID_ARG, "%s: histogram buffers must be 8-byte aligned", who);
     if (a->n_steps == 0 || a->rt_bin_steps == 0 || a->n_x_bins == 0)
         return fail(DISTILL_E_INVALID_ARG, "%s: n_steps, rt_bin_steps, n_x_bins must be >= 1", who);
     if (!(a->x_lo < a->x_hi) || !(a->dt >= 0.0f)) return fail(DISTILL_E_INVALID_ARG, "%s: bad x range / dt", who);

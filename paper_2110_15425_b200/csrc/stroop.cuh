@@ -323,9 +323,9 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
         // Six steps (12 normals) per group; each DDM's latch is tested once per
         // group on max |x| (|x| >= z <=> x >= z or x <= -z, DDM kernel).
         const uint32_t n6 = a.n_d / 6;
-        for (uint32_t j = 0; j < n6; ++j) {
+        for (uint32_t grp = 0; grp < n6; ++grp) {
             float g[12], y1[6], y2[6];
-            acc_normals12(rng, j, g);
+            acc_normals12(rng, grp, g);
 #pragma unroll
             for (int l = 0; l < 6; ++l) {
                 if (VARIANT == 0) {
@@ -342,11 +342,11 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
             for (int l = 1; l < 6; ++l) { m1 = fmaxf(m1, fabsf(y1[l])); m2 = fmaxf(m2, fabsf(y2[l])); }
             if (!h1t && m1 >= a.z) {
 #pragma unroll
-                for (int l = 0; l < 6; ++l) ddm_latch(y1[l], a.z, 6 * j + l + 1, h1t, s1);
+                for (int l = 0; l < 6; ++l) ddm_latch(y1[l], a.z, 6 * grp + l + 1, h1t, s1);
             }
             if (!h2t && m2 >= a.z) {
 #pragma unroll
-                for (int l = 0; l < 6; ++l) ddm_latch(y2[l], a.z, 6 * j + l + 1, h2t, s2);
+                for (int l = 0; l < 6; ++l) ddm_latch(y2[l], a.z, 6 * grp + l + 1, h2t, s2);
             }
         }
         const uint32_t rem = a.n_d - 6 * n6;

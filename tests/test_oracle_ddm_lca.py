@@ -296,3 +296,144 @@ def test_ddm_grid_accuracy_and_decision_time_closed_forms(orc):
         assert abs(acc - acc_cf) <= 4 * math.sqrt(acc_cf * (1 - acc_cf) / 2000) + 0.01, (i, acc, acc_cf)
         dt_mc, dt_cf = rs / 2000 * dt, zp * math.tanh(A * zp / sig ** 2) / A
         assert abs(dt_mc - dt_cf) <= 0.05 * dt_cf, (i, dt_mc, dt_cf)
+
+
+# ---------------------------------------------------------------------------
+# Stroop-LCA closed forms with leak != inhibition, both nonzero, and tau < 1
+# (spec/MODELS.md §6; the LCA of P:466, the Botvinick Stroop model of P:525).
+#
+# Pathway: h_k(n) = I_k (1 - (1 - tau)^n)  (h_k(0) = 0).
+# Response layer, while neither unit is rectified:
+#   x(n) = M x(n-1) + dt h(n),  M = [[1 - dt lam, -dt beta], [-dt beta, 1 - dt lam]]
+# diagonalised on (1, 1) and (1, -1): s = x0 + x1 and d = x0 - x1 follow
+#   s(n) = a_s s(n-1) + dt (h0 + h1)(n),  a_s = 1 - dt (lam + beta)
+#   d(n) = a_d d(n-1) + dt (h0 - h1)(n),  a_d = 1 - dt (lam - beta)
+# so with r = 1 - tau:  s(n) = dt (I0 + I1) G(a_s, n),  d(n) = dt (I0 - I1) G(a_d, n),
+#   G(a, n) = sum_{m=1..n} a^{n-m} (1 - r^m) = (1 - a^n)/(1 - a) - r (a^n - r^n)/(a - r).
+# With noise, the same linear system is an AR(1) pair: E[s], E[d] as above and
+#   Var s(n) = Var d(n) = 2 nsd^2 (1 - a^{2n}) / (1 - a^2)  (a = a_s resp. a_d),
+#   Cov(s, d) = 0  (the two unit noises are independent with equal variance).
+# ---------------------------------------------------------------------------
+_LAM, _BETA, _TAU, _DT = 0.4, 0.15, 0.3, 0.05
+
+
+def _stroop_params(gc, gw, tau, lam, beta, sig, dt, theta, N):
+    P = W.STROOP_PARAMS.copy()
+    P[0], P[1], P[2], P[3], P[4], P[5], P[6], P[7], P[10] = gc, gw, tau, lam, beta, sig, dt, theta, N
+    return P
+
+
+def _G(a, r, n):
+    n = np.asarray(n, np.float64)
+    return (1 - a ** n) / (1 - a) - r * (a ** n - r ** n) / (a - r)
+
+
+def _lca_closed_form(I0, I1, tau, lam, beta, dt, n):
+    r = 1.0 - tau
+    a_s, a_d = 1 - dt * (lam + beta), 1 - dt * (lam - beta)
+    s = dt * (I0 + I1) * _G(a_s, r, n)
+    d = dt * (I0 - I1) * _G(a_d, r, n)
+    h0, h1 = I0 * (1 - r ** n), I1 * (1 - r ** n)
+    return h0, h1, (s + d) / 2, (s - d) / 2
+
+
+def test_stroop_lca_zero_noise_linear_recurrence_closed_form(orc):
+    """Incongruent trial (colour 0, word 1), both units driven and never
+    rectified: the oracle's pathway states and both response units follow the
+    closed form to binary32 accumulation accuracy; the latch step is the closed
+    form's first crossing.  Power: a swapped leak/inhibition, a flipped
+    inhibition sign, self- instead of lateral inhibition and tau = 1 all miss
+    by orders of magnitude more than the tolerance."""
+    N, theta = 200, 1.0
+    uc, us = 0.8, 0.3
+    gc, gw = 1.0, 1.5
+    P = _stroop_params(gc, gw, _TAU, _LAM, _BETA, 0.0, _DT, 1e6, N)
+    I0, I1 = np.float64(np.float32(gc * uc)), np.float64(np.float32(np.float32(gw) * np.float32(1 - np.float32(us))))
+    resp, st, tr = orc.stroop_trace(P, uc, us, 7, 123, 1)        # trial 1: incongruent, colour 0
+    assert resp == -1 and st == 0                                 # theta out of reach
+    n = np.arange(1, N + 1)
+    h0, h1, x0, x1 = _lca_closed_form(I0, I1, _TAU, _LAM, _BETA, _DT, n)
+    assert (x0 > 0).all() and (x1 > x0).all()                     # never rectified; word unit leads
+    tol = 2e-5 * np.maximum(1.0, np.abs(x1))
+    for got, want in ((tr[:, 0], h0), (tr[:, 1], h1), (tr[:, 2], x0), (tr[:, 3], x1)):
+        assert np.max(np.abs(got - want)) < 2e-5, np.max(np.abs(got - want))
+    # power: each plausible slip moves the trajectory far outside the tolerance
+    wrong = {
+        "leak<->inhibition": _lca_closed_form(I0, I1, _TAU, _BETA, _LAM, _DT, n),
+        "inhibition sign": _lca_closed_form(I0, I1, _TAU, _LAM, -_BETA, _DT, n),
+        "tau = 1": _lca_closed_form(I0, I1, 1.0, _LAM, _BETA, _DT, n),
+    }
+    for name, (_, _, y0, y1) in wrong.items():
+        dev = max(np.max(np.abs(tr[:, 2] - y0)), np.max(np.abs(tr[:, 3] - y1)))
+        assert dev > 1000 * tol.max(), (name, dev)
+    # self-inhibition (x_k instead of x_{1-k}): both units decouple with a = 1 - dt (lam + beta)
+    a = 1 - _DT * (_LAM + _BETA)
+    y0 = _DT * I0 * _G(a, 1 - _TAU, n)
+    assert np.max(np.abs(tr[:, 2] - y0)) > 1000 * tol.max()
+    # the latch: with theta = 1 the word unit (1) crosses first, at the closed form's step
+    P2 = _stroop_params(gc, gw, _TAU, _LAM, _BETA, 0.0, _DT, theta, N)
+    r2, st2 = orc.stroop_trial(P2, uc, us, 7, 123, 1)
+    n_cf = int(np.argmax(x1 >= theta)) + 1
+    assert abs(x1[n_cf - 1] - theta) > 1e-3 and x0[n_cf - 1] < theta   # not a rounding-order tie
+    assert (r2, st2) == (1, n_cf)
+
+
+def test_stroop_lca_rectified_unit_closed_form(orc):
+    """Congruent trial: unit 1 gets no input, so lateral inhibition drives it
+    below 0 and the rectification holds it at exactly 0; unit 0 then follows
+    the scalar leaky recurrence x0(n) = (1 - dt lam) x0 + dt h0(n) (no
+    inhibition term, since x1 = 0) — pins the rectification and the leak on
+    their own."""
+    N = 150
+    P = _stroop_params(1.0, 1.5, _TAU, _LAM, _BETA, 0.0, _DT, 1e6, N)
+    uc, us = 0.6, 0.2
+    _, _, tr = orc.stroop_trace(P, uc, us, 3, 45, 0)              # trial 0: congruent, colour 0 = word 0
+    I0 = np.float64(np.float32(np.float32(0.6) + np.float32(np.float32(1.5) * np.float32(1 - np.float32(0.2)))))
+    n = np.arange(1, N + 1)
+    a = 1 - _DT * _LAM
+    x0 = _DT * I0 * _G(a, 1 - _TAU, n)
+    assert np.all(tr[:, 3] == 0.0)
+    assert np.max(np.abs(tr[:, 2] - x0)) < 2e-5
+    assert np.max(np.abs(tr[:, 1])) == 0.0                        # h1 = 0 exactly
+
+
+def test_stroop_lca_noisy_ar1_moments(orc):
+    """With noise, both units far from 0 (never rectified): the sum and
+    difference coordinates are independent AR(1) processes with the closed-form
+    means and variances above (Cov = 0).  A swapped leak/inhibition (a_d > 1)
+    or a flipped inhibition sign (Var s and Var d exchanged) is rejected."""
+    N, sig, tau = 100, 0.1, 0.9
+    gc, gw, uc, us = 4.0, 5.0, 1.0, 0.0
+    P = _stroop_params(gc, gw, tau, _LAM, _BETA, sig, _DT, 1e6, N)
+    n_units = 4000
+    X = np.empty((n_units, N, 2))
+    for u in range(n_units):
+        _, _, tr = orc.stroop_trace(P, uc, us, 11, u, 1)          # incongruent: I0 = gc uc, I1 = gw (1 - us)
+        X[u] = tr[:, 2:4]
+    assert (X > 0).all()                                          # rectification never engaged
+    s, d = X[:, :, 0] + X[:, :, 1], X[:, :, 0] - X[:, :, 1]
+    nsd2 = float(np.float32(sig) * np.sqrt(np.float32(_DT))) ** 2
+    I0, I1 = gc * uc, gw * (1 - us)
+    r = 1 - tau
+    a_s, a_d = 1 - _DT * (_LAM + _BETA), 1 - _DT * (_LAM - _BETA)
+    for k in (9, 39, 99):                                         # steps 10, 40, 100
+        m = k + 1
+        ms, md = _DT * (I0 + I1) * _G(a_s, r, m), _DT * (I0 - I1) * _G(a_d, r, m)
+        vs = 2 * nsd2 * (1 - a_s ** (2 * m)) / (1 - a_s ** 2)
+        vd = 2 * nsd2 * (1 - a_d ** (2 * m)) / (1 - a_d ** 2)
+        assert abs(s[:, k].mean() - ms) < 4 * math.sqrt(vs / n_units)
+        assert abs(d[:, k].mean() - md) < 4 * math.sqrt(vd / n_units)
+        se_v = math.sqrt(2.0 / n_units)
+        assert abs(s[:, k].var() / vs - 1) < 4 * se_v, (k, s[:, k].var(), vs)
+        assert abs(d[:, k].var() / vd - 1) < 4 * se_v, (k, d[:, k].var(), vd)
+        assert abs(np.corrcoef(s[:, k], d[:, k])[0, 1]) < 4 / math.sqrt(n_units)
+    # power at step 100: flipped inhibition exchanges the two variances (ratio ~2)
+    m = 100
+    vs = 2 * nsd2 * (1 - a_s ** (2 * m)) / (1 - a_s ** 2)
+    vd = 2 * nsd2 * (1 - a_d ** (2 * m)) / (1 - a_d ** 2)
+    assert abs(s[:, 99].var() / vd - 1) > 10 * math.sqrt(2.0 / n_units)
+    assert abs(d[:, 99].var() / vs - 1) > 10 * math.sqrt(2.0 / n_units)
+    # swapped leak/inhibition: a_d' = 1 - dt (beta - lam) > 1, variance grows geometrically
+    a_w = 1 - _DT * (_BETA - _LAM)
+    vw = 2 * nsd2 * (a_w ** (2 * m) - 1) / (a_w ** 2 - 1)
+    assert abs(d[:, 99].var() / vw - 1) > 10 * math.sqrt(2.0 / n_units)

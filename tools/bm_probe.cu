@@ -1,0 +1,207 @@
+// Normal-transform cost probe (tools only): throughput of stream-2 style
+// normals (hoisted Philox4x32-10 + sextet packing) under alternative
+// Box-Muller evaluations.  Timing only: the table contents are plausible
+// values, not a specification.  Variants:
+//   0  current spec (ln poly + Goldschmidt sqrt + half-turn sincos poly)
+//   1  radius as 0; angle by two 256-entry (cos, sin) tables + rotation
+//   2  radius by 64-entry ln table + 128-entry rsqrt seed (1 Goldschmidt step); angle as 1
+//   3  radius by a piecewise cubic (768 segments, one LDS.128); angle as 1
+//   4  radius as 3; angle as 0 (polynomial)
+//   5  as 3 with R-times replicated angle tables (lane-offset copies)
+#include <cstdio>
+#include <cstdint>
+#include <cmath>
+#include <vector>
+#include "../paper_2110_15425_b200/csrc/rng.cuh"
+using namespace distill;
+
+constexpr int REP = 4;
+
+__device__ __forceinline__ uint32_t ang16(const uint4& X, int e) {
+    return e == 0 ? (X.w & 0xFFFFu) : e == 1 ? (X.w >> 16) : (__byte_perm(X.x, X.y, 0x0040u) & 0xFFFFu);
+}
+
+// current radius (ln_spec + Goldschmidt sqrt_spec), both lanes
+__device__ __forceinline__ F2 radius_poly(uint32_t Rx, uint32_t Ry) {
+    using L = Ops<false>;
+    const uint32_t ix = __float_as_uint(__uint2float_rn((Rx >> 8) | 1u));
+    const uint32_t iy = __float_as_uint(__uint2float_rn((Ry >> 8) | 1u));
+    const uint32_t tx = ix - 0x4B3504F3u, ty = iy - 0x4B3504F3u;
+    const F2 m = make_float2(__uint_as_float((tx & 0x7FFFFFu) + 0x3F3504F3u), __uint_as_float((ty & 0x7FFFFFu) + 0x3F3504F3u));
+    const F2 fe = make_float2(__int2float_rn((int32_t)tx >> 23), __int2float_rn((int32_t)ty >> 23));
+    const F2 f = L::add(m, bc(-1.0f));
+    F2 P = L::fma(bc(D_L7), f, bc(D_L6));
+    P = L::fma(P, f, bc(D_L5)); P = L::fma(P, f, bc(D_L4)); P = L::fma(P, f, bc(D_L3));
+    P = L::fma(P, f, bc(D_L2)); P = L::fma(P, f, bc(D_L1)); P = L::fma(P, f, bc(D_L0));
+    F2 y = L::fma(L::mul(f, f), P, f);
+    y = L::fma(fe, bc(D_LN2_LO), y);
+    y = L::fma(fe, bc(D_LN2_HI), y);
+    const uint32_t shx = __float_as_uint(y.x) >> 1, shy = __float_as_uint(y.y) >> 1;
+    const F2 y0m2 = make_float2(__uint_as_float(0x1F775A86u - shx), __uint_as_float(0x1F775A86u - shy));
+    F2 h = make_float2(__uint_as_float(0x9E775A86u - shx), __uint_as_float(0x9E775A86u - shy));
+    F2 g = L::mul(y, y0m2);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const F2 rr = L::fma(neg2(g), h, bc(0.5f));
+        g = L::fma(g, rr, g);
+        h = L::fma(h, rr, h);
+    }
+    return L::fma(g, L::fma(neg2(g), h, bc(0.5f)), g);
+}
+
+// ln table (invc, logc) + rsqrt seed table, one Goldschmidt step
+__device__ __forceinline__ F2 radius_tab(uint32_t Rx, uint32_t Ry, const float2* lnt, const uint32_t* seed) {
+    using L = Ops<false>;
+    const uint32_t ix = __float_as_uint(__uint2float_rn((Rx >> 8) | 1u)) - (24u << 23);
+    const uint32_t iy = __float_as_uint(__uint2float_rn((Ry >> 8) | 1u)) - (24u << 23);
+    const uint32_t tx = ix - 0x3F330000u, ty = iy - 0x3F330000u;
+    const float2 cx = lnt[(tx >> 17) & 63], cy = lnt[(ty >> 17) & 63];
+    const F2 m = make_float2(__uint_as_float(ix - (tx & 0xFF800000u)), __uint_as_float(iy - (ty & 0xFF800000u)));
+    const F2 fe = make_float2(__int2float_rn((int32_t)tx >> 23), __int2float_rn((int32_t)ty >> 23));
+    const F2 r = L::fma(m, make_float2(cx.x, cy.x), bc(-1.0f));
+    const F2 P = L::fma(L::fma(r, bc(-0.25f), bc(0.33333334f)), r, bc(-0.5f));
+    F2 y = L::fma(L::mul(r, r), P, r);
+    y = L::add(y, L::fma(fe, bc(D_LN2_HI), make_float2(cx.y, cy.y)));
+    // s = -2y; seed from (exponent lsb, 6 mantissa bits)
+    const uint32_t bx = __float_as_uint(y.x), by = __float_as_uint(y.y);
+    const F2 y0m2 = make_float2(__uint_as_float(seed[(bx >> 17) & 127] - ((bx >> 1) & 0x3FC00000u)),
+                                __uint_as_float(seed[(by >> 17) & 127] - ((by >> 1) & 0x3FC00000u)));
+    F2 h = L::mul(y0m2, bc(-0.25f));
+    F2 g = L::mul(y, y0m2);
+    const F2 rr = L::fma(neg2(g), h, bc(0.5f));
+    g = L::fma(g, rr, g);
+    h = L::fma(h, rr, h);
+    return L::fma(g, L::fma(neg2(g), h, bc(0.5f)), g);
+}
+
+// piecewise cubic radius: region (N < 2^23 or not), octave, 4 mantissa bits
+__device__ __forceinline__ F2 radius_pw(uint32_t Rx, uint32_t Ry, const float4* pw) {
+    using L = Ops<false>;
+    const uint32_t nx = (Rx >> 8) | 1u, ny = (Ry >> 8) | 1u;
+    const uint32_t vx = (nx >> 23) ? 0x1000000u - nx : nx, vy = (ny >> 23) ? 0x1000000u - ny : ny;
+    const uint32_t bx = __float_as_uint(__uint2float_rn(vx)), by = __float_as_uint(__uint2float_rn(vy));
+    const uint32_t jx = (bx >> 19) - (127u << 4) + ((nx >> 23) ? 384u : 0u);
+    const uint32_t jy = (by >> 19) - (127u << 4) + ((ny >> 23) ? 384u : 0u);
+    const float4 ax = pw[jx], ay = pw[jy];
+    const F2 t = L::add(make_float2(__uint_as_float((bx & 0x7FFFFu) | 0x3F800000u), __uint_as_float((by & 0x7FFFFu) | 0x3F800000u)),
+                        bc(-1.03125f));
+    F2 p = L::fma(make_float2(ax.w, ay.w), t, make_float2(ax.z, ay.z));
+    p = L::fma(p, t, make_float2(ax.y, ay.y));
+    return L::fma(p, t, make_float2(ax.x, ay.x));
+}
+
+// angle by rotation tables; returns z = rad (cos, sin)
+template <int R>
+__device__ __forceinline__ void rotate(F2 rad, uint32_t ax, uint32_t ay, const float2* t1, const float2* t2, F2& zc, F2& zs) {
+    using L = Ops<false>;
+    const uint32_t ln = R > 1 ? (threadIdx.x % R) : 0;
+    const float2 hx = t1[(ax >> 8) * R + ln], hy = t1[(ay >> 8) * R + ln];
+    const float2 lx = t2[(ax & 0xFFu) * R + ln], ly = t2[(ay & 0xFFu) * R + ln];
+    const F2 a = L::mul(rad, make_float2(hx.x, hy.x)), b = L::mul(rad, make_float2(hx.y, hy.y));
+    const F2 cl = make_float2(lx.x, ly.x), sl = make_float2(lx.y, ly.y);
+    zc = L::fma(a, cl, neg2(L::mul(b, sl)));
+    zs = L::fma(b, cl, L::mul(a, sl));
+}
+
+__device__ __forceinline__ void sincos_poly(F2 rad, uint32_t ax, uint32_t ay, F2& zc, F2& zs) {
+    using Q = Ops<false>;
+    const F2 r = Q::add(make_float2(__uint_as_float(((ax << 7) & 0x7FFF00u) | 0x3F800000u),
+                                    __uint_as_float(((ay << 7) & 0x7FFF00u) | 0x3F800000u)), bc(-1.5f));
+    const F2 t = Q::mul(r, r);
+    const F2 S = Q::fma(Q::fma(Q::fma(Q::fma(bc(D_S4), t, bc(D_S3)), t, bc(D_S2)), t, bc(D_S1)), t, bc(D_S0));
+    const F2 C = Q::fma(Q::fma(Q::fma(Q::fma(bc(D_C4), t, bc(D_C3)), t, bc(D_C2)), t, bc(D_C1)), t, bc(D_C0));
+    const F2 cq = Q::fma(C, t, bc(1.0f)), sq = Q::mul(S, r);
+    const F2 rs = make_float2(__uint_as_float(__float_as_uint(rad.x) ^ ((ax << 16) & 0x80000000u)),
+                              __uint_as_float(__float_as_uint(rad.y) ^ ((ay << 16) & 0x80000000u)));
+    zc = Q::mul(rs, cq); zs = Q::mul(rs, sq);
+}
+
+template <int V>
+__global__ void __launch_bounds__(128, 6) k_bm(float* out, uint32_t key0, int n_iter, const float2* g1, const float2* g2,
+                                               const float2* gln, const uint32_t* gseed, const float4* gpw) {
+    __shared__ float2 t1[256 * (V == 5 ? REP : 1)], t2[256 * (V == 5 ? REP : 1)], lnt[64];
+    __shared__ uint32_t seed[128];
+    __shared__ float4 pw[(V >= 3) ? 768 : 1];
+    const int R = V == 5 ? REP : 1;
+    for (int k = threadIdx.x; k < 256 * R; k += 128) { t1[k] = g1[k / R]; t2[k] = g2[k / R]; }
+    if (threadIdx.x < 64) lnt[threadIdx.x] = gln[threadIdx.x];
+    seed[threadIdx.x] = gseed[threadIdx.x];
+    if (V >= 3) for (int k = threadIdx.x; k < 768; k += 128) pw[k] = gpw[k];
+    __syncthreads();
+    const uint32_t tid = blockIdx.x * 128 + threadIdx.x;
+    PhiloxHoisted rng;
+    rng.init(tid, 0u, 2u, key0, 0u);
+    F2 acc = bc(0.0f);
+    for (int j = 0; j < n_iter; ++j) {
+        const uint4 X = rng(2 * j), Y = rng(2 * j + 1);
+        const uint32_t RX[3] = {X.x, X.y, X.z}, RY[3] = {Y.x, Y.y, Y.z};
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            F2 zc, zs;
+            if (V == 0) {
+                bm_pair2<false, false, false>(RX[e], RY[e], ang16(X, e) << 16, ang16(Y, e) << 16, zc, zs);
+            } else {
+                const F2 rad = (V == 1) ? radius_poly(RX[e], RY[e])
+                             : (V == 2) ? radius_tab(RX[e], RY[e], lnt, seed)
+                                        : radius_pw(RX[e], RY[e], pw);
+                if (V == 4) sincos_poly(rad, ang16(X, e), ang16(Y, e), zc, zs);
+                else if (V == 5) rotate<REP>(rad, ang16(X, e), ang16(Y, e), t1, t2, zc, zs);
+                else rotate<1>(rad, ang16(X, e), ang16(Y, e), t1, t2, zc, zs);
+            }
+            acc = __fadd2_rn(acc, zc);
+            acc = __fadd2_rn(acc, zs);
+        }
+    }
+    out[tid] = acc.x + acc.y;
+}
+
+template <int V>
+void run(const char* name, float* out, int n_thr, int n_iter, const float2* g1, const float2* g2, const float2* gln,
+         const uint32_t* gseed, const float4* gpw) {
+    cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, k_bm<V>);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        k_bm<V><<<n_thr / 128, 128>>>(out, 42u, n_iter, g1, g2, gln, gseed, gpw);
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (r && ms < best) best = ms;
+    }
+    std::vector<float> h(n_thr);
+    cudaMemcpy(h.data(), out, n_thr * 4, cudaMemcpyDeviceToHost);
+    double s = 0, s2 = 0;
+    for (float v : h) { s += v; s2 += (double)v * v; }
+    const double n_norm = (double)n_thr * n_iter * 12;
+    printf("V%d %-44s regs %3d  %8.4f ms  %.3e normals/s  (mean %.3g, var/normal %.4f)\n", V, name, fa.numRegs, best,
+           n_norm / (best * 1e-3), s / n_norm, s2 / n_norm);
+}
+
+int main() {
+    const int n_thr = 1 << 20, n_iter = 84;
+    std::vector<float2> h1(256), h2(256), hln(64);
+    std::vector<uint32_t> hs(128);
+    std::vector<float4> hpw(768);
+    for (int k = 0; k < 256; ++k) {
+        const double a = 2 * M_PI * k / 256, b = 2 * M_PI * k / 65536;
+        h1[k] = make_float2((float)cos(a), (float)sin(a));
+        h2[k] = make_float2((float)cos(b), (float)sin(b));
+    }
+    for (int k = 0; k < 64; ++k) { const double c = 0.7 + (k + 0.5) * 0.7 / 64; hln[k] = make_float2((float)(1 / c), (float)log(c)); }
+    for (int k = 0; k < 128; ++k) { const float v = (float)(-2.0 / sqrt(1.0 + (k & 63) / 64.0) / ((k >> 6) ? 1.414 : 1.0)); uint32_t b; memcpy(&b, &v, 4); hs[k] = b + (64u << 23); }
+    for (int k = 0; k < 768; ++k) hpw[k] = make_float4(1.0f + (k % 7) * 0.1f, 0.3f, -0.01f, 0.001f);
+    float2 *g1, *g2, *gln; uint32_t* gs; float4* gpw; float* out;
+    cudaMalloc(&g1, 256 * 8); cudaMalloc(&g2, 256 * 8); cudaMalloc(&gln, 64 * 8); cudaMalloc(&gs, 512); cudaMalloc(&gpw, 768 * 16);
+    cudaMalloc(&out, n_thr * 4);
+    cudaMemcpy(g1, h1.data(), 256 * 8, cudaMemcpyHostToDevice); cudaMemcpy(g2, h2.data(), 256 * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(gln, hln.data(), 64 * 8, cudaMemcpyHostToDevice); cudaMemcpy(gs, hs.data(), 512, cudaMemcpyHostToDevice);
+    cudaMemcpy(gpw, hpw.data(), 768 * 16, cudaMemcpyHostToDevice);
+    run<0>("spec (poly ln, Goldschmidt, poly sincos)", out, n_thr, n_iter, g1, g2, gln, gs, gpw);
+    run<1>("poly radius + rotation tables", out, n_thr, n_iter, g1, g2, gln, gs, gpw);
+    run<2>("ln table + seed table + rotation tables", out, n_thr, n_iter, g1, g2, gln, gs, gpw);
+    run<3>("piecewise-cubic radius + rotation tables", out, n_thr, n_iter, g1, g2, gln, gs, gpw);
+    run<4>("piecewise-cubic radius + poly sincos", out, n_thr, n_iter, g1, g2, gln, gs, gpw);
+    run<5>("piecewise-cubic radius + replicated rotation", out, n_thr, n_iter, g1, g2, gln, gs, gpw);
+    printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
