@@ -65,6 +65,7 @@ def _bind(path: str) -> C.CDLL:
         "od_normal_sextet": (None, [u64, u32, u32, u32, _f32p]),
         "od_pp_eval": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u64, u64, u32, u64, u32, C.c_void_p]),
         "od_pp_trace": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u32, u64, u32, _f32p]),
+        "od_pp_trace_f64": (C.c_int, [_u32p, _f32p, _f32p, _f32p, u64, u32, u64, u32, _f64p]),
         "od_pp_eval_f64": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, u64, u64, u32, u64, u32, C.c_void_p]),
         "od_key": (u64, [f32, u32]),
         "od_argmax_random_ties": (C.c_int, [_f32p, u64, u64, u64, u32, C.POINTER(u64), C.POINTER(u64)]),
@@ -221,11 +222,19 @@ def pp_eval(n_levels, levels, w, params, inputs, begin, end, n_samples, seed,
     return out
 
 
-def pp_trace(n_levels, levels, params, inputs, i, n_samples, seed, invocation=0) -> np.ndarray:
+def pp_trace(n_levels, levels, params, inputs, i, n_samples, seed, invocation=0, lib_handle=None) -> np.ndarray:
     """Per-sample objective e_s of allocation i (debug/tests)."""
     out = np.zeros(int(n_samples), np.float32)
-    lib().od_pp_trace(_u32(n_levels), _f32(levels), _f32(params), _f32(inputs), int(i), int(n_samples),
+    (lib_handle or lib()).od_pp_trace(_u32(n_levels), _f32(levels), _f32(params), _f32(inputs), int(i), int(n_samples),
                       int(seed), int(invocation), out)
+    return out
+
+
+def pp_trace_f64(n_levels, levels, params, inputs, i, n_samples, seed, invocation=0, lib_handle=None) -> np.ndarray:
+    """Per-sample binary64 objective of allocation i (the plain definition)."""
+    out = np.zeros(int(n_samples), np.float64)
+    (lib_handle or lib()).od_pp_trace_f64(_u32(n_levels), _f32(levels), _f32(params), _f32(inputs), int(i),
+                                          int(n_samples), int(seed), int(invocation), out)
     return out
 
 

@@ -260,7 +260,12 @@ static void od_observe(uint64_t seed, uint32_t alloc, uint32_t sample, uint32_t 
  * and the true best move u*, with delta = d * y_d - u* fused per component */
 static float od_objective(v2 d, v2 ustar) {
     float yd = od_rsqrt(FFMA(d.y, d.y, FFMA(d.x, d.x, 0x1p-126f)));
+#ifdef OD_UNFUSED_OBJECTIVE
+    /* DESIGN.md R21 comparison build only (tools/r21_error.py): u_hat rounded on its own */
+    v2 dl = { FSUB(FMUL(d.x, yd), ustar.x), FSUB(FMUL(d.y, yd), ustar.y) };
+#else
     v2 dl = { FFMA(d.x, yd, -ustar.x), FFMA(d.y, yd, -ustar.y) };
+#endif
     return FFMA(dl.y, dl.y, FMUL(dl.x, dl.x));
 }
 
@@ -345,6 +350,37 @@ static void d_bm(uint32_t R, uint32_t A, double* z0, double* z1) {
     double rad = sqrt(-2.0 * log(u1));
     *z0 = rad * cos(TWO_PI * t);
     *z1 = rad * sin(TWO_PI * t);
+}
+
+/* Per-sample binary64 objective of one allocation (the plain definition, sample by sample). */
+int od_pp_trace_f64(const uint32_t n_levels[3], const float* levels, const float params[3],
+                    const float inputs[6], uint64_t i, uint32_t n_samples, uint64_t seed,
+                    uint32_t invocation, double* out) {
+    const float* lev[3] = { levels, levels + n_levels[0], levels + n_levels[0] + n_levels[1] };
+    double smax = params[0], smin = params[1], kappa = params[2];
+    d2 p[3] = { { inputs[0], inputs[1] }, { inputs[2], inputs[3] }, { inputs[4], inputs[5] } };
+    d2 ustar = d_unit(d_action(p[0], p[1], p[2], kappa));
+    uint32_t key[2];
+    od_key_of_seed(seed, key);
+    uint32_t k[3];
+    od_decode(i, 3, n_levels, k);
+    double a[3] = { lev[0][k[0]], lev[1][k[1]], lev[2][k[2]] };
+    for (uint32_t s = 0; s < n_samples; ++s) {
+        uint32_t ctr[4] = { (uint32_t)i, s, invocation, 1u }, X[4];
+        od_philox4x32_10(ctr, key, X);
+        uint32_t A[3] = { X[3] << 16, X[3] & 0xFFFF0000u, (X[0] << 24) | ((X[1] & 0xFFu) << 16) };
+        d2 o[3];
+        for (int e = 0; e < 3; ++e) {
+            double zx, zy, sg = smax + a[e] * (smin - smax);
+            d_bm(X[e], A[e], &zx, &zy);
+            o[e].x = p[e].x + sg * zx;
+            o[e].y = p[e].y + sg * zy;
+        }
+        d2 uh = d_unit(d_action(o[0], o[1], o[2], kappa));
+        double dx = uh.x - ustar.x, dy = uh.y - ustar.y;
+        out[s] = dx * dx + dy * dy;
+    }
+    return 0;
 }
 
 int od_pp_eval_f64(const uint32_t n_levels[3], const float* levels, const float w[3],

@@ -71,6 +71,10 @@ int od_pp_trace(const uint32_t n_levels[3], const float* levels, const float par
                 const float inputs[6], uint64_t i, uint32_t n_samples, uint64_t seed,
                 uint32_t invocation, float* out);
 /* Same evaluation in binary64 from the same Philox bits (libm log/sqrt/cos/sin). */
+/* Per-sample binary64 objective of allocation i (out[s], s < n_samples). */
+int od_pp_trace_f64(const uint32_t n_levels[3], const float* levels, const float params[3],
+                    const float inputs[6], uint64_t i, uint32_t n_samples, uint64_t seed,
+                    uint32_t invocation, double* out);
 int od_pp_eval_f64(const uint32_t n_levels[3], const float* levels, const float w[3],
                    const float params[3], const float inputs[6],
                    uint64_t begin, uint64_t end, uint32_t n_samples, uint64_t seed,

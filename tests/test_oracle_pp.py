@@ -299,3 +299,33 @@ def test_noisy_predator_action_matches_angle_law_quadrature(orc):
     want = expect(kap)
     assert abs(C.mean() - want) <= 4 * se + 0.01 * want, (C.mean(), want, se)
     assert abs(C.mean() - expect(-kap)) > 100 * se
+
+
+def test_r21_fused_objective_step_is_closer_to_binary64(orc):
+    """DESIGN.md reading R21, justified by accuracy rather than by the compiler:
+    the objective's difference Delta = fma(d, y_d, -u*) (one rounding) is closer
+    to the binary64 plain definition (od_pp_trace_f64) than the unfused
+    u_hat = d*y_d, Delta = u_hat - u* (two roundings).  A second oracle build
+    that differs only in that step (-DOD_UNFUSED_OBJECTIVE) is compared sample by
+    sample on cfg3 inputs; tools/r21_error.py is the larger run
+    (profiles/r02_r21_error.txt)."""
+    import os
+    import subprocess
+    import tempfile
+    import oracle
+    so = os.path.join(tempfile.mkdtemp(), "liboracle_unfused.so")
+    subprocess.check_call(["gcc", *oracle.CFLAGS, "-DOD_UNFUSED_OBJECTIVE", oracle._SRC, "-o", so, "-lm"])
+    unfused = oracle._bind(so)
+    cfg = W.pp_cfg3()
+    idx = np.random.default_rng(7).choice(cfg.n_alloc, 600, replace=False)
+    rf, ru = [], []
+    for i in idx:
+        args = (cfg.n_levels, cfg.levels, cfg.params, cfg.inputs, int(i), cfg.n_samples, cfg.seed)
+        e64 = orc.pp_trace_f64(*args)
+        rf.append(np.abs(orc.pp_trace(*args).astype(np.float64) - e64) / e64)
+        ru.append(np.abs(orc.pp_trace(*args, lib_handle=unfused).astype(np.float64) - e64) / e64)
+    rf, ru = np.concatenate(rf), np.concatenate(ru)
+    assert not np.array_equal(rf, ru)                       # the two builds really differ
+    closer, farther = np.mean(rf < ru), np.mean(rf > ru)
+    assert closer > farther + 0.01, (closer, farther)
+    assert np.median(rf) < np.median(ru)                    # (the mean is set by a few ill-conditioned samples)
