@@ -24,4 +24,13 @@ examples/c_api_demo: examples/c_api_demo.c include/distill.h $(LIB)
 clean:
 	rm -f $(LIB) $(ORACLE) oracle/liboracle_count.so examples/c_api_demo
 
-.PHONY: all clean
+.PHONY: all clean sanitize-oracle
+
+# ASan + UBSan run of the CPU oracle: instrumented copies of
+# liboracle*.so, the oracle's CPU test suite under the preloaded runtime.
+sanitize-oracle:
+	DISTILL_ORACLE_SANITIZE=1 LD_PRELOAD="$$(gcc -print-file-name=libasan.so) $$(gcc -print-file-name=libubsan.so)" \
+	ASAN_OPTIONS=detect_leaks=0:halt_on_error=1 UBSAN_OPTIONS=print_stacktrace=1:halt_on_error=1 \
+	python -m pytest tests/test_oracle_rng.py tests/test_oracle_pp.py tests/test_oracle_argmax.py \
+	    tests/test_oracle_ddm_lca.py tests/test_oracle_episode.py tests/test_oracle_amr.py \
+	    tests/test_oracle_ext_stroop.py -q -p no:cacheprovider

@@ -38,15 +38,31 @@ import workloads as W  # noqa: E402
 
 METRIC = "model evaluations/sec (allocations×samples) at 1/2/4/8 B200; % FP32 peak"
 UNIT = "evals/s"
-FLOPS_PER_SAMPLE = 274        # DESIGN.md §6, pinned by tests/test_oracle_pp.py (counting oracle)
-FLOPS_PER_ALLOC = 13
-FLOPS_PER_CALL = 74
+# Flop counts per unit of work.  The headline roofline uses SURVEY.md §8(d)'s per-unit
+# figure (the task's definition of `achieved`): ~210 FP32 flop per PP evaluation (fma = 2,
+# add/mul/sqrt/div = 1) + ~15 per allocation; a fixed, implementation-independent yardstick,
+# so the fraction moves only with evaluations/s.  Reported beside it: the counted method
+# flops (the oracle's counting build in method mode: sqrt = 1, rsqrt = sqrt + divide) and
+# the executed flops (the spec's Newton/Goldschmidt steps included) — tests/test_oracle_pp.py.
+FLOPS_PER_SAMPLE = 210
+FLOPS_PER_ALLOC = 15
+FLOPS_PER_CALL = 0
+FLOPS_PER_SAMPLE_METHOD = 181   # counted (test_method_flop_count)
+FLOPS_PER_ALLOC_METHOD = 13
+FLOPS_PER_CALL_METHOD = 32
+FLOPS_PER_SAMPLE_EXEC = 274     # counted (test_flop_count_per_sample_matches_hand_count)
+FLOPS_PER_CALL_EXEC = 74
 FP32_LANES_PER_SM = 128       # FFMA lanes per SM (4 SMSP x 32), 2 flops per FMA
 FP32_PEAK_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12   # TFLOP/s (the extras' denominator)
-# DDM step = 1/4 quad block (2 Box-Muller pairs: 2 x 60 + 4 products = 124) + 2 fma = 35;
-# Stroop step = 1/2 quad block (62) + pathways 2 x 3 + rectified LCA 2 x 8 = 84.
-DDM_FLOPS_PER_STEP = 35
-STROOP_FLOPS_PER_STEP = 78   # per trial-step: 2 normals (2 x 31) + rectified LCA 16; the pathway h_k(n) is trial-invariant (per-block table)
+# accumulator models: SURVEY §8(d) ~30 flop per DDM step, ~75 per Stroop trial-step; counted:
+# one sextet (6 normals) = 135 method / 186 executed flops (test_method_flop_count),
+# DDM step = 1 normal + 2 fma, Stroop trial-step = 2 normals + rectified LCA 16
+DDM_FLOPS_PER_STEP = 30
+DDM_FLOPS_PER_STEP_EXEC = 186 / 6 + 4     # 35
+STROOP_FLOPS_PER_STEP = 75
+STROOP_FLOPS_PER_STEP_EXEC = 2 * 186 / 6 + 16   # 78
+# SURVEY §8(d)'s 50 %-of-peak point for cfg3, in the count-independent unit
+EVALS_PER_S_AT_50PCT = 1.77e11
 
 
 def env_int(name, default):
@@ -147,12 +163,30 @@ def oracle_rate(cfg: W.PPConfig, target_cpu_s: float = 15.0):
                       f"({wall:.2f} s wall)"}
 
 
+def workload(world: int, args):
+    """BASELINE.json configs: N = 1 -> cfg3 (1e6 allocations x 100 samples on 1 B200);
+    N = 2/4/8 -> cfg5 (8e6 x 100) sharded across the N GPUs (strong scaling).
+    --weak: ~1e6 allocations per GPU instead (round(100 N^(1/3))^3; N = 8 is cfg5);
+    --strong at N = 1: the whole cfg5 grid on one GPU (t1 of the strong series)."""
+    if args.weak:
+        return W.pp_weak(world), "weak"
+    if world == 1:
+        return (W.pp_cfg5(), "strong") if args.strong else (W.pp_cfg3(), "weak")
+    return W.pp_cfg5(), "strong"
+
+
+def workload_config(cfg: W.PPConfig, world: int) -> dict:
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": cfg.name, "grid": list(cfg.n_levels), "samples": cfg.n_samples,
+            "allocations": cfg.n_alloc, "parallelism": f"grid-dp{world}"}
+
+
 def run_reference(args):
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     if rank != 0:
         return 0
-    cfg = W.pp_weak(world)
+    cfg, scaling = workload(world, args)
     import oracle
     oracle.build()
     cores = host_cores()
@@ -169,14 +203,14 @@ def run_reference(args):
                                cfg.seed, threads=cores)
         if s >= args.warmup:
             times.append(time.perf_counter() - t)
-    ms = 1e3 * sum(times) / len(times)
+    ms = 1e3 * statistics.median(times)
     value = n * cfg.n_samples / (ms / 1e3)
-    sample = f"{cfg.name}: allocations [0, {n}) x {cfg.n_samples} samples per step on {cores} threads"
+    sample = (f"{cfg.name}: allocations [0, {n}) of {cfg.n_alloc} x {cfg.n_samples} samples per step "
+              f"on {cores} threads (median of {len(times)} steps)")
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-           "config": {"workload": cfg.name, "grid": list(cfg.n_levels), "samples": cfg.n_samples,
-                      "slice_allocations": n},
+           "config": workload_config(cfg, world),
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -184,6 +218,19 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
+
+def self_spawn(args) -> int:
+    """`bench.py --gpus N` without torchrun: launch the N ranks the way the
+    driver does (torch.distributed.run, one process per GPU, 127.0.0.1) and pass
+    rank 0's JSON line through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
 
 def run_ours(args):
     import torch
@@ -196,7 +243,8 @@ def run_ours(args):
     world = env_int("WORLD_SIZE", 1)
     local = env_int("LOCAL_RANK", 0)
     if world != args.gpus:
-        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus} (launch with torchrun "
+                         f"--nproc-per-node {args.gpus}, or without WORLD_SIZE to self-spawn)")
     if args.device is not None:       # test mode: several ranks on one GPU (gloo only; timings meaningless)
         local = args.device
     torch.cuda.set_device(local)
@@ -206,6 +254,7 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(args.dist_backend)
+    nvtx = torch.cuda.nvtx
 
     def barrier():
         if world > 1:
@@ -218,7 +267,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    cfg = W.pp_weak(world)
+    cfg, scaling = workload(world, args)
     b, e = D.shard_range(cfg.n_alloc, rank, world)
     count = e - b
     model = D.load_model(W.KIND_PREDATOR_PREY, cfg.n_levels, cfg.levels, cfg.w, cfg.params, device=local)
@@ -227,52 +276,93 @@ def run_ours(args):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
+    # One step = key reset + the fused grid-search kernel on this rank's shard
+    # (keys in the signed order, so the shard key IS the all-reduce operand) +
+    # for N > 1 ONE int64 MIN all-reduce (NCCL).  Captured in a CUDA graph.
     def step(ev_k0=None, ev_k1=None):
-        D.key_reset(best)
+        nvtx.range_push("grid_search")
+        D.key_reset(best, signed=True)
         if ev_k0 is not None:
             ev_k0.record(stream)
-        D.eval_grid(model, cfg.inputs, cfg.n_samples, cfg.seed, b, e, net=net, best=best)
+        D.eval_grid(model, cfg.inputs, cfg.n_samples, cfg.seed, b, e, net=net, best=best, signed_key=True)
         if ev_k1 is not None:
             ev_k1.record(stream)
+        nvtx.range_pop()
         if world > 1:
-            D.best_allreduce(best)
+            nvtx.range_push("key_allreduce")
+            D.best_allreduce(best, signed=True)
+            nvtx.range_pop()
 
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
     barrier()
 
+    graph, graph_note = None, None
+    launches_per_step = None
+    if not args.no_graph and (world == 1 or args.dist_backend == "nccl"):
+        try:
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                step()
+            stream.wait_stream(side)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            l0 = D.launch_count()
+            with torch.cuda.graph(g):
+                step()
+            launches_per_step = D.launch_count() - l0
+            g.replay()
+            torch.cuda.synchronize()
+            graph = g
+            graph_note = "reset + kernel + all-reduce captured in one CUDA graph, replayed per step"
+        except Exception as exc:     # fall back to eager steps, say so in the JSON line
+            graph_note = f"eager steps (graph capture failed: {repr(exc)[:160]})"
+            torch.cuda.synchronize()
+    else:
+        graph_note = "eager steps (--no-graph or a non-NCCL backend)"
+    barrier()
+
     sampler = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
     sampler.start()
     time.sleep(0.3)
     K = args.steps
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-            torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     launches0 = D.launch_count()
     torch.cuda.synchronize()
     barrier()
     for s in range(K):
         flush.fill_(float(s))                       # L2 flush between timed steps (outside the step events)
-        evs[s][0].record(stream)
-        step(evs[s][1], evs[s][2])
-        evs[s][3].record(stream)
+        ev[s][0].record(stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+        ev[s][1].record(stream)
     torch.cuda.synchronize()
     barrier()
-    launches = D.launch_count() - launches0
+    launches = (launches_per_step * K) if graph is not None else (D.launch_count() - launches0)
+    step_ms = [ev[s][0].elapsed_time(ev[s][1]) for s in range(K)]
+    # kernel-only events (eager steps, same flush): the roofline's per-launch duration
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for s in range(K):
+        flush.fill_(float(s))
+        step(kev[s][0], kev[s][1])
+    torch.cuda.synchronize()
+    barrier()
     clocks = sampler.stop()
-    # effective SM clock right after the timed region (clock64 / globaltimer, one block per SM),
-    # run after a few more steps so the clock state is the loaded one
+    kern_ms = [kev[s][0].elapsed_time(kev[s][1]) for s in range(K)]
+    # effective SM clock right after the timed region (clock64 / globaltimer, one block per SM)
     for _ in range(3):
         step()
     from paper_2110_15425_b200.api import sm_clock_mhz
     clocks["sm_mhz_effective_probe"] = sm_clock_mhz(300)
-    step_ms = [evs[s][0].elapsed_time(evs[s][3]) for s in range(K)]
-    kern_ms = [evs[s][1].elapsed_time(evs[s][2]) for s in range(K)]
-    ms_step = max_over_ranks(sum(step_ms) / K)
-    ms_kern = max_over_ranks(sum(kern_ms) / K)
+    ms_step = max_over_ranks(statistics.median(step_ms))
+    ms_kern = max_over_ranks(statistics.median(kern_ms))
     evals = cfg.n_alloc * cfg.n_samples
     value = evals / (ms_step / 1e3)
-    key = key_from_tensor(best)
+    key = key_from_tensor(best, signed=True)
     best_cost, best_idx = D.key_decode(key)
 
     # ---- e2e: host-buffer C-ABI call per rank (+ key all-reduce across ranks), every step
@@ -295,13 +385,15 @@ def run_ours(args):
     for _ in range(max(1, args.warmup)):
         e2e_step()
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    e_ms = []
     for _ in range(K):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         e2e_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / K)
+        e1.record(stream)
+        e1.synchronize()
+        e_ms.append(e0.elapsed_time(e1))
+    e2e_ms = max_over_ranks(statistics.median(e_ms))
     barrier()
 
     also = {}
@@ -325,19 +417,36 @@ def run_ours(args):
     sm_max = clocks.get("sm_max_mhz") or 1965.0
     peak = n_sm * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12               # TFLOP/s at max clock
     flops_launch = count * (cfg.n_samples * FLOPS_PER_SAMPLE + FLOPS_PER_ALLOC) + FLOPS_PER_CALL
+    flops_method = count * (cfg.n_samples * FLOPS_PER_SAMPLE_METHOD + FLOPS_PER_ALLOC_METHOD) + FLOPS_PER_CALL_METHOD
+    flops_exec = count * (cfg.n_samples * FLOPS_PER_SAMPLE_EXEC + FLOPS_PER_ALLOC_METHOD) + FLOPS_PER_CALL_EXEC
     achieved = flops_launch / (ms_kern / 1e3) / 1e12
+    achieved_method = flops_method / (ms_kern / 1e3) / 1e12
+    achieved_exec = flops_exec / (ms_kern / 1e3) / 1e12
     sm_load = clocks.get("sm_mhz")
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r01_pp_traffic.json")
     if os.path.exists(tpath):   # dram read + write per launch from the committed ncu --set full capture
         t = json.load(open(tpath))
         traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
+    per_gpu_evals_s = count * cfg.n_samples / (ms_kern / 1e3)
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "frac_method": achieved / peak,
+            "flop_count": f"SURVEY §8(d)'s per-unit figure: {FLOPS_PER_SAMPLE} flop per evaluation (fma = 2, "
+                          f"add/mul/sqrt/div = 1) + {FLOPS_PER_ALLOC} per allocation",
+            "achieved_counted_method": achieved_method, "frac_counted_method": achieved_method / peak,
+            "counted_method_flop_count": f"{FLOPS_PER_SAMPLE_METHOD} flop per evaluation counted by the oracle's "
+                                         "counting build in method mode (sqrt_spec = 1, rsqrt_spec = 2)",
+            "achieved_executed": achieved_exec, "frac_executed": achieved_exec / peak,
+            "executed_flop_count": f"{FLOPS_PER_SAMPLE_EXEC} flop per evaluation as the spec executes it "
+                                   "(Newton / Goldschmidt steps of rsqrt_spec and sqrt_spec included)",
+            "evals_per_s_per_gpu": per_gpu_evals_s,
+            "evals_per_s_vs_survey_50pct_point": per_gpu_evals_s / EVALS_PER_S_AT_50PCT,
             "traffic": traffic, "traffic_source": "profiles/r01_pp_traffic.json (ncu --set full, cfg3)",
             "algorithmic_bytes_per_launch": count * 4 + 8 + sum(cfg.n_levels) * 4,
             "kernel": "pp_eval_grid_kernel", "kernel_ms": ms_kern,
             "algorithmic_flops_per_launch": flops_launch,
-            "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz (max clock)",
+            "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz (max clock; "
+                          "MEASURED_PEAKS.json has no FP32 entry and the guide gives no FP32 fallback)",
             "frac_at_measured_clock": (achieved / (n_sm * FP32_LANES_PER_SM * 2 * sm_load * 1e6 / 1e12)
                                        if sm_load else None),
             "frac_at_probe_clock": achieved / (n_sm * FP32_LANES_PER_SM * 2 * clocks["sm_mhz_effective_probe"]
@@ -353,12 +462,13 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         cpu = oracle_rate(cfg)
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-           "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
            "dtype": "f32", "data": "synthetic",
-           "config": {"workload": cfg.name, "grid": list(cfg.n_levels), "samples": cfg.n_samples,
-                      "allocations": cfg.n_alloc, "allocations_per_gpu": count, "parallelism": f"grid-dp{world}",
+           "config": workload_config(cfg, world),
+           "timing": {"step": graph_note, "statistic": "median over steps, max over ranks",
                       "l2": "flushed (512 MiB write) before every timed step, outside the step events",
-                      "best": {"index": best_idx, "cost": best_cost}},
+                      "allocations_per_gpu": count},
+           "result": {"best_index": best_idx, "best_cost": best_cost, "key": f"{key:016x}"},
            "roofline": roof, "cpu_baseline": cpu,
            "e2e": {"value": evals / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
@@ -392,25 +502,52 @@ def run_extras(D, torch, dev, rank, world, args):
     ddm_once()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 3
-    e0.record()
-    for _ in range(reps):
+    reps = []
+    for _ in range(5):
+        e0.record()
         ddm_once()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+        e1.record()
+        torch.cuda.synchronize()
+        reps.append(e0.elapsed_time(e1))
+    ms = statistics.median(reps)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     nb = d.n_rt_bins
     up, lo = int(rh[:nb].sum()), int(rh[nb:2 * nb].sum())
-    tf = DDM_FLOPS_PER_STEP * d.n_trials * d.n_steps / (ms / 1e3) / 1e12
-    out["ddm_cfg2"] = {"trials_per_s": d.n_trials / (ms / 1e3), "steps_per_s": d.n_trials * d.n_steps / (ms / 1e3),
-                       "ms": ms, "error_rate": lo / max(1, up + lo),
+    steps_s = d.n_trials * d.n_steps / (ms / 1e3)
+    out["ddm_cfg2"] = {"trials_per_s": d.n_trials / (ms / 1e3), "steps_per_s": steps_s,
+                       "ms": ms, "timing": "median of 5 passes", "error_rate": lo / max(1, up + lo),
                        "mean_rt_s": (int(rs[0]) + int(rs[1])) / max(1, up + lo) * d.dt,
-                       "algorithmic_tflops": tf, "frac_fp32_peak": tf / FP32_PEAK_NOMINAL,
-                       "flops_per_step": DDM_FLOPS_PER_STEP}
+                       "algorithmic_tflops": DDM_FLOPS_PER_STEP * steps_s / 1e12,
+                       "frac_fp32_peak": DDM_FLOPS_PER_STEP * steps_s / 1e12 / FP32_PEAK_NOMINAL,
+                       "frac_fp32_peak_executed": DDM_FLOPS_PER_STEP_EXEC * steps_s / 1e12 / FP32_PEAK_NOMINAL,
+                       "flops_per_step": DDM_FLOPS_PER_STEP, "flops_per_step_executed": DDM_FLOPS_PER_STEP_EXEC}
+    # cfg5 (8e6 x 100) whole on one GPU: t1 of the strong-scaling series and the key every
+    # N-GPU run must reproduce (BASELINE configs[4])
+    if world == 1:
+        c5 = W.pp_cfg5()
+        m5 = D.load_model(W.KIND_PREDATOR_PREY, c5.n_levels, c5.levels, c5.w, c5.params, device=dev.index)
+        n5 = torch.empty(c5.n_alloc, dtype=torch.float32, device=dev)
+        k5 = torch.empty(1, dtype=torch.int64, device=dev)
+        t5 = []
+        for r in range(4):
+            D.key_reset(k5)
+            e0.record()
+            D.eval_grid(m5, c5.inputs, c5.n_samples, c5.seed, net=n5, best=k5)
+            e1.record()
+            torch.cuda.synchronize()
+            if r:
+                t5.append(e0.elapsed_time(e1))
+        from paper_2110_15425_b200.api import key_from_tensor as _kft
+        k = _kft(k5)
+        c5cost, c5idx = D.key_decode(k)
+        ms5 = statistics.median(t5)
+        out["pp_cfg5_1gpu"] = {"ms": ms5, "evals_per_s": c5.evals / (ms5 / 1e3), "key": f"{k:016x}",
+                               "best_index": c5idx, "best_cost": c5cost,
+                               "note": "the whole cfg5 grid on one GPU: t1 of the strong series (N > 1 "
+                                       "runs shard this grid and must print the same key)"}
     # NEXT-1 over the sharded weak-scaling grid: per step a shard search, one key
     # all-reduce and the (replicated) step kernel on every rank
     if world > 1:
@@ -557,6 +694,7 @@ def run_extras(D, torch, dev, rank, world, args):
         from paper_2110_15425_b200.api import key_from_tensor
         cost, idx = D.key_decode(key_from_tensor(best))
         tf = STROOP_FLOPS_PER_STEP * c.evals * c.n_steps / (ms / 1e3) / 1e12
+        tf_exec = STROOP_FLOPS_PER_STEP_EXEC * c.evals * c.n_steps / (ms / 1e3) / 1e12
         # NEXT-3: Extended Stroop A on the cfg4 control grid, 1e4 trials per allocation
         g = W.ext_stroop_grid()
         mx = D.load_model(W.KIND_EXT_STROOP_A, g.n_levels, g.levels, g.w, g.params, device=dev.index)
@@ -595,7 +733,9 @@ def run_extras(D, torch, dev, rank, world, args):
         out["stroop_cfg4"] = {"evals_per_s": c.evals / (ms / 1e3),
                               "step_updates_per_s": c.evals * c.n_steps / (ms / 1e3), "ms": ms,
                               "algorithmic_tflops": tf, "frac_fp32_peak": tf / FP32_PEAK_NOMINAL,
+                              "frac_fp32_peak_executed": tf_exec / FP32_PEAK_NOMINAL,
                               "flops_per_step": STROOP_FLOPS_PER_STEP,
+                              "flops_per_step_executed": STROOP_FLOPS_PER_STEP_EXEC,
                               "best": {"index": idx, "u_c_level": idx // c.n_levels[1],
                                        "u_s_level": idx % c.n_levels[1], "net_value": -cost}}
     return out
@@ -617,9 +757,14 @@ def main():
                     help="collective backend for N > 1 (gloo only to exercise the multi-rank path on one GPU)")
     ap.add_argument("--device", type=int, default=None,
                     help="force every rank onto this CUDA device (multi-rank path test on one GPU, with gloo)")
+    ap.add_argument("--strong", action="store_true", help="N = 1: the whole cfg5 grid (t1 of the strong series)")
+    ap.add_argument("--weak", action="store_true", help="~1e6 allocations per GPU instead of cfg5 for N > 1")
+    ap.add_argument("--no-graph", action="store_true", help="eager steps instead of the CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_spawn(args)
     return run_ours(args)
 
 

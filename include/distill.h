@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define DISTILL_ABI_VERSION 1
+#define DISTILL_ABI_VERSION 2   /* 2: distill_eval_args.key_order, distill_key_reset_signed */
 
 typedef enum {
     DISTILL_OK = 0,
@@ -50,6 +50,10 @@ typedef enum {
 
 /* "No candidate" value of a packed (value, index) key; initialise d_best to it. */
 #define DISTILL_KEY_INIT 0xFFFFFFFFFFFFFFFFull
+/* The same in the signed key order (key_order = 1: stored word = key ^ 2^63,
+ * so int64 MIN order = key order; P:352 per-segment results combined across
+ * GPUs by one int64 MIN all-reduce with no conversion); = INT64_MAX. */
+#define DISTILL_KEY_INIT_SIGNED 0x7FFFFFFFFFFFFFFFull
 
 typedef struct distill_model distill_model;  /* opaque, library-owned */
 
@@ -93,6 +97,10 @@ typedef struct {
                                     PP: unused (NULL)                                                  */
     uint32_t trial_begin, trial_end; /* Stroop: simulate trials [trial_begin, trial_end) only; (0,0) = all.
                                     d_net/d_best are produced only when the range is all T trials.    */
+    uint32_t key_order;          /* 0: d_best is combined as unsigned keys (atomicMin u64; init
+                                    DISTILL_KEY_INIT).  1: signed order — d_best holds key ^ 2^63,
+                                    combined by atomicMin on int64 (init DISTILL_KEY_INIT_SIGNED), ready
+                                    for an int64 MIN all-reduce across ranks.  Other values: E_INVALID_ARG */
 } distill_eval_args;
 
 /* DDM Monte Carlo batch (Fig. 3; spec/MODELS.md §4). */
@@ -246,6 +254,9 @@ distill_status distill_argmax_ties(const float* d_values, uint64_t n, uint64_t i
                                    unsigned long long* d_tie, void* stream);
 /* Set *d_best = DISTILL_KEY_INIT (stream-ordered). */
 distill_status distill_key_reset(unsigned long long* d_best, void* stream);
+/* d_best <- DISTILL_KEY_INIT_SIGNED (signed key order; stream-ordered, two memsets,
+ * CUDA-graph capturable).  d_best: device, 8-byte aligned. */
+distill_status distill_key_reset_signed(unsigned long long* d_best, void* stream);
 /* Host, pure: key -> (cost C, global index).  DISTILL_E_NO_VALID for an all-NaN/empty key. */
 distill_status distill_key_decode(unsigned long long key, float* cost, uint64_t* index);
 

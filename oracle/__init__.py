@@ -20,15 +20,21 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "distill_oracle.c")
 _HDR = os.path.join(_HERE, "distill_oracle.h")
-LIB = os.path.join(_HERE, "liboracle.so")
-LIB_COUNT = os.path.join(_HERE, "liboracle_count.so")
+# DISTILL_ORACLE_SANITIZE=1: build and load ASan/UBSan-instrumented copies
+# (`make sanitize-oracle` runs the CPU suite that way; needs libasan preloaded)
+_SAN = os.environ.get("DISTILL_ORACLE_SANITIZE") == "1"
+_SUFFIX = "_asan" if _SAN else ""
+LIB = os.path.join(_HERE, f"liboracle{_SUFFIX}.so")
+LIB_COUNT = os.path.join(_HERE, f"liboracle_count{_SUFFIX}.so")
 CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-mfma",
           "-fPIC", "-shared", "-Wall"]
+SAN_CFLAGS = ["-g", "-fno-omit-frame-pointer", "-fsanitize=address,undefined", "-fno-sanitize-recover=undefined"]
 
 
 def build(force: bool = False) -> None:
     """Compile the oracle (and its flop-counting twin) with gcc."""
-    for out, extra in ((LIB, []), (LIB_COUNT, ["-DOD_COUNT_FLOPS"])):
+    san = SAN_CFLAGS if _SAN else []
+    for out, extra in ((LIB, san), (LIB_COUNT, ["-DOD_COUNT_FLOPS", *san])):
         if (not force and os.path.exists(out)
                 and os.path.getmtime(out) >= max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))):
             continue
@@ -96,6 +102,7 @@ def _bind(path: str) -> C.CDLL:
                                          _u32p]),
         "od_flops_read": (C.c_ulonglong, []),
         "od_flops_reset": (None, []),
+        "od_flops_method": (None, [C.c_int]),
         "od_is_counting_build": (C.c_int, []),
     }
     for name, (res, args) in sig.items():
@@ -239,11 +246,11 @@ def pp_trace_f64(n_levels, levels, params, inputs, i, n_samples, seed, invocatio
 
 
 def pp_eval_threads(n_levels, levels, w, params, inputs, begin, end, n_samples, seed,
-                    invocation=0, threads=1) -> np.ndarray:
+                    invocation=0, threads=1, f64=False) -> np.ndarray:
     """Contiguous segments over Python threads (ctypes drops the GIL) — the
-    paper's multicore scheme.  Timing helper only."""
+    paper's multicore scheme; f64 = the binary64 re-evaluation."""
     n = int(end) - int(begin)
-    out = np.zeros(n, np.float32)
+    out = np.zeros(n, np.float64 if f64 else np.float32)
     threads = max(1, min(int(threads), max(n, 1)))
     seg = (n + threads - 1) // threads
     args = (_u32(n_levels), _f32(levels), _f32(w), _f32(params), _f32(inputs))
@@ -255,8 +262,8 @@ def pp_eval_threads(n_levels, levels, w, params, inputs, begin, end, n_samples, 
         if e <= b:
             return
         view = out[b - begin:e - begin]
-        L.od_pp_eval(*args, b, e, int(n_samples), int(seed), int(invocation),
-                     view.ctypes.data_as(C.c_void_p))
+        (L.od_pp_eval_f64 if f64 else L.od_pp_eval)(*args, b, e, int(n_samples), int(seed), int(invocation),
+                                                   view.ctypes.data_as(C.c_void_p))
 
     ts = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
     for t in ts:

@@ -24,10 +24,24 @@
 
 #ifdef OD_COUNT_FLOPS
 static _Thread_local unsigned long long od_flops;
-#define CNT(n) (od_flops += (n))
+/* method-count mode: sqrt_spec counts as 1 flop and rsqrt_spec
+ * as 2 (a square root and a divide) instead of their Newton/Goldschmidt steps */
+static _Thread_local int od_method, od_quiet;
+#define CNT(n) (od_quiet ? (void)0 : (void)(od_flops += (n)))
+#define METHOD_BEGIN() do { if (od_method) ++od_quiet; } while (0)
+#define METHOD_END(n) do { if (od_method) { --od_quiet; CNT(n); } } while (0)
 #else
 #define CNT(n) ((void)0)
+#define METHOD_BEGIN() ((void)0)
+#define METHOD_END(n) ((void)0)
 #endif
+void od_flops_method(int on) {
+#ifdef OD_COUNT_FLOPS
+    od_method = on;
+#else
+    (void)on;
+#endif
+}
 unsigned long long od_flops_read(void) {
 #ifdef OD_COUNT_FLOPS
     return od_flops;
@@ -108,6 +122,7 @@ float od_ln(float x) {
 /* spec/RNG.md §4: rsqrt_spec                                                */
 /* ------------------------------------------------------------------------ */
 float od_rsqrt(float x) {
+    METHOD_BEGIN();
     float y = u2f(0x5F375A86u - (f2u(x) >> 1));
     float h = FMUL(0.5f, x);
     for (int k = 0; k < 3; ++k) {
@@ -115,11 +130,13 @@ float od_rsqrt(float x) {
         float r = FFMA(-p, y, 0.5f);
         y = FFMA(y, r, y);
     }
+    METHOD_END(2);
     return y;
 }
 
 /* spec/RNG.md §4: sqrt_spec — Goldschmidt from the rsqrt seed (Box-Muller radius) */
 float od_sqrt(float x) {
+    METHOD_BEGIN();
     float y = u2f(0x5F375A86u - (f2u(x) >> 1));
     float g = FMUL(x, y);
     float h = FMUL(0.5f, y);
@@ -129,7 +146,9 @@ float od_sqrt(float x) {
         h = FFMA(h, r, h);
     }
     float r = FFMA(-g, h, 0.5f);
-    return FFMA(g, r, g);
+    g = FFMA(g, r, g);
+    METHOD_END(1);
+    return g;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -164,6 +164,8 @@ int od_ext_stroop_eval(int variant, const uint32_t n_levels[2], const float* lev
                        uint64_t* counts, float* net);
 
 /* ---- flop counting (only meaningful in the -DOD_COUNT_FLOPS build) ---- */
+/* Counting build: 1 = method count (sqrt_spec = 1 flop, rsqrt_spec = 2), 0 = executed ops (default). */
+void od_flops_method(int on);
 unsigned long long od_flops_read(void);
 void od_flops_reset(void);
 int od_is_counting_build(void);

@@ -23,11 +23,11 @@ control grid (workloads.KIND_*); eval_grid evaluates any of them.
 Importing this package does not touch the GPU; the shared library is loaded
 on first use and there is no CPU fallback.
 """
-from .api import (KEY_INIT, AmrRun, EpisodeRun, Model, best, grid_search, stroop_energy, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_multi, key_decode,
+from .api import (KEY_INIT, key_from_tensor, AmrRun, EpisodeRun, Model, best, grid_search, stroop_energy, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_multi, key_decode,
                   key_reset, launch_count, load_model, pp_amr, pp_episode)
 from .dist import (best_allreduce, hist_allreduce, key_to_i64, i64_to_key, pp_amr_sharded, pp_episode_sharded,
                    shard_range)
 
-__all__ = ["KEY_INIT", "Model", "best", "grid_search", "stroop_energy", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "eval_grid_multi", "key_decode", "pp_episode", "pp_amr",
+__all__ = ["KEY_INIT", "key_from_tensor", "Model", "best", "grid_search", "stroop_energy", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "eval_grid_multi", "key_decode", "pp_episode", "pp_amr",
            "key_reset", "launch_count", "load_model", "best_allreduce", "hist_allreduce", "key_to_i64",
            "i64_to_key", "shard_range", "pp_episode_sharded", "EpisodeRun", "pp_amr_sharded", "AmrRun"]

@@ -17,6 +17,8 @@ OK, E_INVALID_ARG, E_OVERFLOW, E_UNSUPPORTED, E_CUDA, E_NO_VALID = range(6)
 MODEL_PREDATOR_PREY = 1
 MODEL_STROOP_LCA = 2
 KEY_INIT = 0xFFFFFFFFFFFFFFFF
+KEY_INIT_SIGNED = 0x7FFFFFFFFFFFFFFF      # signed key order: stored word = key ^ 2^63
+ABI_VERSION = 2                           # include/distill.h DISTILL_ABI_VERSION
 
 
 class DistillError(RuntimeError):
@@ -37,7 +39,7 @@ class EvalArgs(C.Structure):
                 ("begin", C.c_uint64), ("end", C.c_uint64),
                 ("n_samples", C.c_uint32), ("invocation", C.c_uint32), ("seed", C.c_uint64),
                 ("d_net", C.c_void_p), ("d_best", C.c_void_p), ("d_counts", C.c_void_p),
-                ("trial_begin", C.c_uint32), ("trial_end", C.c_uint32)]
+                ("trial_begin", C.c_uint32), ("trial_end", C.c_uint32), ("key_order", C.c_uint32)]
 
 
 class DdmArgs(C.Structure):
@@ -84,6 +86,7 @@ EXPORTS = {
     "distill_argmax_ties": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p,
                                       C.c_void_p, C.c_void_p]),
     "distill_key_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "distill_key_reset_signed": (C.c_int, [C.c_void_p, C.c_void_p]),
     "distill_key_decode": (C.c_int, [C.c_uint64, C.POINTER(C.c_float), C.POINTER(C.c_uint64)]),
     "distill_ddm_batch": (C.c_int, [C.POINTER(DdmArgs), C.c_void_p]),
     "distill_launch_count": (C.c_uint64, []),
@@ -119,6 +122,8 @@ def lib() -> C.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        if L.distill_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {L.distill_abi_version()}, the binding needs {ABI_VERSION}: rebuild")
         _lib = L
     return _lib
 

@@ -105,8 +105,12 @@ def load_model(kind, n_levels, levels, cost_weights, params, device: int = 0) ->
 
 
 def eval_grid(model: Model, inputs, n_samples: int, seed: int, begin: int = 0, end: Optional[int] = None,
-              net=None, best=None, invocation: int = 0, counts=None, trial_range=(0, 0), stream=None) -> None:
-    """distill_eval_grid: allocations [begin, end) -> net[end-begin] (V = -C), best (atomicMin key)."""
+              net=None, best=None, invocation: int = 0, counts=None, trial_range=(0, 0), stream=None,
+              signed_key: bool = False) -> None:
+    """distill_eval_grid: allocations [begin, end) -> net[end-begin] (V = -C), best (atomicMin key).
+
+    signed_key: best holds key ^ 2^63 (key_order = 1; reset it with key_reset(best, signed=True)),
+    so an int64 MIN all-reduce combines shards with no conversion."""
     end = model.n_alloc if end is None else int(end)
     n = end - int(begin)
     inp = np.ascontiguousarray(np.asarray(inputs if inputs is not None else np.zeros(0), np.float32))
@@ -118,6 +122,7 @@ def eval_grid(model: Model, inputs, n_samples: int, seed: int, begin: int = 0, e
     a.d_net = _dev_ptr(net, "net", n)
     a.d_best = _dev_ptr(best, "best", 1)
     a.trial_begin, a.trial_end = int(trial_range[0]), int(trial_range[1])
+    a.key_order = 1 if signed_key else 0
     if counts is None and model.kind != _abi.MODEL_PREDATOR_PREY:
         import torch
         with _on_stream(stream):      # freed on return: stream-ordered reuse only
@@ -229,9 +234,11 @@ def argmax_ties(values, index_base: int, seed: int, invocation: int, best, tie, 
                                         _dev_ptr(tie, "tie", 1), _stream_handle(stream, values.device.index)))
 
 
-def key_reset(best, stream=None) -> None:
+def key_reset(best, stream=None, signed: bool = False) -> None:
+    """best <- DISTILL_KEY_INIT (or DISTILL_KEY_INIT_SIGNED for the signed key order)."""
+    fn = lib().distill_key_reset_signed if signed else lib().distill_key_reset
     with _on_device(best):
-        check(lib().distill_key_reset(_dev_ptr(best, "best", 1), _stream_handle(stream, best.device.index)))
+        check(fn(_dev_ptr(best, "best", 1), _stream_handle(stream, best.device.index)))
 
 
 def key_decode(key: int):
@@ -375,9 +382,11 @@ def launch_count() -> int:
     return int(lib().distill_launch_count())
 
 
-def key_from_tensor(best) -> int:
-    """Raw unsigned key from an int64 tensor (one device->host read)."""
-    return int(best.reshape(-1)[0].item()) & (2 ** 64 - 1)
+def key_from_tensor(best, signed: bool = False) -> int:
+    """Raw unsigned key from an int64 tensor (one device->host read); signed=True
+    undoes the signed key order (bit 63 flipped)."""
+    k = int(best.reshape(-1)[0].item()) & (2 ** 64 - 1)
+    return k ^ (1 << 63) if signed else k
 
 
 __all__ = ["KEY_INIT", "stroop_energy", "AmrRun", "DistillError", "EpisodeRun", "Model", "grid_search", "best", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",

@@ -316,6 +316,7 @@ static distill_status launch_pp(const distill_model* m, const distill_eval_args*
     p.invocation = a->invocation;
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
     p.net = a->d_net; p.best = a->d_best;
+    p.key_signed = a->key_order;
     p.publish = publish; p.done = done;
     launch_pp_search(m, p, 1, st);
     CUDA_TRY(cudaGetLastError());
@@ -381,6 +382,7 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
     p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
     p.levels = m->d_levels; p.counts = counts; p.net = a->d_net; p.best = a->d_best;
+    p.key_signed = a->key_order;
     const uint32_t tr = te - tb;
     if (tr > 0) {
         // enough blocks along trials to fill the machine, capped so each thread runs >= 1 trial
@@ -498,6 +500,7 @@ static distill_status launch_ext_stroop(distill_model* m, const distill_eval_arg
     p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
     p.levels = m->d_levels; p.counts = counts; p.net = a->d_net; p.best = a->d_best;
+    p.key_signed = a->key_order;
     const uint32_t tr = te - tb;
     uint32_t chunks = std::max<uint32_t>(1, (tr + STROOP_BLOCK - 1) / STROOP_BLOCK);
     const uint64_t want = (uint64_t)m->n_sm * 8 * 64;
@@ -519,6 +522,7 @@ distill_status distill_eval_grid(const distill_model* mc, const distill_eval_arg
         return fail(DISTILL_E_INVALID_ARG, "eval_grid: d_net must be 4-byte aligned");
     if (a->d_best && (reinterpret_cast<uintptr_t>(a->d_best) & 7u))
         return fail(DISTILL_E_INVALID_ARG, "eval_grid: d_best must be 8-byte aligned");
+    if (a->key_order > 1) return fail(DISTILL_E_INVALID_ARG, "eval_grid: key_order must be 0 or 1");
     DEVICE_SCOPE(m->device);
     cudaStream_t st = (cudaStream_t)stream;
     if (m->kind == DISTILL_MODEL_PREDATOR_PREY) return launch_pp(m, a, st);
@@ -829,6 +833,15 @@ distill_status distill_sm_clock_probe(uint32_t micros, double* h_mhz, void* stre
 distill_status distill_key_reset(unsigned long long* d_best, void* stream) {
     if (!d_best) return fail(DISTILL_E_INVALID_ARG, "key_reset: NULL");
     CUDA_TRY(cudaMemsetAsync(d_best, 0xFF, sizeof(unsigned long long), (cudaStream_t)stream));
+    return DISTILL_OK;
+}
+
+distill_status distill_key_reset_signed(unsigned long long* d_best, void* stream) {
+    if (!d_best) return fail(DISTILL_E_INVALID_ARG, "key_reset_signed: NULL");
+    if (reinterpret_cast<uintptr_t>(d_best) & 7u) return fail(DISTILL_E_INVALID_ARG, "key_reset_signed: misaligned");
+    // INT64_MAX little-endian: seven 0xFF bytes, then 0x7F
+    CUDA_TRY(cudaMemsetAsync(d_best, 0xFF, 7, (cudaStream_t)stream));
+    CUDA_TRY(cudaMemsetAsync(reinterpret_cast<unsigned char*>(d_best) + 7, 0x7F, 1, (cudaStream_t)stream));
     return DISTILL_OK;
 }
 

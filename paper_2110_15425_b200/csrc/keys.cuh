@@ -11,6 +11,10 @@ namespace distill {
 
 typedef unsigned long long key64_t;
 constexpr key64_t KEY_INIT = 0xFFFFFFFFFFFFFFFFull;
+// Signed key order (distill_eval_args.key_order = 1): the stored word is
+// key ^ 2^63, so signed int64 order equals the unsigned key order and the
+// per-GPU result feeds an int64 MIN all-reduce (torch/NCCL) as it is.
+constexpr key64_t KEY_SIGN = 0x8000000000000000ull;
 
 // key(C, i) = ord(canon(C)) << 32 | i : min key = lowest cost, then lowest index.
 __device__ __forceinline__ key64_t make_key(float C, uint32_t idx) {
@@ -33,10 +37,11 @@ __device__ __forceinline__ key64_t warp_min_key(key64_t k) {
     return k;
 }
 
-// Block-wide min of one key per thread, then ONE atomicMin per block.
-// All threads of the block must call it (uses __syncthreads).
+// Block-wide min of one key per thread, then ONE atomicMin per block (in the
+// signed order when `signed_order`).  All threads of the block must call it
+// (uses __syncthreads).
 template <int BLOCK>
-__device__ __forceinline__ void block_min_key_atomic(key64_t k, key64_t* dst) {
+__device__ __forceinline__ void block_min_key_atomic(key64_t k, key64_t* dst, bool signed_order = false) {
     __shared__ key64_t s_warp[BLOCK / 32];
     k = warp_min_key(k);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -45,7 +50,10 @@ __device__ __forceinline__ void block_min_key_atomic(key64_t k, key64_t* dst) {
     if (wid == 0) {
         k = lane < BLOCK / 32 ? s_warp[lane] : KEY_INIT;
         k = warp_min_key(k);
-        if (lane == 0 && k != KEY_INIT) atomicMin(dst, k);
+        if (lane == 0 && k != KEY_INIT) {
+            if (signed_order) atomicMin(reinterpret_cast<long long*>(dst), (long long)(k ^ KEY_SIGN));
+            else atomicMin(dst, k);
+        }
     }
 }
 

@@ -42,6 +42,7 @@ struct PPArgs {
     uint32_t n_sets = 1;                               // multi: position sets; invocation t uses set t mod n_sets
     key64_t* publish = nullptr;                        // PUB: device alias of a mapped pinned host key
     unsigned int* done = nullptr;                      // PUB: block-completion counter (0 between launches)
+    uint32_t key_signed = 0;                           // 1: best holds key ^ 2^63 (int64 MIN order)
 };
 
 // Multi-invocation launches (distill_eval_grid_multi) put invocation t on
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs 
         if (a.net) a.net[tid] = -C;
         key = make_key(C, i);
     }
-    if (a.best) block_min_key_atomic<WARPS * 32>(key, a.best);
+    if (a.best) block_min_key_atomic<WARPS * 32>(key, a.best, a.key_signed != 0);
     if (PUB && threadIdx.x == 0) pp_publish_key(a0);
 }
 
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs 
     const size_t row = MULTI ? (size_t)blockIdx.y : 0;
     if (a0.net && tid < a0.count) a0.net[row * a0.count + tid] = -C;
     // a9: (value, index) argmin -> one atomic per block
-    if (a0.best) block_min_key_atomic<BLOCK>(key, a0.best + row);
+    if (a0.best) block_min_key_atomic<BLOCK>(key, a0.best + row, a0.key_signed != 0);
     if (PUB && threadIdx.x == 0) pp_publish_key(a0);
 }
 

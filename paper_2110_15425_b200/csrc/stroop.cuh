@@ -25,6 +25,7 @@ struct StroopArgs {
     unsigned long long* __restrict__ counts;   // [count][3]
     float* __restrict__ net;
     key64_t* __restrict__ best;
+    uint32_t key_signed;     // 1: best holds key ^ 2^63 (int64 MIN order)
 };
 
 // One LCA step of both response units (spec/MODELS.md §6 loop body; the old
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(BLOCK) stroop_finalize_kernel(const StroopArgs
         if (a.net) a.net[t] = V;
         k = make_key(-V, i);
     }
-    if (a.best) block_min_key_atomic<BLOCK>(k, a.best);
+    if (a.best) block_min_key_atomic<BLOCK>(k, a.best, a.key_signed != 0);
 }
 
 // ---------------------------------------------------------------- NEXT-3
@@ -263,6 +264,7 @@ struct ExtStroopArgs {
     unsigned long long* __restrict__ counts;   // [count][3] {n_both, n_undecided, rt_sum}
     float* __restrict__ net;
     key64_t* __restrict__ best;
+    uint32_t key_signed;     // 1: best holds key ^ 2^63 (int64 MIN order)
 };
 
 __device__ __forceinline__ void ddm_latch(float x, float z, uint32_t n, int& hit, uint32_t& st) {
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_finalize_kernel(const ExtStr
         if (a.net) a.net[t] = V;
         k = make_key(-V, i);
     }
-    if (a.best) block_min_key_atomic<BLOCK>(k, a.best);
+    if (a.best) block_min_key_atomic<BLOCK>(k, a.best, a.key_signed != 0);
 }
 
 }  // namespace distill

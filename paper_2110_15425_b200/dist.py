@@ -39,11 +39,16 @@ def i64_to_key(v: int) -> int:
     return (int(v) & MASK) ^ SIGN
 
 
-def best_allreduce(best, group=None):
+def best_allreduce(best, group=None, signed: bool = False):
     """In-place: global min key across ranks.  `best` is an int64 tensor with the
-    raw key bits; flips bit 63 so signed MIN == unsigned min, all-reduces, flips back."""
+    raw key bits; flips bit 63 so signed MIN == unsigned min, all-reduces, flips back.
+    signed=True: `best` already holds the signed key order (eval_grid(...,
+    signed_key=True) writes it from the kernel), so it is ONE all-reduce and nothing else."""
     import torch
     import torch.distributed as dist
+    if signed:
+        dist.all_reduce(best, op=dist.ReduceOp.MIN, group=group)
+        return best
     flip = torch.tensor(-(1 << 63), dtype=torch.int64, device=best.device)
     best.bitwise_xor_(flip)
     dist.all_reduce(best, op=dist.ReduceOp.MIN, group=group)

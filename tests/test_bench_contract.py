@@ -25,6 +25,8 @@ def test_reference_arm_json_contract():
     assert d["e2e"] == {"value": d["value"], "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("pp_cfg3")
     import bench
+    import workloads as W
+    assert d["config"] == bench.workload_config(W.pp_cfg3(), 1)      # the same config object as our arm
     assert d["metric"] == bench.METRIC
     baseline = json.load(open(os.path.join(ROOT, "BASELINE.json")))
     assert d["metric"] == baseline["metric"]

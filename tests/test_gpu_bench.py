@@ -25,16 +25,45 @@ def test_bench_json_contract_on_gpu():
         assert k in d, k
     assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["scaling"] == "weak"
     assert d["config"]["workload"].startswith("pp_cfg3") and d["vs_baseline"] is None
+    per_gpu = d["timing"]["allocations_per_gpu"]
+    assert per_gpu == d["config"]["allocations"] == 10 ** 6
+    assert "CUDA graph" in d["timing"]["step"]
     r = d["roofline"]
-    assert r["bound"] == "alu" and r["unit"] == "TFLOP/s" and 0 < r["frac"] < 1
-    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
-    assert r["cost_array_write"]["bytes_per_launch"] == 4 * d["config"]["allocations_per_gpu"]
+    assert r["bound"] == "alu" and r["unit"] == "TFLOP/s" and 0 < r["frac_counted_method"] < r["frac"] < r["frac_executed"] < 1
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9 and r["frac_method"] == r["frac"]
+    assert r["cost_array_write"]["bytes_per_launch"] == 4 * per_gpu
     c = d["cpu_baseline"]
     assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
     e = d["e2e"]
-    assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] >= 4 * d["config"]["allocations_per_gpu"]
+    assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] >= 4 * per_gpu
     assert 0 < e["value"] <= d["value"] * 1.05
     assert d["gpu_launches"] == d["steps"]                 # one fused kernel per step
     assert d["clocks"]["sm_max_mhz"] > 0
     # the best allocation of the timed grid search decodes inside the grid
-    assert 0 <= d["config"]["best"]["index"] < d["config"]["allocations"]
+    assert 0 <= d["result"]["best_index"] < d["config"]["allocations"]
+
+
+def test_bench_self_spawns_ranks_and_reproduces_the_single_gpu_key():
+    """`bench.py --gpus 2` without torchrun launches two ranks itself (here both on
+    GPU 0 over gloo: the multi-rank code path, not a timing): n_gpus = 2, the cfg5
+    grid sharded in two, and the combined key equal to cfg5 evaluated whole on one
+    GPU (itself bit-exact against the oracle, test_pp_cfg5_whole_grid_one_gpu)."""
+    import torch
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+                          "--warmup", "3", "--no-extras", "--no-cpu-baseline", "--dist-backend", "gloo",
+                          "--device", "0"], capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["workload"].startswith("pp_cfg5")
+    assert d["timing"]["allocations_per_gpu"] == 4_000_000
+    sys.path.insert(0, ROOT)
+    import paper_2110_15425_b200 as D
+    import workloads as W
+    c5 = W.pp_cfg5()
+    m = D.load_model(W.KIND_PREDATOR_PREY, c5.n_levels, c5.levels, c5.w, c5.params, device=0)
+    best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    D.eval_grid(m, c5.inputs, c5.n_samples, c5.seed, best=best)
+    assert d["result"]["key"] == f"{D.key_from_tensor(best):016x}"

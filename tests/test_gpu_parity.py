@@ -1041,3 +1041,159 @@ def test_ddm_grid_bit_exact(D, orc):
         wc, wn = orc.ddmg_eval(g.n_levels, g.levels, g.w, g.params, b, b + 2, g.n_trials, g.seed,
                                threads=os.cpu_count() or 8)
         assert np.array_equal(cnt, wc) and np.array_equal(_bits(net), _bits(wn))
+
+
+# ---------------------------------------------------------------------------
+# Round 2: full-grid checks (VERDICT r01 "What's missing" 1-2)
+# ---------------------------------------------------------------------------
+def _host_threads():
+    import os
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 8
+
+
+def _observed_gaps(orc, cfg, i, s):
+    """|o_prey - o_player| and |o_pred - o_player| of sample s of allocation i
+    (binary64 from the sample's binary32 normals; spec/MODELS.md §2 Obs nodes)."""
+    z = np.zeros(6, np.float32)
+    orc.lib().od_normal_sextet(int(cfg.seed), int(i), int(s), 0, z)
+    L = cfg.n_levels
+    k = (i // (L[1] * L[2]), (i // L[2]) % L[1], i % L[2])
+    lev = [cfg.levels[k[0]], cfg.levels[L[0] + k[1]], cfg.levels[L[0] + L[1] + k[2]]]
+    smax, smin = float(cfg.params[0]), float(cfg.params[1])
+    p = np.asarray(cfg.inputs, np.float64).reshape(3, 2)
+    o = np.array([p[e] + (smax + float(lev[e]) * (smin - smax)) * z[2 * e:2 * e + 2].astype(np.float64)
+                  for e in range(3)])
+    return np.linalg.norm(o[0] - o[2]), np.linalg.norm(o[1] - o[2])
+
+
+def test_pp_cfg3_full_grid_within_binary64_tolerance(D, orc):
+    """North-star tolerance on the WHOLE cfg3 grid against the binary64 plain
+    definition (od_pp_eval_f64: same Philox bits, libm Box-Muller, exact 1/sqrt;
+    P:155-161).  The binary32 model (the paper's FP32 mode, reading R12) meets
+    1e-5 relative on all but a few allocations; each exception must be ONE
+    ill-conditioned sample — an observation that puts the prey or the predator
+    within 0.05 of the player, where the Action node's unit vector amplifies
+    binary32 rounding — with the other samples still inside the tolerance.  The
+    argmax equals the binary64 argmax (or their binary64 gap is below the
+    deviation bound)."""
+    cfg = W.pp_cfg3()
+    m = _model(D, cfg)
+    C, key = _gpu_pp(D, m, cfg)
+    c64 = orc.pp_eval_threads(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc,
+                              cfg.n_samples, cfg.seed, threads=_host_threads(), f64=True)
+    rel = np.abs(C.astype(np.float64) - c64) / np.abs(c64)
+    assert np.median(rel) < 2e-7 and np.quantile(rel, 0.9999) < 1e-5
+    bad = np.nonzero(rel >= 1e-5)[0]
+    assert len(bad) <= 10, len(bad)
+    for i in bad:
+        args = (cfg.n_levels, cfg.levels, cfg.params, cfg.inputs, int(i), cfg.n_samples, cfg.seed)
+        dev = np.abs(orc.pp_trace(*args).astype(np.float64) - orc.pp_trace_f64(*args))
+        s = int(dev.argmax())
+        rest = (dev.sum() - dev[s]) / cfg.n_samples
+        assert rest < 1e-5 * c64[i], (int(i), rest)                # all other samples within tolerance
+        assert min(_observed_gaps(orc, cfg, int(i), s)) < 0.05, int(i)   # the one outlier is ill-conditioned
+    i32 = key & 0xFFFFFFFF
+    i64 = int(np.argmin(c64))
+    if i32 != i64:
+        assert c64[i32] - c64[i64] <= rel.max() * abs(c64[i64]), (i32, i64, c64[i32] - c64[i64])
+
+
+def test_pp_cfg5_whole_grid_one_gpu(D, orc):
+    """cfg5 (200^3 = 8e6 allocations x 100 samples, BASELINE configs[4]) whole on ONE
+    GPU: all 8e6 costs and the key bit-exact against the full oracle run on the host
+    cores.  This key is the invariant every N-GPU run must reproduce (the sharded
+    bench path is checked against it in test_gpu_bench.py)."""
+    cfg = W.pp_cfg5()
+    m = _model(D, cfg)
+    C, key = _gpu_pp(D, m, cfg)
+    full = orc.pp_eval_threads(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, cfg.n_alloc,
+                               cfg.n_samples, cfg.seed, threads=_host_threads())
+    assert np.array_equal(_bits(C), _bits(full))
+    assert key == orc.argmax_net(-full)[0]
+    # the same grid in 8 shards, keys combined with MIN == the whole-grid key
+    import torch
+    ks = []
+    for r in range(8):
+        b, e = D.shard_range(cfg.n_alloc, r, 8)
+        best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        D.eval_grid(m, cfg.inputs, cfg.n_samples, cfg.seed, b, e, best=best)
+        ks.append(D.key_from_tensor(best))
+    assert min(ks) == key
+
+
+def test_stroop_cfg4_reduced_full_grid_key(D, orc):
+    """SURVEY §8(d)'s argmax parity case for cfg4: all 1e4 allocations of the cfg4
+    control grid x 1e3 trials x 200 steps — every allocation's integer counts, V
+    and the full-grid key bit-exact against the oracle (P:159-161 selection over
+    the Stroop model of P:525)."""
+    c = W.stroop_cfg4()
+    c.n_trials = 1000
+    m = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=0)
+    cnt, net, key = _stroop_gpu(D, m, c, 0, c.n_alloc)
+    wc, wn = orc.stroop_eval(c.n_levels, c.levels, c.w, c.params, 0, c.n_alloc, c.n_trials, c.seed,
+                             threads=_host_threads())
+    assert np.array_equal(cnt, wc)
+    assert np.array_equal(_bits(net), _bits(wn))
+    assert key == orc.argmax_net(wn)[0]
+
+
+def test_ext_stroop_and_ddm_grid_reduced_full_grid_keys(D, orc):
+    """The bench's other control grids (1e4 allocations each) with reduced trial
+    counts: Extended Stroop A x 200 trials and the DDM control grid x 300
+    trials — all counts, V and the full-grid key bit-exact."""
+    g = W.ext_stroop_grid()
+    g.n_trials = 200
+    m = D.load_model(W.KIND_EXT_STROOP_A, g.n_levels, g.levels, g.w, g.params, device=0)
+    cnt, net, key = _stroop_gpu(D, m, g, 0, g.n_alloc)
+    wc, wn = orc.ext_stroop_eval(0, g.n_levels, g.levels, g.w, g.params, 0, g.n_alloc, g.n_trials, g.seed,
+                                 threads=_host_threads())
+    assert np.array_equal(cnt, wc) and np.array_equal(_bits(net), _bits(wn))
+    assert key == orc.argmax_net(wn)[0]
+    d = W.ddmg_grid(100, 300)
+    md = D.load_model(W.KIND_DDM_GRID, d.n_levels, d.levels, d.w, d.params, device=0)
+    cnt, net, key = _stroop_gpu(D, md, d, 0, d.n_alloc)
+    wc, wn = orc.ddmg_eval(d.n_levels, d.levels, d.w, d.params, 0, d.n_alloc, d.n_trials, d.seed,
+                           threads=_host_threads())
+    assert np.array_equal(cnt, wc) and np.array_equal(_bits(net), _bits(wn))
+    assert key == orc.argmax_net(wn)[0]
+
+
+def test_signed_key_order(D, orc):
+    """key_order = 1 (include/distill.h): the kernel stores key ^ 2^63, combined by
+    a signed atomicMin from DISTILL_KEY_INIT_SIGNED — the same key as the unsigned
+    order for PP and Stroop grids, shards combine with a plain int64 min."""
+    import torch
+    cfg = W.PPConfig("sk", (17, 13, 11), 12)
+    m = _model(D, cfg)
+    _, key = _gpu_pp(D, m, cfg)
+    best = torch.empty(1, dtype=torch.int64, device="cuda")
+    D.key_reset(best, signed=True)
+    torch.cuda.synchronize()
+    assert int(best.item()) == 2 ** 63 - 1
+    D.eval_grid(m, cfg.inputs, cfg.n_samples, cfg.seed, best=best, signed_key=True)
+    assert D.key_from_tensor(best, signed=True) == key
+    parts = []
+    for r in range(3):
+        b, e = D.shard_range(cfg.n_alloc, r, 3)
+        t = torch.empty(1, dtype=torch.int64, device="cuda")
+        D.key_reset(t, signed=True)
+        D.eval_grid(m, cfg.inputs, cfg.n_samples, cfg.seed, b, e, best=t, signed_key=True)
+        parts.append(int(t.item()))
+    assert (min(parts) & (2 ** 64 - 1)) ^ (1 << 63) == key
+    c = W.stroop_small()
+    ms = D.load_model(W.KIND_STROOP_LCA, c.n_levels, c.levels, c.w, c.params, device=0)
+    _, _, k_u = _stroop_gpu(D, ms, c, 0, c.n_alloc)
+    counts = torch.zeros(3 * c.n_alloc, dtype=torch.int64, device="cuda")
+    D.key_reset(best, signed=True)
+    D.eval_grid(ms, None, c.n_trials, c.seed, best=best, counts=counts, signed_key=True)
+    assert D.key_from_tensor(best, signed=True) == k_u
+    # an all-NaN grid: no valid candidate (high word 0xFFFFFFFF), as in the unsigned order
+    D.key_reset(best, signed=True)
+    D.eval_grid(m, np.array([np.nan, 0, 1, 1, 0, 0], np.float32), cfg.n_samples, cfg.seed, best=best,
+                signed_key=True)
+    assert D.key_from_tensor(best, signed=True) >> 32 == 0xFFFFFFFF
+    with pytest.raises(D.api.DistillError):
+        D.key_decode(D.key_from_tensor(best, signed=True))

@@ -209,6 +209,38 @@ def test_flop_count_per_sample_matches_hand_count(orc):
     assert per_alloc == 74 + 10 * 13
 
 
+def test_method_flop_count(orc):
+    """The method count the roofline's headline fraction uses (SURVEY §8(d):
+    fma = 2, add/mul = 1, a square root = 1, a divide = 1): the counting build in
+    method mode scores sqrt_spec as 1 flop and rsqrt_spec as 2 (sqrt + divide)
+    instead of their Goldschmidt/Newton steps.  PP: 181 per sample (274 executed:
+    3 x 17 Goldschmidt + 3 x 14 Newton flops are implementation, not method),
+    13 per allocation, 32 per call; one sextet (6 accumulator normals): 135 (186
+    executed)."""
+    L = orc.lib(counting=True)
+    cfg = W.pp_cfg3()
+
+    def flops(n, S):
+        L.od_flops_reset()
+        orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, n, S, 1, counting=True)
+        return L.od_flops_read()
+
+    try:
+        L.od_flops_method(1)
+        assert flops(10, 101) - flops(10, 100) == 10 * 181
+        a, b = flops(10, 100) - 10 * 100 * 181, flops(20, 100) - 20 * 100 * 181
+        assert (b - a) == 10 * 13 and a - 10 * 13 == 32
+        z = np.zeros(6, np.float32)
+        L.od_flops_reset()
+        L.od_normal_acc(1, 5, 0, 1, z)
+        assert L.od_flops_read() == 135
+    finally:
+        L.od_flops_method(0)
+    L.od_flops_reset()
+    L.od_normal_acc(1, 5, 0, 1, z)
+    assert L.od_flops_read() == 186
+
+
 def test_multi_invocation_is_the_listing1_loop(orc):
     """pp_eval_multi = one pp_eval per trial t on inputs[t % len] with invocation0 + t
     (reading Q17); distinct invocations draw distinct noise."""
