@@ -47,20 +47,20 @@ UNIT = "evals/s"
 FLOPS_PER_SAMPLE = 210
 FLOPS_PER_ALLOC = 15
 FLOPS_PER_CALL = 0
-FLOPS_PER_SAMPLE_METHOD = 181   # counted (test_method_flop_count)
+FLOPS_PER_SAMPLE_METHOD = 133   # counted (test_method_flop_count)
 FLOPS_PER_ALLOC_METHOD = 13
 FLOPS_PER_CALL_METHOD = 32
-FLOPS_PER_SAMPLE_EXEC = 274     # counted (test_flop_count_per_sample_matches_hand_count)
+FLOPS_PER_SAMPLE_EXEC = 175     # counted (test_flop_count_per_sample_matches_hand_count)
 FLOPS_PER_CALL_EXEC = 74
 FP32_LANES_PER_SM = 128       # FFMA lanes per SM (4 SMSP x 32), 2 flops per FMA
 FP32_PEAK_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12   # TFLOP/s (the extras' denominator)
 # accumulator models: SURVEY §8(d) ~30 flop per DDM step, ~75 per Stroop trial-step; counted:
-# one sextet (6 normals) = 135 method / 186 executed flops (test_method_flop_count),
+# one sextet (6 normals) = 87 flops, method = executed (test_method_flop_count),
 # DDM step = 1 normal + 2 fma, Stroop trial-step = 2 normals + rectified LCA 16
 DDM_FLOPS_PER_STEP = 30
-DDM_FLOPS_PER_STEP_EXEC = 186 / 6 + 4     # 35
+DDM_FLOPS_PER_STEP_EXEC = 87 / 6 + 4      # 18.5
 STROOP_FLOPS_PER_STEP = 75
-STROOP_FLOPS_PER_STEP_EXEC = 2 * 186 / 6 + 16   # 78
+STROOP_FLOPS_PER_STEP_EXEC = 2 * 87 / 6 + 16    # 45
 # SURVEY §8(d)'s 50 %-of-peak point for cfg3, in the count-independent unit
 EVALS_PER_S_AT_50PCT = 1.77e11
 
@@ -435,10 +435,10 @@ def run_ours(args):
                           f"add/mul/sqrt/div = 1) + {FLOPS_PER_ALLOC} per allocation",
             "achieved_counted_method": achieved_method, "frac_counted_method": achieved_method / peak,
             "counted_method_flop_count": f"{FLOPS_PER_SAMPLE_METHOD} flop per evaluation counted by the oracle's "
-                                         "counting build in method mode (sqrt_spec = 1, rsqrt_spec = 2)",
+                                         "counting build in method mode (rsqrt_spec = sqrt + divide = 2)",
             "achieved_executed": achieved_exec, "frac_executed": achieved_exec / peak,
             "executed_flop_count": f"{FLOPS_PER_SAMPLE_EXEC} flop per evaluation as the spec executes it "
-                                   "(Newton / Goldschmidt steps of rsqrt_spec and sqrt_spec included)",
+                                   "(the Newton steps of rsqrt_spec included)",
             "evals_per_s_per_gpu": per_gpu_evals_s,
             "evals_per_s_vs_survey_50pct_point": per_gpu_evals_s / EVALS_PER_S_AT_50PCT,
             "traffic": traffic, "traffic_source": "profiles/r01_pp_traffic.json (ncu --set full, cfg3)",

@@ -60,12 +60,12 @@ def _bind(path: str) -> C.CDLL:
     u64, u32, f32 = C.c_uint64, C.c_uint32, C.c_float
     sig = {
         "od_philox4x32_10": (None, [_u32p, _u32p, _u32p]),
-        "od_ln": (f32, [f32]),
+        "od_rad": (f32, [u32]),
+        "od_rad_array": (None, [_u32p, _f32p, u64]),
+        "od_rad_table": (None, [_f32p]),
         "od_rsqrt": (f32, [f32]),
         "od_sincos2pi": (None, [u32, C.POINTER(f32), C.POINTER(f32)]),
-        "od_ln_array": (None, [_f32p, _f32p, u64]),
         "od_rsqrt_array": (None, [_f32p, _f32p, u64]),
-        "od_sqrt_array": (None, [_f32p, _f32p, u64]),
         "od_sincos2pi_array": (None, [_u32p, _f32p, _f32p, u64]),
         "od_normal_acc": (None, [u64, u64, u64, u64, _f32p]),
         "od_normal_sextet": (None, [u64, u32, u32, u32, _f32p]),
@@ -147,8 +147,9 @@ def philox(ctr, key) -> np.ndarray:
     return out
 
 
-def ln(x: float) -> float:
-    return lib().od_ln(float(x))
+def rad(R: int) -> float:
+    """rad_spec (spec/RNG.md §3): the Box-Muller radius sqrt(-2 ln u1(R))."""
+    return lib().od_rad(int(R))
 
 
 def rsqrt(x: float) -> float:
@@ -161,24 +162,24 @@ def sincos2pi(a: int):
     return c.value, s.value
 
 
-def ln_array(x) -> np.ndarray:
-    x = _f32(x)
-    y = np.empty_like(x)
-    lib().od_ln_array(x, y, x.size)
+def rad_array(R) -> np.ndarray:
+    R = _u32(R)
+    y = np.empty(R.size, np.float32)
+    lib().od_rad_array(R, y, R.size)
     return y
+
+
+def rad_table() -> np.ndarray:
+    """The 736 x 4 coefficient table RT of spec/RNG.md §3 as this oracle built it."""
+    out = np.zeros((736, 4), np.float32)
+    lib().od_rad_table(out)
+    return out
 
 
 def rsqrt_array(x) -> np.ndarray:
     x = _f32(x)
     y = np.empty_like(x)
     lib().od_rsqrt_array(x, y, x.size)
-    return y
-
-
-def sqrt_array(x) -> np.ndarray:
-    x = _f32(x)
-    y = np.empty_like(x)
-    lib().od_sqrt_array(x, y, x.size)
     return y
 
 

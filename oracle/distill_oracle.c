@@ -95,27 +95,54 @@ void od_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
 }
 
 /* ------------------------------------------------------------------------ */
-/* spec/RNG.md §3: ln_spec                                                   */
+/* spec/RNG.md §3: rad_spec — the Box-Muller radius sqrt(-2 ln u1) as a      */
+/* piecewise cubic over the radius word's 23 random bits (revision R10c)      */
 /* ------------------------------------------------------------------------ */
-#define LN2_HI 0x1.62e4p-1f
-#define LN2_LO 0x1.7f7d1cp-20f
-static const float OD_L[8] = {
-    -0x1.fffff4p-2f, 0x1.5556e8p-2f, -0x1.0006c4p-2f, 0x1.98da38p-3f,
-    -0x1.52fb94p-3f, 0x1.30d0aap-3f, -0x1.277224p-3f, 0x1.6fc72p-4f };
+#define OD_RT_ROWS 736
+static float od_rt[OD_RT_ROWS][4];
 
-float od_ln(float x) {
-    uint32_t i = f2u(x);
-    int32_t e = ((int32_t)(i - 0x3F3504F3u)) >> 23;
-    float m = u2f(i - ((uint32_t)e << 23));
-    float f = FSUB(m, 1.0f);
-    float P = OD_L[7];
-    for (int k = 6; k >= 0; --k) P = FFMA(P, f, OD_L[k]);
-    float f2 = FMUL(f, f);
-    float y = FFMA(f2, P, f);
-    float fe = (float)e;
-    y = FFMA(fe, LN2_LO, y);
-    y = FFMA(fe, LN2_HI, y);
-    return y;
+/* The table construction of spec/RNG.md §3, in binary64, operation by operation. */
+static void od_rt_build(void) {
+    const double tau[4] = { -3.0 / 128, -1.0 / 128, 1.0 / 128, 3.0 / 128 };
+    for (int r = 0; r < 2; ++r)
+        for (int e = 0; e < 23; ++e)
+            for (int j = 0; j < 16; ++j) {
+                double c = 1.0 + (2.0 * j + 1.0) / 32.0;
+                double f[4];
+                for (int k = 0; k < 4; ++k) {
+                    double x = (c + tau[k]) * ldexp(1.0, e);
+                    double N = r ? 16777216.0 - x : x;
+                    f[k] = sqrt(-2.0 * log(N * 0x1p-24));
+                }
+                double d01 = (f[1] - f[0]) / (tau[1] - tau[0]);
+                double d12 = (f[2] - f[1]) / (tau[2] - tau[1]);
+                double d23 = (f[3] - f[2]) / (tau[3] - tau[2]);
+                double d012 = (d12 - d01) / (tau[2] - tau[0]);
+                double d123 = (d23 - d12) / (tau[3] - tau[1]);
+                double A = (d123 - d012) / (tau[3] - tau[0]);
+                double c3 = A;
+                double c2 = d012 - A * ((tau[0] + tau[1]) + tau[2]);
+                double c1 = (d01 - d012 * (tau[0] + tau[1])) + A * ((tau[0] * tau[1] + tau[0] * tau[2]) + tau[1] * tau[2]);
+                double c0 = ((f[0] - d01 * tau[0]) + d012 * (tau[0] * tau[1])) - A * ((tau[0] * tau[1]) * tau[2]);
+                float* row = od_rt[368 * r + 16 * e + j];
+                row[0] = (float)c0; row[1] = (float)c1; row[2] = (float)c2; row[3] = (float)c3;
+            }
+}
+__attribute__((constructor)) static void od_rt_init(void) { od_rt_build(); }
+
+void od_rad_table(float* out) { memcpy(out, od_rt, sizeof od_rt); }
+
+float od_rad(uint32_t R) {
+    uint32_t N = (R >> 8) | 1u;                     /* odd, u1 = N 2^-24 */
+    uint32_t r = N >> 23;                           /* region */
+    uint32_t v = r ? (1u << 24) - N : N;            /* odd, [1, 2^23 - 1] */
+    int e = 0;
+    while ((v >> (e + 1)) != 0) ++e;                /* floor(log2 v) */
+    float m = (float)v / (float)(1u << e);          /* exact, [1, 2) */
+    uint32_t j = (uint32_t)((m - 1.0f) * 16.0f);    /* exact product; floor */
+    float t = FSUB(m, 1.0f + (float)(2 * j + 1) / 32.0f);   /* exact */
+    const float* c = od_rt[368 * r + 16 * e + j];
+    return FFMA(FFMA(FFMA(c[3], t, c[2]), t, c[1]), t, c[0]);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -132,23 +159,6 @@ float od_rsqrt(float x) {
     }
     METHOD_END(2);
     return y;
-}
-
-/* spec/RNG.md §4: sqrt_spec — Goldschmidt from the rsqrt seed (Box-Muller radius) */
-float od_sqrt(float x) {
-    METHOD_BEGIN();
-    float y = u2f(0x5F375A86u - (f2u(x) >> 1));
-    float g = FMUL(x, y);
-    float h = FMUL(0.5f, y);
-    for (int k = 0; k < 2; ++k) {
-        float r = FFMA(-g, h, 0.5f);
-        g = FFMA(g, r, g);
-        h = FFMA(h, r, h);
-    }
-    float r = FFMA(-g, h, 0.5f);
-    g = FFMA(g, r, g);
-    METHOD_END(1);
-    return g;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -172,8 +182,7 @@ void od_sincos2pi(uint32_t a, float* cs, float* sn) {
 }
 
 /* array forms of the three primitives, for the exhaustive accuracy pins */
-void od_sqrt_array(const float* x, float* y, uint64_t n) { for (uint64_t j = 0; j < n; ++j) y[j] = od_sqrt(x[j]); }
-void od_ln_array(const float* x, float* y, uint64_t n) { for (uint64_t j = 0; j < n; ++j) y[j] = od_ln(x[j]); }
+void od_rad_array(const uint32_t* R, float* y, uint64_t n) { for (uint64_t j = 0; j < n; ++j) y[j] = od_rad(R[j]); }
 void od_rsqrt_array(const float* x, float* y, uint64_t n) { for (uint64_t j = 0; j < n; ++j) y[j] = od_rsqrt(x[j]); }
 void od_sincos2pi_array(const uint32_t* a, float* c, float* s, uint64_t n) {
     for (uint64_t j = 0; j < n; ++j) od_sincos2pi(a[j], &c[j], &s[j]);
@@ -181,9 +190,7 @@ void od_sincos2pi_array(const uint32_t* a, float* c, float* s, uint64_t n) {
 
 /* spec/RNG.md §2 + §6: one Box-Muller pair in polar form (radius, cos, sin) */
 static void od_bm_polar(uint32_t R, uint32_t A, float* rad, float* c, float* n) {
-    float u1 = (float)((R >> 8) | 1u) * 0x1p-24f;   /* exact */
-    float s = -2.0f * od_ln(u1);                     /* exact scaling, not counted */
-    *rad = od_sqrt(s);                               /* sqrt_spec */
+    *rad = od_rad(R);                                /* rad_spec = sqrt(-2 ln u1) */
     od_sincos2pi(A, c, n);
 }
 /* ... and as the two normals z = rad * (cos, sin) */

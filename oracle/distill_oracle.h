@@ -13,7 +13,7 @@
  *
  * Parity status per function:
  *   od_philox4x32_10     pinned: Random123 known-answer vectors
- *   od_ln / od_rsqrt / od_sincos2pi   pinned: exhaustive / dense accuracy vs binary64 libm
+ *   od_rad / od_rsqrt / od_sincos2pi  pinned: exhaustive / dense accuracy vs binary64 libm
  *   od_normal_*          pinned: moments, KS vs Phi, closed-form endpoints
  *   od_pp_eval           pinned: zero-noise closed forms, monotonicity, planted optimum, offset-Gaussian
  *                        angle law (noisy objective in closed form), noisy-predator quadrature,
@@ -46,12 +46,11 @@ extern "C" {
 
 /* ---- RNG (spec/RNG.md) ---- */
 void  od_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
-float od_ln(float x);
+float od_rad(uint32_t radius_word);            /* spec/RNG.md §3: sqrt(-2 ln u1) */
+void  od_rad_array(const uint32_t* R, float* y, uint64_t n);
+void  od_rad_table(float* out);                 /* the 736 x 4 table RT of §3 */
 float od_rsqrt(float x);
-float od_sqrt(float x);
-void  od_sqrt_array(const float* x, float* y, uint64_t n);
 void  od_sincos2pi(uint32_t angle_word, float* c, float* s);
-void  od_ln_array(const float* x, float* y, uint64_t n);
 void  od_rsqrt_array(const float* x, float* y, uint64_t n);
 void  od_sincos2pi_array(const uint32_t* a, float* c, float* s, uint64_t n);
 /* normals [first, first+n) of unit U on stream 2 (accumulator models), sextet packing */

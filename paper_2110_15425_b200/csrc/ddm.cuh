@@ -21,6 +21,7 @@ struct DDMArgs {
     unsigned long long* __restrict__ rt_hist;  // [2*nb+1]
     unsigned long long* __restrict__ rt_sum;   // [2]
     unsigned long long* __restrict__ x_hist;   // [nx+2]
+    const float4* __restrict__ rad_tab;        // device RT (spec/RNG.md §3)
 };
 
 // One integrator step: DDM x = fma(nsd, g, fma(dt, A, x)) (§4) or, in LCI
@@ -35,9 +36,10 @@ __device__ __forceinline__ float integ_step(const DDMArgs& a, float nsd, float g
 template <int BLOCK, int MINB = 0, bool LCI = false>
 __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a) {
     extern __shared__ uint32_t s_hist[];  // [2*nb+1] rt bins then [nx+2] x bins
+    __shared__ float4 s_rt[RT_ROWS];
     const uint32_t n_rt = 2 * a.n_rt_bins + 1, n_x = a.n_x_bins + 2, n_all = n_rt + n_x;
     for (uint32_t b = threadIdx.x; b < n_all; b += BLOCK) s_hist[b] = 0;
-    __syncthreads();
+    stage_rad_table(s_rt, a.rad_tab);      // (its barrier also covers the histogram clear)
 
     const float nsd = __fmul_rn(a.noise, __fsqrt_rn(a.dt));
     const float sc = __fdiv_rn(__uint2float_rn(a.n_x_bins), __fadd_rn(a.x_hi, -a.x_lo));
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
         const uint32_t n12 = a.n_steps / 12;
         for (uint32_t j = 0; j < n12; ++j) {
             float g[12], xs[12];
-            acc_normals12(rng, j, g);
+            acc_normals12(rng, s_rt, j, g);
 #pragma unroll
             for (int l = 0; l < 12; ++l) { x = integ_step<LCI>(a, nsd, g[l], x); xs[l] = x; }
             if (st == 0) {
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
         const uint32_t rem = a.n_steps - 12 * n12;
         if (rem) {
             float g[12];
-            acc_normals_tail(rng, n12, rem, g);
+            acc_normals_tail(rng, s_rt, n12, rem, g);
 #pragma unroll
             for (int l = 0; l < 11; ++l) {
                 if ((uint32_t)l < rem) {
@@ -139,10 +141,13 @@ struct DdmgArgs {
     uint32_t n_steps, L0, L1, n_trials, trial_begin, trial_end, key0, key1, begin, count;
     const float* __restrict__ levels;
     unsigned long long* __restrict__ counts;   // [count][3]
+    const float4* __restrict__ rad_tab;        // device RT (spec/RNG.md §3)
 };
 
 template <int BLOCK, int MINB = 0>
 __global__ void __launch_bounds__(BLOCK, MINB) ddmg_sim_kernel(const DdmgArgs a, uint32_t alloc_off) {
+    __shared__ float4 s_rt[RT_ROWS];
+    stage_rad_table(s_rt, a.rad_tab);
     const uint32_t t_alloc = alloc_off + blockIdx.y;
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddmg_sim_kernel(const DdmgArgs a,
         const uint32_t n12 = a.n_steps / 12;
         for (uint32_t grp = 0; grp < n12; ++grp) {
             float g[12], xs[12];
-            acc_normals12(rng, grp, g);
+            acc_normals12(rng, s_rt, grp, g);
 #pragma unroll
             for (int l = 0; l < 12; ++l) { x = __fmaf_rn(nsd, g[l], __fmaf_rn(a.dt, A, x)); xs[l] = x; }
             if (st == 0) {
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddmg_sim_kernel(const DdmgArgs a,
         const uint32_t rem = a.n_steps - 12 * n12;
         if (rem) {
             float g[12];
-            acc_normals_tail(rng, n12, rem, g);
+            acc_normals_tail(rng, s_rt, n12, rem, g);
 #pragma unroll
             for (int l = 0; l < 11; ++l) {
                 if ((uint32_t)l < rem) {

@@ -69,6 +69,66 @@ struct DeviceScope {
     DeviceScope device_scope_(dev); \
     CUDA_TRY(device_scope_.err)
 
+// ---------------------------------------------------------------- radius table
+// spec/RNG.md §3: the 736 x 4 table RT of the Box-Muller radius, built on the
+// host in binary64 in the spec's operation order (the CPU oracle carries out
+// the same construction itself), uploaded once per device, never freed.
+void build_rad_table(float4* rt) {
+    const double nodes[4] = {-3.0 / 128.0, -1.0 / 128.0, 1.0 / 128.0, 3.0 / 128.0};
+    for (int reg = 0; reg < 2; ++reg) {
+        for (int oct = 0; oct < 23; ++oct) {
+            for (int sub = 0; sub < 16; ++sub) {
+                const double centre = 1.0 + (2.0 * sub + 1.0) / 32.0;
+                double f[4];
+                for (int k = 0; k < 4; ++k) {
+                    const double x = (centre + nodes[k]) * std::ldexp(1.0, oct);
+                    const double n = reg ? 16777216.0 - x : x;
+                    f[k] = std::sqrt(-2.0 * std::log(n * 0x1p-24));
+                }
+                const double d01 = (f[1] - f[0]) / (nodes[1] - nodes[0]);
+                const double d12 = (f[2] - f[1]) / (nodes[2] - nodes[1]);
+                const double d23 = (f[3] - f[2]) / (nodes[3] - nodes[2]);
+                const double d012 = (d12 - d01) / (nodes[2] - nodes[0]);
+                const double d123 = (d23 - d12) / (nodes[3] - nodes[1]);
+                const double a3 = (d123 - d012) / (nodes[3] - nodes[0]);
+                const double p01 = nodes[0] * nodes[1];
+                const double a2 = d012 - a3 * ((nodes[0] + nodes[1]) + nodes[2]);
+                const double a1 = (d01 - d012 * (nodes[0] + nodes[1])) + a3 * ((p01 + nodes[0] * nodes[2]) + nodes[1] * nodes[2]);
+                const double a0 = ((f[0] - d01 * nodes[0]) + d012 * p01) - a3 * (p01 * nodes[2]);
+                rt[368 * reg + 16 * oct + sub] = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+            }
+        }
+    }
+}
+
+std::mutex g_rt_mu;
+constexpr int MAX_DEVICES = 64;
+float4* g_rt_dev[MAX_DEVICES] = {nullptr};
+
+// The device copy of RT for `device` (uploaded on first use; the caller has made
+// `device` current).  First use must not happen inside a CUDA-graph capture.
+distill_status rad_table(int device, const float4** out) {
+    std::lock_guard<std::mutex> lock(g_rt_mu);
+    if (device < 0 || device >= MAX_DEVICES) return fail(DISTILL_E_INVALID_ARG, "rad_table: bad device %d", device);
+    if (!g_rt_dev[device]) {
+        static std::vector<float4> host;
+        if (host.empty()) {
+            host.resize(RT_ROWS);
+            build_rad_table(host.data());
+        }
+        float4* d = nullptr;
+        CUDA_TRY(cudaMalloc(&d, RT_ROWS * sizeof(float4)));
+        cudaError_t e = cudaMemcpy(d, host.data(), RT_ROWS * sizeof(float4), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(d);
+            return fail(DISTILL_E_CUDA, "rad_table: %s", cudaGetErrorString(e));
+        }
+        g_rt_dev[device] = d;
+    }
+    *out = g_rt_dev[device];
+    return DISTILL_OK;
+}
+
 constexpr int PP_BLOCK = 128;
 constexpr int ARGMAX_BLOCK = 256;
 // sample / trial loops step a 32-bit counter by up to 2 (PP pairs) or a grid
@@ -108,6 +168,7 @@ struct distill_model {
     float w[8] = {0};
     std::vector<float> params;
     float* d_levels = nullptr;      // device RO block
+    const float4* d_rt = nullptr;   // the device's radius table (spec/RNG.md §3), library-global
     int n_sm = 148;
     // device scratch of the synchronous host-buffer entry (lazily grown, guarded by the mutex)
     std::mutex scratch_mu;
@@ -205,6 +266,12 @@ distill_status distill_load_model(const distill_model_desc* desc, int device, di
         delete m;
         return fail(DISTILL_E_CUDA, "load_model: %s", cudaGetErrorString(e));
     }
+    const distill_status rs = rad_table(device, &m->d_rt);
+    if (rs != DISTILL_OK) {
+        cudaFree(m->d_levels);
+        delete m;
+        return rs;
+    }
     *out = m;
     return DISTILL_OK;
 }
@@ -238,6 +305,7 @@ static PPArgs pp_base_args(const distill_model* m, uint32_t n_samples, uint64_t 
     p.begin = 0; p.count = (uint32_t)m->n_alloc;
     p.levels = m->d_levels;
     p.n_sets = 1;
+    p.rad_tab = m->d_rt;
     return p;
 }
 
@@ -383,6 +451,7 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
     p.levels = m->d_levels; p.counts = counts; p.net = a->d_net; p.best = a->d_best;
     p.key_signed = a->key_order;
+    p.rad_tab = m->d_rt;
     const uint32_t tr = te - tb;
     if (tr > 0) {
         // enough blocks along trials to fill the machine, capped so each thread runs >= 1 trial
@@ -398,14 +467,14 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
             q.A0 = P[0]; q.g_a = P[1]; q.noise = P[2]; q.dt = P[3]; q.n_steps = (uint32_t)P[6];
             q.L0 = m->L[0]; q.L1 = m->L[1]; q.n_trials = a->n_samples; q.trial_begin = tb; q.trial_end = te;
             q.key0 = p.key0; q.key1 = p.key1; q.begin = p.begin; q.count = p.count;
-            q.levels = m->d_levels; q.counts = counts;
+            q.levels = m->d_levels; q.counts = counts; q.rad_tab = m->d_rt;
         }
         for (uint64_t off = 0; off < count; off += 65535) {
             const unsigned gy = (unsigned)std::min<uint64_t>(65535, count - off);
             static_assert(DDM_BLOCK == STROOP_BLOCK, "the trial chunks above are sized for STROOP_BLOCK");
             if (ddmg)
                 ddmg_sim_kernel<DDM_BLOCK, DDM_MINB><<<dim3(chunks, gy), DDM_BLOCK, 0, st>>>(q, (uint32_t)off);
-            else if (table_bytes <= 48 * 1024)      // pathway table in shared memory (trial-invariant h_k(n))
+            else if (table_bytes <= 32 * 1024)      // pathway table in shared memory (trial-invariant h_k(n); + RT <= 48 KB)
                 stroop_sim_kernel<STROOP_BLOCK, STROOP_MINB, true><<<dim3(chunks, gy), STROOP_BLOCK, table_bytes, st>>>(
                     p, (uint32_t)off);
             else
@@ -465,6 +534,7 @@ distill_status distill_stroop_energy(const distill_model* m, uint64_t alloc, uin
     p.n_trials = n_trials; p.trial_begin = trial_begin; p.trial_end = trial_end;
     p.key0 = (uint32_t)seed; p.key1 = (uint32_t)(seed >> 32);
     p.levels = m->d_levels;
+    p.rad_tab = m->d_rt;
     const uint32_t tr = trial_end - trial_begin;
     const unsigned grid = (unsigned)std::min<uint64_t>((tr + STROOP_BLOCK - 1) / STROOP_BLOCK, (uint64_t)m->n_sm * 8);
     stroop_energy_kernel<STROOP_BLOCK><<<grid, STROOP_BLOCK, N * sizeof(unsigned long long), (cudaStream_t)stream>>>(
@@ -501,6 +571,7 @@ static distill_status launch_ext_stroop(distill_model* m, const distill_eval_arg
     p.begin = (uint32_t)a->begin; p.count = (uint32_t)count;
     p.levels = m->d_levels; p.counts = counts; p.net = a->d_net; p.best = a->d_best;
     p.key_signed = a->key_order;
+    p.rad_tab = m->d_rt;
     const uint32_t tr = te - tb;
     uint32_t chunks = std::max<uint32_t>(1, (tr + STROOP_BLOCK - 1) / STROOP_BLOCK);
     const uint64_t want = (uint64_t)m->n_sm * 8 * 64;
@@ -879,7 +950,10 @@ static distill_status launch_integrator(const distill_ddm_args* a, float leak, f
     int dev = 0, n_sm = 148;
     CUDA_TRY(cudaGetDevice(&dev));
     CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-    if (smem > 48 * 1024)
+    const float4* rt = nullptr;
+    const distill_status rs = rad_table(dev, &rt);
+    if (rs != DISTILL_OK) return rs;
+    if (smem + RT_ROWS * sizeof(float4) > 48 * 1024)   // dynamic histograms + the static radius table
         CUDA_TRY(cudaFuncSetAttribute(ddm_batch_kernel<DDM_BLOCK, DDM_MINB, LCI>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DDMArgs p;
@@ -890,6 +964,7 @@ static distill_status launch_integrator(const distill_ddm_args* a, float leak, f
     p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
     p.trial_begin = a->trial_begin; p.n_trials = n;
     p.rt_hist = a->d_rt_hist; p.rt_sum = a->d_rt_sum; p.x_hist = a->d_x_hist;
+    p.rad_tab = rt;
     const uint64_t need = (n + DDM_BLOCK - 1) / DDM_BLOCK;
     const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)n_sm * 1024);
     ddm_batch_kernel<DDM_BLOCK, DDM_MINB, LCI><<<grid, DDM_BLOCK, smem, (cudaStream_t)stream>>>(p);

@@ -44,17 +44,7 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 }
 
 // ---------------------------------------------------------------- frozen polynomials
-// spec/RNG.md §3 (ln), §5 (sin/cos of pi/2 r) — hex-float binary32 constants.
-#define D_LN2_HI 0x1.62e4p-1f
-#define D_LN2_LO 0x1.7f7d1cp-20f
-#define D_L0 (-0x1.fffff4p-2f)
-#define D_L1 0x1.5556e8p-2f
-#define D_L2 (-0x1.0006c4p-2f)
-#define D_L3 0x1.98da38p-3f
-#define D_L4 (-0x1.52fb94p-3f)
-#define D_L5 0x1.30d0aap-3f
-#define D_L6 (-0x1.277224p-3f)
-#define D_L7 0x1.6fc72p-4f
+// spec/RNG.md §5 (sin/cos of pi r) — hex-float binary32 constants.
 #define D_S0 0x1.921fb4p+1f
 #define D_S1 (-0x1.4abbb6p+2f)
 #define D_S2 0x1.46676ep+1f
@@ -66,26 +56,16 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 #define D_C3 0x1.e12f96p-3f
 #define D_C4 (-0x1.901cb4p-6f)
 
-// ln_spec(x) for positive normal x (spec/RNG.md §3)
-__device__ __forceinline__ float ln_spec(float x) {
-    const uint32_t i = __float_as_uint(x);
-    const int32_t e = ((int32_t)(i - 0x3F3504F3u)) >> 23;
-    const float m = __uint_as_float(i - ((uint32_t)e << 23));
-    const float f = __fadd_rn(m, -1.0f);
-    float P = D_L7;
-    P = __fmaf_rn(P, f, D_L6);
-    P = __fmaf_rn(P, f, D_L5);
-    P = __fmaf_rn(P, f, D_L4);
-    P = __fmaf_rn(P, f, D_L3);
-    P = __fmaf_rn(P, f, D_L2);
-    P = __fmaf_rn(P, f, D_L1);
-    P = __fmaf_rn(P, f, D_L0);
-    const float f2 = __fmul_rn(f, f);
-    float y = __fmaf_rn(f2, P, f);
-    const float fe = __int2float_rn(e);
-    y = __fmaf_rn(fe, D_LN2_LO, y);
-    y = __fmaf_rn(fe, D_LN2_HI, y);
-    return y;
+// ---------------------------------------------------------------- radius table
+// spec/RNG.md §3 (revision R10c): rad = sqrt(-2 ln u1) as a piecewise cubic in
+// the radius word's 23 random bits; the 736-row table RT is built by the host
+// (distill.cu, binary64, the spec's operation order), uploaded once per device,
+// and staged into shared memory by every kernel that draws normals.
+constexpr int RT_ROWS = 736;
+
+__device__ __forceinline__ void stage_rad_table(float4* s_rt, const float4* __restrict__ g_rt) {
+    for (int k = threadIdx.x; k < RT_ROWS; k += blockDim.x) s_rt[k] = __ldg(g_rt + k);
+    __syncthreads();
 }
 
 // rsqrt_spec(x) (spec/RNG.md §4): magic seed + 3 Newton steps, no MUFU.
@@ -100,60 +80,6 @@ __device__ __forceinline__ float rsqrt_spec(float x) {
     }
     return y;
 }
-
-// sqrt_spec(x) (spec/RNG.md §4): Goldschmidt from the rsqrt seed, 3 steps, last h skipped.
-__device__ __forceinline__ float sqrt_spec(float x) {
-    const float y = __uint_as_float(0x5F375A86u - (__float_as_uint(x) >> 1));
-    float g = __fmul_rn(x, y);
-    float h = __fmul_rn(0.5f, y);
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const float r = __fmaf_rn(-g, h, 0.5f);
-        g = __fmaf_rn(g, r, g);
-        h = __fmaf_rn(h, r, h);
-    }
-    const float r = __fmaf_rn(-g, h, 0.5f);
-    return __fmaf_rn(g, r, g);
-}
-
-// r of sincos_spec: (A mod 2^31)/2^31 - 1/2, built from the bits (exact, spec/RNG.md §5)
-__device__ __forceinline__ float half_turn_r(uint32_t a) {
-    return __fadd_rn(__uint_as_float(((a >> 8) & 0x7FFFFFu) | 0x3F800000u), -1.5f);
-}
-
-// sincos_spec(A) = (cos, sin)(2 pi A/2^32 - pi/2), half-turn reduction (spec/RNG.md §5)
-__device__ __forceinline__ void sincos_spec(uint32_t a, float& c, float& s) {
-    const float r = half_turn_r(a);
-    const float t = __fmul_rn(r, r);
-    const float S = __fmaf_rn(__fmaf_rn(__fmaf_rn(__fmaf_rn(D_S4, t, D_S3), t, D_S2), t, D_S1), t, D_S0);
-    const float C = __fmaf_rn(__fmaf_rn(__fmaf_rn(__fmaf_rn(D_C4, t, D_C3), t, D_C2), t, D_C1), t, D_C0);
-    const float cq = __fmaf_rn(C, t, 1.0f);
-    const float sq = __fmul_rn(S, r);
-    const bool h = (a >> 31) != 0;
-    c = h ? -cq : cq;
-    s = h ? -sq : sq;
-}
-
-// One Box-Muller pair from a radius word R and an angle word A (spec/RNG.md §6)
-__device__ __forceinline__ void bm_pair(uint32_t R, uint32_t A, float& z0, float& z1) {
-    const float u1 = __fmul_rn(__uint2float_rn((R >> 8) | 1u), 0x1p-24f);  // exact
-    const float s = __fmul_rn(-2.0f, ln_spec(u1));                          // exact scaling
-    const float rad = sqrt_spec(s);
-    float c, n;
-    sincos_spec(A, c, n);
-    z0 = __fmul_rn(rad, c);
-    z1 = __fmul_rn(rad, n);
-}
-
-// Quad block k of unit U on stream 2: normals 4k..4k+3
-__device__ __forceinline__ float4 normal_quad(uint64_t unit, uint32_t k, uint32_t key0, uint32_t key1) {
-    const uint4 X = philox4x32_10(make_uint4((uint32_t)unit, k, (uint32_t)(unit >> 32), 2u), key0, key1);
-    float4 z;
-    bm_pair(X.x, X.y & 0xFFFFFF00u, z.x, z.y);
-    bm_pair(X.z, X.w & 0xFFFFFF00u, z.z, z.w);
-    return z;
-}
-
 
 // ------------------------------------------------------------ two-lane binary32 helpers
 // Ops<false>: one packed FFMA2/FMUL2/FADD2 per step (both lanes in one
@@ -196,56 +122,39 @@ __device__ __forceinline__ F2 rsqrt2_from(F2 x, F2 mh) {
     return y;
 }
 
+// rad_spec on both lanes (spec/RNG.md §3): region r, v = r ? 2^24 - N : N, and
+// the row index 368 r + 16 e + j read straight off the bits of float(v) (exact:
+// its exponent field is 127 + e and its top four mantissa bits are j);
+// t = m - (1 + (2j + 1)/32) from the remaining mantissa bits (exact).
+template <bool SC>
+__device__ __forceinline__ F2 rad2(uint32_t Rx, uint32_t Ry, const float4* __restrict__ rt) {
+    using L = Ops<SC>;
+    const uint32_t nx = (Rx >> 8) | 1u, ny = (Ry >> 8) | 1u;
+    const uint32_t hx = nx >> 23, hy = ny >> 23;
+    const uint32_t vx = hx ? 0x1000000u - nx : nx, vy = hy ? 0x1000000u - ny : ny;
+    const uint32_t bx = __float_as_uint(__uint2float_rn(vx)), by = __float_as_uint(__uint2float_rn(vy));
+    const float4 cx = rt[(bx >> 19) - (127u << 4) + (hx ? 368u : 0u)];
+    const float4 cy = rt[(by >> 19) - (127u << 4) + (hy ? 368u : 0u)];
+    const F2 t = L::add(make_float2(__uint_as_float((bx & 0x7FFFFu) | 0x3F800000u),
+                                    __uint_as_float((by & 0x7FFFFu) | 0x3F800000u)), bc(-1.03125f));
+    F2 p = L::fma(make_float2(cx.w, cy.w), t, make_float2(cx.z, cy.z));
+    p = L::fma(p, t, make_float2(cx.y, cy.y));
+    return L::fma(p, t, make_float2(cx.x, cy.x));
+}
+
 // Two Box-Muller pairs at once (lane x: (Rx, Ax), lane y: (Ry, Ay)); angle words
-// have their low 8 bits clear.  zc = rad * cos phi, zs = rad * sin phi per lane
-// (spec/RNG.md §2-§6).  SLN/SRS/SSC choose scalar lanes for the ln, sqrt and
-// sincos parts (scheduling only; identical results).
+// have their low 8 bits clear.  rs = +-rad (half-turn sign), (cq, sq) = the
+// half-turn sin/cos polynomials, so z = (rs cq, rs sq) per lane (spec/RNG.md
+// §2-§6).  SRS/SSC choose scalar lanes for the radius and sincos parts
+// (scheduling only; identical results).
 // Angle given as (F, S): F holds the turn fraction bits of A >> 8 in MASK (bits 8..22
 // of A's bits 16..30 for 16-bit angles, 0..22 for 24-bit ones), S holds the half-turn
 // bit in bit 31.  The generic entry below derives them from an angle word A.
-template <bool SLN, bool SRS, bool SSC, uint32_t MASK>
+template <bool SRS, bool SSC, uint32_t MASK>
 __device__ __forceinline__ void bm_polar2_fs(uint32_t Rx, uint32_t Ry, uint32_t Fx, uint32_t Fy, uint32_t Sx,
-                                             uint32_t Sy, F2& rs, F2& cq, F2& sq) {
-    using L = Ops<SLN>;
+                                             uint32_t Sy, const float4* __restrict__ rt, F2& rs, F2& cq, F2& sq) {
     using Q = Ops<SSC>;
-    // u1 = ((R >> 8) | 1) * 2^-24: convert the odd integer exactly and fold the
-    // 2^-24 into the exponent constants of ln_spec (bits(u1) = bits(float(m)) - 24<<23)
-    const uint32_t ix = __float_as_uint(__uint2float_rn((Rx >> 8) | 1u));
-    const uint32_t iy = __float_as_uint(__uint2float_rn((Ry >> 8) | 1u));
-    const uint32_t tx = ix - 0x4B3504F3u, ty = iy - 0x4B3504F3u;        // = bits(u1) - 0x3F3504F3
-    const F2 m = make_float2(__uint_as_float((tx & 0x7FFFFFu) + 0x3F3504F3u),
-                             __uint_as_float((ty & 0x7FFFFFu) + 0x3F3504F3u));
-    const F2 fe = make_float2(__int2float_rn((int32_t)tx >> 23), __int2float_rn((int32_t)ty >> 23));
-    const F2 f = L::add(m, bc(-1.0f));
-    F2 P = L::fma(bc(D_L7), f, bc(D_L6));
-    P = L::fma(P, f, bc(D_L5));
-    P = L::fma(P, f, bc(D_L4));
-    P = L::fma(P, f, bc(D_L3));
-    P = L::fma(P, f, bc(D_L2));
-    P = L::fma(P, f, bc(D_L1));
-    P = L::fma(P, f, bc(D_L0));
-    F2 y = L::fma(L::mul(f, f), P, f);
-    y = L::fma(fe, bc(D_LN2_LO), y);
-    y = L::fma(fe, bc(D_LN2_HI), y);                          // y = ln_spec(u1) < 0
-    // rad = sqrt_spec(s), s = -2y (spec/RNG.md §4, Goldschmidt).  s is never formed:
-    // its bits are bits(y) + 0x80800000 (sign off, exponent + 1), and the first
-    // product g = s * y0 equals y * (-2 y0) exactly, with -2 y0 and h = 0.5 y0
-    // obtained by adjusting the seed's exponent bits.
-    using G = Ops<SRS>;
-    // y < 0, so bits(s) = bits(y) - 0x7F800000 and bits(s) >> 1 = (bits(y) >> 1) - 0x3FC00000
-    // exactly (even subtrahend, no wrap): the seed 0x5F375A86 - (bits(s) >> 1) and its
-    // exponent-adjusted forms fold the constant, leaving one shift and one subtract each.
-    const uint32_t shx = __float_as_uint(y.x) >> 1, shy = __float_as_uint(y.y) >> 1;
-    const F2 y0m2 = make_float2(__uint_as_float(0x1F775A86u - shx), __uint_as_float(0x1F775A86u - shy));  // -2 y0
-    F2 h = make_float2(__uint_as_float(0x9E775A86u - shx), __uint_as_float(0x9E775A86u - shy));           // y0 / 2
-    F2 g = G::mul(y, y0m2);
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const F2 rr = G::fma(neg2(g), h, bc(0.5f));
-        g = G::fma(g, rr, g);
-        h = G::fma(h, rr, h);
-    }
-    const F2 rad = G::fma(g, G::fma(neg2(g), h, bc(0.5f)), g);
+    const F2 rad = rad2<SRS>(Rx, Ry, rt);
     // sincos_spec: r from the angle bits, half-turn sign applied to rad
     const F2 r = Q::add(make_float2(__uint_as_float((Fx & MASK) | 0x3F800000u),
                                     __uint_as_float((Fy & MASK) | 0x3F800000u)),
@@ -261,9 +170,10 @@ __device__ __forceinline__ void bm_polar2_fs(uint32_t Rx, uint32_t Ry, uint32_t 
 }
 
 // Generic: angle words A with their low 8 bits clear.
-template <bool SLN, bool SRS, bool SSC>
-__device__ __forceinline__ void bm_polar2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay, F2& rs, F2& cq, F2& sq) {
-    bm_polar2_fs<SLN, SRS, SSC, 0x7FFFFFu>(Rx, Ry, Ax >> 8, Ay >> 8, Ax, Ay, rs, cq, sq);
+template <bool SRS, bool SSC>
+__device__ __forceinline__ void bm_polar2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay,
+                                          const float4* __restrict__ rt, F2& rs, F2& cq, F2& sq) {
+    bm_polar2_fs<SRS, SSC, 0x7FFFFFu>(Rx, Ry, Ax >> 8, Ay >> 8, Ax, Ay, rt, rs, cq, sq);
 }
 
 // Sextet packing (spec/RNG.md §6) for entity e of a Philox block X: one byte permute
@@ -274,15 +184,6 @@ __device__ __forceinline__ uint32_t sextet_angle_word(const uint4& X, int e) {
     return e == 0 ? __byte_perm(X.w, 0u, 0x1100u)        // bytes: -, X3.b0, X3.b1, X3.b1
          : e == 1 ? __byte_perm(X.w, 0u, 0x3320u)        // bytes: -, X3.b2, X3.b3, X3.b3
                   : __byte_perm(X.y, X.x, 0x4400u);      // bytes: X1.b0, X1.b0, X0.b0, X0.b0
-}
-
-// ... and as normals zc = rad cos phi, zs = rad sin phi.
-template <bool SLN, bool SRS, bool SSC>
-__device__ __forceinline__ void bm_pair2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay, F2& zc, F2& zs) {
-    F2 rs, cq, sq;
-    bm_polar2<SLN, SRS, SSC>(Rx, Ry, Ax, Ay, rs, cq, sq);
-    zc = Ops<SSC>::mul(rs, cq);
-    zs = Ops<SSC>::mul(rs, sq);
 }
 
 // Philox4x32-10 on counter (c0, s, c2, c3) for a loop over the block index s
@@ -325,23 +226,25 @@ struct PhiloxHoisted {
 // Sextet normals 12j..12j+11 of a hoisted stream unit: blocks 2j (lane x) and
 // 2j+1 (lane y), entity pairs e = 0, 1, 2 of each (spec/RNG.md §6 sextet
 // packing): normal 6b + 2e is zc[e], 6b + 2e + 1 is zs[e] of block b's lane.
-__device__ __forceinline__ void normal_sextet2_h(const PhiloxHoisted& rng, uint32_t j, F2 zc[3], F2 zs[3]) {
+__device__ __forceinline__ void normal_sextet2_h(const PhiloxHoisted& rng, const float4* __restrict__ rt, uint32_t j,
+                                                 F2 zc[3], F2 zs[3]) {
     const uint4 X = rng(2 * j), Y = rng(2 * j + 1);
     const uint32_t RX[3] = {X.x, X.y, X.z}, RY[3] = {Y.x, Y.y, Y.z};
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
         const uint32_t wx = sextet_angle_word(X, e), wy = sextet_angle_word(Y, e);
         F2 rs, cq, sq;
-        bm_polar2_fs<false, false, false, 0x7FFF00u>(RX[e], RY[e], wx, wy, wx, wy, rs, cq, sq);
+        bm_polar2_fs<false, false, 0x7FFF00u>(RX[e], RY[e], wx, wy, wx, wy, rt, rs, cq, sq);
         zc[e] = Ops<false>::mul(rs, cq);
         zs[e] = Ops<false>::mul(rs, sq);
     }
 }
 
 // Twelve stream-2 normals 12j..12j+11 as an array in stream order (blocks 2j, 2j+1).
-__device__ __forceinline__ void acc_normals12(const PhiloxHoisted& rng, uint32_t j, float g[12]) {
+__device__ __forceinline__ void acc_normals12(const PhiloxHoisted& rng, const float4* __restrict__ rt, uint32_t j,
+                                              float g[12]) {
     F2 zc[3], zs[3];
-    normal_sextet2_h(rng, j, zc, zs);
+    normal_sextet2_h(rng, rt, j, zc, zs);
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
         g[2 * e] = zc[e].x; g[2 * e + 1] = zs[e].x;
@@ -352,14 +255,15 @@ __device__ __forceinline__ void acc_normals12(const PhiloxHoisted& rng, uint32_t
 // Ragged tail: normals 12j..12j+n-1 (n <= 11).  When n <= 6 only block 2j is
 // drawn (pairs 0/1 in the two lanes, pair 2 in a second evaluation), saving a
 // Philox block and a third of the Box-Muller work; same values as acc_normals12.
-__device__ __forceinline__ void acc_normals_tail(const PhiloxHoisted& rng, uint32_t j, uint32_t n, float g[12]) {
-    if (n > 6) { acc_normals12(rng, j, g); return; }
+__device__ __forceinline__ void acc_normals_tail(const PhiloxHoisted& rng, const float4* __restrict__ rt, uint32_t j,
+                                                 uint32_t n, float g[12]) {
+    if (n > 6) { acc_normals12(rng, rt, j, g); return; }
     const uint4 X = rng(2 * j);
     const uint32_t w0 = sextet_angle_word(X, 0), w1 = sextet_angle_word(X, 1), w2 = sextet_angle_word(X, 2);
     F2 rs, cq, sq;
-    bm_polar2_fs<false, false, false, 0x7FFF00u>(X.x, X.y, w0, w1, w0, w1, rs, cq, sq);
+    bm_polar2_fs<false, false, 0x7FFF00u>(X.x, X.y, w0, w1, w0, w1, rt, rs, cq, sq);
     const F2 zc01 = Ops<false>::mul(rs, cq), zs01 = Ops<false>::mul(rs, sq);
-    bm_polar2_fs<false, false, false, 0x7FFF00u>(X.z, X.z, w2, w2, w2, w2, rs, cq, sq);
+    bm_polar2_fs<false, false, 0x7FFF00u>(X.z, X.z, w2, w2, w2, w2, rt, rs, cq, sq);
     const F2 zc2 = Ops<false>::mul(rs, cq), zs2 = Ops<false>::mul(rs, sq);
     g[0] = zc01.x; g[1] = zs01.x; g[2] = zc01.y; g[3] = zs01.y; g[4] = zc2.x; g[5] = zs2.x;
 #pragma unroll

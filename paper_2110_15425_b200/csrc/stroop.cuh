@@ -26,6 +26,7 @@ struct StroopArgs {
     float* __restrict__ net;
     key64_t* __restrict__ best;
     uint32_t key_signed;     // 1: best holds key ^ 2^63 (int64 MIN order)
+    const float4* __restrict__ rad_tab;        // device RT (spec/RNG.md §3)
 };
 
 // One LCA step of both response units (spec/MODELS.md §6 loop body; the old
@@ -59,6 +60,8 @@ struct Pathway {
 template <int BLOCK, int MINB = 0, bool TABLE = true>
 __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArgs a, uint32_t alloc_off) {
     extern __shared__ float s_htab[];                         // TABLE: [4][n_steps]
+    __shared__ float4 s_rt[RT_ROWS];
+    stage_rad_table(s_rt, a.rad_tab);
     const uint32_t t_alloc = alloc_off + blockIdx.y;           // index within [0, count)
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
         const uint32_t n6 = N / 6;
         for (uint32_t grp = 0; grp < n6; ++grp) {
             float g[12], s0[6], s1[6];
-            acc_normals12(rng, grp, g);
+            acc_normals12(rng, s_rt, grp, g);
 #pragma unroll
             for (int l = 0; l < 6; ++l) {
                 float h0, h1;
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
         const uint32_t rem = N - 6 * n6;
         if (rem) {  // ragged last group
             float g[12];
-            acc_normals_tail(rng, n6, 2 * rem, g);
+            acc_normals_tail(rng, s_rt, n6, 2 * rem, g);
 #pragma unroll
             for (int l = 0; l < 5; ++l) {
                 if ((uint32_t)l < rem) {
@@ -179,9 +182,10 @@ template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) stroop_energy_kernel(const StroopArgs a, uint32_t alloc,
                                                               unsigned long long* __restrict__ esum) {
     extern __shared__ unsigned long long s_esum[];          // [n_steps]
+    __shared__ float4 s_rt[RT_ROWS];
     const uint32_t N = a.n_steps;
     for (uint32_t n = threadIdx.x; n < N; n += BLOCK) s_esum[n] = 0ull;
-    __syncthreads();
+    stage_rad_table(s_rt, a.rad_tab);       // (its barrier also covers the clear)
     const uint32_t i = alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
     const float uc = __ldg(a.levels + k0), us = __ldg(a.levels + a.L0 + k1);
@@ -211,8 +215,8 @@ __global__ void __launch_bounds__(BLOCK) stroop_energy_kernel(const StroopArgs a
         for (uint32_t n = 1; n <= N; ++n) {
             const uint32_t grp = (n - 1) / 6, l = (n - 1) % 6;
             if (l == 0) {                                    // normals of steps 6grp+1 .. 6grp+6
-                if (N - 6 * grp >= 6) acc_normals12(rng, grp, g);
-                else acc_normals_tail(rng, grp, 2 * (N - 6 * grp), g);
+                if (N - 6 * grp >= 6) acc_normals12(rng, s_rt, grp, g);
+                else acc_normals_tail(rng, s_rt, grp, 2 * (N - 6 * grp), g);
             }
             float h0, h1;
             pw.at(n, h0, h1);
@@ -265,6 +269,7 @@ struct ExtStroopArgs {
     float* __restrict__ net;
     key64_t* __restrict__ best;
     uint32_t key_signed;     // 1: best holds key ^ 2^63 (int64 MIN order)
+    const float4* __restrict__ rad_tab;        // device RT (spec/RNG.md §3)
 };
 
 __device__ __forceinline__ void ddm_latch(float x, float z, uint32_t n, int& hit, uint32_t& st) {
@@ -276,6 +281,8 @@ __device__ __forceinline__ void ddm_latch(float x, float z, uint32_t n, int& hit
 
 template <int BLOCK, int VARIANT>
 __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopArgs a, uint32_t alloc_off) {
+    __shared__ float4 s_rt[RT_ROWS];
+    stage_rad_table(s_rt, a.rad_tab);
     const uint32_t t_alloc = alloc_off + blockIdx.y;
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
         const uint32_t n6 = a.n_d / 6;
         for (uint32_t grp = 0; grp < n6; ++grp) {
             float g[12], y1[6], y2[6];
-            acc_normals12(rng, grp, g);
+            acc_normals12(rng, s_rt, grp, g);
 #pragma unroll
             for (int l = 0; l < 6; ++l) {
                 if (VARIANT == 0) {
@@ -354,7 +361,7 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
         const uint32_t rem = a.n_d - 6 * n6;
         if (rem) {  // ragged last group
             float g[12];
-            acc_normals_tail(rng, n6, 2 * rem, g);
+            acc_normals_tail(rng, s_rt, n6, 2 * rem, g);
 #pragma unroll
             for (int l = 0; l < 5; ++l) {
                 if ((uint32_t)l < rem) {

@@ -29,7 +29,7 @@ def test_bench_json_contract_on_gpu():
     assert per_gpu == d["config"]["allocations"] == 10 ** 6
     assert "CUDA graph" in d["timing"]["step"]
     r = d["roofline"]
-    assert r["bound"] == "alu" and r["unit"] == "TFLOP/s" and 0 < r["frac_counted_method"] < r["frac"] < r["frac_executed"] < 1
+    assert r["bound"] == "alu" and r["unit"] == "TFLOP/s" and 0 < r["frac_counted_method"] < r["frac_executed"] < r["frac"] < 1
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9 and r["frac_method"] == r["frac"]
     assert r["cost_array_write"]["bytes_per_launch"] == 4 * per_gpu
     c = d["cpu_baseline"]

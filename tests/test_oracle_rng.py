@@ -54,26 +54,46 @@ def test_philox_matches_curand_host_generator(orc):
             assert np.array_equal(blk[t], orc.philox((t >> 16, 0, t & 0xFFFF, 0), key)), (seed, t)
 
 
-def test_ln_exhaustive_on_uniform_domain(orc):
-    """Every binary32 in [2^-24, 1): |ln_spec - log| <= 4 ulp (binary64 libm)."""
-    worst = 0.0
-    for e in range(-24, 0):
-        b0 = np.float32(2.0 ** e).view(np.uint32)
-        b1 = np.float32(2.0 ** (e + 1)).view(np.uint32)
-        x = np.arange(b0, b1, dtype=np.uint32).view(np.float32)
-        y = orc.ln_array(x).astype(np.float64)
-        ref = np.log(x.astype(np.float64))
-        worst = max(worst, float((np.abs(y - ref) / _ulp32(ref)).max()))
-    assert worst <= 4.0, worst
-    assert orc.ln(1.0) == 0.0
+def test_rad_exhaustive_over_all_radius_words(orc):
+    """rad_spec (spec/RNG.md §3) for every one of the 2^23 radius values
+    N = (R >> 8) | 1: within 4 * 2^-24 relative of sqrt(-2 ln(N 2^-24)) in
+    binary64 libm (the plain definition of the Box-Muller radius)."""
+    N = np.arange(1, 2 ** 24, 2, dtype=np.uint64)
+    R = (N << np.uint64(8)).astype(np.uint32)          # (R >> 8) | 1 == N
+    y = orc.rad_array(R).astype(np.float64)
+    ref = np.sqrt(-2.0 * np.log(N.astype(np.float64) * 2.0 ** -24))
+    rel = np.abs(y - ref) / ref
+    assert rel.max() <= 4 * 2.0 ** -24, rel.max() / 2.0 ** -24
+    # the low byte of the word and its lowest retained bit do not matter: N is forced odd
+    assert np.array_equal(orc.rad_array(R | np.uint32(0xFF)), y.astype(np.float32))
+    assert np.array_equal(orc.rad_array(R ^ np.uint32(0x100)), y.astype(np.float32))
 
 
-def test_ln_wide_range_sampled(orc):
-    x = np.random.default_rng(1).uniform(-60, 60, 200000)
-    x = np.exp2(x).astype(np.float32)
-    y = orc.ln_array(x).astype(np.float64)
-    ref = np.log(x.astype(np.float64))
-    assert (np.abs(y - ref) / _ulp32(ref)).max() <= 4.0
+def test_rad_table_is_the_interpolating_cubic(orc):
+    """Independent check of the table RT: in every segment (region r, octave e,
+    sub-segment j) the stored cubic, evaluated in binary64 from its binary32
+    coefficients, passes through sqrt(-2 ln u1) at the four nodes
+    t = (-3, -1, 1, 3)/128 (numpy's own interpolant through those points agrees
+    coefficient by coefficient to binary32 rounding)."""
+    T = orc.rad_table().astype(np.float64)
+    tau = np.array([-3, -1, 1, 3], np.float64) / 128
+    worst_val, worst_coef = 0.0, 0.0
+    for r in (0, 1):
+        for e in range(23):
+            for j in range(16):
+                c = 1 + (2 * j + 1) / 32
+                x = (c + tau) * 2.0 ** e
+                Nk = 2.0 ** 24 - x if r else x
+                f = np.sqrt(-2 * np.log(Nk * 2.0 ** -24))
+                row = T[368 * r + 16 * e + j]
+                p = row[0] + tau * (row[1] + tau * (row[2] + tau * row[3]))
+                worst_val = max(worst_val, float(np.max(np.abs(p - f) / f)))
+                want = np.polyfit(tau, f, 3)[::-1]
+                scale = np.abs(want) * np.array([1, 1 / 32, 1 / 32 ** 2, 1 / 32 ** 3]) / abs(want[0])
+                dev = np.abs(row - want) * np.array([1, 1 / 32, 1 / 32 ** 2, 1 / 32 ** 3]) / abs(want[0])
+                worst_coef = max(worst_coef, float(dev.max()))
+    assert worst_val < 2e-7, worst_val
+    assert worst_coef < 1e-7, worst_coef
 
 
 def test_rsqrt_dense(orc):
@@ -84,19 +104,6 @@ def test_rsqrt_dense(orc):
         x = np.arange(b0, b1, 5, dtype=np.uint32).view(np.float32)
         y = orc.rsqrt_array(x).astype(np.float64)
         ref = 1.0 / np.sqrt(x.astype(np.float64))
-        worst = max(worst, float((np.abs(y - ref) / ref).max()))
-    assert worst <= 4 * 2.0 ** -24, worst
-
-
-def test_sqrt_goldschmidt_on_radius_domain(orc):
-    """sqrt_spec over every binary32 in [6e-8, 34] (the Box-Muller s = -2 ln u1 range)."""
-    lo = np.float32(5.9e-8).view(np.uint32)
-    hi = np.float32(34.0).view(np.uint32)
-    worst = 0.0
-    for b0 in range(int(lo), int(hi), 1 << 23):
-        x = np.arange(b0, min(int(hi), b0 + (1 << 23)), dtype=np.uint32).view(np.float32)
-        y = orc.sqrt_array(x).astype(np.float64)
-        ref = np.sqrt(x.astype(np.float64))
         worst = max(worst, float((np.abs(y - ref) / ref).max()))
     assert worst <= 4 * 2.0 ** -24, worst
 
@@ -170,8 +177,10 @@ def test_sextet_normals_moments_independence(orc):
 
 
 def test_uniform_endpoints(orc):
-    """u1 = 2^-24 gives the largest radius sqrt(48 ln 2); u1 = 1-2^-24 the smallest."""
-    big = orc.ln(2.0 ** -24)
-    assert abs(-2 * big - 48 * math.log(2)) < 1e-5
-    small = orc.ln(1 - 2.0 ** -24)
-    assert small < 0 and abs(small + 2.0 ** -24) < 1e-12
+    """u1 = 2^-24 (N = 1) gives the largest radius sqrt(48 ln 2); u1 = 1 - 2^-24
+    (N = 2^24 - 1) the smallest, sqrt(-2 ln(1 - 2^-24)) ~ 2^-11.5."""
+    big = orc.rad(0)
+    assert abs(big - math.sqrt(48 * math.log(2))) <= 4 * 2.0 ** -24 * big
+    small = orc.rad(0xFFFFFFFF)
+    ref = math.sqrt(-2 * math.log1p(-2.0 ** -24))
+    assert abs(small - ref) <= 4 * 2.0 ** -24 * ref
