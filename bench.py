@@ -47,11 +47,11 @@ UNIT = "evals/s"
 FLOPS_PER_SAMPLE = 210
 FLOPS_PER_ALLOC = 15
 FLOPS_PER_CALL = 0
-FLOPS_PER_SAMPLE_METHOD = 133   # counted (test_method_flop_count)
+FLOPS_PER_SAMPLE_METHOD = 131   # counted (test_method_flop_count)
 FLOPS_PER_ALLOC_METHOD = 13
-FLOPS_PER_CALL_METHOD = 32
-FLOPS_PER_SAMPLE_EXEC = 175     # counted (test_flop_count_per_sample_matches_hand_count)
-FLOPS_PER_CALL_EXEC = 74
+FLOPS_PER_CALL_METHOD = 30
+FLOPS_PER_SAMPLE_EXEC = 159     # counted (test_flop_count_per_sample_matches_hand_count)
+FLOPS_PER_CALL_EXEC = 58
 FP32_LANES_PER_SM = 128       # FFMA lanes per SM (4 SMSP x 32), 2 flops per FMA
 FP32_PEAK_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12   # TFLOP/s (the extras' denominator)
 # accumulator models: SURVEY §8(d) ~30 flop per DDM step, ~75 per Stroop trial-step; counted:

@@ -259,8 +259,8 @@ static v2 od_action(v2 prey, v2 pred, v2 player, float kappa) {
     v2 vp = od_sub(prey, player), vd = od_sub(pred, player);
     float np = FFMA(vp.y, vp.y, FFMA(vp.x, vp.x, 0x1p-126f));
     float nd = FFMA(vd.y, vd.y, FFMA(vd.x, vd.x, 0x1p-126f));
-    float yp = od_rsqrt(np), yd = od_rsqrt(nd);
-    float c = FMUL(FMUL(-kappa, yd), FMUL(np, yp));       /* -kappa |v_p| / |v_d| */
+    float q = od_rsqrt(FMUL(np, nd));                     /* 1 / (|v_p| |v_d|), spec/MODELS.md §2 (R22b) */
+    float c = FMUL(FMUL(-kappa, np), q);                  /* -kappa |v_p| / |v_d| */
     v2 d = { FFMA(c, vd.x, vp.x), FFMA(c, vd.y, vp.y) };
     return d;
 }

@@ -78,15 +78,16 @@ __device__ __forceinline__ V2 vunit(V2 v) {
 
 // Action node (spec/MODELS.md §2): d = v_p + c v_d with c = -kappa |v_p| / |v_d|,
 // i.e. |v_p| (unit(v_p) - kappa unit(v_d)); only its direction is used downstream.
+// |v_p| / |v_d| = n_p rsqrt(n_p n_d): one rsqrt_spec (revision R22b).
 template <bool SC>
 __device__ __forceinline__ V2 action2(V2 q0, V2 q1, V2 q2, F2 mk) {
     using O = Ops<SC>;
     const V2 vp = vsub<SC>(q0, q2), vd = vsub<SC>(q1, q2);
     const F2 np = O::fma(vp.y, vp.y, O::fma(vp.x, vp.x, bc(0x1p-126f)));
     const F2 nd = O::fma(vd.y, vd.y, O::fma(vd.x, vd.x, bc(0x1p-126f)));
-    const F2 yp = rsqrt2_from<SC>(np, O::mul(np, bc(-0.5f)));
-    const F2 yd = rsqrt2_from<SC>(nd, O::mul(nd, bc(-0.5f)));
-    const F2 c = O::mul(O::mul(mk, yd), O::mul(np, yp));
+    const F2 pd = O::mul(np, nd);
+    const F2 q = rsqrt2_from<SC>(pd, O::mul(pd, bc(-0.5f)));
+    const F2 c = O::mul(O::mul(mk, np), q);
     return {O::fma(c, vd.x, vp.x), O::fma(c, vd.y, vp.y)};
 }
 
@@ -230,14 +231,22 @@ __device__ __forceinline__ void pp_publish_key(const PPArgs& a) {
 // and sub-lane 0 adds them in ascending sample order, so C is the same sum as
 // in the one-thread-per-allocation kernel, bit for bit.  Used when the grid is
 // too small to fill the GPU one thread per allocation and n_samples <= SMAX.
+// STAGE: copy the radius table into shared memory first (worth it when each
+// lane evaluates many samples); otherwise read it through L1 (the smallest grids,
+// where staging 11.8 KB per block would dominate a ~3 us launch).
+#ifndef DISTILL_PP_SMALL_STAGE_LANES
+#define DISTILL_PP_SMALL_STAGE_LANES 4     // stage for LANES <= this
+#endif
 template <int WARPS, int SMAX, int LANES = 32, bool PUB = false>
 __global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs a0) {
     constexpr int GPW = 32 / LANES;                          // allocations per warp
+    constexpr bool STAGE = LANES <= DISTILL_PP_SMALL_STAGE_LANES;
     __shared__ float s_e[WARPS][GPW][SMAX];
-    __shared__ float4 s_rt[RT_ROWS];
+    __shared__ float4 s_rt[STAGE ? RT_ROWS : 1];
     if (a0.status_dev && *a0.status_dev != 0) return;   // episode already over (uniform branch)
     const PPArgs a = pp_resolve_positions(a0);
-    stage_rad_table(s_rt, a.rad_tab);
+    if (STAGE) stage_rad_table(s_rt, a.rad_tab);
+    const float4* __restrict__ rt = STAGE ? s_rt : a.rad_tab;
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t grp = lane / LANES, sl = lane % LANES;
     const uint32_t tid = (blockIdx.x * WARPS + w) * GPW + grp;   // allocation within the launch
@@ -262,7 +271,7 @@ __global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs 
         rng.init(i, a.invocation, 1u, a.key0, a.key1);
         for (uint32_t s = 2 * sl; s < a.n_samples; s += 2 * LANES) {
             const F2 e = pp_pair_errors<false, false, false>(rng(s), rng(s + 1), s0, s1, s2, P0, P1, P2,
-                                                             bc(-a.kappa), us, s_rt);
+                                                             bc(-a.kappa), us, rt);
             s_e[w][grp][s] = e.x;
             if (s + 1 < a.n_samples) s_e[w][grp][s + 1] = e.y;
         }

@@ -189,10 +189,10 @@ def test_golden_cfg1(orc):
 
 
 def test_flop_count_per_sample_matches_hand_count(orc):
-    """Counting build: 175 binary32 flops per PP sample (fma = 2), the figure
+    """Counting build: 159 binary32 flops per PP sample (fma = 2), the figure
     DESIGN.md §6 derives by hand from spec/RNG.md + spec/MODELS.md:
     3 x (Box-Muller polar 27 (radius table cubic 7, sincos 20) + obs 5)
-    + action 51 + objective 28."""
+    + action 35 (one rsqrt_spec since R22b) + objective 28."""
     L = orc.lib(counting=True)
     assert L.od_is_counting_build() == 1
     cfg = W.pp_cfg3()
@@ -202,20 +202,20 @@ def test_flop_count_per_sample_matches_hand_count(orc):
         orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, 10, S, 1, counting=True)
         return L.od_flops_read()
 
-    assert (flops(101) - flops(100)) == 10 * 175
-    per_alloc = (flops(100) - 10 * 100 * 175)
-    # per call: u_star = action 51 + unit 22 = 73, plus dsig 1;
+    assert (flops(101) - flops(100)) == 10 * 159
+    per_alloc = (flops(100) - 10 * 100 * 159)
+    # per call: u_star = action 35 + unit 22 = 57, plus dsig 1;
     # per allocation: 3 sigma fma (6) + K (5) + mean (2) = 13
-    assert per_alloc == 74 + 10 * 13
+    assert per_alloc == 58 + 10 * 13
 
 
 def test_method_flop_count(orc):
     """The method count the roofline's headline fraction uses (SURVEY §8(d):
     fma = 2, add/mul = 1, a square root = 1, a divide = 1): the counting build in
     method mode scores sqrt_spec as 1 flop and rsqrt_spec as 2 (sqrt + divide)
-    instead of their Newton steps.  PP: 133 per sample (175 executed: the 3 x 14
+    instead of their Newton steps.  PP: 131 per sample (159 executed: the 2 x 14
     Newton flops of the body's rsqrt_spec are implementation, not method), 13 per
-    allocation, 32 per call; one sextet (6 accumulator normals): 87, no square
+    allocation, 30 per call; one sextet (6 accumulator normals): 87, no square
     root left in it since the radius became a table cubic (spec/RNG.md §3)."""
     L = orc.lib(counting=True)
     cfg = W.pp_cfg3()
@@ -227,9 +227,9 @@ def test_method_flop_count(orc):
 
     try:
         L.od_flops_method(1)
-        assert flops(10, 101) - flops(10, 100) == 10 * 133
-        a, b = flops(10, 100) - 10 * 100 * 133, flops(20, 100) - 20 * 100 * 133
-        assert (b - a) == 10 * 13 and a - 10 * 13 == 32
+        assert flops(10, 101) - flops(10, 100) == 10 * 131
+        a, b = flops(10, 100) - 10 * 100 * 131, flops(20, 100) - 20 * 100 * 131
+        assert (b - a) == 10 * 13 and a - 10 * 13 == 30
         z = np.zeros(6, np.float32)
         L.od_flops_reset()
         L.od_normal_acc(1, 5, 0, 1, z)
