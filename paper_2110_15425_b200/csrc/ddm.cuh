@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
     __shared__ float4 s_rt[RT_ROWS];
     const uint32_t n_rt = 2 * a.n_rt_bins + 1, n_x = a.n_x_bins + 2, n_all = n_rt + n_x;
     for (uint32_t b = threadIdx.x; b < n_all; b += BLOCK) s_hist[b] = 0;
-    stage_rad_table(s_rt, a.rad_tab);      // (its barrier also covers the histogram clear)
+    stage_rad_table<BLOCK>(s_rt, a.rad_tab);      // (its barrier also covers the histogram clear)
 
     const float nsd = __fmul_rn(a.noise, __fsqrt_rn(a.dt));
     const float sc = __fdiv_rn(__uint2float_rn(a.n_x_bins), __fadd_rn(a.x_hi, -a.x_lo));
@@ -147,7 +147,7 @@ struct DdmgArgs {
 template <int BLOCK, int MINB = 0>
 __global__ void __launch_bounds__(BLOCK, MINB) ddmg_sim_kernel(const DdmgArgs a, uint32_t alloc_off) {
     __shared__ float4 s_rt[RT_ROWS];
-    stage_rad_table(s_rt, a.rad_tab);
+    stage_rad_table<BLOCK>(s_rt, a.rad_tab);
     const uint32_t t_alloc = alloc_off + blockIdx.y;
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;

@@ -162,17 +162,18 @@ __device__ __forceinline__ F2 pp_pair_errors(const uint4& X, const uint4& Y, flo
     return objective2<SOBJ>(d, us);
 }
 
-template <int MASK, bool PIPE, bool EVEN = false>
+// SMEM_LEV (tools/pp_tune.cu A/B only): `lev` is a shared-memory copy of the level table.
+template <int MASK, bool PIPE, bool EVEN = false, bool SMEM_LEV = false>
 __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, float2 ustar,
-                                               const float4* __restrict__ rt) {
+                                               const float4* __restrict__ rt, const float* lev = nullptr) {
     constexpr bool SOBJ = MASK & PP_SC_OBJECTIVE;
     constexpr bool SRS2 = MASK & PP_SC_RSQ2, SSC2 = MASK & PP_SC_SC2;
     // a1: mixed-radix decode, signal 0 most significant
     const uint32_t k2 = i % a.L2, r = i / a.L2;
     const uint32_t k1 = r % a.L1, k0 = r / a.L1;
-    const float a0 = __ldg(a.levels + k0);
-    const float a1 = __ldg(a.levels + a.L0 + k1);
-    const float a2 = __ldg(a.levels + a.L0 + a.L1 + k2);
+    const float a0 = SMEM_LEV ? lev[k0] : __ldg(a.levels + k0);
+    const float a1 = SMEM_LEV ? lev[a.L0 + k1] : __ldg(a.levels + a.L0 + k1);
+    const float a2 = SMEM_LEV ? lev[a.L0 + a.L1 + k2] : __ldg(a.levels + a.L0 + a.L1 + k2);
     const float dsig = __fadd_rn(a.sigma_min, -a.sigma_max);
     const float s0 = __fmaf_rn(a0, dsig, a.sigma_max);
     const float s1 = __fmaf_rn(a1, dsig, a.sigma_max);
@@ -231,22 +232,15 @@ __device__ __forceinline__ void pp_publish_key(const PPArgs& a) {
 // and sub-lane 0 adds them in ascending sample order, so C is the same sum as
 // in the one-thread-per-allocation kernel, bit for bit.  Used when the grid is
 // too small to fill the GPU one thread per allocation and n_samples <= SMAX.
-// STAGE: copy the radius table into shared memory first (worth it when each
-// lane evaluates many samples); otherwise read it through L1 (the smallest grids,
-// where staging 11.8 KB per block would dominate a ~3 us launch).
-#ifndef DISTILL_PP_SMALL_STAGE_LANES
-#define DISTILL_PP_SMALL_STAGE_LANES 4     // stage for LANES <= this
-#endif
 template <int WARPS, int SMAX, int LANES = 32, bool PUB = false>
 __global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs a0) {
     constexpr int GPW = 32 / LANES;                          // allocations per warp
-    constexpr bool STAGE = LANES <= DISTILL_PP_SMALL_STAGE_LANES;
     __shared__ float s_e[WARPS][GPW][SMAX];
-    __shared__ float4 s_rt[STAGE ? RT_ROWS : 1];
+    __shared__ float4 s_rt[RT_ROWS];
     if (a0.status_dev && *a0.status_dev != 0) return;   // episode already over (uniform branch)
     const PPArgs a = pp_resolve_positions(a0);
-    if (STAGE) stage_rad_table(s_rt, a.rad_tab);
-    const float4* __restrict__ rt = STAGE ? s_rt : a.rad_tab;
+    stage_rad_table_async<WARPS * 32>(s_rt, a.rad_tab);   // completed by pp_ustar_block's barrier
+    const float4* __restrict__ rt = s_rt;
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t grp = lane / LANES, sl = lane % LANES;
     const uint32_t tid = (blockIdx.x * WARPS + w) * GPW + grp;   // allocation within the launch
@@ -304,7 +298,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs 
     }
     a = pp_resolve_positions(a);
     __shared__ float4 s_rt[RT_ROWS];
-    stage_rad_table(s_rt, a.rad_tab);
+    stage_rad_table_async<BLOCK>(s_rt, a.rad_tab);      // completed by pp_ustar_block's barrier
     const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
     const float2 ustar = pp_ustar_block(a);
     key64_t key = KEY_INIT;

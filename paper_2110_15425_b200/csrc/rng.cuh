@@ -63,8 +63,28 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 // and staged into shared memory by every kernel that draws normals.
 constexpr int RT_ROWS = 736;
 
+// The copy without its barrier (callers whose next step is a block barrier
+// anyway).  Fully unrolled for the block size, so all of a thread's row loads
+// are in flight at once (one L2 latency, not RT_ROWS / BLOCK of them).
+template <int BLOCK>
+__device__ __forceinline__ void stage_rad_table_async(float4* s_rt, const float4* __restrict__ g_rt) {
+    constexpr int PER = (RT_ROWS + BLOCK - 1) / BLOCK;
+    float4 v[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int k = q * BLOCK + (int)threadIdx.x;
+        if (k < RT_ROWS) v[q] = __ldg(g_rt + k);
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int k = q * BLOCK + (int)threadIdx.x;
+        if (k < RT_ROWS) s_rt[k] = v[q];
+    }
+}
+
+template <int BLOCK>
 __device__ __forceinline__ void stage_rad_table(float4* s_rt, const float4* __restrict__ g_rt) {
-    for (int k = threadIdx.x; k < RT_ROWS; k += blockDim.x) s_rt[k] = __ldg(g_rt + k);
+    stage_rad_table_async<BLOCK>(s_rt, g_rt);
     __syncthreads();
 }
 

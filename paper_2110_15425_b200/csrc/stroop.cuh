@@ -61,7 +61,7 @@ template <int BLOCK, int MINB = 0, bool TABLE = true>
 __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArgs a, uint32_t alloc_off) {
     extern __shared__ float s_htab[];                         // TABLE: [4][n_steps]
     __shared__ float4 s_rt[RT_ROWS];
-    stage_rad_table(s_rt, a.rad_tab);
+    stage_rad_table<BLOCK>(s_rt, a.rad_tab);
     const uint32_t t_alloc = alloc_off + blockIdx.y;           // index within [0, count)
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(BLOCK) stroop_energy_kernel(const StroopArgs a
     __shared__ float4 s_rt[RT_ROWS];
     const uint32_t N = a.n_steps;
     for (uint32_t n = threadIdx.x; n < N; n += BLOCK) s_esum[n] = 0ull;
-    stage_rad_table(s_rt, a.rad_tab);       // (its barrier also covers the clear)
+    stage_rad_table<BLOCK>(s_rt, a.rad_tab);       // (its barrier also covers the clear)
     const uint32_t i = alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
     const float uc = __ldg(a.levels + k0), us = __ldg(a.levels + a.L0 + k1);
@@ -282,7 +282,7 @@ __device__ __forceinline__ void ddm_latch(float x, float z, uint32_t n, int& hit
 template <int BLOCK, int VARIANT>
 __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopArgs a, uint32_t alloc_off) {
     __shared__ float4 s_rt[RT_ROWS];
-    stage_rad_table(s_rt, a.rad_tab);
+    stage_rad_table<BLOCK>(s_rt, a.rad_tab);
     const uint32_t t_alloc = alloc_off + blockIdx.y;
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;

@@ -6,6 +6,7 @@
 #include <vector>
 #include "../paper_2110_15425_b200/csrc/ddm.cuh"
 #include "../paper_2110_15425_b200/csrc/stroop.cuh"
+#include "../paper_2110_15425_b200/csrc/rad_table.h"
 using namespace distill;
 
 static std::vector<unsigned long long> g_ref_ddm, g_ref_st;
@@ -68,8 +69,12 @@ void stroop(const char* name, StroopArgs a, bool ref) {
 }
 
 int main() {
+    std::vector<float4> rt(RT_ROWS);
+    build_rad_table(rt.data());
+    float4* drt; cudaMalloc(&drt, RT_ROWS * 16); cudaMemcpy(drt, rt.data(), RT_ROWS * 16, cudaMemcpyHostToDevice);
     // DDM cfg2
     DDMArgs d{};
+    d.rad_tab = drt;
     d.drift = 1; d.noise = 1; d.threshold = 1; d.x0 = 0; d.dt = 0.01f;
     d.n_steps = 1000; d.rt_bin_steps = 10; d.n_rt_bins = 100; d.n_x_bins = 128;
     d.x_lo = 10.f - 6.f * 3.16227766f; d.x_hi = 10.f + 6.f * 3.16227766f;
@@ -86,6 +91,7 @@ int main() {
     for (int k = 0; k < 100; ++k) lev[k] = lev[100 + k] = (float)k / 99.f;
     float* dl; cudaMalloc(&dl, 800); cudaMemcpy(dl, lev.data(), 800, cudaMemcpyHostToDevice);
     StroopArgs s{};
+    s.rad_tab = drt;
     s.g_c = 1; s.g_w = 1.5f; s.tau = 0.1f; s.leak = 0.2f; s.inh = 0.2f; s.noise = 0.5f; s.dt = 0.05f; s.thr = 1;
     s.reward = 1; s.rt_cost = 0.1f; s.n_steps = 200; s.w0 = 0.3f; s.w1 = 0.1f; s.L0 = 100; s.L1 = 100;
     s.n_trials = 100000; s.trial_begin = 0; s.trial_end = 100000; s.key0 = 42; s.key1 = 0;

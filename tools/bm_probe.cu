@@ -15,6 +15,19 @@
 #include "../paper_2110_15425_b200/csrc/rng.cuh"
 using namespace distill;
 
+// The round-1 radius polynomials this probe compared against (spec/RNG.md §3-4
+// before revision R10c; kept here so the probe still builds).
+#define D_LN2_HI 0x1.62e4p-1f
+#define D_LN2_LO 0x1.7f7d1cp-20f
+#define D_L0 (-0x1.fffff4p-2f)
+#define D_L1 0x1.5556e8p-2f
+#define D_L2 (-0x1.0006c4p-2f)
+#define D_L3 0x1.98da38p-3f
+#define D_L4 (-0x1.52fb94p-3f)
+#define D_L5 0x1.30d0aap-3f
+#define D_L6 (-0x1.277224p-3f)
+#define D_L7 0x1.6fc72p-4f
+
 constexpr int REP = 4;
 
 __device__ __forceinline__ uint32_t ang16(const uint4& X, int e) {
@@ -139,7 +152,7 @@ __global__ void __launch_bounds__(128, 6) k_bm(float* out, uint32_t key0, int n_
         for (int e = 0; e < 3; ++e) {
             F2 zc, zs;
             if (V == 0) {
-                bm_pair2<false, false, false>(RX[e], RY[e], ang16(X, e) << 16, ang16(Y, e) << 16, zc, zs);
+                sincos_poly(radius_poly(RX[e], RY[e]), ang16(X, e), ang16(Y, e), zc, zs);
             } else {
                 const F2 rad = (V == 1) ? radius_poly(RX[e], RY[e])
                              : (V == 2) ? radius_tab(RX[e], RY[e], lnt, seed)

@@ -1,20 +1,25 @@
 // Scheduling-variant sweep for pp_eval_grid (tools only, not product code):
 // every variant must produce bit-identical net values and key; prints ms and
 // registers per variant on cfg3 (1e6 allocations x 100 samples).
+// Round 2 adds the north star's two layout items as A/B variants:
+//   SMEM levels  — the level table staged in shared memory instead of __ldg;
+//   float4 store — each warp's 32 net values staged in shared memory and
+//                  written by 8 lanes as float4 instead of 32 scalar stores.
 #include <cstdio>
 #include <cstring>
 #include <vector>
 #include "../paper_2110_15425_b200/csrc/pp.cuh"
+#include "../paper_2110_15425_b200/csrc/rad_table.h"
 using namespace distill;
 
-// Tuning-only variant (not in the library; measured +0.4 %).
 // Persistent variant: a fixed grid of resident blocks pulls BLOCK-allocation
-// chunks from a device counter (zeroed by the caller before the launch), so
-// the last wave has no idle SMs; keys are min-combined per block across chunks.
-template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false, bool EVEN = false>
+// chunks from a device counter (zeroed by the caller before the launch).
+template <int BLOCK, int MINB = DISTILL_PP_MINB, bool EVEN = false>
 __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_persistent_kernel(const PPArgs a,
                                                                                unsigned int* __restrict__ counter) {
     __shared__ unsigned int s_chunk;
+    __shared__ float4 s_rt[RT_ROWS];
+    stage_rad_table_async<BLOCK>(s_rt, a.rad_tab);
     const uint32_t n_chunks = (a.count + BLOCK - 1) / BLOCK;
     const float2 ustar = pp_ustar_block(a);
     key64_t key = KEY_INIT;
@@ -27,7 +32,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_persistent_kernel(co
         const uint32_t tid = c * BLOCK + threadIdx.x;
         if (tid < a.count) {
             const uint32_t i = a.begin + tid;
-            const float C = pp_eval_alloc<MASK, PIPE, EVEN>(a, i, ustar);
+            const float C = pp_eval_alloc<0, false, EVEN>(a, i, ustar, s_rt);
             if (a.net) a.net[tid] = -C;
             const key64_t k = make_key(C, i);
             key = k < key ? k : key;
@@ -36,36 +41,52 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_persistent_kernel(co
     if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
 }
 
+// Layout A/B variant of pp_eval_grid_kernel (SMEM_LEV, STORE4).
+template <int BLOCK, int MINB, bool EVEN, bool SMEM_LEV, bool STORE4>
+__global__ void __launch_bounds__(BLOCK, MINB) pp_eval_layout_kernel(const PPArgs a) {
+    __shared__ float4 s_rt[RT_ROWS];
+    __shared__ float s_lev[SMEM_LEV ? 1024 : 1];
+    __shared__ float s_out[STORE4 ? BLOCK : 1];
+    stage_rad_table_async<BLOCK>(s_rt, a.rad_tab);
+    if (SMEM_LEV)
+        for (uint32_t k = threadIdx.x; k < a.L0 + a.L1 + a.L2; k += BLOCK) s_lev[k] = __ldg(a.levels + k);
+    const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
+    const float2 ustar = pp_ustar_block(a);
+    key64_t key = KEY_INIT;
+    float C = 0.0f;
+    if (tid < a.count) {
+        const uint32_t i = a.begin + tid;
+        C = pp_eval_alloc<0, false, EVEN, SMEM_LEV>(a, i, ustar, s_rt, s_lev);
+        key = make_key(C, i);
+    }
+    if (STORE4) {
+        s_out[threadIdx.x] = -C;
+        __syncwarp();
+        const uint32_t lane = threadIdx.x & 31, w0 = threadIdx.x & ~31u;
+        const uint32_t base = blockIdx.x * BLOCK + w0;
+        if (lane < 8 && base + 4 * lane + 3 < a.count)
+            reinterpret_cast<float4*>(a.net + base)[lane] = reinterpret_cast<const float4*>(s_out + w0)[lane];
+        else if (lane < 8)
+            for (uint32_t q = 0; q < 4; ++q)
+                if (base + 4 * lane + q < a.count) a.net[base + 4 * lane + q] = s_out[w0 + 4 * lane + q];
+    } else if (tid < a.count) {
+        a.net[tid] = -C;
+    }
+    if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
+}
 
 static unsigned int* g_counter = nullptr;
 
-template <int BLOCK, int MASK, int MINB, bool PIPE = false, bool PERS = false, bool EVEN = false>
-void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_ref) {
-    cudaFuncAttributes fa;
-    unsigned grid;
-    if (PERS) {
-        cudaFuncGetAttributes(&fa, pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE, EVEN>);
-        int per_sm = 0, n_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE, EVEN>,
-                                                      BLOCK, 0);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
-        grid = per_sm * n_sm;
-    } else {
-        cudaFuncGetAttributes(&fa, pp_eval_grid_kernel<BLOCK, MASK, MINB, PIPE, EVEN>);
-        grid = (a.count + BLOCK - 1) / BLOCK;
-    }
+template <typename F>
+void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_ref, F launch, int regs) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     float best = 1e30f;
-    for (int rep = 0; rep < 6; ++rep) {
+    for (int rep = 0; rep < 8; ++rep) {
         cudaMemset(a.best, 0xFF, 8);
+        cudaMemsetAsync(g_counter, 0, 4);
         cudaEventRecord(e0);
-        if (PERS) {
-            cudaMemsetAsync(g_counter, 0, 4);
-            pp_eval_grid_persistent_kernel<BLOCK, MASK, MINB, PIPE, EVEN><<<grid, BLOCK>>>(a, g_counter);
-        } else {
-            pp_eval_grid_kernel<BLOCK, MASK, MINB, PIPE, EVEN><<<grid, BLOCK>>>(a);
-        }
+        launch();
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -77,48 +98,62 @@ void run(const char* name, PPArgs a, float* ref_net, key64_t ref_key, bool is_re
     bool same = true;
     if (is_ref) memcpy(ref_net, h.data(), a.count * 4);
     else same = memcmp(ref_net, h.data(), a.count * 4) == 0 && k == ref_key;
-    const double flops = (double)a.count * (a.n_samples * 274.0 + 13) + 74;
-    printf("%-26s even%d b%4d m%2d minb%d pipe%d pers%d grid %6u regs %3d %8.4f ms %6.2f TF/s frac %.3f %s\n", name, (int)EVEN, BLOCK,
-           MASK, MINB, (int)PIPE, (int)PERS, grid, fa.numRegs, best, flops / best / 1e9, flops / best / 1e9 / 74.45,
+    printf("%-34s regs %3d %8.4f ms  %.3e evals/s  %s\n", name, regs, best, (double)a.count * a.n_samples / (best * 1e-3),
            same ? "bit-identical" : "MISMATCH");
 }
+
+template <typename K> int regs_of(K k) { cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, k); return fa.numRegs; }
 
 int main() {
     const int L = 100;
     std::vector<float> lev(3 * L);
     for (int d = 0; d < 3; ++d) for (int k = 0; k < L; ++k) lev[d * L + k] = (float)k / (float)(L - 1);
     float* dl; cudaMalloc(&dl, lev.size() * 4); cudaMemcpy(dl, lev.data(), lev.size() * 4, cudaMemcpyHostToDevice);
+    std::vector<float4> rt(RT_ROWS);
+    build_rad_table(rt.data());
+    float4* drt; cudaMalloc(&drt, RT_ROWS * 16); cudaMemcpy(drt, rt.data(), RT_ROWS * 16, cudaMemcpyHostToDevice);
     PPArgs a{};
     a.prey_x = 4; a.prey_y = 1; a.pred_x = -3; a.pred_y = 2; a.pl_x = 0; a.pl_y = 0;
     a.sigma_max = 2; a.sigma_min = 0.1f; a.kappa = 0.5f; a.w0 = a.w1 = a.w2 = 0.1f;
     a.L0 = a.L1 = a.L2 = L; a.n_samples = 100; a.invocation = 0; a.key0 = 42; a.key1 = 0;
-    a.begin = 0; a.count = L * L * L; a.levels = dl;
+    a.begin = 0; a.count = L * L * L; a.levels = dl; a.rad_tab = drt;
     cudaMalloc((void**)&a.net, a.count * 4); cudaMalloc((void**)&a.best, 8);
     std::vector<float> ref(a.count);
     cudaMalloc((void**)&g_counter, 4);
-    run<256, 0, 0>("packed (ref)", a, ref.data(), 0, true);
+    const unsigned grid = (a.count + 127) / 128;
+    run("shipped b128 minb7 (ref)", a, ref.data(), 0, true,
+        [&] { pp_eval_grid_kernel<128, 0, 7, false, true><<<grid, 128>>>(a); },
+        regs_of(pp_eval_grid_kernel<128, 0, 7, false, true>));
     key64_t rk; cudaMemcpy(&rk, a.best, 8, cudaMemcpyDeviceToHost);
+    printf("ref key %016llx\n", (unsigned long long)rk);
+    run("layout: ldg levels, scalar store", a, ref.data(), rk, false,
+        [&] { pp_eval_layout_kernel<128, 7, true, false, false><<<grid, 128>>>(a); },
+        regs_of(pp_eval_layout_kernel<128, 7, true, false, false>));
+    run("layout: SMEM levels", a, ref.data(), rk, false,
+        [&] { pp_eval_layout_kernel<128, 7, true, true, false><<<grid, 128>>>(a); },
+        regs_of(pp_eval_layout_kernel<128, 7, true, true, false>));
+    run("layout: float4 store", a, ref.data(), rk, false,
+        [&] { pp_eval_layout_kernel<128, 7, true, false, true><<<grid, 128>>>(a); },
+        regs_of(pp_eval_layout_kernel<128, 7, true, false, true>));
+    run("layout: SMEM levels + float4 store", a, ref.data(), rk, false,
+        [&] { pp_eval_layout_kernel<128, 7, true, true, true><<<grid, 128>>>(a); },
+        regs_of(pp_eval_layout_kernel<128, 7, true, true, true>));
+#define SHIP(B, N, name) run(name, a, ref.data(), rk, false, [&] { pp_eval_grid_kernel<B, 0, N, false, true><<<(a.count + B - 1) / B, B>>>(a); }, regs_of(pp_eval_grid_kernel<B, 0, N, false, true>))
+    SHIP(128, 6, "b128 minb6");
+    SHIP(128, 8, "b128 minb8");
+    SHIP(128, 0, "b128 minb0");
+    SHIP(256, 3, "b256 minb3");
+    SHIP(256, 4, "b256 minb4");
+    SHIP(64, 14, "b64 minb14");
     {
-        unsigned long long hsh = 1469598103934665603ull;
-        const unsigned char* b = (const unsigned char*)ref.data();
-        for (size_t q = 0; q < ref.size() * 4; ++q) hsh = (hsh ^ b[q]) * 1099511628211ull;
-        printf("ref key %016llx net fnv1a %016llx\n", (unsigned long long)rk, hsh);
+        int per_sm = 0, n_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pp_eval_grid_persistent_kernel<128, 7, true>, 128, 0);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+        const unsigned pg = per_sm * n_sm;
+        run("persistent b128 minb7", a, ref.data(), rk, false,
+            [&] { pp_eval_grid_persistent_kernel<128, 7, true><<<pg, 128>>>(a, g_counter); },
+            regs_of(pp_eval_grid_persistent_kernel<128, 7, true>));
     }
-#define V(B, M, N, P, Q, E, name) run<B, M, N, P, Q, E>(name, a, ref.data(), rk, false)
-    V(128, 0, 0, false, false, true, "b128 even");
-    V(128, 0, 6, false, false, true, "b128 even minb6");
-    V(128, 0, 7, false, false, true, "b128 even minb7");
-    V(128, 0, 8, false, false, true, "b128 even minb8");
-    V(128, 0, 9, false, false, true, "b128 even minb9");
-    V(128, 0, 10, false, false, true, "b128 even minb10");
-    V(128, 0, 12, false, false, true, "b128 even minb12");
-    V(128, 0, 8, false, true, true, "b128 even minb8 pers");
-    V(128, 0, 7, false, true, true, "b128 even minb7 pers");
-    V(64, 0, 16, false, false, true, "b64 even minb16");
-    V(64, 0, 16, false, true, true, "b64 even minb16 pers");
-    V(256, 0, 4, false, false, true, "b256 even minb4");
-    V(256, 0, 4, false, true, true, "b256 even minb4 pers");
-    V(128, 0, 8, true, false, true, "b128 even minb8 pipe");
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
