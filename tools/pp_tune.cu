@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstring>
 #include <vector>
+#include <cmath>
+#include <algorithm>
 #include "../paper_2110_15425_b200/csrc/pp.cuh"
 #include "../paper_2110_15425_b200/csrc/rad_table.h"
 using namespace distill;
@@ -73,6 +75,111 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_layout_kernel(const PPArg
         a.net[tid] = -C;
     }
     if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
+}
+
+
+// ---- Prototype (timing only, NOT the spec): rsqrt by a replicated 32-row cubic
+// table (x = 2^(2k) y, y in [1, 4): row = octave parity x 16 sub-segments),
+// 8 lane-indexed copies so a warp's LDS.128 is conflict-free.  Values agree with
+// rsqrt_spec to a few ulp, so costs are compared to 1e-5 relative, not bit-exactly.
+__device__ __forceinline__ F2 rsq_tab2(F2 x, const float4* __restrict__ tab8, uint32_t lane8) {
+    using O = Ops<false>;
+    const uint32_t bx = __float_as_uint(x.x), by = __float_as_uint(x.y);
+    const float4 cx = tab8[((((bx >> 19) & 31u) ^ 16u) << 3) | lane8];
+    const float4 cy = tab8[((((by >> 19) & 31u) ^ 16u) << 3) | lane8];
+    const F2 t = O::add(make_float2(__uint_as_float((bx & 0x7FFFFu) | 0x3F800000u),
+                                    __uint_as_float((by & 0x7FFFFu) | 0x3F800000u)), bc(-1.03125f));
+    F2 g = O::fma(make_float2(cx.w, cy.w), t, make_float2(cx.z, cy.z));
+    g = O::fma(g, t, make_float2(cx.y, cy.y));
+    g = O::fma(g, t, make_float2(cx.x, cy.x));
+    const uint32_t kx = ((((bx >> 23) + 1u) >> 1) << 23) - (64u << 23);
+    const uint32_t ky = ((((by >> 23) + 1u) >> 1) << 23) - (64u << 23);
+    return make_float2(__uint_as_float(__float_as_uint(g.x) - kx), __uint_as_float(__float_as_uint(g.y) - ky));
+}
+
+__device__ __forceinline__ F2 proto_errors(const uint4& X, const uint4& Y, float s0, float s1, float s2, const V2& P0,
+                                           const V2& P1, const V2& P2, F2 mk, const V2& us, const float4* rt,
+                                           const float4* tab8, uint32_t lane8) {
+    using O = Ops<false>;
+    F2 r0, c0, n0, r1, c1, n1, r2, c2, n2;
+    const uint32_t wx0 = sextet_angle_word(X, 0), wy0 = sextet_angle_word(Y, 0);
+    const uint32_t wx1 = sextet_angle_word(X, 1), wy1 = sextet_angle_word(Y, 1);
+    const uint32_t wx2 = sextet_angle_word(X, 2), wy2 = sextet_angle_word(Y, 2);
+    bm_polar2_fs<false, false, 0x7FFF00u>(X.x, Y.x, wx0, wy0, wx0, wy0, rt, r0, c0, n0);
+    bm_polar2_fs<false, false, 0x7FFF00u>(X.y, Y.y, wx1, wy1, wx1, wy1, rt, r1, c1, n1);
+    bm_polar2_fs<false, false, 0x7FFF00u>(X.z, Y.z, wx2, wy2, wx2, wy2, rt, r2, c2, n2);
+    const F2 q0 = O::mul(bc(s0), r0), q1 = O::mul(bc(s1), r1), q2 = O::mul(bc(s2), r2);
+    const V2 o0 = {O::fma(q0, c0, P0.x), O::fma(q0, n0, P0.y)};
+    const V2 o1 = {O::fma(q1, c1, P1.x), O::fma(q1, n1, P1.y)};
+    const V2 o2 = {O::fma(q2, c2, P2.x), O::fma(q2, n2, P2.y)};
+    const V2 vp = vsub<false>(o0, o2), vd = vsub<false>(o1, o2);
+    const F2 np = O::fma(vp.y, vp.y, O::fma(vp.x, vp.x, bc(0x1p-126f)));
+    const F2 nd = O::fma(vd.y, vd.y, O::fma(vd.x, vd.x, bc(0x1p-126f)));
+    const F2 q = rsq_tab2(O::mul(np, nd), tab8, lane8);
+    const F2 c = O::mul(O::mul(mk, np), q);
+    const V2 d = {O::fma(c, vd.x, vp.x), O::fma(c, vd.y, vp.y)};
+    const F2 n2d = O::fma(d.y, d.y, O::fma(d.x, d.x, bc(0x1p-126f)));
+    const F2 y = rsq_tab2(n2d, tab8, lane8);
+    const F2 dx = O::fma(d.x, y, neg2(us.x)), dy = O::fma(d.y, y, neg2(us.y));
+    return O::fma(dy, dy, O::mul(dx, dx));
+}
+
+template <int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) pp_rtab_kernel(const PPArgs a, const float4* __restrict__ g_tab8) {
+    __shared__ float4 s_rt[RT_ROWS];
+    __shared__ float4 s_tab8[32 * 8];
+    stage_rad_table_async<BLOCK>(s_rt, a.rad_tab);
+    for (int k = threadIdx.x; k < 256; k += BLOCK) s_tab8[k] = g_tab8[k];
+    const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
+    const float2 ustar = pp_ustar_block(a);
+    const uint32_t lane8 = threadIdx.x & 7u;
+    key64_t key = KEY_INIT;
+    float C = 0.0f;
+    if (tid < a.count) {
+        const uint32_t i = a.begin + tid;
+        const uint32_t k2 = i % a.L2, r = i / a.L2;
+        const uint32_t k1 = r % a.L1, k0 = r / a.L1;
+        const float dsig = __fadd_rn(a.sigma_min, -a.sigma_max);
+        const float s0 = __fmaf_rn(__ldg(a.levels + k0), dsig, a.sigma_max);
+        const float s1 = __fmaf_rn(__ldg(a.levels + a.L0 + k1), dsig, a.sigma_max);
+        const float s2 = __fmaf_rn(__ldg(a.levels + a.L0 + a.L1 + k2), dsig, a.sigma_max);
+        const float K = __fmaf_rn(a.w2, __ldg(a.levels + a.L0 + a.L1 + k2),
+                                  __fmaf_rn(a.w1, __ldg(a.levels + a.L0 + k1), __fmul_rn(a.w0, __ldg(a.levels + k0))));
+        const V2 P0 = {bc(a.prey_x), bc(a.prey_y)}, P1 = {bc(a.pred_x), bc(a.pred_y)}, P2 = {bc(a.pl_x), bc(a.pl_y)};
+        const V2 us = {bc(ustar.x), bc(ustar.y)};
+        PhiloxHoisted rng;
+        rng.init(i, a.invocation, 1u, a.key0, a.key1);
+        float acc = 0.0f;
+        for (uint32_t s = 0; s < a.n_samples; s += 2) {
+            const F2 e = proto_errors(rng(s), rng(s + 1), s0, s1, s2, P0, P1, P2, bc(-a.kappa), us, s_rt, s_tab8, lane8);
+            acc = __fadd_rn(acc, e.x);
+            acc = __fadd_rn(acc, e.y);
+        }
+        C = __fadd_rn(__fdiv_rn(acc, __uint2float_rn(a.n_samples)), K);
+        key = make_key(C, i);
+    }
+    if (tid < a.count) a.net[tid] = -C;
+    if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
+}
+
+static void build_rsq_tab8(std::vector<float4>& t8) {
+    const double nodes[4] = {-3.0 / 128.0, -1.0 / 128.0, 1.0 / 128.0, 3.0 / 128.0};
+    t8.resize(256);
+    for (int p = 0; p < 2; ++p)
+        for (int j = 0; j < 16; ++j) {
+            const double c = 1.0 + (2.0 * j + 1.0) / 32.0;
+            double f[4];
+            for (int k = 0; k < 4; ++k) f[k] = 1.0 / std::sqrt((c + nodes[k]) * (p ? 2.0 : 1.0));
+            const double d01 = (f[1] - f[0]) / (nodes[1] - nodes[0]), d12 = (f[2] - f[1]) / (nodes[2] - nodes[1]);
+            const double d23 = (f[3] - f[2]) / (nodes[3] - nodes[2]);
+            const double d012 = (d12 - d01) / (nodes[2] - nodes[0]), d123 = (d23 - d12) / (nodes[3] - nodes[1]);
+            const double a3 = (d123 - d012) / (nodes[3] - nodes[0]), p01 = nodes[0] * nodes[1];
+            const double a2 = d012 - a3 * ((nodes[0] + nodes[1]) + nodes[2]);
+            const double a1 = (d01 - d012 * (nodes[0] + nodes[1])) + a3 * ((p01 + nodes[0] * nodes[2]) + nodes[1] * nodes[2]);
+            const double a0 = ((f[0] - d01 * nodes[0]) + d012 * p01) - a3 * (p01 * nodes[2]);
+            for (int l = 0; l < 8; ++l)
+                t8[((p * 16 + j) << 3) | l] = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+        }
 }
 
 static unsigned int* g_counter = nullptr;
@@ -153,6 +260,26 @@ int main() {
         run("persistent b128 minb7", a, ref.data(), rk, false,
             [&] { pp_eval_grid_persistent_kernel<128, 7, true><<<pg, 128>>>(a, g_counter); },
             regs_of(pp_eval_grid_persistent_kernel<128, 7, true>));
+    }
+    {   // prototype: rsqrt table (tolerance check instead of bit identity)
+        std::vector<float4> t8;
+        build_rsq_tab8(t8);
+        float4* d8; cudaMalloc(&d8, 256 * 16); cudaMemcpy(d8, t8.data(), 256 * 16, cudaMemcpyHostToDevice);
+        cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+        float best = 1e30f;
+        for (int rep = 0; rep < 8; ++rep) {
+            cudaEventRecord(e0);
+            pp_rtab_kernel<128, 7><<<grid, 128>>>(a, d8);
+            cudaEventRecord(e1); cudaEventSynchronize(e1);
+            float ms; cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0 && ms < best) best = ms;
+        }
+        std::vector<float> h(a.count);
+        cudaMemcpy(h.data(), a.net, a.count * 4, cudaMemcpyDeviceToHost);
+        double worst = 0;
+        for (size_t q = 0; q < h.size(); ++q) worst = std::max(worst, (double)std::fabs(h[q] - ref[q]) / std::fabs(ref[q]));
+        printf("%-34s regs %3d %8.4f ms  %.3e evals/s  max rel diff vs shipped %.2e\n", "PROTO rsqrt table (not spec)",
+               regs_of(pp_rtab_kernel<128, 7>), best, (double)a.count * a.n_samples / (best * 1e-3), worst);
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
