@@ -424,7 +424,7 @@ def run_ours(args):
     achieved_exec = flops_exec / (ms_kern / 1e3) / 1e12
     sm_load = clocks.get("sm_mhz")
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_pp_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02_pp_traffic.json")
     if os.path.exists(tpath):   # dram read + write per launch from the committed ncu --set full capture
         t = json.load(open(tpath))
         traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
@@ -441,7 +441,7 @@ def run_ours(args):
                                    "(the Newton steps of rsqrt_spec included)",
             "evals_per_s_per_gpu": per_gpu_evals_s,
             "evals_per_s_vs_survey_50pct_point": per_gpu_evals_s / EVALS_PER_S_AT_50PCT,
-            "traffic": traffic, "traffic_source": "profiles/r01_pp_traffic.json (ncu --set full, cfg3)",
+            "traffic": traffic, "traffic_source": "profiles/r02_pp_traffic.json (ncu --set full, cfg3)",
             "algorithmic_bytes_per_launch": count * 4 + 8 + sum(cfg.n_levels) * 4,
             "kernel": "pp_eval_grid_kernel", "kernel_ms": ms_kern,
             "algorithmic_flops_per_launch": flops_launch,
