@@ -109,7 +109,6 @@ enum : int {
     PP_SC_OBJECTIVE = 1,    // unit(d) + objective
     PP_SC_UNIT_PRED = 2,    // unit(o_pred - o_player)
     PP_SC_UNIT_PREY = 4,    // unit(o_prey - o_player)
-    PP_SC_RSQ2 = 16,        // radius of entity 2
     PP_SC_SC2 = 32,         // sincos of entity 2
 };
 #ifndef DISTILL_PP_MASK
@@ -140,7 +139,7 @@ __device__ __forceinline__ float2 pp_ustar_block(const PPArgs& a) {
 // a3 + a4 for the sample pair whose Philox blocks are X (lane x) and Y (lane y):
 // sextet packing -> three 2-D Box-Muller pairs (spec/RNG.md §6), observations
 // p + sigma rad (cos, sin), Action, Objective.  Returns the two squared chords.
-template <bool SOBJ, bool SRS2, bool SSC2>
+template <bool SOBJ, bool SSC2>
 __device__ __forceinline__ F2 pp_pair_errors(const uint4& X, const uint4& Y, float s0, float s1, float s2,
                                              const V2& P0, const V2& P1, const V2& P2, F2 mk, const V2& us,
                                              const float4* __restrict__ rt) {
@@ -149,9 +148,9 @@ __device__ __forceinline__ F2 pp_pair_errors(const uint4& X, const uint4& Y, flo
         const uint32_t wx0 = sextet_angle_word(X, 0), wy0 = sextet_angle_word(Y, 0);
         const uint32_t wx1 = sextet_angle_word(X, 1), wy1 = sextet_angle_word(Y, 1);
         const uint32_t wx2 = sextet_angle_word(X, 2), wy2 = sextet_angle_word(Y, 2);
-        bm_polar2_fs<false, false, 0x7FFF00u>(X.x, Y.x, wx0, wy0, wx0, wy0, rt, r0, c0, n0);
-        bm_polar2_fs<false, false, 0x7FFF00u>(X.y, Y.y, wx1, wy1, wx1, wy1, rt, r1, c1, n1);
-        bm_polar2_fs<SRS2, SSC2, 0x7FFF00u>(X.z, Y.z, wx2, wy2, wx2, wy2, rt, r2, c2, n2);
+        bm_polar2_fs<false, 0x7FFF00u>(X.x, Y.x, wx0, wy0, wx0, wy0, rt, r0, c0, n0);
+        bm_polar2_fs<false, 0x7FFF00u>(X.y, Y.y, wx1, wy1, wx1, wy1, rt, r1, c1, n1);
+        bm_polar2_fs<SSC2, 0x7FFF00u>(X.z, Y.z, wx2, wy2, wx2, wy2, rt, r2, c2, n2);
     }
     using O = Ops<false>;
     const F2 q0 = O::mul(bc(s0), r0), q1 = O::mul(bc(s1), r1), q2 = O::mul(bc(s2), r2);
@@ -167,7 +166,7 @@ template <int MASK, bool PIPE, bool EVEN = false, bool SMEM_LEV = false>
 __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, float2 ustar,
                                                const float4* __restrict__ rt, const float* lev = nullptr) {
     constexpr bool SOBJ = MASK & PP_SC_OBJECTIVE;
-    constexpr bool SRS2 = MASK & PP_SC_RSQ2, SSC2 = MASK & PP_SC_SC2;
+    constexpr bool SSC2 = MASK & PP_SC_SC2;
     // a1: mixed-radix decode, signal 0 most significant
     const uint32_t k2 = i % a.L2, r = i / a.L2;
     const uint32_t k1 = r % a.L1, k0 = r / a.L1;
@@ -199,7 +198,7 @@ __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, floa
         } else {
             X = rng(s); Y = rng(s + 1);
         }
-        const F2 e = pp_pair_errors<SOBJ, SRS2, SSC2>(X, Y, s0, s1, s2, P0, P1, P2, mk, us, rt);
+        const F2 e = pp_pair_errors<SOBJ, SSC2>(X, Y, s0, s1, s2, P0, P1, P2, mk, us, rt);
         // a7: sequential sum in ascending sample order
         acc = __fadd_rn(acc, e.x);
         if (EVEN || s + 1 < a.n_samples) acc = __fadd_rn(acc, e.y);
@@ -264,7 +263,7 @@ __global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs 
         PhiloxHoisted rng;
         rng.init(i, a.invocation, 1u, a.key0, a.key1);
         for (uint32_t s = 2 * sl; s < a.n_samples; s += 2 * LANES) {
-            const F2 e = pp_pair_errors<false, false, false>(rng(s), rng(s + 1), s0, s1, s2, P0, P1, P2,
+            const F2 e = pp_pair_errors<false, false>(rng(s), rng(s + 1), s0, s1, s2, P0, P1, P2,
                                                              bc(-a.kappa), us, rt);
             s_e[w][grp][s] = e.x;
             if (s + 1 < a.n_samples) s_e[w][grp][s + 1] = e.y;
@@ -360,7 +359,7 @@ __global__ void pp_episode_step_kernel(const PPArgs a, const EpisodeArgs e, uint
     float o[6];
     for (int q = 0; q < 3; ++q) {
         F2 rs, cq, sq;    // lane x only is used
-        bm_polar2<true, true>(R[q], R[q], A[q], A[q], a.rad_tab, rs, cq, sq);
+        bm_polar2<true>(R[q], R[q], A[q], A[q], a.rad_tab, rs, cq, sq);
         const float sr = __fmul_rn(sg[q], rs.x);
         o[2 * q] = __fmaf_rn(sr, cq.x, cur[2 * q]);
         o[2 * q + 1] = __fmaf_rn(sr, sq.x, cur[2 * q + 1]);

@@ -145,10 +145,12 @@ __device__ __forceinline__ F2 rsqrt2_from(F2 x, F2 mh) {
 // rad_spec on both lanes (spec/RNG.md §3): region r, v = r ? 2^24 - N : N, and
 // the row index 368 r + 16 e + j read straight off the bits of float(v) (exact:
 // its exponent field is 127 + e and its top four mantissa bits are j);
-// t = m - (1 + (2j + 1)/32) from the remaining mantissa bits (exact).
-template <bool SC>
+// t = m - (1 + (2j + 1)/32) from the remaining mantissa bits (exact).  Scalar
+// lanes: each lane's coefficients arrive as one LDS.128 in four consecutive
+// registers, and pairing them for FFMA2 costs a register move per operand
+// (measured: scalar is 3-5 % faster on every hot kernel, bit-identical).
 __device__ __forceinline__ F2 rad2(uint32_t Rx, uint32_t Ry, const float4* __restrict__ rt) {
-    using L = Ops<SC>;
+    using L = Ops<true>;
     const uint32_t nx = (Rx >> 8) | 1u, ny = (Ry >> 8) | 1u;
     const uint32_t hx = nx >> 23, hy = ny >> 23;
     const uint32_t vx = hx ? 0x1000000u - nx : nx, vy = hy ? 0x1000000u - ny : ny;
@@ -165,16 +167,16 @@ __device__ __forceinline__ F2 rad2(uint32_t Rx, uint32_t Ry, const float4* __res
 // Two Box-Muller pairs at once (lane x: (Rx, Ax), lane y: (Ry, Ay)); angle words
 // have their low 8 bits clear.  rs = +-rad (half-turn sign), (cq, sq) = the
 // half-turn sin/cos polynomials, so z = (rs cq, rs sq) per lane (spec/RNG.md
-// §2-§6).  SRS/SSC choose scalar lanes for the radius and sincos parts
-// (scheduling only; identical results).
+// §2-§6).  SSC chooses scalar lanes for the sincos part (scheduling only;
+// identical results); the radius is always scalar (rad2).
 // Angle given as (F, S): F holds the turn fraction bits of A >> 8 in MASK (bits 8..22
 // of A's bits 16..30 for 16-bit angles, 0..22 for 24-bit ones), S holds the half-turn
 // bit in bit 31.  The generic entry below derives them from an angle word A.
-template <bool SRS, bool SSC, uint32_t MASK>
+template <bool SSC, uint32_t MASK>
 __device__ __forceinline__ void bm_polar2_fs(uint32_t Rx, uint32_t Ry, uint32_t Fx, uint32_t Fy, uint32_t Sx,
                                              uint32_t Sy, const float4* __restrict__ rt, F2& rs, F2& cq, F2& sq) {
     using Q = Ops<SSC>;
-    const F2 rad = rad2<SRS>(Rx, Ry, rt);
+    const F2 rad = rad2(Rx, Ry, rt);
     // sincos_spec: r from the angle bits, half-turn sign applied to rad
     const F2 r = Q::add(make_float2(__uint_as_float((Fx & MASK) | 0x3F800000u),
                                     __uint_as_float((Fy & MASK) | 0x3F800000u)),
@@ -190,10 +192,10 @@ __device__ __forceinline__ void bm_polar2_fs(uint32_t Rx, uint32_t Ry, uint32_t 
 }
 
 // Generic: angle words A with their low 8 bits clear.
-template <bool SRS, bool SSC>
+template <bool SSC>
 __device__ __forceinline__ void bm_polar2(uint32_t Rx, uint32_t Ry, uint32_t Ax, uint32_t Ay,
                                           const float4* __restrict__ rt, F2& rs, F2& cq, F2& sq) {
-    bm_polar2_fs<SRS, SSC, 0x7FFFFFu>(Rx, Ry, Ax >> 8, Ay >> 8, Ax, Ay, rt, rs, cq, sq);
+    bm_polar2_fs<SSC, 0x7FFFFFu>(Rx, Ry, Ax >> 8, Ay >> 8, Ax, Ay, rt, rs, cq, sq);
 }
 
 // Sextet packing (spec/RNG.md §6) for entity e of a Philox block X: one byte permute
@@ -254,7 +256,7 @@ __device__ __forceinline__ void normal_sextet2_h(const PhiloxHoisted& rng, const
     for (int e = 0; e < 3; ++e) {
         const uint32_t wx = sextet_angle_word(X, e), wy = sextet_angle_word(Y, e);
         F2 rs, cq, sq;
-        bm_polar2_fs<false, false, 0x7FFF00u>(RX[e], RY[e], wx, wy, wx, wy, rt, rs, cq, sq);
+        bm_polar2_fs<false, 0x7FFF00u>(RX[e], RY[e], wx, wy, wx, wy, rt, rs, cq, sq);
         zc[e] = Ops<false>::mul(rs, cq);
         zs[e] = Ops<false>::mul(rs, sq);
     }
@@ -281,9 +283,9 @@ __device__ __forceinline__ void acc_normals_tail(const PhiloxHoisted& rng, const
     const uint4 X = rng(2 * j);
     const uint32_t w0 = sextet_angle_word(X, 0), w1 = sextet_angle_word(X, 1), w2 = sextet_angle_word(X, 2);
     F2 rs, cq, sq;
-    bm_polar2_fs<false, false, 0x7FFF00u>(X.x, X.y, w0, w1, w0, w1, rt, rs, cq, sq);
+    bm_polar2_fs<false, 0x7FFF00u>(X.x, X.y, w0, w1, w0, w1, rt, rs, cq, sq);
     const F2 zc01 = Ops<false>::mul(rs, cq), zs01 = Ops<false>::mul(rs, sq);
-    bm_polar2_fs<false, false, 0x7FFF00u>(X.z, X.z, w2, w2, w2, w2, rt, rs, cq, sq);
+    bm_polar2_fs<false, 0x7FFF00u>(X.z, X.z, w2, w2, w2, w2, rt, rs, cq, sq);
     const F2 zc2 = Ops<false>::mul(rs, cq), zs2 = Ops<false>::mul(rs, sq);
     g[0] = zc01.x; g[1] = zs01.x; g[2] = zc01.y; g[3] = zs01.y; g[4] = zc2.x; g[5] = zs2.x;
 #pragma unroll

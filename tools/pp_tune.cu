@@ -105,9 +105,9 @@ __device__ __forceinline__ F2 proto_errors(const uint4& X, const uint4& Y, float
     const uint32_t wx0 = sextet_angle_word(X, 0), wy0 = sextet_angle_word(Y, 0);
     const uint32_t wx1 = sextet_angle_word(X, 1), wy1 = sextet_angle_word(Y, 1);
     const uint32_t wx2 = sextet_angle_word(X, 2), wy2 = sextet_angle_word(Y, 2);
-    bm_polar2_fs<false, false, 0x7FFF00u>(X.x, Y.x, wx0, wy0, wx0, wy0, rt, r0, c0, n0);
-    bm_polar2_fs<false, false, 0x7FFF00u>(X.y, Y.y, wx1, wy1, wx1, wy1, rt, r1, c1, n1);
-    bm_polar2_fs<false, false, 0x7FFF00u>(X.z, Y.z, wx2, wy2, wx2, wy2, rt, r2, c2, n2);
+    bm_polar2_fs<false, 0x7FFF00u>(X.x, Y.x, wx0, wy0, wx0, wy0, rt, r0, c0, n0);
+    bm_polar2_fs<false, 0x7FFF00u>(X.y, Y.y, wx1, wy1, wx1, wy1, rt, r1, c1, n1);
+    bm_polar2_fs<false, 0x7FFF00u>(X.z, Y.z, wx2, wy2, wx2, wy2, rt, r2, c2, n2);
     const F2 q0 = O::mul(bc(s0), r0), q1 = O::mul(bc(s1), r1), q2 = O::mul(bc(s2), r2);
     const V2 o0 = {O::fma(q0, c0, P0.x), O::fma(q0, n0, P0.y)};
     const V2 o1 = {O::fma(q1, c1, P1.x), O::fma(q1, n1, P1.y)};
