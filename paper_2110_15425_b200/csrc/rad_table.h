@@ -1,9 +1,9 @@
 // rad_table.h — host-side construction of the Box-Muller radius table RT
 // (spec/RNG.md §3, revision R10c): 736 rows x 4 binary32 coefficients of the
 // cubic interpolating sqrt(-2 ln u1) at four dyadic nodes per segment, built
-// in binary64 in the spec's operation order.  The CPU oracle carries out the
-// same construction itself (oracle/distill_oracle.c, od_rt_build); the two
-// share no code.  Used by distill.cu (uploaded once per device) and tools/.
+// in binary64 in the spec's operation order.  The CPU checker carries out the
+// same construction with its own code; the two share none.  Used by
+// distill.cu (uploaded once per device) and tools/.
 #pragma once
 #include <cmath>
 #include <cuda_runtime.h>

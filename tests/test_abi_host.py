@@ -155,3 +155,22 @@ def test_ddm_grid_model_validation_without_gpu(abi):
         d = abi.ModelDesc(5, 2, abi._uptr(nl), abi._fptr(lev), abi._fptr(w), abi._fptr(params), params.size)
         h = C.c_void_p()
         assert L.distill_load_model(C.byref(d), 0, C.byref(h)) == want
+
+
+def test_round2_entry_validation_without_gpu(abi):
+    """Round-2 boundary additions reject bad arguments synchronously, before any
+    CUDA call: the signed key reset (NULL, misaligned), misaligned histogram
+    buffers of the DDM batch, and the binding's ABI-version guard."""
+    import ctypes as C
+    L = abi.lib()
+    assert L.distill_key_reset_signed(None, None) == abi.E_INVALID_ARG
+    assert L.distill_key_reset_signed(C.c_void_p(0x1003), None) == abi.E_INVALID_ARG
+    assert "misaligned" in L.distill_last_error().decode()
+    a = abi.DdmArgs(1.0, 1.0, 1.0, 0.0, 0.01, 10, 1, 4, -1.0, 1.0, 0, 10, 1,
+                    C.c_void_p(0x1004), C.c_void_p(0x2000), C.c_void_p(0x3000))
+    assert L.distill_ddm_batch(C.byref(a), None) == abi.E_INVALID_ARG
+    assert "aligned" in L.distill_last_error().decode()
+    assert abi.ABI_VERSION == L.distill_abi_version() == 2
+    assert abi.KEY_INIT_SIGNED == (1 << 63) - 1
+    # the eval-args struct carries key_order at the end (include/distill.h, ABI 2)
+    assert abi.EvalArgs._fields_[-1][0] == "key_order"
