@@ -191,7 +191,12 @@ distill_status distill_pp_amr_refine(const distill_model* model, const distill_a
 int            distill_abi_version(void);
 const char*    distill_last_error(void);
 
-/* Validate the description and copy its read-only block to `device`. */
+/* Validate the description and copy its read-only block to `device`.  The
+ * first load on a device (or the first DDM/LCI batch there) also uploads the
+ * library's Box-Muller radius table (spec/RNG.md §3, 11.8 KB, kept for the
+ * process lifetime); that one-time step is synchronous and must not happen
+ * inside a CUDA-graph capture (E_CUDA otherwise).  The caller's current device
+ * is restored before return (as by every entry point). */
 distill_status distill_load_model(const distill_model_desc* desc, int device, distill_model** out);
 /* NULL-safe.  The caller synchronises streams that use the model first. */
 void           distill_free_model(distill_model* model);
@@ -272,7 +277,10 @@ distill_status distill_stroop_energy(const distill_model* model, uint64_t alloc,
                                      uint32_t trial_begin, uint32_t trial_end, uint64_t seed,
                                      unsigned long long* d_esum, void* stream);
 
-/* DDM batch over trials [trial_begin, trial_end): histograms accumulated with atomics. */
+/* DDM batch over trials [trial_begin, trial_end): histograms accumulated with atomics.
+ * Runs on the caller's current device (the first call there uploads the radius
+ * table, see distill_load_model).  The three histogram buffers must be 8-byte
+ * aligned (E_INVALID_ARG otherwise). */
 distill_status distill_ddm_batch(const distill_ddm_args* args, void* stream);
 /* Leaky competing integrator batch (spec/MODELS.md §5): the same
  * arguments, outputs and RNG units as distill_ddm_batch with `drift` read as
