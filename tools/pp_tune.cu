@@ -245,6 +245,10 @@ int main() {
     run("layout: SMEM levels + float4 store", a, ref.data(), rk, false,
         [&] { pp_eval_layout_kernel<128, 7, true, true, true><<<grid, 128>>>(a); },
         regs_of(pp_eval_layout_kernel<128, 7, true, true, true>));
+#define MASKV(M, name) run(name, a, ref.data(), rk, false, [&] { pp_eval_grid_kernel<128, M, 7, false, true><<<grid, 128>>>(a); }, regs_of(pp_eval_grid_kernel<128, M, 7, false, true>))
+    MASKV(1, "scalar action+objective");
+    MASKV(32, "scalar sincos of entity 2");
+    MASKV(33, "scalar action+objective+sincos2");
 #define SHIP(B, N, name) run(name, a, ref.data(), rk, false, [&] { pp_eval_grid_kernel<B, 0, N, false, true><<<(a.count + B - 1) / B, B>>>(a); }, regs_of(pp_eval_grid_kernel<B, 0, N, false, true>))
     SHIP(128, 6, "b128 minb6");
     SHIP(128, 8, "b128 minb8");
