@@ -301,25 +301,35 @@ def run_ours(args):
     graph, graph_note = None, None
     launches_per_step = None
     if not args.no_graph and (world == 1 or args.dist_backend == "nccl"):
+        # warm-up on a side stream (every rank runs it: it contains the all-reduce)
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            step()
+        stream.wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        ok, err = 1, None
         try:
-            side = torch.cuda.Stream()
-            side.wait_stream(stream)
-            with torch.cuda.stream(side):
-                step()
-            stream.wait_stream(side)
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
             l0 = D.launch_count()
-            with torch.cuda.graph(g):
+            # thread-local capture: the NCCL watchdog thread keeps querying events meanwhile
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
                 step()
             launches_per_step = D.launch_count() - l0
+        except Exception as exc:     # fall back to eager steps, say so in the JSON line
+            ok, err = 0, repr(exc)[:160]
+        torch.cuda.synchronize()
+        if world > 1:                # all ranks replay the captured collective, or none does
+            agree = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(agree, op=dist.ReduceOp.MIN)
+            ok = int(agree.item())
+        if ok:
             g.replay()
             torch.cuda.synchronize()
             graph = g
             graph_note = "reset + kernel + all-reduce captured in one CUDA graph, replayed per step"
-        except Exception as exc:     # fall back to eager steps, say so in the JSON line
-            graph_note = f"eager steps (graph capture failed: {repr(exc)[:160]})"
-            torch.cuda.synchronize()
+        else:
+            graph_note = "eager steps (graph capture failed" + (f": {err})" if err else " on another rank)")
     else:
         graph_note = "eager steps (--no-graph or a non-NCCL backend)"
     barrier()
