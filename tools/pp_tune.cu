@@ -43,6 +43,34 @@ __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_persistent_kernel(co
     if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
 }
 
+// Persistent with per-WARP dynamic chunks of 32 allocations (no block barriers
+// inside the loop); the counter is zeroed by the caller before the launch.
+template <int BLOCK, int MINB, bool EVEN>
+__global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_warp_persistent_kernel(const PPArgs a,
+                                                                                    unsigned int* __restrict__ counter) {
+    __shared__ float4 s_rt[RT_ROWS];
+    stage_rad_table_async<BLOCK>(s_rt, a.rad_tab);
+    const float2 ustar = pp_ustar_block(a);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t n_chunks = (a.count + 31u) / 32u;
+    key64_t key = KEY_INIT;
+    for (;;) {
+        uint32_t c = 0;
+        if (lane == 0) c = atomicAdd(counter, 1u);
+        c = __shfl_sync(0xFFFFFFFFu, c, 0);
+        if (c >= n_chunks) break;
+        const uint32_t tid = c * 32u + lane;
+        if (tid < a.count) {
+            const uint32_t i = a.begin + tid;
+            const float C = pp_eval_alloc<0, false, EVEN>(a, i, ustar, s_rt);
+            a.net[tid] = -C;
+            const key64_t k = make_key(C, i);
+            key = k < key ? k : key;
+        }
+    }
+    if (a.best) block_min_key_atomic<BLOCK>(key, a.best);
+}
+
 // Layout A/B variant of pp_eval_grid_kernel (SMEM_LEV, STORE4).
 template <int BLOCK, int MINB, bool EVEN, bool SMEM_LEV, bool STORE4>
 __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_layout_kernel(const PPArgs a) {
@@ -264,6 +292,22 @@ int main() {
         run("persistent b128 minb7", a, ref.data(), rk, false,
             [&] { pp_eval_grid_persistent_kernel<128, 7, true><<<pg, 128>>>(a, g_counter); },
             regs_of(pp_eval_grid_persistent_kernel<128, 7, true>));
+        run("warp-persistent b128 minb7", a, ref.data(), rk, false,
+            [&] { pp_eval_grid_warp_persistent_kernel<128, 7, true><<<pg, 128>>>(a, g_counter); },
+            regs_of(pp_eval_grid_warp_persistent_kernel<128, 7, true>));
+        int per_sm2 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, pp_eval_grid_warp_persistent_kernel<256, 3, true>, 256, 0);
+        const unsigned pg2 = per_sm2 * n_sm;
+        run("warp-persistent b256 minb3", a, ref.data(), rk, false,
+            [&] { pp_eval_grid_warp_persistent_kernel<256, 3, true><<<pg2, 256>>>(a, g_counter); },
+            regs_of(pp_eval_grid_warp_persistent_kernel<256, 3, true>));
+        int per_sm3 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, pp_eval_grid_warp_persistent_kernel<448, 2, true>, 448, 0);
+        const unsigned pg3 = per_sm3 * n_sm;
+        run("warp-persistent b448 minb2", a, ref.data(), rk, false,
+            [&] { pp_eval_grid_warp_persistent_kernel<448, 2, true><<<pg3, 448>>>(a, g_counter); },
+            regs_of(pp_eval_grid_warp_persistent_kernel<448, 2, true>));
+        printf("resident blocks: b128 %d/SM, b256 %d/SM, b448 %d/SM\n", per_sm, per_sm2, per_sm3);
     }
     {   // prototype: rsqrt table (tolerance check instead of bit identity)
         std::vector<float4> t8;
