@@ -1,4 +1,6 @@
-"""DESIGN.md reading R21: is the fused objective step Delta = fma(d, y_d, -u*)
+"""Test infrastructure (it runs the CPU oracle, so it lives under tests/; not a
+pytest module — `test_r21_fused_objective_step_is_closer_to_binary64` is the
+pinned version).  DESIGN.md reading R21: is the fused objective step Delta = fma(d, y_d, -u*)
 closer to the plain binary64 definition than the unfused u_hat = d*y_d; Delta =
 u_hat - u* ?  (Test infrastructure: runs only the CPU oracle.)
 
@@ -8,7 +10,7 @@ allocations with both, and compares each against the binary64 re-evaluation
 od_pp_trace_f64 (same Philox bits, libm Box-Muller, exact 1/sqrt).  Prints the
 error statistics; `profiles/r02_r21_error.txt` holds the committed output.
 
-    python tools/r21_error.py [n_alloc]
+    python tests/r21_error.py [n_alloc]
 """
 import os
 import subprocess

@@ -339,7 +339,7 @@ def test_r21_fused_objective_step_is_closer_to_binary64(orc):
     to the binary64 plain definition (od_pp_trace_f64) than the unfused
     u_hat = d*y_d, Delta = u_hat - u* (two roundings).  A second oracle build
     that differs only in that step (-DOD_UNFUSED_OBJECTIVE) is compared sample by
-    sample on cfg3 inputs; tools/r21_error.py is the larger run
+    sample on cfg3 inputs; tests/r21_error.py is the larger run
     (profiles/r02_r21_error.txt)."""
     import os
     import subprocess
