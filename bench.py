@@ -370,6 +370,7 @@ def run_ours(args):
     clocks["sm_mhz_effective_probe"] = sm_clock_mhz(300)
     ms_step = max_over_ranks(statistics.median(step_ms))
     ms_kern = max_over_ranks(statistics.median(kern_ms))
+    ms_kern_mean = max_over_ranks(sum(kern_ms) / K)
     evals = cfg.n_alloc * cfg.n_samples
     value = evals / (ms_step / 1e3)
     key = key_from_tensor(best, signed=True)
@@ -454,6 +455,9 @@ def run_ours(args):
             "traffic": traffic, "traffic_source": "profiles/r02_pp_traffic.json (ncu --set full, cfg3)",
             "algorithmic_bytes_per_launch": count * 4 + 8 + sum(cfg.n_levels) * 4,
             "kernel": "pp_eval_grid_kernel", "kernel_ms": ms_kern,
+            "kernel_ms_mean": ms_kern_mean,
+            "kernel_timing": "CUDA events around the kernel alone on its launching stream, K eager steps right "
+                             "after the timed graph loop (same L2 flush); median (kernel_ms) and mean",
             "algorithmic_flops_per_launch": flops_launch,
             "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz (max clock; "
                           "MEASURED_PEAKS.json has no FP32 entry and the guide gives no FP32 fallback)",
