@@ -43,7 +43,7 @@ UNIT = "evals/s"
 # add/mul/sqrt/div = 1) + ~15 per allocation; a fixed, implementation-independent yardstick,
 # so the fraction moves only with evaluations/s.  Reported beside it: the counted method
 # flops (the oracle's counting build in method mode: sqrt = 1, rsqrt = sqrt + divide) and
-# the executed flops (the spec's Newton/Goldschmidt steps included) — tests/test_oracle_pp.py.
+# the executed flops (the spec's Newton steps included) — tests/test_oracle_pp.py.
 FLOPS_PER_SAMPLE = 210
 FLOPS_PER_ALLOC = 15
 FLOPS_PER_CALL = 0
