@@ -693,14 +693,17 @@ def run_extras(D, torch, dev, rank, world, args):
         net = torch.empty(max(1, se - sb), dtype=torch.float32, device=dev)
         best = torch.empty(1, dtype=torch.int64, device=dev)
         counts = torch.empty(3 * max(1, se - sb), dtype=torch.int64, device=dev)
-        D.key_reset(best)
-        e0.record()
-        D.eval_grid(m, None, c.n_trials, c.seed, sb, se, net=net, best=best, counts=counts)
-        if world > 1:
-            D.best_allreduce(best)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
+        passes = []
+        for _ in range(3):                      # median of 3 passes (~0.4 s each on one GPU)
+            D.key_reset(best)
+            e0.record()
+            D.eval_grid(m, None, c.n_trials, c.seed, sb, se, net=net, best=best, counts=counts)
+            if world > 1:
+                D.best_allreduce(best)
+            e1.record()
+            torch.cuda.synchronize()
+            passes.append(e0.elapsed_time(e1))
+        ms = statistics.median(passes)
         if world > 1:
             t = torch.tensor([ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -744,7 +747,7 @@ def run_extras(D, torch, dev, rank, world, args):
         out["stroop_energy_best"] = {"ms": e2.elapsed_time(e3), "allocation": idx, "trials": c.n_trials,
                                      "mean_energy_at_steps": {str(n): float(trace[n - 1])
                                                               for n in (1, 10, 50, 100, c.n_steps)}}
-        out["stroop_cfg4"] = {"evals_per_s": c.evals / (ms / 1e3),
+        out["stroop_cfg4"] = {"timing": "median of 3 passes", "evals_per_s": c.evals / (ms / 1e3),
                               "step_updates_per_s": c.evals * c.n_steps / (ms / 1e3), "ms": ms,
                               "algorithmic_tflops": tf, "frac_fp32_peak": tf / FP32_PEAK_NOMINAL,
                               "frac_fp32_peak_executed": tf_exec / FP32_PEAK_NOMINAL,
