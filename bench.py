@@ -676,11 +676,18 @@ def run_extras(D, torch, dev, rank, world, args):
             dms = float(t.item())
         from paper_2110_15425_b200.api import key_from_tensor
         dcost, didx = D.key_decode(key_from_tensor(dbest))
-        steps = int(gd.params[6])
+        N = int(gd.params[6])
+        dc = dcounts.reshape(-1, 3)[:de - db]
+        steps_t = torch.stack([dc[:, 2].sum(), dc[:, 1].sum() * N]).sum().reshape(1)
+        if world > 1:
+            dist.all_reduce(steps_t, op=dist.ReduceOp.SUM)
+        steps = int(steps_t.item())             # trial-steps up to each first passage (R14b)
         out["ddm_grid"] = {"workload": gd.name, "ms": dms, "evals_per_s": gd.evals / (dms / 1e3),
-                           "steps_per_s": gd.evals * steps / (dms / 1e3),
-                           "frac_fp32_peak": DDM_FLOPS_PER_STEP * gd.evals * steps / (dms / 1e3) / 1e12
-                           / FP32_PEAK_NOMINAL,
+                           "trial_steps_to_passage": steps, "trial_steps_fixed_trip": gd.evals * N,
+                           "steps_per_s": steps / (dms / 1e3),
+                           "frac_fp32_peak": DDM_FLOPS_PER_STEP * steps / (dms / 1e3) / 1e12 / FP32_PEAK_NOMINAL,
+                           "note": "trials end at their first passage (DESIGN R14b); rates count the steps up "
+                                   "to each passage (+ N for undecided trials)",
                            "best": {"index": didx, "attention": float(gd.levels[didx // gd.n_levels[1]]),
                                     "threshold": float(gd.levels[gd.n_levels[0] + didx % gd.n_levels[1]]),
                                     "net_value": -dcost}}
@@ -710,8 +717,15 @@ def run_extras(D, torch, dev, rank, world, args):
             ms = float(t.item())
         from paper_2110_15425_b200.api import key_from_tensor
         cost, idx = D.key_decode(key_from_tensor(best))
-        tf = STROOP_FLOPS_PER_STEP * c.evals * c.n_steps / (ms / 1e3) / 1e12
-        tf_exec = STROOP_FLOPS_PER_STEP_EXEC * c.evals * c.n_steps / (ms / 1e3) / 1e12
+        # trials stop at their response (R14b): the steps that enter the result are the
+        # response times plus N for every undecided trial (exact integer sums)
+        cnt = counts.reshape(-1, 3)[:se - sb]
+        steps = torch.stack([cnt[:, 2].sum(), cnt[:, 1].sum() * c.n_steps]).sum().reshape(1)
+        if world > 1:
+            dist.all_reduce(steps, op=dist.ReduceOp.SUM)
+        steps = int(steps.item())
+        tf = STROOP_FLOPS_PER_STEP * steps / (ms / 1e3) / 1e12
+        tf_exec = STROOP_FLOPS_PER_STEP_EXEC * steps / (ms / 1e3) / 1e12
         # NEXT-3: Extended Stroop A on the cfg4 control grid, 1e4 trials per allocation
         g = W.ext_stroop_grid()
         mx = D.load_model(W.KIND_EXT_STROOP_A, g.n_levels, g.levels, g.w, g.params, device=dev.index)
@@ -734,8 +748,14 @@ def run_extras(D, torch, dev, rank, world, args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             xms = float(t.item())
         xsteps = int(g.params[3]) + int(g.params[10])
+        xc = xcounts.reshape(-1, 3)[:xe - xb]
+        xst = torch.stack([xc[:, 2].sum(), xc[:, 1].sum() * int(g.params[10])]).sum().reshape(1)
+        if world > 1:
+            dist.all_reduce(xst, op=dist.ReduceOp.SUM)
         out["ext_stroop_a"] = {"workload": g.name, "evals_per_s": g.evals / (xms / 1e3), "ms": xms,
-                               "trial_steps": xsteps, "best_index": key_from_tensor(xbest) & 0xFFFFFFFF}
+                               "trial_steps_max": xsteps, "ddm_steps_to_both_passages": int(xst.item()),
+                               "best_index": key_from_tensor(xbest) & 0xFFFFFFFF,
+                               "note": "trials end when both DDMs have passed (DESIGN R14b)"}
         # decision energy over time of the chosen allocation, all 1e5 trials
         en = torch.zeros(c.n_steps, dtype=torch.int64, device=dev)
         e2.record()
@@ -748,7 +768,11 @@ def run_extras(D, torch, dev, rank, world, args):
                                      "mean_energy_at_steps": {str(n): float(trace[n - 1])
                                                               for n in (1, 10, 50, 100, c.n_steps)}}
         out["stroop_cfg4"] = {"timing": "median of 3 passes", "evals_per_s": c.evals / (ms / 1e3),
-                              "step_updates_per_s": c.evals * c.n_steps / (ms / 1e3), "ms": ms,
+                              "trial_steps_to_response": steps,
+                              "trial_steps_fixed_trip": c.evals * c.n_steps,
+                              "step_updates_per_s": steps / (ms / 1e3), "ms": ms,
+                              "note": "trials end at their response (DESIGN R14b); flops and step rates count the "
+                                      "steps up to each response (+ N for undecided trials), not the fixed trip",
                               "algorithmic_tflops": tf, "frac_fp32_peak": tf / FP32_PEAK_NOMINAL,
                               "frac_fp32_peak_executed": tf_exec / FP32_PEAK_NOMINAL,
                               "flops_per_step": STROOP_FLOPS_PER_STEP,

@@ -9,6 +9,7 @@
 // blocks are few and the flush is amortised over many trials).
 #pragma once
 #include "rng.cuh"
+#include "trials.cuh"
 
 namespace distill {
 
@@ -131,9 +132,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
 // ---------------------------------------------------------------- DDM control grid
 // spec/MODELS.md §6c (north star: every control allocation runs a DDM): grid
 // (trial chunks, allocations) like the Stroop kernel; per allocation the
-// drift A = fma(g_a, u0, A0) and threshold z = u1; one thread = one trial of
-// N fixed-trip steps, 12 steps per pair of sextet blocks with the max-|x|
-// latch test of the batch kernel; integer outcomes {n_correct (upper),
+// drift A = fma(g_a, u0, A0) and threshold z = u1; a lane runs a trial until
+// its first passage (at most N steps; R14b: the outputs are the boundary and
+// the step), 12 steps per pair of sextet blocks with the max-|x| latch test of
+// the batch kernel, then takes the next trial of its block; integer outcomes {n_correct (upper),
 // n_undecided, rt_sum} block-reduced and added per allocation.  The value is
 // stroop_finalize_kernel's binary64 formula (same counts, same cost form).
 struct DdmgArgs {
@@ -147,7 +149,10 @@ struct DdmgArgs {
 template <int BLOCK, int MINB = 0>
 __global__ void __launch_bounds__(BLOCK, MINB) ddmg_sim_kernel(const DdmgArgs a, uint32_t alloc_off) {
     __shared__ float4 s_rt[RT_ROWS];
-    stage_rad_table<BLOCK>(s_rt, a.rad_tab);
+    __shared__ uint32_t s_next;
+    uint32_t t_end;
+    block_trial_range(a.trial_begin, a.trial_end, s_next, t_end);
+    stage_rad_table<BLOCK>(s_rt, a.rad_tab);                  // (its barrier publishes s_next)
     const uint32_t t_alloc = alloc_off + blockIdx.y;
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
@@ -155,37 +160,42 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddmg_sim_kernel(const DdmgArgs a,
     const float A = __fmaf_rn(a.g_a, u0, a.A0);
     const float z = u1, nz = -u1;
     const float nsd = __fmul_rn(a.noise, __fsqrt_rn(a.dt));
+    const uint32_t n12 = a.n_steps / 12, rem = a.n_steps - 12 * n12;
     uint32_t n_corr = 0, n_und = 0;
     unsigned long long rts = 0;
-    for (uint32_t j = a.trial_begin + blockIdx.x * BLOCK + threadIdx.x; j < a.trial_end; j += gridDim.x * BLOCK) {
-        const uint64_t unit = (uint64_t)i * a.n_trials + j;
-        PhiloxHoisted rng;
+    // trials stream until their first passage (R14b, trials.cuh)
+    uint32_t j = next_trial(s_next, t_end);
+    uint32_t st = 0, ch = 2, grp = 0;                             // ch: 0 correct (upper), 1 error, 2 none
+    float x = 0.0f;
+    PhiloxHoisted rng;
+    auto start = [&](uint32_t jj) {
+        const uint64_t unit = (uint64_t)i * a.n_trials + jj;
         rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
-        float x = 0.0f;
-        uint32_t st = 0, ch = 2;                                  // ch: 0 correct (upper), 1 error, 2 none
-        const uint32_t n12 = a.n_steps / 12;
-        for (uint32_t grp = 0; grp < n12; ++grp) {
+        x = 0.0f; st = 0; ch = 2; grp = 0;
+    };
+    if (j < t_end) start(j);
+    while (j < t_end) {
+        if (grp < n12) {
             float g[12], xs[12];
             acc_normals12(rng, s_rt, grp, g);
 #pragma unroll
             for (int l = 0; l < 12; ++l) { x = __fmaf_rn(nsd, g[l], __fmaf_rn(a.dt, A, x)); xs[l] = x; }
-            if (st == 0) {
-                float mx = fabsf(xs[0]);
+            float mx = fabsf(xs[0]);
 #pragma unroll
-                for (int l = 1; l < 12; ++l) mx = fmaxf(mx, fabsf(xs[l]));
-                if (mx >= z) {
+            for (int l = 1; l < 12; ++l) mx = fmaxf(mx, fabsf(xs[l]));
+            if (mx >= z) {
 #pragma unroll
-                    for (int l = 0; l < 12; ++l) {
-                        if (st == 0) {
-                            if (xs[l] >= z) { st = 12 * grp + l + 1; ch = 0; }
-                            else if (xs[l] <= nz) { st = 12 * grp + l + 1; ch = 1; }
-                        }
+                for (int l = 0; l < 12; ++l) {
+                    if (st == 0) {
+                        if (xs[l] >= z) { st = 12 * grp + l + 1; ch = 0; }
+                        else if (xs[l] <= nz) { st = 12 * grp + l + 1; ch = 1; }
                     }
                 }
             }
+            ++grp;
+            if (st == 0 && grp < n12) continue;          // the trial goes on (the hot path)
         }
-        const uint32_t rem = a.n_steps - 12 * n12;
-        if (rem) {
+        if (st == 0 && rem) {                            // undecided through the last full group
             float g[12];
             acc_normals_tail(rng, s_rt, n12, rem, g);
 #pragma unroll
@@ -201,6 +211,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddmg_sim_kernel(const DdmgArgs a,
         }
         if (ch == 2) ++n_und;
         else { n_corr += (ch == 0); rts += st; }
+        j = next_trial(s_next, t_end);
+        if (j < t_end) start(j);
     }
     __shared__ unsigned long long s_red[3][BLOCK / 32];
 #pragma unroll

@@ -10,6 +10,7 @@
 #pragma once
 #include "keys.cuh"
 #include "rng.cuh"
+#include "trials.cuh"
 
 namespace distill {
 
@@ -61,7 +62,10 @@ template <int BLOCK, int MINB = 0, bool TABLE = true>
 __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArgs a, uint32_t alloc_off) {
     extern __shared__ float s_htab[];                         // TABLE: [4][n_steps]
     __shared__ float4 s_rt[RT_ROWS];
-    stage_rad_table<BLOCK>(s_rt, a.rad_tab);
+    __shared__ uint32_t s_next;                               // next trial of this block's range
+    uint32_t t_end;
+    block_trial_range(a.trial_begin, a.trial_end, s_next, t_end);
+    stage_rad_table<BLOCK>(s_rt, a.rad_tab);                  // (its barrier publishes s_next)
     const uint32_t t_alloc = alloc_off + blockIdx.y;           // index within [0, count)
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
@@ -83,13 +87,24 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
         __syncthreads();
     }
 
+    // Trials run until their response latches (R14b): the outputs are the
+    // response and its step, so the steps after the latch are never computed.
+    // Each lane streams trials from a per-block counter (contiguous block range,
+    // integer sums are order-free), so a lane whose trial ends early starts the
+    // next one instead of idling until the warp's slowest trial is done.
     uint32_t n_corr = 0, n_und = 0;
     unsigned long long rts = 0;
-    for (uint32_t j = a.trial_begin + blockIdx.x * BLOCK + threadIdx.x; j < a.trial_end;
-         j += gridDim.x * BLOCK) {
-        const uint32_t kind = j % 3, colour = (j / 3) & 1;
+    const uint32_t n6 = N / 6, rem = N - 6 * n6;
+    uint32_t j = next_trial(s_next, t_end);
+    uint32_t colour = 0, grp = 0, st = 0;
+    int resp = -1;
+    float x0 = 0.f, x1 = 0.f;
+    Pathway<TABLE> pw;
+    PhiloxHoisted rng;
+    auto start = [&](uint32_t jj) {
+        const uint32_t kind = jj % 3;
+        colour = (jj / 3) & 1;
         const int word = (kind == 0) ? (int)colour : (kind == 1) ? (int)(1 - colour) : -1;
-        Pathway<TABLE> pw;
         if (TABLE) {
             pw.row0 = s_htab + N * ((colour == 0 ? 1u : 0u) + (word == 0 ? 2u : 0u));
             pw.row1 = s_htab + N * ((colour == 1 ? 1u : 0u) + (word == 1 ? 2u : 0u));
@@ -98,18 +113,17 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
             pw.I1 = __fadd_rn(colour == 1 ? ic : 0.0f, word == 1 ? iw : 0.0f);
             pw.tau = a.tau; pw.h0 = 0.0f; pw.h1 = 0.0f;
         }
-        const uint64_t unit = (uint64_t)i * a.n_trials + j;
-        PhiloxHoisted rng;
+        const uint64_t unit = (uint64_t)i * a.n_trials + jj;
         rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
-        float x0 = 0.f, x1 = 0.f;
-        int resp = -1;
-        uint32_t st = 0;
-        // Six steps (12 normals, two sextet blocks) per group.  x_k >= 0 after
-        // the rectification (fmaxf(NaN, 0) = 0 as well), so "x0 >= θ or x1 >= θ"
-        // at any step of the group <=> the max of its 12 states >= θ: one test
-        // per group; the rare group that passes is resolved in the spec's order.
-        const uint32_t n6 = N / 6;
-        for (uint32_t grp = 0; grp < n6; ++grp) {
+        x0 = 0.f; x1 = 0.f; resp = -1; st = 0; grp = 0;
+    };
+    if (j < t_end) start(j);
+    while (j < t_end) {
+        if (grp < n6) {
+            // Six steps (12 normals, two sextet blocks) per group.  x_k >= 0 after
+            // the rectification (fmaxf(NaN, 0) = 0 as well), so "x0 >= θ or x1 >= θ"
+            // at any step of the group <=> the max of its 12 states >= θ: one test
+            // per group; the rare group that passes is resolved in the spec's order.
             float g[12], s0[6], s1[6];
             acc_normals12(rng, s_rt, grp, g);
 #pragma unroll
@@ -119,23 +133,22 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
                 lca_update(a, nleak, ninh, nsd, g[2 * l], g[2 * l + 1], h0, h1, x0, x1);
                 s0[l] = x0; s1[l] = x1;
             }
-            if (resp < 0) {
-                float m = fmaxf(s0[0], s1[0]);
+            float m = fmaxf(s0[0], s1[0]);
 #pragma unroll
-                for (int l = 1; l < 6; ++l) m = fmaxf(m, fmaxf(s0[l], s1[l]));
-                if (m >= a.thr) {
+            for (int l = 1; l < 6; ++l) m = fmaxf(m, fmaxf(s0[l], s1[l]));
+            if (m >= a.thr) {
 #pragma unroll
-                    for (int l = 0; l < 6; ++l) {
-                        if (resp < 0) {
-                            if (s0[l] >= a.thr) { resp = 0; st = 6 * grp + l + 1; }
-                            else if (s1[l] >= a.thr) { resp = 1; st = 6 * grp + l + 1; }
-                        }
+                for (int l = 0; l < 6; ++l) {
+                    if (resp < 0) {
+                        if (s0[l] >= a.thr) { resp = 0; st = 6 * grp + l + 1; }
+                        else if (s1[l] >= a.thr) { resp = 1; st = 6 * grp + l + 1; }
                     }
                 }
             }
+            ++grp;
+            if (resp < 0 && grp < n6) continue;          // the trial goes on (the hot path)
         }
-        const uint32_t rem = N - 6 * n6;
-        if (rem) {  // ragged last group
+        if (resp < 0 && rem) {  // undecided through the last full group: the ragged last steps
             float g[12];
             acc_normals_tail(rng, s_rt, n6, 2 * rem, g);
 #pragma unroll
@@ -153,6 +166,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
         }
         if (resp < 0) ++n_und;
         else { n_corr += ((uint32_t)resp == colour); rts += st; }
+        j = next_trial(s_next, t_end);
+        if (j < t_end) start(j);
     }
     // block reduction of the three integer outcomes
     __shared__ unsigned long long s_red[3][BLOCK / 32];
@@ -282,7 +297,10 @@ __device__ __forceinline__ void ddm_latch(float x, float z, uint32_t n, int& hit
 template <int BLOCK, int VARIANT>
 __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopArgs a, uint32_t alloc_off) {
     __shared__ float4 s_rt[RT_ROWS];
-    stage_rad_table<BLOCK>(s_rt, a.rad_tab);
+    __shared__ uint32_t s_next;
+    uint32_t t_end;
+    block_trial_range(a.trial_begin, a.trial_end, s_next, t_end);
+    stage_rad_table<BLOCK>(s_rt, a.rad_tab);                  // (its barrier publishes s_next)
     const uint32_t t_alloc = alloc_off + blockIdx.y;
     const uint32_t i = a.begin + t_alloc;
     const uint32_t k1 = i % a.L1, k0 = i / a.L1;
@@ -320,19 +338,26 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
     __syncthreads();
     uint32_t n_both = 0, n_und = 0;
     unsigned long long rts = 0;
-    for (uint32_t j = a.trial_begin + blockIdx.x * BLOCK + threadIdx.x; j < a.trial_end; j += gridDim.x * BLOCK) {
-        const uint32_t kind = j % 3, colour = (j / 3) & 1;
-        const float A1 = s_drift[2 * kind + colour][0], A2 = s_drift[2 * kind + colour][1];
-        const uint64_t unit = (uint64_t)i * a.n_trials + j;
-        PhiloxHoisted rng;
+    // Trials stream until both DDMs have latched (R14b, trials.cuh): the outputs
+    // are the two first passages, so no step after the later one is computed.
+    const uint32_t n6 = a.n_d / 6, rem = a.n_d - 6 * n6;
+    uint32_t j = next_trial(s_next, t_end);
+    float A1 = 0.f, A2 = 0.f, x1 = 0.f, x2 = 0.f;
+    int h1t = 0, h2t = 0;
+    uint32_t s1 = 0, s2 = 0, grp = 0;
+    PhiloxHoisted rng;
+    auto start = [&](uint32_t jj) {
+        const uint32_t kind = jj % 3, colour = (jj / 3) & 1;
+        A1 = s_drift[2 * kind + colour][0]; A2 = s_drift[2 * kind + colour][1];
+        const uint64_t unit = (uint64_t)i * a.n_trials + jj;
         rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
-        float x1 = 0.0f, x2 = 0.0f;
-        int h1t = 0, h2t = 0;
-        uint32_t s1 = 0, s2 = 0;
-        // Six steps (12 normals) per group; each DDM's latch is tested once per
-        // group on max |x| (|x| >= z <=> x >= z or x <= -z, DDM kernel).
-        const uint32_t n6 = a.n_d / 6;
-        for (uint32_t grp = 0; grp < n6; ++grp) {
+        x1 = 0.f; x2 = 0.f; h1t = 0; h2t = 0; s1 = 0; s2 = 0; grp = 0;
+    };
+    if (j < t_end) start(j);
+    while (j < t_end) {
+        if (grp < n6) {
+            // Six steps (12 normals) per group; each DDM's latch is tested once per
+            // group on max |x| (|x| >= z <=> x >= z or x <= -z, DDM kernel).
             float g[12], y1[6], y2[6];
             acc_normals12(rng, s_rt, grp, g);
 #pragma unroll
@@ -357,9 +382,10 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
 #pragma unroll
                 for (int l = 0; l < 6; ++l) ddm_latch(y2[l], a.z, 6 * grp + l + 1, h2t, s2);
             }
+            ++grp;
+            if (!(h1t && h2t) && grp < n6) continue;     // the trial goes on (the hot path)
         }
-        const uint32_t rem = a.n_d - 6 * n6;
-        if (rem) {  // ragged last group
+        if (!(h1t && h2t) && rem) {  // a DDM still open after the last full group: the ragged steps
             float g[12];
             acc_normals_tail(rng, s_rt, n6, 2 * rem, g);
 #pragma unroll
@@ -372,9 +398,10 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
                 }
             }
         }
-        if (h1t == 0 || h2t == 0) { ++n_und; continue; }
-        n_both += (h1t == 1 && h2t == 1);
-        rts += s1 > s2 ? s1 : s2;
+        if (h1t == 0 || h2t == 0) ++n_und;
+        else { n_both += (h1t == 1 && h2t == 1); rts += s1 > s2 ? s1 : s2; }
+        j = next_trial(s_next, t_end);
+        if (j < t_end) start(j);
     }
     __shared__ unsigned long long s_red[3][BLOCK / 32];
 #pragma unroll

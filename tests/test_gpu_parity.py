@@ -1197,3 +1197,61 @@ def test_signed_key_order(D, orc):
     assert D.key_from_tensor(best, signed=True) >> 32 == 0xFFFFFFFF
     with pytest.raises(D.api.DistillError):
         D.key_decode(D.key_from_tensor(best, signed=True))
+
+
+@pytest.mark.parametrize("model", ["stroop", "ext_a", "ext_b", "ddmg"])
+@pytest.mark.parametrize("case", ["latch_at_step_1", "never_latch", "short_trip", "ragged_trial_range"])
+def test_trial_streaming_edges_bit_exact(D, orc, model, case):
+    """Trial streaming (DESIGN R14b: a trial ends at its response; lanes take the
+    next trial of their block) against the fixed-trip oracle: every trial
+    latching at step 1, none latching (all N steps), N below one group (tail
+    only), and a trial sub-range too small to give every block and lane a trial
+    — counts bit-exact (and V / key for full ranges)."""
+    if model == "stroop":
+        c, kind = W.stroop_small(), W.KIND_STROOP_LCA
+        thr_i, n_i = 7, 10
+    elif model == "ddmg":
+        c, kind = W.ddmg_grid(6, 257), W.KIND_DDM_GRID
+        thr_i, n_i = None, 6
+    else:
+        c, kind = W.ext_stroop_small(), (W.KIND_EXT_STROOP_A if model == "ext_a" else W.KIND_EXT_STROOP_B)
+        thr_i, n_i = 9, 10
+    c.params = c.params.copy()
+    c.levels = c.levels.copy()
+    rng_ = (0, 0)
+    if case == "latch_at_step_1":                             # threshold 0: the first step passes
+        if thr_i is None:
+            c.levels[c.n_levels[0]:] = 0.0
+        else:
+            c.params[thr_i] = 0.0
+    elif case == "never_latch":
+        if thr_i is None:
+            c.levels[c.n_levels[0]:] = 1e6
+        else:
+            c.params[thr_i] = 1e6
+    elif case == "short_trip":
+        c.params[n_i] = 4 if model != "ddmg" else 7
+    else:
+        if model.startswith("ext"):
+            pytest.skip("the Ext-Stroop oracle entry evaluates whole trial ranges only")
+        rng_ = (5, 9)
+    m = D.load_model(kind, c.n_levels, c.levels, c.w, c.params, device=0)
+    cnt, net, key = _stroop_gpu(D, m, c, 0, c.n_alloc, trial_range=rng_)
+    tb, te = rng_ if rng_ != (0, 0) else (0, c.n_trials)
+    if model == "stroop":
+        wc, wn = orc.stroop_eval(c.n_levels, c.levels, c.w, c.params, 0, c.n_alloc, c.n_trials, c.seed, tb, te,
+                                 threads=8)
+    elif model == "ddmg":
+        wc, wn = orc.ddmg_eval(c.n_levels, c.levels, c.w, c.params, 0, c.n_alloc, c.n_trials, c.seed, tb, te,
+                               threads=8)
+    else:
+        wc, wn = orc.ext_stroop_eval(0 if model == "ext_a" else 1, c.n_levels, c.levels, c.w, c.params, 0,
+                                     c.n_alloc, c.n_trials, c.seed, threads=8)
+    assert np.array_equal(cnt, wc)
+    if rng_ == (0, 0):
+        assert np.array_equal(_bits(net), _bits(wn))
+        assert key == orc.argmax_net(wn)[0]
+    if case == "latch_at_step_1":
+        assert cnt[:, 1].sum() == 0 and (cnt[:, 2] == (te - tb)).all()   # every trial decides at step 1
+    if case == "never_latch":
+        assert (cnt[:, 1] == (te - tb)).all()
