@@ -1,6 +1,6 @@
 """Small driver for ncu captures of the DDM and Stroop kernels (tools only).
 
-    python tools/profile_extras.py [--pp]      # cfg2 DDM batch + 100-allocation slices of cfg4 and the Ext Stroop grid
+    python tools/profile_extras.py [--pp]      # cfg2 DDM batch + 100-allocation slices of cfg4 (around its optimum) and the Ext Stroop grid
 """
 import os
 import sys
@@ -34,8 +34,8 @@ def main():
     net = torch.empty(n, device="cuda")
     best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
     counts = torch.empty(3 * n, dtype=torch.int64, device="cuda")
-    for _ in range(2):
-        D.eval_grid(m, None, c.n_trials, c.seed, 0, n, net=net, best=best, counts=counts)
+    for _ in range(2):       # a slice around the cfg4 optimum (allocation 8083): representative response times
+        D.eval_grid(m, None, c.n_trials, c.seed, 8000, 8000 + n, net=net, best=best, counts=counts)
     g = W.ext_stroop_grid()
     mx = D.load_model(W.KIND_EXT_STROOP_A, g.n_levels, g.levels, g.w, g.params, device=0)
     for _ in range(2):
