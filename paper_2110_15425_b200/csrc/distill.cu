@@ -122,7 +122,7 @@ constexpr uint32_t PP_SMALL_SMAX8 = 256;   // per-allocation buffer with 8 lanes
 constexpr uint64_t PP_SMALL8_THREADS_PER_SM = DISTILL_PP_SMALL8_THREADS_PER_SM;
 constexpr uint32_t PP_SMALL_SMAX4 = 128;   // per-allocation buffer with 4 lanes per allocation
 #ifndef DISTILL_PP_SMALL4_THREADS_PER_SM
-#define DISTILL_PP_SMALL4_THREADS_PER_SM 1024   // 4 lanes per allocation up to 256 allocations per SM
+#define DISTILL_PP_SMALL4_THREADS_PER_SM 768    // 4 lanes per allocation up to 192 allocations per SM (r02_small_threshold.txt)
 #endif
 constexpr uint64_t PP_SMALL4_THREADS_PER_SM = DISTILL_PP_SMALL4_THREADS_PER_SM;
 constexpr int DDM_BLOCK = 128;
