@@ -361,3 +361,49 @@ def test_r21_fused_objective_step_is_closer_to_binary64(orc):
     closer, farther = np.mean(rf < ru), np.mean(rf > ru)
     assert closer > farther + 0.01, (closer, farther)
     assert np.median(rf) < np.median(ru)                    # (the mean is set by a few ill-conditioned samples)
+
+
+def _objective_expectation_2d(noisy, sig, kap, P, h=0.004, span=6.0):
+    """E[|unit(action(o)) - u*|^2] with entity `noisy` observed as p + sig z,
+    z ~ N(0, I), by a midpoint sum over z in [-span, span]^2 (binary64; the
+    integrand is bounded, the Gaussian weight beyond 6 sigma is < 1e-7)."""
+    P = np.asarray(P, np.float64).reshape(3, 2)
+
+    def unit(v):
+        return v / np.linalg.norm(v, axis=-1, keepdims=True)
+
+    def action(o0, o1, o2):
+        return unit(o0 - o2) - kap * unit(o1 - o2)
+
+    us = unit(action(P[0], P[1], P[2]))
+    g = np.arange(-span + h / 2, span, h)
+    zx, zy = np.meshgrid(g, g, indexing="ij")
+    z = np.stack([zx.ravel(), zy.ravel()], axis=1)
+    w = np.exp(-0.5 * (z ** 2).sum(1)) * h * h / (2 * math.pi)
+    o = [np.broadcast_to(P[e], z.shape) for e in range(3)]
+    o[noisy] = P[noisy] + sig * z
+    u = unit(action(*o))
+    e = ((u - us) ** 2).sum(1)
+    return float((w * e).sum() / w.sum())
+
+
+def test_noisy_player_objective_matches_2d_integral(orc):
+    """Pin of the third Box-Muller pair of the sextet (the player's observation,
+    angle packed from the low bytes of X0 and X1, spec/RNG.md §6) and of both
+    Action terms at once: prey and predator noise-free, the player observed with
+    std sigma, so v_p and v_d share the same noise.  The oracle's mean objective
+    over 64 x 10^4 samples must match the binary64 2-D integral over the
+    player's Gaussian within 4 SE + 1 %; the same noise applied to the prey or to
+    the predator instead (a swapped entity in the sextet) is rejected."""
+    sig, kap = 1.0, 0.5
+    P = [4.0, 0.0, -3.0, 2.0, 0.0, 0.0]
+    L = 64
+    levels = np.array([1.0, 1.0] + [0.0] * L, np.float32)      # prey level 1, predator level 1, player level 0
+    C = orc.pp_eval((1, 1, L), levels, np.zeros(3, np.float32), np.array([sig, 0.0, kap], np.float32),
+                    np.array(P, np.float32), 0, L, 10000, 23).astype(np.float64)
+    se = C.std() / math.sqrt(L)
+    want = _objective_expectation_2d(2, sig, kap, P)
+    assert abs(C.mean() - want) <= 4 * se + 0.01 * want, (C.mean(), want, se)
+    for wrong in (0, 1):
+        other = _objective_expectation_2d(wrong, sig, kap, P)
+        assert abs(C.mean() - other) > 20 * se + 0.01 * want, (wrong, C.mean(), other)
