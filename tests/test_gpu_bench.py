@@ -39,8 +39,16 @@ def test_bench_json_contract_on_gpu():
     assert 0 < e["value"] <= d["value"] * 1.05
     assert d["gpu_launches"] == d["steps"]                 # one fused kernel per step
     assert d["clocks"]["sm_max_mhz"] > 0
-    # the best allocation of the timed grid search decodes inside the grid
+    # the best allocation of the timed grid search decodes inside the grid, and the
+    # key of the graph-captured, signed-order step IS the oracle's cfg3 key
     assert 0 <= d["result"]["best_index"] < d["config"]["allocations"]
+    sys.path.insert(0, ROOT)
+    import oracle
+    import workloads as W
+    c = W.pp_cfg3()
+    full = oracle.pp_eval_threads(c.n_levels, c.levels, c.w, c.params, c.inputs, 0, c.n_alloc, c.n_samples, c.seed,
+                                  threads=os.cpu_count() or 8)
+    assert d["result"]["key"] == f"{oracle.argmax_net(-full)[0]:016x}"
 
 
 def test_bench_self_spawns_ranks_and_reproduces_the_single_gpu_key():
