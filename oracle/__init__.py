@@ -96,6 +96,8 @@ def _bind(path: str) -> C.CDLL:
         "od_pp_amr": (C.c_int, [_u32p, _f32p, _f32p, _f32p, _f32p, _f32p, u32, u32, u64, u32, _u64p, _f32p]),
         "od_ext_stroop_eval": (C.c_int, [C.c_int, _u32p, _f32p, _f32p, _f32p, u64, u64, u32, u64,
                                          C.c_void_p, C.c_void_p]),
+        "od_ext_stroop_eval_range": (C.c_int, [C.c_int, _u32p, _f32p, _f32p, _f32p, u64, u64, u32, u32, u32, u64,
+                                               C.c_void_p, C.c_void_p]),
         "od_ext_stroop_trial_a": (None, [_f32p, f32, f32, u64, u64, u32, np.ctypeslib.ndpointer(np.int32, flags="C"),
                                          _u32p]),
         "od_ext_stroop_trial_b": (None, [_f32p, f32, f32, u64, u64, u32, np.ctypeslib.ndpointer(np.int32, flags="C"),
@@ -501,10 +503,15 @@ def stroop_value(params, w, u_c, u_s, n_trials, n_correct, n_undecided, rt_sum):
 
 # ---------------------------------------------------------------- Extended Stroop A/B
 
-def ext_stroop_eval(variant, n_levels, levels, w, params, begin, end, n_trials, seed, threads=1):
-    """variant 0 = A, 1 = B (spec/MODELS.md §10): (counts[n,3] uint64, net[n] float32)."""
+def ext_stroop_eval(variant, n_levels, levels, w, params, begin, end, n_trials, seed, threads=1,
+                    trial_begin=0, trial_end=None):
+    """variant 0 = A, 1 = B (spec/MODELS.md §10): (counts[n,3] uint64, net[n] float32 or None for a
+    trial sub-range)."""
+    if trial_end is None:
+        trial_end = n_trials
     n = int(end) - int(begin)
     counts = np.zeros((n, 3), np.uint64)
+    full = (trial_begin == 0 and trial_end == n_trials)
     net = np.zeros(n, np.float32)
     args = (_u32(n_levels), _f32(levels), _f32(w), _f32(params))
     L = lib()
@@ -516,9 +523,9 @@ def ext_stroop_eval(variant, n_levels, levels, w, params, begin, end, n_trials, 
         e = min(begin + n, b + seg)
         if e <= b:
             return
-        rc = L.od_ext_stroop_eval(int(variant), *args, b, e, int(n_trials), int(seed),
-                                  counts[b - begin:e - begin].ctypes.data_as(C.c_void_p),
-                                  net[b - begin:e - begin].ctypes.data_as(C.c_void_p))
+        rc = L.od_ext_stroop_eval_range(int(variant), *args, b, e, int(n_trials), int(trial_begin), int(trial_end),
+                                        int(seed), counts[b - begin:e - begin].ctypes.data_as(C.c_void_p),
+                                        net[b - begin:e - begin].ctypes.data_as(C.c_void_p) if full else None)
         if rc != 0:
             raise ValueError("od_ext_stroop_eval rejected its arguments")
 
@@ -527,7 +534,7 @@ def ext_stroop_eval(variant, n_levels, levels, w, params, begin, end, n_trials, 
         t.start()
     for t in ts:
         t.join()
-    return counts, net
+    return counts, (net if full else None)
 
 
 def ext_stroop_trial(variant, params, u_c, u_s, seed, unit, trial):

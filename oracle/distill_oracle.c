@@ -943,10 +943,11 @@ float od_ext_stroop_value(int variant, const float P[13], const float w[2], floa
     return (float)v;
 }
 
-int od_ext_stroop_eval(int variant, const uint32_t n_levels[2], const float* levels, const float w[2],
-                       const float P[13], uint64_t begin, uint64_t end, uint32_t n_trials, uint64_t seed,
-                       uint64_t* counts, float* net) {
-    if (!n_levels || !levels || !w || !P || n_trials == 0 || end < begin) return -1;
+int od_ext_stroop_eval_range(int variant, const uint32_t n_levels[2], const float* levels, const float w[2],
+                             const float P[13], uint64_t begin, uint64_t end, uint32_t n_trials,
+                             uint32_t trial_begin, uint32_t trial_end, uint64_t seed, uint64_t* counts, float* net) {
+    if (!n_levels || !levels || !w || !P || n_trials == 0 || end < begin ||
+        trial_end < trial_begin || trial_end > n_trials) return -1;
     uint64_t N = (uint64_t)n_levels[0] * n_levels[1];
     if (N == 0 || end > N) return -1;
     for (uint64_t i = begin; i < end; ++i) {
@@ -955,7 +956,7 @@ int od_ext_stroop_eval(int variant, const uint32_t n_levels[2], const float* lev
         float uc = levels[k[0]], us = levels[n_levels[0] + k[1]];
         uint64_t* c = counts + 3 * (i - begin);
         c[0] = c[1] = c[2] = 0;
-        for (uint32_t j = 0; j < n_trials; ++j) {
+        for (uint32_t j = trial_begin; j < trial_end; ++j) {
             int hit[2]; uint32_t st[2];
             if (variant == 0) od_ext_stroop_trial_a(P, uc, us, seed, i * (uint64_t)n_trials + j, j, hit, st);
             else od_ext_stroop_trial_b(P, uc, us, seed, i * (uint64_t)n_trials + j, j, hit, st);
@@ -966,4 +967,11 @@ int od_ext_stroop_eval(int variant, const uint32_t n_levels[2], const float* lev
         if (net) net[i - begin] = od_ext_stroop_value(variant, P, w, uc, us, n_trials, c[0], c[1], c[2]);
     }
     return 0;
+}
+
+int od_ext_stroop_eval(int variant, const uint32_t n_levels[2], const float* levels, const float w[2],
+                       const float P[13], uint64_t begin, uint64_t end, uint32_t n_trials, uint64_t seed,
+                       uint64_t* counts, float* net) {
+    return od_ext_stroop_eval_range(variant, n_levels, levels, w, P, begin, end, n_trials, 0, n_trials, seed,
+                                    counts, net);
 }

@@ -158,6 +158,10 @@ void od_ext_stroop_trial_b(const float P[13], float u_c, float u_s, uint64_t see
                            uint32_t trial, int hit[2], uint32_t step[2]);
 float od_ext_stroop_value(int variant, const float P[13], const float w[2], float u_c, float u_s,
                           uint32_t n_trials, uint64_t n_both, uint64_t n_undecided, uint64_t rt_sum);
+/* od_ext_stroop_eval over the trial sub-range [trial_begin, trial_end) of T (net: pass NULL unless the full range). */
+int od_ext_stroop_eval_range(int variant, const uint32_t n_levels[2], const float* levels, const float w[2],
+                             const float P[13], uint64_t begin, uint64_t end, uint32_t n_trials,
+                             uint32_t trial_begin, uint32_t trial_end, uint64_t seed, uint64_t* counts, float* net);
 int od_ext_stroop_eval(int variant, const uint32_t n_levels[2], const float* levels, const float w[2],
                        const float P[13], uint64_t begin, uint64_t end, uint32_t n_trials, uint64_t seed,
                        uint64_t* counts, float* net);

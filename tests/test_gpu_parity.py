@@ -1232,8 +1232,6 @@ def test_trial_streaming_edges_bit_exact(D, orc, model, case):
     elif case == "short_trip":
         c.params[n_i] = 4 if model != "ddmg" else 7
     else:
-        if model.startswith("ext"):
-            pytest.skip("the Ext-Stroop oracle entry evaluates whole trial ranges only")
         rng_ = (5, 9)
     m = D.load_model(kind, c.n_levels, c.levels, c.w, c.params, device=0)
     cnt, net, key = _stroop_gpu(D, m, c, 0, c.n_alloc, trial_range=rng_)
@@ -1246,7 +1244,7 @@ def test_trial_streaming_edges_bit_exact(D, orc, model, case):
                                threads=8)
     else:
         wc, wn = orc.ext_stroop_eval(0 if model == "ext_a" else 1, c.n_levels, c.levels, c.w, c.params, 0,
-                                     c.n_alloc, c.n_trials, c.seed, threads=8)
+                                     c.n_alloc, c.n_trials, c.seed, threads=8, trial_begin=tb, trial_end=te)
     assert np.array_equal(cnt, wc)
     if rng_ == (0, 0):
         assert np.array_equal(_bits(net), _bits(wn))

@@ -103,3 +103,13 @@ def test_both_ddms_follow_the_closed_form_error_rates(orc):
             wrong_sign = (1 - er(A1)) * (1 - er(a_p + gam * hc * hw))
             swapped = (1 - er(-A1)) * (1 - er(A2))
             assert abs(p - wrong_sign) > 4 * se and abs(p - swapped) > 4 * se
+
+
+def test_ext_stroop_trial_subranges_add_up(orc):
+    """Counts over trial sub-ranges sum to the whole-range counts (exact integers;
+    the GPU's trial-range launches are checked against these)."""
+    c = W.ext_stroop_small()
+    full, net = orc.ext_stroop_eval(1, c.n_levels, c.levels, c.w, c.params, 3, 17, c.n_trials, c.seed)
+    a, na = orc.ext_stroop_eval(1, c.n_levels, c.levels, c.w, c.params, 3, 17, c.n_trials, c.seed, trial_end=77)
+    b, _ = orc.ext_stroop_eval(1, c.n_levels, c.levels, c.w, c.params, 3, 17, c.n_trials, c.seed, trial_begin=77)
+    assert np.array_equal(full, a + b) and na is None and net is not None
