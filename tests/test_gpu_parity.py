@@ -865,7 +865,8 @@ def test_concurrent_streams_and_threads_on_one_model(D, orc):
 def test_randomised_parity_fuzz(D, orc):
     """Deterministic fuzz: 60 random PP configurations (shapes, sample counts
     odd/even, params, positions, seeds, shards, both the warp-per-allocation and
-    the thread-per-allocation kernels) and 12 random DDM / Stroop configurations,
+    the thread-per-allocation kernels), 12 random DDM / Stroop configurations and
+    8 random DDM-grid / Extended Stroop configurations with trial sub-ranges,
     each bit-exact against the oracle."""
     import os
     import torch
@@ -918,6 +919,41 @@ def test_randomised_parity_fuzz(D, orc):
         wc, wn = orc.stroop_eval(Ls, lev, W.STROOP_W, P, 0, n, T, sd)
         assert np.array_equal(counts.cpu().numpy().astype(np.uint64).reshape(n, 3), wc), case
         assert np.array_equal(_bits(net.cpu().numpy()), _bits(wn)), case
+    # the trial-streaming kernels (R14b) on random DDM-grid / Extended Stroop configurations
+    # and random trial sub-ranges
+    for case in range(8):
+        ext = case % 2 == 1
+        Ls = (int(rng.integers(1, 6)), int(rng.integers(1, 6)))
+        n = Ls[0] * Ls[1]
+        T = int(rng.integers(1, 300))
+        tb = int(rng.integers(0, T))
+        te = int(rng.integers(tb + 1, T + 1)) if case % 4 < 2 else T
+        if case % 4 >= 2:
+            tb = 0
+        sd = int(rng.integers(0, 2 ** 63))
+        if ext:
+            P = W.EXT_STROOP_PARAMS.copy()
+            P[3] = int(rng.integers(0, 40))
+            P[9] = rng.uniform(0.1, 1.0)
+            P[10] = int(rng.integers(1, 150))
+            lev = rng.uniform(0, 1, sum(Ls)).astype(np.float32)
+            kind, variant = (W.KIND_EXT_STROOP_A, 0) if case % 3 else (W.KIND_EXT_STROOP_B, 1)
+        else:
+            P = W.DDMG_PARAMS.copy()
+            P[0], P[1], P[2] = rng.uniform(-0.5, 0.5), rng.uniform(0, 2), rng.uniform(0.3, 1.5)
+            P[6] = int(rng.integers(1, 500))
+            lev = np.concatenate([rng.uniform(0, 1, Ls[0]), rng.uniform(0.05, 1.5, Ls[1])]).astype(np.float32)
+            kind = W.KIND_DDM_GRID
+        w = np.array([0.3, 0.1], np.float32)
+        mg = D.load_model(kind, Ls, lev, w, P, device=0)
+        counts = torch.zeros(3 * n, dtype=torch.int64, device="cuda")
+        D.eval_grid(mg, None, T, sd, 0, n, counts=counts, trial_range=(tb, te))
+        torch.cuda.synchronize()
+        if ext:
+            wc, _ = orc.ext_stroop_eval(variant, Ls, lev, w, P, 0, n, T, sd, trial_begin=tb, trial_end=te)
+        else:
+            wc, _ = orc.ddmg_eval(Ls, lev, w, P, 0, n, T, sd, tb, te)
+        assert np.array_equal(counts.cpu().numpy().astype(np.uint64).reshape(n, 3), wc), (case, ext, tb, te)
 
 
 @pytest.mark.slow
