@@ -249,7 +249,19 @@ def run_ours(args):
         local = args.device
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # --collective-at-1: a one-rank NCCL group and the key all-reduce inside the step at
+    # N = 1 — exercises NCCL + graph capture of the collective on a single GPU (a test mode)
+    coll = world > 1 or args.collective_at_1
+    if coll:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if "MASTER_PORT" not in os.environ:
+                import socket
+                with socket.socket() as sk:
+                    sk.bind(("127.0.0.1", 0))
+                    os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -288,7 +300,7 @@ def run_ours(args):
         if ev_k1 is not None:
             ev_k1.record(stream)
         nvtx.range_pop()
-        if world > 1:
+        if coll:
             nvtx.range_push("key_allreduce")
             D.best_allreduce(best, signed=True)
             nvtx.range_pop()
@@ -319,7 +331,7 @@ def run_ours(args):
         except Exception as exc:     # fall back to eager steps, say so in the JSON line
             ok, err = 0, repr(exc)[:160]
         torch.cuda.synchronize()
-        if world > 1:                # all ranks replay the captured collective, or none does
+        if coll:                     # all ranks replay the captured collective, or none does
             agree = torch.tensor([ok], dtype=torch.int32, device=dev)
             dist.all_reduce(agree, op=dist.ReduceOp.MIN)
             ok = int(agree.item())
@@ -419,7 +431,7 @@ def run_ours(args):
                 pass
 
     if rank != 0:
-        if world > 1:
+        if coll:
             dist.destroy_process_group()
         return 0
 
@@ -479,7 +491,9 @@ def run_ours(args):
            "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
            "dtype": "f32", "data": "synthetic",
            "config": workload_config(cfg, world),
-           "timing": {"step": graph_note, "statistic": "median over steps, max over ranks",
+           "timing": {"step": graph_note + (" (one-rank NCCL all-reduce in the step: --collective-at-1)"
+                                             if coll and world == 1 else ""),
+                      "statistic": "median over steps, max over ranks",
                       "l2": "flushed (512 MiB write) before every timed step, outside the step events",
                       "allocations_per_gpu": count},
            "result": {"best_index": best_idx, "best_cost": best_cost, "key": f"{key:016x}"},
@@ -492,7 +506,7 @@ def run_ours(args):
            "clocks": clocks, "gpu_launches": launches, "gpu_launches_per_step": launches / K,
            "also": also}
     print(json.dumps(out), flush=True)
-    if world > 1:
+    if coll:
         dist.destroy_process_group()
     return 0
 
@@ -801,6 +815,8 @@ def main():
     ap.add_argument("--strong", action="store_true", help="N = 1: the whole cfg5 grid (t1 of the strong series)")
     ap.add_argument("--weak", action="store_true", help="~1e6 allocations per GPU instead of cfg5 for N > 1")
     ap.add_argument("--no-graph", action="store_true", help="eager steps instead of the CUDA graph")
+    ap.add_argument("--collective-at-1", action="store_true",
+                    help="N = 1 test mode: a one-rank NCCL group and the key all-reduce inside the (graph-captured) step")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

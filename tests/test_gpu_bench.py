@@ -75,3 +75,18 @@ def test_bench_self_spawns_ranks_and_reproduces_the_single_gpu_key():
     best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
     D.eval_grid(m, c5.inputs, c5.n_samples, c5.seed, best=best)
     assert d["result"]["key"] == f"{D.key_from_tensor(best):016x}"
+
+
+def test_bench_graph_captures_the_nccl_allreduce_on_one_gpu():
+    """The multi-GPU step's riskiest piece — the NCCL key all-reduce captured in
+    the CUDA graph with the kernel, and the capture agreement — run on one GPU
+    as a one-rank NCCL group (--collective-at-1): the graph is used, and the
+    all-reduced key is the oracle's cfg3 key (as at N = 1 without the collective)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "5", "--warmup", "3",
+                          "--no-extras", "--no-cpu-baseline", "--collective-at-1"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert "captured in one CUDA graph" in d["timing"]["step"] and "collective-at-1" in d["timing"]["step"]
+    assert d["result"]["key"] == "be0a43c0000642d1"          # test_bench_json_contract_on_gpu derives it from the oracle
