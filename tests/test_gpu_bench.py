@@ -89,4 +89,10 @@ def test_bench_graph_captures_the_nccl_allreduce_on_one_gpu():
     assert out.returncode == 0, out.stderr[-3000:]
     d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     assert "captured in one CUDA graph" in d["timing"]["step"] and "collective-at-1" in d["timing"]["step"]
-    assert d["result"]["key"] == "be0a43c0000642d1"          # test_bench_json_contract_on_gpu derives it from the oracle
+    sys.path.insert(0, ROOT)
+    import oracle
+    import workloads as W
+    c = W.pp_cfg3()
+    full = oracle.pp_eval_threads(c.n_levels, c.levels, c.w, c.params, c.inputs, 0, c.n_alloc, c.n_samples, c.seed,
+                                  threads=os.cpu_count() or 8)
+    assert d["result"]["key"] == f"{oracle.argmax_net(-full)[0]:016x}"
