@@ -180,17 +180,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddmg_sim_kernel(const DdmgArgs a,
             acc_normals12(rng, s_rt, grp, g);
 #pragma unroll
             for (int l = 0; l < 12; ++l) { x = __fmaf_rn(nsd, g[l], __fmaf_rn(a.dt, A, x)); xs[l] = x; }
-            float mx = fabsf(xs[0]);
+            // the first step with x >= z (correct, tested first) or x <= -z, from two
+            // 12-bit masks: no branches in the resolution
+            uint32_t mu = 0, ml = 0;
 #pragma unroll
-            for (int l = 1; l < 12; ++l) mx = fmaxf(mx, fabsf(xs[l]));
-            if (mx >= z) {
-#pragma unroll
-                for (int l = 0; l < 12; ++l) {
-                    if (st == 0) {
-                        if (xs[l] >= z) { st = 12 * grp + l + 1; ch = 0; }
-                        else if (xs[l] <= nz) { st = 12 * grp + l + 1; ch = 1; }
-                    }
-                }
+            for (int l = 0; l < 12; ++l) {
+                mu |= (uint32_t)(xs[l] >= z) << l;
+                ml |= (uint32_t)(xs[l] <= nz) << l;
+            }
+            if (mu | ml) {
+                const int l = __ffs(mu | ml) - 1;
+                ch = ((mu >> l) & 1u) ? 0u : 1u;
+                st = 12 * grp + l + 1;
             }
             ++grp;
             if (st == 0 && grp < n12) continue;          // the trial goes on (the hot path)

@@ -387,6 +387,18 @@ distill_status distill_eval_grid_multi(const distill_model* m, const distill_mul
     return DISTILL_OK;
 }
 
+// Blocks along the trial axis per allocation for the trial-streaming kernels
+// (R14b): enough blocks in all for ~8 waves of 8 resident blocks per SM, but
+// each lane's stream at least 16 trials long, so that the end of a lane's
+// stream (its warp waiting for the last trials) stays short against it.
+static uint32_t trial_chunks(int n_sm, uint64_t count, uint32_t tr) {
+    const uint64_t fill = (uint64_t)n_sm * 8 * 8;
+    const uint64_t want = (fill + count - 1) / count;
+    const uint64_t cap = std::max<uint64_t>(1, tr / (STROOP_BLOCK * 16u));
+    const uint64_t most = std::max<uint64_t>(1, (tr + STROOP_BLOCK - 1) / STROOP_BLOCK);
+    return (uint32_t)std::max<uint64_t>(1, std::min(std::min(want, cap), most));
+}
+
 static distill_status launch_stroop(distill_model* m, const distill_eval_args* a, cudaStream_t st) {
     if (a->n_samples == 0 || a->n_samples > MAX_SAMPLES)
         return fail(DISTILL_E_INVALID_ARG, "eval_grid(Stroop): n_samples (trials) must be in [1, 2^31]");
@@ -426,13 +438,7 @@ static distill_status launch_stroop(distill_model* m, const distill_eval_args* a
     p.rad_tab = m->d_rt;
     const uint32_t tr = te - tb;
     if (tr > 0) {
-        // enough blocks along trials to fill the machine, capped so each thread runs >= 1 trial
-        uint32_t chunks = (tr + STROOP_BLOCK - 1) / STROOP_BLOCK;
-        const uint64_t want = (uint64_t)m->n_sm * 8;
-        if ((uint64_t)chunks * count > want * 64) {
-            const uint64_t c2 = (want * 64 + count - 1) / count;
-            chunks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(chunks, c2));
-        }
+        const uint32_t chunks = trial_chunks(m->n_sm, count, tr);
         const size_t table_bytes = 4ull * p.n_steps * sizeof(float);
         DdmgArgs q;
         if (ddmg) {
@@ -545,9 +551,7 @@ static distill_status launch_ext_stroop(distill_model* m, const distill_eval_arg
     p.key_signed = a->key_order;
     p.rad_tab = m->d_rt;
     const uint32_t tr = te - tb;
-    uint32_t chunks = std::max<uint32_t>(1, (tr + STROOP_BLOCK - 1) / STROOP_BLOCK);
-    const uint64_t want = (uint64_t)m->n_sm * 8 * 64;
-    if ((uint64_t)chunks * count > want) chunks = (uint32_t)std::max<uint64_t>(1, (want + count - 1) / count);
+    const uint32_t chunks = trial_chunks(m->n_sm, count, tr);
     const bool fin = full && (a->d_net || a->d_best);
     if (m->kind == DISTILL_MODEL_EXT_STROOP_A) launch_ext_stroop_kernels<0>(p, chunks, count, tr > 0, fin, st);
     else launch_ext_stroop_kernels<1>(p, chunks, count, tr > 0, fin, st);

@@ -120,10 +120,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
     if (j < t_end) start(j);
     while (j < t_end) {
         if (grp < n6) {
-            // Six steps (12 normals, two sextet blocks) per group.  x_k >= 0 after
-            // the rectification (fmaxf(NaN, 0) = 0 as well), so "x0 >= θ or x1 >= θ"
-            // at any step of the group <=> the max of its 12 states >= θ: one test
-            // per group; the rare group that passes is resolved in the spec's order.
+            // Six steps (12 normals, two sextet blocks) per group, then the latch
+            // test on the group's 12 states in the spec's order.
             float g[12], s0[6], s1[6];
             acc_normals12(rng, s_rt, grp, g);
 #pragma unroll
@@ -133,17 +131,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
                 lca_update(a, nleak, ninh, nsd, g[2 * l], g[2 * l + 1], h0, h1, x0, x1);
                 s0[l] = x0; s1[l] = x1;
             }
-            float m = fmaxf(s0[0], s1[0]);
+            // the first step of the group with x0 >= θ or x1 >= θ, unit 0 first at a tie
+            // (spec order), from two 6-bit masks: no branches in the resolution
+            uint32_t m0 = 0, m1 = 0;
 #pragma unroll
-            for (int l = 1; l < 6; ++l) m = fmaxf(m, fmaxf(s0[l], s1[l]));
-            if (m >= a.thr) {
-#pragma unroll
-                for (int l = 0; l < 6; ++l) {
-                    if (resp < 0) {
-                        if (s0[l] >= a.thr) { resp = 0; st = 6 * grp + l + 1; }
-                        else if (s1[l] >= a.thr) { resp = 1; st = 6 * grp + l + 1; }
-                    }
-                }
+            for (int l = 0; l < 6; ++l) {
+                m0 |= (uint32_t)(s0[l] >= a.thr) << l;
+                m1 |= (uint32_t)(s1[l] >= a.thr) << l;
+            }
+            if (m0 | m1) {
+                const int l = __ffs(m0 | m1) - 1;
+                resp = ((m0 >> l) & 1u) ? 0 : 1;
+                st = 6 * grp + l + 1;
             }
             ++grp;
             if (resp < 0 && grp < n6) continue;          // the trial goes on (the hot path)
@@ -356,8 +355,7 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
     if (j < t_end) start(j);
     while (j < t_end) {
         if (grp < n6) {
-            // Six steps (12 normals) per group; each DDM's latch is tested once per
-            // group on max |x| (|x| >= z <=> x >= z or x <= -z, DDM kernel).
+            // Six steps (12 normals) per group, then each DDM's latch test.
             float g[12], y1[6], y2[6];
             acc_normals12(rng, s_rt, grp, g);
 #pragma unroll
@@ -371,16 +369,23 @@ __global__ void __launch_bounds__(BLOCK) ext_stroop_sim_kernel(const ExtStroopAr
                 }
                 y1[l] = x1; y2[l] = x2;
             }
-            float m1 = fabsf(y1[0]), m2 = fabsf(y2[0]);
+            // each DDM's first passage in the group (upper tested first, spec order)
+            // from bit masks of the six states: no branches in the resolution
+            uint32_t u1 = 0, d1 = 0, u2 = 0, d2 = 0;
 #pragma unroll
-            for (int l = 1; l < 6; ++l) { m1 = fmaxf(m1, fabsf(y1[l])); m2 = fmaxf(m2, fabsf(y2[l])); }
-            if (!h1t && m1 >= a.z) {
-#pragma unroll
-                for (int l = 0; l < 6; ++l) ddm_latch(y1[l], a.z, 6 * grp + l + 1, h1t, s1);
+            for (int l = 0; l < 6; ++l) {
+                u1 |= (uint32_t)(y1[l] >= a.z) << l;  d1 |= (uint32_t)(y1[l] <= -a.z) << l;
+                u2 |= (uint32_t)(y2[l] >= a.z) << l;  d2 |= (uint32_t)(y2[l] <= -a.z) << l;
             }
-            if (!h2t && m2 >= a.z) {
-#pragma unroll
-                for (int l = 0; l < 6; ++l) ddm_latch(y2[l], a.z, 6 * grp + l + 1, h2t, s2);
+            if (!h1t && (u1 | d1)) {
+                const int l = __ffs(u1 | d1) - 1;
+                h1t = ((u1 >> l) & 1u) ? 1 : 2;
+                s1 = 6 * grp + l + 1;
+            }
+            if (!h2t && (u2 | d2)) {
+                const int l = __ffs(u2 | d2) - 1;
+                h2t = ((u2 >> l) & 1u) ? 1 : 2;
+                s2 = 6 * grp + l + 1;
             }
             ++grp;
             if (!(h1t && h2t) && grp < n6) continue;     // the trial goes on (the hot path)

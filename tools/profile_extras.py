@@ -36,6 +36,11 @@ def main():
     counts = torch.empty(3 * n, dtype=torch.int64, device="cuda")
     for _ in range(2):       # a slice around the cfg4 optimum (allocation 8083): representative response times
         D.eval_grid(m, None, c.n_trials, c.seed, 8000, 8000 + n, net=net, best=best, counts=counts)
+    if "--stroop-full" in sys.argv:   # the whole cfg4 grid in the library's launch shape
+        nf = c.n_alloc
+        netf = torch.empty(nf, device="cuda")
+        countsf = torch.empty(3 * nf, dtype=torch.int64, device="cuda")
+        D.eval_grid(m, None, c.n_trials, c.seed, 0, nf, net=netf, best=best, counts=countsf)
     g = W.ext_stroop_grid()
     mx = D.load_model(W.KIND_EXT_STROOP_A, g.n_levels, g.levels, g.w, g.params, device=0)
     for _ in range(2):
