@@ -106,8 +106,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
         colour = (jj / 3) & 1;
         const int word = (kind == 0) ? (int)colour : (kind == 1) ? (int)(1 - colour) : -1;
         if (TABLE) {
-            pw.row0 = s_htab + N * ((colour == 0 ? 1u : 0u) + (word == 0 ? 2u : 0u));
-            pw.row1 = s_htab + N * ((colour == 1 ? 1u : 0u) + (word == 1 ? 2u : 0u));
+            // table rows (1: colour input, 2: word input, 3: both) without branches: the
+            // colour unit gets row 3 in congruent trials (word = colour) and 1 otherwise;
+            // the other unit gets row 2 in incongruent trials (word = other) and 0 otherwise
+            const uint32_t rc = kind == 0 ? 3u : 1u, ro = kind == 1 ? 2u : 0u;
+            pw.row0 = s_htab + N * (colour == 0 ? rc : ro);
+            pw.row1 = s_htab + N * (colour == 1 ? rc : ro);
         } else {
             pw.I0 = __fadd_rn(colour == 0 ? ic : 0.0f, word == 0 ? iw : 0.0f);
             pw.I1 = __fadd_rn(colour == 1 ? ic : 0.0f, word == 1 ? iw : 0.0f);
