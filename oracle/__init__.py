@@ -38,8 +38,9 @@ def build(force: bool = False) -> None:
         if (not force and os.path.exists(out)
                 and os.path.getmtime(out) >= max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))):
             continue
-        subprocess.check_call(["gcc", *CFLAGS, *extra, _SRC, "-o", out + ".tmp", "-lm"])
-        os.replace(out + ".tmp", out)
+        tmp = f"{out}.{os.getpid()}.tmp"          # per-process name: concurrent builders never share a file
+        subprocess.check_call(["gcc", *CFLAGS, *extra, _SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, out)
 
 
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C")
