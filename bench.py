@@ -7,16 +7,17 @@ One *step* = one controller grid search over the whole grid: key reset,
 fused pp_eval_grid kernel on this rank's contiguous shard (decode, Philox,
 Box-Muller, Obs/Action/Objective, mean + cost, net-value store, (value,
 index) argmin), and for N > 1 the single NCCL all-reduce of the packed key.
-Workload (weak scaling, ~1e6 allocations per GPU): N=1 -> cfg3 (100^3 x 100
-samples), N=8 -> cfg5 (200^3 x 100), N=2/4 -> round(100 N^(1/3))^3 x 100.
+Workload: N=1 -> cfg3 (100^3 x 100 samples); N=2/4/8 -> cfg5 (200^3 x 100)
+sharded across the N GPUs (strong scaling; --weak: ~1e6 allocations per GPU,
+round(100 N^(1/3))^3 x 100; --strong at N=1: cfg5 whole on one GPU).
 
 Prints ONE JSON line (rank 0).  `value` = allocations x samples per second
 over all ranks (max-over-ranks device time), `e2e` = the same metric through
 the host-buffer C-ABI call (positions in, net values + best key out),
 `roofline` = the fused kernel's algorithmic FP32 rate against the FP32 ALU
 peak, `cpu_baseline` = the CPU oracle on this host's cores on a bounded slice.
-DDM (cfg2) and Stroop-LCA (cfg4) are measured once each and reported under
-`also` (they are §8 rows a5/a6/a10, not the headline).
+DDM (cfg2), Stroop-LCA (cfg4) and the other kernels are timed (median of a few
+passes) and reported under `also` (they are §8 rows a5/a6/a10, not the headline).
 """
 from __future__ import annotations
 
@@ -517,13 +518,33 @@ def run_extras(D, torch, dev, rank, world, args):
     out = {}
     d = W.ddm_cfg2()
     tb, te = D.shard_range(d.n_trials, rank, world)
-    rh, rs, xh = (torch.zeros(n, dtype=torch.int64, device=dev) for n in d.hist_sizes)
+    # the three histograms are views of one buffer: one zeroing launch per pass
+    hbuf = torch.zeros(sum(d.hist_sizes), dtype=torch.int64, device=dev)
+    rh, rs, xh = torch.split(hbuf, list(d.hist_sizes))
 
-    def ddm_once():
-        for t in (rh, rs, xh):
-            t.zero_()
+    def ddm_local():
+        hbuf.zero_()
         D.ddm_batch(d.drift, d.noise, d.threshold, d.x0, d.dt, d.n_steps, d.rt_bin_steps, d.n_x_bins,
                     d.x_lo, d.x_hi, tb, te, d.seed, rh, rs, xh)
+
+    ddm_local()
+    torch.cuda.synchronize()
+    # zeroing + kernel captured in a CUDA graph (no host gap between them inside the timed
+    # pass); the cross-rank histogram all-reduce (N > 1) runs eagerly after the replay
+    ddm_graph = None
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            ddm_local()
+        ddm_graph = g
+    except RuntimeError:
+        torch.cuda.synchronize()
+
+    def ddm_once():
+        if ddm_graph is not None:
+            ddm_graph.replay()
+        else:
+            ddm_local()
         if world > 1:
             D.hist_allreduce([rh, rs, xh])
 
@@ -546,7 +567,9 @@ def run_extras(D, torch, dev, rank, world, args):
     up, lo = int(rh[:nb].sum()), int(rh[nb:2 * nb].sum())
     steps_s = d.n_trials * d.n_steps / (ms / 1e3)
     out["ddm_cfg2"] = {"trials_per_s": d.n_trials / (ms / 1e3), "steps_per_s": steps_s,
-                       "ms": ms, "timing": "median of 5 passes", "error_rate": lo / max(1, up + lo),
+                       "ms": ms, "timing": "median of 5 passes" + (", histogram zeroing + kernel replayed as one CUDA graph"
+                                                            if ddm_graph is not None else ", eager"),
+                       "error_rate": lo / max(1, up + lo),
                        "mean_rt_s": (int(rs[0]) + int(rs[1])) / max(1, up + lo) * d.dt,
                        "algorithmic_tflops": DDM_FLOPS_PER_STEP * steps_s / 1e12,
                        "frac_fp32_peak": DDM_FLOPS_PER_STEP * steps_s / 1e12 / FP32_PEAK_NOMINAL,
