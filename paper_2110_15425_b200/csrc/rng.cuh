@@ -142,23 +142,34 @@ __device__ __forceinline__ F2 rsqrt2_from(F2 x, F2 mh) {
     return y;
 }
 
+// (a & b) | c in one LOP3 (ptxas otherwise emits an AND and an OR for two immediates)
+template <uint32_t B>
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(B), "r"(c));
+    return d;
+}
+
 // rad_spec on both lanes (spec/RNG.md §3): region r, v = r ? 2^24 - N : N, and
 // the row index 368 r + 16 e + j read straight off the bits of float(v) (exact:
 // its exponent field is 127 + e and its top four mantissa bits are j);
-// t = m - (1 + (2j + 1)/32) from the remaining mantissa bits (exact).  Scalar
+// t = m - (1 + (2j + 1)/32) from the remaining mantissa bits (exact).  Integer
+// steps: with the arithmetic shifts s = R >> 8 and m = R >> 31 (all ones in
+// region 1), v = (s ^ m) | 1 (for N = x | 1 >= 2^23: 2^24 - N = (x ^ 0xFFFFFF) | 1)
+// and 368 r = m & 368; the mantissa mask-and-set is one LOP3 (measured: -3 to -6 %
+// on every hot kernel against the select form, bit-identical; tools/ab_lib.py).  Scalar
 // lanes: each lane's coefficients arrive as one LDS.128 in four consecutive
 // registers, and pairing them for FFMA2 costs a register move per operand
 // (measured: scalar is 3-5 % faster on every hot kernel, bit-identical).
 __device__ __forceinline__ F2 rad2(uint32_t Rx, uint32_t Ry, const float4* __restrict__ rt) {
     using L = Ops<true>;
-    const uint32_t nx = (Rx >> 8) | 1u, ny = (Ry >> 8) | 1u;
-    const uint32_t hx = nx >> 23, hy = ny >> 23;
-    const uint32_t vx = hx ? 0x1000000u - nx : nx, vy = hy ? 0x1000000u - ny : ny;
+    const uint32_t mx = (uint32_t)((int32_t)Rx >> 31), my = (uint32_t)((int32_t)Ry >> 31);
+    const uint32_t vx = (((uint32_t)((int32_t)Rx >> 8)) ^ mx) | 1u, vy = (((uint32_t)((int32_t)Ry >> 8)) ^ my) | 1u;
     const uint32_t bx = __float_as_uint(__uint2float_rn(vx)), by = __float_as_uint(__uint2float_rn(vy));
-    const float4 cx = rt[(bx >> 19) - (127u << 4) + (hx ? 368u : 0u)];
-    const float4 cy = rt[(by >> 19) - (127u << 4) + (hy ? 368u : 0u)];
-    const F2 t = L::add(make_float2(__uint_as_float((bx & 0x7FFFFu) | 0x3F800000u),
-                                    __uint_as_float((by & 0x7FFFFu) | 0x3F800000u)), bc(-1.03125f));
+    const float4 cx = (rt - (127u << 4))[(bx >> 19) + (mx & 368u)];
+    const float4 cy = (rt - (127u << 4))[(by >> 19) + (my & 368u)];
+    const F2 t = L::add(make_float2(__uint_as_float(lop3_and_or<0x7FFFFu>(bx, 0x3F800000u)),
+                                    __uint_as_float(lop3_and_or<0x7FFFFu>(by, 0x3F800000u))), bc(-1.03125f));
     F2 p = L::fma(make_float2(cx.w, cy.w), t, make_float2(cx.z, cy.z));
     p = L::fma(p, t, make_float2(cx.y, cy.y));
     return L::fma(p, t, make_float2(cx.x, cy.x));
@@ -178,8 +189,8 @@ __device__ __forceinline__ void bm_polar2_fs(uint32_t Rx, uint32_t Ry, uint32_t 
     using Q = Ops<SSC>;
     const F2 rad = rad2(Rx, Ry, rt);
     // sincos_spec: r from the angle bits, half-turn sign applied to rad
-    const F2 r = Q::add(make_float2(__uint_as_float((Fx & MASK) | 0x3F800000u),
-                                    __uint_as_float((Fy & MASK) | 0x3F800000u)),
+    const F2 r = Q::add(make_float2(__uint_as_float(lop3_and_or<MASK>(Fx, 0x3F800000u)),
+                                    __uint_as_float(lop3_and_or<MASK>(Fy, 0x3F800000u))),
                         bc(-1.5f));
     const F2 t = Q::mul(r, r);
     const F2 S = Q::fma(Q::fma(Q::fma(Q::fma(bc(D_S4), t, bc(D_S3)), t, bc(D_S2)), t, bc(D_S1)), t, bc(D_S0));
