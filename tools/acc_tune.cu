@@ -145,13 +145,15 @@ void ddm(const char* name, DDMArgs a, size_t n_all, bool ref) {
 }
 
 template <int BLOCK, int MINB, bool TABLE = true>
-void stroop(const char* name, StroopArgs a, bool ref) {
+void stroop(const char* name, StroopArgs a, bool ref, uint32_t per_lane = 16, uint32_t fill_per_sm = 64) {
     cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, stroop_sim_kernel<BLOCK, MINB, TABLE>);
-    // the library's launch shape (distill.cu launch_stroop): chunks capped so the
-    // grid holds ~64 blocks per resident slot
-    uint32_t chunks = (a.trial_end + BLOCK - 1) / BLOCK;
-    const uint64_t want = 148ull * 8 * 64;
-    if ((uint64_t)chunks * a.count > want) chunks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(chunks, (want + a.count - 1) / a.count));
+    // the library's launch shape (distill.cu trial_chunks): enough blocks to fill
+    // `fill_per_sm` per SM, but at least `per_lane` trials per lane of a block
+    const uint32_t tr = a.trial_end - a.trial_begin;
+    const uint64_t want = (148ull * fill_per_sm + a.count - 1) / a.count;
+    const uint64_t cap = std::max<uint64_t>(1, tr / (BLOCK * per_lane));
+    const uint64_t most = std::max<uint64_t>(1, (tr + BLOCK - 1) / BLOCK);
+    const uint32_t chunks = (uint32_t)std::max<uint64_t>(1, std::min(std::min(want, cap), most));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     float best = 1e30f;
     for (int r = 0; r < 3; ++r) {
@@ -170,8 +172,8 @@ void stroop(const char* name, StroopArgs a, bool ref) {
         for (auto v : h) hsh = (hsh ^ v) * 1099511628211ull;
         printf("stroop ref hash %016llx\n", hsh);
     }
-    printf("stroop %-18s b%4d minb%2d regs %3d %9.4f ms  %s\n", name, BLOCK, MINB, fa.numRegs, best,
-           h == g_ref_st ? "identical" : "MISMATCH");
+    printf("stroop %-18s b%4d minb%2d regs %3d lane>=%2u fill %3u chunks %4u %9.4f ms  %s\n", name, BLOCK, MINB,
+           fa.numRegs, per_lane, fill_per_sm, chunks, best, h == g_ref_st ? "identical" : "MISMATCH");
 }
 
 int main() {
@@ -205,11 +207,14 @@ int main() {
     s.n_trials = 100000; s.trial_begin = 0; s.trial_end = 100000; s.key0 = 42; s.key1 = 0;
     s.begin = 5000; s.count = 200; s.levels = dl;
     cudaMalloc((void**)&s.counts, 200 * 24);
-    stroop<128, 6, false>("ref (no table)", s, true);
-    stroop<128, 6, true>("table", s, false);
-    stroop<256, 0>("", s, false);
-    stroop<256, 3>("", s, false); stroop<256, 4>("", s, false); stroop<128, 0>("", s, false);
-    stroop<128, 6>("", s, false); stroop<128, 8>("", s, false); stroop<64, 0>("", s, false);
+    stroop<128, 0, true>("shipped (ref)", s, true);
+    stroop<128, 0, false>("no table", s, false);
+    for (uint32_t pl : {4u, 8u, 32u, 64u}) stroop<128, 0>("", s, false, pl);
+    for (uint32_t fl : {32u, 128u, 256u}) stroop<128, 0>("", s, false, 16, fl);
+    stroop<128, 6>("", s, false); stroop<128, 8>("", s, false);
+    stroop<64, 0>("", s, false); stroop<64, 0>("", s, false, 32); stroop<64, 0>("", s, false, 16, 128);
+    stroop<64, 12>("", s, false); stroop<64, 16>("", s, false);
+    stroop<256, 0>("", s, false); stroop<256, 4>("", s, false); stroop<256, 0>("", s, false, 8);
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
