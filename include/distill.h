@@ -289,6 +289,30 @@ distill_status distill_ddm_batch(const distill_ddm_args* args, void* stream);
  * "computationally equivalent" pair). */
 distill_status distill_lci_batch(const distill_ddm_args* args, float leak, float offset, void* stream);
 
+/* Rows a2 + a3 on their own (spec/RNG.md §1-§6; "each
+ * evaluation uses its own random number generator", P:157 noisy observations):
+ * the Philox4x32-10 -> Box-Muller path every kernel inlines, over caller-chosen
+ * inputs, so that it can be compared with the oracle directly.  All run on the
+ * caller's current device (the first call there uploads the radius table, see
+ * distill_load_model — not inside a CUDA-graph capture), are stream-ordered and
+ * enqueue nothing on an argument error.  Output buffers: device, caller-owned,
+ * 4-byte aligned.
+ *
+ * distill_rng_rad: d_rad[k] = rad_spec(d_words[k]) (spec/RNG.md §3, the radius
+ *   sqrt(-2 ln u1) of a raw radius word), k < n.
+ * distill_rng_normals_acc: d_out[u * n_per_unit + j] = normal j of RNG unit
+ *   unit_begin + u on stream 2 (the DDM / Stroop / LCI noise, sextet packing §6),
+ *   j < n_per_unit (1..2^30); n_units * n_per_unit <= 2^62 (E_OVERFLOW otherwise).
+ * distill_rng_normals_pp: d_out[(t * n_samples + s) * 6 + 2e + {0,1}] = the
+ *   2-D noise vector of entity e (prey, predator, player) of sample s of
+ *   allocation alloc_begin + t, invocation word `invocation`, on stream 1;
+ *   n_samples in [1, 2^31]; alloc_begin + n_alloc <= 2^32 (E_OVERFLOW). */
+distill_status distill_rng_rad(const uint32_t* d_words, uint64_t n, float* d_rad, void* stream);
+distill_status distill_rng_normals_acc(uint64_t seed, uint64_t unit_begin, uint64_t n_units, uint32_t n_per_unit,
+                                       float* d_out, void* stream);
+distill_status distill_rng_normals_pp(uint64_t seed, uint32_t alloc_begin, uint32_t n_alloc, uint32_t n_samples,
+                                      uint32_t invocation, float* d_out, void* stream);
+
 /* Measurement utility: median effective SM clock (MHz) over one spinning block per
  * SM for `micros` microseconds (clock64 ticks / globaltimer ns).  Synchronous.
  * bench.py runs it right after the timed region to report the fraction of the

@@ -91,6 +91,10 @@ EXPORTS = {
     "distill_ddm_batch": (C.c_int, [C.POINTER(DdmArgs), C.c_void_p]),
     "distill_launch_count": (C.c_uint64, []),
     "distill_sm_clock_probe": (C.c_int, [C.c_uint32, C.POINTER(C.c_double), C.c_void_p]),
+    "distill_rng_rad": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "distill_rng_normals_acc": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "distill_rng_normals_pp": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
+                                         C.c_void_p]),
     "distill_pp_amr": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_void_p]),
     "distill_pp_amr_begin": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_void_p]),
     "distill_pp_amr_levels": (C.c_int, [C.c_void_p, C.POINTER(AmrArgs), C.c_uint32, C.c_void_p]),

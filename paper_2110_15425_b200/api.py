@@ -45,7 +45,7 @@ def _on_stream(stream):
 # element type each named buffer must have (the C ABI's float* / u64* / int*);
 # u64 buffers are int64 tensors holding the raw bit pattern
 _BUF_DTYPE = {"esum": "int64", "net": "float32", "values": "float32", "inputs": "float32", "traj": "float32",
-              "boxes": "float32", "levels": "float32",
+              "boxes": "float32", "levels": "float32", "rad": "float32",
               "best": "int64", "tie": "int64", "keys": "int64", "counts": "int64",
               "rt_hist": "int64", "rt_sum": "int64", "x_hist": "int64", "status": "int32"}
 
@@ -371,6 +371,48 @@ class AmrRun:
         check(lib().distill_pp_amr_refine(self.model.handle, C.byref(self._a), int(r), _stream_handle(self.stream, self.model.device)))
 
 
+def rng_rad(words, device: int = 0, out=None, stream=None):
+    """distill_rng_rad: rad_spec of raw radius words -> float32 CUDA tensor.  `words`: uint32
+    bit patterns as an int32 CUDA tensor, or any host array (copied to `device`)."""
+    import torch
+    if not getattr(words, "is_cuda", False):
+        w = np.ascontiguousarray(np.asarray(words, dtype=np.uint32)).view(np.int32)
+        words = torch.from_numpy(w).to(torch.device("cuda", device))
+    if words.dtype != torch.int32 or not words.is_contiguous():
+        raise ValueError("words must be a contiguous int32 CUDA tensor of uint32 bit patterns")
+    with _on_device(words), _on_stream(stream):
+        out = torch.empty(words.numel(), dtype=torch.float32, device=words.device) if out is None else out
+        check(lib().distill_rng_rad(words.data_ptr(), words.numel(), _dev_ptr(out, "rad", words.numel()),
+                                    _stream_handle(stream, words.device.index)))
+    return out
+
+
+def rng_normals_acc(seed: int, unit_begin: int, n_units: int, n_per_unit: int, device: int = 0, stream=None):
+    """distill_rng_normals_acc: stream-2 normals 0..n_per_unit-1 of RNG units
+    [unit_begin, unit_begin + n_units) -> float32 CUDA tensor [n_units, n_per_unit]."""
+    import torch
+    with torch.cuda.device(device), _on_stream(stream):
+        out = torch.empty((max(int(n_units), 1), int(n_per_unit)), dtype=torch.float32,
+                          device=torch.device("cuda", device))
+        check(lib().distill_rng_normals_acc(int(seed) & (2 ** 64 - 1), int(unit_begin), int(n_units),
+                                            int(n_per_unit), out.data_ptr(), _stream_handle(stream, device)))
+    return out[:int(n_units)]
+
+
+def rng_normals_pp(seed: int, alloc_begin: int, n_alloc: int, n_samples: int, invocation: int = 0,
+                   device: int = 0, stream=None):
+    """distill_rng_normals_pp: the predator-prey observation noise (stream 1) of
+    allocations [alloc_begin, alloc_begin + n_alloc) -> float32 CUDA tensor [n_alloc, n_samples, 6]."""
+    import torch
+    with torch.cuda.device(device), _on_stream(stream):
+        out = torch.empty((max(int(n_alloc), 1), int(n_samples), 6), dtype=torch.float32,
+                          device=torch.device("cuda", device))
+        check(lib().distill_rng_normals_pp(int(seed) & (2 ** 64 - 1), int(alloc_begin), int(n_alloc),
+                                           int(n_samples), int(invocation), out.data_ptr(),
+                                           _stream_handle(stream, device)))
+    return out[:int(n_alloc)]
+
+
 def sm_clock_mhz(micros: int = 200, stream=None) -> float:
     """distill_sm_clock_probe: median effective SM clock in MHz (measurement utility)."""
     v = C.c_double()
@@ -390,4 +432,5 @@ def key_from_tensor(best, signed: bool = False) -> int:
 
 
 __all__ = ["KEY_INIT", "stroop_energy", "AmrRun", "DistillError", "EpisodeRun", "Model", "grid_search", "best", "load_model", "eval_grid", "eval_grid_host", "eval_grid_multi", "argmax",
-           "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode", "argmax_ties", "pp_amr", "sm_clock_mhz"]
+           "key_reset", "key_decode", "ddm_batch", "launch_count", "key_from_tensor", "pp_episode", "argmax_ties", "pp_amr", "sm_clock_mhz",
+           "rng_rad", "rng_normals_acc", "rng_normals_pp"]

@@ -20,6 +20,7 @@
 #include "pp.cuh"
 #include "stroop.cuh"
 #include "rad_table.h"
+#include "rng_probe.cuh"
 
 using namespace distill;
 
@@ -957,6 +958,78 @@ distill_status distill_ddm_batch(const distill_ddm_args* a, void* stream) {
 
 distill_status distill_lci_batch(const distill_ddm_args* a, float leak, float offset, void* stream) {
     return launch_integrator<true>(a, leak, offset, stream, "lci_batch");
+}
+
+// ------------------------------------------------------------------ rows a2 / a3 on their own
+constexpr int RNG_BLOCK = 128;
+
+static distill_status rng_device_table(const float4** rt, int* n_sm) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(n_sm, cudaDevAttrMultiProcessorCount, dev));
+    return rad_table(dev, rt);
+}
+
+distill_status distill_rng_rad(const uint32_t* d_words, uint64_t n, float* d_rad, void* stream) {
+    if (n && (!d_words || !d_rad)) return fail(DISTILL_E_INVALID_ARG, "rng_rad: NULL pointer");
+    if ((reinterpret_cast<uintptr_t>(d_words) | reinterpret_cast<uintptr_t>(d_rad)) & 3u)
+        return fail(DISTILL_E_INVALID_ARG, "rng_rad: buffers must be 4-byte aligned");
+    if (n == 0) return DISTILL_OK;
+    const float4* rt = nullptr;
+    int n_sm = 148;
+    const distill_status rs = rng_device_table(&rt, &n_sm);
+    if (rs != DISTILL_OK) return rs;
+    const uint64_t need = (n + 2 * RNG_BLOCK - 1) / (2 * RNG_BLOCK);
+    const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)n_sm * 16);
+    rng_rad_kernel<RNG_BLOCK><<<grid, RNG_BLOCK, 0, (cudaStream_t)stream>>>(d_words, n, d_rad, rt);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+distill_status distill_rng_normals_acc(uint64_t seed, uint64_t unit_begin, uint64_t n_units, uint32_t n_per_unit,
+                                       float* d_out, void* stream) {
+    if (n_units && !d_out) return fail(DISTILL_E_INVALID_ARG, "rng_normals_acc: NULL output");
+    if (reinterpret_cast<uintptr_t>(d_out) & 3u)
+        return fail(DISTILL_E_INVALID_ARG, "rng_normals_acc: output must be 4-byte aligned");
+    if (n_per_unit == 0 || n_per_unit > (1u << 30))
+        return fail(DISTILL_E_INVALID_ARG, "rng_normals_acc: n_per_unit must be in [1, 2^30]");
+    if (n_units > (1ull << 62) / n_per_unit || unit_begin + n_units < unit_begin)
+        return fail(DISTILL_E_OVERFLOW, "rng_normals_acc: unit range or output size overflows");
+    if (n_units == 0) return DISTILL_OK;
+    const float4* rt = nullptr;
+    int n_sm = 148;
+    const distill_status rs = rng_device_table(&rt, &n_sm);
+    if (rs != DISTILL_OK) return rs;
+    const uint64_t grid = (n_units + RNG_BLOCK - 1) / RNG_BLOCK;
+    if (grid > 0x7FFFFFFFull) return fail(DISTILL_E_UNSUPPORTED, "rng_normals_acc: too many units for one launch");
+    rng_normals_acc_kernel<RNG_BLOCK><<<(unsigned)grid, RNG_BLOCK, 0, (cudaStream_t)stream>>>(
+        (uint32_t)seed, (uint32_t)(seed >> 32), unit_begin, n_units, n_per_unit, d_out, rt);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
+}
+
+distill_status distill_rng_normals_pp(uint64_t seed, uint32_t alloc_begin, uint32_t n_alloc, uint32_t n_samples,
+                                      uint32_t invocation, float* d_out, void* stream) {
+    if (n_alloc && !d_out) return fail(DISTILL_E_INVALID_ARG, "rng_normals_pp: NULL output");
+    if (reinterpret_cast<uintptr_t>(d_out) & 3u)
+        return fail(DISTILL_E_INVALID_ARG, "rng_normals_pp: output must be 4-byte aligned");
+    if (n_samples == 0 || n_samples > MAX_SAMPLES)
+        return fail(DISTILL_E_INVALID_ARG, "rng_normals_pp: n_samples must be in [1, 2^31]");
+    if ((uint64_t)alloc_begin + n_alloc > 0x100000000ull)
+        return fail(DISTILL_E_OVERFLOW, "rng_normals_pp: allocation index exceeds 32 bits");
+    if (n_alloc == 0) return DISTILL_OK;
+    const float4* rt = nullptr;
+    int n_sm = 148;
+    const distill_status rs = rng_device_table(&rt, &n_sm);
+    if (rs != DISTILL_OK) return rs;
+    const unsigned grid = (unsigned)(((uint64_t)n_alloc + RNG_BLOCK - 1) / RNG_BLOCK);
+    rng_normals_pp_kernel<RNG_BLOCK><<<grid, RNG_BLOCK, 0, (cudaStream_t)stream>>>(
+        (uint32_t)seed, (uint32_t)(seed >> 32), alloc_begin, n_alloc, n_samples, invocation, d_out, rt);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return DISTILL_OK;
 }
 
 }  // extern "C"

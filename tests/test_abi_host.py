@@ -174,3 +174,25 @@ def test_round2_entry_validation_without_gpu(abi):
     assert abi.KEY_INIT_SIGNED == (1 << 63) - 1
     # the eval-args struct carries key_order at the end (include/distill.h, ABI 2)
     assert abi.EvalArgs._fields_[-1][0] == "key_order"
+
+
+def test_rng_entry_validation_without_gpu(abi):
+    """Rows a2/a3 on their own (distill_rng_*): NULL / misaligned buffers, empty
+    ranges, zero per-unit counts and index overflow are decided synchronously,
+    before any CUDA call (include/distill.h)."""
+    import ctypes as C
+    L = abi.lib()
+    ok, bad, ovf = 0, abi.E_INVALID_ARG, abi.E_OVERFLOW
+    assert L.distill_rng_rad(None, 0, None, None) == ok                  # empty: nothing enqueued
+    assert L.distill_rng_rad(None, 5, C.c_void_p(0x1000), None) == bad
+    assert L.distill_rng_rad(C.c_void_p(0x1002), 5, C.c_void_p(0x1000), None) == bad
+    assert "aligned" in L.distill_last_error().decode()
+    assert L.distill_rng_normals_acc(1, 0, 0, 12, None, None) == ok
+    assert L.distill_rng_normals_acc(1, 0, 4, 12, None, None) == bad
+    assert L.distill_rng_normals_acc(1, 0, 4, 0, C.c_void_p(0x1000), None) == bad
+    assert L.distill_rng_normals_acc(1, 0, 1 << 40, 1 << 30, C.c_void_p(0x1000), None) == ovf
+    assert L.distill_rng_normals_acc(1, (1 << 64) - 2, 4, 12, C.c_void_p(0x1000), None) == ovf
+    assert L.distill_rng_normals_pp(1, 0, 0, 10, 0, None, None) == ok
+    assert L.distill_rng_normals_pp(1, 0, 4, 0, 0, C.c_void_p(0x1000), None) == bad
+    assert L.distill_rng_normals_pp(1, 0xFFFFFFF0, 32, 10, 0, C.c_void_p(0x1000), None) == ovf
+    assert L.distill_rng_normals_pp(1, 0, 4, 10, 0, C.c_void_p(0x1001), None) == bad
