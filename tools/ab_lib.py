@@ -7,8 +7,8 @@ Each round loads every library in a fresh subprocess (one CUDA context per
 build, alternating A B A B ...) and times, with CUDA events on the launching
 stream: PP cfg3 (20 graph-replayed grid searches, median), DDM cfg2 (graph:
 zeroing + kernel, median of 5), a Stroop cfg4 slice (allocations [8000, 8100)
-x 1e5 trials, median of 3), Extended Stroop A and the DDM control grid (one
-pass each).  Every output array is hashed: the two builds must agree bit for
+x 1e5 trials, median of 3), Extended Stroop A, the DDM control grid and the
+whole cfg4 grid (one pass each).  Every output array is hashed: the two builds must agree bit for
 bit, so an A/B is only reported for equivalent code.
 """
 from __future__ import annotations
@@ -114,9 +114,10 @@ def child(lib_path: str) -> dict:
     out["stroop_slice_ms"] = statistics.median(ts)
     out["stroop_hash"] = h(snet, sbest, scounts)
 
-    # Extended Stroop A and the DDM control grid, whole grids, one pass each
+    # Extended Stroop A, the DDM control grid and the whole cfg4 grid, one timed pass each
     for name, cfg, kind in (("ext_stroop", W.ext_stroop_grid(), W.KIND_EXT_STROOP_A),
-                            ("ddm_grid", W.ddmg_grid(), W.KIND_DDM_GRID)):
+                            ("ddm_grid", W.ddmg_grid(), W.KIND_DDM_GRID),
+                            ("stroop_cfg4", W.stroop_cfg4(), W.KIND_STROOP_LCA)):
         mm = D.load_model(kind, cfg.n_levels, cfg.levels, cfg.w, cfg.params, device=0)
         xn = torch.empty(cfg.n_alloc, dtype=torch.float32, device=dev)
         xb = torch.empty(1, dtype=torch.int64, device=dev)
