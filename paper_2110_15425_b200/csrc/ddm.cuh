@@ -18,7 +18,9 @@ struct DDMArgs {
     float leak, offset;                        // LCI mode only (spec/MODELS.md §5; drift = input I)
     uint32_t n_steps, rt_bin_steps, n_rt_bins, n_x_bins;
     uint32_t key0, key1;
-    uint64_t trial_begin, n_trials;
+    uint64_t trial_begin, n_trials;            // one launch: all units share the high word unit_hi
+    uint32_t unit_hi;                          // (trial_begin + t) >> 32, the counter's c2 (uniform)
+    uint32_t c2_a1, c2_x1;                     // round 1 of c2: hi(M1 c2) ^ key0, lo(M1 c2) (host)
     unsigned long long* __restrict__ rt_hist;  // [2*nb+1]
     unsigned long long* __restrict__ rt_sum;   // [2]
     unsigned long long* __restrict__ x_hist;   // [nx+2]
@@ -48,36 +50,56 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
     const float z = a.threshold, nz = -a.threshold;
     unsigned long long sum_up = 0, sum_lo = 0;
 
-    for (uint64_t t = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; t < a.n_trials;
-         t += (uint64_t)gridDim.x * BLOCK) {
-        const uint64_t unit = a.trial_begin + t;
+    // Grid-stride over blocks of BLOCK consecutive trials with every lane
+    // stepping (a lane past the end walks the block's first trial again and
+    // records nothing), so the walk is warp-uniform control flow.
+    for (uint64_t base = (uint64_t)blockIdx.x * BLOCK; base < a.n_trials; base += (uint64_t)gridDim.x * BLOCK) {
+        const bool valid = base + threadIdx.x < a.n_trials;
+        const uint64_t t = valid ? base + threadIdx.x : base;
+        // c2 = the unit's high word, the same for every unit of the launch (the host
+        // splits a range at multiples of 2^32), and its round-1 product comes with
+        // the launch: with the uniform walk, a1 ^ k and its product M0 (a1 ^ k) for
+        // block k are warp-uniform and run on the uniform datapath (one IMAD.WIDE
+        // per Philox block fewer on the FMA pipe)
         PhiloxHoisted rng;
-        rng.init((uint32_t)unit, (uint32_t)(unit >> 32), 2u, a.key0, a.key1);
+        rng.init_c2((uint32_t)(a.trial_begin + t), a.c2_a1, a.c2_x1, 2u, a.key0, a.key1);
         float x = a.x0;
         uint32_t st = 0, ch = 2;
         // 12 steps per pair of sextet blocks.  Latch test: (x >= z) || (x <= -z)
         // <=> |x| >= z for every z and non-NaN x (NaN fails both), so one
         // max-|x| over the 12 states (ALU pipe) finds the group that holds the
-        // first passage; that rare group is resolved step by step in the spec's
-        // order.  The ragged last group is peeled.
+        // first passage.  The loop only records that group and the state it
+        // started from (selects, no branch: the walk stays warp-uniform, which
+        // keeps the uniform Philox product on the uniform datapath); after the
+        // walk the group's 12 steps are replayed from that state with the same
+        // normals and resolved step by step in the spec's order — the same
+        // values, so the same passage.  The ragged last group is peeled.
         const uint32_t n12 = a.n_steps / 12;
+        uint32_t jl = 0xFFFFFFFFu;   // the first group holding a passage (none yet)
+        float xl = 0.0f;             // the state entering it
         for (uint32_t j = 0; j < n12; ++j) {
             float g[12], xs[12];
             acc_normals12(rng, s_rt, j, g);
+            const float xin = x;
 #pragma unroll
             for (int l = 0; l < 12; ++l) { x = integ_step<LCI>(a, nsd, g[l], x); xs[l] = x; }
-            if (st == 0) {
-                float m = fabsf(xs[0]);
+            float m = fabsf(xs[0]);
 #pragma unroll
-                for (int l = 1; l < 12; ++l) m = fmaxf(m, fabsf(xs[l]));
-                if (m >= z) {
+            for (int l = 1; l < 12; ++l) m = fmaxf(m, fabsf(xs[l]));
+            const bool hit = (jl == 0xFFFFFFFFu) & (m >= z);
+            jl = hit ? j : jl;
+            xl = hit ? xin : xl;
+        }
+        if (jl != 0xFFFFFFFFu) {
+            float g[12];
+            acc_normals12(rng, s_rt, jl, g);
+            float xr = xl;
 #pragma unroll
-                    for (int l = 0; l < 12; ++l) {
-                        if (st == 0) {
-                            if (xs[l] >= z) { st = 12 * j + l + 1; ch = 0; }
-                            else if (xs[l] <= nz) { st = 12 * j + l + 1; ch = 1; }
-                        }
-                    }
+            for (int l = 0; l < 12; ++l) {
+                xr = integ_step<LCI>(a, nsd, g[l], xr);
+                if (st == 0) {
+                    if (xr >= z) { st = 12 * jl + l + 1; ch = 0; }
+                    else if (xr <= nz) { st = 12 * jl + l + 1; ch = 1; }
                 }
             }
         }
@@ -96,6 +118,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
                 }
             }
         }
+        if (!valid) continue;
         uint32_t rb;
         if (ch == 2) rb = 2 * a.n_rt_bins;
         else rb = ch * a.n_rt_bins + (st - 1) / a.rt_bin_steps;

@@ -939,14 +939,24 @@ static distill_status launch_integrator(const distill_ddm_args* a, float leak, f
     p.leak = leak; p.offset = offset;
     p.n_steps = a->n_steps; p.rt_bin_steps = a->rt_bin_steps; p.n_rt_bins = nb; p.n_x_bins = a->n_x_bins;
     p.key0 = (uint32_t)a->seed; p.key1 = (uint32_t)(a->seed >> 32);
-    p.trial_begin = a->trial_begin; p.n_trials = n;
     p.rt_hist = a->d_rt_hist; p.rt_sum = a->d_rt_sum; p.x_hist = a->d_x_hist;
     p.rad_tab = rt;
-    const uint64_t need = (n + DDM_BLOCK - 1) / DDM_BLOCK;
-    const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)n_sm * 1024);
-    ddm_batch_kernel<DDM_BLOCK, DDM_MINB, LCI><<<grid, DDM_BLOCK, smem, (cudaStream_t)stream>>>(p);
-    g_launches++;
-    CUDA_TRY(cudaGetLastError());
+    // one launch per 2^32-aligned segment of RNG units (one high word each)
+    for (uint64_t u = a->trial_begin; u < a->trial_end;) {
+        const uint64_t seg_end =
+            (u >> 32) == 0xFFFFFFFFull ? a->trial_end : std::min<uint64_t>(a->trial_end, ((u >> 32) + 1) << 32);
+        const uint64_t m = seg_end - u;
+        p.trial_begin = u; p.n_trials = m; p.unit_hi = (uint32_t)(u >> 32);
+        const uint64_t prod = (uint64_t)0xCD9E8D57u * p.unit_hi;   // Philox round 1: M1 * c2
+        p.c2_a1 = (uint32_t)(prod >> 32) ^ p.key0;
+        p.c2_x1 = (uint32_t)prod;
+        const uint64_t need = (m + DDM_BLOCK - 1) / DDM_BLOCK;
+        const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)n_sm * 1024);
+        ddm_batch_kernel<DDM_BLOCK, DDM_MINB, LCI><<<grid, DDM_BLOCK, smem, (cudaStream_t)stream>>>(p);
+        g_launches++;
+        CUDA_TRY(cudaGetLastError());
+        u = seg_end;
+    }
     return DISTILL_OK;
 }
 

@@ -245,6 +245,27 @@ struct PhiloxHoisted {
         c3k = G0h ^ (k1 + 2u * PHILOX_W1);               // z2 = c3k ^ y3
         z3 = G0l;
     }
+    // The same state when round 1's c2 product is already known: M1 * c2 = (hi1, lo1)
+    // given as a1 = hi1 ^ key0 and x1 = lo1 (launches whose units share c2 pass them
+    // as kernel parameters, so a1 ^ s and its product are warp-uniform).
+    __device__ __forceinline__ void init_c2(uint32_t c0, uint32_t a1_, uint32_t x1, uint32_t c3, uint32_t key0,
+                                            uint32_t key1) {
+        k0 = key0; k1 = key1;
+        uint32_t hi0, lo0;
+        mulhilo(PHILOX_M0, c0, hi0, lo0);
+        a1 = a1_;
+        const uint32_t x2 = hi0 ^ c3 ^ k1, x3 = lo0;
+        uint32_t H1, L1;
+        mulhilo(PHILOX_M1, x2, H1, L1);
+        const uint32_t y0 = H1 ^ x1 ^ (k0 + PHILOX_W0);
+        const uint32_t y1 = L1;
+        x3k = x3 ^ (k1 + PHILOX_W1);
+        uint32_t G0h, G0l;
+        mulhilo(PHILOX_M0, y0, G0h, G0l);
+        b_c1k = y1 ^ (k0 + 2u * PHILOX_W0);
+        c3k = G0h ^ (k1 + 2u * PHILOX_W1);
+        z3 = G0l;
+    }
     __device__ __forceinline__ uint4 operator()(uint32_t s) const {
         uint32_t P0h, P0l;
         mulhilo(PHILOX_M0, a1 ^ s, P0h, P0l);            // round 2: p0 = M0 * x0
