@@ -219,7 +219,11 @@ def _ddm_p(orc, d):
                                        ({"n_steps": 1}, 0, 100), ({"n_steps": 12, "threshold": 0.3}, 0, 3000),
                                        ({"n_steps": 23, "threshold": 0.4, "rt_bin_steps": 1}, 7, 2500),
                                        ({"n_steps": 24, "threshold": -0.5}, 0, 100),
-                                       ({"n_steps": 36, "threshold": 0.0, "noise": 0.01}, 0, 50)])
+                                       ({"n_steps": 36, "threshold": 0.0, "noise": 0.01}, 0, 50),
+                                       # RNG units across a multiple of 2^32 (the launch splits there: the
+                                       # counter's c2 word changes) and at the top of the 64-bit range
+                                       ({"n_steps": 120}, (1 << 32) - 700, (1 << 32) + 500),
+                                       ({"n_steps": 61, "threshold": 0.6}, (1 << 64) - 600, (1 << 64) - 1)])
 def test_ddm_histograms_bit_exact(D, orc, kw, t0, t1):
     import os
     d = W.DDMConfig(**kw)

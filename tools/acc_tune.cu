@@ -187,6 +187,7 @@ int main() {
     d.n_steps = 1000; d.rt_bin_steps = 10; d.n_rt_bins = 100; d.n_x_bins = 128;
     d.x_lo = 10.f - 6.f * 3.16227766f; d.x_hi = 10.f + 6.f * 3.16227766f;
     d.key0 = 42; d.key1 = 0; d.trial_begin = 0; d.n_trials = 1000000;
+    d.unit_hi = 0; d.c2_a1 = d.key0; d.c2_x1 = 0;   // Philox round 1 of c2 = 0: M1 * 0 = 0 (the library's host does this)
     const size_t n_all = 201 + 2 + 130;
     unsigned long long* buf; cudaMalloc(&buf, n_all * 8);
     d.rt_hist = buf; d.rt_sum = buf + 201; d.x_hist = buf + 203;
