@@ -69,6 +69,37 @@ def child(lib_path: str) -> dict:
     out["pp_cfg3_ms"] = statistics.median(ts)
     out["pp_hash"] = h(net, best)
 
+    # PP latency mode: the paper's PP-L (6^3 = 216 allocations) and a 40^3 grid (4-lane
+    # mode), 20 graph-replayed grid searches, device time per search in microseconds
+    for name, L in (("pp_L_us", 6), ("pp_40c_us", 40)):
+        cs = W.PPConfig(f"pp_{L}", (L, L, L), 100)
+        ms2 = D.load_model(W.KIND_PREDATOR_PREY, cs.n_levels, cs.levels, cs.w, cs.params, device=0)
+        n2 = torch.empty(cs.n_alloc, dtype=torch.float32, device=dev)
+        b2 = torch.empty(1, dtype=torch.int64, device=dev)
+
+        def small():
+            D.key_reset(b2)
+            D.eval_grid(ms2, cs.inputs, cs.n_samples, cs.seed, net=n2, best=b2)
+
+        small()
+        torch.cuda.synchronize()
+        g3 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g3):
+            for _ in range(20):
+                small()
+        g3.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            e0, e1 = ev()
+            e0.record()
+            g3.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3 / 20)
+        out[name] = statistics.median(ts)
+        out[name.replace("_us", "_hash")] = h(n2, b2)
+
     # DDM cfg2
     d = W.ddm_cfg2()
     hbuf = torch.zeros(sum(d.hist_sizes), dtype=torch.int64, device=dev)
@@ -154,7 +185,7 @@ def main():
                 print(p.stderr[-3000:])
                 return 1
             res[lib].append(json.loads(p.stdout.strip().splitlines()[-1]))
-    keys = [k for k in res[libs[0]][0] if k.endswith("_ms")]
+    keys = [k for k in res[libs[0]][0] if k.endswith("_ms") or k.endswith("_us")]
     print("build".ljust(28) + "".join(k.rjust(18) for k in keys))
     for lib in libs:
         row = [statistics.median(r[k] for r in res[lib]) for k in keys]
