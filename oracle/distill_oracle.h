@@ -20,21 +20,27 @@
  *                        small-noise delta-method expectation, fp64 re-evaluation
  *   od_argmax_keys       pinned: brute-force min over (C, i), NaN/-0 rules
  *   od_normal_acc        pinned: raw-word Box-Muller definition, moments/kurtosis/KS; cuRAND Philox
- *   od_ddm_*             pinned: zero-noise first passage, closed-form ER/DT, endpoint law
+ *   od_ddm_*             pinned: zero-noise first passage, closed-form ER/DT, endpoint law; the cfg2 RT
+ *                        histogram against the exact first-passage law of the Euler walk (tests/exact_law.py)
  *   od_lci_trial/_batch  pinned: Fig. 3 clone relation to od_ddm_* (bit-identical), AR(1) endpoint law
  *   od_stroop_eval       pinned: zero-noise deterministic RT, conservation, Stroop effect,
- *                        reflected-BM closed-form mean first passage of the noisy unit;
+ *                        reflected-BM closed-form mean first passage of the noisy unit; linear-recurrence,
+ *                        rectified-unit and AR(1) closed forms (leak != inhibition, tau < 1); at the cfg4
+ *                        constants the first-response law per kind and colour and the counts against the
+ *                        exact law of the rectified two-unit Euler process (tests/exact_law.py)
  *   od_stroop_energy     pinned: zero-noise closed form n^2 dt^2 I0 I1, congruent = 0, range additivity;
  *                        absolute values at the cfg4 constants parity unpinned (the paper prints none)
  *   od_ddmg_*            pinned: zero-noise binary32 passage step, Siegmund-corrected closed-form accuracy and
- *                        decision time per allocation, exact-rational value formula
+ *                        decision time per allocation, exact-rational value formula; counts at the
+ *                        grid's own horizon against the exact first-passage law
  *   od_pp_episode        pinned: closed-form straight-chase capture step, one-step predator capture,
  *                        per-step keys = ordinary grid searches
  *   od_argmax_random_ties pinned: uniform 1/8 frequency over 10^4 seeds, unique minimum wins
  *   od_pp_amr            pinned: zero-noise planted corner every round, Fig. 4 analogue vs a fine scan
  *   od_ext_stroop_*      pinned: A == B bit-identical, zero-noise drift signs / conflict
  *                        slowing / binary32 first passage, closed-form P(both correct) from the
- *                        two DDM error rates; absolute values at the bench constants parity unpinned
+ *                        two DDM error rates; at the bench constants both DDMs' first-passage laws
+ *                        and the counts against their exact laws (tests/exact_law.py)
  */
 #ifndef DISTILL_ORACLE_H
 #define DISTILL_ORACLE_H
