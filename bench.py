@@ -159,9 +159,20 @@ def oracle_rate(cfg: W.PPConfig, target_cpu_s: float = 15.0):
     oracle.pp_eval_threads(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, 0, n, cfg.n_samples,
                            cfg.seed, threads=cores)
     wall = time.perf_counter() - t
+    # single-thread figures: the slice timed above, and cfg1 whole (repeated ~0.5 s)
+    c1 = W.pp_cfg1()
+    reps, t = 0, time.perf_counter()
+    while reps == 0 or time.perf_counter() - t < 0.5:
+        oracle.pp_eval(c1.n_levels, c1.levels, c1.w, c1.params, c1.inputs, 0, c1.n_alloc, c1.n_samples, c1.seed)
+        reps += 1
+    t1 = (time.perf_counter() - t) / reps
+    single = {"cfg3_slice": {"value": cfg.n_samples / per_alloc, "unit": UNIT,
+                             "sample": f"{cfg.name}: allocations [0, 500) x {cfg.n_samples} samples, 1 thread"},
+              "cfg1": {"value": c1.evals / t1, "unit": UNIT, "ms": 1e3 * t1,
+                       "sample": f"{c1.name}: whole grid ({c1.n_alloc} x {c1.n_samples}), 1 thread, mean of {reps}"}}
     return {"value": n * cfg.n_samples / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{cfg.name}: allocations [0, {n}) x {cfg.n_samples} samples on {cores} threads "
-                      f"({wall:.2f} s wall)"}
+                      f"({wall:.2f} s wall)", "single_thread": single}
 
 
 def workload(world: int, args):

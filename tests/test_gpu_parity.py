@@ -1293,3 +1293,20 @@ def test_trial_streaming_edges_bit_exact(D, orc, model, case):
         assert cnt[:, 1].sum() == 0 and (cnt[:, 2] == (te - tb)).all()   # every trial decides at step 1
     if case == "never_latch":
         assert (cnt[:, 1] == (te - tb)).all()
+
+
+@pytest.mark.parametrize("b,e", [(1625 ** 3 - 600, 1625 ** 3), (2 ** 31 - 300, 2 ** 31 + 301),
+                                 (1625 ** 3 - 70_001, 1625 ** 3)])
+def test_pp_top_of_the_index_range(D, orc, b, e):
+    """The largest grid the packed key admits (reading R20: global index < 2^32):
+    1625^3 = 4.29e9 allocations; shards at the very top (latency-mode and
+    one-thread-per-allocation kernels) and across 2^31 — costs and the shard
+    key bit-exact against the oracle; a grid of 2^32 allocations is refused."""
+    cfg = W.PPConfig("pp_max", (1625, 1625, 1625), 6)
+    m = _model(D, cfg)
+    C, key = _gpu_pp(D, m, cfg, begin=b, end=e)
+    want = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, b, e, cfg.n_samples, cfg.seed)
+    assert np.array_equal(_bits(C), _bits(want))
+    assert key == orc.argmax_net(-want, b)[0]
+    with pytest.raises(D.api.DistillError):
+        _model(D, W.PPConfig("pp_too_big", (65536, 65536, 1), 6))
