@@ -127,7 +127,10 @@ constexpr uint32_t PP_SMALL_SMAX4 = 128;   // per-allocation buffer with 4 lanes
 #endif
 constexpr uint64_t PP_SMALL4_THREADS_PER_SM = DISTILL_PP_SMALL4_THREADS_PER_SM;
 constexpr int DDM_BLOCK = 128;
-constexpr int DDM_MINB = 6;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt, v5)
+#ifndef DISTILL_DDM_MINB
+#define DISTILL_DDM_MINB 6
+#endif
+constexpr int DDM_MINB = DISTILL_DDM_MINB;     // tools/acc_tune.cu sweep (profiles/r01_acc_tune.txt, v5)
 constexpr int STROOP_BLOCK = 128;
 constexpr int STROOP_MINB = 0;   // same sweep
 
@@ -328,14 +331,14 @@ static void launch_pp_search(const distill_model* m, const PPArgs& p, uint32_t n
         const bool even = (p.n_samples & 1u) == 0;
         constexpr int B = PP_BLOCK, MK = DISTILL_PP_MASK, MB = DISTILL_PP_MINB;
         if (n_invocations > 1) {
-            if (even) pp_eval_grid_kernel<B, MK, MB, false, true, true><<<grid, B, 0, st>>>(p);
-            else pp_eval_grid_kernel<B, MK, MB, false, false, true><<<grid, B, 0, st>>>(p);
+            if (even) pp_eval_grid_kernel<B, MK, MB, DISTILL_PP_PIPE, true, true><<<grid, B, 0, st>>>(p);
+            else pp_eval_grid_kernel<B, MK, MB, DISTILL_PP_PIPE, false, true><<<grid, B, 0, st>>>(p);
         } else if (p.publish) {
-            if (even) pp_eval_grid_kernel<B, MK, MB, false, true, false, true><<<grid, B, 0, st>>>(p);
-            else pp_eval_grid_kernel<B, MK, MB, false, false, false, true><<<grid, B, 0, st>>>(p);
+            if (even) pp_eval_grid_kernel<B, MK, MB, DISTILL_PP_PIPE, true, false, true><<<grid, B, 0, st>>>(p);
+            else pp_eval_grid_kernel<B, MK, MB, DISTILL_PP_PIPE, false, false, true><<<grid, B, 0, st>>>(p);
         } else {
-            if (even) pp_eval_grid_kernel<B, MK, MB, false, true><<<grid, B, 0, st>>>(p);
-            else pp_eval_grid_kernel<B, MK, MB><<<grid, B, 0, st>>>(p);
+            if (even) pp_eval_grid_kernel<B, MK, MB, DISTILL_PP_PIPE, true><<<grid, B, 0, st>>>(p);
+            else pp_eval_grid_kernel<B, MK, MB, DISTILL_PP_PIPE><<<grid, B, 0, st>>>(p);
         }
     }
     g_launches++;

@@ -114,8 +114,18 @@ enum : int {
 #ifndef DISTILL_PP_MASK
 #define DISTILL_PP_MASK 0
 #endif
+// Software pipelining of the sample loop (PIPE: the next pair's Philox blocks are
+// drawn while this pair's math runs) frees enough registers for 8 blocks of 128
+// per SM at 61 registers: cfg3 0.561 -> 0.549 ms, bit-identical (profiles/r02_ab_pipe.txt;
+// without the pipelining, 64 registers and 8 blocks are slower, 0.580 ms).
 #ifndef DISTILL_PP_MINB
-#define DISTILL_PP_MINB 7
+#define DISTILL_PP_MINB 8
+#endif
+#ifndef DISTILL_PP_PIPE
+#define DISTILL_PP_PIPE 1
+#endif
+#ifndef DISTILL_PP_UNROLL
+#define DISTILL_PP_UNROLL 1
 #endif
 
 // Full evaluation of allocation i (a1-a8): returns the cost C.
@@ -162,7 +172,7 @@ __device__ __forceinline__ F2 pp_pair_errors(const uint4& X, const uint4& Y, flo
 }
 
 // SMEM_LEV (tools/pp_tune.cu A/B only): `lev` is a shared-memory copy of the level table.
-template <int MASK, bool PIPE, bool EVEN = false, bool SMEM_LEV = false>
+template <int MASK, int PIPE, bool EVEN = false, bool SMEM_LEV = false>
 __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, float2 ustar,
                                                const float4* __restrict__ rt, const float* lev = nullptr) {
     constexpr bool SOBJ = MASK & PP_SC_OBJECTIVE;
@@ -189,6 +199,8 @@ __device__ __forceinline__ float pp_eval_alloc(const PPArgs& a, uint32_t i, floa
     float acc = 0.0f;
     uint4 Xn, Yn;
     if (PIPE) { Xn = rng(0); Yn = rng(1); }
+    constexpr int UNR = DISTILL_PP_UNROLL;
+#pragma unroll UNR
     for (uint32_t s = 0; s < a.n_samples; s += 2) {
         // a2: one Philox block per sample, two samples per iteration
         uint4 X, Y;
@@ -283,7 +295,7 @@ __global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs 
 }
 
 // One thread per allocation; one atomicMin per block.
-template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, bool PIPE = false, bool EVEN = false,
+template <int BLOCK, int MASK = DISTILL_PP_MASK, int MINB = DISTILL_PP_MINB, int PIPE = DISTILL_PP_PIPE, bool EVEN = false,
           bool MULTI = false, bool PUB = false>
 __global__ void __launch_bounds__(BLOCK, MINB) pp_eval_grid_kernel(const PPArgs a0) {
     if (a0.status_dev && *a0.status_dev != 0) return;   // episode already over (uniform branch)
