@@ -36,11 +36,6 @@ __device__ __forceinline__ float integ_step(const DDMArgs& a, float nsd, float g
     return __fmaf_rn(nsd, g, __fmaf_rn(a.dt, a.drift, x));
 }
 
-#ifndef DISTILL_DDM_PIPE
-#define DISTILL_DDM_PIPE 0
-#endif
-constexpr bool DDM_PIPE = DISTILL_DDM_PIPE;
-
 template <int BLOCK, int MINB = 0, bool LCI = false>
 __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a) {
     extern __shared__ uint32_t s_hist[];  // [2*nb+1] rt bins then [nx+2] x bins
@@ -82,17 +77,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
         const uint32_t n12 = a.n_steps / 12;
         uint32_t jl = 0xFFFFFFFFu;   // the first group holding a passage (none yet)
         float xl = 0.0f;             // the state entering it
-        uint4 Xn, Yn;                // DDM_PIPE: group j+1's Philox blocks, drawn during group j
-        if (DDM_PIPE) { Xn = rng(0u); Yn = rng(1u); }
         for (uint32_t j = 0; j < n12; ++j) {
             float g[12], xs[12];
-            if (DDM_PIPE) {
-                const uint4 X = Xn, Y = Yn;
-                Xn = rng(2 * j + 2); Yn = rng(2 * j + 3);
-                acc_normals12_xy(X, Y, s_rt, g);
-            } else {
-                acc_normals12(rng, s_rt, j, g);
-            }
+            acc_normals12(rng, s_rt, j, g);
             const float xin = x;
 #pragma unroll
             for (int l = 0; l < 12; ++l) { x = integ_step<LCI>(a, nsd, g[l], x); xs[l] = x; }

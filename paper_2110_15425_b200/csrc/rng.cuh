@@ -294,22 +294,6 @@ __device__ __forceinline__ void normal_sextet2_h(const PhiloxHoisted& rng, const
     }
 }
 
-// The same twelve normals from the two Philox blocks X = block 2j, Y = block 2j+1
-// already drawn (software-pipelined walks draw the next group's blocks early).
-__device__ __forceinline__ void acc_normals12_xy(const uint4& X, const uint4& Y, const float4* __restrict__ rt,
-                                                 float g[12]) {
-    const uint32_t RX[3] = {X.x, X.y, X.z}, RY[3] = {Y.x, Y.y, Y.z};
-#pragma unroll
-    for (int e = 0; e < 3; ++e) {
-        const uint32_t wx = sextet_angle_word(X, e), wy = sextet_angle_word(Y, e);
-        F2 rs, cq, sq;
-        bm_polar2_fs<false, 0x7FFF00u>(RX[e], RY[e], wx, wy, wx, wy, rt, rs, cq, sq);
-        const F2 zc = Ops<false>::mul(rs, cq), zs = Ops<false>::mul(rs, sq);
-        g[2 * e] = zc.x; g[2 * e + 1] = zs.x;
-        g[6 + 2 * e] = zc.y; g[6 + 2 * e + 1] = zs.y;
-    }
-}
-
 // Twelve stream-2 normals 12j..12j+11 as an array in stream order (blocks 2j, 2j+1).
 __device__ __forceinline__ void acc_normals12(const PhiloxHoisted& rng, const float4* __restrict__ rt, uint32_t j,
                                               float g[12]) {
