@@ -29,7 +29,8 @@
  *                        constants the first-response law per kind and colour and the counts against the
  *                        exact law of the rectified two-unit Euler process (tests/exact_law.py)
  *   od_stroop_energy     pinned: zero-noise closed form n^2 dt^2 I0 I1, congruent = 0, range additivity;
- *                        absolute values at the cfg4 constants parity unpinned (the paper prints none)
+ *                        with noise, the mean and variance per step of the Gaussian product x0 x1 in the
+ *                        linear (never rectified) regime, from the AR(1) moments of s = x0 + x1, d = x0 - x1
  *   od_ddmg_*            pinned: zero-noise binary32 passage step, Siegmund-corrected closed-form accuracy and
  *                        decision time per allocation, exact-rational value formula; counts at the
  *                        grid's own horizon against the exact first-passage law

@@ -437,3 +437,48 @@ def test_stroop_lca_noisy_ar1_moments(orc):
     a_w = 1 - _DT * (_BETA - _LAM)
     vw = 2 * nsd2 * (a_w ** (2 * m) - 1) / (a_w ** 2 - 1)
     assert abs(d[:, 99].var() / vw - 1) > 10 * math.sqrt(2.0 / n_units)
+
+
+def test_stroop_energy_noisy_gaussian_product_moments(orc):
+    """Decision energy with noise (spec/MODELS.md §6b), in the linear
+    regime of the AR(1) pin above (both units far from 0, theta out of reach):
+    x0 = (s + d)/2 and x1 = (s - d)/2 are jointly Gaussian with s, d independent,
+    so per step
+        m_k = E[x_k],  v = Var x0 = Var x1 = (Var s + Var d)/4,  c = Cov(x0, x1) = (Var s - Var d)/4,
+        E[x0 x1]   = m0 m1 + c,
+        Var(x0 x1) = m0^2 v + m1^2 v + 2 m0 m1 c + v^2 + c^2   (product of bivariate normals).
+    4000 single incongruent colour-0 trials (j = 1 mod 6), each its own energy
+    trace; the mean and the variance of llrint(x0 x1 2^24)/2^24 at steps 1 … 100
+    within 4.5 SE.  Power: a flipped inhibition sign, a swapped leak/inhibition
+    and x0^2 instead of x0 x1 miss the mean; 10 % more noise misses the variance."""
+    N, sig, tau = 100, 0.3, 0.9
+    gc, gw, uc, us = 8.0, 10.0, 1.0, 0.0
+    P = _stroop_params(gc, gw, tau, _LAM, _BETA, sig, _DT, 1e6, N)
+    n = 4000
+    T = 6 * n
+    E = np.stack([orc.stroop_energy(P, uc, us, 11, 0, T, 1 + 6 * k, 2 + 6 * k)
+                  for k in range(n)]).astype(np.float64) / 2 ** 24
+    nsd2 = float(np.float32(sig) * np.sqrt(np.float32(_DT))) ** 2
+    I0, I1, r = gc * uc, gw * (1 - us), 1 - tau
+
+    def moments(m, lam=_LAM, beta=_BETA, noise2=nsd2):
+        a_s, a_d = 1 - _DT * (lam + beta), 1 - _DT * (lam - beta)
+        ms, md = _DT * (I0 + I1) * _G(a_s, r, m), _DT * (I0 - I1) * _G(a_d, r, m)
+        vs = 2 * noise2 * (1 - a_s ** (2 * m)) / (1 - a_s ** 2)
+        vd = 2 * noise2 * (1 - a_d ** (2 * m)) / (1 - a_d ** 2)
+        m0, m1, v, c = (ms + md) / 2, (ms - md) / 2, (vs + vd) / 4, (vs - vd) / 4
+        return m0, m1, v, c, m0 * m1 + c, m0 ** 2 * v + m1 ** 2 * v + 2 * m0 * m1 * c + v * v + c * c
+
+    for k in (0, 4, 9, 39, 99):
+        m = k + 1
+        e = E[:, k]
+        m0, m1, v, c, mean, var = moments(m)
+        se_m = math.sqrt(var / n)
+        se_v = math.sqrt(max(np.mean((e - e.mean()) ** 4) - e.var() ** 2, 0.0) / n)
+        assert abs(e.mean() - mean) < 4.5 * se_m, (m, e.mean(), mean)
+        assert abs(e.var() - var) < 4.5 * se_v, (m, e.var(), var)
+        if m >= 40:
+            # power: each plausible slip is > 10 SE away
+            for wrong in (moments(m, beta=-_BETA)[4], moments(m, lam=_BETA, beta=_LAM)[4], m0 * m0 + v):
+                assert abs(e.mean() - wrong) > 10 * se_m, (m, wrong)
+            assert abs(e.var() - moments(m, noise2=1.21 * nsd2)[5]) > 6 * se_v
