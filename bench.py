@@ -124,6 +124,13 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
+def smi_device(local: int) -> str:
+    """nvidia-smi's -i for CUDA device `local`: the physical index (or UUID) that
+    CUDA_VISIBLE_DEVICES maps it to, else the index itself."""
+    ids = [x.strip() for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
+    return ids[local] if local < len(ids) else str(local)
+
+
 # ------------------------------------------------------------------ CPU oracle arm
 
 def host_cores() -> int:
@@ -358,7 +365,7 @@ def run_ours(args):
         graph_note = "eager steps (--no-graph or a non-NCCL backend)"
     barrier()
 
-    sampler = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
+    sampler = ClockSampler(smi_device(local))
     sampler.start()
     time.sleep(0.3)
     K = args.steps
