@@ -33,4 +33,4 @@ sanitize-oracle:
 	ASAN_OPTIONS=detect_leaks=0:halt_on_error=1 UBSAN_OPTIONS=print_stacktrace=1:halt_on_error=1 \
 	python -m pytest tests/test_oracle_rng.py tests/test_oracle_pp.py tests/test_oracle_argmax.py \
 	    tests/test_oracle_ddm_lca.py tests/test_oracle_episode.py tests/test_oracle_amr.py \
-	    tests/test_oracle_ext_stroop.py -q -p no:cacheprovider
+	    tests/test_oracle_ext_stroop.py tests/test_oracle_exact_law.py -q -p no:cacheprovider
