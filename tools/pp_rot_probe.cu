@@ -325,6 +325,79 @@ __global__ void __launch_bounds__(1024, 1) persist_v2_kernel(const PPArgs a, con
     block_min_key_atomic<1024>(key, a.best);
 }
 
+
+// ---- v3 (timing prototype of a counter-layout change, NOT the spec): stream-1 counter
+// (c0, c1, c2, c3) = (U0, i, U2, s) with U0, U2 launch-uniform.  The allocation i enters
+// round 1 through the XOR into x0 and the sample s through the XOR into x2, so round 2's
+// M0*x0 and round 3's M1*y2 are per-thread and sample-invariant (hoisted), and round 2's
+// M1*x2 and round 3's M0*y0 are warp-uniform (uniform datapath): 14 per-thread IMAD.WIDE
+// per block (rounds 4-10) instead of 15.
+struct PhiloxL2 {
+    uint32_t x1, x2b, Bh, Bl, y3, k0, k1;
+    __device__ __forceinline__ void init(uint32_t U0, uint32_t i, uint32_t U2, uint32_t key0, uint32_t key1) {
+        k0 = key0; k1 = key1;
+        uint32_t h0, l0, h1, l1;
+        mulhilo(PHILOX_M0, U0, h0, l0);
+        mulhilo(PHILOX_M1, U2, h1, l1);
+        const uint32_t x0 = h1 ^ i ^ k0;
+        x1 = l1;
+        x2b = h0 ^ k1;
+        const uint32_t x3 = l0;
+        uint32_t Ah, Al;
+        mulhilo(PHILOX_M0, x0, Ah, Al);
+        const uint32_t y2 = Ah ^ x3 ^ (k1 + PHILOX_W1);
+        y3 = Al;
+        mulhilo(PHILOX_M1, y2, Bh, Bl);
+    }
+    __device__ __forceinline__ uint4 operator()(uint32_t s) const {
+        uint32_t Ch, Cl, Dh, Dl;
+        mulhilo(PHILOX_M1, x2b ^ s, Ch, Cl);
+        const uint32_t y0 = Ch ^ x1 ^ (k0 + PHILOX_W0);
+        mulhilo(PHILOX_M0, y0, Dh, Dl);
+        const uint4 c = make_uint4(Bh ^ Cl ^ (k0 + 2u * PHILOX_W0), Bl, Dh ^ y3 ^ (k1 + 2u * PHILOX_W1), Dl);
+        return philox_from<3>(c, k0, k1);
+    }
+};
+
+template <int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) layout2_kernel(const PPArgs a) {
+    __shared__ float4 s_rt[RT_ROWS];
+    stage_rad_table_async<BLOCK>(s_rt, a.rad_tab);
+    const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
+    const float2 ustar = pp_ustar_block(a);
+    key64_t key = KEY_INIT;
+    float C = 0.0f;
+    if (tid < a.count) {
+        const uint32_t i = a.begin + tid;
+        const uint32_t k2 = i % a.L2, r = i / a.L2;
+        const uint32_t k1 = r % a.L1, k0 = r / a.L1;
+        const float a0 = __ldg(a.levels + k0), a1 = __ldg(a.levels + a.L0 + k1);
+        const float a2 = __ldg(a.levels + a.L0 + a.L1 + k2);
+        const float dsig = __fadd_rn(a.sigma_min, -a.sigma_max);
+        const float s0 = __fmaf_rn(a0, dsig, a.sigma_max), s1 = __fmaf_rn(a1, dsig, a.sigma_max);
+        const float s2 = __fmaf_rn(a2, dsig, a.sigma_max);
+        const float K = __fmaf_rn(a.w2, a2, __fmaf_rn(a.w1, a1, __fmul_rn(a.w0, a0)));
+        const V2 P0 = {bc(a.prey_x), bc(a.prey_y)}, P1 = {bc(a.pred_x), bc(a.pred_y)};
+        const V2 P2 = {bc(a.pl_x), bc(a.pl_y)};
+        const V2 us = {bc(ustar.x), bc(ustar.y)};
+        PhiloxL2 rng;
+        rng.init(a.invocation, i, 0x80000001u, a.key0, a.key1);
+        float acc = 0.0f;
+        uint4 Xn = rng(0), Yn = rng(1);
+        for (uint32_t s = 0; s < a.n_samples; s += 2) {
+            const uint4 X = Xn, Y = Yn;
+            Xn = rng(s + 2); Yn = rng(s + 3);
+            const F2 e = pp_pair_errors<false, false>(X, Y, s0, s1, s2, P0, P1, P2, bc(-a.kappa), us, s_rt);
+            acc = __fadd_rn(acc, e.x);
+            acc = __fadd_rn(acc, e.y);
+        }
+        C = __fadd_rn(__fdiv_rn(acc, __uint2float_rn(a.n_samples)), K);
+        key = make_key(C, i);
+    }
+    if (tid < a.count) a.net[tid] = -C;
+    block_min_key_atomic<BLOCK>(key, a.best);
+}
+
 static unsigned int* g_counter = nullptr;
 
 template <typename F>
@@ -428,6 +501,15 @@ int main() {
     run_persist<false, true, true>("P rotRep", a, g1r, ref, rk, nsm);
     run_persist<true, true, false>("P repR rot", a, g8, ref, rk, nsm);
     run_persist<true, true, true>("P repR rotRep", a, g8r, ref, rk, nsm);
+    {
+        const unsigned g128 = (a.count + 127) / 128;
+        float ms = time_it(a, [&] { layout2_kernel<128, 8><<<g128, 128>>>(a); });
+        report("L2 counter layout b128x8", a, ms, regs_of(layout2_kernel<128, 8>), ref, rk);
+        ms = time_it(a, [&] { layout2_kernel<128, 7><<<g128, 128>>>(a); });
+        report("L2 counter layout b128x7", a, ms, regs_of(layout2_kernel<128, 7>), ref, rk);
+        ms = time_it(a, [&] { pp_eval_grid_kernel<128, 0, 8, 1, true><<<g128, 128>>>(a); });
+        report("ref again", a, ms, regs_of(pp_eval_grid_kernel<128, 0, 8, 1, true>), ref, rk);
+    }
     {
         auto k1 = persist_v2_kernel<true>;
         auto k0 = persist_v2_kernel<false>;
