@@ -398,6 +398,29 @@ __global__ void __launch_bounds__(BLOCK, MINB) layout2_kernel(const PPArgs a) {
     block_min_key_atomic<BLOCK>(key, a.best);
 }
 
+
+// ---- v4: the shipped kernel without the end-of-block barrier: each warp reduces its 32
+// keys with shuffles and issues its own atomicMin (4 atomics per block instead of 1), so
+// a warp that finishes its allocations leaves at once instead of waiting at a barrier
+// for the block's slowest warp (ncu: barrier stall 1.7 per issue in the shipped kernel).
+template <int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) nobar_kernel(const PPArgs a) {
+    __shared__ float4 s_rt[RT_ROWS];
+    stage_rad_table_async<BLOCK>(s_rt, a.rad_tab);
+    const uint32_t tid = blockIdx.x * BLOCK + threadIdx.x;
+    const float2 ustar = pp_ustar_block(a);
+    key64_t key = KEY_INIT;
+    float C = 0.0f;
+    if (tid < a.count) {
+        const uint32_t i = a.begin + tid;
+        C = pp_eval_alloc<0, 1, true>(a, i, ustar, s_rt);
+        key = make_key(C, i);
+    }
+    if (tid < a.count) a.net[tid] = -C;
+    key = warp_min_key(key);
+    if ((threadIdx.x & 31u) == 0 && key != KEY_INIT) atomicMin(a.best, key);
+}
+
 static unsigned int* g_counter = nullptr;
 
 template <typename F>
@@ -507,6 +530,12 @@ int main() {
         report("L2 counter layout b128x8", a, ms, regs_of(layout2_kernel<128, 8>), ref, rk);
         ms = time_it(a, [&] { layout2_kernel<128, 7><<<g128, 128>>>(a); });
         report("L2 counter layout b128x7", a, ms, regs_of(layout2_kernel<128, 7>), ref, rk);
+        ms = time_it(a, [&] { nobar_kernel<128, 8><<<g128, 128>>>(a); });
+        report("noBar b128x8", a, ms, regs_of(nobar_kernel<128, 8>), ref, rk);
+        ms = time_it(a, [&] { nobar_kernel<256, 4><<<(a.count + 255) / 256, 256>>>(a); });
+        report("noBar b256x4", a, ms, regs_of(nobar_kernel<256, 4>), ref, rk);
+        ms = time_it(a, [&] { nobar_kernel<64, 16><<<(a.count + 63) / 64, 64>>>(a); });
+        report("noBar b64x16", a, ms, regs_of(nobar_kernel<64, 16>), ref, rk);
         ms = time_it(a, [&] { pp_eval_grid_kernel<128, 0, 8, 1, true><<<g128, 128>>>(a); });
         report("ref again", a, ms, regs_of(pp_eval_grid_kernel<128, 0, 8, 1, true>), ref, rk);
     }
