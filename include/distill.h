@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define DISTILL_ABI_VERSION 2   /* 2: distill_eval_args.key_order, distill_key_reset_signed */
+#define DISTILL_ABI_VERSION 3   /* 2: distill_eval_args.key_order, distill_key_reset_signed; 3: distill_eval_grid_host_async */
 
 typedef enum {
     DISTILL_OK = 0,
@@ -243,6 +243,20 @@ distill_status distill_eval_grid_host(const distill_model* model, const float* h
                                       uint64_t begin, uint64_t end, uint32_t n_samples,
                                       uint32_t invocation, uint64_t seed,
                                       float* h_net, unsigned long long* h_best, void* stream);
+
+/* The same end-to-end call without the final synchronisation, for callers that keep
+ * several grid searches in flight (double-buffered host slots): the work is enqueued on
+ * `stream` and the call returns.  h_best and h_net (if non-NULL) must be pinned,
+ * device-mapped host memory (cudaHostAlloc / page-locked; 8- and 4-byte aligned), else
+ * DISTILL_E_INVALID_ARG and nothing is enqueued; they hold the key and V once `stream`
+ * has completed the call's work (synchronise the stream or an event recorded on it after
+ * the call) and must not be reused by another call before that.  The positions are
+ * copied at the call (launch parameters).  Host-buffer calls on one handle run in call
+ * order whatever their streams (each waits for the previous one's kernel). */
+distill_status distill_eval_grid_host_async(const distill_model* model, const float* h_inputs, uint32_t n_inputs,
+                                            uint64_t begin, uint64_t end, uint32_t n_samples,
+                                            uint32_t invocation, uint64_t seed,
+                                            float* h_net, unsigned long long* h_best, void* stream);
 
 /* argmax over a device array of net values: atomicMin of key(-d_values[j], index_base + j)
  * into *d_best (max V <=> min key, lowest index on ties). */

@@ -7,6 +7,7 @@ Public Python API (thin wrappers over the C ABI in include/distill.h):
     best(key, group=None) -> (cost, index)        # all-reduce across ranks + decode
     eval_grid(model, inputs, n_samples, seed, begin=0, end=None, net=None, best=None, ...)
     eval_grid_host(model, inputs, n_samples, seed, ...)   # host buffers, end to end
+    eval_grid_host_async(model, inputs, ..., net_out=, key_out=)   # the same, enqueue only (pinned slots)
     eval_grid_multi(model, d_inputs, n_invocations, n_samples, seed, ...)   # many invocations, one launch
     argmax(values, index_base, best) / argmax_ties(values, base, seed, t, best, tie)
     key_reset(best) / key_decode(key)
@@ -24,12 +25,12 @@ control grid (workloads.KIND_*); eval_grid evaluates any of them.
 Importing this package does not touch the GPU; the shared library is loaded
 on first use and there is no CPU fallback.
 """
-from .api import (KEY_INIT, key_from_tensor, AmrRun, EpisodeRun, Model, best, grid_search, stroop_energy, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_multi, key_decode,
+from .api import (KEY_INIT, key_from_tensor, AmrRun, EpisodeRun, Model, best, grid_search, stroop_energy, argmax, argmax_ties, ddm_batch, eval_grid, eval_grid_host, eval_grid_host_async, eval_grid_multi, key_decode,
                   key_reset, launch_count, load_model, pp_amr, pp_episode, rng_normals_acc, rng_normals_pp, rng_rad)
 from .dist import (best_allreduce, hist_allreduce, key_to_i64, i64_to_key, pp_amr_sharded, pp_episode_sharded,
                    shard_range)
 
-__all__ = ["KEY_INIT", "key_from_tensor", "Model", "best", "grid_search", "stroop_energy", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "eval_grid_multi", "key_decode", "pp_episode", "pp_amr",
+__all__ = ["KEY_INIT", "key_from_tensor", "Model", "best", "grid_search", "stroop_energy", "argmax", "argmax_ties", "ddm_batch", "eval_grid", "eval_grid_host", "eval_grid_host_async", "eval_grid_multi", "key_decode", "pp_episode", "pp_amr",
            "key_reset", "launch_count", "load_model", "best_allreduce", "hist_allreduce", "key_to_i64",
            "i64_to_key", "shard_range", "pp_episode_sharded", "EpisodeRun", "pp_amr_sharded", "AmrRun",
            "rng_rad", "rng_normals_acc", "rng_normals_pp"]

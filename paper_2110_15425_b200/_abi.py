@@ -18,7 +18,7 @@ MODEL_PREDATOR_PREY = 1
 MODEL_STROOP_LCA = 2
 KEY_INIT = 0xFFFFFFFFFFFFFFFF
 KEY_INIT_SIGNED = 0x7FFFFFFFFFFFFFFF      # signed key order: stored word = key ^ 2^63
-ABI_VERSION = 2                           # include/distill.h DISTILL_ABI_VERSION
+ABI_VERSION = 3                           # include/distill.h DISTILL_ABI_VERSION
 
 
 class DistillError(RuntimeError):
@@ -82,6 +82,9 @@ EXPORTS = {
     "distill_eval_grid_host": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_uint32, C.c_uint64, C.c_uint64,
                                          C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p,
                                          C.POINTER(C.c_uint64), C.c_void_p]),
+    "distill_eval_grid_host_async": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_uint32, C.c_uint64,
+                                               C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p,
+                                               C.c_void_p, C.c_void_p]),
     "distill_argmax": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
     "distill_argmax_ties": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p,
                                       C.c_void_p, C.c_void_p]),

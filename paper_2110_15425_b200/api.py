@@ -217,6 +217,29 @@ def eval_grid_host(model: Model, inputs, n_samples: int, seed: int, begin: int =
         return int(model._h_key_np[0]) & (2 ** 64 - 1)
 
 
+def eval_grid_host_async(model: Model, inputs, n_samples: int, seed: int, begin: int = 0,
+                         end: Optional[int] = None, net_out: Optional[np.ndarray] = None, key_out=None,
+                         invocation: int = 0, stream=None) -> None:
+    """distill_eval_grid_host_async: the end-to-end call without the final synchronisation.
+    net_out (optional) and key_out (>= 1 int64 element) must be pinned host memory (e.g. the
+    .numpy() view of a torch pin_memory tensor); they hold V and the raw key bits once
+    `stream` has passed the call (record an event after it and wait for that).  Keep two
+    sets of slots to have the next grid search in flight while reading this one."""
+    end = model.n_alloc if end is None else int(end)
+    inp = np.ascontiguousarray(np.asarray(inputs, np.float32).reshape(-1))
+    if key_out is None or key_out.dtype != np.int64 or not key_out.flags.c_contiguous or key_out.size < 1:
+        raise ValueError("key_out must be a contiguous int64 array (pinned) of at least one element")
+    net_ptr = None
+    if net_out is not None:
+        if net_out.dtype != np.float32 or not net_out.flags.c_contiguous or net_out.size < end - begin:
+            raise ValueError("net_out must be a contiguous float32 array of end-begin elements")
+        net_ptr = net_out.ctypes.data
+    check(lib().distill_eval_grid_host_async(model.handle, _abi._fptr(inp) if inp.size else None, inp.size,
+                                             int(begin), end, int(n_samples), int(invocation),
+                                             int(seed) & (2 ** 64 - 1), net_ptr, key_out.ctypes.data,
+                                             _stream_handle(stream, model.device)))
+
+
 def stroop_energy(model: Model, alloc: int, n_trials: int, seed: int, trial_range=None, esum=None, stream=None):
     """distill_stroop_energy: per-step sums of llrint(x0·x1·2^24) over the trials of
     one Stroop-LCA allocation (int64 CUDA tensor [N], accumulated; zeroed if allocated here)."""

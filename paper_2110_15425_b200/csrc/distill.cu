@@ -150,6 +150,9 @@ struct distill_model {
     std::mutex scratch_mu;
     void* d_scratch = nullptr;
     size_t scratch_bytes = 0;
+    // completion of the last host-buffer launch (any stream): the next one waits for it,
+    // so launches sharing the scratch key/counter never overlap (the async entry)
+    cudaEvent_t host_ev = nullptr;
 };
 
 // Scratch layout (eval_grid_host): [0, 8) published-path key (kept at KEY_INIT
@@ -257,6 +260,7 @@ void distill_free_model(distill_model* m) {
     DeviceScope scope(m->device);
     if (m->d_levels) cudaFree(m->d_levels);
     if (m->d_scratch) cudaFree(m->d_scratch);
+    if (m->host_ev) cudaEventDestroy(m->host_ev);
     delete m;
 }
 
@@ -581,9 +585,13 @@ distill_status distill_eval_grid(const distill_model* mc, const distill_eval_arg
     return launch_ext_stroop(m, a, st);
 }
 
-distill_status distill_eval_grid_host(const distill_model* mc, const float* h_inputs, uint32_t n_inputs,
-                                      uint64_t begin, uint64_t end, uint32_t n_samples, uint32_t invocation,
-                                      uint64_t seed, float* h_net, unsigned long long* h_best, void* stream) {
+// The host-buffer entries: `sync` = distill_eval_grid_host (synchronises the stream;
+// pageable buffers allowed), !sync = distill_eval_grid_host_async (enqueue only;
+// pinned, device-mapped buffers required).
+static distill_status eval_grid_host_impl(const distill_model* mc, const float* h_inputs, uint32_t n_inputs,
+                                          uint64_t begin, uint64_t end, uint32_t n_samples, uint32_t invocation,
+                                          uint64_t seed, float* h_net, unsigned long long* h_best, void* stream,
+                                          bool sync) {
     if (!mc || !h_best) return fail(DISTILL_E_INVALID_ARG, "eval_grid_host: NULL model/h_best");
     distill_model* m = const_cast<distill_model*>(mc);
     if (m->kind != DISTILL_MODEL_PREDATOR_PREY)
@@ -626,6 +634,12 @@ distill_status distill_eval_grid_host(const distill_model* mc, const float* h_in
     // Host->device: this step's inputs (the 6 positions, 24 B) travel inside the
     // kernel's launch parameters; device->host: V (if h_net) and the best key.
     if (!h_inputs || n_inputs != 6) return fail(DISTILL_E_INVALID_ARG, "eval_grid_host: needs 6 inputs");
+    if (!sync && (!publish || (h_net && !direct)))
+        return fail(DISTILL_E_INVALID_ARG, "eval_grid_host_async: h_net and h_best must be pinned, device-mapped "
+                                           "host memory (4- and 8-byte aligned)");
+    // order after the previous host-buffer launch of this handle (it may be in flight on another stream)
+    if (!m->host_ev) CUDA_TRY(cudaEventCreateWithFlags(&m->host_ev, cudaEventDisableTiming));
+    else CUDA_TRY(cudaStreamWaitEvent(st, m->host_ev, 0));
     distill_eval_args a;
     memset(&a, 0, sizeof a);
     a.inputs = h_inputs; a.n_inputs = n_inputs; a.begin = begin; a.end = end;
@@ -645,8 +659,23 @@ distill_status distill_eval_grid_host(const distill_model* mc, const float* h_in
         if (h_net && !direct) CUDA_TRY(cudaMemcpyAsync(h_net, d_net, count * sizeof(float), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaMemcpyAsync(h_best, d_best, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     }
-    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaEventRecord(m->host_ev, st));
+    if (sync) CUDA_TRY(cudaStreamSynchronize(st));
     return DISTILL_OK;
+}
+
+distill_status distill_eval_grid_host(const distill_model* mc, const float* h_inputs, uint32_t n_inputs,
+                                      uint64_t begin, uint64_t end, uint32_t n_samples, uint32_t invocation,
+                                      uint64_t seed, float* h_net, unsigned long long* h_best, void* stream) {
+    return eval_grid_host_impl(mc, h_inputs, n_inputs, begin, end, n_samples, invocation, seed, h_net, h_best,
+                               stream, true);
+}
+
+distill_status distill_eval_grid_host_async(const distill_model* mc, const float* h_inputs, uint32_t n_inputs,
+                                            uint64_t begin, uint64_t end, uint32_t n_samples, uint32_t invocation,
+                                            uint64_t seed, float* h_net, unsigned long long* h_best, void* stream) {
+    return eval_grid_host_impl(mc, h_inputs, n_inputs, begin, end, n_samples, invocation, seed, h_net, h_best,
+                               stream, false);
 }
 
 static distill_status episode_check(const distill_model* m, const distill_episode_args* e, const char* who) {

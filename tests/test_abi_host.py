@@ -170,7 +170,7 @@ def test_round2_entry_validation_without_gpu(abi):
                     C.c_void_p(0x1004), C.c_void_p(0x2000), C.c_void_p(0x3000))
     assert L.distill_ddm_batch(C.byref(a), None) == abi.E_INVALID_ARG
     assert "aligned" in L.distill_last_error().decode()
-    assert abi.ABI_VERSION == L.distill_abi_version() == 2
+    assert abi.ABI_VERSION == L.distill_abi_version() == 3
     assert abi.KEY_INIT_SIGNED == (1 << 63) - 1
     # the eval-args struct carries key_order at the end (include/distill.h, ABI 2)
     assert abi.EvalArgs._fields_[-1][0] == "key_order"

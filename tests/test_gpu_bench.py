@@ -37,6 +37,9 @@ def test_bench_json_contract_on_gpu():
     e = d["e2e"]
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] >= 4 * per_gpu
     assert 0 < e["value"] <= d["value"] * 1.05
+    # the pipelined host-buffer calls (distill_eval_grid_host_async) each returned the step's key;
+    # the one-call-per-step synchronous figure is reported beside it
+    assert e["keys_match_step"] is True and 0 < e["sync"]["value"] <= e["value"] * 1.05
     assert d["gpu_launches"] == d["steps"]                 # one fused kernel per step
     assert d["clocks"]["sm_max_mhz"] > 0
     # the best allocation of the timed grid search decodes inside the grid, and the

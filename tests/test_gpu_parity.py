@@ -670,6 +670,53 @@ def test_eval_grid_host_published_key_rearms_between_calls(D, orc):
             assert got == k_or, (rep, seed, b, e, S)
 
 
+def test_eval_grid_host_async_pipelined_slots(D, orc):
+    """distill_eval_grid_host_async: several grid searches in flight at once on
+    double-buffered pinned slots (other seeds, ranges and sample parities), first on
+    one stream, then alternating between two streams (the handle orders its
+    host-buffer launches across streams): every net array and key bit-exact
+    against the oracle, a call's slots untouched by the calls after it; pageable
+    slots are refused with E_INVALID_ARG and nothing is enqueued."""
+    import torch
+    from paper_2110_15425_b200 import _abi
+    cfg = W.PPConfig("ha", (9, 8, 7), 6)
+    m = _model(D, cfg)
+    calls = [(11, 0, cfg.n_alloc, 6), (3, 100, 300, 7), (42, 200, cfg.n_alloc, 5), (99, 7, 8, 2),
+             (11, 0, cfg.n_alloc, 6), (5, 1, cfg.n_alloc - 1, 9)]
+    wants = []
+    for seed, b, e, S in calls:
+        w = orc.pp_eval(cfg.n_levels, cfg.levels, cfg.w, cfg.params, cfg.inputs, b, e, S, seed)
+        wants.append((w, orc.argmax_net(-w, b)[0]))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for mode in ("one stream", "two streams"):
+        slots = [(torch.full((cfg.n_alloc,), float("nan"), dtype=torch.float32, pin_memory=True).numpy(),
+                  torch.zeros(1, dtype=torch.int64, pin_memory=True).numpy()) for _ in calls]
+        evs = []
+        for q, (seed, b, e, S) in enumerate(calls):      # all enqueued before any is read
+            st = streams[0] if mode == "one stream" else streams[q % 2]
+            net, key = slots[q]
+            D.eval_grid_host_async(m, cfg.inputs, S, seed, b, e, net_out=net[:e - b], key_out=key, stream=st)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            evs.append(ev)
+        for q, (seed, b, e, S) in enumerate(calls):
+            evs[q].synchronize()
+            net, key = slots[q]
+            w, k_or = wants[q]
+            assert int(key[0]) & (2 ** 64 - 1) == k_or, (mode, q)
+            assert np.array_equal(_bits(-net[:e - b]), _bits(w)), (mode, q)
+            assert np.isnan(net[e - b:]).all()
+    # pageable slots: refused before anything is enqueued
+    with pytest.raises(_abi.DistillError):
+        D.eval_grid_host_async(m, cfg.inputs, 6, 11, 0, cfg.n_alloc, key_out=np.zeros(1, np.int64))
+    pk = torch.zeros(1, dtype=torch.int64, pin_memory=True).numpy()
+    with pytest.raises(_abi.DistillError):
+        D.eval_grid_host_async(m, cfg.inputs, 6, 11, 0, cfg.n_alloc, net_out=np.empty(cfg.n_alloc, np.float32),
+                               key_out=pk)
+    # and the synchronous call still works right after
+    assert D.eval_grid_host(m, cfg.inputs, 6, 11, 0, cfg.n_alloc) == wants[0][1]
+
+
 def test_pp_episode_in_pieces_over_shards(D, orc):
     """NEXT-1 over a sharded grid, emulated in one process: per step, three shard
     searches atomicMin into keys[t] (the MIN all-reduce), then advance — every
