@@ -75,6 +75,10 @@ def test_null_arguments_rejected(abi):
     assert L.distill_eval_grid(None, None, None) == abi.E_INVALID_ARG
     assert L.distill_ddm_batch(None, None) == abi.E_INVALID_ARG
     assert L.distill_argmax(None, 10, 0, None, None) == abi.E_INVALID_ARG
+    k = C.c_uint64()
+    for fn in (L.distill_eval_grid_host, L.distill_eval_grid_host_async):
+        assert fn(None, None, 6, 0, 1, 1, 0, 0, None, C.byref(k), None) == abi.E_INVALID_ARG
+        assert "NULL" in L.distill_last_error().decode()
     L.distill_free_model(None)  # NULL-safe
 
 
