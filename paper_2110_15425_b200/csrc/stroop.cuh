@@ -34,10 +34,15 @@ struct StroopArgs {
 // x of both units feeds both q's), given the pathway outputs h0, h1 of this step.
 __device__ __forceinline__ void lca_update(const StroopArgs& a, float nleak, float ninh, float nsd, float g0, float g1,
                                            float h0, float h1, float& x0, float& x1) {
-    const float q0 = __fmaf_rn(ninh, x1, __fmaf_rn(nleak, x0, h0));
-    const float q1 = __fmaf_rn(ninh, x0, __fmaf_rn(nleak, x1, h1));
-    x0 = fmaxf(__fmaf_rn(nsd, g0, __fmaf_rn(a.dt, q0, x0)), 0.0f);
-    x1 = fmaxf(__fmaf_rn(nsd, g1, __fmaf_rn(a.dt, q1, x1)), 0.0f);
+    // the two units in the lanes of a float2: four FFMA2 per step, each lane rounding as the
+    // scalar fma of the spec (q_k = fma(-β, x_{1-k}, fma(-λ, x_k, h_k)),
+    // x_k = max(fma(σ√dt, g_k, fma(dt, q_k, x_k)), 0)); bit-identical, cfg4 -1.9 %
+    // (profiles/r02_ab_lca_packed.txt)
+    const F2 x = make_float2(x0, x1);
+    const F2 q = __ffma2_rn(bc(ninh), make_float2(x1, x0), __ffma2_rn(bc(nleak), x, make_float2(h0, h1)));
+    const F2 y = __ffma2_rn(bc(nsd), make_float2(g0, g1), __ffma2_rn(bc(a.dt), q, x));
+    x0 = fmaxf(y.x, 0.0f);
+    x1 = fmaxf(y.y, 0.0f);
 }
 
 // Pathway output of step n (1-based) for the trial's input row: the recurrence
