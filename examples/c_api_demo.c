@@ -3,7 +3,7 @@
  *
  *   gcc -O2 -I include examples/c_api_demo.c -L paper_2110_15425_b200 -ldistill \
  *       -L /usr/local/cuda/lib64 -lcudart -Wl,-rpath,paper_2110_15425_b200 -o c_api_demo
- *   ./c_api_demo          # prints the 27 net values and the best allocation
+ *   ./c_api_demo          # prints the 27 net values, the host-buffer calls' keys and the best allocation
  *
  * Device buffers come from the CUDA runtime; the library only owns the model. */
 #include <stdio.h>
@@ -54,6 +54,29 @@ int main(void) {
     uint64_t idx = 0;
     CHECK(distill_key_decode(key, &cost, &idx));
     for (uint64_t i = 0; i < n; ++i) printf("%llu %a\n", (unsigned long long)i, -net[i]);
+
+    /* The same search from host buffers: the synchronous end-to-end call, then two
+     * calls in flight at once on two pinned slots (distill_eval_grid_host_async,
+     * results valid once the stream has passed them). */
+    float* h_net[2] = {NULL, NULL};
+    unsigned long long* h_key[2] = {NULL, NULL};
+    for (int q = 0; q < 2; ++q)
+        if (cudaHostAlloc((void**)&h_net[q], n * sizeof(float), cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostAlloc((void**)&h_key[q], sizeof(unsigned long long), cudaHostAllocMapped) != cudaSuccess) {
+            fprintf(stderr, "cudaHostAlloc failed\n");
+            return 1;
+        }
+    unsigned long long key_sync = 0;
+    CHECK(distill_eval_grid_host(m, inputs, 6, 0, n, 10, 0, 42, h_net[0], &key_sync, NULL));
+    CHECK(distill_eval_grid_host_async(m, inputs, 6, 0, n, 10, 0, 42, h_net[0], h_key[0], NULL));
+    CHECK(distill_eval_grid_host_async(m, inputs, 6, 0, n, 10, 0, 42, h_net[1], h_key[1], NULL));
+    if (cudaStreamSynchronize(NULL) != cudaSuccess) { fprintf(stderr, "sync failed\n"); return 1; }
+    int same = 1;
+    for (uint64_t i = 0; i < n; ++i) same &= (h_net[0][i] == net[i]) & (h_net[1][i] == net[i]);
+    printf("host key 0x%016llx async 0x%016llx 0x%016llx nets %s\n", key_sync, *h_key[0], *h_key[1],
+           same ? "same" : "DIFFER");
+    for (int q = 0; q < 2; ++q) { cudaFreeHost(h_net[q]); cudaFreeHost(h_key[q]); }
+
     printf("best %llu cost %a key 0x%016llx\n", (unsigned long long)idx, cost, key);
     cudaFree(d_net);
     cudaFree(d_best);
