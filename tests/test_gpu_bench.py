@@ -54,22 +54,23 @@ def test_bench_json_contract_on_gpu():
     assert d["result"]["key"] == f"{oracle.argmax_net(-full)[0]:016x}"
 
 
-def test_bench_self_spawns_ranks_and_reproduces_the_single_gpu_key():
-    """`bench.py --gpus 2` without torchrun launches two ranks itself (here both on
-    GPU 0 over gloo: the multi-rank code path, not a timing): n_gpus = 2, the cfg5
-    grid sharded in two, and the combined key equal to cfg5 evaluated whole on one
+@pytest.mark.parametrize("n", [2, 8])
+def test_bench_self_spawns_ranks_and_reproduces_the_single_gpu_key(n):
+    """`bench.py --gpus N` without torchrun launches N ranks itself (here all on
+    GPU 0 over gloo: the multi-rank code path, not a timing): n_gpus = N, the cfg5
+    grid sharded N ways, and the combined key equal to cfg5 evaluated whole on one
     GPU (itself bit-exact against the oracle, test_pp_cfg5_whole_grid_one_gpu)."""
     import torch
     env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--steps", "3",
                           "--warmup", "3", "--no-extras", "--no-cpu-baseline", "--dist-backend", "gloo",
                           "--device", "0"], capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["workload"].startswith("pp_cfg5")
-    assert d["timing"]["allocations_per_gpu"] == 4_000_000
+    assert d["n_gpus"] == n and d["scaling"] == "strong" and d["config"]["workload"].startswith("pp_cfg5")
+    assert d["timing"]["allocations_per_gpu"] == 8_000_000 // n
     sys.path.insert(0, ROOT)
     import paper_2110_15425_b200 as D
     import workloads as W
