@@ -141,6 +141,25 @@ def test_pp_cfg3_full_size_argmax_and_sampled_costs(D, orc):
     assert key == orc.argmax_net(-full)[0]
 
 
+def test_pp_cfg3_full_grid_over_seeds_invocations_and_positions(D, orc):
+    """cfg3 at full size beyond the bench's seed: five more (seed, invocation,
+    positions) triples — seeds 1..3 (SURVEY §8(d)'s sweep range), a high
+    invocation word, random positions from the input recipe — each with all 1e6
+    costs and the argmax key bit-exact against a full oracle grid search."""
+    import os
+    cfg = W.pp_cfg3()
+    m = _model(D, cfg)
+    pos = W.pp_positions(2)
+    cases = [(1, 0, cfg.inputs), (2, 0, cfg.inputs), (3, 0, cfg.inputs), (42, 0xFFFFFFFF, cfg.inputs),
+             (7, 5, pos[1])]
+    for seed, inv, inputs in cases:
+        C, key = _gpu_pp(D, m, cfg, invocation=inv, seed=seed, inputs=inputs)
+        full = orc.pp_eval_threads(cfg.n_levels, cfg.levels, cfg.w, cfg.params, inputs, 0, cfg.n_alloc,
+                                   cfg.n_samples, seed, threads=os.cpu_count() or 8, invocation=inv)
+        assert np.array_equal(_bits(C), _bits(full)), (seed, inv)
+        assert key == orc.argmax_net(-full)[0], (seed, inv)
+
+
 def test_pp_within_north_star_tolerance_of_binary64(D, orc):
     cfg = W.pp_cfg3()
     m = _model(D, cfg)
