@@ -58,7 +58,25 @@ __device__ __forceinline__ void block_min_key_atomic(key64_t k, key64_t* dst, bo
 }
 
 // K2: argmax over a device array of net values V -> atomicMin(key(-V[j], base+j)).
-// Grid-stride, vectorised float4 loads when the pointer is 16-B aligned.
+// HBM-bound (4 B read per value), so the per-value work must stay under ~0.7
+// instructions to keep up with HBM.  Each thread visits its groups of eight values
+// (two float4 loads) in DECREASING index order and keeps the largest V seen with
+// `max(group) >= best` (fmaxf ignores NaN; -0 == +0), resolving the group's first
+// index of that value only when the test passes — rarely, after the first few
+// groups — so equal values end at their lowest index, as the key order wants.  A
+// thread that saw no non-NaN value rescans its share for its first NaN (the key of
+// an all-NaN array is key(NaN, lowest index), as before).  Then the block min of
+// the per-thread keys and one atomicMin.  Misaligned pointers: the scalar loop.
+__device__ __forceinline__ float max8(const float4& a, const float4& b) {
+    return fmaxf(fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)), fmaxf(fmaxf(b.x, b.y), fmaxf(b.z, b.w)));
+}
+
+// first l in 0..7 with value == m (m is one of the group's non-NaN values)
+__device__ __forceinline__ uint32_t first_eq8(const float4& a, const float4& b, float m) {
+    return a.x == m ? 0u : a.y == m ? 1u : a.z == m ? 2u : a.w == m ? 3u
+         : b.x == m ? 4u : b.y == m ? 5u : b.z == m ? 6u : 7u;
+}
+
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) argmax_net_kernel(const float* __restrict__ v, uint64_t n,
                                                            uint32_t base, key64_t* __restrict__ best) {
@@ -66,21 +84,39 @@ __global__ void __launch_bounds__(BLOCK) argmax_net_kernel(const float* __restri
     const uint64_t tid = (uint64_t)blockIdx.x * BLOCK + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
     if ((reinterpret_cast<uintptr_t>(v) & 15u) == 0) {
-        const uint64_t n4 = n >> 2;
+        const uint64_t n8 = n >> 3;
         const float4* v4 = reinterpret_cast<const float4*>(v);
-        for (uint64_t j = tid; j < n4; j += stride) {
-            const float4 x = __ldg(v4 + j);
-            const uint32_t i0 = base + (uint32_t)(4 * j);
-            key64_t a = make_key(-x.x, i0), b = make_key(-x.y, i0 + 1);
-            key64_t c = make_key(-x.z, i0 + 2), d = make_key(-x.w, i0 + 3);
-            a = a < b ? a : b;
-            c = c < d ? c : d;
-            a = a < c ? a : c;
-            k = a < k ? a : k;
+        float bv = -INFINITY;
+        uint64_t bi = ~0ull;
+        // the ragged tail (indices above every group): one value per thread, first
+        const uint64_t jt = 8 * n8 + tid;
+        if (jt < n) {
+            const float x = __ldg(v + jt);
+            if (x >= bv) { bv = x; bi = jt; }
         }
-        for (uint64_t j = 4 * n4 + tid; j < n; j += stride) {
-            const key64_t a = make_key(-__ldg(v + j), base + (uint32_t)j);
-            k = a < k ? a : k;
+        // this thread's groups g = tid + q * stride, q = cnt-1 .. 0, two at a time
+        const uint64_t cnt = n8 > tid ? (n8 - 1 - tid) / stride + 1 : 0;
+        int64_t q = (int64_t)cnt - 1;
+        for (; q >= 1; q -= 2) {
+            const uint64_t g1 = tid + (uint64_t)q * stride, g0 = g1 - stride;
+            const float4 a1 = __ldg(v4 + 2 * g1), b1 = __ldg(v4 + 2 * g1 + 1);
+            const float4 a0 = __ldg(v4 + 2 * g0), b0 = __ldg(v4 + 2 * g0 + 1);
+            const float m1 = max8(a1, b1), m0 = max8(a0, b0);
+            if (m1 >= bv) { bv = m1; bi = 8 * g1 + first_eq8(a1, b1, m1); }
+            if (m0 >= bv) { bv = m0; bi = 8 * g0 + first_eq8(a0, b0, m0); }
+        }
+        if (q == 0) {
+            const float4 a0 = __ldg(v4 + 2 * tid), b0 = __ldg(v4 + 2 * tid + 1);
+            const float m0 = max8(a0, b0);
+            if (m0 >= bv) { bv = m0; bi = 8 * tid + first_eq8(a0, b0, m0); }
+        }
+        if (bi != ~0ull) {
+            k = make_key(-bv, base + (uint32_t)bi);
+        } else {                                   // no non-NaN value here: the first NaN, if any
+            for (uint64_t g = tid; g < n8 && k == KEY_INIT; g += stride)
+                for (uint32_t l = 0; l < 8; ++l)
+                    if (__ldg(v + 8 * g + l) != __ldg(v + 8 * g + l)) { k = make_key(__int_as_float(0x7FC00000), base + (uint32_t)(8 * g + l)); break; }
+            if (k == KEY_INIT && jt < n) k = make_key(-__ldg(v + jt), base + (uint32_t)jt);
         }
     } else {
         for (uint64_t j = tid; j < n; j += stride) {

@@ -184,6 +184,33 @@ def test_argmax_kernel_vs_oracle(D, orc, n, off):
     assert (int(best.item()) & (2 ** 64 - 1)) == k_or
 
 
+@pytest.mark.parametrize("n", [7, 8, 9, 4100, 1_000_003, 6_000_001])
+def test_argmax_kernel_edge_cases_aligned(D, orc, n):
+    """K2's aligned path (groups of eight visited in decreasing order, a group's
+    first index resolved only when its max reaches the thread's best): random
+    values, all -inf, NaN everywhere but one value, +-0 ties everywhere, the
+    maximum tied at scattered indices, all NaN — keys bit-exact against the
+    oracle (sizes below one group, ragged tails, several groups per thread)."""
+    import torch
+    rng = np.random.default_rng(n)
+    cases = {
+        "random": rng.standard_normal(n).astype(np.float32),
+        "all -inf": np.full(n, -np.inf, np.float32),
+        "nan but one": np.full(n, np.nan, np.float32),
+        "signed zeros": np.where(rng.random(n) < 0.5, np.float32(-0.0), np.float32(0.0)).astype(np.float32),
+        "scattered max": rng.integers(-3, 1, size=n).astype(np.float32),
+        "all nan": np.full(n, np.nan, np.float32),
+    }
+    cases["nan but one"][rng.integers(0, n)] = -np.inf
+    for name, v in cases.items():
+        t = torch.from_numpy(v).cuda()
+        best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        D.argmax(t, 12345, best)
+        torch.cuda.synchronize()
+        k_or, _ = orc.argmax_net(v, 12345)
+        assert (int(best.item()) & (2 ** 64 - 1)) == k_or, (n, name)
+
+
 def test_argmax_all_nan_and_empty(D, orc):
     import torch
     t = torch.full((10,), float("nan"), device="cuda")
