@@ -130,6 +130,21 @@ __global__ void __launch_bounds__(BLOCK) argmax_net_kernel(const float* __restri
 // NEXT-2 random tie-break (spec/MODELS.md §8): among the entries whose
 // canonical cost equals the best key's (pass A result in *best), min over
 // (pi_i << 32 | i) with pi_i = Philox(key, (i, 0, t, 3)).x -> atomicMin(*tie).
+// The tie test compares values, not keys: canon(-v) has the best key's high word
+// exactly when v == -C* (C* decoded from that word; -0 == +0, and the all-NaN key
+// never reaches the loop), so the scan is one float compare per value (float4
+// loads on aligned arrays) and the Philox priority is drawn for the ties only.
+__device__ __forceinline__ float key_cost(uint32_t hi) {        // inverse of make_key's order map
+    return __uint_as_float((hi & 0x80000000u) ? (hi & 0x7FFFFFFFu) : ~hi);
+}
+
+__device__ __forceinline__ void tie_candidate(uint32_t idx, uint32_t key0, uint32_t key1, uint32_t invocation,
+                                              key64_t& k) {
+    const uint4 X = philox4x32_10(make_uint4(idx, 0u, invocation, 3u), key0, key1);
+    const key64_t t = ((key64_t)X.x << 32) | idx;
+    k = t < k ? t : k;
+}
+
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) argmax_ties_kernel(const float* __restrict__ v, uint64_t n, uint32_t base,
                                                             const key64_t* __restrict__ best, uint32_t key0,
@@ -138,13 +153,26 @@ __global__ void __launch_bounds__(BLOCK) argmax_ties_kernel(const float* __restr
     const uint32_t hi = (uint32_t)(*best >> 32);
     key64_t k = KEY_INIT;
     if (hi != 0xFFFFFFFFu) {
-        for (uint64_t j = (uint64_t)blockIdx.x * BLOCK + threadIdx.x; j < n; j += (uint64_t)gridDim.x * BLOCK) {
-            const uint32_t idx = base + (uint32_t)j;
-            if ((uint32_t)(make_key(-__ldg(v + j), idx) >> 32) != hi) continue;
-            const uint4 X = philox4x32_10(make_uint4(idx, 0u, invocation, 3u), key0, key1);
-            const key64_t t = ((key64_t)X.x << 32) | idx;
-            k = t < k ? t : k;
+        const float T = -key_cost(hi);
+        const uint64_t tid = (uint64_t)blockIdx.x * BLOCK + threadIdx.x, stride = (uint64_t)gridDim.x * BLOCK;
+        uint64_t j0 = 0;
+        if ((reinterpret_cast<uintptr_t>(v) & 15u) == 0) {
+            const uint64_t n4 = n >> 2;
+            const float4* v4 = reinterpret_cast<const float4*>(v);
+            for (uint64_t j = tid; j < n4; j += stride) {
+                const float4 x = __ldg(v4 + j);
+                if (x.x == T || x.y == T || x.z == T || x.w == T) {
+                    const uint32_t i0 = base + (uint32_t)(4 * j);
+                    if (x.x == T) tie_candidate(i0, key0, key1, invocation, k);
+                    if (x.y == T) tie_candidate(i0 + 1, key0, key1, invocation, k);
+                    if (x.z == T) tie_candidate(i0 + 2, key0, key1, invocation, k);
+                    if (x.w == T) tie_candidate(i0 + 3, key0, key1, invocation, k);
+                }
+            }
+            j0 = 4 * n4;
         }
+        for (uint64_t j = j0 + tid; j < n; j += stride)
+            if (__ldg(v + j) == T) tie_candidate(base + (uint32_t)j, key0, key1, invocation, k);
     }
     block_min_key_atomic<BLOCK>(k, tie);
 }

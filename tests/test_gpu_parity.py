@@ -396,6 +396,36 @@ def test_pp_episode_capture_and_graph_replay(D, orc):
     assert torch.equal(t2, ref[0]) and torch.equal(k2, ref[1]) and torch.equal(s2, ref[2])
 
 
+@pytest.mark.parametrize("n,off", [(1_000_003, 0), (1_000_003, 1), (4_194_304, 2), (13, 0)])
+def test_argmax_ties_large_arrays_vs_oracle(D, orc, n, off):
+    """NEXT-2's second pass on large arrays (float4 path and the misaligned scalar
+    path): maxima tied at scattered indices incl. +-0 and -inf cases, NaN around
+    them — the tie key bit-exact against the oracle for several seeds."""
+    import torch
+    rng = np.random.default_rng(n + off)
+    for case in ("scattered", "zeros", "neg inf"):
+        v = rng.standard_normal(n + off).astype(np.float32) - 10.0
+        v[rng.integers(0, n + off, size=max(1, n // 40))] = np.nan
+        hit = rng.integers(0, n + off, size=min(n, 50))
+        if case == "scattered":
+            v[hit] = 3.5
+        elif case == "zeros":
+            v = np.minimum(v, -1.0)
+            v[hit] = np.where(rng.random(hit.size) < 0.5, np.float32(-0.0), np.float32(0.0))
+        else:
+            v[:] = np.where(np.isnan(v), np.nan, -np.inf).astype(np.float32)
+        t = torch.from_numpy(v).cuda()[off:]
+        for seed in (1, 2, 99):
+            best = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+            tie = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+            D.argmax(t, 777, best)
+            D.argmax_ties(t, 777, seed, 4, best, tie)
+            torch.cuda.synchronize()
+            k_or, t_or, _ = orc.argmax_random_ties(v[off:], 777, seed, 4)
+            assert (int(best.item()) & (2 ** 64 - 1)) == k_or, (n, off, case, seed)
+            assert (int(tie.item()) & (2 ** 64 - 1)) == t_or, (n, off, case, seed)
+
+
 def test_argmax_random_ties_bit_exact_and_uniform(D, orc):
     """NEXT-2: GPU tie keys equal the oracle's for every seed; 8 tied minima each
     win 1/8 +- 0.02 of 4000 reseeded runs; a PP grid with all-equal costs picks
