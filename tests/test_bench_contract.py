@@ -30,3 +30,29 @@ def test_reference_arm_json_contract():
     assert d["metric"] == bench.METRIC
     baseline = json.load(open(os.path.join(ROOT, "BASELINE.json")))
     assert d["metric"] == baseline["metric"]
+
+
+def test_bench_host_helpers(monkeypatch):
+    """Host-side helpers of the GPU arm: nvidia-smi's -i follows CUDA_VISIBLE_DEVICES
+    (each rank samples its own physical GPU), the workload per world size (N = 1 cfg3,
+    N > 1 cfg5 strong, --weak ~1e6 per GPU) and the contiguous 4-aligned shards."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2110_15425_b200 as D
+    monkeypatch.delenv("CUDA_VISIBLE_DEVICES", raising=False)
+    assert bench.smi_device(3) == "3"
+    monkeypatch.setenv("CUDA_VISIBLE_DEVICES", "4,5,6,7")
+    assert [bench.smi_device(r) for r in range(4)] == ["4", "5", "6", "7"]
+    monkeypatch.setenv("CUDA_VISIBLE_DEVICES", "GPU-abc, GPU-def")
+    assert bench.smi_device(1) == "GPU-def"
+    args = argparse.Namespace(weak=False, strong=False)
+    assert bench.workload(1, args)[0].n_alloc == 10 ** 6 and bench.workload(1, args)[1] == "weak"
+    for n in (2, 4, 8):
+        cfg, scaling = bench.workload(n, args)
+        assert cfg.n_alloc == 8 * 10 ** 6 and scaling == "strong"
+        shards = [D.shard_range(cfg.n_alloc, r, n) for r in range(n)]
+        assert shards[0][0] == 0 and shards[-1][1] == cfg.n_alloc
+        assert all(a[1] == b[0] for a, b in zip(shards, shards[1:])) and all(b % 4 == 0 for b, _ in shards)
+    args.weak = True
+    assert bench.workload(8, args)[0].n_alloc == 8 * 10 ** 6 and bench.workload(8, args)[1] == "weak"
