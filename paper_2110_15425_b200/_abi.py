@@ -11,7 +11,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdistill.so")
+# DISTILL_LIB selects another build of the same library (e.g. the bounds-checked debug
+# build, -DDISTILL_BOUNDS_CHECK=1, tools/gpu/r2_bounds.sh); default: the in-tree product build
+LIB_PATH = os.environ.get("DISTILL_LIB") or os.path.join(_HERE, "libdistill.so")
 
 OK, E_INVALID_ARG, E_OVERFLOW, E_UNSUPPORTED, E_CUDA, E_NO_VALID = range(6)
 MODEL_PREDATOR_PREY = 1

@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
         uint32_t rb;
         if (ch == 2) rb = 2 * a.n_rt_bins;
         else rb = ch * a.n_rt_bins + (st - 1) / a.rt_bin_steps;
+        DCHECK(rb < n_rt);
         atomicAdd(&s_hist[rb], 1u);
         if (ch == 0) sum_up += st;
         else if (ch == 1) sum_lo += st;
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) ddm_batch_kernel(const DDMArgs a)
         if (u < 0.0f) xb = 0;
         else if (!(u < fnx)) xb = a.n_x_bins + 1;
         else xb = 1 + (uint32_t)u;
+        DCHECK(xb < n_x);
         atomicAdd(&s_hist[n_rt + xb], 1u);
     }
     // rt sums: warp reduce then one atomic per warp

@@ -277,7 +277,9 @@ __global__ void __launch_bounds__(WARPS * 32) pp_eval_small_kernel(const PPArgs 
         for (uint32_t s = 2 * sl; s < a.n_samples; s += 2 * LANES) {
             const F2 e = pp_pair_errors<false, false>(rng(s), rng(s + 1), s0, s1, s2, P0, P1, P2,
                                                              bc(-a.kappa), us, rt);
+            DCHECK(s < (uint32_t)SMAX);
             s_e[w][grp][s] = e.x;
+            DCHECK(s + 1 >= a.n_samples || s + 1 < (uint32_t)SMAX);
             if (s + 1 < a.n_samples) s_e[w][grp][s + 1] = e.y;
         }
     }

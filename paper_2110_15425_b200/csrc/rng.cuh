@@ -10,6 +10,20 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side bounds checks (the library's debug build, -DDISTILL_BOUNDS_CHECK=1:
+// every shared-memory table / histogram index is asserted in range; the product
+// build compiles them out).  compute-sanitizer is closed on this GPU pool, so this
+// build run over the GPU suite is the memory-safety check of the kernels.
+#ifndef DISTILL_BOUNDS_CHECK
+#define DISTILL_BOUNDS_CHECK 0
+#endif
+#if DISTILL_BOUNDS_CHECK
+#include <cassert>
+#define DCHECK(cond) assert(cond)
+#else
+#define DCHECK(cond) ((void)0)
+#endif
+
 namespace distill {
 
 // ---------------------------------------------------------------- Philox4x32-10
@@ -166,6 +180,8 @@ __device__ __forceinline__ F2 rad2(uint32_t Rx, uint32_t Ry, const float4* __res
     const uint32_t mx = (uint32_t)((int32_t)Rx >> 31), my = (uint32_t)((int32_t)Ry >> 31);
     const uint32_t vx = (((uint32_t)((int32_t)Rx >> 8)) ^ mx) | 1u, vy = (((uint32_t)((int32_t)Ry >> 8)) ^ my) | 1u;
     const uint32_t bx = __float_as_uint(__uint2float_rn(vx)), by = __float_as_uint(__uint2float_rn(vy));
+    DCHECK((bx >> 19) + (mx & 368u) - (127u << 4) < (uint32_t)RT_ROWS);
+    DCHECK((by >> 19) + (my & 368u) - (127u << 4) < (uint32_t)RT_ROWS);
     const float4 cx = (rt - (127u << 4))[(bx >> 19) + (mx & 368u)];
     const float4 cy = (rt - (127u << 4))[(by >> 19) + (my & 368u)];
     const F2 t = L::add(make_float2(__uint_as_float(lop3_and_or<0x7FFFFu>(bx, 0x3F800000u)),

@@ -52,9 +52,10 @@ __device__ __forceinline__ void lca_update(const StroopArgs& a, float nleak, flo
 template <bool TABLE>
 struct Pathway {
     const float* row0; const float* row1;   // TABLE
+    uint32_t n_rows = 0;                    // TABLE: row length (bounds checks only)
     float I0, I1, tau, h0, h1;              // !TABLE
     __device__ __forceinline__ void at(uint32_t n, float& o0, float& o1) {
-        if (TABLE) { o0 = row0[n - 1]; o1 = row1[n - 1]; }
+        if (TABLE) { DCHECK(n >= 1 && n <= n_rows); o0 = row0[n - 1]; o1 = row1[n - 1]; }
         else {
             h0 = __fmaf_rn(tau, __fadd_rn(I0, -h0), h0);
             h1 = __fmaf_rn(tau, __fadd_rn(I1, -h1), h1);
@@ -115,6 +116,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) stroop_sim_kernel(const StroopArg
             // colour unit gets row 3 in congruent trials (word = colour) and 1 otherwise;
             // the other unit gets row 2 in incongruent trials (word = other) and 0 otherwise
             const uint32_t rc = kind == 0 ? 3u : 1u, ro = kind == 1 ? 2u : 0u;
+            pw.n_rows = N;
             pw.row0 = s_htab + N * (colour == 0 ? rc : ro);
             pw.row1 = s_htab + N * (colour == 1 ? rc : ro);
         } else {
@@ -247,6 +249,7 @@ __global__ void __launch_bounds__(BLOCK) stroop_energy_kernel(const StroopArgs a
             long long q = valid ? __float2ll_rn(__fmul_rn(__fmul_rn(x0, x1), 0x1p24f)) : 0ll;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xFFFFFFFFu, q, o);
+            DCHECK(n >= 1 && n <= N);
             if (lane == 0 && q) atomicAdd(&s_esum[n - 1], (unsigned long long)q);
         }
     }
